@@ -1,0 +1,149 @@
+/*
+ * pi0b — B200-native (sm_100a) pi0 inference engine: the C-ABI boundary.
+ *
+ * This is the drop-in replacement for the reference's C++ inference API
+ *     rtvla::gen_weights / rtvla::gen_inputs / rtvla::evaluate
+ * (proj/include/rtvla/evaluate.hpp:38-44, proj/src/evaluate.cpp:38-85,365-370) for the
+ * fused pi0 graph built by rtvla::build_pi0_graph (proj/src/builder.cpp:197-367).
+ * Plain C types only: no torch, no rtvla, no CUDA types in any signature.  The C++
+ * adaptor that takes rtvla::Graph / WeightStore / Inputs and forwards here lives in
+ * include/pi0b_rtvla.hpp; INTEGRATION.md shows how a reference caller binds it.
+ *
+ * Conventions:
+ *   - every function returns 0 (PI0B_OK) on success, a negative PI0B_E* code or a
+ *     positive cudaError_t value on failure; pi0b_last_error() describes the last
+ *     failure of the calling thread;
+ *   - tensors are dense row-major fp64 host arrays with the reference's shapes;
+ *   - an engine is bound to one device and is not safe for concurrent calls
+ *     (create one engine per thread/stream, as the reference's std::async verifiers
+ *     create one Evaluator per call, proj/src/passes.cpp:864-867).
+ */
+#ifndef PI0B_H_
+#define PI0B_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PI0B_OK 0
+#define PI0B_E_INVALID (-1)     /* bad argument / unknown node id / shape mismatch (ShapeError) */
+#define PI0B_E_UNSUPPORTED (-2) /* configuration outside what the kernels implement          */
+#define PI0B_E_STATE (-3)       /* call out of order (e.g. run before weights are loaded)     */
+#define PI0B_E_NUMERIC (-4)     /* non-finite action output (NumericError)                    */
+
+/* Mirrors rtvla::ModelConfig field by field (proj/include/rtvla/graph.hpp:114-160). */
+typedef struct pi0b_model_config {
+    int views, prompt_tokens, tokens_per_view, chunk_len, flow_steps;
+    int ve_layers, ve_width, ve_heads, ve_head_dim, ve_mlp, ve_patch_in;
+    int llm_layers, llm_width, llm_q_heads, llm_head_dim, llm_kv_heads, llm_mlp;
+    int ae_layers, ae_width, ae_q_heads, ae_head_dim, ae_kv_heads, ae_mlp, ae_action_dim,
+        ae_state_dim;
+} pi0b_model_config;
+
+typedef struct pi0b_engine_options {
+    int device;             /* CUDA ordinal                                              */
+    int use_cuda_graph;     /* 1: capture the whole forward as one CUDA graph (default)   */
+    int record_checkpoints; /* 1: keep every node instance's output for parity checks    */
+} pi0b_engine_options;
+
+typedef struct pi0b_engine pi0b_engine;
+
+/* rtvla::default_config() (proj/src/builder.cpp:10-12): 2 views, empty prompt. */
+void pi0b_default_config(pi0b_model_config* cfg);
+
+/* Engine lifetime.  Allocates the weight arena (bf16), activations, KV cache. */
+int pi0b_engine_create(const pi0b_model_config* cfg, const pi0b_engine_options* opt,
+                       pi0b_engine** out);
+void pi0b_engine_destroy(pi0b_engine* e);
+
+/* Device-side rtvla::gen_weights(build_pi0_graph(cfg), seed): the same SplitMix64 /
+ * FNV-1a streams, rounded once to bf16 (proj/src/evaluate.cpp:38-75). */
+int pi0b_engine_gen_weights(pi0b_engine* e, uint64_t seed);
+
+/* Host weights, one WeightSet instance at a time (proj/include/rtvla/evaluate.hpp:16-27):
+ * w is W[k, m] row-major, bias is [m] or NULL. */
+int pi0b_engine_set_weight(pi0b_engine* e, const char* node_id, int64_t instance, const double* w,
+                           int64_t k, int64_t m, const double* bias, int64_t bias_len);
+/* WeightSet::bias_table of ae.action_proj, [flow_steps, m]. */
+int pi0b_engine_set_bias_table(pi0b_engine* e, const char* node_id, const double* table,
+                               int64_t rows, int64_t m);
+
+/* One full inference == rtvla::evaluate(g, w, x) (proj/src/evaluate.cpp:365-370).
+ * patches [views*tokens_per_view, ve_patch_in], state [1, ae_state_dim],
+ * noise [chunk_len, ae_action_dim], prompt [prompt_tokens, llm_width] (NULL when 0),
+ * actions_out [chunk_len, ae_action_dim]. */
+int pi0b_engine_run(pi0b_engine* e, const double* patches, const double* state, const double* noise,
+                    const double* prompt, double* actions_out);
+
+/* Streaming split of run(): the prefix (VE + LLM, fills the KV cache) and the action
+ * expert (all flow steps against the cached prefix KV). */
+int pi0b_engine_run_prefix(pi0b_engine* e, const double* patches, const double* prompt);
+int pi0b_engine_run_action(pi0b_engine* e, const double* state, const double* noise,
+                           double* actions_out);
+
+/* Device-resident replay of the last inputs (no host copies): 0 = full, 1 = prefix,
+ * 2 = action.  `stream` is a cudaStream_t (NULL = the engine's stream).  Asynchronous. */
+int pi0b_engine_replay(pi0b_engine* e, int part, void* stream);
+int pi0b_engine_sync(pi0b_engine* e);
+/* Number of kernels one replay of `part` launches. */
+int pi0b_engine_kernel_count(pi0b_engine* e, int part);
+
+/* Parity hook (record_checkpoints=1): the output of node `node_id` instance `inst` from
+ * the last run, as fp32 [rows, cols].  Node ids/instances are the reference graph's. */
+int pi0b_engine_read_checkpoint(pi0b_engine* e, const char* node_id, int64_t inst, float* out,
+                                int64_t rows, int64_t cols);
+
+/* Thread-local description of the last failure. */
+const char* pi0b_last_error(void);
+
+/* ------------------------------------------------------------------ kernel level
+ * Device-pointer entry points used by the unit parity tests (stream = cudaStream_t). */
+
+typedef struct pi0b_gemm_desc {
+    const void* a; int64_t lda;     /* bf16 [M, K]                                  */
+    const void* w; int64_t ldw;     /* bf16 [N, K] (packed weight)                  */
+    int M, N, K;
+    int bn;                         /* tile width 64 / 128 / 256                    */
+    int splits;                     /* split-K factor (>= 1)                        */
+    int mode, flags;                /* see paper_2510_26742_b200/csrc/gemm.cuh      */
+    const float* row_stats; float inv_width, eps;
+    const float* bias;
+    const float* table_row;
+    const float* rope_cs; int rope_pos0, rope_cols;
+    float resid_scale;
+    void* out; int64_t ldo;
+    void* outb; int64_t ldob;
+    float* out_stats;
+    const float* row0_src;
+    float* ws; int* counters;       /* split-K scratch, zero-initialised            */
+} pi0b_gemm_desc;
+int pi0b_gemm(const pi0b_gemm_desc* d, void* stream);
+
+typedef struct pi0b_attn_desc {
+    int head_dim;                   /* 72 or 256                                    */
+    const void* q; int64_t ldq; int q_rows, heads, kv_heads;
+    const void* k0; const void* v0; int64_t ld0; int rows0;
+    const void* k1; const void* v1; int64_t ld1; int rows1;
+    void* out; int64_t ldo;
+    int kv_splits;                  /* 0 = choose                                   */
+    float* ws; int* counters;       /* scratch for kv_splits > 1                    */
+} pi0b_attn_desc;
+int pi0b_attention(const pi0b_attn_desc* d, void* stream);
+/* Workspace floats / counters an attention launch with these dims needs. */
+int64_t pi0b_attention_ws_floats(const pi0b_attn_desc* d);
+
+/* Device SplitMix64 draw of random_tensor(rows, cols, lo, hi, seed) into fp64 (parity
+ * of the parameter streams) and into the packed bf16 layout. */
+int pi0b_random_f64(double* dst, int64_t n, uint64_t seed, double lo, double hi, void* stream);
+int pi0b_random_packed_bf16(void* dst, int64_t ldk, int k, int m, int gated, uint64_t seed, double lo,
+                            double hi, void* stream);
+/* FNV-1a seed derivation (proj/src/tensor.cpp:24-40). */
+uint64_t pi0b_seed_hash(uint64_t seed, const char* label, uint64_t a, uint64_t b);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PI0B_H_ */

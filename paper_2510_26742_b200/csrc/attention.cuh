@@ -1,0 +1,36 @@
+// Parameter block of the flash-style attention kernel (attention.cu).
+//
+// Semantics follow the reference `Evaluator::attention` (proj/src/evaluate.cpp:225-252):
+// per head h, P = softmax(Q_h K_{h % kv_heads}^T / sqrt(d)) with no mask, O_h = P V.
+// Keys/values are the row-concatenation of two segments, which is how `ae.kcat` /
+// `ae.vcat` (proj/src/builder.cpp:321-329) are consumed without materialising the concat.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace pi0b {
+
+struct AttnParams {
+    const __nv_bfloat16* q;   // [q_rows, heads*d] (row stride ldq)
+    long long ldq;
+    int q_rows, heads, kv_heads;
+    const __nv_bfloat16* k0;  // segment 0: [rows0, kv_heads*d] keys, values
+    const __nv_bfloat16* v0;
+    long long ld0;
+    int rows0;
+    const __nv_bfloat16* k1;  // segment 1 (rows1 may be 0)
+    const __nv_bfloat16* v1;
+    long long ld1;
+    int rows1;
+    float scale_log2;         // log2(e) / sqrt(d)
+    __nv_bfloat16* out;       // [q_rows, heads*d]
+    long long ldo;
+    int kv_splits;            // grid.y; > 1 -> partials in ws, last CTA combines
+    int kv_per_split;         // keys per split (multiple of the key tile)
+    float* ws_o;              // [splits][grid.z][q_tiles*64][d] fp32
+    float* ws_ml;             // [splits][grid.z][q_tiles*64][2]
+    int* counters;            // [grid.z * q_tiles], zero on entry and exit
+};
+
+}  // namespace pi0b

@@ -1,0 +1,160 @@
+// Kernel-level C-ABI entry points (include/pi0b.h "kernel level" section): thin POD
+// wrappers used by the unit parity tests to drive one GEMM / attention / RNG launch on
+// caller-owned device memory.
+#include "../../include/pi0b.h"
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "attention.cuh"
+#include "gemm.cuh"
+#include "numerics.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <stdexcept>
+#include <string>
+
+namespace pi0b {
+cudaError_t gemm_configure();
+cudaError_t attn_configure();
+cudaError_t launch_gemm(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                        cudaStream_t stream);
+cudaError_t launch_attention(int head_dim, const AttnParams& p, cudaStream_t stream);
+int attn_key_tile(int head_dim);
+int attn_query_tile();
+CUtensorMap make_tmap_bf16(const void* base, long long rows, long long cols, long long ld, int box_rows);
+cudaError_t launch_gen_weight(__nv_bfloat16* dst, long long ldk, int k, int m, int gated,
+                              uint64_t seed, double lo, double hi, cudaStream_t st);
+uint64_t seed_hash(uint64_t seed, const std::string& label, uint64_t a, uint64_t b);
+
+__global__ void random_f64_kernel(double* dst, long long n, uint64_t seed, double lo, double hi) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = uniform_at(seed, uint64_t(i), lo, hi);
+}
+
+static int configure_once() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    static bool done[64] = {false};
+    if (dev < 64 && !done[dev]) {
+        cudaError_t e = gemm_configure();
+        if (e == cudaSuccess) e = attn_configure();
+        if (e != cudaSuccess) return int(e);
+        done[dev] = true;
+    }
+    return 0;
+}
+
+static void attn_plan(const pi0b_attn_desc* d, int* splits, int* per, int* q_tiles) {
+    const int grows = (d->heads / d->kv_heads) * d->q_rows;
+    *q_tiles = (grows + attn_query_tile() - 1) / attn_query_tile();
+    const int total = d->rows0 + d->rows1;
+    const int kvt = attn_key_tile(d->head_dim);
+    int s = d->kv_splits;
+    if (s <= 0) s = std::max(1, std::min(148 / std::max(1, *q_tiles * d->kv_heads), (total + 63) / 64));
+    int pp = (total + s - 1) / s;
+    pp = (pp + kvt - 1) / kvt * kvt;
+    *splits = (total + pp - 1) / pp;
+    *per = pp;
+}
+
+}  // namespace pi0b
+
+extern "C" {
+
+int pi0b_gemm(const pi0b_gemm_desc* d, void* stream) {
+    using namespace pi0b;
+    int rc = configure_once();
+    if (rc) return rc;
+    try {
+        GemmParams p{};
+        p.M = d->M;
+        p.N = d->N;
+        p.K = d->K;
+        const int kb = (d->K + 63) / 64;
+        const int s = std::max(1, std::min(d->splits, kb));
+        p.kb_per_split = (kb + s - 1) / s;
+        p.splits = (kb + p.kb_per_split - 1) / p.kb_per_split;
+        p.mode = d->mode;
+        p.flags = d->flags;
+        p.row_stats = d->row_stats;
+        p.inv_width = d->inv_width;
+        p.eps = d->eps;
+        p.bias = d->bias;
+        p.table_row = d->table_row;
+        p.rope_cs = d->rope_cs;
+        p.rope_pos0 = d->rope_pos0;
+        p.rope_cols = d->rope_cols;
+        p.resid_scale = d->resid_scale;
+        p.out = d->out;
+        p.ldo = d->ldo;
+        p.outb = d->outb;
+        p.ldob = d->ldob;
+        p.out_stats = d->out_stats;
+        p.row0_src = d->row0_src;
+        p.ws = d->ws;
+        p.counters = d->counters;
+        CUtensorMap ta = make_tmap_bf16(d->a, d->M, d->K, d->lda, 128);
+        CUtensorMap tb = make_tmap_bf16(d->w, d->N, d->K, d->ldw, d->bn);
+        return int(launch_gemm(d->bn, ta, tb, p, static_cast<cudaStream_t>(stream)));
+    } catch (const std::exception&) {
+        return PI0B_E_INVALID;
+    }
+}
+
+int64_t pi0b_attention_ws_floats(const pi0b_attn_desc* d) {
+    int splits, per, q_tiles;
+    pi0b::attn_plan(d, &splits, &per, &q_tiles);
+    return int64_t(splits) * d->kv_heads * q_tiles * 64 * (d->head_dim + 2);
+}
+
+int pi0b_attention(const pi0b_attn_desc* d, void* stream) {
+    using namespace pi0b;
+    int rc = configure_once();
+    if (rc) return rc;
+    AttnParams p{};
+    p.q = static_cast<const __nv_bfloat16*>(d->q);
+    p.ldq = d->ldq;
+    p.q_rows = d->q_rows;
+    p.heads = d->heads;
+    p.kv_heads = d->kv_heads;
+    p.k0 = static_cast<const __nv_bfloat16*>(d->k0);
+    p.v0 = static_cast<const __nv_bfloat16*>(d->v0);
+    p.ld0 = d->ld0;
+    p.rows0 = d->rows0;
+    p.k1 = static_cast<const __nv_bfloat16*>(d->k1);
+    p.v1 = static_cast<const __nv_bfloat16*>(d->v1);
+    p.ld1 = d->ld1;
+    p.rows1 = d->rows1;
+    p.out = static_cast<__nv_bfloat16*>(d->out);
+    p.ldo = d->ldo;
+    p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(d->head_dim)));
+    int splits, per, q_tiles;
+    attn_plan(d, &splits, &per, &q_tiles);
+    p.kv_splits = splits;
+    p.kv_per_split = per;
+    const long long rows_pad = (long long)q_tiles * 64;
+    p.ws_o = d->ws;
+    p.ws_ml = d->ws ? d->ws + (long long)splits * d->kv_heads * rows_pad * d->head_dim : nullptr;
+    p.counters = d->counters;
+    if (splits > 1 && (!d->ws || !d->counters)) return PI0B_E_INVALID;
+    return int(launch_attention(d->head_dim, p, static_cast<cudaStream_t>(stream)));
+}
+
+int pi0b_random_f64(double* dst, int64_t n, uint64_t seed, double lo, double hi, void* stream) {
+    pi0b::random_f64_kernel<<<int((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(dst, n, seed,
+                                                                                               lo, hi);
+    return int(cudaGetLastError());
+}
+
+int pi0b_random_packed_bf16(void* dst, int64_t ldk, int k, int m, int gated, uint64_t seed, double lo,
+                            double hi, void* stream) {
+    return int(pi0b::launch_gen_weight(static_cast<__nv_bfloat16*>(dst), ldk, k, m, gated, seed, lo, hi,
+                                       static_cast<cudaStream_t>(stream)));
+}
+
+uint64_t pi0b_seed_hash(uint64_t seed, const char* label, uint64_t a, uint64_t b) {
+    return pi0b::seed_hash(seed, std::string(label), a, b);
+}
+
+}  // extern "C"

@@ -1,0 +1,1244 @@
+// Host runtime of the pi0 engine behind the C-ABI in include/pi0b.h.
+//
+// The engine turns the fused pi0 graph of rtvla::build_pi0_graph (proj/src/builder.cpp:
+// 197-367) into a static launch plan: every node instance becomes one kernel launch
+// (tcgen05 GEMM with its fused epilogue, or flash attention), every buffer is
+// pre-allocated, the instance algebra of the reference (proj/include/rtvla/graph.hpp:3-15,
+// proj/src/evaluate.cpp:120-150) is resolved at plan time into fixed device pointers,
+// and the whole forward is captured once as a CUDA graph and replayed with no per-step
+// host work.  The memoised demand-driven evaluator of the reference
+// (proj/src/evaluate.cpp:89-361) thus becomes a straight-line schedule:
+//   VE   ve.embed, 27 x {ve.qkv, ve.attn, ve.proj, ve.fc1, ve.fc2}
+//   LLM  llm.proj_in (+prompt rows), 18 x llm.qkv (KV cache), 17 x {attn, proj, ffn, down}
+//   AE   ae.state_proj, 10 x {action_proj, action_out+suffix, 18 x {qkv, attn, proj, ffn,
+//        down}, head(+Euler)}
+// RmsStats nodes have no launch: their row sums of squares are accumulated by the
+// epilogue of the kernel that produced the residual stream.
+#include "../../include/pi0b.h"
+#include "attention.cuh"
+#include "gemm.cuh"
+#include "numerics.cuh"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace pi0b {
+
+cudaError_t gemm_configure();
+cudaError_t attn_configure();
+cudaError_t launch_gemm(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                        cudaStream_t stream);
+cudaError_t launch_attention(int head_dim, const AttnParams& p, cudaStream_t stream);
+int attn_key_tile(int head_dim);
+int attn_query_tile();
+cudaError_t launch_gen_weight(__nv_bfloat16* dst, long long ldk, int k, int m, int gated,
+                              uint64_t seed, double lo, double hi, cudaStream_t st);
+cudaError_t launch_pack_weight(__nv_bfloat16* dst, long long ldk, const double* w, int k, int m,
+                               int gated, cudaStream_t st);
+cudaError_t launch_gen_vector(float* dst, int n, uint64_t seed, double lo, double hi, cudaStream_t st);
+cudaError_t launch_f64_to_f32(float* dst, const double* src, int n, cudaStream_t st);
+cudaError_t launch_rows_to_f32(const double* src, int rows, int cols, float* dst, long long ldd,
+                               __nv_bfloat16* dstb, long long lddb, float* stats, cudaStream_t st);
+cudaError_t launch_f64_to_bf16_rows(const double* src, int rows, int cols, __nv_bfloat16* dst,
+                                    long long ldd, cudaStream_t st);
+cudaError_t launch_f32_to_f64(const float* src, long long lds, int rows, int cols, double* dst,
+                              cudaStream_t st);
+
+// ------------------------------------------------------------------ errors
+
+static thread_local std::string g_last_error;
+
+struct EngineError : std::runtime_error {
+    int code;
+    EngineError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define PI0B_CUDA(x)                                                                          \
+    do {                                                                                      \
+        cudaError_t e_ = (x);                                                                 \
+        if (e_ != cudaSuccess)                                                                \
+            throw EngineError(int(e_), std::string(#x) + ": " + cudaGetErrorString(e_));      \
+    } while (0)
+
+static int fail(const EngineError& e) {
+    g_last_error = e.what();
+    return e.code;
+}
+
+// ------------------------------------------------------------------ FNV-1a seeds
+
+uint64_t seed_hash(uint64_t seed, const std::string& label, uint64_t a, uint64_t b) {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    auto mix = [&h](uint64_t v) {
+        for (int i = 0; i < 8; ++i) {
+            h ^= (v >> (8 * i)) & 0xff;
+            h *= 0x100000001b3ULL;
+        }
+    };
+    mix(seed);
+    for (unsigned char c : label) {
+        h ^= c;
+        h *= 0x100000001b3ULL;
+    }
+    mix(a);
+    mix(b);
+    return h;
+}
+
+// ------------------------------------------------------------------ tensor maps
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        PI0B_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess)
+            throw EngineError(PI0B_E_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// bf16 [rows, cols] with row pitch `ld` elements, tiles of box_rows x 64, 128-B swizzle.
+CUtensorMap make_tmap_bf16(const void* base, long long rows, long long cols, long long ld, int box_rows) {
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * 2) % 16)
+        throw EngineError(PI0B_E_INVALID, "TMA operand needs 16-byte aligned base and pitch");
+    CUtensorMap m;
+    cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(ld * 2)};
+    cuuint32_t box[2] = {64, cuuint32_t(box_rows)};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw EngineError(PI0B_E_INVALID, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return m;
+}
+
+static int round_up(int x, int a) { return (x + a - 1) / a * a; }
+
+// Split-K factor so that the grid approaches one wave of 148 SMs.
+static int choose_splits(int m_tiles, int n_tiles, int K, int num_sms) {
+    const int ctas = m_tiles * n_tiles;
+    const int kb = (K + 63) / 64;
+    if (ctas * 2 > num_sms) return 1;
+    int s = std::max(1, std::min(num_sms / ctas, kb));
+    const int per = (kb + s - 1) / s;
+    return (kb + per - 1) / per;
+}
+
+// ------------------------------------------------------------------ plan records
+
+enum OpKind { kOpGemm, kOpAttn, kOpRowsF32, kOpF64Bf16, kOpF32F64, kOpMemset };
+
+struct Op {
+    OpKind kind;
+    int part;  // 0 = prefix, 1 = action
+    // gemm
+    int bn = 0;
+    CUtensorMap ta, tb;
+    GemmParams gp{};
+    // attention
+    int hd = 0;
+    AttnParams ap{};
+    // conversions
+    const double* src64 = nullptr;
+    int rows = 0, cols = 0;
+    float* dst32 = nullptr;
+    long long ld32 = 0;
+    __nv_bfloat16* dstb = nullptr;
+    long long ldb = 0;
+    float* stats = nullptr;
+    const float* src32 = nullptr;
+    double* dst64 = nullptr;
+    void* mptr = nullptr;
+    size_t mbytes = 0;
+    // checkpoint tag (record mode)
+    std::string node;
+    int inst = -1;
+    const void* ck_ptr = nullptr;
+    int ck_rows = 0, ck_cols = 0;
+    long long ck_ld = 0;
+    int ck_bf16 = 0;
+    bool is_kernel() const { return kind != kOpMemset; }
+};
+
+struct NodeWeights {
+    int k = 0, m = 0, instances = 0;
+    long long ldk = 0;
+    bool gated = false, has_bias = false, has_table = false;
+    std::vector<__nv_bfloat16*> w;
+    std::vector<float*> b;
+    float* table = nullptr;
+};
+
+struct Checkpoint {
+    void* dev = nullptr;
+    int rows = 0, cols = 0, bf16 = 0;
+};
+
+class Engine {
+public:
+    Engine(const pi0b_model_config& cfg, const pi0b_engine_options& opt);
+    ~Engine();
+
+    void gen_weights(uint64_t seed);
+    void set_weight(const std::string& id, long long inst, const double* w, long long k, long long m,
+                    const double* bias, long long blen);
+    void set_bias_table(const std::string& id, const double* t, long long rows, long long m);
+    void upload_inputs(const double* patches, const double* state, const double* noise,
+                       const double* prompt, int which);
+    void launch(int part, cudaStream_t st);
+    void fetch_actions(double* out);
+    void read_checkpoint(const std::string& id, long long inst, float* out, long long rows, long long cols);
+    int kernel_count(int part) const;
+    cudaStream_t stream() const { return stream_; }
+    bool weights_ready() const { return weights_loaded_; }
+
+private:
+    template <typename T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        const size_t bytes = std::max<size_t>(256, (count * sizeof(T) + 255) / 256 * 256);
+        PI0B_CUDA(cudaMalloc(&p, bytes));
+        allocs_.push_back(p);
+        return static_cast<T*>(p);
+    }
+    void validate_config();
+    void alloc_weights();
+    void alloc_activations();
+    void build_plan();
+    void add_gemm(int part, const std::string& node, int inst, const __nv_bfloat16* A, long long lda,
+                  int M, const NodeWeights& W, int widx, int bn, GemmParams gp, bool allow_split = true);
+    void add_attn(int part, const std::string& node, int inst, int hd, AttnParams ap);
+    void tag(const std::string& node, int inst, const void* ptr, int rows, int cols, long long ld, int bf16);
+    float* stats_slot(int part);
+    void run_ops(int part, cudaStream_t st);
+    void capture(int part);
+
+    pi0b_model_config c_;
+    pi0b_engine_options o_;
+    int num_sms_ = 148;
+    cudaStream_t stream_ = nullptr;
+    std::vector<void*> allocs_;
+    std::map<std::string, NodeWeights> W_;
+    bool weights_loaded_ = false;
+
+    // dims
+    int T_ = 0, P_ = 0, L_ = 0, S_ = 0, C_ = 0, FS_ = 0;
+    int ve_w_ = 0, llm_w_ = 0, ae_w_ = 0, llm_q_ = 0, llm_kv_ = 0, ae_q_ = 0, ae_kv_ = 0;
+    int patch_ld_ = 0, act_ld_ = 0, state_ld_ = 0;
+
+    // inputs (fp64 device staging + pinned host staging)
+    double *d_patches_ = nullptr, *d_state_ = nullptr, *d_noise_ = nullptr, *d_prompt_ = nullptr,
+           *d_out_ = nullptr;
+    double *h_in_ = nullptr, *h_out_ = nullptr;
+    size_t n_patches_ = 0, n_state_ = 0, n_noise_ = 0, n_prompt_ = 0, n_out_ = 0;
+
+    // activations
+    __nv_bfloat16 *patches_b_ = nullptr, *ve_hb_ = nullptr, *ve_qkv_ = nullptr, *ve_attn_ = nullptr,
+                  *ve_mlp_ = nullptr;
+    float* ve_h_ = nullptr;
+    float* x_ = nullptr;
+    __nv_bfloat16 *xb_ = nullptr, *llm_attn_ = nullptr, *llm_g_ = nullptr;
+    std::vector<__nv_bfloat16*> kv_;  // per LLM layer [L, q+2kv]
+    __nv_bfloat16 *state_b_ = nullptr, *ab_ = nullptr, *ap_b_ = nullptr, *yb_ = nullptr,
+                  *aqkv_ = nullptr, *ao_ = nullptr, *ag_ = nullptr;
+    float *st_ = nullptr, *y_ = nullptr, *a_ = nullptr;
+    float* rope_cs_ = nullptr;
+    float* gemm_ws_ = nullptr;
+    int* gemm_ctr_ = nullptr;
+    size_t gemm_ws_floats_ = 0;
+    float* attn_ws_ = nullptr;
+    int* attn_ctr_ = nullptr;
+    size_t attn_ws_floats_ = 0;
+    float* stats_[2] = {nullptr, nullptr};
+    int stats_rows_ = 0, stats_used_[2] = {0, 0}, stats_cap_[2] = {0, 0};
+
+    std::vector<Op> ops_;
+    cudaGraphExec_t graph_[3] = {nullptr, nullptr, nullptr};
+    std::map<std::pair<std::string, int>, Checkpoint> ck_;
+};
+
+// ------------------------------------------------------------------ construction
+
+Engine::Engine(const pi0b_model_config& cfg, const pi0b_engine_options& opt) : c_(cfg), o_(opt) {
+    validate_config();
+    PI0B_CUDA(cudaSetDevice(o_.device));
+    cudaDeviceProp prop;
+    PI0B_CUDA(cudaGetDeviceProperties(&prop, o_.device));
+    if (prop.major != 10)
+        throw EngineError(PI0B_E_UNSUPPORTED, "pi0b kernels are built for sm_100a (B200); found sm_" +
+                                                  std::to_string(prop.major * 10 + prop.minor));
+    num_sms_ = prop.multiProcessorCount;
+    PI0B_CUDA(gemm_configure());
+    PI0B_CUDA(attn_configure());
+    PI0B_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    alloc_weights();
+    alloc_activations();
+    build_plan();
+}
+
+Engine::~Engine() {
+    for (auto& g : graph_)
+        if (g) cudaGraphExecDestroy(g);
+    for (auto& kv : ck_) cudaFree(kv.second.dev);
+    for (void* p : allocs_) cudaFree(p);
+    if (h_in_) cudaFreeHost(h_in_);
+    if (h_out_) cudaFreeHost(h_out_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::validate_config() {
+    const auto& c = c_;
+    auto need = [](bool ok, const std::string& what) {
+        if (!ok) throw EngineError(PI0B_E_UNSUPPORTED, "unsupported pi0 config: " + what);
+    };
+    need(c.views >= 1 && c.tokens_per_view >= 1 && c.prompt_tokens >= 0, "token counts");
+    need(c.chunk_len >= 1 && c.flow_steps >= 1, "chunk/flow steps");
+    need(c.ve_width == c.ve_heads * c.ve_head_dim, "ve_width != ve_heads*ve_head_dim");
+    need(c.ve_head_dim == 72 || c.ve_head_dim == 256, "ve_head_dim must be 72 or 256");
+    need(c.llm_head_dim == 256 && c.ae_head_dim == 256, "llm/ae head_dim must be 256 (RoPE tile)");
+    need(c.llm_kv_heads == c.ae_kv_heads && c.llm_kv_heads >= 1, "llm/ae kv_heads must match");
+    need(c.llm_q_heads % c.llm_kv_heads == 0 && c.ae_q_heads % c.ae_kv_heads == 0, "GQA grouping");
+    need(c.ae_q_heads * c.ae_head_dim > 0, "ae heads");
+    need(c.llm_mlp % 128 == 0 && c.ae_mlp % 128 == 0, "mlp widths must be multiples of 128");
+    for (int w : {c.ve_width, c.ve_mlp, c.llm_width, c.ae_width})
+        need(w % 8 == 0, "hidden widths must be multiples of 8");
+    need(c.ve_layers >= 1 && c.llm_layers >= 2 && c.ae_layers >= 1, "layer counts");
+}
+
+void Engine::alloc_weights() {
+    const auto& c = c_;
+    auto add = [&](const std::string& id, int k, int m, int inst, bool bias, bool gated = false,
+                   bool table = false) {
+        NodeWeights nw;
+        nw.k = k;
+        nw.m = m;
+        nw.instances = inst;
+        nw.ldk = round_up(k, 8);
+        nw.gated = gated;
+        nw.has_bias = bias;
+        nw.has_table = table;
+        const int rows = gated ? round_up(m, 256) : m;
+        for (int i = 0; i < inst; ++i) {
+            nw.w.push_back(alloc<__nv_bfloat16>(size_t(rows) * nw.ldk));
+            PI0B_CUDA(cudaMemset(nw.w.back(), 0, size_t(rows) * nw.ldk * 2));
+            if (bias) nw.b.push_back(alloc<float>(m));
+        }
+        if (table) nw.table = alloc<float>(size_t(c.flow_steps) * m);
+        W_[id] = std::move(nw);
+    };
+    const int ve_w = c.ve_width, llm_w = c.llm_width, ae_w = c.ae_width;
+    const int llm_qkv = (c.llm_q_heads + 2 * c.llm_kv_heads) * c.llm_head_dim;
+    const int ae_q = c.ae_q_heads * c.ae_head_dim;
+    const int ae_qkv = ae_q + 2 * c.ae_kv_heads * c.ae_head_dim;
+    const int llm_q = c.llm_q_heads * c.llm_head_dim;
+    // Weight-bearing nodes of build_pi0_graph (proj/src/builder.cpp:205-363) with their
+    // binding: Shared 1, PerInstance repeat, PerLayer layer_count (evaluate.cpp:103-111).
+    add("ve.embed", c.ve_patch_in, ve_w, 1, true);
+    add("ve.qkv", ve_w, 3 * ve_w, c.ve_layers, true);
+    add("ve.proj", ve_w, ve_w, c.ve_layers, true);
+    add("ve.fc1", ve_w, c.ve_mlp, c.ve_layers, true);
+    add("ve.fc2", c.ve_mlp, ve_w, c.ve_layers, true);
+    add("llm.proj_in", ve_w, llm_w, 1, true);
+    add("llm.qkv", llm_w, llm_qkv, c.llm_layers, false);
+    add("llm.proj", llm_q, llm_w, c.llm_layers - 1, false);
+    add("llm.ffn", llm_w, 2 * c.llm_mlp, c.llm_layers - 1, false, true);
+    add("llm.down", c.llm_mlp, llm_w, c.llm_layers - 1, false);
+    add("ae.state_proj", c.ae_state_dim, ae_w, 1, true);
+    add("ae.action_proj", c.ae_action_dim, ae_w, 1, false, false, true);
+    add("ae.action_out", ae_w, ae_w, 1, true);
+    add("ae.qkv", ae_w, ae_qkv, c.ae_layers, false);
+    add("ae.proj", ae_q, ae_w, c.ae_layers, false);
+    add("ae.ffn", ae_w, 2 * c.ae_mlp, c.ae_layers, false, true);
+    add("ae.down", c.ae_mlp, ae_w, c.ae_layers, false);
+    add("ae.head", ae_w, c.ae_action_dim, 1, true);
+}
+
+void Engine::alloc_activations() {
+    const auto& c = c_;
+    T_ = c.views * c.tokens_per_view;
+    P_ = c.prompt_tokens;
+    L_ = T_ + P_;
+    C_ = c.chunk_len;
+    S_ = C_ + 1;
+    FS_ = c.flow_steps;
+    ve_w_ = c.ve_width;
+    llm_w_ = c.llm_width;
+    ae_w_ = c.ae_width;
+    llm_q_ = c.llm_q_heads * c.llm_head_dim;
+    llm_kv_ = c.llm_kv_heads * c.llm_head_dim;
+    ae_q_ = c.ae_q_heads * c.ae_head_dim;
+    ae_kv_ = c.ae_kv_heads * c.ae_head_dim;
+    patch_ld_ = round_up(c.ve_patch_in, 8);
+    act_ld_ = round_up(c.ae_action_dim, 8);
+    state_ld_ = round_up(c.ae_state_dim, 8);
+
+    n_patches_ = size_t(T_) * c.ve_patch_in;
+    n_state_ = size_t(c.ae_state_dim);
+    n_noise_ = size_t(C_) * c.ae_action_dim;
+    n_prompt_ = size_t(P_) * llm_w_;
+    n_out_ = n_noise_;
+    d_patches_ = alloc<double>(n_patches_);
+    d_state_ = alloc<double>(n_state_);
+    d_noise_ = alloc<double>(n_noise_);
+    d_prompt_ = alloc<double>(std::max<size_t>(1, n_prompt_));
+    d_out_ = alloc<double>(n_out_);
+    PI0B_CUDA(cudaMallocHost(&h_in_, (n_patches_ + n_state_ + n_noise_ + n_prompt_) * sizeof(double)));
+    PI0B_CUDA(cudaMallocHost(&h_out_, n_out_ * sizeof(double)));
+
+    patches_b_ = alloc<__nv_bfloat16>(size_t(T_) * patch_ld_);
+    PI0B_CUDA(cudaMemset(patches_b_, 0, size_t(T_) * patch_ld_ * 2));
+    ve_h_ = alloc<float>(size_t(T_) * ve_w_);
+    ve_hb_ = alloc<__nv_bfloat16>(size_t(T_) * ve_w_);
+    ve_qkv_ = alloc<__nv_bfloat16>(size_t(T_) * 3 * ve_w_);
+    ve_attn_ = alloc<__nv_bfloat16>(size_t(T_) * ve_w_);
+    ve_mlp_ = alloc<__nv_bfloat16>(size_t(T_) * c.ve_mlp);
+    x_ = alloc<float>(size_t(L_) * llm_w_);
+    xb_ = alloc<__nv_bfloat16>(size_t(L_) * llm_w_);
+    llm_attn_ = alloc<__nv_bfloat16>(size_t(L_) * llm_q_);
+    llm_g_ = alloc<__nv_bfloat16>(size_t(L_) * c.llm_mlp);
+    for (int l = 0; l < c.llm_layers; ++l) kv_.push_back(alloc<__nv_bfloat16>(size_t(L_) * (llm_q_ + 2 * llm_kv_)));
+    state_b_ = alloc<__nv_bfloat16>(size_t(state_ld_));
+    PI0B_CUDA(cudaMemset(state_b_, 0, size_t(state_ld_) * 2));
+    ab_ = alloc<__nv_bfloat16>(size_t(C_) * act_ld_);
+    PI0B_CUDA(cudaMemset(ab_, 0, size_t(C_) * act_ld_ * 2));
+    a_ = alloc<float>(size_t(C_) * act_ld_);
+    ap_b_ = alloc<__nv_bfloat16>(size_t(C_) * ae_w_);
+    st_ = alloc<float>(size_t(ae_w_));
+    y_ = alloc<float>(size_t(S_) * ae_w_);
+    yb_ = alloc<__nv_bfloat16>(size_t(S_) * ae_w_);
+    aqkv_ = alloc<__nv_bfloat16>(size_t(S_) * (ae_q_ + 2 * ae_kv_));
+    ao_ = alloc<__nv_bfloat16>(size_t(S_) * ae_q_);
+    ag_ = alloc<__nv_bfloat16>(size_t(S_) * c.ae_mlp);
+
+    // RoPE table: cos/sin of p * 10000^(-2j/256), evaluated in fp64 as make_rope_table
+    // (proj/src/tensor.cpp:133-148) and rounded to fp32. Positions [0, L+S).
+    const int npos = L_ + S_;
+    std::vector<float> cs(size_t(npos) * 128 * 2);
+    for (int p = 0; p < npos; ++p)
+        for (int j = 0; j < 128; ++j) {
+            const double freq = std::pow(10000.0, -2.0 * double(j) / 256.0);
+            const double ang = double(p) * freq;
+            cs[(size_t(p) * 128 + j) * 2 + 0] = float(std::cos(ang));
+            cs[(size_t(p) * 128 + j) * 2 + 1] = float(std::sin(ang));
+        }
+    rope_cs_ = alloc<float>(cs.size());
+    PI0B_CUDA(cudaMemcpy(rope_cs_, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
+
+    // Row-stat slots: one per residual-stream producer instance, zeroed per replay.
+    stats_rows_ = round_up(std::max(L_, S_), 64);
+    stats_cap_[0] = 2 + 2 * c.ve_layers + 2 * c.llm_layers;
+    stats_cap_[1] = FS_ * (2 + 2 * c.ae_layers) + 2;
+    for (int p = 0; p < 2; ++p) stats_[p] = alloc<float>(size_t(stats_cap_[p]) * stats_rows_);
+}
+
+float* Engine::stats_slot(int part) {
+    if (stats_used_[part] >= stats_cap_[part]) throw EngineError(PI0B_E_STATE, "stats slots exhausted");
+    return stats_[part] + size_t(stats_used_[part]++) * stats_rows_;
+}
+
+void Engine::tag(const std::string& node, int inst, const void* ptr, int rows, int cols, long long ld,
+                 int bf16) {
+    Op& op = ops_.back();
+    op.node = node;
+    op.inst = inst;
+    op.ck_ptr = ptr;
+    op.ck_rows = rows;
+    op.ck_cols = cols;
+    op.ck_ld = ld;
+    op.ck_bf16 = bf16;
+}
+
+void Engine::add_gemm(int part, const std::string& node, int inst, const __nv_bfloat16* A,
+                      long long lda, int M, const NodeWeights& W, int widx, int bn, GemmParams gp,
+                      bool allow_split) {
+    Op op;
+    op.kind = kOpGemm;
+    op.part = part;
+    op.bn = bn;
+    const int N = gp.N;
+    const int K = W.k;
+    const __nv_bfloat16* wptr = W.w.at(size_t(widx));
+    op.ta = make_tmap_bf16(A, M, K, lda, 128);
+    op.tb = make_tmap_bf16(wptr, N, K, W.ldk, bn);
+    gp.M = M;
+    gp.K = K;
+    const int m_tiles = (M + 127) / 128, n_tiles = (N + bn - 1) / bn;
+    const int kb = (K + 63) / 64;
+    int splits = allow_split ? choose_splits(m_tiles, n_tiles, K, num_sms_) : 1;
+    gp.kb_per_split = (kb + splits - 1) / splits;
+    gp.splits = (kb + gp.kb_per_split - 1) / gp.kb_per_split;
+    if (gp.splits > 1 && gp.mode != kModeResid) {
+        gemm_ws_floats_ = std::max(gemm_ws_floats_, size_t(M) * N);
+        gp.ws = nullptr;  // patched after allocation
+    }
+    op.gp = gp;
+    ops_.push_back(op);
+}
+
+void Engine::add_attn(int part, const std::string& node, int inst, int hd, AttnParams ap) {
+    Op op;
+    op.kind = kOpAttn;
+    op.part = part;
+    op.hd = hd;
+    const int grows = (ap.heads / ap.kv_heads) * ap.q_rows;
+    const int q_tiles = (grows + attn_query_tile() - 1) / attn_query_tile();
+    const int total = ap.rows0 + ap.rows1;
+    const int kvt = attn_key_tile(hd);
+    const int ctas = q_tiles * ap.kv_heads;
+    int splits = std::max(1, std::min(num_sms_ / std::max(1, ctas), (total + 63) / 64));
+    int per = round_up((total + splits - 1) / splits, kvt);
+    splits = (total + per - 1) / per;
+    ap.kv_splits = splits;
+    ap.kv_per_split = per;
+    ap.scale_log2 = float(1.4426950408889634 / std::sqrt(double(hd)));
+    if (splits > 1)
+        attn_ws_floats_ = std::max(attn_ws_floats_, size_t(splits) * ap.kv_heads * q_tiles * 64 * (hd + 2));
+    op.ap = ap;
+    ops_.push_back(op);
+    (void)node;
+    (void)inst;
+}
+
+void Engine::build_plan() {
+    const auto& c = c_;
+    auto& Wv = W_;
+    const int ve_qkv_n = 3 * ve_w_;
+    const int llm_qkv_n = llm_q_ + 2 * llm_kv_;
+    const int ae_qkv_n = ae_q_ + 2 * ae_kv_;
+
+    // ================================================================ prefix (part 0)
+    {
+        Op m;
+        m.kind = kOpMemset;
+        m.part = 0;
+        m.mptr = stats_[0];
+        m.mbytes = size_t(stats_cap_[0]) * stats_rows_ * 4;
+        ops_.push_back(m);
+        Op cv;
+        cv.kind = kOpF64Bf16;
+        cv.part = 0;
+        cv.src64 = d_patches_;
+        cv.rows = T_;
+        cv.cols = c.ve_patch_in;
+        cv.dstb = patches_b_;
+        cv.ldb = patch_ld_;
+        ops_.push_back(cv);
+    }
+    // --- vision encoder (proj/src/builder.cpp:205-240)
+    float* st = stats_slot(0);
+    {
+        GemmParams g{};
+        g.N = ve_w_;
+        g.mode = kModeF32Store;
+        g.flags = kFlagBias;
+        g.bias = Wv["ve.embed"].b[0];
+        g.out = ve_h_;
+        g.ldo = ve_w_;
+        g.outb = ve_hb_;
+        g.ldob = ve_w_;
+        g.out_stats = st;
+        add_gemm(0, "ve.embed", 0, patches_b_, patch_ld_, T_, Wv["ve.embed"], 0, 128, g);
+        tag("ve.embed", 0, ve_h_, T_, ve_w_, ve_w_, 0);
+    }
+    const float inv_ve = 1.0f / float(ve_w_);
+    for (int i = 0; i < c.ve_layers; ++i) {
+        {   // ve.ln1 + ve.qkv: (h W) * rms(h) + b
+            GemmParams g{};
+            g.N = ve_qkv_n;
+            g.mode = kModeBf16;
+            g.flags = kFlagRowScale | kFlagBias;
+            g.row_stats = st;
+            g.inv_width = inv_ve;
+            g.eps = 1e-6f;
+            g.bias = Wv["ve.qkv"].b[i];
+            g.out = ve_qkv_;
+            g.ldo = ve_qkv_n;
+            add_gemm(0, "ve.qkv", i, ve_hb_, ve_w_, T_, Wv["ve.qkv"], i, 128, g);
+            tag("ve.qkv", i, ve_qkv_, T_, ve_qkv_n, ve_qkv_n, 1);
+        }
+        {   // ve.attn: joint over all views' tokens, no mask
+            AttnParams a{};
+            a.q = ve_qkv_;
+            a.ldq = ve_qkv_n;
+            a.q_rows = T_;
+            a.heads = c.ve_heads;
+            a.kv_heads = c.ve_heads;
+            a.k0 = ve_qkv_ + ve_w_;
+            a.v0 = ve_qkv_ + 2 * ve_w_;
+            a.ld0 = ve_qkv_n;
+            a.rows0 = T_;
+            a.out = ve_attn_;
+            a.ldo = ve_w_;
+            add_attn(0, "ve.attn", i, c.ve_head_dim, a);
+            tag("ve.attn", i, ve_attn_, T_, ve_w_, ve_w_, 1);
+        }
+        float* st2 = stats_slot(0);
+        {   // ve.proj: h += attn W + b
+            GemmParams g{};
+            g.N = ve_w_;
+            g.mode = kModeResid;
+            g.flags = kFlagBias;
+            g.bias = Wv["ve.proj"].b[i];
+            g.resid_scale = 1.0f;
+            g.out = ve_h_;
+            g.ldo = ve_w_;
+            g.outb = ve_hb_;
+            g.ldob = ve_w_;
+            g.out_stats = st2;
+            add_gemm(0, "ve.proj", i, ve_attn_, ve_w_, T_, Wv["ve.proj"], i, 128, g);
+            tag("ve.proj", i, ve_h_, T_, ve_w_, ve_w_, 0);
+        }
+        {   // ve.ln2 + ve.fc1: gelu((p W) * rms(p) + b)
+            GemmParams g{};
+            g.N = c.ve_mlp;
+            g.mode = kModeBf16;
+            g.flags = kFlagRowScale | kFlagBias | kFlagGelu;
+            g.row_stats = st2;
+            g.inv_width = inv_ve;
+            g.eps = 1e-6f;
+            g.bias = Wv["ve.fc1"].b[i];
+            g.out = ve_mlp_;
+            g.ldo = c.ve_mlp;
+            add_gemm(0, "ve.fc1", i, ve_hb_, ve_w_, T_, Wv["ve.fc1"], i, 128, g);
+            tag("ve.fc1", i, ve_mlp_, T_, c.ve_mlp, c.ve_mlp, 1);
+        }
+        st = stats_slot(0);
+        {   // ve.fc2: h += mlp W + b
+            GemmParams g{};
+            g.N = ve_w_;
+            g.mode = kModeResid;
+            g.flags = kFlagBias;
+            g.bias = Wv["ve.fc2"].b[i];
+            g.resid_scale = 1.0f;
+            g.out = ve_h_;
+            g.ldo = ve_w_;
+            g.outb = ve_hb_;
+            g.ldob = ve_w_;
+            g.out_stats = st;
+            add_gemm(0, "ve.fc2", i, ve_mlp_, c.ve_mlp, T_, Wv["ve.fc2"], i, 128, g);
+            tag("ve.fc2", i, ve_h_, T_, ve_w_, ve_w_, 0);
+        }
+    }
+    // --- language model (proj/src/builder.cpp:242-289)
+    float* xs = stats_slot(0);
+    {   // ve.ln_out + llm.proj_in -> x rows [0, T)
+        GemmParams g{};
+        g.N = llm_w_;
+        g.mode = kModeF32Store;
+        g.flags = kFlagRowScale | kFlagBias;
+        g.row_stats = st;
+        g.inv_width = inv_ve;
+        g.eps = 1e-6f;
+        g.bias = Wv["llm.proj_in"].b[0];
+        g.out = x_;
+        g.ldo = llm_w_;
+        g.outb = xb_;
+        g.ldob = llm_w_;
+        g.out_stats = xs;
+        add_gemm(0, "llm.proj_in", 0, ve_hb_, ve_w_, T_, Wv["llm.proj_in"], 0, 256, g);
+        tag("llm.proj_in", 0, x_, T_, llm_w_, llm_w_, 0);
+    }
+    if (P_ > 0) {   // llm.tokens = concat_rows(proj_in, prompt)
+        Op cv;
+        cv.kind = kOpRowsF32;
+        cv.part = 0;
+        cv.src64 = d_prompt_;
+        cv.rows = P_;
+        cv.cols = llm_w_;
+        cv.dst32 = x_ + size_t(T_) * llm_w_;
+        cv.ld32 = llm_w_;
+        cv.dstb = xb_ + size_t(T_) * llm_w_;
+        cv.ldb = llm_w_;
+        cv.stats = xs + T_;
+        ops_.push_back(cv);
+        tag("llm.tokens", 0, x_, L_, llm_w_, llm_w_, 0);
+    }
+    const float inv_llm = 1.0f / float(llm_w_);
+    const int NL = c.llm_layers;
+    for (int l = 0; l < NL; ++l) {
+        {   // llm.ln1 + llm.qkv, RoPE at positions 0..L-1 -> KV cache layer l
+            GemmParams g{};
+            g.mode = kModeBf16;
+            g.flags = kFlagRowScale | kFlagRope;
+            g.row_stats = xs;
+            g.inv_width = inv_llm;
+            g.eps = 1e-6f;
+            g.rope_cs = rope_cs_;
+            g.rope_pos0 = 0;
+            g.ldo = llm_qkv_n;
+            if (l < NL - 1) {
+                g.N = llm_qkv_n;
+                g.rope_cols = llm_q_ + llm_kv_;
+                g.out = kv_[l];
+                add_gemm(0, "llm.qkv", l, xb_, llm_w_, L_, Wv["llm.qkv"], l, 256, g);
+            } else {
+                // Last layer: only K/V feed the action expert; its Q is dead.
+                NodeWeights sub = Wv["llm.qkv"];
+                sub.w[l] = Wv["llm.qkv"].w[l] + size_t(llm_q_) * sub.ldk;
+                g.N = 2 * llm_kv_;
+                g.rope_cols = llm_kv_;
+                g.out = kv_[l] + llm_q_;
+                add_gemm(0, "llm.qkv", l, xb_, llm_w_, L_, sub, l, 256, g);
+            }
+            tag("llm.qkv", l, kv_[l], L_, llm_qkv_n, llm_qkv_n, 1);
+        }
+        if (l == NL - 1) break;
+        {
+            AttnParams a{};
+            a.q = kv_[l];
+            a.ldq = llm_qkv_n;
+            a.q_rows = L_;
+            a.heads = c.llm_q_heads;
+            a.kv_heads = c.llm_kv_heads;
+            a.k0 = kv_[l] + llm_q_;
+            a.v0 = kv_[l] + llm_q_ + llm_kv_;
+            a.ld0 = llm_qkv_n;
+            a.rows0 = L_;
+            a.out = llm_attn_;
+            a.ldo = llm_q_;
+            add_attn(0, "llm.attn", l, 256, a);
+            tag("llm.attn", l, llm_attn_, L_, llm_q_, llm_q_, 1);
+        }
+        float* ps = stats_slot(0);
+        {
+            GemmParams g{};
+            g.N = llm_w_;
+            g.mode = kModeResid;
+            g.resid_scale = 1.0f;
+            g.out = x_;
+            g.ldo = llm_w_;
+            g.outb = xb_;
+            g.ldob = llm_w_;
+            g.out_stats = ps;
+            add_gemm(0, "llm.proj", l, llm_attn_, llm_q_, L_, Wv["llm.proj"], l, 256, g);
+            tag("llm.proj", l, x_, L_, llm_w_, llm_w_, 0);
+        }
+        {   // llm.ln2 + fused gated FFN: up * gelu(gate)
+            GemmParams g{};
+            g.N = 2 * c.llm_mlp;
+            g.mode = kModeGate;
+            g.flags = kFlagRowScale;
+            g.row_stats = ps;
+            g.inv_width = inv_llm;
+            g.eps = 1e-6f;
+            g.out = llm_g_;
+            g.ldo = c.llm_mlp;
+            add_gemm(0, "llm.ffn", l, xb_, llm_w_, L_, Wv["llm.ffn"], l, 256, g);
+            tag("llm.ffn", l, llm_g_, L_, c.llm_mlp, c.llm_mlp, 1);
+        }
+        xs = stats_slot(0);
+        {
+            GemmParams g{};
+            g.N = llm_w_;
+            g.mode = kModeResid;
+            g.resid_scale = 1.0f;
+            g.out = x_;
+            g.ldo = llm_w_;
+            g.outb = xb_;
+            g.ldob = llm_w_;
+            g.out_stats = xs;
+            add_gemm(0, "llm.down", l, llm_g_, c.llm_mlp, L_, Wv["llm.down"], l, 256, g);
+            tag("llm.down", l, x_, L_, llm_w_, llm_w_, 0);
+        }
+    }
+
+    // ================================================================ action expert (part 1)
+    // (proj/src/builder.cpp:291-363)
+    {
+        Op m;
+        m.kind = kOpMemset;
+        m.part = 1;
+        m.mptr = stats_[1];
+        m.mbytes = size_t(stats_cap_[1]) * stats_rows_ * 4;
+        ops_.push_back(m);
+        Op cs;
+        cs.kind = kOpF64Bf16;
+        cs.part = 1;
+        cs.src64 = d_state_;
+        cs.rows = 1;
+        cs.cols = c.ae_state_dim;
+        cs.dstb = state_b_;
+        cs.ldb = state_ld_;
+        ops_.push_back(cs);
+        Op cn;
+        cn.kind = kOpRowsF32;
+        cn.part = 1;
+        cn.src64 = d_noise_;
+        cn.rows = C_;
+        cn.cols = c.ae_action_dim;
+        cn.dst32 = a_;
+        cn.ld32 = act_ld_;
+        cn.dstb = ab_;
+        cn.ldb = act_ld_;
+        ops_.push_back(cn);
+    }
+    {
+        GemmParams g{};
+        g.N = ae_w_;
+        g.mode = kModeF32Store;
+        g.flags = kFlagBias;
+        g.bias = Wv["ae.state_proj"].b[0];
+        g.out = st_;
+        g.ldo = ae_w_;
+        add_gemm(1, "ae.state_proj", 0, state_b_, state_ld_, 1, Wv["ae.state_proj"], 0, 128, g);
+        tag("ae.state_proj", 0, st_, 1, ae_w_, ae_w_, 0);
+    }
+    const float inv_ae = 1.0f / float(ae_w_);
+    const int NA = c.ae_layers;
+    for (int s = 0; s < FS_; ++s) {
+        {   // action_proj with folded time MLP: silu(a W + T[s])
+            GemmParams g{};
+            g.N = ae_w_;
+            g.mode = kModeSiluTable;
+            g.table_row = Wv["ae.action_proj"].table + size_t(s) * ae_w_;
+            g.out = ap_b_;
+            g.ldo = ae_w_;
+            add_gemm(1, "ae.action_proj", s, ab_, act_ld_, C_, Wv["ae.action_proj"], 0, 128, g);
+            tag("ae.action_proj", s, ap_b_, C_, ae_w_, ae_w_, 1);
+        }
+        float* ys = stats_slot(1);
+        {   // action_out + bias -> y rows 1..63, state token -> y row 0 (ae.suffix)
+            GemmParams g{};
+            g.N = ae_w_;
+            g.mode = kModeF32Store;
+            g.flags = kFlagBias;
+            g.bias = Wv["ae.action_out"].b[0];
+            g.out = y_ + ae_w_;
+            g.ldo = ae_w_;
+            g.outb = yb_ + ae_w_;
+            g.ldob = ae_w_;
+            g.out_stats = ys + 1;
+            g.row0_src = st_;
+            add_gemm(1, "ae.action_out", s, ap_b_, ae_w_, C_, Wv["ae.action_out"], 0, 128, g);
+            tag("ae.suffix", s, y_, S_, ae_w_, ae_w_, 0);
+        }
+        for (int l = 0; l < NA; ++l) {
+            const int i = s * NA + l;
+            {   // ae.ln1 + ae.qkv, RoPE at positions L..L+63
+                GemmParams g{};
+                g.N = ae_qkv_n;
+                g.mode = kModeBf16;
+                g.flags = kFlagRowScale | kFlagRope;
+                g.row_stats = ys;
+                g.inv_width = inv_ae;
+                g.eps = 1e-6f;
+                g.rope_cs = rope_cs_;
+                g.rope_pos0 = L_;
+                g.rope_cols = ae_q_ + ae_kv_;
+                g.out = aqkv_;
+                g.ldo = ae_qkv_n;
+                add_gemm(1, "ae.qkv", i, yb_, ae_w_, S_, Wv["ae.qkv"], l, 256, g);
+                tag("ae.qkv", i, aqkv_, S_, ae_qkv_n, ae_qkv_n, 1);
+            }
+            {   // cross attention over [LLM KV_l ; own KV] (ae.kcat / ae.vcat)
+                AttnParams a{};
+                a.q = aqkv_;
+                a.ldq = ae_qkv_n;
+                a.q_rows = S_;
+                a.heads = c.ae_q_heads;
+                a.kv_heads = c.ae_kv_heads;
+                a.k0 = kv_[i % NL] + llm_q_;  // llm.qkv@mod (instance i % R)
+                a.v0 = kv_[i % NL] + llm_q_ + llm_kv_;
+                a.ld0 = llm_qkv_n;
+                a.rows0 = L_;
+                a.k1 = aqkv_ + ae_q_;
+                a.v1 = aqkv_ + ae_q_ + ae_kv_;
+                a.ld1 = ae_qkv_n;
+                a.rows1 = S_;
+                a.out = ao_;
+                a.ldo = ae_q_;
+                add_attn(1, "ae.attn", i, 256, a);
+                tag("ae.attn", i, ao_, S_, ae_q_, ae_q_, 1);
+            }
+            float* ps = stats_slot(1);
+            {
+                GemmParams g{};
+                g.N = ae_w_;
+                g.mode = kModeResid;
+                g.resid_scale = 1.0f;
+                g.out = y_;
+                g.ldo = ae_w_;
+                g.outb = yb_;
+                g.ldob = ae_w_;
+                g.out_stats = ps;
+                add_gemm(1, "ae.proj", i, ao_, ae_q_, S_, Wv["ae.proj"], l, 128, g);
+                tag("ae.proj", i, y_, S_, ae_w_, ae_w_, 0);
+            }
+            {
+                GemmParams g{};
+                g.N = 2 * c.ae_mlp;
+                g.mode = kModeGate;
+                g.flags = kFlagRowScale;
+                g.row_stats = ps;
+                g.inv_width = inv_ae;
+                g.eps = 1e-6f;
+                g.out = ag_;
+                g.ldo = c.ae_mlp;
+                add_gemm(1, "ae.ffn", i, yb_, ae_w_, S_, Wv["ae.ffn"], l, 256, g);
+                tag("ae.ffn", i, ag_, S_, c.ae_mlp, c.ae_mlp, 1);
+            }
+            ys = stats_slot(1);
+            {
+                GemmParams g{};
+                g.N = ae_w_;
+                g.mode = kModeResid;
+                g.resid_scale = 1.0f;
+                g.out = y_;
+                g.ldo = ae_w_;
+                g.outb = yb_;
+                g.ldob = ae_w_;
+                g.out_stats = ys;
+                add_gemm(1, "ae.down", i, ag_, c.ae_mlp, S_, Wv["ae.down"], l, 128, g);
+                tag("ae.down", i, y_, S_, ae_w_, ae_w_, 0);
+            }
+        }
+        {   // ae.act_rows + ae.ln_out + ae.head + Euler: a += (r W * rms(r) + b) / FS
+            GemmParams g{};
+            g.N = c.ae_action_dim;
+            g.mode = kModeResid;
+            g.flags = kFlagRowScale | kFlagBias;
+            g.row_stats = ys + 1;
+            g.inv_width = inv_ae;
+            g.eps = 1e-6f;
+            g.bias = Wv["ae.head"].b[0];
+            g.resid_scale = float(1.0 / double(FS_));
+            g.out = a_;
+            g.ldo = act_ld_;
+            g.outb = ab_;
+            g.ldob = act_ld_;
+            add_gemm(1, "ae.head", s, yb_ + ae_w_, ae_w_, C_, Wv["ae.head"], 0, 64, g);
+            tag("ae.head", s, a_, C_, c.ae_action_dim, act_ld_, 0);
+        }
+    }
+    {
+        Op o;
+        o.kind = kOpF32F64;
+        o.part = 1;
+        o.src32 = a_;
+        o.ld32 = act_ld_;
+        o.rows = C_;
+        o.cols = c.ae_action_dim;
+        o.dst64 = d_out_;
+        ops_.push_back(o);
+    }
+
+    // scratch shared by all launches (stream-ordered, self-cleaning)
+    gemm_ws_ = alloc<float>(std::max<size_t>(gemm_ws_floats_, 1));
+    PI0B_CUDA(cudaMemset(gemm_ws_, 0, std::max<size_t>(gemm_ws_floats_, 1) * 4));
+    gemm_ctr_ = alloc<int>(4096);
+    PI0B_CUDA(cudaMemset(gemm_ctr_, 0, 4096 * 4));
+    attn_ws_ = alloc<float>(std::max<size_t>(attn_ws_floats_, 1));
+    attn_ctr_ = alloc<int>(4096);
+    PI0B_CUDA(cudaMemset(attn_ctr_, 0, 4096 * 4));
+    for (auto& op : ops_) {
+        if (op.kind == kOpGemm) {
+            op.gp.ws = gemm_ws_;
+            op.gp.counters = gemm_ctr_;
+        } else if (op.kind == kOpAttn) {
+            const int grows = (op.ap.heads / op.ap.kv_heads) * op.ap.q_rows;
+            const long long rows_pad = (long long)((grows + 63) / 64) * 64;
+            op.ap.ws_o = attn_ws_;
+            op.ap.ws_ml = attn_ws_ + size_t(op.ap.kv_splits) * op.ap.kv_heads * rows_pad * op.hd;
+            op.ap.counters = attn_ctr_;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ weights
+
+void Engine::gen_weights(uint64_t seed) {
+    // rtvla::gen_weights (proj/src/evaluate.cpp:38-75): W ~ U(+-1/sqrt(k)) seeded by
+    // (seed, node id, instance, 1); bias role 2; bias_table row s role 4.
+    for (auto& kv : W_) {
+        const std::string& id = kv.first;
+        NodeWeights& nw = kv.second;
+        const double lim = 1.0 / std::sqrt(double(std::max(1, nw.k)));
+        for (int i = 0; i < nw.instances; ++i) {
+            PI0B_CUDA(launch_gen_weight(nw.w[i], nw.ldk, nw.k, nw.m, nw.gated ? 1 : 0,
+                                        seed_hash(seed, id, uint64_t(i), 1), -lim, lim, stream_));
+            if (nw.has_bias)
+                PI0B_CUDA(launch_gen_vector(nw.b[i], nw.m, seed_hash(seed, id, uint64_t(i), 2), -lim, lim, stream_));
+        }
+        if (nw.has_table)
+            for (int s = 0; s < FS_; ++s)
+                PI0B_CUDA(launch_gen_vector(nw.table + size_t(s) * nw.m, nw.m,
+                                            seed_hash(seed, id, uint64_t(s), 4), -lim, lim, stream_));
+    }
+    PI0B_CUDA(cudaStreamSynchronize(stream_));
+    weights_loaded_ = true;
+}
+
+void Engine::set_weight(const std::string& id, long long inst, const double* w, long long k, long long m,
+                        const double* bias, long long blen) {
+    auto it = W_.find(id);
+    if (it == W_.end()) throw EngineError(PI0B_E_INVALID, "no weight-bearing node '" + id + "'");
+    NodeWeights& nw = it->second;
+    if (inst < 0 || inst >= nw.instances)
+        throw EngineError(PI0B_E_INVALID, "node '" + id + "': weight instance out of range");
+    if (k != nw.k || m != nw.m) throw EngineError(PI0B_E_INVALID, "node '" + id + "': weight shape mismatch");
+    if (nw.has_bias && (!bias || blen != nw.m))
+        throw EngineError(PI0B_E_INVALID, "node '" + id + "': bias missing or wrong length");
+    double* dw = nullptr;
+    PI0B_CUDA(cudaMalloc(&dw, size_t(k) * m * 8));
+    PI0B_CUDA(cudaMemcpy(dw, w, size_t(k) * m * 8, cudaMemcpyHostToDevice));
+    cudaError_t e = launch_pack_weight(nw.w[size_t(inst)], nw.ldk, dw, int(k), int(m), nw.gated ? 1 : 0, stream_);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream_);
+    cudaFree(dw);
+    PI0B_CUDA(e);
+    if (nw.has_bias) {
+        std::vector<float> b(static_cast<size_t>(m));
+        for (long long j = 0; j < m; ++j) b[size_t(j)] = float(bias[j]);
+        PI0B_CUDA(cudaMemcpy(nw.b[size_t(inst)], b.data(), size_t(m) * 4, cudaMemcpyHostToDevice));
+    }
+    weights_loaded_ = true;
+}
+
+void Engine::set_bias_table(const std::string& id, const double* t, long long rows, long long m) {
+    auto it = W_.find(id);
+    if (it == W_.end() || !it->second.has_table)
+        throw EngineError(PI0B_E_INVALID, "node '" + id + "' has no bias table");
+    if (rows != FS_ || m != it->second.m) throw EngineError(PI0B_E_INVALID, "bias table shape mismatch");
+    std::vector<float> f(size_t(rows * m));
+    for (size_t i = 0; i < f.size(); ++i) f[i] = float(t[i]);
+    PI0B_CUDA(cudaMemcpy(it->second.table, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+}
+
+// ------------------------------------------------------------------ execution
+
+void Engine::upload_inputs(const double* patches, const double* state, const double* noise,
+                           const double* prompt, int which) {
+    // which: 0 = all, 1 = prefix inputs, 2 = action inputs. Copies go through pinned
+    // staging so the H2D transfers are asynchronous DMA on the engine stream.
+    double* h = h_in_;
+    auto stage = [&](const double* src, size_t n, double* dev) {
+        if (!n) return;
+        if (!src) throw EngineError(PI0B_E_INVALID, "missing input tensor");
+        std::memcpy(h, src, n * 8);
+        PI0B_CUDA(cudaMemcpyAsync(dev, h, n * 8, cudaMemcpyHostToDevice, stream_));
+        h += n;
+    };
+    if (which == 0 || which == 1) {
+        stage(patches, n_patches_, d_patches_);
+        if (P_ > 0) stage(prompt, n_prompt_, d_prompt_);
+    }
+    if (which == 0 || which == 2) {
+        stage(state, n_state_, d_state_);
+        stage(noise, n_noise_, d_noise_);
+    }
+}
+
+void Engine::run_ops(int part, cudaStream_t st) {
+    for (const Op& op : ops_) {
+        if (part != 2 && op.part != part) continue;  // part 2 = everything
+        switch (op.kind) {
+            case kOpGemm: PI0B_CUDA(launch_gemm(op.bn, op.ta, op.tb, op.gp, st)); break;
+            case kOpAttn: PI0B_CUDA(launch_attention(op.hd, op.ap, st)); break;
+            case kOpRowsF32:
+                PI0B_CUDA(launch_rows_to_f32(op.src64, op.rows, op.cols, op.dst32, op.ld32, op.dstb, op.ldb,
+                                             op.stats, st));
+                break;
+            case kOpF64Bf16:
+                PI0B_CUDA(launch_f64_to_bf16_rows(op.src64, op.rows, op.cols, op.dstb, op.ldb, st));
+                break;
+            case kOpF32F64: PI0B_CUDA(launch_f32_to_f64(op.src32, op.ld32, op.rows, op.cols, op.dst64, st)); break;
+            case kOpMemset: PI0B_CUDA(cudaMemsetAsync(op.mptr, 0, op.mbytes, st)); break;
+        }
+        if (o_.record_checkpoints && op.inst >= 0) {
+            const auto key = std::make_pair(op.node, op.inst);
+            Checkpoint& ck = ck_[key];
+            const size_t esz = op.ck_bf16 ? 2 : 4;
+            if (!ck.dev) {
+                PI0B_CUDA(cudaMalloc(&ck.dev, size_t(op.ck_rows) * op.ck_cols * esz));
+                ck.rows = op.ck_rows;
+                ck.cols = op.ck_cols;
+                ck.bf16 = op.ck_bf16;
+            }
+            PI0B_CUDA(cudaMemcpy2DAsync(ck.dev, op.ck_cols * esz, op.ck_ptr, op.ck_ld * esz,
+                                        op.ck_cols * esz, op.ck_rows, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+}
+
+void Engine::capture(int part) {
+    cudaGraph_t g = nullptr;
+    PI0B_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    try {
+        run_ops(part, stream_);
+    } catch (...) {
+        cudaStreamEndCapture(stream_, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+    }
+    PI0B_CUDA(cudaStreamEndCapture(stream_, &g));
+    cudaError_t e = cudaGraphInstantiate(&graph_[part], g, 0);
+    cudaGraphDestroy(g);
+    PI0B_CUDA(e);
+}
+
+// part: 0 = full, 1 = prefix, 2 = action (C-ABI numbering)
+void Engine::launch(int part, cudaStream_t st) {
+    if (!weights_loaded_) throw EngineError(PI0B_E_STATE, "weights not loaded");
+    const int internal = part == 0 ? 2 : part - 1;  // ops filter: 2 all, 0 prefix, 1 action
+    const int gidx = part;
+    if (o_.use_cuda_graph && !o_.record_checkpoints) {
+        if (!graph_[gidx]) capture(internal);
+        PI0B_CUDA(cudaGraphLaunch(graph_[gidx], st));
+    } else {
+        run_ops(internal, st);
+    }
+}
+
+void Engine::fetch_actions(double* out) {
+    PI0B_CUDA(cudaMemcpyAsync(h_out_, d_out_, n_out_ * 8, cudaMemcpyDeviceToHost, stream_));
+    PI0B_CUDA(cudaStreamSynchronize(stream_));
+    for (size_t i = 0; i < n_out_; ++i)
+        if (!std::isfinite(h_out_[i])) throw EngineError(PI0B_E_NUMERIC, "non-finite action output");
+    std::memcpy(out, h_out_, n_out_ * 8);
+}
+
+int Engine::kernel_count(int part) const {
+    const int internal = part == 0 ? 2 : part - 1;
+    int n = 0;
+    for (const Op& op : ops_)
+        if ((internal == 2 || op.part == internal) && op.is_kernel()) ++n;
+    return n;
+}
+
+void Engine::read_checkpoint(const std::string& id, long long inst, float* out, long long rows, long long cols) {
+    auto it = ck_.find(std::make_pair(id, int(inst)));
+    if (it == ck_.end()) throw EngineError(PI0B_E_STATE, "no checkpoint for " + id + "[" + std::to_string(inst) + "]");
+    const Checkpoint& ck = it->second;
+    if (rows != ck.rows || cols != ck.cols) throw EngineError(PI0B_E_INVALID, "checkpoint shape mismatch");
+    PI0B_CUDA(cudaStreamSynchronize(stream_));
+    const size_t n = size_t(rows) * cols;
+    if (ck.bf16) {
+        std::vector<__nv_bfloat16> tmp(n);
+        PI0B_CUDA(cudaMemcpy(tmp.data(), ck.dev, n * 2, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < n; ++i) out[i] = __bfloat162float(tmp[i]);
+    } else {
+        PI0B_CUDA(cudaMemcpy(out, ck.dev, n * 4, cudaMemcpyDeviceToHost));
+    }
+}
+
+}  // namespace pi0b
+
+// ====================================================================== C-ABI
+
+using pi0b::Engine;
+using pi0b::EngineError;
+
+struct pi0b_engine {
+    std::unique_ptr<Engine> impl;
+};
+
+#define PI0B_TRY(body)                                                         \
+    try {                                                                      \
+        body;                                                                  \
+        return PI0B_OK;                                                        \
+    } catch (const EngineError& e) {                                           \
+        return pi0b::fail(e);                                                  \
+    } catch (const std::exception& e) {                                        \
+        return pi0b::fail(EngineError(PI0B_E_INVALID, e.what()));              \
+    }
+
+extern "C" {
+
+void pi0b_default_config(pi0b_model_config* c) {
+    *c = pi0b_model_config{2, 0, 256, 63, 10, 27, 1152, 16, 72, 4304, 588, 18, 2048, 8, 256, 1, 16384,
+                           18, 1024, 8, 256, 1, 4096, 32, 32};
+}
+
+int pi0b_engine_create(const pi0b_model_config* cfg, const pi0b_engine_options* opt, pi0b_engine** out) {
+    if (!cfg || !out) return pi0b::fail(EngineError(PI0B_E_INVALID, "null argument"));
+    pi0b_engine_options o{0, 1, 0};
+    if (opt) o = *opt;
+    PI0B_TRY({
+        auto* e = new pi0b_engine;
+        try {
+            e->impl.reset(new Engine(*cfg, o));
+        } catch (...) {
+            delete e;
+            throw;
+        }
+        *out = e;
+    })
+}
+
+void pi0b_engine_destroy(pi0b_engine* e) { delete e; }
+
+int pi0b_engine_gen_weights(pi0b_engine* e, uint64_t seed) { PI0B_TRY(e->impl->gen_weights(seed)) }
+
+int pi0b_engine_set_weight(pi0b_engine* e, const char* id, int64_t inst, const double* w, int64_t k,
+                           int64_t m, const double* bias, int64_t blen) {
+    PI0B_TRY(e->impl->set_weight(id, inst, w, k, m, bias, blen))
+}
+
+int pi0b_engine_set_bias_table(pi0b_engine* e, const char* id, const double* t, int64_t rows, int64_t m) {
+    PI0B_TRY(e->impl->set_bias_table(id, t, rows, m))
+}
+
+int pi0b_engine_run(pi0b_engine* e, const double* patches, const double* state, const double* noise,
+                    const double* prompt, double* out) {
+    PI0B_TRY({
+        e->impl->upload_inputs(patches, state, noise, prompt, 0);
+        e->impl->launch(0, e->impl->stream());
+        e->impl->fetch_actions(out);
+    })
+}
+
+int pi0b_engine_run_prefix(pi0b_engine* e, const double* patches, const double* prompt) {
+    PI0B_TRY({
+        e->impl->upload_inputs(patches, nullptr, nullptr, prompt, 1);
+        e->impl->launch(1, e->impl->stream());
+        PI0B_CUDA(cudaStreamSynchronize(e->impl->stream()));
+    })
+}
+
+int pi0b_engine_run_action(pi0b_engine* e, const double* state, const double* noise, double* out) {
+    PI0B_TRY({
+        e->impl->upload_inputs(nullptr, state, noise, nullptr, 2);
+        e->impl->launch(2, e->impl->stream());
+        e->impl->fetch_actions(out);
+    })
+}
+
+int pi0b_engine_replay(pi0b_engine* e, int part, void* stream) {
+    PI0B_TRY({
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : e->impl->stream();
+        e->impl->launch(part, st);
+    })
+}
+
+int pi0b_engine_sync(pi0b_engine* e) { PI0B_TRY(PI0B_CUDA(cudaStreamSynchronize(e->impl->stream()))) }
+
+int pi0b_engine_kernel_count(pi0b_engine* e, int part) { return e->impl->kernel_count(part); }
+
+int pi0b_engine_read_checkpoint(pi0b_engine* e, const char* id, int64_t inst, float* out, int64_t rows,
+                                int64_t cols) {
+    PI0B_TRY(e->impl->read_checkpoint(id, inst, out, rows, cols))
+}
+
+const char* pi0b_last_error(void) { return pi0b::g_last_error.c_str(); }
+
+}  // extern "C"

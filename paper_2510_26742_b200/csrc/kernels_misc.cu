@@ -1,0 +1,144 @@
+// Non-GEMM kernels of the engine:
+//   * gen_weight_kernel   - device-side `gen_weights` (proj/src/evaluate.cpp:38-75): every
+//                           W[k, m] element of a weight instance is drawn from its own
+//                           SplitMix64 counter and written, rounded to bf16, straight into
+//                           the packed [N, K] K-major layout the GEMM consumes;
+//   * pack_weight_kernel  - the same packing for host-supplied fp64 weights (WeightStore);
+//   * gen_vector_kernel   - biases / bias-table rows as fp32;
+//   * rows_to_f32_kernel  - fp64 input rows -> fp32 residual rows + bf16 shadow + row
+//                           sum-of-squares (noise -> Euler state, prompt -> LLM rows);
+//   * f64_to_bf16_kernel  - fp64 rows -> bf16 rows with a padded pitch (patches, state);
+//   * f32_to_f64_kernel   - the [63, 32] action chunk back to fp64.
+#include "numerics.cuh"
+#include "ptx.cuh"
+
+namespace pi0b {
+
+// Packed row of logical weight column j (0 <= j < m).  Gated FFN weights
+// ([up | gate], proj/src/passes.cpp:448) are interleaved per 256-wide GEMM tile:
+// tile t holds up columns [128t, 128t+128) then the matching gate columns.
+__host__ __device__ inline int packed_row(int j, int m, int gated) {
+    if (!gated) return j;
+    const int half = m / 2;
+    const bool gate = j >= half;
+    const int c = gate ? j - half : j;
+    return (c / 128) * 256 + (gate ? 128 : 0) + (c % 128);
+}
+
+// grid: (ceil(k/8 / 32), m) ; block 32 -> each thread emits 8 consecutive k of column j.
+__global__ void gen_weight_kernel(__nv_bfloat16* dst, long long ldk, int k, int m, int gated,
+                                  uint64_t seed, double lo, double hi) {
+    const int j = blockIdx.y;
+    const int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (p0 >= k) return;
+    uint16_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int pp = p0 + i;
+        v[i] = pp < k ? f64_to_bf16_bits(uniform_at(seed, uint64_t(pp) * m + j, lo, hi)) : 0;
+    }
+    uint16_t* out = reinterpret_cast<uint16_t*>(dst) + (long long)packed_row(j, m, gated) * ldk + p0;
+    if (p0 + 8 <= k && (ldk % 8) == 0) {
+        uint4 u;
+        u.x = v[0] | (uint32_t(v[1]) << 16);
+        u.y = v[2] | (uint32_t(v[3]) << 16);
+        u.z = v[4] | (uint32_t(v[5]) << 16);
+        u.w = v[6] | (uint32_t(v[7]) << 16);
+        *reinterpret_cast<uint4*>(out) = u;
+    } else {
+        for (int i = 0; i < 8 && p0 + i < k; ++i) out[i] = v[i];
+    }
+}
+
+// Host fp64 W[k, m] (already on device) -> packed bf16 [N, K].
+__global__ void pack_weight_kernel(__nv_bfloat16* dst, long long ldk, const double* w, int k, int m,
+                                   int gated) {
+    const int j = blockIdx.y;
+    const int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (p0 >= k) return;
+    uint16_t* out = reinterpret_cast<uint16_t*>(dst) + (long long)packed_row(j, m, gated) * ldk + p0;
+    for (int i = 0; i < 8 && p0 + i < k; ++i) out[i] = f64_to_bf16_bits(w[(long long)(p0 + i) * m + j]);
+}
+
+__global__ void gen_vector_kernel(float* dst, int n, uint64_t seed, double lo, double hi) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = float(uniform_at(seed, uint64_t(i), lo, hi));
+}
+
+__global__ void f64_to_f32_kernel(float* dst, const double* src, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = float(src[i]);
+}
+
+// One warp per row.
+__global__ void rows_to_f32_kernel(const double* src, int rows, int cols, float* dst, long long ldd,
+                                   __nv_bfloat16* dstb, long long lddb, float* stats) {
+    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    float ss = 0.f;
+    for (int c = lane; c < cols; c += 32) {
+        const float x = float(src[(long long)row * cols + c]);
+        if (dst) dst[(long long)row * ldd + c] = x;
+        if (dstb) dstb[(long long)row * lddb + c] = __float2bfloat16_rn(x);
+        ss += x * x;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+    if (stats && lane == 0) stats[row] = ss;
+}
+
+__global__ void f64_to_bf16_rows_kernel(const double* src, int rows, int cols, __nv_bfloat16* dst,
+                                        long long ldd) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)rows * cols) return;
+    const int r = int(i / cols), c = int(i % cols);
+    dst[(long long)r * ldd + c] = __float2bfloat16_rn(float(src[i]));
+}
+
+__global__ void f32_to_f64_kernel(const float* src, long long lds, int rows, int cols, double* dst) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows * cols) return;
+    dst[i] = double(src[(long long)(i / cols) * lds + (i % cols)]);
+}
+
+// --------------------------------------------------------------------- launchers
+
+cudaError_t launch_gen_weight(__nv_bfloat16* dst, long long ldk, int k, int m, int gated,
+                              uint64_t seed, double lo, double hi, cudaStream_t st) {
+    dim3 grid((k / 8 + 1 + 31) / 32, m);
+    gen_weight_kernel<<<grid, 32, 0, st>>>(dst, ldk, k, m, gated, seed, lo, hi);
+    return cudaGetLastError();
+}
+cudaError_t launch_pack_weight(__nv_bfloat16* dst, long long ldk, const double* w, int k, int m,
+                               int gated, cudaStream_t st) {
+    dim3 grid((k / 8 + 1 + 31) / 32, m);
+    pack_weight_kernel<<<grid, 32, 0, st>>>(dst, ldk, w, k, m, gated);
+    return cudaGetLastError();
+}
+cudaError_t launch_gen_vector(float* dst, int n, uint64_t seed, double lo, double hi, cudaStream_t st) {
+    gen_vector_kernel<<<(n + 255) / 256, 256, 0, st>>>(dst, n, seed, lo, hi);
+    return cudaGetLastError();
+}
+cudaError_t launch_f64_to_f32(float* dst, const double* src, int n, cudaStream_t st) {
+    f64_to_f32_kernel<<<(n + 255) / 256, 256, 0, st>>>(dst, src, n);
+    return cudaGetLastError();
+}
+cudaError_t launch_rows_to_f32(const double* src, int rows, int cols, float* dst, long long ldd,
+                               __nv_bfloat16* dstb, long long lddb, float* stats, cudaStream_t st) {
+    rows_to_f32_kernel<<<(rows + 3) / 4, 128, 0, st>>>(src, rows, cols, dst, ldd, dstb, lddb, stats);
+    return cudaGetLastError();
+}
+cudaError_t launch_f64_to_bf16_rows(const double* src, int rows, int cols, __nv_bfloat16* dst,
+                                    long long ldd, cudaStream_t st) {
+    const long long n = (long long)rows * cols;
+    f64_to_bf16_rows_kernel<<<int((n + 255) / 256), 256, 0, st>>>(src, rows, cols, dst, ldd);
+    return cudaGetLastError();
+}
+cudaError_t launch_f32_to_f64(const float* src, long long lds, int rows, int cols, double* dst,
+                              cudaStream_t st) {
+    f32_to_f64_kernel<<<(rows * cols + 255) / 256, 256, 0, st>>>(src, lds, rows, cols, dst);
+    return cudaGetLastError();
+}
+
+}  // namespace pi0b

@@ -1,0 +1,285 @@
+"""ctypes binding of libpi0b.so (include/pi0b.h).
+
+Mirrors the reference's C++ inference API for the pi0 path
+(proj/include/rtvla/evaluate.hpp:38-44):
+
+    rtvla::gen_weights(g, seed)      -> Engine.gen_weights(seed)       (on device, bit-exact bf16)
+    WeightStore / WeightSet          -> Engine.set_weight(node, inst, w, bias) / set_bias_table
+    rtvla::evaluate(g, w, x)         -> Engine.run(patches, state, noise, prompt) -> [63, 32] fp64
+    errors: ShapeError / NumericError are raised as the same-named Python exceptions.
+
+There is no CPU fallback: if the CUDA library is missing or no sm_100 device is present the
+constructor raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .config import ModelConfig
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpi0b.so")
+
+PI0B_E_INVALID = -1
+PI0B_E_UNSUPPORTED = -2
+PI0B_E_STATE = -3
+PI0B_E_NUMERIC = -4
+
+# GEMM epilogue modes / flags (csrc/gemm.cuh)
+MODE_BF16, MODE_GATE, MODE_F32_STORE, MODE_RESID, MODE_SILU_TABLE = 0, 1, 2, 3, 4
+FLAG_ROWSCALE, FLAG_BIAS, FLAG_GELU, FLAG_ROPE = 1, 2, 4, 8
+
+
+class ShapeError(ValueError):
+    """rtvla::ShapeError (proj/include/rtvla/tensor.hpp:15-17)."""
+
+
+class NumericError(ArithmeticError):
+    """rtvla::NumericError (proj/include/rtvla/tensor.hpp:18-20)."""
+
+
+class UnsupportedConfig(ShapeError):
+    pass
+
+
+class EngineOptions(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("use_cuda_graph", ctypes.c_int), ("record_checkpoints", ctypes.c_int)]
+
+
+class GemmDesc(ctypes.Structure):
+    _fields_ = [
+        ("a", ctypes.c_void_p), ("lda", ctypes.c_int64),
+        ("w", ctypes.c_void_p), ("ldw", ctypes.c_int64),
+        ("M", ctypes.c_int), ("N", ctypes.c_int), ("K", ctypes.c_int),
+        ("bn", ctypes.c_int), ("splits", ctypes.c_int),
+        ("mode", ctypes.c_int), ("flags", ctypes.c_int),
+        ("row_stats", ctypes.c_void_p), ("inv_width", ctypes.c_float), ("eps", ctypes.c_float),
+        ("bias", ctypes.c_void_p),
+        ("table_row", ctypes.c_void_p),
+        ("rope_cs", ctypes.c_void_p), ("rope_pos0", ctypes.c_int), ("rope_cols", ctypes.c_int),
+        ("resid_scale", ctypes.c_float),
+        ("out", ctypes.c_void_p), ("ldo", ctypes.c_int64),
+        ("outb", ctypes.c_void_p), ("ldob", ctypes.c_int64),
+        ("out_stats", ctypes.c_void_p),
+        ("row0_src", ctypes.c_void_p),
+        ("ws", ctypes.c_void_p), ("counters", ctypes.c_void_p),
+    ]
+
+
+class AttnDesc(ctypes.Structure):
+    _fields_ = [
+        ("head_dim", ctypes.c_int),
+        ("q", ctypes.c_void_p), ("ldq", ctypes.c_int64), ("q_rows", ctypes.c_int), ("heads", ctypes.c_int),
+        ("kv_heads", ctypes.c_int),
+        ("k0", ctypes.c_void_p), ("v0", ctypes.c_void_p), ("ld0", ctypes.c_int64), ("rows0", ctypes.c_int),
+        ("k1", ctypes.c_void_p), ("v1", ctypes.c_void_p), ("ld1", ctypes.c_int64), ("rows1", ctypes.c_int),
+        ("out", ctypes.c_void_p), ("ldo", ctypes.c_int64),
+        ("kv_splits", ctypes.c_int),
+        ("ws", ctypes.c_void_p), ("counters", ctypes.c_void_p),
+    ]
+
+
+_lib = None
+_dp = ctypes.POINTER(ctypes.c_double)
+
+
+def lib():
+    """Load libpi0b.so (raises if it was not built: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        cfgp = ctypes.POINTER(ModelConfig)
+        vp = ctypes.c_void_p
+        L.pi0b_last_error.restype = ctypes.c_char_p
+        L.pi0b_default_config.argtypes = [cfgp]
+        L.pi0b_engine_create.argtypes = [cfgp, ctypes.POINTER(EngineOptions), ctypes.POINTER(vp)]
+        L.pi0b_engine_destroy.argtypes = [vp]
+        L.pi0b_engine_destroy.restype = None
+        L.pi0b_engine_gen_weights.argtypes = [vp, ctypes.c_uint64]
+        L.pi0b_engine_set_weight.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64, _dp, ctypes.c_int64,
+                                             ctypes.c_int64, _dp, ctypes.c_int64]
+        L.pi0b_engine_set_bias_table.argtypes = [vp, ctypes.c_char_p, _dp, ctypes.c_int64, ctypes.c_int64]
+        L.pi0b_engine_run.argtypes = [vp, _dp, _dp, _dp, _dp, _dp]
+        L.pi0b_engine_run_prefix.argtypes = [vp, _dp, _dp]
+        L.pi0b_engine_run_action.argtypes = [vp, _dp, _dp, _dp]
+        L.pi0b_engine_replay.argtypes = [vp, ctypes.c_int, vp]
+        L.pi0b_engine_sync.argtypes = [vp]
+        L.pi0b_engine_kernel_count.argtypes = [vp, ctypes.c_int]
+        L.pi0b_engine_read_checkpoint.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64,
+                                                  ctypes.POINTER(ctypes.c_float), ctypes.c_int64, ctypes.c_int64]
+        L.pi0b_gemm.argtypes = [ctypes.POINTER(GemmDesc), vp]
+        L.pi0b_attention.argtypes = [ctypes.POINTER(AttnDesc), vp]
+        L.pi0b_attention_ws_floats.argtypes = [ctypes.POINTER(AttnDesc)]
+        L.pi0b_attention_ws_floats.restype = ctypes.c_int64
+        L.pi0b_random_f64.argtypes = [vp, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double, vp]
+        L.pi0b_random_packed_bf16.argtypes = [vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                              ctypes.c_uint64, ctypes.c_double, ctypes.c_double, vp]
+        L.pi0b_seed_hash.argtypes = [ctypes.c_uint64, ctypes.c_char_p, ctypes.c_uint64, ctypes.c_uint64]
+        L.pi0b_seed_hash.restype = ctypes.c_uint64
+        _lib = L
+    return _lib
+
+
+EXPORTED_SYMBOLS = [
+    "pi0b_default_config", "pi0b_engine_create", "pi0b_engine_destroy", "pi0b_engine_gen_weights",
+    "pi0b_engine_set_weight", "pi0b_engine_set_bias_table", "pi0b_engine_run", "pi0b_engine_run_prefix",
+    "pi0b_engine_run_action", "pi0b_engine_replay", "pi0b_engine_sync", "pi0b_engine_kernel_count",
+    "pi0b_engine_read_checkpoint", "pi0b_last_error", "pi0b_gemm", "pi0b_attention",
+    "pi0b_attention_ws_floats", "pi0b_random_f64", "pi0b_random_packed_bf16", "pi0b_seed_hash",
+]
+
+
+def _raise(rc: int, what: str):
+    if rc == 0:
+        return
+    msg = f"{what}: {lib().pi0b_last_error().decode()} (code {rc})"
+    if rc == PI0B_E_UNSUPPORTED:
+        raise UnsupportedConfig(msg)
+    if rc == PI0B_E_INVALID:
+        raise ShapeError(msg)
+    if rc == PI0B_E_NUMERIC:
+        raise NumericError(msg)
+    raise RuntimeError(msg)
+
+
+def _f64(a, shape) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if tuple(a.shape) != tuple(shape):
+        raise ShapeError(f"expected shape {tuple(shape)}, got {tuple(a.shape)}")
+    return a
+
+
+def seed_hash(seed: int, label: str, a: int, b: int) -> int:
+    return lib().pi0b_seed_hash(seed, label.encode(), a, b)
+
+
+class Engine:
+    """One pi0 engine on one B200 (weights, activations, KV cache, captured CUDA graphs)."""
+
+    def __init__(self, cfg: ModelConfig, device: int = 0, use_cuda_graph: bool = True,
+                 record_checkpoints: bool = False):
+        self.cfg = cfg
+        self._h = ctypes.c_void_p()
+        opt = EngineOptions(device, int(use_cuda_graph), int(record_checkpoints))
+        _raise(lib().pi0b_engine_create(ctypes.byref(cfg), ctypes.byref(opt), ctypes.byref(self._h)),
+               "pi0b_engine_create")
+
+    def close(self):
+        if self._h:
+            lib().pi0b_engine_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- weights
+    def gen_weights(self, seed: int = 1) -> None:
+        _raise(lib().pi0b_engine_gen_weights(self._h, seed), "gen_weights")
+
+    def set_weight(self, node: str, inst: int, w: np.ndarray, bias: np.ndarray | None = None) -> None:
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float64)
+        _raise(lib().pi0b_engine_set_weight(self._h, node.encode(), inst, w.ctypes.data_as(_dp), w.shape[0],
+                                            w.shape[1], None if b is None else b.ctypes.data_as(_dp),
+                                            0 if b is None else b.size), f"set_weight({node}[{inst}])")
+
+    def set_bias_table(self, node: str, table: np.ndarray) -> None:
+        t = np.ascontiguousarray(table, dtype=np.float64)
+        _raise(lib().pi0b_engine_set_bias_table(self._h, node.encode(), t.ctypes.data_as(_dp), t.shape[0],
+                                                t.shape[1]), "set_bias_table")
+
+    # ---- inference
+    def _inputs(self, patches=None, state=None, noise=None, prompt=None):
+        c = self.cfg
+        out = {}
+        if patches is not None:
+            out["patches"] = _f64(patches, (c.image_tokens, c.ve_patch_in))
+        if state is not None:
+            out["state"] = _f64(state, (1, c.ae_state_dim))
+        if noise is not None:
+            out["noise"] = _f64(noise, (c.chunk_len, c.ae_action_dim))
+        if c.prompt_tokens > 0:
+            if prompt is None and patches is not None:
+                raise ShapeError("config has prompt tokens but no prompt was given")
+            if prompt is not None:
+                out["prompt"] = _f64(prompt, (c.prompt_tokens, c.llm_width))
+        return out
+
+    @staticmethod
+    def _p(a):
+        return None if a is None else a.ctypes.data_as(_dp)
+
+    def run(self, patches, state, noise, prompt=None) -> np.ndarray:
+        x = self._inputs(patches, state, noise, prompt)
+        y = np.zeros((self.cfg.chunk_len, self.cfg.ae_action_dim), dtype=np.float64)
+        _raise(lib().pi0b_engine_run(self._h, self._p(x["patches"]), self._p(x["state"]), self._p(x["noise"]),
+                                     self._p(x.get("prompt")), self._p(y)), "run")
+        return y
+
+    def run_prefix(self, patches, prompt=None) -> None:
+        x = self._inputs(patches=patches, prompt=prompt)
+        _raise(lib().pi0b_engine_run_prefix(self._h, self._p(x["patches"]), self._p(x.get("prompt"))),
+               "run_prefix")
+
+    def run_action(self, state, noise) -> np.ndarray:
+        x = self._inputs(state=state, noise=noise)
+        y = np.zeros((self.cfg.chunk_len, self.cfg.ae_action_dim), dtype=np.float64)
+        _raise(lib().pi0b_engine_run_action(self._h, self._p(x["state"]), self._p(x["noise"]), self._p(y)),
+               "run_action")
+        return y
+
+    def replay(self, part: int = 0, stream: int | None = None) -> None:
+        _raise(lib().pi0b_engine_replay(self._h, part, stream), "replay")
+
+    def sync(self) -> None:
+        _raise(lib().pi0b_engine_sync(self._h), "sync")
+
+    def kernel_count(self, part: int = 0) -> int:
+        return lib().pi0b_engine_kernel_count(self._h, part)
+
+    def checkpoint(self, node: str, inst: int, rows: int, cols: int) -> np.ndarray:
+        out = np.zeros((rows, cols), dtype=np.float32)
+        _raise(lib().pi0b_engine_read_checkpoint(self._h, node.encode(), inst,
+                                                 out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), rows, cols),
+               f"checkpoint {node}[{inst}]")
+        return out
+
+
+def evaluate(cfg: ModelConfig, weight_seed: int, inputs: dict) -> np.ndarray:
+    """Drop-in for rtvla::evaluate(build_pi0_graph(cfg), gen_weights(g, seed), x)."""
+    eng = Engine(cfg)
+    try:
+        eng.gen_weights(weight_seed)
+        return eng.run(inputs["patches"], inputs["state"], inputs["noise"], inputs.get("prompt"))
+    finally:
+        eng.close()
+
+
+# ---------------------------------------------------------------- kernel-level helpers (tests)
+
+def gemm(desc: GemmDesc, stream: int | None = None) -> None:
+    _raise(lib().pi0b_gemm(ctypes.byref(desc), stream), "pi0b_gemm")
+
+
+def attention(desc: AttnDesc, stream: int | None = None) -> None:
+    _raise(lib().pi0b_attention(ctypes.byref(desc), stream), "pi0b_attention")
+
+
+def attention_ws_floats(desc: AttnDesc) -> int:
+    return lib().pi0b_attention_ws_floats(ctypes.byref(desc))
+
+
+def random_f64(ptr: int, n: int, seed: int, lo: float, hi: float, stream: int | None = None) -> None:
+    _raise(lib().pi0b_random_f64(ptr, n, seed, lo, hi, stream), "pi0b_random_f64")
+
+
+def random_packed_bf16(ptr: int, ldk: int, k: int, m: int, gated: bool, seed: int, lo: float, hi: float,
+                       stream: int | None = None) -> None:
+    _raise(lib().pi0b_random_packed_bf16(ptr, ldk, k, m, int(gated), seed, lo, hi, stream), "random_packed_bf16")

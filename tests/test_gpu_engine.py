@@ -1,0 +1,176 @@
+"""End-to-end parity of the B200 engine against the fp64 oracle.
+
+* device `gen_weights` is bit-exact (bf16 RNE of the reference's fp64 draws);
+* the full forward (VE -> LLM -> AE, all flow steps) on the mid config matches the oracle:
+  actions within the stated bf16 tolerance, per-layer hidden-state cosine >= 0.999
+  (north star), through both weight paths (device generation and host WeightStore upload);
+* the streaming split (run_prefix + run_action) equals run();
+* full-scale 1-view and 2-view actions match the reference's published golden values.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from _util import bf16_bits_from_f64, cosine, rel_err
+from oracle import oracle as O
+from paper_2510_26742_b200 import engine as E
+from paper_2510_26742_b200.config import default_config, mid_config
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+# bf16 tolerance on the [63, 32] action chunk (north star: "a stated bf16 tolerance").
+ACT_MAX_ABS = 0.05      # of actions whose rms is ~1
+ACT_REL = 0.10          # max |d| / max(|ref|, 1e-2*rms(ref))
+LAYER_COS = 0.999
+
+
+def test_device_weight_stream_bitexact():
+    import torch
+    k, m = 1152, 3456
+    seed = E.seed_hash(1, "ve.qkv", 3, 1)
+    assert seed == O.ref_lib().ref_seed_hash(1, b"ve.qkv", 3, 1)
+    lim = 1.0 / np.sqrt(k)
+    d64 = torch.zeros(k * m, dtype=torch.float64, device="cuda")
+    E.random_f64(d64.data_ptr(), k * m, seed, -lim, lim)
+    w_ref, _ = O.port_weight("ve.qkv", 3, k, m)
+    assert np.array_equal(d64.cpu().numpy().reshape(k, m), w_ref)
+    packed = torch.zeros(m, k, dtype=torch.int16, device="cuda")
+    E.random_packed_bf16(packed.data_ptr(), k, k, m, False, seed, -lim, lim)
+    got = packed.cpu().numpy().view(np.uint16)
+    assert np.array_equal(got, bf16_bits_from_f64(w_ref).T)
+
+
+def _record_list(cfg):
+    T, L, S = cfg.image_tokens, cfg.prefix_tokens, cfg.suffix_tokens
+    rec = [("ve.embed", 0, (T, cfg.ve_width))]
+    rec += [("ve.fc2", i, (T, cfg.ve_width)) for i in range(cfg.ve_layers)]
+    rec += [("ve.qkv", 0, (T, 3 * cfg.ve_width)), ("ve.attn", 0, (T, cfg.ve_width))]
+    rec += [("llm.proj_in", 0, (T, cfg.llm_width))]
+    qkv = (cfg.llm_q_heads + 2 * cfg.llm_kv_heads) * cfg.llm_head_dim
+    rec += [("llm.qkv", l, (L, qkv)) for l in range(cfg.llm_layers)]
+    rec += [("llm.down", l, (L, cfg.llm_width)) for l in range(cfg.llm_layers - 1)]
+    AR = cfg.ae_layers * cfg.flow_steps
+    rec += [("ae.down", i, (S, cfg.ae_width)) for i in range(AR)]
+    rec += [("ae.head", s, (cfg.chunk_len, cfg.ae_action_dim)) for s in range(cfg.flow_steps)]
+    return rec
+
+
+def _compare_layers(eng, cfg, recs, lq):
+    worst = 1.0
+    for (node, inst), ref in recs.items():
+        got = eng.checkpoint(node, inst, *ref.shape)
+        if node == "llm.qkv" and inst == cfg.llm_layers - 1:
+            got, ref = got[:, lq:], ref[:, lq:]        # dead Q of the last layer is skipped
+        c = cosine(got, ref)
+        worst = min(worst, c)
+        assert c >= LAYER_COS, f"{node}[{inst}] cosine {c:.6f}"
+    return worst
+
+
+@pytest.mark.parametrize("views,prompt", [(1, 0), (2, 0), (3, 32)])
+def test_engine_mid_config_matches_oracle(views, prompt):
+    cfg = mid_config(views=views, prompt_tokens=prompt)
+    x = O.gen_inputs(cfg, 1)
+    ref, recs = O.port_forward(cfg, x, record=_record_list(cfg))
+    eng = E.Engine(cfg, record_checkpoints=True)
+    eng.gen_weights(1)
+    y = eng.run(x["patches"], x["state"], x["noise"], x.get("prompt"))
+    assert np.abs(y - ref).max() < ACT_MAX_ABS, np.abs(y - ref).max()
+    assert rel_err(y, ref) < ACT_REL
+    lq = cfg.llm_q_heads * cfg.llm_head_dim
+    _compare_layers(eng, cfg, recs, lq)
+    # graph-captured replay gives the same actions as the eager recorded run
+    g = E.Engine(cfg, use_cuda_graph=True)
+    g.gen_weights(1)
+    y2 = g.run(x["patches"], x["state"], x["noise"], x.get("prompt"))
+    assert np.abs(y2 - y).max() < 1e-3
+
+
+def test_engine_host_weightstore_path():
+    """Weights uploaded one WeightSet at a time from the reference's gen_weights."""
+    cfg = mid_config()
+    x = O.gen_inputs(cfg, 1)
+    ref, _ = O.port_forward(cfg, x)
+    eng = E.Engine(cfg)
+    vw, lw, aw = cfg.ve_width, cfg.llm_width, cfg.ae_width
+    lqkv = (cfg.llm_q_heads + 2 * cfg.llm_kv_heads) * 256
+    aq = cfg.ae_q_heads * 256
+    nodes = [("ve.embed", 1, cfg.ve_patch_in, vw, True), ("ve.qkv", cfg.ve_layers, vw, 3 * vw, True),
+             ("ve.proj", cfg.ve_layers, vw, vw, True), ("ve.fc1", cfg.ve_layers, vw, cfg.ve_mlp, True),
+             ("ve.fc2", cfg.ve_layers, cfg.ve_mlp, vw, True), ("llm.proj_in", 1, vw, lw, True),
+             ("llm.qkv", cfg.llm_layers, lw, lqkv, False),
+             ("llm.proj", cfg.llm_layers - 1, cfg.llm_q_heads * 256, lw, False),
+             ("llm.ffn", cfg.llm_layers - 1, lw, 2 * cfg.llm_mlp, False),
+             ("llm.down", cfg.llm_layers - 1, cfg.llm_mlp, lw, False),
+             ("ae.state_proj", 1, cfg.ae_state_dim, aw, True), ("ae.action_proj", 1, cfg.ae_action_dim, aw, False),
+             ("ae.action_out", 1, aw, aw, True), ("ae.qkv", cfg.ae_layers, aw, aq + 512, False),
+             ("ae.proj", cfg.ae_layers, aq, aw, False), ("ae.ffn", cfg.ae_layers, aw, 2 * cfg.ae_mlp, False),
+             ("ae.down", cfg.ae_layers, cfg.ae_mlp, aw, False), ("ae.head", 1, aw, cfg.ae_action_dim, True)]
+    for node, n, k, m, has_b in nodes:
+        for i in range(n):
+            w, b = O.port_weight(node, i, k, m, bias=has_b)
+            eng.set_weight(node, i, w, b)
+    # bias table rows: U(+-1/sqrt(act)) seeded per flow step (proj/src/evaluate.cpp:64-71)
+    lim = 1.0 / np.sqrt(cfg.ae_action_dim)
+    tab = np.zeros((cfg.flow_steps, aw))
+    import torch
+    for s in range(cfg.flow_steps):
+        t = torch.zeros(aw, dtype=torch.float64, device="cuda")
+        E.random_f64(t.data_ptr(), aw, E.seed_hash(1, "ae.action_proj", s, 4), -lim, lim)
+        tab[s] = t.cpu().numpy()
+    eng.set_bias_table("ae.action_proj", tab)
+    y = eng.run(x["patches"], x["state"], x["noise"])
+    assert np.abs(y - ref).max() < ACT_MAX_ABS
+    gen = E.Engine(cfg)
+    gen.gen_weights(1)
+    y2 = gen.run(x["patches"], x["state"], x["noise"])
+    assert np.abs(y2 - y).max() < 1e-3
+
+
+def test_streaming_split_equals_full_run():
+    cfg = mid_config(views=2)
+    x = O.gen_inputs(cfg, 1)
+    eng = E.Engine(cfg)
+    eng.gen_weights(1)
+    y = eng.run(x["patches"], x["state"], x["noise"])
+    eng.run_prefix(x["patches"])
+    y2 = eng.run_action(x["state"], x["noise"])
+    assert np.abs(y2 - y).max() < 1e-3
+    # fresh noise on the cached prefix == a full run with that noise
+    x2 = O.gen_inputs(cfg, 7)
+    y3 = eng.run_action(x["state"], x2["noise"])
+    y4 = eng.run(x["patches"], x["state"], x2["noise"])
+    assert np.abs(y3 - y4).max() < 1e-3
+
+
+def test_engine_rejects_bad_inputs():
+    cfg = mid_config()
+    eng = E.Engine(cfg)
+    x = O.gen_inputs(cfg, 1)
+    with pytest.raises(E.ShapeError):
+        eng.run(x["patches"][:-1], x["state"], x["noise"])
+    with pytest.raises(E.ShapeError):
+        E.Engine(cfg.replace(llm_head_dim=128))
+    with pytest.raises(E.ShapeError):
+        eng.set_weight("ve.qkv", 99, np.zeros((cfg.ve_width, 3 * cfg.ve_width)), np.zeros(3 * cfg.ve_width))
+
+
+@pytest.mark.parametrize("views", [1, 2])
+def test_full_scale_actions_match_reference_golden(views):
+    """Full-scale pi0 (seed 1) vs the reference's fp64 output (tests/golden/full_{v}v.json,
+    generated by tests/golden/make_golden.py through the compiled reference)."""
+    path = os.path.join(GOLDEN, f"full_{views}v.json")
+    gold = json.load(open(path))
+    ref = np.array(gold["actions"], dtype=np.float64).reshape(63, 32)
+    cfg = default_config(views=views)
+    x = O.gen_inputs(cfg, 1)
+    eng = E.Engine(cfg)
+    eng.gen_weights(1)
+    y = eng.run(x["patches"], x["state"], x["noise"])
+    assert np.abs(y - ref).max() < ACT_MAX_ABS, np.abs(y - ref).max()
+    assert rel_err(y, ref) < ACT_REL
+    assert cosine(y, ref) > 0.9995
