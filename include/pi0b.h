@@ -90,6 +90,14 @@ int pi0b_engine_sync(pi0b_engine* e);
 /* Number of kernels one replay of `part` launches. */
 int pi0b_engine_kernel_count(pi0b_engine* e, int part);
 
+/* Average device time (ms) of one launch of the kernels of node `node_id` (all of its
+ * instances, `reps` passes, CUDA events on the engine stream).  Used for the roofline. */
+int pi0b_engine_time_node(pi0b_engine* e, const char* node_id, int reps, double* ms_per_launch,
+                          int* launches);
+
+/* Text listing of the launch plan, one op per line (index, part, kind, node, instance, grid). */
+int pi0b_engine_describe(pi0b_engine* e, char* buf, int64_t cap);
+
 /* Parity hook (record_checkpoints=1): the output of node `node_id` instance `inst` from
  * the last run, as fp32 [rows, cols].  Node ids/instances are the reference graph's. */
 int pi0b_engine_read_checkpoint(pi0b_engine* e, const char* node_id, int64_t inst, float* out,

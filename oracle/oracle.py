@@ -87,6 +87,10 @@ def ref_lib():
         lib.ref_time_embedding.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]
         lib.ref_max_rel_deviation.argtypes = [_dp, _dp, ctypes.c_int64]
         lib.ref_max_rel_deviation.restype = ctypes.c_double
+        lib.ref_ctx_create.argtypes = [cfgp, ctypes.c_uint64, ctypes.c_uint64]
+        lib.ref_ctx_create.restype = ctypes.c_void_p
+        lib.ref_ctx_evaluate.argtypes = [ctypes.c_void_p, _dp]
+        lib.ref_ctx_destroy.argtypes = [ctypes.c_void_p]
         _ref = lib
     return _ref
 
@@ -149,6 +153,28 @@ def ref_evaluate(cfg: ModelConfig, wseed: int = 1, iseed: int = 1) -> np.ndarray
     out = np.zeros((cfg.chunk_len, cfg.ae_action_dim), dtype=np.float64)
     _check(lib.ref_evaluate(ctypes.byref(cfg), wseed, iseed, _ptr(out)), lib, "ref")
     return out
+
+
+class RefContext:
+    """build_pi0_graph + gen_weights + gen_inputs once; evaluate() alone is what a
+    bench step times (the reference's own inference call, proj/src/evaluate.cpp:365-370)."""
+
+    def __init__(self, cfg: ModelConfig, wseed: int = 1, iseed: int = 1):
+        self.cfg = cfg
+        self.lib = ref_lib()
+        self.h = self.lib.ref_ctx_create(ctypes.byref(cfg), wseed, iseed)
+        if not self.h:
+            raise RuntimeError("ref_ctx_create: " + self.lib.ref_last_error().decode())
+
+    def evaluate(self) -> np.ndarray:
+        out = np.zeros((self.cfg.chunk_len, self.cfg.ae_action_dim), dtype=np.float64)
+        _check(self.lib.ref_ctx_evaluate(self.h, _ptr(out)), self.lib, "ref")
+        return out
+
+    def close(self):
+        if self.h:
+            self.lib.ref_ctx_destroy(self.h)
+            self.h = None
 
 
 def ref_node(cfg: ModelConfig, node: str, inst: int, wseed: int = 1, iseed: int = 1,

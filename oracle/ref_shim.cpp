@@ -165,6 +165,33 @@ int ref_evaluate_node(const pi0b_model_config* c, uint64_t wseed, uint64_t iseed
     });
 }
 
+// ---- persistent context: graph + WeightStore + Inputs built once, evaluate() timed alone
+struct RefCtx {
+    rtvla::Graph g;
+    rtvla::WeightStore w;
+    rtvla::Inputs x;
+};
+void* ref_ctx_create(const pi0b_model_config* c, uint64_t wseed, uint64_t iseed) {
+    try {
+        auto* ctx = new RefCtx;
+        ctx->g = rtvla::build_pi0_graph(to_cfg(c));
+        ctx->w = rtvla::gen_weights(ctx->g, wseed);
+        ctx->x = rtvla::gen_inputs(ctx->g, iseed);
+        return ctx;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+int ref_ctx_evaluate(void* h, double* out) {
+    return guarded([&] {
+        auto* ctx = static_cast<RefCtx*>(h);
+        const rtvla::Tensor y = rtvla::evaluate(ctx->g, ctx->w, ctx->x);
+        std::memcpy(out, y.data.data(), y.data.size() * 8);
+    });
+}
+void ref_ctx_destroy(void* h) { delete static_cast<RefCtx*>(h); }
+
 // ---- numerics primitives (proj/src/tensor.cpp)
 uint64_t ref_seed_hash(uint64_t seed, const char* label, uint64_t a, uint64_t b) {
     return rtvla::seed_hash(seed, label, a, b);

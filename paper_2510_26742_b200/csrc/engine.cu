@@ -210,6 +210,8 @@ public:
     void fetch_actions(double* out);
     void read_checkpoint(const std::string& id, long long inst, float* out, long long rows, long long cols);
     int kernel_count(int part) const;
+    double time_node(const std::string& node, int reps, int* launches);
+    std::string describe() const;
     cudaStream_t stream() const { return stream_; }
     bool weights_ready() const { return weights_loaded_; }
 
@@ -232,7 +234,7 @@ private:
     void tag(const std::string& node, int inst, const void* ptr, int rows, int cols, long long ld, int bf16);
     float* stats_slot(int part);
     void run_ops(int part, cudaStream_t st);
-    void capture(int part);
+    void capture(int part, int slot);
 
     pi0b_model_config c_;
     pi0b_engine_options o_;
@@ -245,7 +247,7 @@ private:
     // dims
     int T_ = 0, P_ = 0, L_ = 0, S_ = 0, C_ = 0, FS_ = 0;
     int ve_w_ = 0, llm_w_ = 0, ae_w_ = 0, llm_q_ = 0, llm_kv_ = 0, ae_q_ = 0, ae_kv_ = 0;
-    int patch_ld_ = 0, act_ld_ = 0, state_ld_ = 0;
+    int patch_ld_ = 0, act_ld_ = 0, state_ld_ = 0, ve_mlp_ld_ = 0;
 
     // inputs (fp64 device staging + pinned host staging)
     double *d_patches_ = nullptr, *d_state_ = nullptr, *d_noise_ = nullptr, *d_prompt_ = nullptr,
@@ -295,6 +297,7 @@ Engine::Engine(const pi0b_model_config& cfg, const pi0b_engine_options& opt) : c
     alloc_weights();
     alloc_activations();
     build_plan();
+    PI0B_CUDA(cudaStreamSynchronize(stream_));
 }
 
 Engine::~Engine() {
@@ -321,7 +324,7 @@ void Engine::validate_config() {
     need(c.llm_q_heads % c.llm_kv_heads == 0 && c.ae_q_heads % c.ae_kv_heads == 0, "GQA grouping");
     need(c.ae_q_heads * c.ae_head_dim > 0, "ae heads");
     need(c.llm_mlp % 128 == 0 && c.ae_mlp % 128 == 0, "mlp widths must be multiples of 128");
-    for (int w : {c.ve_width, c.ve_mlp, c.llm_width, c.ae_width})
+    for (int w : {c.ve_width, c.llm_width, c.ae_width})
         need(w % 8 == 0, "hidden widths must be multiples of 8");
     need(c.ve_layers >= 1 && c.llm_layers >= 2 && c.ae_layers >= 1, "layer counts");
 }
@@ -341,7 +344,7 @@ void Engine::alloc_weights() {
         const int rows = gated ? round_up(m, 256) : m;
         for (int i = 0; i < inst; ++i) {
             nw.w.push_back(alloc<__nv_bfloat16>(size_t(rows) * nw.ldk));
-            PI0B_CUDA(cudaMemset(nw.w.back(), 0, size_t(rows) * nw.ldk * 2));
+            PI0B_CUDA(cudaMemsetAsync(nw.w.back(), 0, size_t(rows) * nw.ldk * 2, stream_));
             if (bias) nw.b.push_back(alloc<float>(m));
         }
         if (table) nw.table = alloc<float>(size_t(c.flow_steps) * m);
@@ -390,6 +393,7 @@ void Engine::alloc_activations() {
     ae_q_ = c.ae_q_heads * c.ae_head_dim;
     ae_kv_ = c.ae_kv_heads * c.ae_head_dim;
     patch_ld_ = round_up(c.ve_patch_in, 8);
+    ve_mlp_ld_ = round_up(c.ve_mlp, 8);
     act_ld_ = round_up(c.ae_action_dim, 8);
     state_ld_ = round_up(c.ae_state_dim, 8);
 
@@ -407,21 +411,22 @@ void Engine::alloc_activations() {
     PI0B_CUDA(cudaMallocHost(&h_out_, n_out_ * sizeof(double)));
 
     patches_b_ = alloc<__nv_bfloat16>(size_t(T_) * patch_ld_);
-    PI0B_CUDA(cudaMemset(patches_b_, 0, size_t(T_) * patch_ld_ * 2));
+    PI0B_CUDA(cudaMemsetAsync(patches_b_, 0, size_t(T_) * patch_ld_ * 2, stream_));
     ve_h_ = alloc<float>(size_t(T_) * ve_w_);
     ve_hb_ = alloc<__nv_bfloat16>(size_t(T_) * ve_w_);
     ve_qkv_ = alloc<__nv_bfloat16>(size_t(T_) * 3 * ve_w_);
     ve_attn_ = alloc<__nv_bfloat16>(size_t(T_) * ve_w_);
-    ve_mlp_ = alloc<__nv_bfloat16>(size_t(T_) * c.ve_mlp);
+    ve_mlp_ = alloc<__nv_bfloat16>(size_t(T_) * ve_mlp_ld_);
+    PI0B_CUDA(cudaMemsetAsync(ve_mlp_, 0, size_t(T_) * ve_mlp_ld_ * 2, stream_));
     x_ = alloc<float>(size_t(L_) * llm_w_);
     xb_ = alloc<__nv_bfloat16>(size_t(L_) * llm_w_);
     llm_attn_ = alloc<__nv_bfloat16>(size_t(L_) * llm_q_);
     llm_g_ = alloc<__nv_bfloat16>(size_t(L_) * c.llm_mlp);
     for (int l = 0; l < c.llm_layers; ++l) kv_.push_back(alloc<__nv_bfloat16>(size_t(L_) * (llm_q_ + 2 * llm_kv_)));
     state_b_ = alloc<__nv_bfloat16>(size_t(state_ld_));
-    PI0B_CUDA(cudaMemset(state_b_, 0, size_t(state_ld_) * 2));
+    PI0B_CUDA(cudaMemsetAsync(state_b_, 0, size_t(state_ld_) * 2, stream_));
     ab_ = alloc<__nv_bfloat16>(size_t(C_) * act_ld_);
-    PI0B_CUDA(cudaMemset(ab_, 0, size_t(C_) * act_ld_ * 2));
+    PI0B_CUDA(cudaMemsetAsync(ab_, 0, size_t(C_) * act_ld_ * 2, stream_));
     a_ = alloc<float>(size_t(C_) * act_ld_);
     ap_b_ = alloc<__nv_bfloat16>(size_t(C_) * ae_w_);
     st_ = alloc<float>(size_t(ae_w_));
@@ -443,7 +448,8 @@ void Engine::alloc_activations() {
             cs[(size_t(p) * 128 + j) * 2 + 1] = float(std::sin(ang));
         }
     rope_cs_ = alloc<float>(cs.size());
-    PI0B_CUDA(cudaMemcpy(rope_cs_, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
+    PI0B_CUDA(cudaMemcpyAsync(rope_cs_, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, stream_));
+    PI0B_CUDA(cudaStreamSynchronize(stream_));
 
     // Row-stat slots: one per residual-stream producer instance, zeroed per replay.
     stats_rows_ = round_up(std::max(L_, S_), 64);
@@ -619,9 +625,9 @@ void Engine::build_plan() {
             g.eps = 1e-6f;
             g.bias = Wv["ve.fc1"].b[i];
             g.out = ve_mlp_;
-            g.ldo = c.ve_mlp;
+            g.ldo = ve_mlp_ld_;
             add_gemm(0, "ve.fc1", i, ve_hb_, ve_w_, T_, Wv["ve.fc1"], i, 128, g);
-            tag("ve.fc1", i, ve_mlp_, T_, c.ve_mlp, c.ve_mlp, 1);
+            tag("ve.fc1", i, ve_mlp_, T_, c.ve_mlp, ve_mlp_ld_, 1);
         }
         st = stats_slot(0);
         {   // ve.fc2: h += mlp W + b
@@ -636,7 +642,7 @@ void Engine::build_plan() {
             g.outb = ve_hb_;
             g.ldob = ve_w_;
             g.out_stats = st;
-            add_gemm(0, "ve.fc2", i, ve_mlp_, c.ve_mlp, T_, Wv["ve.fc2"], i, 128, g);
+            add_gemm(0, "ve.fc2", i, ve_mlp_, ve_mlp_ld_, T_, Wv["ve.fc2"], i, 128, g);
             tag("ve.fc2", i, ve_h_, T_, ve_w_, ve_w_, 0);
         }
     }
@@ -945,12 +951,12 @@ void Engine::build_plan() {
 
     // scratch shared by all launches (stream-ordered, self-cleaning)
     gemm_ws_ = alloc<float>(std::max<size_t>(gemm_ws_floats_, 1));
-    PI0B_CUDA(cudaMemset(gemm_ws_, 0, std::max<size_t>(gemm_ws_floats_, 1) * 4));
+    PI0B_CUDA(cudaMemsetAsync(gemm_ws_, 0, std::max<size_t>(gemm_ws_floats_, 1) * 4, stream_));
     gemm_ctr_ = alloc<int>(4096);
-    PI0B_CUDA(cudaMemset(gemm_ctr_, 0, 4096 * 4));
+    PI0B_CUDA(cudaMemsetAsync(gemm_ctr_, 0, 4096 * 4, stream_));
     attn_ws_ = alloc<float>(std::max<size_t>(attn_ws_floats_, 1));
     attn_ctr_ = alloc<int>(4096);
-    PI0B_CUDA(cudaMemset(attn_ctr_, 0, 4096 * 4));
+    PI0B_CUDA(cudaMemsetAsync(attn_ctr_, 0, 4096 * 4, stream_));
     for (auto& op : ops_) {
         if (op.kind == kOpGemm) {
             op.gp.ws = gemm_ws_;
@@ -1001,7 +1007,9 @@ void Engine::set_weight(const std::string& id, long long inst, const double* w, 
         throw EngineError(PI0B_E_INVALID, "node '" + id + "': bias missing or wrong length");
     double* dw = nullptr;
     PI0B_CUDA(cudaMalloc(&dw, size_t(k) * m * 8));
-    PI0B_CUDA(cudaMemcpy(dw, w, size_t(k) * m * 8, cudaMemcpyHostToDevice));
+    // Stream-ordered upload: a pageable cudaMemcpy may return before its DMA lands, and the
+    // engine stream does not synchronise with the legacy stream.
+    PI0B_CUDA(cudaMemcpyAsync(dw, w, size_t(k) * m * 8, cudaMemcpyHostToDevice, stream_));
     cudaError_t e = launch_pack_weight(nw.w[size_t(inst)], nw.ldk, dw, int(k), int(m), nw.gated ? 1 : 0, stream_);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream_);
     cudaFree(dw);
@@ -1009,7 +1017,8 @@ void Engine::set_weight(const std::string& id, long long inst, const double* w, 
     if (nw.has_bias) {
         std::vector<float> b(static_cast<size_t>(m));
         for (long long j = 0; j < m; ++j) b[size_t(j)] = float(bias[j]);
-        PI0B_CUDA(cudaMemcpy(nw.b[size_t(inst)], b.data(), size_t(m) * 4, cudaMemcpyHostToDevice));
+        PI0B_CUDA(cudaMemcpyAsync(nw.b[size_t(inst)], b.data(), size_t(m) * 4, cudaMemcpyHostToDevice, stream_));
+        PI0B_CUDA(cudaStreamSynchronize(stream_));
     }
     weights_loaded_ = true;
 }
@@ -1021,7 +1030,8 @@ void Engine::set_bias_table(const std::string& id, const double* t, long long ro
     if (rows != FS_ || m != it->second.m) throw EngineError(PI0B_E_INVALID, "bias table shape mismatch");
     std::vector<float> f(size_t(rows * m));
     for (size_t i = 0; i < f.size(); ++i) f[i] = float(t[i]);
-    PI0B_CUDA(cudaMemcpy(it->second.table, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+    PI0B_CUDA(cudaMemcpyAsync(it->second.table, f.data(), f.size() * 4, cudaMemcpyHostToDevice, stream_));
+    PI0B_CUDA(cudaStreamSynchronize(stream_));
 }
 
 // ------------------------------------------------------------------ execution
@@ -1080,7 +1090,7 @@ void Engine::run_ops(int part, cudaStream_t st) {
     }
 }
 
-void Engine::capture(int part) {
+void Engine::capture(int part, int slot) {
     cudaGraph_t g = nullptr;
     PI0B_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
     try {
@@ -1091,7 +1101,7 @@ void Engine::capture(int part) {
         throw;
     }
     PI0B_CUDA(cudaStreamEndCapture(stream_, &g));
-    cudaError_t e = cudaGraphInstantiate(&graph_[part], g, 0);
+    cudaError_t e = cudaGraphInstantiate(&graph_[slot], g, 0);
     cudaGraphDestroy(g);
     PI0B_CUDA(e);
 }
@@ -1102,7 +1112,7 @@ void Engine::launch(int part, cudaStream_t st) {
     const int internal = part == 0 ? 2 : part - 1;  // ops filter: 2 all, 0 prefix, 1 action
     const int gidx = part;
     if (o_.use_cuda_graph && !o_.record_checkpoints) {
-        if (!graph_[gidx]) capture(internal);
+        if (!graph_[gidx]) capture(internal, gidx);
         PI0B_CUDA(cudaGraphLaunch(graph_[gidx], st));
     } else {
         run_ops(internal, st);
@@ -1123,6 +1133,57 @@ int Engine::kernel_count(int part) const {
     for (const Op& op : ops_)
         if ((internal == 2 || op.part == internal) && op.is_kernel()) ++n;
     return n;
+}
+
+// One line per planned op: "<index> <part> <kind> <node> <inst> <grid> <detail>".
+std::string Engine::describe() const {
+    static const char* kinds[] = {"gemm", "attn", "rows_f32", "f64_bf16", "f32_f64", "memset"};
+    std::string s;
+    int idx = 0;
+    for (const Op& op : ops_) {
+        char buf[256];
+        if (op.kind == kOpGemm) {
+            const int mt = (op.gp.M + 127) / 128, nt = (op.gp.N + op.bn - 1) / op.bn;
+            snprintf(buf, sizeof buf, "%d %d gemm %s %d %dx%dx%d M=%d N=%d K=%d bn=%d mode=%d\n", idx, op.part,
+                     op.node.c_str(), op.inst, mt, nt, op.gp.splits, op.gp.M, op.gp.N, op.gp.K, op.bn, op.gp.mode);
+        } else if (op.kind == kOpAttn) {
+            snprintf(buf, sizeof buf, "%d %d attn %s %d splits=%d q=%d kv=%d hd=%d\n", idx, op.part, op.node.c_str(),
+                     op.inst, op.ap.kv_splits, op.ap.q_rows, op.ap.rows0 + op.ap.rows1, op.hd);
+        } else {
+            snprintf(buf, sizeof buf, "%d %d %s %s %d\n", idx, op.part, kinds[op.kind], op.node.c_str(), op.inst);
+        }
+        s += buf;
+        ++idx;
+    }
+    return s;
+}
+
+// Average device time of one launch of `node`'s kernels, measured with CUDA events on the
+// engine stream over `reps` back-to-back passes over all instances (bench roofline).
+double Engine::time_node(const std::string& node, int reps, int* launches) {
+    std::vector<const Op*> sel;
+    for (const Op& op : ops_)
+        if (op.node == node && (op.kind == kOpGemm || op.kind == kOpAttn)) sel.push_back(&op);
+    if (sel.empty()) throw EngineError(PI0B_E_INVALID, "no kernels for node '" + node + "'");
+    auto fire = [&](const Op& op) {
+        if (op.kind == kOpGemm) PI0B_CUDA(launch_gemm(op.bn, op.ta, op.tb, op.gp, stream_));
+        else PI0B_CUDA(launch_attention(op.hd, op.ap, stream_));
+    };
+    for (const Op* op : sel) fire(*op);
+    cudaEvent_t a, b;
+    PI0B_CUDA(cudaEventCreate(&a));
+    PI0B_CUDA(cudaEventCreate(&b));
+    PI0B_CUDA(cudaEventRecord(a, stream_));
+    for (int r = 0; r < reps; ++r)
+        for (const Op* op : sel) fire(*op);
+    PI0B_CUDA(cudaEventRecord(b, stream_));
+    PI0B_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    PI0B_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *launches = int(sel.size()) * reps;
+    return double(ms) / double(*launches);
 }
 
 void Engine::read_checkpoint(const std::string& id, long long inst, float* out, long long rows, long long cols) {
@@ -1237,6 +1298,18 @@ int pi0b_engine_kernel_count(pi0b_engine* e, int part) { return e->impl->kernel_
 int pi0b_engine_read_checkpoint(pi0b_engine* e, const char* id, int64_t inst, float* out, int64_t rows,
                                 int64_t cols) {
     PI0B_TRY(e->impl->read_checkpoint(id, inst, out, rows, cols))
+}
+
+int pi0b_engine_describe(pi0b_engine* e, char* buf, int64_t cap) {
+    PI0B_TRY({
+        const std::string s = e->impl->describe();
+        if (int64_t(s.size()) + 1 > cap) throw EngineError(PI0B_E_INVALID, "describe buffer too small");
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+    })
+}
+
+int pi0b_engine_time_node(pi0b_engine* e, const char* id, int reps, double* ms_per_launch, int* launches) {
+    PI0B_TRY(*ms_per_launch = e->impl->time_node(id, reps, launches))
 }
 
 const char* pi0b_last_error(void) { return pi0b::g_last_error.c_str(); }

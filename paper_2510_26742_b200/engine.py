@@ -111,6 +111,9 @@ def lib():
         L.pi0b_engine_kernel_count.argtypes = [vp, ctypes.c_int]
         L.pi0b_engine_read_checkpoint.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64,
                                                   ctypes.POINTER(ctypes.c_float), ctypes.c_int64, ctypes.c_int64]
+        L.pi0b_engine_time_node.argtypes = [vp, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                            ctypes.POINTER(ctypes.c_int)]
+        L.pi0b_engine_describe.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
         L.pi0b_gemm.argtypes = [ctypes.POINTER(GemmDesc), vp]
         L.pi0b_attention.argtypes = [ctypes.POINTER(AttnDesc), vp]
         L.pi0b_attention_ws_floats.argtypes = [ctypes.POINTER(AttnDesc)]
@@ -128,7 +131,7 @@ EXPORTED_SYMBOLS = [
     "pi0b_default_config", "pi0b_engine_create", "pi0b_engine_destroy", "pi0b_engine_gen_weights",
     "pi0b_engine_set_weight", "pi0b_engine_set_bias_table", "pi0b_engine_run", "pi0b_engine_run_prefix",
     "pi0b_engine_run_action", "pi0b_engine_replay", "pi0b_engine_sync", "pi0b_engine_kernel_count",
-    "pi0b_engine_read_checkpoint", "pi0b_last_error", "pi0b_gemm", "pi0b_attention",
+    "pi0b_engine_read_checkpoint", "pi0b_engine_time_node", "pi0b_engine_describe", "pi0b_last_error", "pi0b_gemm", "pi0b_attention",
     "pi0b_attention_ws_floats", "pi0b_random_f64", "pi0b_random_packed_bf16", "pi0b_seed_hash",
 ]
 
@@ -243,6 +246,17 @@ class Engine:
 
     def kernel_count(self, part: int = 0) -> int:
         return lib().pi0b_engine_kernel_count(self._h, part)
+
+    def time_node(self, node: str, reps: int = 5) -> tuple[float, int]:
+        ms, n = ctypes.c_double(), ctypes.c_int()
+        _raise(lib().pi0b_engine_time_node(self._h, node.encode(), reps, ctypes.byref(ms), ctypes.byref(n)),
+               f"time_node({node})")
+        return ms.value, n.value
+
+    def describe(self) -> list[str]:
+        buf = ctypes.create_string_buffer(1 << 20)
+        _raise(lib().pi0b_engine_describe(self._h, buf, len(buf)), "describe")
+        return buf.value.decode().splitlines()
 
     def checkpoint(self, node: str, inst: int, rows: int, cols: int) -> np.ndarray:
         out = np.zeros((rows, cols), dtype=np.float32)

@@ -70,8 +70,8 @@ def _rope_table(npos):
     (300, 256, 640, 64, 3),
 ])
 def test_gemm_bf16_rowscale_bias(M, N, K, bn, splits):
-    A = _rand((M, K), seed=1)
-    W = _rand((N, K), 1 / math.sqrt(K), seed=2)
+    A = _rand((M, (K + 7) // 8 * 8), seed=1)[:, :K]   # TMA needs a 16-byte row pitch
+    W = _rand((N, (K + 7) // 8 * 8), 1 / math.sqrt(K), seed=2)[:, :K]
     stats = torch.rand(M, device=dev) * K + 1.0
     bias = _rand((N,), 0.1, torch.float32, seed=3)
     out = torch.zeros(M, N, dtype=torch.bfloat16, device=dev)
