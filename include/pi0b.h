@@ -128,6 +128,11 @@ typedef struct pi0b_gemm_desc {
     float* ws; int* counters;       /* split-K scratch, zero-initialised            */
 } pi0b_gemm_desc;
 int pi0b_gemm(const pi0b_gemm_desc* d, void* stream);
+/* Swap-AB small-M GEMM (M <= 64; the action expert's weight-streaming kernel): `w` is the
+ * packed [N, K] weight, `a` the [M, K] activations, K split over a cluster of `cluster`
+ * (1, 2, 4, 8) CTAs reduced through distributed shared memory.  rope_cols > 0 selects the
+ * RoPE pair packing, mode 1 (gate) the 64-granule gate packing. */
+int pi0b_gemm_skinny(const pi0b_gemm_desc* d, int cluster, void* stream);
 
 typedef struct pi0b_attn_desc {
     int head_dim;                   /* 72 or 256                                    */
@@ -145,8 +150,9 @@ int64_t pi0b_attention_ws_floats(const pi0b_attn_desc* d);
 /* Device SplitMix64 draw of random_tensor(rows, cols, lo, hi, seed) into fp64 (parity
  * of the parameter streams) and into the packed bf16 layout. */
 int pi0b_random_f64(double* dst, int64_t n, uint64_t seed, double lo, double hi, void* stream);
-int pi0b_random_packed_bf16(void* dst, int64_t ldk, int k, int m, int gated, uint64_t seed, double lo,
-                            double hi, void* stream);
+/* perm: 0 identity, 1 gate (128 granule), 2 gate (64 granule), 3 RoPE pairs (rope_cols). */
+int pi0b_random_packed_bf16(void* dst, int64_t ldk, int k, int m, int perm, int rope_cols, uint64_t seed,
+                            double lo, double hi, void* stream);
 /* FNV-1a seed derivation (proj/src/tensor.cpp:24-40). */
 uint64_t pi0b_seed_hash(uint64_t seed, const char* label, uint64_t a, uint64_t b);
 

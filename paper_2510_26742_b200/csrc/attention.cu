@@ -21,11 +21,14 @@ namespace pi0b {
 
 constexpr int kAttnThreads = 128;
 constexpr int kAttnQT = 64;
+constexpr int kMaxSplits = 8;
+
+constexpr int kKvStages = 3;   // key/value tiles in flight (prefetch distance 2)
 
 template <int HD, int HDP, int KVT>
 struct AttnCfg {
     static constexpr int LDS = HDP + 8;  // padded smem row (elements)
-    static constexpr int SMEM = (kAttnQT + 4 * KVT) * LDS * 2;
+    static constexpr int SMEM = (kAttnQT + 2 * kKvStages * KVT) * LDS * 2;
 };
 
 template <int HD, int HDP, int KVT>
@@ -38,7 +41,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const AttnParams p) 
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);
     __nv_bfloat16* sK = sQ + kAttnQT * LDS;
-    __nv_bfloat16* sV = sK + 2 * KVT * LDS;
+    __nv_bfloat16* sV = sK + kKvStages * KVT * LDS;
     __shared__ int last_flag;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -92,8 +95,12 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const AttnParams p) 
         }
     };
 
-    if (ntiles > 0) load_kv(0, 0);
-    cp_async_commit();
+    // Q and the first kKvStages-1 key/value tiles go out immediately; one commit group per tile.
+#pragma unroll
+    for (int t = 0; t < kKvStages - 1; ++t) {
+        if (t < ntiles) load_kv(t, t);
+        cp_async_commit();
+    }
 
     float o[NT][4];
 #pragma unroll
@@ -102,12 +109,12 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const AttnParams p) 
     const int g4 = lane >> 2, t4 = lane & 3;
 
     for (int t = 0; t < ntiles; ++t) {
-        if (t + 1 < ntiles) load_kv(t + 1, (t + 1) & 1);
+        if (t + kKvStages - 1 < ntiles) load_kv(t + kKvStages - 1, (t + kKvStages - 1) % kKvStages);
         cp_async_commit();
-        cp_async_wait<1>();
+        cp_async_wait<kKvStages - 1>();
         __syncthreads();
-        const __nv_bfloat16* cK = sK + (t & 1) * KVT * LDS;
-        const __nv_bfloat16* cV = sV + (t & 1) * KVT * LDS;
+        const __nv_bfloat16* cK = sK + (t % kKvStages) * KVT * LDS;
+        const __nv_bfloat16* cV = sV + (t % kKvStages) * KVT * LDS;
 
         float s[KVT / 8][4];
 #pragma unroll
@@ -248,27 +255,54 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const AttnParams p) 
     __syncthreads();
     if (!last_flag) return;
     __threadfence();
-    for (int idx = tid; idx < kAttnQT * (HD / 2); idx += kAttnThreads) {
-        const int rr = idx / (HD / 2), d = (idx % (HD / 2)) * 2;
-        const int g = qt * kAttnQT + rr;
-        if (g >= grows) continue;
+    // Merge: per stacked row, weights w_s = l_s 2^(m_s - M) / sum (threads 0..63), then all
+    // threads sweep (row, d-pair) items with the split loads of 8 rows in flight.
+    __shared__ float wts[kAttnQT][kMaxSplits];
+    if (tid < kAttnQT) {
+        const int g = qt * kAttnQT + tid;
         float M = -INFINITY;
+        for (int s2 = 0; s2 < p.kv_splits; ++s2)
+            M = fmaxf(M, __ldcg(p.ws_ml + (((long long)s2 * gridDim.z + grp) * rows_pad + g) * 2));
+        float W = 0.f;
         for (int s2 = 0; s2 < p.kv_splits; ++s2) {
-            const long long sl = ((long long)s2 * gridDim.z + grp) * rows_pad + g;
-            M = fmaxf(M, __ldcg(p.ws_ml + sl * 2));
-        }
-        float W = 0.f, a0 = 0.f, a1 = 0.f;
-        for (int s2 = 0; s2 < p.kv_splits; ++s2) {
-            const long long sl = ((long long)s2 * gridDim.z + grp) * rows_pad + g;
-            const float ms = __ldcg(p.ws_ml + sl * 2), ls = __ldcg(p.ws_ml + sl * 2 + 1);
-            const float w = ls > 0.f ? ls * exp2f(ms - M) : 0.f;
-            const float2 ov = __ldcg(reinterpret_cast<const float2*>(p.ws_o + sl * HD + d));
+            const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml) + ((long long)s2 * gridDim.z + grp) * rows_pad + g);
+            const float w = ml.y > 0.f ? ml.y * exp2f(ml.x - M) : 0.f;
+            wts[tid][s2] = w;
             W += w;
-            a0 += w * ov.x;
-            a1 += w * ov.y;
         }
         const float iw = W > 0.f ? 1.f / W : 0.f;
-        *reinterpret_cast<uint32_t*>(out_ptr(g) + d) = pack_bf16(a0 * iw, a1 * iw);
+        for (int s2 = 0; s2 < p.kv_splits; ++s2) wts[tid][s2] *= iw;
+    }
+    __syncthreads();
+    constexpr int PAIRS = HD / 2;
+    const int S = p.kv_splits;
+    for (int pr = tid; pr < PAIRS; pr += kAttnThreads) {
+        const int d = pr * 2;
+#pragma unroll 1
+        for (int rr = 0; rr < kAttnQT; rr += 4) {
+            float2 ov[4][kMaxSplits];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int g = min(qt * kAttnQT + rr + u, grows - 1);
+#pragma unroll
+                for (int s2 = 0; s2 < kMaxSplits; ++s2)
+                    if (s2 < S)
+                        ov[u][s2] = __ldcg(reinterpret_cast<const float2*>(
+                            p.ws_o + (((long long)s2 * gridDim.z + grp) * rows_pad + g) * HD + d));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int g = qt * kAttnQT + rr + u;
+                float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+                for (int s2 = 0; s2 < kMaxSplits; ++s2)
+                    if (s2 < S) {
+                        a0 += wts[rr + u][s2] * ov[u][s2].x;
+                        a1 += wts[rr + u][s2] * ov[u][s2].y;
+                    }
+                if (g < grows) *reinterpret_cast<uint32_t*>(out_ptr(g) + d) = pack_bf16(a0, a1);
+            }
+        }
     }
 }
 

@@ -23,8 +23,11 @@ cudaError_t launch_attention(int head_dim, const AttnParams& p, cudaStream_t str
 int attn_key_tile(int head_dim);
 int attn_query_tile();
 CUtensorMap make_tmap_bf16(const void* base, long long rows, long long cols, long long ld, int box_rows);
-cudaError_t launch_gen_weight(__nv_bfloat16* dst, long long ldk, int k, int m, int gated,
+cudaError_t launch_gen_weight(__nv_bfloat16* dst, long long ldk, int k, int m, int perm, int rope_cols,
                               uint64_t seed, double lo, double hi, cudaStream_t st);
+cudaError_t skinny_configure();
+cudaError_t launch_skinny(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p, int n_packed,
+                          int cluster, bool pdl, cudaStream_t stream);
 uint64_t seed_hash(uint64_t seed, const std::string& label, uint64_t a, uint64_t b);
 
 __global__ void random_f64_kernel(double* dst, long long n, uint64_t seed, double lo, double hi) {
@@ -39,6 +42,7 @@ static int configure_once() {
     if (dev < 64 && !done[dev]) {
         cudaError_t e = gemm_configure();
         if (e == cudaSuccess) e = attn_configure();
+        if (e == cudaSuccess) e = skinny_configure();
         if (e != cudaSuccess) return int(e);
         done[dev] = true;
     }
@@ -51,7 +55,8 @@ static void attn_plan(const pi0b_attn_desc* d, int* splits, int* per, int* q_til
     const int total = d->rows0 + d->rows1;
     const int kvt = attn_key_tile(d->head_dim);
     int s = d->kv_splits;
-    if (s <= 0) s = std::max(1, std::min(148 / std::max(1, *q_tiles * d->kv_heads), (total + 63) / 64));
+    if (s <= 0) s = std::max(1, std::min(std::min(64 / std::max(1, *q_tiles * d->kv_heads), (total + 2 * kvt - 1) / (2 * kvt)), 8));
+    s = std::min(s, 8);
     int pp = (total + s - 1) / s;
     pp = (pp + kvt - 1) / kvt * kvt;
     *splits = (total + pp - 1) / pp;
@@ -61,6 +66,50 @@ static void attn_plan(const pi0b_attn_desc* d, int* splits, int* per, int* q_til
 }  // namespace pi0b
 
 extern "C" {
+
+static pi0b::GemmParams params_of(const pi0b_gemm_desc* d) {
+    using namespace pi0b;
+    GemmParams p{};
+    p.M = d->M;
+    p.N = d->N;
+    p.K = d->K;
+    p.mode = d->mode;
+    p.flags = d->flags;
+    p.row_stats = d->row_stats;
+    p.inv_width = d->inv_width;
+    p.eps = d->eps;
+    p.bias = d->bias;
+    p.table_row = d->table_row;
+    p.rope_cs = d->rope_cs;
+    p.rope_pos0 = d->rope_pos0;
+    p.rope_cols = d->rope_cols;
+    p.resid_scale = d->resid_scale;
+    p.out = d->out;
+    p.ldo = d->ldo;
+    p.outb = d->outb;
+    p.ldob = d->ldob;
+    p.out_stats = d->out_stats;
+    p.row0_src = d->row0_src;
+    p.ws = d->ws;
+    p.counters = d->counters;
+    p.splits = 1;
+    p.kb_per_split = (d->K + 63) / 64;
+    return p;
+}
+
+int pi0b_gemm_skinny(const pi0b_gemm_desc* d, int cluster, void* stream) {
+    using namespace pi0b;
+    int rc = configure_once();
+    if (rc) return rc;
+    try {
+        const GemmParams p = params_of(d);
+        CUtensorMap tx = make_tmap_bf16(d->a, d->M, d->K, d->lda, 64);
+        CUtensorMap tw = make_tmap_bf16(d->w, d->N, d->K, d->ldw, 128);
+        return int(launch_skinny(tw, tx, p, d->N, cluster, false, static_cast<cudaStream_t>(stream)));
+    } catch (const std::exception&) {
+        return PI0B_E_INVALID;
+    }
+}
 
 int pi0b_gemm(const pi0b_gemm_desc* d, void* stream) {
     using namespace pi0b;
@@ -147,9 +196,9 @@ int pi0b_random_f64(double* dst, int64_t n, uint64_t seed, double lo, double hi,
     return int(cudaGetLastError());
 }
 
-int pi0b_random_packed_bf16(void* dst, int64_t ldk, int k, int m, int gated, uint64_t seed, double lo,
-                            double hi, void* stream) {
-    return int(pi0b::launch_gen_weight(static_cast<__nv_bfloat16*>(dst), ldk, k, m, gated, seed, lo, hi,
+int pi0b_random_packed_bf16(void* dst, int64_t ldk, int k, int m, int perm, int rope_cols, uint64_t seed,
+                            double lo, double hi, void* stream) {
+    return int(pi0b::launch_gen_weight(static_cast<__nv_bfloat16*>(dst), ldk, k, m, perm, rope_cols, seed, lo, hi,
                                        static_cast<cudaStream_t>(stream)));
 }
 

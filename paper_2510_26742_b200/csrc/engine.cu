@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -41,10 +42,15 @@ cudaError_t launch_gemm(int bn, const CUtensorMap& ta, const CUtensorMap& tb, co
 cudaError_t launch_attention(int head_dim, const AttnParams& p, cudaStream_t stream);
 int attn_key_tile(int head_dim);
 int attn_query_tile();
-cudaError_t launch_gen_weight(__nv_bfloat16* dst, long long ldk, int k, int m, int gated,
+cudaError_t launch_gen_weight(__nv_bfloat16* dst, long long ldk, int k, int m, int perm, int rope_cols,
                               uint64_t seed, double lo, double hi, cudaStream_t st);
 cudaError_t launch_pack_weight(__nv_bfloat16* dst, long long ldk, const double* w, int k, int m,
-                               int gated, cudaStream_t st);
+                               int perm, int rope_cols, cudaStream_t st);
+cudaError_t skinny_configure();
+int skinny_tiles(int n_packed);
+cudaError_t launch_skinny(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p, int n_packed,
+                          int cluster, bool pdl, cudaStream_t stream);
+enum PackPerm { kPermNone = 0, kPermGate128 = 1, kPermGate64 = 2, kPermRope = 3 };
 cudaError_t launch_gen_vector(float* dst, int n, uint64_t seed, double lo, double hi, cudaStream_t st);
 cudaError_t launch_f64_to_f32(float* dst, const double* src, int n, cudaStream_t st);
 cudaError_t launch_rows_to_f32(const double* src, int rows, int cols, float* dst, long long ldd,
@@ -136,24 +142,31 @@ CUtensorMap make_tmap_bf16(const void* base, long long rows, long long cols, lon
 static int round_up(int x, int a) { return (x + a - 1) / a * a; }
 
 // Split-K factor so that the grid approaches one wave of 148 SMs.
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
 static int choose_splits(int m_tiles, int n_tiles, int K, int num_sms) {
     const int ctas = m_tiles * n_tiles;
     const int kb = (K + 63) / 64;
     if (ctas * 2 > num_sms) return 1;
     int s = std::max(1, std::min(num_sms / ctas, kb));
+    s = std::min(s, env_int("PI0B_MAX_SPLITS", 1 << 20));
     const int per = (kb + s - 1) / s;
     return (kb + per - 1) / per;
 }
 
 // ------------------------------------------------------------------ plan records
 
-enum OpKind { kOpGemm, kOpAttn, kOpRowsF32, kOpF64Bf16, kOpF32F64, kOpMemset };
+enum OpKind { kOpGemm, kOpAttn, kOpRowsF32, kOpF64Bf16, kOpF32F64, kOpMemset, kOpSkinny };
 
 struct Op {
     OpKind kind;
     int part;  // 0 = prefix, 1 = action
-    // gemm
+    // gemm (bn = tile width; for kOpSkinny: cluster = K-split, n_packed = weight rows)
     int bn = 0;
+    int cluster = 1, n_packed = 0;
     CUtensorMap ta, tb;
     GemmParams gp{};
     // attention
@@ -184,7 +197,8 @@ struct Op {
 struct NodeWeights {
     int k = 0, m = 0, instances = 0;
     long long ldk = 0;
-    bool gated = false, has_bias = false, has_table = false;
+    int perm = 0, rope_cols = 0;
+    bool has_bias = false, has_table = false;
     std::vector<__nv_bfloat16*> w;
     std::vector<float*> b;
     float* table = nullptr;
@@ -230,6 +244,8 @@ private:
     void build_plan();
     void add_gemm(int part, const std::string& node, int inst, const __nv_bfloat16* A, long long lda,
                   int M, const NodeWeights& W, int widx, int bn, GemmParams gp, bool allow_split = true);
+    void add_skinny(int part, const std::string& node, int inst, const __nv_bfloat16* X, long long ldx, int M,
+                    const NodeWeights& W, int widx, GemmParams gp);
     void add_attn(int part, const std::string& node, int inst, int hd, AttnParams ap);
     void tag(const std::string& node, int inst, const void* ptr, int rows, int cols, long long ld, int bf16);
     float* stats_slot(int part);
@@ -278,6 +294,7 @@ private:
     std::vector<Op> ops_;
     cudaGraphExec_t graph_[3] = {nullptr, nullptr, nullptr};
     std::map<std::pair<std::string, int>, Checkpoint> ck_;
+    bool pdl_ = true;
 };
 
 // ------------------------------------------------------------------ construction
@@ -291,8 +308,10 @@ Engine::Engine(const pi0b_model_config& cfg, const pi0b_engine_options& opt) : c
         throw EngineError(PI0B_E_UNSUPPORTED, "pi0b kernels are built for sm_100a (B200); found sm_" +
                                                   std::to_string(prop.major * 10 + prop.minor));
     num_sms_ = prop.multiProcessorCount;
+    pdl_ = env_int("PI0B_PDL", 1) != 0;
     PI0B_CUDA(gemm_configure());
     PI0B_CUDA(attn_configure());
+    PI0B_CUDA(skinny_configure());
     PI0B_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     alloc_weights();
     alloc_activations();
@@ -331,17 +350,18 @@ void Engine::validate_config() {
 
 void Engine::alloc_weights() {
     const auto& c = c_;
-    auto add = [&](const std::string& id, int k, int m, int inst, bool bias, bool gated = false,
-                   bool table = false) {
+    auto add = [&](const std::string& id, int k, int m, int inst, bool bias, int perm = kPermNone,
+                   bool table = false, int rope_cols = 0) {
         NodeWeights nw;
         nw.k = k;
         nw.m = m;
         nw.instances = inst;
         nw.ldk = round_up(k, 8);
-        nw.gated = gated;
+        nw.perm = perm;
+        nw.rope_cols = rope_cols;
         nw.has_bias = bias;
         nw.has_table = table;
-        const int rows = gated ? round_up(m, 256) : m;
+        const int rows = perm == kPermGate128 ? round_up(m, 256) : m;
         for (int i = 0; i < inst; ++i) {
             nw.w.push_back(alloc<__nv_bfloat16>(size_t(rows) * nw.ldk));
             PI0B_CUDA(cudaMemsetAsync(nw.w.back(), 0, size_t(rows) * nw.ldk * 2, stream_));
@@ -365,14 +385,14 @@ void Engine::alloc_weights() {
     add("llm.proj_in", ve_w, llm_w, 1, true);
     add("llm.qkv", llm_w, llm_qkv, c.llm_layers, false);
     add("llm.proj", llm_q, llm_w, c.llm_layers - 1, false);
-    add("llm.ffn", llm_w, 2 * c.llm_mlp, c.llm_layers - 1, false, true);
+    add("llm.ffn", llm_w, 2 * c.llm_mlp, c.llm_layers - 1, false, kPermGate128);
     add("llm.down", c.llm_mlp, llm_w, c.llm_layers - 1, false);
     add("ae.state_proj", c.ae_state_dim, ae_w, 1, true);
-    add("ae.action_proj", c.ae_action_dim, ae_w, 1, false, false, true);
+    add("ae.action_proj", c.ae_action_dim, ae_w, 1, false, kPermNone, true);
     add("ae.action_out", ae_w, ae_w, 1, true);
-    add("ae.qkv", ae_w, ae_qkv, c.ae_layers, false);
+    add("ae.qkv", ae_w, ae_qkv, c.ae_layers, false, kPermRope, false, ae_q + c.ae_kv_heads * c.ae_head_dim);
     add("ae.proj", ae_q, ae_w, c.ae_layers, false);
-    add("ae.ffn", ae_w, 2 * c.ae_mlp, c.ae_layers, false, true);
+    add("ae.ffn", ae_w, 2 * c.ae_mlp, c.ae_layers, false, kPermGate64);
     add("ae.down", c.ae_mlp, ae_w, c.ae_layers, false);
     add("ae.head", ae_w, c.ae_action_dim, 1, true);
 }
@@ -502,6 +522,30 @@ void Engine::add_gemm(int part, const std::string& node, int inst, const __nv_bf
     ops_.push_back(op);
 }
 
+// Action-expert GEMM on the swap-AB skinny kernel: K split over a cluster of up to 8 CTAs so
+// that tiles x cluster approaches one wave while every CTA keeps >= 2 k-blocks.
+void Engine::add_skinny(int part, const std::string& node, int inst, const __nv_bfloat16* X, long long ldx, int M,
+                        const NodeWeights& W, int widx, GemmParams gp) {
+    Op op;
+    op.kind = kOpSkinny;
+    op.part = part;
+    const int n_packed = W.perm == kPermGate64 ? W.m : gp.N;
+    op.n_packed = n_packed;
+    op.tb = make_tmap_bf16(X, M, W.k, ldx, 64);
+    op.ta = make_tmap_bf16(W.w.at(size_t(widx)), n_packed, W.k, W.ldk, 128);
+    gp.M = M;
+    gp.K = W.k;
+    gp.splits = 1;
+    gp.kb_per_split = (W.k + 63) / 64;
+    if (W.perm == kPermRope) gp.rope_cols = W.rope_cols;
+    const int tiles = skinny_tiles(n_packed), kb = (W.k + 63) / 64;
+    int cl = 1;
+    while (cl < 8 && tiles * cl * 2 <= num_sms_ && kb >= cl * 4) cl *= 2;
+    op.cluster = std::min(cl, env_int("PI0B_MAX_CLUSTER", 8));
+    op.gp = gp;
+    ops_.push_back(op);
+}
+
 void Engine::add_attn(int part, const std::string& node, int inst, int hd, AttnParams ap) {
     Op op;
     op.kind = kOpAttn;
@@ -512,7 +556,10 @@ void Engine::add_attn(int part, const std::string& node, int inst, int hd, AttnP
     const int total = ap.rows0 + ap.rows1;
     const int kvt = attn_key_tile(hd);
     const int ctas = q_tiles * ap.kv_heads;
-    int splits = std::max(1, std::min(num_sms_ / std::max(1, ctas), (total + 63) / 64));
+    // Split the keys only when the query tiles cannot fill ~64 CTAs (the action expert's
+    // 8 stacked tiles); each split keeps >= 2 key tiles and the merge reads <= 16 partials.
+    int splits = std::max(1, std::min(std::min(env_int("PI0B_ATTN_CTAS", 32) / std::max(1, ctas),
+                                               (total + 2 * kvt - 1) / (2 * kvt)), 8));
     int per = round_up((total + splits - 1) / splits, kvt);
     splits = (total + per - 1) / per;
     ap.kv_splits = splits;
@@ -807,7 +854,7 @@ void Engine::build_plan() {
         g.bias = Wv["ae.state_proj"].b[0];
         g.out = st_;
         g.ldo = ae_w_;
-        add_gemm(1, "ae.state_proj", 0, state_b_, state_ld_, 1, Wv["ae.state_proj"], 0, 128, g);
+        add_skinny(1, "ae.state_proj", 0, state_b_, state_ld_, 1, Wv["ae.state_proj"], 0, g);
         tag("ae.state_proj", 0, st_, 1, ae_w_, ae_w_, 0);
     }
     const float inv_ae = 1.0f / float(ae_w_);
@@ -820,7 +867,7 @@ void Engine::build_plan() {
             g.table_row = Wv["ae.action_proj"].table + size_t(s) * ae_w_;
             g.out = ap_b_;
             g.ldo = ae_w_;
-            add_gemm(1, "ae.action_proj", s, ab_, act_ld_, C_, Wv["ae.action_proj"], 0, 128, g);
+            add_skinny(1, "ae.action_proj", s, ab_, act_ld_, C_, Wv["ae.action_proj"], 0, g);
             tag("ae.action_proj", s, ap_b_, C_, ae_w_, ae_w_, 1);
         }
         float* ys = stats_slot(1);
@@ -836,7 +883,7 @@ void Engine::build_plan() {
             g.ldob = ae_w_;
             g.out_stats = ys + 1;
             g.row0_src = st_;
-            add_gemm(1, "ae.action_out", s, ap_b_, ae_w_, C_, Wv["ae.action_out"], 0, 128, g);
+            add_skinny(1, "ae.action_out", s, ap_b_, ae_w_, C_, Wv["ae.action_out"], 0, g);
             tag("ae.suffix", s, y_, S_, ae_w_, ae_w_, 0);
         }
         for (int l = 0; l < NA; ++l) {
@@ -854,7 +901,7 @@ void Engine::build_plan() {
                 g.rope_cols = ae_q_ + ae_kv_;
                 g.out = aqkv_;
                 g.ldo = ae_qkv_n;
-                add_gemm(1, "ae.qkv", i, yb_, ae_w_, S_, Wv["ae.qkv"], l, 256, g);
+                add_skinny(1, "ae.qkv", i, yb_, ae_w_, S_, Wv["ae.qkv"], l, g);
                 tag("ae.qkv", i, aqkv_, S_, ae_qkv_n, ae_qkv_n, 1);
             }
             {   // cross attention over [LLM KV_l ; own KV] (ae.kcat / ae.vcat)
@@ -888,7 +935,7 @@ void Engine::build_plan() {
                 g.outb = yb_;
                 g.ldob = ae_w_;
                 g.out_stats = ps;
-                add_gemm(1, "ae.proj", i, ao_, ae_q_, S_, Wv["ae.proj"], l, 128, g);
+                add_skinny(1, "ae.proj", i, ao_, ae_q_, S_, Wv["ae.proj"], l, g);
                 tag("ae.proj", i, y_, S_, ae_w_, ae_w_, 0);
             }
             {
@@ -901,7 +948,7 @@ void Engine::build_plan() {
                 g.eps = 1e-6f;
                 g.out = ag_;
                 g.ldo = c.ae_mlp;
-                add_gemm(1, "ae.ffn", i, yb_, ae_w_, S_, Wv["ae.ffn"], l, 256, g);
+                add_skinny(1, "ae.ffn", i, yb_, ae_w_, S_, Wv["ae.ffn"], l, g);
                 tag("ae.ffn", i, ag_, S_, c.ae_mlp, c.ae_mlp, 1);
             }
             ys = stats_slot(1);
@@ -915,7 +962,7 @@ void Engine::build_plan() {
                 g.outb = yb_;
                 g.ldob = ae_w_;
                 g.out_stats = ys;
-                add_gemm(1, "ae.down", i, ag_, c.ae_mlp, S_, Wv["ae.down"], l, 128, g);
+                add_skinny(1, "ae.down", i, ag_, c.ae_mlp, S_, Wv["ae.down"], l, g);
                 tag("ae.down", i, y_, S_, ae_w_, ae_w_, 0);
             }
         }
@@ -933,7 +980,7 @@ void Engine::build_plan() {
             g.ldo = act_ld_;
             g.outb = ab_;
             g.ldob = act_ld_;
-            add_gemm(1, "ae.head", s, yb_ + ae_w_, ae_w_, C_, Wv["ae.head"], 0, 64, g);
+            add_skinny(1, "ae.head", s, yb_ + ae_w_, ae_w_, C_, Wv["ae.head"], 0, g);
             tag("ae.head", s, a_, C_, c.ae_action_dim, act_ld_, 0);
         }
     }
@@ -981,7 +1028,7 @@ void Engine::gen_weights(uint64_t seed) {
         NodeWeights& nw = kv.second;
         const double lim = 1.0 / std::sqrt(double(std::max(1, nw.k)));
         for (int i = 0; i < nw.instances; ++i) {
-            PI0B_CUDA(launch_gen_weight(nw.w[i], nw.ldk, nw.k, nw.m, nw.gated ? 1 : 0,
+            PI0B_CUDA(launch_gen_weight(nw.w[i], nw.ldk, nw.k, nw.m, nw.perm, nw.rope_cols,
                                         seed_hash(seed, id, uint64_t(i), 1), -lim, lim, stream_));
             if (nw.has_bias)
                 PI0B_CUDA(launch_gen_vector(nw.b[i], nw.m, seed_hash(seed, id, uint64_t(i), 2), -lim, lim, stream_));
@@ -1010,7 +1057,7 @@ void Engine::set_weight(const std::string& id, long long inst, const double* w, 
     // Stream-ordered upload: a pageable cudaMemcpy may return before its DMA lands, and the
     // engine stream does not synchronise with the legacy stream.
     PI0B_CUDA(cudaMemcpyAsync(dw, w, size_t(k) * m * 8, cudaMemcpyHostToDevice, stream_));
-    cudaError_t e = launch_pack_weight(nw.w[size_t(inst)], nw.ldk, dw, int(k), int(m), nw.gated ? 1 : 0, stream_);
+    cudaError_t e = launch_pack_weight(nw.w[size_t(inst)], nw.ldk, dw, int(k), int(m), nw.perm, nw.rope_cols, stream_);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream_);
     cudaFree(dw);
     PI0B_CUDA(e);
@@ -1063,6 +1110,9 @@ void Engine::run_ops(int part, cudaStream_t st) {
         if (part != 2 && op.part != part) continue;  // part 2 = everything
         switch (op.kind) {
             case kOpGemm: PI0B_CUDA(launch_gemm(op.bn, op.ta, op.tb, op.gp, st)); break;
+            case kOpSkinny:
+                PI0B_CUDA(launch_skinny(op.ta, op.tb, op.gp, op.n_packed, op.cluster, pdl_, st));
+                break;
             case kOpAttn: PI0B_CUDA(launch_attention(op.hd, op.ap, st)); break;
             case kOpRowsF32:
                 PI0B_CUDA(launch_rows_to_f32(op.src64, op.rows, op.cols, op.dst32, op.ld32, op.dstb, op.ldb,
@@ -1137,7 +1187,7 @@ int Engine::kernel_count(int part) const {
 
 // One line per planned op: "<index> <part> <kind> <node> <inst> <grid> <detail>".
 std::string Engine::describe() const {
-    static const char* kinds[] = {"gemm", "attn", "rows_f32", "f64_bf16", "f32_f64", "memset"};
+    static const char* kinds[] = {"gemm", "attn", "rows_f32", "f64_bf16", "f32_f64", "memset", "skinny"};
     std::string s;
     int idx = 0;
     for (const Op& op : ops_) {
@@ -1146,6 +1196,10 @@ std::string Engine::describe() const {
             const int mt = (op.gp.M + 127) / 128, nt = (op.gp.N + op.bn - 1) / op.bn;
             snprintf(buf, sizeof buf, "%d %d gemm %s %d %dx%dx%d M=%d N=%d K=%d bn=%d mode=%d\n", idx, op.part,
                      op.node.c_str(), op.inst, mt, nt, op.gp.splits, op.gp.M, op.gp.N, op.gp.K, op.bn, op.gp.mode);
+        } else if (op.kind == kOpSkinny) {
+            snprintf(buf, sizeof buf, "%d %d skinny %s %d tiles=%d cluster=%d M=%d N=%d K=%d mode=%d\n", idx, op.part,
+                     op.node.c_str(), op.inst, skinny_tiles(op.n_packed), op.cluster, op.gp.M, op.gp.N, op.gp.K,
+                     op.gp.mode);
         } else if (op.kind == kOpAttn) {
             snprintf(buf, sizeof buf, "%d %d attn %s %d splits=%d q=%d kv=%d hd=%d\n", idx, op.part, op.node.c_str(),
                      op.inst, op.ap.kv_splits, op.ap.q_rows, op.ap.rows0 + op.ap.rows1, op.hd);
@@ -1163,10 +1217,11 @@ std::string Engine::describe() const {
 double Engine::time_node(const std::string& node, int reps, int* launches) {
     std::vector<const Op*> sel;
     for (const Op& op : ops_)
-        if (op.node == node && (op.kind == kOpGemm || op.kind == kOpAttn)) sel.push_back(&op);
+        if (op.node == node && (op.kind == kOpGemm || op.kind == kOpAttn || op.kind == kOpSkinny)) sel.push_back(&op);
     if (sel.empty()) throw EngineError(PI0B_E_INVALID, "no kernels for node '" + node + "'");
     auto fire = [&](const Op& op) {
         if (op.kind == kOpGemm) PI0B_CUDA(launch_gemm(op.bn, op.ta, op.tb, op.gp, stream_));
+        else if (op.kind == kOpSkinny) PI0B_CUDA(launch_skinny(op.ta, op.tb, op.gp, op.n_packed, op.cluster, pdl_, stream_));
         else PI0B_CUDA(launch_attention(op.hd, op.ap, stream_));
     };
     for (const Op* op : sel) fire(*op);

@@ -22,14 +22,15 @@ namespace pi0b {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kGemmThreads = 192;
+constexpr int kGemmThreads = 64 + 8 * 32;  // TMA warp, MMA warp, 8 epilogue warps
 
 template <int BN, int STAGES>
 struct GemmCfg {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int BAR_BYTES = 256;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + BAR_BYTES + BN * 4 + 1024;
     static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
 };
 
@@ -53,25 +54,40 @@ PI0B_DEV void store_bf16x32(__nv_bfloat16* dst, const float (&v)[32], int nvalid
     }
 }
 
-// Read 32 fp32 split-K partial sums of one row from the workspace and clear them.
-PI0B_DEV void ws_take32(float* src, float (&v)[32], int nvalid) {
+PI0B_DEV void store_f32x32(float* dst, const float (&v)[32], int nvalid) {
+    if (nvalid >= 32) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < nvalid) dst[j] = v[j];
+    }
+}
+
+PI0B_DEV void load_f32x32(const float* src, float (&v)[32], int nvalid, bool cg) {
     if (nvalid >= 32) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
-            float4 f = __ldcg(reinterpret_cast<const float4*>(src + j));
+            const float4 f = cg ? __ldcg(reinterpret_cast<const float4*>(src + j)) : *reinterpret_cast<const float4*>(src + j);
             v[j] = f.x; v[j + 1] = f.y; v[j + 2] = f.z; v[j + 3] = f.w;
-            __stcg(reinterpret_cast<float4*>(src + j), make_float4(0.f, 0.f, 0.f, 0.f));
         }
     } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            if (j < nvalid) {
-                v[j] = __ldcg(src + j);
-                __stcg(src + j, 0.f);
-            } else {
-                v[j] = 0.f;
-            }
-        }
+        for (int j = 0; j < 32; ++j) v[j] = j < nvalid ? (cg ? __ldcg(src + j) : src[j]) : 0.f;
+    }
+}
+
+// Read 32 fp32 split-K partial sums of one row from the workspace and clear them.
+PI0B_DEV void ws_take32(float* src, float (&v)[32], int nvalid) {
+    load_f32x32(src, v, nvalid, true);
+    if (nvalid >= 32) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) __stcg(reinterpret_cast<float4*>(src + j), make_float4(0.f, 0.f, 0.f, 0.f));
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < nvalid) __stcg(src + j, 0.f);
     }
 }
 
@@ -86,13 +102,23 @@ PI0B_DEV void ws_add32(float* dst, const float (&v)[32], int nvalid) {
     }
 }
 
+PI0B_DEV float sumsq32(const float (&v)[32], int nvalid) {
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) s += j < nvalid ? v[j] * v[j] : 0.f;
+    return s;
+}
+
 }  // namespace
 
-template <int BN, int STAGES>
+// MODE is a GemmMode; each instantiation carries only its own epilogue so the code a
+// CTA executes once (cold instruction cache) stays small.
+template <int BN, int STAGES, int MODE>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmParams p) {
     using Cfg = GemmCfg<BN, STAGES>;
+    constexpr bool kPaired = MODE == kModeGate || (MODE == kModeBf16 && BN == 256);
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -103,6 +129,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint64_t* accum_full = empty + STAGES;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_full + 1);
     int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+    float* sm_vec = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::BAR_BYTES);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -161,49 +188,56 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         __syncwarp();
     } else {
-        // ------------------------------------------------------------ epilogue
+        // ------------------------------------------------------------ epilogue (8 warps)
+        // Warp w may only touch TMEM lanes [32*(w%4), +32): two warps share each lane
+        // quarter and split the tile's columns (hsel).
         const int q = warp & 3;
+        const int hsel = (warp - 2) >> 2;
+        const int etid = threadIdx.x - 64;  // 0..255
         const int row_in_tile = q * 32 + lane;
         const int r = m_tile * BM + row_in_tile;
         const bool valid = r < p.M;
         const uint32_t trow = tmem + (uint32_t(q * 32) << 16);
         const int n0 = n_tile * BN;
-        const int etid = threadIdx.x - 64;  // 0..127
+        const bool split_k = p.splits > 1;
+
+        // Stage the per-column vector (bias or SiluBias table row), zero-padded, while the
+        // mainloop runs; prefetch the row scale.
+        const float* vec = MODE == kModeSiluTable ? p.table_row : ((p.flags & kFlagBias) ? p.bias : nullptr);
+        for (int c = etid; c < BN; c += 256) sm_vec[c] = (vec && n0 + c < p.N) ? vec[n0 + c] : 0.f;
+        float rs = 1.0f;
+        if ((p.flags & kFlagRowScale) && valid) rs = 1.0f / sqrtf(p.row_stats[r] * p.inv_width + p.eps);
+        named_bar_sync(1, 256);
 
         mbar_wait(accum_full, 0);
         tc_fence_after();
 
-        const bool split_k = p.splits > 1;
-        const bool resid = p.mode == kModeResid;
-        float rs = 1.0f;
-        if ((p.flags & kFlagRowScale) && valid)
-            rs = 1.0f / sqrtf(p.row_stats[r] * p.inv_width + p.eps);
+        constexpr int NC = BN / 32;                 // 32-column chunks in the tile
+        constexpr int NP = NC / 2;                  // (c, c + NP) pairs
+        const int c_begin = kPaired ? hsel * (NP / 2) : hsel * (NC / 2);
+        const int c_end = kPaired ? c_begin + NP / 2 : c_begin + NC / 2;
+        bool from_ws = false;
 
         if (split_k) {
             // Partial sums -> global; the last-arriving CTA of the tile finishes.
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = hsel * (NC / 2); c < (hsel + 1) * (NC / 2); ++c) {
                 float v[32];
                 tmem_ld32(trow + c * 32, v);
                 const int col0 = n0 + c * 32;
                 const int nv = min(32, p.N - col0);
-                if (valid && nv > 0) {
-                    if (resid) {
-                        float* dst = reinterpret_cast<float*>(p.out) + (long long)r * p.ldo + col0;
+                if (!valid || nv <= 0) continue;
+                if (MODE == kModeResid) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            float b = 0.f;
-                            if ((p.flags & kFlagBias) && split == 0 && j < nv) b = p.bias[col0 + j];
-                            v[j] = p.resid_scale * (v[j] * rs + b);
-                        }
-                        ws_add32(dst, v, nv);
-                    } else {
-                        ws_add32(p.ws + (long long)r * p.N + col0, v, nv);
-                    }
+                    for (int j = 0; j < 32; ++j)
+                        v[j] = p.resid_scale * (v[j] * rs + (split == 0 ? sm_vec[c * 32 + j] : 0.f));
+                    ws_add32(reinterpret_cast<float*>(p.out) + (long long)r * p.ldo + col0, v, nv);
+                } else {
+                    ws_add32(p.ws + (long long)r * p.N + col0, v, nv);
                 }
             }
             __threadfence();
-            named_bar_sync(1, 128);
+            named_bar_sync(1, 256);
             if (etid == 0) {
                 const int tile = m_tile * gridDim.y + n_tile;
                 const int prev = atomicAdd(&p.counters[tile], 1);
@@ -211,139 +245,115 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 if (last) atomicExch(&p.counters[tile], 0);
                 *last_flag = last;
             }
-            named_bar_sync(1, 128);
+            named_bar_sync(1, 256);
             if (!*last_flag) goto epilogue_done;
             __threadfence();
+            from_ws = true;
         }
 
-        if (resid) {
-            // h += scale*(rs*z + b) (already accumulated when split), bf16 shadow, row stats.
+        if constexpr (MODE == kModeResid) {
+            // h += scale*(rs*z + b) in place (already accumulated when split), bf16 shadow, row stats.
             float ss = 0.f;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                float v[32];
-                if (!split_k) tmem_ld32(trow + c * 32, v);
+            for (int c = c_begin; c < c_end; ++c) {
+                float v[32], h[32];
+                if (!from_ws) tmem_ld32(trow + c * 32, v);
                 const int col0 = n0 + c * 32;
                 const int nv = min(32, p.N - col0);
                 if (!valid || nv <= 0) continue;
-                float* h = reinterpret_cast<float*>(p.out) + (long long)r * p.ldo + col0;
+                float* hp = reinterpret_cast<float*>(p.out) + (long long)r * p.ldo + col0;
+                load_f32x32(hp, h, nv, from_ws);
+                if (!from_ws) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    if (j < nv) {
-                        float x;
-                        if (split_k) {
-                            x = __ldcg(h + j);
-                        } else {
-                            float b = (p.flags & kFlagBias) ? p.bias[col0 + j] : 0.f;
-                            x = h[j] + p.resid_scale * (v[j] * rs + b);
-                            h[j] = x;
-                        }
-                        v[j] = x;
-                        ss += x * x;
-                    }
+                    for (int j = 0; j < 32; ++j) h[j] += p.resid_scale * (v[j] * rs + sm_vec[c * 32 + j]);
+                    store_f32x32(hp, h, nv);
                 }
+                ss += sumsq32(h, nv);
                 if (p.outb)
-                    store_bf16x32(reinterpret_cast<__nv_bfloat16*>(p.outb) + (long long)r * p.ldob + col0, v, nv);
+                    store_bf16x32(reinterpret_cast<__nv_bfloat16*>(p.outb) + (long long)r * p.ldob + col0, h, nv);
             }
             if (valid && p.out_stats) atomicAdd(p.out_stats + r, ss);
-        } else if (p.mode == kModeGate) {
-            // Tile columns [0, BN/2) are up, [BN/2, BN) the matching gate columns.
-            constexpr int H = BN / 2;
-#pragma unroll 1
-            for (int c = 0; c < H / 32; ++c) {
-                float u[32], g[32];
-                const int ocol0 = n_tile * H + c * 32;
-                const int nv = min(32, p.N / 2 - ocol0);
-                if (split_k) {
-                    if (valid) {
-                        ws_take32(p.ws + (long long)r * p.N + n0 + c * 32, u, 32);
-                        ws_take32(p.ws + (long long)r * p.N + n0 + H + c * 32, g, 32);
-                    }
-                } else {
-                    tmem_ld32(trow + c * 32, u);
-                    tmem_ld32(trow + H + c * 32, g);
-                }
-                if (!valid || nv <= 0) continue;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) u[j] = (u[j] * rs) * gelu_tanh(g[j] * rs);
-                store_bf16x32(reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)r * p.ldo + ocol0, u, nv);
-            }
-        } else if ((p.flags & kFlagRope) && n0 < p.rope_cols) {
-            // RoPE, half-split pairing (j, j+128) inside each 256-wide head
-            // (proj/src/tensor.cpp:150-178). BN == 256 so a tile is exactly one head.
+        } else if constexpr (kPaired) {
+            // Gate: tile columns [0, BN/2) are up, [BN/2, BN) the matching gate columns.
+            // RoPE (BN == 256, one head per tile): pairs (j, j+128), proj/src/tensor.cpp:150-178.
+            const bool rope = MODE == kModeBf16 && (p.flags & kFlagRope) && n0 < p.rope_cols;
             const float2* cs = reinterpret_cast<const float2*>(p.rope_cs) + (long long)(p.rope_pos0 + r) * 128;
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
+            for (int c = c_begin; c < c_end; ++c) {
                 float a[32], b[32];
-                if (split_k) {
+                if (from_ws) {
                     if (valid) {
                         ws_take32(p.ws + (long long)r * p.N + n0 + c * 32, a, 32);
-                        ws_take32(p.ws + (long long)r * p.N + n0 + 128 + c * 32, b, 32);
+                        ws_take32(p.ws + (long long)r * p.N + n0 + (c + NP) * 32, b, 32);
                     }
                 } else {
                     tmem_ld32(trow + c * 32, a);
-                    tmem_ld32(trow + 128 + c * 32, b);
+                    tmem_ld32(trow + (c + NP) * 32, b);
                 }
                 if (!valid) continue;
+                if (MODE == kModeGate) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    float x = a[j] * rs, y = b[j] * rs;
-                    if (p.flags & kFlagBias) {
-                        x += p.bias[n0 + c * 32 + j];
-                        y += p.bias[n0 + 128 + c * 32 + j];
+                    for (int j = 0; j < 32; ++j) a[j] = (a[j] * rs) * gelu_tanh(b[j] * rs);
+                    const int ocol0 = n_tile * (BN / 2) + c * 32;
+                    store_bf16x32(reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)r * p.ldo + ocol0, a,
+                                  min(32, p.N / 2 - ocol0));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        a[j] = a[j] * rs + sm_vec[c * 32 + j];
+                        b[j] = b[j] * rs + sm_vec[(c + NP) * 32 + j];
                     }
-                    const float2 t = cs[c * 32 + j];
-                    a[j] = x * t.x - y * t.y;
-                    b[j] = x * t.y + y * t.x;
+                    if (rope) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 2) {
+                            const float4 t = *reinterpret_cast<const float4*>(cs + c * 32 + j);
+                            const float x0 = a[j], y0 = b[j], x1 = a[j + 1], y1 = b[j + 1];
+                            a[j] = x0 * t.x - y0 * t.y;
+                            b[j] = x0 * t.y + y0 * t.x;
+                            a[j + 1] = x1 * t.z - y1 * t.w;
+                            b[j + 1] = x1 * t.w + y1 * t.z;
+                        }
+                    }
+                    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)r * p.ldo + n0;
+                    store_bf16x32(o + c * 32, a, min(32, p.N - (n0 + c * 32)));
+                    store_bf16x32(o + (c + NP) * 32, b, min(32, p.N - (n0 + (c + NP) * 32)));
                 }
-                __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)r * p.ldo + n0;
-                store_bf16x32(o + c * 32, a, 32);
-                store_bf16x32(o + 128 + c * 32, b, 32);
             }
         } else {
-            // kModeBf16 / kModeF32Store / kModeSiluTable, 32 columns at a time.
+            // kModeBf16 (BN < 256) / kModeF32Store / kModeSiluTable, 32 columns at a time.
             float ss = 0.f;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = c_begin; c < c_end; ++c) {
                 float v[32];
                 const int col0 = n0 + c * 32;
                 const int nv = min(32, p.N - col0);
-                if (split_k) {
+                if (from_ws) {
                     if (valid && nv > 0) ws_take32(p.ws + (long long)r * p.N + col0, v, nv);
                 } else {
                     tmem_ld32(trow + c * 32, v);
                 }
                 if (!valid || nv <= 0) continue;
+                if constexpr (MODE == kModeSiluTable) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    float x = v[j];
-                    if (j < nv) {
-                        if (p.mode == kModeSiluTable) {
-                            x = silu_f(x + p.table_row[col0 + j]);
-                        } else {
-                            x *= rs;
-                            if (p.flags & kFlagBias) x += p.bias[col0 + j];
-                            if (p.flags & kFlagGelu) x = gelu_tanh(x);
-                        }
+                    for (int j = 0; j < 32; ++j) v[j] = silu_f(v[j] + sm_vec[c * 32 + j]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = v[j] * rs + sm_vec[c * 32 + j];
+                    if (MODE == kModeBf16 && (p.flags & kFlagGelu)) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
                     }
-                    v[j] = x;
                 }
-                if (p.mode == kModeF32Store) {
-                    float* o = reinterpret_cast<float*>(p.out) + (long long)r * p.ldo + col0;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        if (j < nv) {
-                            o[j] = v[j];
-                            ss += v[j] * v[j];
-                        }
-                    }
+                if constexpr (MODE == kModeF32Store) {
+                    store_f32x32(reinterpret_cast<float*>(p.out) + (long long)r * p.ldo + col0, v, nv);
+                    ss += sumsq32(v, nv);
                     if (p.outb)
                         store_bf16x32(reinterpret_cast<__nv_bfloat16*>(p.outb) + (long long)r * p.ldob + col0, v, nv);
                 } else {
                     store_bf16x32(reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)r * p.ldo + col0, v, nv);
                 }
             }
-            if (p.mode == kModeF32Store) {
+            if constexpr (MODE == kModeF32Store) {
                 if (valid && p.out_stats) atomicAdd(p.out_stats + r, ss);
                 // Optional extra row -1 (the state token of ae.suffix,
                 // proj/src/builder.cpp:311-312), written by the first tile row.
@@ -351,7 +361,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     float* o = reinterpret_cast<float*>(p.out) - p.ldo;
                     __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(p.outb) - p.ldob;
                     float s0 = 0.f;
-                    for (int j = n0; j < min(n0 + BN, p.N); ++j) {
+                    for (int j = n0 + c_begin * 32; j < min(n0 + c_end * 32, p.N); ++j) {
                         const float x = p.row0_src[j];
                         o[j] = x;
                         if (p.outb) ob[j] = __float2bfloat16_rn(x);
@@ -371,36 +381,60 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 // ------------------------------------------------------------------ host side
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int MODE>
 static cudaError_t configure_t() {
-    return cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 GemmCfg<BN, STAGES>::SMEM);
 }
 
 template <int BN, int STAGES>
-static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
-                                 int m_tiles, int n_tiles, cudaStream_t stream) {
-    dim3 grid(m_tiles, n_tiles, p.splits);
-    gemm_tc_kernel<BN, STAGES><<<grid, kGemmThreads, GemmCfg<BN, STAGES>::SMEM, stream>>>(ta, tb, p);
-    return cudaGetLastError();
+static cudaError_t configure_bn() {
+    cudaError_t e = configure_t<BN, STAGES, kModeBf16>();
+    if (e == cudaSuccess) e = configure_t<BN, STAGES, kModeF32Store>();
+    if (e == cudaSuccess) e = configure_t<BN, STAGES, kModeResid>();
+    if (e == cudaSuccess) e = configure_t<BN, STAGES, kModeSiluTable>();
+    return e;
 }
 
 // Must run once per device before any launch (not capturable).
 cudaError_t gemm_configure() {
-    cudaError_t e = configure_t<256, 4>();
-    if (e == cudaSuccess) e = configure_t<128, 6>();
-    if (e == cudaSuccess) e = configure_t<64, 8>();
+    cudaError_t e = configure_bn<256, 4>();
+    if (e == cudaSuccess) e = configure_t<256, 4, kModeGate>();
+    if (e == cudaSuccess) e = configure_bn<128, 6>();
+    if (e == cudaSuccess) e = configure_bn<64, 8>();
     return e;
+}
+
+template <int BN, int STAGES, int MODE>
+static cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, dim3 grid,
+                            cudaStream_t stream) {
+    gemm_tc_kernel<BN, STAGES, MODE><<<grid, kGemmThreads, GemmCfg<BN, STAGES>::SMEM, stream>>>(ta, tb, p);
+    return cudaGetLastError();
+}
+
+template <int BN, int STAGES>
+static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, dim3 grid,
+                             cudaStream_t stream) {
+    switch (p.mode) {
+        case kModeBf16: return launch_t<BN, STAGES, kModeBf16>(ta, tb, p, grid, stream);
+        case kModeF32Store: return launch_t<BN, STAGES, kModeF32Store>(ta, tb, p, grid, stream);
+        case kModeResid: return launch_t<BN, STAGES, kModeResid>(ta, tb, p, grid, stream);
+        case kModeSiluTable: return launch_t<BN, STAGES, kModeSiluTable>(ta, tb, p, grid, stream);
+        case kModeGate:
+            if constexpr (BN == 256) return launch_t<BN, STAGES, kModeGate>(ta, tb, p, grid, stream);
+            return cudaErrorInvalidValue;
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 cudaError_t launch_gemm(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                         cudaStream_t stream) {
-    const int m_tiles = (p.M + BM - 1) / BM;
-    const int n_tiles = (p.N + bn - 1) / bn;
+    if ((p.flags & kFlagRope) && bn != 256) return cudaErrorInvalidValue;
+    const dim3 grid((p.M + BM - 1) / BM, (p.N + bn - 1) / bn, p.splits);
     switch (bn) {
-        case 256: return launch_gemm_t<256, 4>(ta, tb, p, m_tiles, n_tiles, stream);
-        case 128: return launch_gemm_t<128, 6>(ta, tb, p, m_tiles, n_tiles, stream);
-        case 64: return launch_gemm_t<64, 8>(ta, tb, p, m_tiles, n_tiles, stream);
+        case 256: return launch_bn<256, 4>(ta, tb, p, grid, stream);
+        case 128: return launch_bn<128, 6>(ta, tb, p, grid, stream);
+        case 64: return launch_bn<64, 8>(ta, tb, p, grid, stream);
         default: return cudaErrorInvalidValue;
     }
 }

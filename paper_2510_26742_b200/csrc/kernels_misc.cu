@@ -14,19 +14,33 @@
 
 namespace pi0b {
 
-// Packed row of logical weight column j (0 <= j < m).  Gated FFN weights
-// ([up | gate], proj/src/passes.cpp:448) are interleaved per 256-wide GEMM tile:
-// tile t holds up columns [128t, 128t+128) then the matching gate columns.
-__host__ __device__ inline int packed_row(int j, int m, int gated) {
-    if (!gated) return j;
-    const int half = m / 2;
-    const bool gate = j >= half;
-    const int c = gate ? j - half : j;
-    return (c / 128) * 256 + (gate ? 128 : 0) + (c % 128);
+// Packed row of logical weight column j (0 <= j < m) — the weight layout the GEMMs consume.
+//   kPermNone   identity;
+//   kPermGate*  gated FFN weights [up | gate] (proj/src/passes.cpp:448) interleaved per tile:
+//               tile t holds up columns [G t, G t + G) then the matching gate columns
+//               (G = 128 for the 256-wide prefill tiles, 64 for the 128-row skinny tiles);
+//   kPermRope   skinny qkv: inside every 256-wide head the RoPE partners (j, j + 128) land
+//               64 rows apart in the same 128-row tile; columns >= rope_cols (V) stay put.
+enum PackPerm { kPermNone = 0, kPermGate128 = 1, kPermGate64 = 2, kPermRope = 3 };
+
+__host__ __device__ inline int packed_row(int j, int m, int perm, int rope_cols) {
+    if (perm == kPermGate128 || perm == kPermGate64) {
+        const int G = perm == kPermGate128 ? 128 : 64;
+        const int half = m / 2;
+        const bool gate = j >= half;
+        const int c = gate ? j - half : j;
+        return (c / G) * (2 * G) + (gate ? G : 0) + (c % G);
+    }
+    if (perm == kPermRope && j < rope_cols) {
+        const int h = j >> 8, w = j & 255;
+        const int part = w >> 7, i = w & 127;
+        return (h << 8) + (i >> 6) * 128 + part * 64 + (i & 63);
+    }
+    return j;
 }
 
 // grid: (ceil(k/8 / 32), m) ; block 32 -> each thread emits 8 consecutive k of column j.
-__global__ void gen_weight_kernel(__nv_bfloat16* dst, long long ldk, int k, int m, int gated,
+__global__ void gen_weight_kernel(__nv_bfloat16* dst, long long ldk, int k, int m, int perm, int rope_cols,
                                   uint64_t seed, double lo, double hi) {
     const int j = blockIdx.y;
     const int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
@@ -37,7 +51,7 @@ __global__ void gen_weight_kernel(__nv_bfloat16* dst, long long ldk, int k, int 
         const int pp = p0 + i;
         v[i] = pp < k ? f64_to_bf16_bits(uniform_at(seed, uint64_t(pp) * m + j, lo, hi)) : 0;
     }
-    uint16_t* out = reinterpret_cast<uint16_t*>(dst) + (long long)packed_row(j, m, gated) * ldk + p0;
+    uint16_t* out = reinterpret_cast<uint16_t*>(dst) + (long long)packed_row(j, m, perm, rope_cols) * ldk + p0;
     if (p0 + 8 <= k && (ldk % 8) == 0) {
         uint4 u;
         u.x = v[0] | (uint32_t(v[1]) << 16);
@@ -52,11 +66,11 @@ __global__ void gen_weight_kernel(__nv_bfloat16* dst, long long ldk, int k, int 
 
 // Host fp64 W[k, m] (already on device) -> packed bf16 [N, K].
 __global__ void pack_weight_kernel(__nv_bfloat16* dst, long long ldk, const double* w, int k, int m,
-                                   int gated) {
+                                   int perm, int rope_cols) {
     const int j = blockIdx.y;
     const int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
     if (p0 >= k) return;
-    uint16_t* out = reinterpret_cast<uint16_t*>(dst) + (long long)packed_row(j, m, gated) * ldk + p0;
+    uint16_t* out = reinterpret_cast<uint16_t*>(dst) + (long long)packed_row(j, m, perm, rope_cols) * ldk + p0;
     for (int i = 0; i < 8 && p0 + i < k; ++i) out[i] = f64_to_bf16_bits(w[(long long)(p0 + i) * m + j]);
 }
 
@@ -104,16 +118,16 @@ __global__ void f32_to_f64_kernel(const float* src, long long lds, int rows, int
 
 // --------------------------------------------------------------------- launchers
 
-cudaError_t launch_gen_weight(__nv_bfloat16* dst, long long ldk, int k, int m, int gated,
+cudaError_t launch_gen_weight(__nv_bfloat16* dst, long long ldk, int k, int m, int perm, int rope_cols,
                               uint64_t seed, double lo, double hi, cudaStream_t st) {
     dim3 grid((k / 8 + 1 + 31) / 32, m);
-    gen_weight_kernel<<<grid, 32, 0, st>>>(dst, ldk, k, m, gated, seed, lo, hi);
+    gen_weight_kernel<<<grid, 32, 0, st>>>(dst, ldk, k, m, perm, rope_cols, seed, lo, hi);
     return cudaGetLastError();
 }
 cudaError_t launch_pack_weight(__nv_bfloat16* dst, long long ldk, const double* w, int k, int m,
-                               int gated, cudaStream_t st) {
+                               int perm, int rope_cols, cudaStream_t st) {
     dim3 grid((k / 8 + 1 + 31) / 32, m);
-    pack_weight_kernel<<<grid, 32, 0, st>>>(dst, ldk, w, k, m, gated);
+    pack_weight_kernel<<<grid, 32, 0, st>>>(dst, ldk, w, k, m, perm, rope_cols);
     return cudaGetLastError();
 }
 cudaError_t launch_gen_vector(float* dst, int n, uint64_t seed, double lo, double hi, cudaStream_t st) {

@@ -115,12 +115,13 @@ def lib():
                                             ctypes.POINTER(ctypes.c_int)]
         L.pi0b_engine_describe.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
         L.pi0b_gemm.argtypes = [ctypes.POINTER(GemmDesc), vp]
+        L.pi0b_gemm_skinny.argtypes = [ctypes.POINTER(GemmDesc), ctypes.c_int, vp]
         L.pi0b_attention.argtypes = [ctypes.POINTER(AttnDesc), vp]
         L.pi0b_attention_ws_floats.argtypes = [ctypes.POINTER(AttnDesc)]
         L.pi0b_attention_ws_floats.restype = ctypes.c_int64
         L.pi0b_random_f64.argtypes = [vp, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double, vp]
         L.pi0b_random_packed_bf16.argtypes = [vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                              ctypes.c_uint64, ctypes.c_double, ctypes.c_double, vp]
+                                              ctypes.c_int, ctypes.c_uint64, ctypes.c_double, ctypes.c_double, vp]
         L.pi0b_seed_hash.argtypes = [ctypes.c_uint64, ctypes.c_char_p, ctypes.c_uint64, ctypes.c_uint64]
         L.pi0b_seed_hash.restype = ctypes.c_uint64
         _lib = L
@@ -131,7 +132,7 @@ EXPORTED_SYMBOLS = [
     "pi0b_default_config", "pi0b_engine_create", "pi0b_engine_destroy", "pi0b_engine_gen_weights",
     "pi0b_engine_set_weight", "pi0b_engine_set_bias_table", "pi0b_engine_run", "pi0b_engine_run_prefix",
     "pi0b_engine_run_action", "pi0b_engine_replay", "pi0b_engine_sync", "pi0b_engine_kernel_count",
-    "pi0b_engine_read_checkpoint", "pi0b_engine_time_node", "pi0b_engine_describe", "pi0b_last_error", "pi0b_gemm", "pi0b_attention",
+    "pi0b_engine_read_checkpoint", "pi0b_engine_time_node", "pi0b_engine_describe", "pi0b_last_error", "pi0b_gemm", "pi0b_gemm_skinny", "pi0b_attention",
     "pi0b_attention_ws_floats", "pi0b_random_f64", "pi0b_random_packed_bf16", "pi0b_seed_hash",
 ]
 
@@ -282,6 +283,10 @@ def gemm(desc: GemmDesc, stream: int | None = None) -> None:
     _raise(lib().pi0b_gemm(ctypes.byref(desc), stream), "pi0b_gemm")
 
 
+def gemm_skinny(desc: GemmDesc, cluster: int = 1, stream: int | None = None) -> None:
+    _raise(lib().pi0b_gemm_skinny(ctypes.byref(desc), cluster, stream), "pi0b_gemm_skinny")
+
+
 def attention(desc: AttnDesc, stream: int | None = None) -> None:
     _raise(lib().pi0b_attention(ctypes.byref(desc), stream), "pi0b_attention")
 
@@ -294,6 +299,10 @@ def random_f64(ptr: int, n: int, seed: int, lo: float, hi: float, stream: int | 
     _raise(lib().pi0b_random_f64(ptr, n, seed, lo, hi, stream), "pi0b_random_f64")
 
 
-def random_packed_bf16(ptr: int, ldk: int, k: int, m: int, gated: bool, seed: int, lo: float, hi: float,
-                       stream: int | None = None) -> None:
-    _raise(lib().pi0b_random_packed_bf16(ptr, ldk, k, m, int(gated), seed, lo, hi, stream), "random_packed_bf16")
+PERM_NONE, PERM_GATE128, PERM_GATE64, PERM_ROPE = 0, 1, 2, 3
+
+
+def random_packed_bf16(ptr: int, ldk: int, k: int, m: int, perm: int, seed: int, lo: float, hi: float,
+                       rope_cols: int = 0, stream: int | None = None) -> None:
+    _raise(lib().pi0b_random_packed_bf16(ptr, ldk, k, m, perm, rope_cols, seed, lo, hi, stream),
+           "random_packed_bf16")

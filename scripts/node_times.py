@@ -26,7 +26,7 @@ y = eng.run(x["patches"], x["state"], x["noise"])
 plan = eng.describe()
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 open(os.path.join(ROOT, "gpurun_out", "plan.txt"), "w").write("\n".join(plan))
-counts = collections.Counter(l.split()[3] for l in plan if l.split()[2] in ("gemm", "attn"))
+counts = collections.Counter(l.split()[3] for l in plan if l.split()[2] in ("gemm", "attn", "skinny"))
 rows = []
 for node, n in counts.items():
     ms, launches = eng.time_node(node, reps=3)

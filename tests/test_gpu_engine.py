@@ -40,7 +40,7 @@ def test_device_weight_stream_bitexact():
     w_ref, _ = O.port_weight("ve.qkv", 3, k, m)
     assert np.array_equal(d64.cpu().numpy().reshape(k, m), w_ref)
     packed = torch.zeros(m, k, dtype=torch.int16, device="cuda")
-    E.random_packed_bf16(packed.data_ptr(), k, k, m, False, seed, -lim, lim)
+    E.random_packed_bf16(packed.data_ptr(), k, k, m, E.PERM_NONE, seed, -lim, lim)
     got = packed.cpu().numpy().view(np.uint16)
     assert np.array_equal(got, bf16_bits_from_f64(w_ref).T)
 

@@ -237,3 +237,135 @@ def test_attention(hd, heads, kv_heads, q_rows, rows0, rows1, splits):
     ref = _attn_ref(q, kk, vv, heads, kv_heads, hd)
     _close(out, ref, 2e-2)
     assert int(ctr.abs().max()) == 0
+
+
+# ------------------------------------------------------------------ skinny (action expert) GEMM
+
+def _pack_rows(perm, m, rope_cols=0):
+    """packed row index of every logical column (csrc/kernels_misc.cu packed_row)."""
+    j = np.arange(m)
+    if perm == E.PERM_GATE64:
+        half = m // 2
+        gate = j >= half
+        c = np.where(gate, j - half, j)
+        return (c // 64) * 128 + np.where(gate, 64, 0) + c % 64
+    if perm == E.PERM_ROPE:
+        h, w = j >> 8, j & 255
+        part, i = w >> 7, w & 127
+        r = (h << 8) + (i >> 6) * 128 + part * 64 + (i & 63)
+        return np.where(j < rope_cols, r, j)
+    return j
+
+
+def _run_skinny(X, Wlog, mode, flags=0, *, perm=E.PERM_NONE, cluster=1, row_stats=None, bias=None, table_row=None,
+                rope_cs=None, rope_pos0=0, rope_cols=0, resid_scale=1.0, out=None, outb=None, out_stats=None,
+                row0_src=None):
+    M, K = X.shape
+    N = Wlog.shape[0]
+    rows = torch.as_tensor(_pack_rows(perm, N, rope_cols), device=dev)
+    Wp = torch.empty_like(Wlog)
+    Wp[rows] = Wlog
+    d = E.GemmDesc()
+    d.a, d.lda = X.data_ptr(), X.stride(0)
+    d.w, d.ldw = Wp.data_ptr(), Wp.stride(0)
+    d.M, d.N, d.K = M, N, K
+    d.mode, d.flags = mode, flags
+    d.row_stats, d.inv_width, d.eps = _ptr(row_stats), 1.0 / K, 1e-6
+    d.bias, d.table_row = _ptr(bias), _ptr(table_row)
+    d.rope_cs, d.rope_pos0, d.rope_cols = _ptr(rope_cs), rope_pos0, rope_cols
+    d.resid_scale = resid_scale
+    d.out, d.ldo = out.data_ptr(), out.stride(0)
+    d.outb, d.ldob = _ptr(outb), (outb.stride(0) if outb is not None else 0)
+    d.out_stats, d.row0_src = _ptr(out_stats), _ptr(row0_src)
+    E.gemm_skinny(d, cluster)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("M,N,K,cluster", [(64, 1024, 2048, 8), (63, 1024, 1024, 4), (1, 1024, 32, 1),
+                                           (64, 384, 640, 2), (64, 32, 1024, 8)])
+def test_skinny_plain(M, N, K, cluster):
+    X, W = _rand((M, K), seed=31), _rand((N, K), 1 / math.sqrt(K), seed=32)
+    stats = torch.rand(M, device=dev) * K + 1.0
+    bias = _rand((N,), 0.1, torch.float32, seed=33)
+    out = torch.zeros(M, N, dtype=torch.bfloat16, device=dev)
+    _run_skinny(X, W, E.MODE_BF16, E.FLAG_ROWSCALE | E.FLAG_BIAS, cluster=cluster, row_stats=stats, bias=bias, out=out)
+    ref = (X.float() @ W.float().T) / torch.sqrt(stats / K + 1e-6)[:, None] + bias
+    _close(out, ref, 1e-2)
+
+
+@pytest.mark.parametrize("cluster", [1, 4, 8])
+def test_skinny_rope(cluster):
+    M, K, q, kv = 64, 1024, 2048, 256
+    N = q + 2 * kv
+    X, W = _rand((M, K), seed=34), _rand((N, K), 1 / math.sqrt(K), seed=35)
+    stats = torch.rand(M, device=dev) * K + 1.0
+    pos0 = 512
+    cs = _rope_table(pos0 + M)
+    out = torch.zeros(M, N, dtype=torch.bfloat16, device=dev)
+    _run_skinny(X, W, E.MODE_BF16, E.FLAG_ROWSCALE | E.FLAG_ROPE, perm=E.PERM_ROPE, cluster=cluster, row_stats=stats,
+                rope_cs=cs, rope_pos0=pos0, rope_cols=q + kv, out=out)
+    z = (X.float() @ W.float().T) / torch.sqrt(stats / K + 1e-6)[:, None]
+    c, s = cs[pos0:pos0 + M, :, 0], cs[pos0:pos0 + M, :, 1]
+    ref = z.clone()
+    for h0 in range(0, q + kv, 256):
+        a, b = z[:, h0:h0 + 128], z[:, h0 + 128:h0 + 256]
+        ref[:, h0:h0 + 128] = a * c - b * s
+        ref[:, h0 + 128:h0 + 256] = a * s + b * c
+    _close(out, ref, 1e-2)
+
+
+@pytest.mark.parametrize("mlp,cluster", [(4096, 2), (512, 1), (512, 8)])
+def test_skinny_gate(mlp, cluster):
+    M, K = 64, 1024
+    X, W = _rand((M, K), seed=36), _rand((2 * mlp, K), 1 / math.sqrt(K), seed=37)
+    stats = torch.rand(M, device=dev) * K + 1.0
+    out = torch.zeros(M, mlp, dtype=torch.bfloat16, device=dev)
+    _run_skinny(X, W, E.MODE_GATE, E.FLAG_ROWSCALE, perm=E.PERM_GATE64, cluster=cluster, row_stats=stats, out=out)
+    z = (X.float() @ W.float().T) / torch.sqrt(stats / K + 1e-6)[:, None]
+    ref = z[:, :mlp] * torch.nn.functional.gelu(z[:, mlp:], approximate="tanh")
+    _close(out, ref, 1e-2)
+
+
+@pytest.mark.parametrize("M,N,K,cluster,scale,flags", [(64, 1024, 4096, 8, 1.0, 0), (64, 1024, 2048, 1, 1.0, 0),
+                                                       (63, 32, 1024, 8, 0.1, 3)])
+def test_skinny_residual(M, N, K, cluster, scale, flags):
+    X, W = _rand((M, K), seed=38), _rand((N, K), 1 / math.sqrt(K), seed=39)
+    h0 = _rand((M, N), 1.0, torch.float32, seed=40)
+    h = h0.clone()
+    hb = torch.zeros(M, N, dtype=torch.bfloat16, device=dev)
+    st = torch.zeros(M, device=dev)
+    stats = torch.rand(M, device=dev) * K + 1.0
+    bias = _rand((N,), 0.1, torch.float32, seed=41)
+    _run_skinny(X, W, E.MODE_RESID, flags, cluster=cluster, row_stats=stats, bias=bias, resid_scale=scale, out=h,
+                outb=hb, out_stats=st)
+    z = X.float() @ W.float().T
+    if flags & E.FLAG_ROWSCALE:
+        z = z / torch.sqrt(stats / K + 1e-6)[:, None]
+    if flags & E.FLAG_BIAS:
+        z = z + bias
+    ref = h0 + scale * z
+    _close(h, ref, 2e-5 * max(1.0, K / 1024))
+    _close(hb, ref, 1e-2)
+    _close(st, (ref * ref).sum(1), 1e-4)
+
+
+@pytest.mark.parametrize("cluster", [1, 8])
+def test_skinny_f32_store_row0_and_silu(cluster):
+    M, N, K = 63, 1024, 1024
+    X, W = _rand((M, K), seed=42), _rand((N, K), 1 / math.sqrt(K), seed=43)
+    bias = _rand((N,), 0.1, torch.float32, seed=44)
+    row0 = _rand((N,), 1.0, torch.float32, seed=45)
+    y = torch.zeros(M + 1, N, device=dev)
+    yb = torch.zeros(M + 1, N, dtype=torch.bfloat16, device=dev)
+    st = torch.zeros(M + 1, device=dev)
+    _run_skinny(X, W, E.MODE_F32_STORE, E.FLAG_BIAS, cluster=cluster, bias=bias, out=y[1:], outb=yb[1:],
+                out_stats=st[1:], row0_src=row0)
+    ref = torch.cat([row0[None], X.float() @ W.float().T + bias], 0)
+    _close(y, ref, 2e-5)
+    _close(yb, ref, 1e-2)
+    _close(st, (ref * ref).sum(1), 1e-4)
+    Xs, Ws = _rand((M, 32), seed=46), _rand((N, 32), 1 / math.sqrt(32), seed=47)
+    tab = _rand((N,), 0.2, torch.float32, seed=48)
+    out = torch.zeros(M, N, dtype=torch.bfloat16, device=dev)
+    _run_skinny(Xs, Ws, E.MODE_SILU_TABLE, 0, cluster=1, table_row=tab, out=out)
+    _close(out, torch.nn.functional.silu(Xs.float() @ Ws.float().T + tab), 1e-2)
