@@ -1,4 +1,4 @@
-// Parameter block of the flash-style attention kernel (attention.cu).
+// Parameter block of the tcgen05 flash-attention kernel (fattn.cu).
 //
 // Semantics follow the reference `Evaluator::attention` (proj/src/evaluate.cpp:225-252):
 // per head h, P = softmax(Q_h K_{h % kv_heads}^T / sqrt(d)) with no mask, O_h = P V.

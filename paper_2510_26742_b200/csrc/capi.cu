@@ -16,12 +16,14 @@
 
 namespace pi0b {
 cudaError_t gemm_configure();
-cudaError_t attn_configure();
 cudaError_t launch_gemm(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                         cudaStream_t stream);
-cudaError_t launch_attention(int head_dim, const AttnParams& p, cudaStream_t stream);
-int attn_key_tile(int head_dim);
-int attn_query_tile();
+struct FaMaps {
+    CUtensorMap k0, v0, k1, v1;
+};
+cudaError_t fattn_configure();
+FaMaps make_fattn_maps(const AttnParams& p, int head_dim);
+cudaError_t launch_fattn(int head_dim, const FaMaps& maps, const AttnParams& p, cudaStream_t stream);
 CUtensorMap make_tmap_bf16(const void* base, long long rows, long long cols, long long ld, int box_rows);
 cudaError_t launch_gen_weight(__nv_bfloat16* dst, long long ldk, int k, int m, int perm, int rope_cols,
                               uint64_t seed, double lo, double hi, cudaStream_t st);
@@ -41,26 +43,12 @@ static int configure_once() {
     static bool done[64] = {false};
     if (dev < 64 && !done[dev]) {
         cudaError_t e = gemm_configure();
-        if (e == cudaSuccess) e = attn_configure();
+        if (e == cudaSuccess) e = fattn_configure();
         if (e == cudaSuccess) e = skinny_configure();
         if (e != cudaSuccess) return int(e);
         done[dev] = true;
     }
     return 0;
-}
-
-static void attn_plan(const pi0b_attn_desc* d, int* splits, int* per, int* q_tiles) {
-    const int grows = (d->heads / d->kv_heads) * d->q_rows;
-    *q_tiles = (grows + attn_query_tile() - 1) / attn_query_tile();
-    const int total = d->rows0 + d->rows1;
-    const int kvt = attn_key_tile(d->head_dim);
-    int s = d->kv_splits;
-    if (s <= 0) s = std::max(1, std::min(std::min(64 / std::max(1, *q_tiles * d->kv_heads), (total + 2 * kvt - 1) / (2 * kvt)), 8));
-    s = std::min(s, 8);
-    int pp = (total + s - 1) / s;
-    pp = (pp + kvt - 1) / kvt * kvt;
-    *splits = (total + pp - 1) / pp;
-    *per = pp;
 }
 
 }  // namespace pi0b
@@ -152,9 +140,8 @@ int pi0b_gemm(const pi0b_gemm_desc* d, void* stream) {
 }
 
 int64_t pi0b_attention_ws_floats(const pi0b_attn_desc* d) {
-    int splits, per, q_tiles;
-    pi0b::attn_plan(d, &splits, &per, &q_tiles);
-    return int64_t(splits) * d->kv_heads * q_tiles * 64 * (d->head_dim + 2);
+    (void)d;
+    return 0;  // single-pass tcgen05 attention needs no workspace
 }
 
 int pi0b_attention(const pi0b_attn_desc* d, void* stream) {
@@ -178,16 +165,14 @@ int pi0b_attention(const pi0b_attn_desc* d, void* stream) {
     p.out = static_cast<__nv_bfloat16*>(d->out);
     p.ldo = d->ldo;
     p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(d->head_dim)));
-    int splits, per, q_tiles;
-    attn_plan(d, &splits, &per, &q_tiles);
-    p.kv_splits = splits;
-    p.kv_per_split = per;
-    const long long rows_pad = (long long)q_tiles * 64;
-    p.ws_o = d->ws;
-    p.ws_ml = d->ws ? d->ws + (long long)splits * d->kv_heads * rows_pad * d->head_dim : nullptr;
-    p.counters = d->counters;
-    if (splits > 1 && (!d->ws || !d->counters)) return PI0B_E_INVALID;
-    return int(launch_attention(d->head_dim, p, static_cast<cudaStream_t>(stream)));
+    p.kv_splits = 1;
+    p.kv_per_split = d->rows0 + d->rows1;
+    try {
+        const FaMaps m = make_fattn_maps(p, d->head_dim);
+        return int(launch_fattn(d->head_dim, m, p, static_cast<cudaStream_t>(stream)));
+    } catch (const std::exception&) {
+        return PI0B_E_INVALID;
+    }
 }
 
 int pi0b_random_f64(double* dst, int64_t n, uint64_t seed, double lo, double hi, void* stream) {

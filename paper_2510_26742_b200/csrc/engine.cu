@@ -36,12 +36,14 @@
 namespace pi0b {
 
 cudaError_t gemm_configure();
-cudaError_t attn_configure();
 cudaError_t launch_gemm(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                         cudaStream_t stream);
-cudaError_t launch_attention(int head_dim, const AttnParams& p, cudaStream_t stream);
-int attn_key_tile(int head_dim);
-int attn_query_tile();
+struct FaMaps {
+    CUtensorMap k0, v0, k1, v1;
+};
+cudaError_t fattn_configure();
+FaMaps make_fattn_maps(const AttnParams& p, int head_dim);
+cudaError_t launch_fattn(int head_dim, const FaMaps& maps, const AttnParams& p, cudaStream_t stream);
 cudaError_t launch_gen_weight(__nv_bfloat16* dst, long long ldk, int k, int m, int perm, int rope_cols,
                               uint64_t seed, double lo, double hi, cudaStream_t st);
 cudaError_t launch_pack_weight(__nv_bfloat16* dst, long long ldk, const double* w, int k, int m,
@@ -172,6 +174,7 @@ struct Op {
     // attention
     int hd = 0;
     AttnParams ap{};
+    FaMaps fm;
     // conversions
     const double* src64 = nullptr;
     int rows = 0, cols = 0;
@@ -285,9 +288,6 @@ private:
     float* gemm_ws_ = nullptr;
     int* gemm_ctr_ = nullptr;
     size_t gemm_ws_floats_ = 0;
-    float* attn_ws_ = nullptr;
-    int* attn_ctr_ = nullptr;
-    size_t attn_ws_floats_ = 0;
     float* stats_[2] = {nullptr, nullptr};
     int stats_rows_ = 0, stats_used_[2] = {0, 0}, stats_cap_[2] = {0, 0};
 
@@ -310,7 +310,7 @@ Engine::Engine(const pi0b_model_config& cfg, const pi0b_engine_options& opt) : c
     num_sms_ = prop.multiProcessorCount;
     pdl_ = env_int("PI0B_PDL", 1) != 0;
     PI0B_CUDA(gemm_configure());
-    PI0B_CUDA(attn_configure());
+    PI0B_CUDA(fattn_configure());
     PI0B_CUDA(skinny_configure());
     PI0B_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     alloc_weights();
@@ -551,22 +551,12 @@ void Engine::add_attn(int part, const std::string& node, int inst, int hd, AttnP
     op.kind = kOpAttn;
     op.part = part;
     op.hd = hd;
-    const int grows = (ap.heads / ap.kv_heads) * ap.q_rows;
-    const int q_tiles = (grows + attn_query_tile() - 1) / attn_query_tile();
-    const int total = ap.rows0 + ap.rows1;
-    const int kvt = attn_key_tile(hd);
-    const int ctas = q_tiles * ap.kv_heads;
-    // Split the keys only when the query tiles cannot fill ~64 CTAs (the action expert's
-    // 8 stacked tiles); each split keeps >= 2 key tiles and the merge reads <= 16 partials.
-    int splits = std::max(1, std::min(std::min(env_int("PI0B_ATTN_CTAS", 32) / std::max(1, ctas),
-                                               (total + 2 * kvt - 1) / (2 * kvt)), 8));
-    int per = round_up((total + splits - 1) / splits, kvt);
-    splits = (total + per - 1) / per;
-    ap.kv_splits = splits;
-    ap.kv_per_split = per;
+    ap.kv_splits = 1;
+    ap.kv_per_split = ap.rows0 + ap.rows1;
     ap.scale_log2 = float(1.4426950408889634 / std::sqrt(double(hd)));
-    if (splits > 1)
-        attn_ws_floats_ = std::max(attn_ws_floats_, size_t(splits) * ap.kv_heads * q_tiles * 64 * (hd + 2));
+    if ((ap.rows0 % 32) || (ap.rows1 % 32))
+        throw EngineError(PI0B_E_UNSUPPORTED, "attention key segments must be multiples of 32 rows");
+    op.fm = make_fattn_maps(ap, hd);
     op.ap = ap;
     ops_.push_back(op);
     (void)node;
@@ -1001,19 +991,10 @@ void Engine::build_plan() {
     PI0B_CUDA(cudaMemsetAsync(gemm_ws_, 0, std::max<size_t>(gemm_ws_floats_, 1) * 4, stream_));
     gemm_ctr_ = alloc<int>(4096);
     PI0B_CUDA(cudaMemsetAsync(gemm_ctr_, 0, 4096 * 4, stream_));
-    attn_ws_ = alloc<float>(std::max<size_t>(attn_ws_floats_, 1));
-    attn_ctr_ = alloc<int>(4096);
-    PI0B_CUDA(cudaMemsetAsync(attn_ctr_, 0, 4096 * 4, stream_));
     for (auto& op : ops_) {
         if (op.kind == kOpGemm) {
             op.gp.ws = gemm_ws_;
             op.gp.counters = gemm_ctr_;
-        } else if (op.kind == kOpAttn) {
-            const int grows = (op.ap.heads / op.ap.kv_heads) * op.ap.q_rows;
-            const long long rows_pad = (long long)((grows + 63) / 64) * 64;
-            op.ap.ws_o = attn_ws_;
-            op.ap.ws_ml = attn_ws_ + size_t(op.ap.kv_splits) * op.ap.kv_heads * rows_pad * op.hd;
-            op.ap.counters = attn_ctr_;
         }
     }
 }
@@ -1113,7 +1094,7 @@ void Engine::run_ops(int part, cudaStream_t st) {
             case kOpSkinny:
                 PI0B_CUDA(launch_skinny(op.ta, op.tb, op.gp, op.n_packed, op.cluster, pdl_, st));
                 break;
-            case kOpAttn: PI0B_CUDA(launch_attention(op.hd, op.ap, st)); break;
+            case kOpAttn: PI0B_CUDA(launch_fattn(op.hd, op.fm, op.ap, st)); break;
             case kOpRowsF32:
                 PI0B_CUDA(launch_rows_to_f32(op.src64, op.rows, op.cols, op.dst32, op.ld32, op.dstb, op.ldb,
                                              op.stats, st));
@@ -1222,7 +1203,7 @@ double Engine::time_node(const std::string& node, int reps, int* launches) {
     auto fire = [&](const Op& op) {
         if (op.kind == kOpGemm) PI0B_CUDA(launch_gemm(op.bn, op.ta, op.tb, op.gp, stream_));
         else if (op.kind == kOpSkinny) PI0B_CUDA(launch_skinny(op.ta, op.tb, op.gp, op.n_packed, op.cluster, pdl_, stream_));
-        else PI0B_CUDA(launch_attention(op.hd, op.ap, stream_));
+        else PI0B_CUDA(launch_fattn(op.hd, op.fm, op.ap, stream_));
     };
     for (const Op* op : sel) fire(*op);
     cudaEvent_t a, b;
