@@ -171,6 +171,14 @@ PI0B_DEV float ld_dsmem_f32(uint32_t addr) {
     asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
     return v;
 }
+PI0B_DEV float4 ld_dsmem_f32x4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
 // Programmatic dependent launch: wait for the producer grid / allow the consumer grid to start.
 PI0B_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 PI0B_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }

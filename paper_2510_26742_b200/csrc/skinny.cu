@@ -169,76 +169,92 @@ __global__ void __launch_bounds__(kSkThreads, 1)
     cluster_sync_all();
 
     if (warp >= 2) {
-        // ---- epilogue part 2: this CTA owns feature pairs [crank*P, (crank+1)*P)
+        // ---- epilogue part 2: this CTA owns feature pairs [crank*P, (crank+1)*P); one item =
+        // (pair, 4 rows): all peer partials are fetched with 16-byte DSMEM loads before use.
         const int et = threadIdx.x - 64;
         const int P = 64 / CL;
         const int i0 = crank * P;
         const bool rope = perm == 2 && tile * kSkBN < p.rope_cols && MODE == kModeBf16;
         const uint32_t xbase = smem_u32(xch);
-        for (int idx = et; idx < P * kSkRows; idx += 128) {
+        for (int idx = et; idx < P * (kSkRows / 4); idx += 128) {
             const int i = i0 + idx % P;
-            const int r = idx / P;
-            if (r >= p.M) continue;
-            float a = 0.f, b = 0.f;
-            for (int s = 0; s < CL; ++s) {
-                const uint32_t base = mapa_shared(xbase, uint32_t(s));
-                a += ld_dsmem_f32(base + uint32_t((i * kSkXLd + r) * 4));
-                b += ld_dsmem_f32(base + uint32_t(((i + 64) * kSkXLd + r) * 4));
-            }
-            const float rs = sm_rs[r];
-            if constexpr (MODE == kModeGate) {
-                const int col = tile * 64 + i;
-                if (col < p.N / 2) {
-                    const float g = (a * rs) * gelu_tanh(b * rs);
-                    reinterpret_cast<__nv_bfloat16*>(p.out)[(long long)r * p.ldo + col] = __float2bfloat16_rn(g);
-                }
-            } else if constexpr (MODE == kModeBf16) {
-                __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)r * p.ldo;
-                float xa = a * rs + sm_vec[i], xb = b * rs + sm_vec[i + 64];
-                if (rope) {
-                    const int ca = rope_col(tile, i);
-                    const float2 t = reinterpret_cast<const float2*>(p.rope_cs)[(long long)(p.rope_pos0 + r) * 128 + (ca & 255)];
-                    const float ra = xa * t.x - xb * t.y;
-                    const float rb = xa * t.y + xb * t.x;
-                    o[ca] = __float2bfloat16_rn(ra);
-                    o[ca + 128] = __float2bfloat16_rn(rb);
-                } else {
-                    if (p.flags & kFlagGelu) {
-                        xa = gelu_tanh(xa);
-                        xb = gelu_tanh(xb);
-                    }
-                    const int fa = tile * kSkBN + i;
-                    if (fa < p.N) o[fa] = __float2bfloat16_rn(xa);
-                    if (fa + 64 < p.N) o[fa + 64] = __float2bfloat16_rn(xb);
-                }
-            } else if constexpr (MODE == kModeSiluTable) {
-                __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)r * p.ldo;
-                const int fa = tile * kSkBN + i;
-                if (fa < p.N) o[fa] = __float2bfloat16_rn(silu_f(a + sm_vec[i]));
-                if (fa + 64 < p.N) o[fa + 64] = __float2bfloat16_rn(silu_f(b + sm_vec[i + 64]));
-            } else {
-                // kModeResid / kModeF32Store: fp32 stream + bf16 shadow + row sum of squares
-                const int fa = tile * kSkBN + i;
-                float* h = reinterpret_cast<float*>(p.out) + (long long)r * p.ldo;
-                __nv_bfloat16* hb = reinterpret_cast<__nv_bfloat16*>(p.outb) + (long long)r * p.ldob;
-                float ss = 0.f;
+            const int r0 = (idx / P) * 4;
+            if (r0 >= p.M) continue;
+            float4 pa[8], pb[8];
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    const int f = fa + half * 64;
-                    if (f >= p.N) continue;
-                    const float z = (half ? b : a) * rs + sm_vec[i + half * 64];
-                    const float x = MODE == kModeResid ? h[f] + p.resid_scale * z : z;
-                    h[f] = x;
-                    if (p.outb) hb[f] = __float2bfloat16_rn(x);
-                    ss += x * x;
-                    if (MODE == kModeF32Store && p.row0_src && r == 0) {
-                        const float x0 = p.row0_src[f];
-                        h[f - p.ldo] = x0;
-                        if (p.outb) hb[f - p.ldob] = __float2bfloat16_rn(x0);
-                        atomicAdd(&sm_ss[64], x0 * x0);
-                    }
+            for (int s = 0; s < 8; ++s) {
+                if (s < CL) {
+                    const uint32_t base = mapa_shared(xbase, uint32_t(s));
+                    pa[s] = ld_dsmem_f32x4(base + uint32_t((i * kSkXLd + r0) * 4));
+                    pb[s] = ld_dsmem_f32x4(base + uint32_t(((i + 64) * kSkXLd + r0) * 4));
                 }
-                if (p.out_stats) atomicAdd(&sm_ss[r], ss);
+            }
+            float a4[4] = {0.f, 0.f, 0.f, 0.f}, b4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+                if (s < CL) {
+                    a4[0] += pa[s].x; a4[1] += pa[s].y; a4[2] += pa[s].z; a4[3] += pa[s].w;
+                    b4[0] += pb[s].x; b4[1] += pb[s].y; b4[2] += pb[s].z; b4[3] += pb[s].w;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int r = r0 + u;
+                if (r >= p.M) break;
+                const float a = a4[u], b = b4[u];
+                const float rs = sm_rs[r];
+                if constexpr (MODE == kModeGate) {
+                    const int col = tile * 64 + i;
+                    if (col < p.N / 2) {
+                        const float g = (a * rs) * gelu_tanh(b * rs);
+                        reinterpret_cast<__nv_bfloat16*>(p.out)[(long long)r * p.ldo + col] = __float2bfloat16_rn(g);
+                    }
+                } else if constexpr (MODE == kModeBf16) {
+                    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)r * p.ldo;
+                    float xa = a * rs + sm_vec[i], xb = b * rs + sm_vec[i + 64];
+                    if (rope) {
+                        const int ca = rope_col(tile, i);
+                        const float2 t = reinterpret_cast<const float2*>(p.rope_cs)[(long long)(p.rope_pos0 + r) * 128 + (ca & 255)];
+                        o[ca] = __float2bfloat16_rn(xa * t.x - xb * t.y);
+                        o[ca + 128] = __float2bfloat16_rn(xa * t.y + xb * t.x);
+                    } else {
+                        if (p.flags & kFlagGelu) {
+                            xa = gelu_tanh(xa);
+                            xb = gelu_tanh(xb);
+                        }
+                        const int fa = tile * kSkBN + i;
+                        if (fa < p.N) o[fa] = __float2bfloat16_rn(xa);
+                        if (fa + 64 < p.N) o[fa + 64] = __float2bfloat16_rn(xb);
+                    }
+                } else if constexpr (MODE == kModeSiluTable) {
+                    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)r * p.ldo;
+                    const int fa = tile * kSkBN + i;
+                    if (fa < p.N) o[fa] = __float2bfloat16_rn(silu_f(a + sm_vec[i]));
+                    if (fa + 64 < p.N) o[fa + 64] = __float2bfloat16_rn(silu_f(b + sm_vec[i + 64]));
+                } else {
+                    // kModeResid / kModeF32Store: fp32 stream + bf16 shadow + row sum of squares
+                    const int fa = tile * kSkBN + i;
+                    float* h = reinterpret_cast<float*>(p.out) + (long long)r * p.ldo;
+                    __nv_bfloat16* hb = reinterpret_cast<__nv_bfloat16*>(p.outb) + (long long)r * p.ldob;
+                    float ss = 0.f;
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {
+                        const int f = fa + half * 64;
+                        if (f >= p.N) continue;
+                        const float z = (half ? b : a) * rs + sm_vec[i + half * 64];
+                        const float x = MODE == kModeResid ? h[f] + p.resid_scale * z : z;
+                        h[f] = x;
+                        if (p.outb) hb[f] = __float2bfloat16_rn(x);
+                        ss += x * x;
+                        if (MODE == kModeF32Store && p.row0_src && r == 0) {
+                            const float x0 = p.row0_src[f];
+                            h[f - p.ldo] = x0;
+                            if (p.outb) hb[f - p.ldob] = __float2bfloat16_rn(x0);
+                            atomicAdd(&sm_ss[64], x0 * x0);
+                        }
+                    }
+                    if (p.out_stats) atomicAdd(&sm_ss[r], ss);
+                }
             }
         }
         if constexpr (MODE == kModeResid || MODE == kModeF32Store) {
