@@ -15,6 +15,7 @@
 // RmsStats nodes have no launch: their row sums of squares are accumulated by the
 // epilogue of the kernel that produced the residual stream.
 #include "../../include/pi0b.h"
+#include "aemk.cuh"
 #include "attention.cuh"
 #include "gemm.cuh"
 #include "numerics.cuh"
@@ -141,6 +142,26 @@ CUtensorMap make_tmap_bf16(const void* base, long long rows, long long cols, lon
     return m;
 }
 
+// [rows, cols] with row pitch `ld` elements, boxes of (128 B of columns) x box_rows, 128-B
+// swizzle: 64 bf16 or 32 fp32 columns per box.
+CUtensorMap make_tmap_2d(const void* base, bool f32, long long rows, long long cols, long long ld, int box_rows) {
+    const int esz = f32 ? 4 : 2;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * esz) % 16)
+        throw EngineError(PI0B_E_INVALID, "TMA operand needs 16-byte aligned base and pitch");
+    CUtensorMap m;
+    cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(ld * esz)};
+    cuuint32_t box[2] = {cuuint32_t(128 / esz), cuuint32_t(box_rows)};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                             const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw EngineError(PI0B_E_INVALID, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return m;
+}
+
 static int round_up(int x, int a) { return (x + a - 1) / a * a; }
 
 // Split-K factor so that the grid approaches one wave of 148 SMs.
@@ -161,7 +182,16 @@ static int choose_splits(int m_tiles, int n_tiles, int K, int num_sms) {
 
 // ------------------------------------------------------------------ plan records
 
-enum OpKind { kOpGemm, kOpAttn, kOpRowsF32, kOpF64Bf16, kOpF32F64, kOpMemset, kOpSkinny };
+enum OpKind { kOpGemm, kOpAttn, kOpRowsF32, kOpF64Bf16, kOpF32F64, kOpMemset, kOpSkinny, kOpAeMega };
+
+// A checkpoint the megakernel leaves in a record buffer (record mode).
+struct CkTag {
+    std::string node;
+    int inst;
+    const void* ptr;
+    int rows, cols;
+    long long ld;
+};
 
 struct Op {
     OpKind kind;
@@ -194,6 +224,7 @@ struct Op {
     int ck_rows = 0, ck_cols = 0;
     long long ck_ld = 0;
     int ck_bf16 = 0;
+    std::vector<CkTag> extra_ck;
     bool is_kernel() const { return kind != kOpMemset; }
 };
 
@@ -229,6 +260,7 @@ public:
     int kernel_count(int part) const;
     double time_node(const std::string& node, int reps, int* launches);
     std::string describe() const;
+    void ae_trace(void* tasks, unsigned long long* stamps, long long cap, int* ctas, int* stride);
     cudaStream_t stream() const { return stream_; }
     bool weights_ready() const { return weights_loaded_; }
 
@@ -293,6 +325,15 @@ private:
 
     std::vector<Op> ops_;
     cudaGraphExec_t graph_[3] = {nullptr, nullptr, nullptr};
+
+    // action-expert megakernel (aemk.cu)
+    bool ae_mega_ = true;
+    AePlan ae_plan_;
+    AeParams ae_p_{};
+    float* state32_ = nullptr;
+    void* ae_zero_ = nullptr;
+    size_t ae_zero_bytes_ = 0;
+    void build_ae_mega();
     std::map<std::pair<std::string, int>, Checkpoint> ck_;
     bool pdl_ = true;
 };
@@ -312,6 +353,8 @@ Engine::Engine(const pi0b_model_config& cfg, const pi0b_engine_options& opt) : c
     PI0B_CUDA(gemm_configure());
     PI0B_CUDA(fattn_configure());
     PI0B_CUDA(skinny_configure());
+    PI0B_CUDA(aemk_configure());
+    ae_mega_ = env_int("PI0B_AE_MEGA", 1) != 0;
     PI0B_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     alloc_weights();
     alloc_activations();
@@ -807,6 +850,9 @@ void Engine::build_plan() {
     }
 
     // ================================================================ action expert (part 1)
+    if (ae_mega_) {
+        build_ae_mega();
+    } else {
     // (proj/src/builder.cpp:291-363)
     {
         Op m;
@@ -974,6 +1020,7 @@ void Engine::build_plan() {
             tag("ae.head", s, a_, C_, c.ae_action_dim, act_ld_, 0);
         }
     }
+    }
     {
         Op o;
         o.kind = kOpF32F64;
@@ -997,6 +1044,196 @@ void Engine::build_plan() {
             op.gp.counters = gemm_ctr_;
         }
     }
+}
+
+// ------------------------------------------------------------------ action-expert megakernel
+
+// The whole action expert (proj/src/builder.cpp:291-363) as one persistent launch: a zeroing
+// memset (phase counters + attention accumulators), the two input conversions, the kernel.
+void Engine::build_ae_mega() {
+    const auto& c = c_;
+    const int W = ae_w_, NQ = ae_q_ + 2 * ae_kv_, MLP = c.ae_mlp, NA = c.ae_layers;
+    if (c.ae_kv_heads != 1 || c.llm_kv_heads != 1)
+        throw EngineError(PI0B_E_UNSUPPORTED, "action-expert megakernel: MQA (1 kv head) only");
+    state32_ = alloc<float>(size_t(std::max(c.ae_state_dim, 8)));
+    std::vector<CUtensorMap> maps;
+    auto add = [&](const CUtensorMap& m) {
+        maps.push_back(m);
+        return int(maps.size()) - 1;
+    };
+    auto wmap = [&](const char* node, int inst, int rows) {
+        const NodeWeights& nw = W_.at(node);
+        return add(make_tmap_2d(nw.w.at(size_t(inst)), false, rows, nw.k, nw.ldk, 128));
+    };
+    AePlanInput in;
+    in.num_ctas = num_sms_;
+    in.width = W;
+    in.n_qkv = NQ;
+    in.q_width = ae_q_;
+    in.mlp = MLP;
+    in.layers = NA;
+    in.flow_steps = FS_;
+    in.heads = c.ae_q_heads;
+    in.chunk = C_;
+    in.act_dim = c.ae_action_dim;
+    in.state_dim = c.ae_state_dim;
+    in.rope_cols = ae_q_ + ae_kv_;
+    in.kv_rows0 = L_;
+    in.key_blocks = (L_ + S_ + 63) / 64;
+    in.record = o_.record_checkpoints != 0;
+    in.map_wst = wmap("ae.state_proj", 0, W);
+    in.map_wap = wmap("ae.action_proj", 0, W);
+    in.map_wao = wmap("ae.action_out", 0, W);
+    in.map_whead = wmap("ae.head", 0, c.ae_action_dim);
+    for (int l = 0; l < NA; ++l) {
+        in.map_wqkv.push_back(wmap("ae.qkv", l, NQ));
+        in.map_wproj.push_back(wmap("ae.proj", l, W));
+        in.map_wffn.push_back(wmap("ae.ffn", l, 2 * MLP));
+        in.map_wdown.push_back(wmap("ae.down", l, W));
+    }
+    const int llm_qkv_n = llm_q_ + 2 * llm_kv_;
+    for (int l = 0; l < c.llm_layers; ++l)  // AE instance i reads LLM layer i % llm_layers (@mod)
+        in.map_kv.push_back(add(make_tmap_2d(kv_[size_t(l)], false, L_, llm_qkv_n, llm_qkv_n, 32)));
+    in.map_y = add(make_tmap_2d(y_, true, S_, W, W, 64));
+    in.map_yh = add(make_tmap_2d(y_ + W, true, C_, W, W, 64));
+    in.map_ap = add(make_tmap_2d(ap_b_, false, C_, W, W, 64));
+    in.map_g = add(make_tmap_2d(ag_, false, S_, MLP, MLP, 64));
+    in.map_q = add(make_tmap_2d(aqkv_, false, S_, NQ, NQ, 64));
+    in.map_kvown = add(make_tmap_2d(aqkv_, false, S_, NQ, NQ, 32));
+
+    // zero-on-entry region: counters | O_acc[2] | l[2] | m[2]
+    const size_t n_o = size_t(64) * ae_q_, n_h = size_t(c.ae_q_heads) * 64;
+    float* oacc[2];
+    try {
+        ae_plan_ = ae_plan([&] {
+            AePlanInput t = in;
+            t.map_oacc = {0, 0};
+            return t;
+        }());
+    } catch (const std::invalid_argument& e) {
+        throw EngineError(PI0B_E_UNSUPPORTED, e.what());
+    }
+    const size_t bar_bytes = size_t(round_up(ae_plan_.n_bars * 4, 256)) +
+                             size_t(round_up(num_sms_ * ae_plan_.n_bars * 4, 256));
+    ae_zero_bytes_ = bar_bytes + 2 * n_o * 4 + 4 * round_up(int(n_h * 4), 256);
+    uint8_t* z = alloc<uint8_t>(ae_zero_bytes_);
+    ae_zero_ = z;
+    unsigned* bars = reinterpret_cast<unsigned*>(z);
+    oacc[0] = reinterpret_cast<float*>(z + bar_bytes);
+    oacc[1] = oacc[0] + n_o;
+    uint8_t* zz = reinterpret_cast<uint8_t*>(oacc[1] + n_o);
+    const size_t hb = size_t(round_up(int(n_h * 4), 256));
+    float* lacc[2] = {reinterpret_cast<float*>(zz), reinterpret_cast<float*>(zz + hb)};
+    unsigned* mmax[2] = {reinterpret_cast<unsigned*>(zz + 2 * hb), reinterpret_cast<unsigned*>(zz + 3 * hb)};
+    in.map_oacc = {add(make_tmap_2d(oacc[0], true, 64, ae_q_, ae_q_, 64)),
+                   add(make_tmap_2d(oacc[1], true, 64, ae_q_, ae_q_, 64))};
+    try {
+        ae_plan_ = ae_plan(in);
+    } catch (const std::invalid_argument& e) {
+        throw EngineError(PI0B_E_UNSUPPORTED, e.what());
+    }
+
+    CUtensorMap* dmaps = alloc<CUtensorMap>(maps.size());
+    PI0B_CUDA(cudaMemcpyAsync(dmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice, stream_));
+    AeTask* dtasks = alloc<AeTask>(ae_plan_.table.size());
+    PI0B_CUDA(cudaMemcpyAsync(dtasks, ae_plan_.table.data(), ae_plan_.table.size() * sizeof(AeTask),
+                              cudaMemcpyHostToDevice, stream_));
+    float* rec_y = nullptr;
+    float* rec_a = nullptr;
+    if (in.record) {
+        rec_y = alloc<float>(size_t(FS_) * NA * 64 * W);
+        rec_a = alloc<float>(size_t(FS_) * C_ * act_ld_);
+    }
+    PI0B_CUDA(cudaStreamSynchronize(stream_));
+
+    AeParams& P = ae_p_;
+    P.tasks = dtasks;
+    P.task_stride = ae_plan_.stride;
+    P.maps = dmaps;
+    P.bars = bars;
+    P.mbox = bars + round_up(ae_plan_.n_bars * 4, 256) / 4;
+    P.n_bars = ae_plan_.n_bars;
+    P.y = y_;
+    P.a = a_;
+    P.lda = act_ld_;
+    P.state = state32_;
+    P.st = st_;
+    P.qkv = aqkv_;
+    P.ap = ap_b_;
+    P.g = ag_;
+    for (int i = 0; i < 2; ++i) {
+        P.oacc[i] = oacc[i];
+        P.lacc[i] = lacc[i];
+        P.mmax[i] = mmax[i];
+    }
+    P.rope_cs = rope_cs_;
+    P.table = W_.at("ae.action_proj").table;
+    P.b_state = W_.at("ae.state_proj").b.at(0);
+    P.b_out = W_.at("ae.action_out").b.at(0);
+    P.b_head = W_.at("ae.head").b.at(0);
+    P.rec_y = rec_y;
+    P.rec_a = rec_a;
+    P.width = W;
+    P.n_qkv = NQ;
+    P.q_width = ae_q_;
+    P.mlp = MLP;
+    P.act_dim = c.ae_action_dim;
+    P.state_dim = c.ae_state_dim;
+    P.chunk = C_;
+    P.heads = c.ae_q_heads;
+    P.rope_pos0 = L_;
+    P.rope_cols = ae_q_ + ae_kv_;
+    P.kv_rows0 = L_;
+    P.kcol_cache = llm_q_;
+    P.kcol_own = ae_q_;
+    P.key_blocks = in.key_blocks;
+    P.scale_log2 = float(1.4426950408889634 / std::sqrt(double(c.ae_head_dim)));
+    P.inv_width = 1.0f / float(W);
+    P.eps = 1e-6f;
+    P.euler = float(1.0 / double(FS_));
+    P.limit_phase = env_int("PI0B_AE_LIMIT", 1 << 30);
+    P.w_inflight = env_int("PI0B_AE_WINFLIGHT", 2);
+    P.trace = nullptr;
+    if (env_int("PI0B_AE_TRACE", 0)) {
+        P.trace = alloc<unsigned long long>(ae_plan_.table.size() * 8);
+        PI0B_CUDA(cudaMemset(P.trace, 0, ae_plan_.table.size() * 64));
+    }
+
+    Op m;
+    m.kind = kOpMemset;
+    m.part = 1;
+    m.mptr = ae_zero_;
+    m.mbytes = ae_zero_bytes_;
+    ops_.push_back(m);
+    Op cs;   // robot state -> fp32 (ae.state_proj input)
+    cs.kind = kOpRowsF32;
+    cs.part = 1;
+    cs.src64 = d_state_;
+    cs.rows = 1;
+    cs.cols = c.ae_state_dim;
+    cs.dst32 = state32_;
+    cs.ld32 = c.ae_state_dim;
+    ops_.push_back(cs);
+    Op cn;   // noise -> Euler state a_0
+    cn.kind = kOpRowsF32;
+    cn.part = 1;
+    cn.src64 = d_noise_;
+    cn.rows = C_;
+    cn.cols = c.ae_action_dim;
+    cn.dst32 = a_;
+    cn.ld32 = act_ld_;
+    ops_.push_back(cn);
+    Op k;
+    k.kind = kOpAeMega;
+    k.part = 1;
+    k.node = "ae.mega";
+    if (in.record) {
+        for (int i = 0; i < FS_ * NA; ++i)
+            k.extra_ck.push_back({"ae.down", i, rec_y + size_t(i) * 64 * W, S_, W, W});
+        for (int s2 = 0; s2 < FS_; ++s2)
+            k.extra_ck.push_back({"ae.head", s2, rec_a + size_t(s2) * C_ * act_ld_, C_, c.ae_action_dim, act_ld_});
+    }
+    ops_.push_back(k);
 }
 
 // ------------------------------------------------------------------ weights
@@ -1104,7 +1341,20 @@ void Engine::run_ops(int part, cudaStream_t st) {
                 break;
             case kOpF32F64: PI0B_CUDA(launch_f32_to_f64(op.src32, op.ld32, op.rows, op.cols, op.dst64, st)); break;
             case kOpMemset: PI0B_CUDA(cudaMemsetAsync(op.mptr, 0, op.mbytes, st)); break;
+            case kOpAeMega: PI0B_CUDA(aemk_launch(ae_p_, num_sms_, st)); break;
         }
+        if (o_.record_checkpoints)
+            for (const CkTag& tg : op.extra_ck) {
+                Checkpoint& ck = ck_[std::make_pair(tg.node, tg.inst)];
+                if (!ck.dev) {
+                    PI0B_CUDA(cudaMalloc(&ck.dev, size_t(tg.rows) * tg.cols * 4));
+                    ck.rows = tg.rows;
+                    ck.cols = tg.cols;
+                    ck.bf16 = 0;
+                }
+                PI0B_CUDA(cudaMemcpy2DAsync(ck.dev, tg.cols * 4, tg.ptr, tg.ld * 4, tg.cols * 4, tg.rows,
+                                            cudaMemcpyDeviceToDevice, st));
+            }
         if (o_.record_checkpoints && op.inst >= 0) {
             const auto key = std::make_pair(op.node, op.inst);
             Checkpoint& ck = ck_[key];
@@ -1168,7 +1418,7 @@ int Engine::kernel_count(int part) const {
 
 // One line per planned op: "<index> <part> <kind> <node> <inst> <grid> <detail>".
 std::string Engine::describe() const {
-    static const char* kinds[] = {"gemm", "attn", "rows_f32", "f64_bf16", "f32_f64", "memset", "skinny"};
+    static const char* kinds[] = {"gemm", "attn", "rows_f32", "f64_bf16", "f32_f64", "memset", "skinny", "ae_mega"};
     std::string s;
     int idx = 0;
     for (const Op& op : ops_) {
@@ -1181,6 +1431,10 @@ std::string Engine::describe() const {
             snprintf(buf, sizeof buf, "%d %d skinny %s %d tiles=%d cluster=%d M=%d N=%d K=%d mode=%d\n", idx, op.part,
                      op.node.c_str(), op.inst, skinny_tiles(op.n_packed), op.cluster, op.gp.M, op.gp.N, op.gp.K,
                      op.gp.mode);
+        } else if (op.kind == kOpAeMega) {
+            snprintf(buf, sizeof buf, "%d %d ae_mega %s 0 ctas=%d tasks=%d phases=%d counters=%d stride=%d wload=%.0f..%.0fKB\n",
+                     idx, op.part, op.node.c_str(), num_sms_, ae_plan_.n_tasks, ae_plan_.n_phases, ae_plan_.n_bars,
+                     ae_plan_.stride, ae_plan_.min_load / 1024, ae_plan_.max_load / 1024);
         } else if (op.kind == kOpAttn) {
             snprintf(buf, sizeof buf, "%d %d attn %s %d splits=%d q=%d kv=%d hd=%d\n", idx, op.part, op.node.c_str(),
                      op.inst, op.ap.kv_splits, op.ap.q_rows, op.ap.rows0 + op.ap.rows1, op.hd);
@@ -1198,11 +1452,16 @@ std::string Engine::describe() const {
 double Engine::time_node(const std::string& node, int reps, int* launches) {
     std::vector<const Op*> sel;
     for (const Op& op : ops_)
-        if (op.node == node && (op.kind == kOpGemm || op.kind == kOpAttn || op.kind == kOpSkinny)) sel.push_back(&op);
+        if (op.node == node && (op.kind == kOpGemm || op.kind == kOpAttn || op.kind == kOpSkinny || op.kind == kOpAeMega))
+            sel.push_back(&op);
     if (sel.empty()) throw EngineError(PI0B_E_INVALID, "no kernels for node '" + node + "'");
     auto fire = [&](const Op& op) {
         if (op.kind == kOpGemm) PI0B_CUDA(launch_gemm(op.bn, op.ta, op.tb, op.gp, stream_));
         else if (op.kind == kOpSkinny) PI0B_CUDA(launch_skinny(op.ta, op.tb, op.gp, op.n_packed, op.cluster, pdl_, stream_));
+        else if (op.kind == kOpAeMega) {
+            PI0B_CUDA(cudaMemsetAsync(ae_zero_, 0, ae_zero_bytes_, stream_));
+            PI0B_CUDA(aemk_launch(ae_p_, num_sms_, stream_));
+        }
         else PI0B_CUDA(launch_fattn(op.hd, op.fm, op.ap, stream_));
     };
     for (const Op* op : sel) fire(*op);
@@ -1220,6 +1479,17 @@ double Engine::time_node(const std::string& node, int reps, int* launches) {
     cudaEventDestroy(b);
     *launches = int(sel.size()) * reps;
     return double(ms) / double(*launches);
+}
+
+void Engine::ae_trace(void* tasks, unsigned long long* stamps, long long cap, int* ctas, int* stride) {
+    if (!ae_mega_ || !ae_p_.trace) throw EngineError(PI0B_E_STATE, "no megakernel trace (set PI0B_AE_TRACE=1)");
+    *ctas = num_sms_;
+    *stride = ae_plan_.stride;
+    const size_t n = ae_plan_.table.size();
+    if (cap < (long long)n) throw EngineError(PI0B_E_INVALID, "trace buffer too small");
+    PI0B_CUDA(cudaStreamSynchronize(stream_));
+    std::memcpy(tasks, ae_plan_.table.data(), n * sizeof(AeTask));
+    PI0B_CUDA(cudaMemcpy(stamps, ae_p_.trace, n * 64, cudaMemcpyDeviceToHost));
 }
 
 void Engine::read_checkpoint(const std::string& id, long long inst, float* out, long long rows, long long cols) {
@@ -1346,6 +1616,11 @@ int pi0b_engine_describe(pi0b_engine* e, char* buf, int64_t cap) {
 
 int pi0b_engine_time_node(pi0b_engine* e, const char* id, int reps, double* ms_per_launch, int* launches) {
     PI0B_TRY(*ms_per_launch = e->impl->time_node(id, reps, launches))
+}
+
+// Debug: the megakernel task table and its per-task globaltimer stamps (PI0B_AE_TRACE=1).
+int pi0b_engine_ae_trace(pi0b_engine* e, void* tasks, unsigned long long* stamps, int64_t cap, int* ctas, int* stride) {
+    PI0B_TRY(e->impl->ae_trace(tasks, stamps, cap, ctas, stride))
 }
 
 const char* pi0b_last_error(void) { return pi0b::g_last_error.c_str(); }

@@ -1,0 +1,19 @@
+"""Run the mid-config engine once (eager, no graph) and print the status: used for bisecting the
+megakernel with PI0B_AE_LIMIT=<phases> and under compute-sanitizer."""
+import os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from oracle import oracle as O
+from paper_2510_26742_b200 import engine as E
+from paper_2510_26742_b200.config import mid_config
+cfg = mid_config(views=int(sys.argv[1]) if len(sys.argv) > 1 else 1)
+x = O.gen_inputs(cfg, 1)
+eng = E.Engine(cfg, use_cuda_graph=False)
+eng.gen_weights(1)
+try:
+    eng.run_prefix(x["patches"])
+    print("prefix ok", flush=True)
+    y = eng.run_action(x["state"], x["noise"])
+    print("ok", float(abs(y).max()))
+except Exception as e:
+    print("FAIL", e)

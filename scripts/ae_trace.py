@@ -1,0 +1,101 @@
+"""Per-phase timeline of the action-expert megakernel from its globaltimer trace
+(PI0B_AE_TRACE=1): where the time of one AE launch goes."""
+import collections
+import ctypes
+import os
+import sys
+
+os.environ["PI0B_AE_TRACE"] = "1"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+
+from paper_2510_26742_b200 import engine as E  # noqa: E402
+from paper_2510_26742_b200.config import default_config  # noqa: E402
+from paper_2510_26742_b200.inputs import gen_inputs  # noqa: E402
+
+views = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+cfg = default_config(views=views)
+eng = E.Engine(cfg, use_cuda_graph=False)
+eng.gen_weights(1)
+x = gen_inputs(cfg, 1)
+for _ in range(3):
+    eng.run(x["patches"], x["state"], x["noise"])
+lib = E.lib()
+lib.pi0b_engine_ae_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                     ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+cap = 148 * 4096
+dt = np.dtype([("kind", "u1"), ("xsrc", "u1"), ("epi", "u1"), ("par", "u1"), ("wmap", "<u2"), ("xmap", "<u2"),
+               ("omap", "<u2"), ("tile", "<u2"), ("kb0", "<u2"), ("nkb", "<u2"), ("wait_bar", "<u2"),
+               ("wait_cnt", "<u2"), ("sig_bar", "<u2"), ("aux", "<u2"), ("step", "<u2"), ("layer", "<u2"),
+               ("phase", "<u2"), ("pad", "<u2")])
+tasks = np.zeros(cap, dtype=dt)
+st = np.zeros((cap, 8), dtype=np.uint64)
+ctas, stride = ctypes.c_int(), ctypes.c_int()
+rc = lib.pi0b_engine_ae_trace(eng._h, tasks.ctypes.data, st.ctypes.data, cap, ctypes.byref(ctas), ctypes.byref(stride))
+assert rc == 0, E.lib().pi0b_last_error()
+n = ctas.value * stride.value
+tasks, st = tasks[:n], st[:n].astype(np.int64)
+ok = (tasks["kind"] != 0) & (st[:, 3] > 0)
+t0 = st[ok, 0].min()
+st = np.where(st > 0, st - t0, -1)
+names = {(1, 5): "INIT", (1, 3): "AP", (1, 0): "RED", (1, 1): "QKV", (1, 2): "FFN", (1, 4): "HEAD"}
+ph = collections.defaultdict(list)
+for i in np.nonzero(ok)[0]:
+    ph[int(tasks["phase"][i])].append(i)
+kind_of = {}
+rows = []
+for p in sorted(ph):
+    idx = ph[p]
+    tk = tasks[idx[0]]
+    if tk["kind"] == 2:
+        nm = "ATTN"
+    elif tk["kind"] == 1 and tk["epi"] == 0:
+        nm = {0: "AO/DOWN", 2: "PROJ"}.get(int(tk["xsrc"]), "RED")
+        if tk["xsrc"] == 0 and tk["omap"] != tasks[ph[max(ph)][0]]["omap"]:
+            nm = "AO"
+    else:
+        nm = names.get((int(tk["kind"]), int(tk["epi"])), f"K{tk['kind']}")
+    s = st[idx]
+    rows.append((p, nm, len(idx), s[:, 0].min(), s[:, 1].max(), s[:, 3].max(),
+                 np.mean(s[:, 1] - s[:, 0]), np.mean(s[:, 2] - s[:, 1]), np.mean(s[:, 3] - s[:, 2])))
+tot = max(r[5] for r in rows)
+print(f"AE megakernel: {len(rows)} phases, {ok.sum()} tasks, span {tot / 1e3:.1f} us")
+agg = collections.defaultdict(lambda: np.zeros(6))
+prev_end = 0
+for r in rows:
+    p, nm, cnt, smin, rmax, emax, wait, stage, epi = r
+    a = agg[nm]
+    a += [1, emax - prev_end, cnt, wait, stage, epi]
+    prev_end = emax
+print(f"{'phase':8s} {'n':>4s} {'tasks':>6s} {'us/phase(end-to-end)':>21s} {'wait':>8s} {'stage':>8s} {'mma+epi':>8s}")
+for nm, a in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    print(f"{nm:8s} {int(a[0]):4d} {a[2] / a[0]:6.0f} {a[1] / a[0] / 1e3:21.2f} {a[3] / a[0] / 1e3:8.2f} "
+          f"{a[4] / a[0] / 1e3:8.2f} {a[5] / a[0] / 1e3:8.2f}")
+print("first 16 phases:")
+for r in rows[:16]:
+    print("  %3d %-8s n=%3d start %8.2f ready(max) %8.2f end(max) %8.2f  wait %.2f stage %.2f epi %.2f" %
+          (r[0], r[1], r[2], r[3] / 1e3, r[4] / 1e3, r[5] / 1e3, r[6] / 1e3, r[7] / 1e3, r[8] / 1e3))
+
+# detail of one mid-inference layer: per phase, percentiles of each stamp relative to the
+# completion of the previous phase
+cta_of = np.arange(n) // stride.value
+mid = [r for r in rows if r[0] >= len(rows) // 2][:6]
+prev_end = None
+for r in rows:
+    if r[0] == mid[0][0] - 1:
+        prev_end = r[5]
+print("\nlayer detail (us relative to the previous phase's last publish):")
+for r in mid:
+    idx = np.array(ph[r[0]])
+    s8 = st[idx].astype(np.float64)
+    rel = lambda c: (s8[:, c] - prev_end) / 1e3
+    def q(v):
+        v = v[np.isfinite(v)]
+        return "%7.2f/%7.2f/%7.2f" % (np.min(v), np.median(v), np.max(v)) if len(v) else "      -"
+    print(f"  {r[1]:8s} n={r[2]:3d} start {q(rel(0))} ready {q(rel(1))} staged {q(rel(2))} pub {q(rel(3))}")
+    if tasks["kind"][idx[0]] == 1:
+        print(f"  {'':8s}       w_first_issue {q(rel(4))} w_last_issue {q(rel(5))} w_last_full {q(rel(6))} acc {q(rel(7))}")
+    elif tasks["kind"][idx[0]] == 2:
+        print(f"  {'':8s}       s_landed {q(rel(4))} rendezvous {q(rel(5))} o_done {q(rel(6))} reduced {q(rel(7))}")
+    prev_end = r[5]
