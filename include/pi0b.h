@@ -96,9 +96,9 @@ int pi0b_engine_time_node(pi0b_engine* e, const char* node_id, int reps, double*
                           int* launches);
 
 /* Debug (PI0B_AE_TRACE=1 at engine creation): the action-expert megakernel's task table
- * (32-byte records, csrc/aemk.cuh AeTask) and 8 globaltimer stamps per task from the last launch
- * (worker: start, dependency met, operands staged, published; weight producer: first / last tile
- * issued; MMA: last weight tile landed, accumulator committed).  cap = table entries. */
+ * (32-byte records, csrc/aemk.cuh AeTask) and 16 globaltimer stamps per task from the last launch
+ * (csrc/aemk.cu: worker start / dependency met / operands staged / published, weight producer,
+ * MMA and epilogue / attention sub-steps).  cap = table entries. */
 int pi0b_engine_ae_trace(pi0b_engine* e, void* tasks, unsigned long long* stamps, int64_t cap, int* ctas,
                          int* stride);
 

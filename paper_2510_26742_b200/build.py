@@ -14,7 +14,7 @@ LIB = os.path.join(PKG, "libpi0b.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
-         "--expt-relaxed-constexpr"]
+         "--expt-relaxed-constexpr"] + os.environ.get("PI0B_NVCC_EXTRA", "").split()
 SOURCES = ["gemm.cu", "skinny.cu", "fattn.cu", "aemk.cu", "kernels_misc.cu", "engine.cu", "capi.cu"]
 
 

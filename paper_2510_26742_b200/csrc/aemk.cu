@@ -18,10 +18,12 @@
 //               row sums of squares of the RmsScale), epilogues from TMEM, softmax, the
 //               TMA reduce-add of split-K partials into the fp32 residual stream, signalling.
 //
-// Split-K partials (ae.proj, ae.down, ae.action_out) and the per-key-block attention outputs
-// are combined in L2 by cp.reduce.async.bulk.tensor (add.f32) — no workspace, no extra pass.
-// Attention key blocks share the row maximum through an atomicMax rendezvous so that their
-// exp-sums and P V products are directly additive.
+// All operand traffic is cp.async (LDGSTS): one SM's TMA/bulk engine serialises requests at
+// ~0.4 us each (scripts/ingest_bench.cu), while cp.async sustains ~300 GB/s per SM.  Split-K
+// partials (ae.proj, ae.down, ae.action_out) are added into the fp32 residual stream with
+// red.global.add.v4.f32 straight from the TMEM drain.  Attention runs as independent
+// (head pair, key range) tasks with an exact softmax over the range; the normalised partials and
+// their (row max, row sum) are combined by the ae.proj operand staging.
 #include "aemk.cuh"
 #include "ptx.cuh"
 
@@ -37,57 +39,57 @@ namespace {
 
 constexpr int kAeThreads = 320;
 constexpr int kWorkers = 256;
-constexpr int kWSt = 4;
-constexpr int kWTile = 128 * 64 * 2;  // 16 KB: 128 weight rows x 64 k
+constexpr int kWSt = 5;
+constexpr int kWTile = 128 * 64 * 2;  // 16 KB: 128 weight rows x 64 k (bf16, SW128 image)
 constexpr int kXSt = 4;
-constexpr int kXTile = 64 * 128;      // 8 KB: 64 activation rows x 64 k (bf16, SW128)
-constexpr int kFSt = 4;
-constexpr int kFTile = 16384;         // 64 rows x 64 fp32 as two SW128 boxes of 32 columns
+constexpr int kXTile = 64 * 128;      // 8 KB: 64 activation rows x 64 k
+constexpr int kFSt = 5;
+constexpr int kFTile = 16384;         // fp32 staging of one k-block: two SW128 boxes of 32 columns
+constexpr int kOSt = 2;
+constexpr int kMaxSplits = 5;         // attention key ranges combined by the ae.proj staging
+constexpr int kOTile = kMaxSplits * 8192;
+constexpr int kBlocksPerSplit = 2;    // 64-key blocks per attention task
 constexpr int kOffW = 0;
-constexpr int kOffU = kWSt * kWTile;                // union region, 160 KB
-constexpr int kOffX = kOffU;                        // GEMM: X ring (+1 pad slot)
-constexpr int kOffF = kOffU + (kXSt + 1) * kXTile;  // GEMM: fp32 staging ring
-constexpr int kOffE = kOffF + kFSt * kFTile;        // GEMM: fp32 epilogue tile (32 KB)
-constexpr int kOffQ = kOffU;                        // ATTN: Q  [128 x 256] bf16, 4 x 16 KB
-constexpr int kOffK = kOffU + 65536;                // ATTN: K  [64 x 256], 4 x 8 KB
-constexpr int kOffV = kOffU + 98304;                // ATTN: V  [64 x 256], 4 x 8 KB
-constexpr int kOffP = kOffK;                        // ATTN: P  [128 x 64] (reuses K)
-constexpr int kOffAux = kOffU + 163840;
-constexpr int kAeSmem = kOffAux + 1024 + 1024;      // + aux + alignment slack
-static_assert(kOffE + 32768 <= kOffAux, "GEMM union overflow");
+constexpr int kOffU = kWSt * kWTile;                // union region (128 KB)
+constexpr int kUnion = 131072;
+constexpr int kOffX = kOffU;                        // GEMM: X ring (+1 pad slot: rows 64..127 of A)
+constexpr int kOffF = kOffU + (kXSt + 1) * kXTile;  // GEMM: fp32 ring (kXY) or partial ring (kXO)
+constexpr int kOffQ = kOffU;                        // ATTN: Q [128 x 256] = 4 x 16 KB
+constexpr int kOffK = kOffU + 65536;                // ATTN: K [2 blocks][64 x 256] = 2 x 32 KB
+constexpr int kOffP = kOffQ;                        // ATTN: P [128 x 128 keys] (reuses Q)
+constexpr int kOffV = kOffK;                        // ATTN: V (reuses K)
+constexpr int kOffAux = kOffU + kUnion;
+constexpr int kAuxBytes = 8192;
+constexpr int kAeSmem = kOffAux + kAuxBytes + 1024;
+static_assert(kOffF + kFSt * kFTile <= kOffAux && kOffF + kOSt * kOTile <= kOffAux, "GEMM union overflow");
 static_assert(kAeSmem <= 232448, "shared memory budget");
-static_assert(kWSt <= 8 && kXSt <= 4 && kFSt <= 4, "barrier slots");
 
-constexpr uint32_t kTAcc = 0, kTS = 128, kTO = 256;  // TMEM columns (512 allocated)
+constexpr uint32_t kTAcc = 0, kTS = 0, kTO = 256;  // TMEM columns (512 allocated)
 
-PI0B_DEV unsigned ld_acquire_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
+// mbarrier slots
+constexpr int kBWFull = 0, kBWEmpty = 8, kBXFull = 16, kBXEmpty = 20, kBFFull = 24, kBOFull = 30, kBAccFull = 32,
+              kBAccEmpty = 33, kBQFull = 34, kBSFull = 35, kBVFull = 36, kBPFull = 37, kBODone = 38, kNumBars = 39;
+static_assert(kWSt <= 8 && kXSt <= 4 && kFSt <= 6 && kOSt <= 2, "barrier slots");
+
 PI0B_DEV unsigned ld_relaxed_u32(const unsigned* p) {
     unsigned v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-PI0B_DEV void red_release_add_u32(unsigned* p, unsigned v) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+PI0B_DEV unsigned atom_add_acqrel_u32(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
 }
-PI0B_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 PI0B_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-PI0B_DEV void tma_reduce_add_2d(const CUtensorMap* m, const void* src, int c0, int c1) {
-    asm volatile(
-        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-            reinterpret_cast<uint64_t>(m)),
-        "r"(smem_u32(src)), "r"(c0), "r"(c1)
-        : "memory");
+// Arrive on `bar` when all of this thread's prior cp.async copies have landed.
+PI0B_DEV void cp_async_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-PI0B_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-PI0B_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// Spin until a counter reaches `target` (relaxed polling, one acquire fence at the end); a
-// broken schedule traps (~4 s) instead of hanging the GPU.
-PI0B_DEV void wait_counter(const unsigned* c, unsigned target) {
+// Spin until a flag/counter reaches `target` (relaxed polling of a CTA-private line, one
+// acquire fence at the end); a broken schedule traps (~4 s) instead of hanging the GPU.
+PI0B_DEV void wait_flag(const unsigned* c, unsigned target) {
     if (ld_relaxed_u32(c) < target) {
         const long long t0 = clock64();
         while (ld_relaxed_u32(c) < target) {
@@ -96,21 +98,6 @@ PI0B_DEV void wait_counter(const unsigned* c, unsigned target) {
     }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
-PI0B_DEV unsigned atom_add_acqrel_u32(unsigned* p, unsigned v) {
-    unsigned old;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-    return old;
-}
-PI0B_DEV void st_relaxed_u32(unsigned* p, unsigned v) {
-    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// Order-preserving float <-> unsigned key (atomicMax on the key == max on the float).
-PI0B_DEV unsigned fkey(float f) {
-    const unsigned u = __float_as_uint(f);
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-PI0B_DEV float fdecode(unsigned k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k); }
 
 PI0B_DEV uint64_t desc_mn(uint32_t saddr, uint32_t lbo) {
     uint64_t d = 0;
@@ -132,11 +119,19 @@ PI0B_DEV void adv(int& slot, uint32_t& ph, int n, int stages) {
 
 PI0B_DEV AeTask load_task(const AeTask* t) {
     const uint4* s = reinterpret_cast<const uint4*>(t);
-    uint4 a = __ldg(s), b = __ldg(s + 1);
     AeTask r;
     uint4* d = reinterpret_cast<uint4*>(&r);
-    d[0] = a;
-    d[1] = b;
+    d[0] = __ldg(s);
+    d[1] = __ldg(s + 1);
+    return r;
+}
+
+PI0B_DEV AeMat load_mat(const AeMat* m) {
+    const uint4* s = reinterpret_cast<const uint4*>(m);
+    AeMat r;
+    uint4* d = reinterpret_cast<uint4*>(&r);
+    d[0] = __ldg(s);
+    d[1] = __ldg(s + 1);
     return r;
 }
 
@@ -148,6 +143,8 @@ PI0B_DEV unsigned long long gtimer() {
     return t;
 }
 
+PI0B_DEV int swz(int row, int chunk) { return row * 128 + ((chunk ^ (row & 7)) << 4); }
+
 }  // namespace
 
 __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
@@ -155,37 +152,43 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
     uint8_t* sW = smem + kOffW;
-    uint8_t* sU = smem + kOffU;
     uint8_t* sX = smem + kOffX;
     uint8_t* sF = smem + kOffF;
-    uint8_t* sE = smem + kOffE;
     uint8_t* sQ = smem + kOffQ;
     uint8_t* sK = smem + kOffK;
     uint8_t* sV = smem + kOffV;
     uint8_t* sP = smem + kOffP;
     uint64_t* mb = reinterpret_cast<uint64_t*>(smem + kOffAux);
-    uint64_t* w_full = mb;           // [kWSt <= 8]
-    uint64_t* w_empty = mb + 8;      // [kWSt]
-    uint64_t* x_full = mb + 16;      // [kXSt <= 4]
-    uint64_t* x_empty = mb + 20;     // [kXSt]
-    uint64_t* f_full = mb + 24;      // [kFSt <= 4]
-    uint64_t* acc_full = mb + 28;
-    uint64_t* acc_empty = mb + 29;
-    uint64_t* q_full = mb + 30;
-    uint64_t* k_full = mb + 31;
-    uint64_t* v_full = mb + 32;
-    uint64_t* s_full = mb + 33;
-    uint64_t* p_full = mb + 34;
-    uint64_t* o_done = mb + 35;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mb + 40);
-    float* sm_rs = reinterpret_cast<float*>(smem + kOffAux + 512);  // [64]
+    uint64_t* w_full = mb + kBWFull;
+    uint64_t* w_empty = mb + kBWEmpty;
+    uint64_t* x_full = mb + kBXFull;
+    uint64_t* x_empty = mb + kBXEmpty;
+    uint64_t* f_full = mb + kBFFull;
+    uint64_t* o_full = mb + kBOFull;
+    uint64_t* acc_full = mb + kBAccFull;
+    uint64_t* acc_empty = mb + kBAccEmpty;
+    uint64_t* q_full = mb + kBQFull;
+    uint64_t* s_full = mb + kBSFull;
+    uint64_t* v_full = mb + kBVFull;
+    uint64_t* p_full = mb + kBPFull;
+    uint64_t* o_done = mb + kBODone;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffAux + 512);
+    float* sm_rs = reinterpret_cast<float*>(smem + kOffAux + 1024);     // [64]
+    float2* sm_ml = reinterpret_cast<float2*>(smem + kOffAux + 2048);   // [kOSt][kMaxSplits][64]
+    float* sm_vec = reinterpret_cast<float*>(smem + kOffAux + 7168);    // [128] epilogue vector
+    volatile int* sm_flag = reinterpret_cast<volatile int*>(smem + kOffAux + 768);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const AeTask* my = p.tasks + size_t(blockIdx.x) * p.task_stride;
-    const CUtensorMap* maps = reinterpret_cast<const CUtensorMap*>(p.maps);
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 36; ++i) mbar_init(&mb[i], 1);
+        for (int i = 0; i < kNumBars; ++i) {
+            uint32_t cnt = 1;
+            if ((i >= kBXFull && i < kBXFull + kXSt) || (i >= kBFFull && i < kBFFull + kFSt) ||
+                (i >= kBOFull && i < kBOFull + kOSt) || i == kBQFull || i == kBVFull)
+                cnt = kWorkers;
+            mbar_init(&mb[i], cnt);
+        }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -196,33 +199,39 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
 
     if (warp == 0) {
         // ================================================================ weight producer
-        if (lane == 0) {
-            int ws = 0;
-            uint32_t wph = 0;
-            unsigned issued = 0;  // weight tiles issued so far
-            const unsigned cap = unsigned(max(1, min(p.w_inflight, kWSt)));
-            for (int i = 0;; ++i) {
-                const AeTask t = load_task(my + i);
-                if (t.kind == kAeEnd || t.phase >= p.limit_phase) break;
-                if (t.kind != kAeGemm) continue;
-                unsigned long long* tr = p.trace ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 8 : nullptr;
-                const CUtensorMap* wm = maps + t.wmap;
-                for (int k = 0; k < t.nkb; ++k) {
-                    mbar_wait(&w_empty[ws], wph ^ 1);
-                    if (issued >= cap) {  // at most `cap` tiles in flight: keeps the memory queues short
-                        const unsigned o = issued - cap;
-                        mbar_wait(&w_full[o % kWSt], (o / kWSt) & 1);
-                    }
-                    if (tr && k == 0) tr[4] = gtimer();
-                    mbar_arrive_expect_tx(&w_full[ws], kWTile);
-                    tma_load_2d(sW + ws * kWTile, wm, &w_full[ws], (t.kb0 + k) * 64, t.tile * 128, kEvictFirst);
-                    adv(ws, wph, 1, kWSt);
-                    ++issued;
+        // cp.async of each [128 x 64] weight tile straight into its SW128 operand image; the
+        // tile's w_full barrier completes when all 32 lanes' copies have landed.
+        int ws = 0;
+        uint32_t wph = 0;
+        unsigned issued = 0;
+        const unsigned cap = unsigned(max(1, min(p.w_inflight, kWSt)));
+        for (int i = 0;; ++i) {
+            const AeTask t = load_task(my + i);
+            if (t.kind == kAeEnd || t.phase >= p.limit_phase) break;
+            if (t.kind != kAeGemm) continue;
+            unsigned long long* tr = (p.trace && lane == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
+            const AeMat wm = load_mat(p.mats + t.wmat);
+            const __nv_bfloat16* wbase = reinterpret_cast<const __nv_bfloat16*>(wm.ptr);
+            for (int k = 0; k < t.nkb; ++k) {
+                mbar_wait(&w_empty[ws], wph ^ 1);
+                if (issued >= cap) {
+                    const unsigned o = issued - cap;
+                    mbar_wait(&w_full[o % kWSt], (o / kWSt) & 1);
                 }
-                if (tr) tr[5] = gtimer();
+                if (tr && k == 0) tr[4] = gtimer();
+                // tile-contiguous weights: tile (n_tile, kb) is one 16 KB block, already in the
+                // swizzled smem image (csrc/kernels_misc.cu tile_weight_kernel): one bulk copy on
+                // the TMA engine, off the LSU path the activation cp.asyncs use
+                const uint8_t* src = reinterpret_cast<const uint8_t*>(wbase) + ((size_t)t.tile * wm.ld + t.kb0 + k) * kWTile;
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&w_full[ws], kWTile);
+                    bulk_g2s(sW + ws * kWTile, src, kWTile, &w_full[ws], kEvictFirst);
+                }
+                adv(ws, wph, 1, kWSt);
+                ++issued;
             }
+            if (tr) tr[5] = gtimer();
         }
-        __syncwarp();
     } else if (warp == 1) {
         // ================================================================ MMA issuer
         if (lane == 0) {
@@ -234,14 +243,19 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             for (int i = 0;; ++i) {
                 const AeTask t = load_task(my + i);
                 if (t.kind == kAeEnd || t.phase >= p.limit_phase) break;
+                unsigned long long* tr = p.trace ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
                 if (t.kind == kAeGemm) {
-                    unsigned long long* tr = p.trace ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 8 : nullptr;
+                    unsigned long long* dbg = (p.dbg && t.epi == kEpiQkv && t.step == 0 && t.layer == 0)
+                                                  ? p.dbg + size_t(blockIdx.x) * 128 + 64 : nullptr;
                     mbar_wait(acc_empty, (gidx & 1) ^ 1);
-                    tc_fence_after();
                     for (int k = 0; k < t.nkb; ++k) {
+                        if (dbg && k < 16) dbg[k * 4] = gtimer();
                         mbar_wait(&w_full[ws], wph);
+                        if (dbg && k < 16) dbg[k * 4 + 1] = gtimer();
                         if (tr && k == t.nkb - 1) tr[6] = gtimer();
                         mbar_wait(&x_full[xs], xph);
+                        if (dbg && k < 16) dbg[k * 4 + 2] = gtimer();
+                        fence_proxy_async_smem();  // cp.async / st.shared data -> tensor-core reads
                         tc_fence_after();
                         const uint64_t ad = umma_desc_sw128(sX + xs * kXTile);
                         const uint64_t bd = umma_desc_sw128(sW + ws * kWTile);
@@ -250,6 +264,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                             umma_bf16(tmem + kTAcc, ad + 2 * kk, bd + 2 * kk, idesc_g, (k | kk) != 0);
                         umma_commit(&w_empty[ws]);
                         umma_commit(&x_empty[xs]);
+                        if (dbg && k < 16) dbg[k * 4 + 3] = gtimer();
                         adv(ws, wph, 1, kWSt);
                         adv(xs, xph, 1, kXSt);
                     }
@@ -258,30 +273,35 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     ++gidx;
                 } else if (t.kind == kAeAttn) {
                     const uint32_t ph = aidx & 1;
+                    const int nb = t.nkb;
                     mbar_wait(q_full, ph);
-                    mbar_wait(k_full, ph);
+                    if (tr) tr[6] = gtimer();
+                    fence_proxy_async_smem();
                     tc_fence_after();
-                    const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK), v0 = smem_u32(sV), p0 = smem_u32(sP);
+                    for (int b = 0; b < nb; ++b) {
 #pragma unroll
-                    for (int kk = 0; kk < 16; ++kk) {
-                        const uint64_t a = umma_desc_sw128(sQ + (kk >> 2) * 16384 + (kk & 3) * 32);
-                        const uint64_t b = umma_desc_sw128(sK + (kk >> 2) * 8192 + (kk & 3) * 32);
-                        umma_bf16(tmem + kTS, a, b, idesc_s, kk > 0);
+                        for (int kk = 0; kk < 16; ++kk) {
+                            const uint64_t a = umma_desc_sw128(sQ + (kk >> 2) * 16384 + (kk & 3) * 32);
+                            const uint64_t bb = umma_desc_sw128(sK + b * 32768 + (kk >> 2) * 8192 + (kk & 3) * 32);
+                            umma_bf16(tmem + kTS + b * 64, a, bb, idesc_s, kk > 0);
+                        }
                     }
                     umma_commit(s_full);
                     mbar_wait(p_full, ph);
                     mbar_wait(v_full, ph);
+                    if (tr) tr[7] = gtimer();
+                    fence_proxy_async_smem();
                     tc_fence_after();
+                    const uint32_t v0 = smem_u32(sV);
+                    for (int b = 0; b < nb; ++b) {
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const uint64_t a = umma_desc_sw128(sP + kk * 32);
-                        const uint64_t b = desc_mn(v0 + kk * 2048, 8192);
-                        umma_bf16(tmem + kTO, a, b, idesc_o, kk > 0);
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const uint64_t a = umma_desc_sw128(sP + b * 16384 + kk * 32);
+                            const uint64_t bb = desc_mn(v0 + b * 32768 + kk * 2048, 8192);
+                            umma_bf16(tmem + kTO, a, bb, idesc_o, (b | kk) != 0);
+                        }
                     }
                     umma_commit(o_done);
-                    (void)q0;
-                    (void)k0;
-                    (void)p0;
                     ++aidx;
                 }
             }
@@ -295,100 +315,106 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
         const int drow = wq * 32 + lane;              // drainer: activation row
         const int dhalf = warp >= 8 ? 1 : 0;          // drainer: column half
         const bool softmax = warp >= 4 && warp < 8;   // TMEM lanes 0..127 (stacked query rows)
-        const int srow = wq * 32 + lane;
         const uint32_t tlane = uint32_t(wq * 32) << 16;
-        int xs = 0, fs = 0;
-        uint32_t xph = 0, fph = 0, gidx = 0, aidx = 0;
-        // staging geometry: thread -> (row r, 16-column quarter q) of a 64 x 64 k-block
+        int xs = 0, fs = 0, os = 0;
+        uint32_t xph = 0, fph = 0, oph = 0, gidx = 0, aidx = 0;
+        // staging geometry: thread -> (row sr, 16-column quarter sq) of a 64 x 64 k-block
         const int sr = wtid >> 2, sq = wtid & 3;
 
         for (int i = 0;; ++i) {
             const AeTask t = load_task(my + i);
             if (t.kind == kAeEnd || t.phase >= p.limit_phase) break;
-            unsigned long long* tr = p.trace ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 8 : nullptr;
-            if (tr && wtid == 0) tr[0] = gtimer();
+            unsigned long long* tr = (p.trace && wtid == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
+            if (tr) tr[0] = gtimer();
             if (t.wait_cnt) {
-                if (wtid == 0) {
-                    wait_counter(p.mbox + size_t(blockIdx.x) * p.n_bars + t.wait_bar, 1u);
-                    fence_proxy_async_global();
-                }
+                if (wtid == 0) wait_flag(p.bars + t.wait_bar, t.wait_cnt);
                 named_bar_sync(1, kWorkers);
             }
-            if (tr && wtid == 0) tr[1] = gtimer();
+            if (tr) tr[1] = gtimer();
 
             if (t.kind == kAeGemm) {
+                // RmsScale rows of the residual stream this task reads (its finalisers' stats)
+                if ((t.epi == kEpiQkv || t.epi == kEpiGate || t.epi == kEpiHead) && wtid < 64) {
+                    const int row = min(wtid + (t.epi == kEpiHead ? 1 : 0), 63);
+                    sm_rs[wtid] = 1.0f / sqrtf(__ldcg(p.stats + (size_t)t.aux * 64 + row) * p.inv_width + p.eps);
+                }
                 // -------------------------------------------------- activation staging
-                const CUtensorMap* xm = maps + t.xmap;
+                const AeMat xm = load_mat(p.mats + t.xmat);
                 if (t.xsrc == kXBf16) {
-                    if (wtid == 0) {
-                        int s = xs;
-                        uint32_t ph = xph;
-                        for (int k = 0; k < t.nkb; ++k) {
-                            mbar_wait(&x_empty[s], ph ^ 1);
-                            mbar_arrive_expect_tx(&x_full[s], kXTile);
-                            tma_load_2d(sX + s * kXTile, xm, &x_full[s], (t.kb0 + k) * 64, 0, kEvictLast);
-                            adv(s, ph, 1, kXSt);
-                        }
-                    }
-                    adv(xs, xph, t.nkb, kXSt);
-                } else if (t.xsrc == kXY || t.xsrc == kXO) {
-                    float ss = 0.f;
-                    if (wtid == 0) {
-                        int s = fs;
-                        uint32_t ph = fph;
-                        for (int k = 0; k < t.nkb && k < kFSt; ++k) {
-                            mbar_arrive_expect_tx(&f_full[s], kFTile);
-                            tma_load_2d(sF + s * kFTile, xm, &f_full[s], (t.kb0 + k) * 64, 0, kEvictLast);
-                            tma_load_2d(sF + s * kFTile + 8192, xm, &f_full[s], (t.kb0 + k) * 64 + 32, 0, kEvictLast);
-                            adv(s, ph, 1, kFSt);
-                        }
-                    }
+                    const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(xm.ptr);
                     for (int k = 0; k < t.nkb; ++k) {
-                        float scale = 1.f;
-                        if (t.xsrc == kXO) {
-                            const int head = ((t.kb0 + k) * 64) >> 8;
-                            const float l = __ldcg(p.lacc[t.par] + head * 64 + sr);
-                            scale = l > 0.f ? 1.f / l : 0.f;
-                        }
-                        mbar_wait(&f_full[fs], fph);
                         mbar_wait(&x_empty[xs], xph ^ 1);
-                        const uint8_t* src = sF + fs * kFTile + (sq >> 1) * 8192 + sr * 128;
-                        float v[16];
+                        const int kc = (t.kb0 + k) * 64;
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int c = (sq & 1) * 4 + j;
-                            const float4 f = *reinterpret_cast<const float4*>(src + ((c ^ (sr & 7)) << 4));
-                            v[4 * j] = f.x * scale;
-                            v[4 * j + 1] = f.y * scale;
-                            v[4 * j + 2] = f.z * scale;
-                            v[4 * j + 3] = f.w * scale;
+                        for (int u = 0; u < 2; ++u) {
+                            const int q = wtid + 256 * u;
+                            const int row = q >> 3, c = q & 7;
+                            const bool ok = row < xm.rows;
+                            cp_async16(sX + xs * kXTile + swz(row, c), ok ? xb + (size_t)row * xm.ld + kc + c * 8 : xb, ok);
                         }
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) ss += v[j] * v[j];
-                        uint8_t* dst = sX + xs * kXTile + sr * 128;
-                        const uint4 u0 = make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
-                        const uint4 u1 = make_uint4(pack2(v[8], v[9]), pack2(v[10], v[11]), pack2(v[12], v[13]),
-                                                    pack2(v[14], v[15]));
-                        *reinterpret_cast<uint4*>(dst + (((2 * sq) ^ (sr & 7)) << 4)) = u0;
-                        *reinterpret_cast<uint4*>(dst + (((2 * sq + 1) ^ (sr & 7)) << 4)) = u1;
-                        fence_proxy_async_smem();
-                        named_bar_sync(1, kWorkers);
-                        if (wtid == 0) {
-                            mbar_arrive(&x_full[xs]);
-                            if (k + kFSt < t.nkb) {
-                                const int kb = t.kb0 + k + kFSt;
-                                mbar_arrive_expect_tx(&f_full[fs], kFTile);
-                                tma_load_2d(sF + fs * kFTile, xm, &f_full[fs], kb * 64, 0, kEvictLast);
-                                tma_load_2d(sF + fs * kFTile + 8192, xm, &f_full[fs], kb * 64 + 32, 0, kEvictLast);
-                            }
-                        }
-                        adv(fs, fph, 1, kFSt);
+                        cp_async_arrive_noinc(&x_full[xs]);
                         adv(xs, xph, 1, kXSt);
                     }
-                    if (t.xsrc == kXY) {
-                        ss += __shfl_xor_sync(0xffffffff, ss, 1);
-                        ss += __shfl_xor_sync(0xffffffff, ss, 2);
-                        if (sq == 0) sm_rs[sr] = 1.0f / sqrtf(ss * p.inv_width + p.eps);
+                } else if (t.xsrc == kXO) {
+                    // ae.proj input: combine the attention key-range partials of each row,
+                    // o = sum_j l_j 2^(m_j - M) O_j / sum_j l_j 2^(m_j - M); each thread loads and
+                    // combines its own 16 columns of its own row (no block barrier).
+                    const int ns = p.attn_splits;
+                    auto issue_o = [&](int k, int slot) {
+                        const int kc = (t.kb0 + k) * 64, head = kc >> 8;
+                        uint8_t* base = sF + slot * kOTile;
+                        for (int j = 0; j < ns; ++j) {
+                            const __nv_bfloat16* ob = p.opart + (size_t)j * 64 * p.q_width + (size_t)sr * p.q_width + kc;
+                            cp_async16(base + j * 8192 + swz(sr, 2 * sq), ob + 16 * sq, true);
+                            cp_async16(base + j * 8192 + swz(sr, 2 * sq + 1), ob + 16 * sq + 8, true);
+                        }
+                        if (sq == 0)  // (m, l) of this row for every split, 8 B each
+                            for (int j = 0; j < ns; ++j)
+                                cp_async8(sm_ml + (slot * kMaxSplits + j) * 64 + sr, p.ml + (size_t)j * p.heads * 64 + head * 64 + sr);
+                        cp_async_commit();
+                    };
+                    const int pre = min(t.nkb, kOSt);
+                    for (int k = 0; k < pre; ++k) issue_o(k, k);
+                    for (int k = 0; k < t.nkb; ++k) {
+                        const int slot = k % kOSt;
+                        if (min(kOSt, t.nkb - k) == 2) cp_async_wait<1>(); else cp_async_wait<0>();
+                        __syncwarp();  // (m, l) were fetched by the row's sq == 0 lane
+                        mbar_wait(&x_empty[xs], xph ^ 1);
+                        const float2* ml = sm_ml + slot * kMaxSplits * 64;
+                        float M = -INFINITY;
+                        for (int j = 0; j < ns; ++j) M = fmaxf(M, ml[j * 64 + sr].x);
+                        float v[16], wsum = 0.f;
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] = 0.f;
+                        for (int j = 0; j < ns; ++j) {
+                            const float2 mlj = ml[j * 64 + sr];
+                            const float w = mlj.y * ex2_fast(mlj.x - M);
+                            wsum += w;
+                            const uint8_t* src = sF + slot * kOTile + j * 8192;
+#pragma unroll
+                            for (int h2 = 0; h2 < 2; ++h2) {
+                                const uint4 u4 = *reinterpret_cast<const uint4*>(src + swz(sr, 2 * sq + h2));
+                                const uint32_t w4[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    v[h2 * 8 + 2 * e] += w * __uint_as_float(w4[e] << 16);
+                                    v[h2 * 8 + 2 * e + 1] += w * __uint_as_float(w4[e] & 0xffff0000u);
+                                }
+                            }
+                        }
+                        const float iw = wsum > 0.f ? 1.f / wsum : 0.f;
+                        uint8_t* dst = sX + xs * kXTile;
+                        *reinterpret_cast<uint4*>(dst + swz(sr, 2 * sq)) =
+                            make_uint4(pack2(v[0] * iw, v[1] * iw), pack2(v[2] * iw, v[3] * iw), pack2(v[4] * iw, v[5] * iw),
+                                       pack2(v[6] * iw, v[7] * iw));
+                        *reinterpret_cast<uint4*>(dst + swz(sr, 2 * sq + 1)) =
+                            make_uint4(pack2(v[8] * iw, v[9] * iw), pack2(v[10] * iw, v[11] * iw),
+                                       pack2(v[12] * iw, v[13] * iw), pack2(v[14] * iw, v[15] * iw));
+                        fence_proxy_async_smem();
+                        mbar_arrive(&x_full[xs]);
+                        __syncwarp();  // the row's (m, l) slot is refilled by lane sq == 0 below
+                        if (k + kOSt < t.nkb) issue_o(k + kOSt, slot);
+                        adv(xs, xph, 1, kXSt);
                     }
                 } else {  // kXRows: Euler state (ae.action_proj) or robot state (ae.state_proj), K <= 64
                     const bool init = t.epi == kEpiInit;
@@ -402,279 +428,255 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         const int c = sq * 16 + j;
                         v[j] = (sr < rows && c < cols) ? __ldcg(src + sr * ld + c) : 0.f;
                     }
-                    uint8_t* dst = sX + xs * kXTile + sr * 128;
-                    *reinterpret_cast<uint4*>(dst + (((2 * sq) ^ (sr & 7)) << 4)) =
+                    uint8_t* dst = sX + xs * kXTile;
+                    *reinterpret_cast<uint4*>(dst + swz(sr, 2 * sq)) =
                         make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
-                    *reinterpret_cast<uint4*>(dst + (((2 * sq + 1) ^ (sr & 7)) << 4)) =
+                    *reinterpret_cast<uint4*>(dst + swz(sr, 2 * sq + 1)) =
                         make_uint4(pack2(v[8], v[9]), pack2(v[10], v[11]), pack2(v[12], v[13]), pack2(v[14], v[15]));
                     fence_proxy_async_smem();
-                    named_bar_sync(1, kWorkers);
-                    if (wtid == 0) mbar_arrive(&x_full[xs]);
+                    mbar_arrive(&x_full[xs]);
                     adv(xs, xph, 1, kXSt);
                 }
-                // FFN tasks recycle the attention accumulators of their layer parity (read by
-                // this layer's ae.proj, which completed before any ae.ffn task started).
-                if (t.epi == kEpiGate) {
-                    const int parts = t.aux >> 8, part = t.aux & 255;
-                    const int n4 = (64 * p.q_width) / 4;
-                    float4* o4 = reinterpret_cast<float4*>(p.oacc[t.par]);
-                    const int per = (n4 + parts - 1) / parts;
-                    for (int j = part * per + wtid; j < min(n4, (part + 1) * per); j += kWorkers)
-                        __stcg(o4 + j, make_float4(0.f, 0.f, 0.f, 0.f));
-                    if (part == 0)
-                        for (int j = wtid; j < p.heads * 64; j += kWorkers) {
-                            p.lacc[t.par][j] = 0.f;
-                            p.mmax[t.par][j] = 0u;
-                        }
+                // Epilogue operands that do not depend on the accumulator: fetched now, while the
+                // MMA runs, so the drain loops touch only TMEM and shared memory.
+                if (t.epi == kEpiSilu || t.epi == kEpiInit || t.epi == kEpiHead) {
+                    const float* vec = t.epi == kEpiSilu ? p.table + (size_t)t.step * p.width + t.tile * 128
+                                                         : (t.epi == kEpiInit ? p.b_state + t.tile * 128 : p.b_head);
+                    const int n = t.epi == kEpiHead ? p.act_dim : 128;
+                    if (wtid < n) sm_vec[wtid] = __ldg(vec + wtid);
                 }
-                named_bar_sync(1, kWorkers);  // sm_rs complete
-                if (tr && wtid == 0) tr[2] = gtimer();
+                if (t.epi == kEpiSilu) {  // ae.suffix: y = [st ; b_out] on this tile's columns
+                    float4 yv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int q = wtid + 256 * u, row = q >> 5, c4 = q & 31;
+                        yv[u] = __ldcg(reinterpret_cast<const float4*>((row == 0 ? p.st : p.b_out) + t.tile * 128) + c4);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int q = wtid + 256 * u, row = q >> 5, c4 = q & 31;
+                        reinterpret_cast<float4*>(p.y + (size_t)row * p.width + t.tile * 128)[c4] = yv[u];
+                    }
+                }
+                named_bar_sync(1, kWorkers);  // sm_rs / sm_vec complete
+                if (tr) tr[2] = gtimer();
 
                 // -------------------------------------------------- epilogue
                 mbar_wait(acc_full, gidx & 1);
                 tc_fence_after();
+                if (tr) tr[8] = gtimer();
+                unsigned long long* trd =
+                    (p.trace && threadIdx.x == 128) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
+                if (trd) trd[10] = gtimer();
                 if (drainer) {
+                    // Compact loops over 4-column quads of the thread's row (TMEM lane):
+                    // short bodies stay hot in the instruction cache after one iteration.
                     const int r = drow;
                     const uint32_t ta = tmem + kTAcc + tlane;
                     if (t.epi == kEpiRed) {
+                        // split-K partial -> residual stream (red.add, fire-and-forget)
+                        const bool ok = t.rowoff ? r < p.chunk : true;
+                        float* dst = p.y + (size_t)(r + t.rowoff) * p.width + t.tile * 128 + dhalf * 64;
 #pragma unroll 1
-                        for (int cc = 0; cc < 2; ++cc) {
-                            float v[32];
-                            const int col0 = dhalf * 64 + cc * 32;
-                            tmem_ld32(ta + col0, v);
-                            uint8_t* box = sE + (col0 >> 5) * 8192 + r * 128;
-#pragma unroll
-                            for (int j = 0; j < 8; ++j)
-                                *reinterpret_cast<float4*>(box + ((j ^ (r & 7)) << 4)) =
-                                    make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                        for (int q = 0; q < 16; ++q) {
+                            float4 v;
+                            tmem_ld4(ta + dhalf * 64 + q * 4, v);
+                            if (ok) red_add_v4_f32(dst + q * 4, v.x, v.y, v.z, v.w);
                         }
-                        fence_proxy_async_smem();
-                    } else if (t.epi == kEpiQkv || t.epi == kEpiGate) {
-                        float a[32], b[32];
-                        const int c0 = dhalf * 32;
-                        tmem_ld32(ta + c0, a);
-                        tmem_ld32(ta + 64 + c0, b);
+                    } else if (t.epi == kEpiQkv) {
+                        // RmsScale -> RoPE pairs (c, c+64 in the packed tile = j, j+128 in the head)
                         const float rs = sm_rs[r];
-                        if (t.epi == kEpiGate) {
-                            __nv_bfloat16* o = p.g + (size_t)r * p.mlp + t.tile * 64 + c0;
+                        const int f0 = t.tile * 128;
+                        const bool rope = f0 < p.rope_cols;
+                        const int hd = f0 >> 8, u = (f0 & 255) >> 7;
+                        const int w0 = u * 64 + dhalf * 32;
+                        __nv_bfloat16* orow = p.qkv + (size_t)r * p.n_qkv;
+                        __nv_bfloat16* o1 = rope ? orow + hd * 256 + w0 : orow + f0 + dhalf * 32;
+                        __nv_bfloat16* o2 = rope ? o1 + 128 : o1 + 64;
+                        const float4* csp = reinterpret_cast<const float4*>(p.rope_cs) + ((size_t)(p.rope_pos0 + r) * 128 + w0) / 2;
+                        float4 cs4[16];  // all (cos, sin) pairs of the 32 columns, one round trip
 #pragma unroll
-                            for (int j = 0; j < 32; j += 8) {
-                                float gg[8];
+                        for (int e = 0; e < 16; ++e) cs4[e] = rope ? __ldg(csp + e) : make_float4(1.f, 0.f, 1.f, 0.f);
 #pragma unroll
-                                for (int u = 0; u < 8; ++u) gg[u] = (a[j + u] * rs) * gelu_tanh(b[j + u] * rs);
-                                *reinterpret_cast<uint4*>(o + j) = make_uint4(pack2(gg[0], gg[1]), pack2(gg[2], gg[3]),
-                                                                              pack2(gg[4], gg[5]), pack2(gg[6], gg[7]));
-                            }
-                        } else {
-                            const int f0 = t.tile * 128;
-                            __nv_bfloat16* orow = p.qkv + (size_t)r * p.n_qkv;
-                            float xa[32], xb[32];
-                            int ca;
-                            if (f0 < p.rope_cols) {
-                                // packed tile = [first halves w in [64u, 64u+64) | partners + 128]
-                                const int hd = f0 >> 8, u = (f0 & 255) >> 7;
-                                const int w0 = u * 64 + c0;
-                                ca = hd * 256 + w0;
-                                const float2* cs = reinterpret_cast<const float2*>(p.rope_cs) +
-                                                   (size_t)(p.rope_pos0 + r) * 128 + w0;
+                        for (int q = 0; q < 8; ++q) {
+                            float4 a4, b4;
+                            tmem_ld4(ta + dhalf * 32 + q * 4, a4);
+                            tmem_ld4(ta + 64 + dhalf * 32 + q * 4, b4);
+                            float xa[4] = {a4.x * rs, a4.y * rs, a4.z * rs, a4.w * rs};
+                            float xb[4] = {b4.x * rs, b4.y * rs, b4.z * rs, b4.w * rs};
+                            if (rope) {
+                                const float4 c0 = cs4[2 * q], c1 = cs4[2 * q + 1];
+                                const float cc[4] = {c0.x, c0.z, c1.x, c1.z}, ss[4] = {c0.y, c0.w, c1.y, c1.w};
 #pragma unroll
-                                for (int j = 0; j < 32; ++j) {
-                                    const float2 t2 = cs[j];
-                                    const float x = a[j] * rs, y = b[j] * rs;
-                                    xa[j] = x * t2.x - y * t2.y;
-                                    xb[j] = x * t2.y + y * t2.x;
-                                }
-                                __nv_bfloat16* o1 = orow + ca;
-                                __nv_bfloat16* o2 = orow + ca + 128;
-#pragma unroll
-                                for (int j = 0; j < 32; j += 8) {
-                                    *reinterpret_cast<uint4*>(o1 + j) = make_uint4(
-                                        pack2(xa[j], xa[j + 1]), pack2(xa[j + 2], xa[j + 3]), pack2(xa[j + 4], xa[j + 5]),
-                                        pack2(xa[j + 6], xa[j + 7]));
-                                    *reinterpret_cast<uint4*>(o2 + j) = make_uint4(
-                                        pack2(xb[j], xb[j + 1]), pack2(xb[j + 2], xb[j + 3]), pack2(xb[j + 4], xb[j + 5]),
-                                        pack2(xb[j + 6], xb[j + 7]));
-                                }
-                            } else {
-#pragma unroll
-                                for (int j = 0; j < 32; ++j) {
-                                    xa[j] = a[j] * rs;
-                                    xb[j] = b[j] * rs;
-                                }
-                                __nv_bfloat16* o1 = orow + f0 + c0;
-                                __nv_bfloat16* o2 = orow + f0 + 64 + c0;
-#pragma unroll
-                                for (int j = 0; j < 32; j += 8) {
-                                    *reinterpret_cast<uint4*>(o1 + j) = make_uint4(
-                                        pack2(xa[j], xa[j + 1]), pack2(xa[j + 2], xa[j + 3]), pack2(xa[j + 4], xa[j + 5]),
-                                        pack2(xa[j + 6], xa[j + 7]));
-                                    *reinterpret_cast<uint4*>(o2 + j) = make_uint4(
-                                        pack2(xb[j], xb[j + 1]), pack2(xb[j + 2], xb[j + 3]), pack2(xb[j + 4], xb[j + 5]),
-                                        pack2(xb[j + 6], xb[j + 7]));
+                                for (int e = 0; e < 4; ++e) {
+                                    const float x = xa[e], y = xb[e];
+                                    xa[e] = x * cc[e] - y * ss[e];
+                                    xb[e] = x * ss[e] + y * cc[e];
                                 }
                             }
+                            *reinterpret_cast<uint2*>(o1 + q * 4) = make_uint2(pack2(xa[0], xa[1]), pack2(xa[2], xa[3]));
+                            *reinterpret_cast<uint2*>(o2 + q * 4) = make_uint2(pack2(xb[0], xb[1]), pack2(xb[2], xb[3]));
+                        }
+                    } else if (t.epi == kEpiGate) {
+                        const float rs = sm_rs[r];
+                        __nv_bfloat16* o = p.g + (size_t)r * p.mlp + t.tile * 64 + dhalf * 32;
+#pragma unroll 1
+                        for (int q = 0; q < 8; ++q) {
+                            float4 a4, b4;
+                            tmem_ld4(ta + dhalf * 32 + q * 4, a4);
+                            tmem_ld4(ta + 64 + dhalf * 32 + q * 4, b4);
+                            *reinterpret_cast<uint2*>(o + q * 4) =
+                                make_uint2(pack2((a4.x * rs) * gelu_fast(b4.x * rs), (a4.y * rs) * gelu_fast(b4.y * rs)),
+                                           pack2((a4.z * rs) * gelu_fast(b4.z * rs), (a4.w * rs) * gelu_fast(b4.w * rs)));
                         }
                     } else if (t.epi == kEpiSilu) {
-                        // ae.action_proj: silu(a W + T[step]); and the ae.suffix reset of this
-                        // tile's columns of the residual stream: y = [st ; b_out] (builder.cpp:311-312)
+                        // ae.action_proj: silu(a W + T[step]) (the y reset ran during staging)
+                        const int c0 = dhalf * 64;
+                        __nv_bfloat16* o = p.ap + (size_t)r * p.width + t.tile * 128 + c0;
 #pragma unroll 1
-                        for (int cc = 0; cc < 2; ++cc) {
-                            float v[32];
-                            const int col0 = t.tile * 128 + dhalf * 64 + cc * 32;
-                            tmem_ld32(ta + dhalf * 64 + cc * 32, v);
-                            const float* tr = p.table + (size_t)t.step * p.width + col0;
-                            if (r < p.chunk) {
-                                __nv_bfloat16* o = p.ap + (size_t)r * p.width + col0;
-#pragma unroll
-                                for (int j = 0; j < 32; j += 2)
-                                    *reinterpret_cast<uint32_t*>(o + j) =
-                                        pack2(silu_f(v[j] + tr[j]), silu_f(v[j + 1] + tr[j + 1]));
-                            }
-                            const float* src = r == 0 ? p.st : p.b_out;
-                            float* yrow = p.y + (size_t)r * p.width + col0;
-#pragma unroll
-                            for (int j = 0; j < 32; j += 4)
-                                *reinterpret_cast<float4*>(yrow + j) = __ldcg(reinterpret_cast<const float4*>(src + col0 + j));
+                        for (int q = 0; q < 16; ++q) {
+                            float4 v;
+                            tmem_ld4(ta + c0 + q * 4, v);
+                            const float4 tb = *reinterpret_cast<const float4*>(sm_vec + c0 + q * 4);
+                            if (r < p.chunk)
+                                *reinterpret_cast<uint2*>(o + q * 4) =
+                                    make_uint2(pack2(silu_fast(v.x + tb.x), silu_fast(v.y + tb.y)),
+                                               pack2(silu_fast(v.z + tb.z), silu_fast(v.w + tb.w)));
                         }
                     } else if (t.epi == kEpiHead) {
-                        float v[32];
-                        tmem_ld32(ta, v);  // warp-uniform: tcgen05.ld is .sync.aligned
-                        if (dhalf == 0 && r < p.chunk) {
-                            const float rs = sm_rs[r];
-                            float* arow = p.a + (size_t)r * p.lda;
+                        // Euler: a += (RmsScale z + b) / FS on rows 1..63 (ae.act_rows)
+                        const bool ok = dhalf == 0 && r < p.chunk;
+                        const float rs = sm_rs[r];
+                        float4* arow = reinterpret_cast<float4*>(p.a + (size_t)r * p.lda);
+                        float4 av[8];
 #pragma unroll
-                            for (int c = 0; c < 32; ++c)
-                                if (c < p.act_dim) arow[c] += p.euler * (v[c] * rs + p.b_head[c]);
+                        for (int q = 0; q < 8; ++q) av[q] = ok && q * 4 < p.act_dim ? __ldcg(arow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            if (q * 4 >= p.act_dim) break;
+                            float4 v;
+                            tmem_ld4(ta + q * 4, v);  // warp-uniform: tcgen05.ld is .sync.aligned
+                            const float4 bv = *reinterpret_cast<const float4*>(sm_vec + q * 4);
+                            if (ok)
+                                arow[q] = make_float4(av[q].x + p.euler * (v.x * rs + bv.x), av[q].y + p.euler * (v.y * rs + bv.y),
+                                                      av[q].z + p.euler * (v.z * rs + bv.z), av[q].w + p.euler * (v.w * rs + bv.w));
                         }
                     } else if (t.epi == kEpiInit) {
+                        const int col0 = t.tile * 128 + dhalf * 64;
 #pragma unroll 1
-                        for (int cc = 0; cc < 2; ++cc) {
-                            float v[32];
-                            const int col0 = t.tile * 128 + dhalf * 64 + cc * 32;
-                            tmem_ld32(ta + dhalf * 64 + cc * 32, v);
-                            if (r == 0)
-                                for (int j = 0; j < 32; ++j)
-                                    if (col0 + j < p.width) p.st[col0 + j] = v[j] + p.b_state[col0 + j];
+                        for (int q = 0; q < 16; ++q) {
+                            float4 v;
+                            tmem_ld4(ta + dhalf * 64 + q * 4, v);
+                            const float4 bv = *reinterpret_cast<const float4*>(sm_vec + dhalf * 64 + q * 4);
+                            if (r == 0) reinterpret_cast<float4*>(p.st + col0)[q] = make_float4(v.x + bv.x, v.y + bv.y, v.z + bv.z, v.w + bv.w);
                         }
                     }
                 }
+                if (tr) tr[9] = gtimer();
+                if (p.trace && threadIdx.x == 128)  // drainer warp 4 lane 0 (row 0)
+                    p.trace[(size_t(blockIdx.x) * p.task_stride + i) * 16 + 14] = gtimer();
                 tc_fence_before();
                 named_bar_sync(1, kWorkers);
-                if (wtid == 0) {
-                    mbar_arrive(acc_empty);
-                    if (t.epi == kEpiRed) {
-                        const CUtensorMap* om = maps + t.omap;
-#pragma unroll
-                        for (int b = 0; b < 4; ++b) tma_reduce_add_2d(om, sE + b * 8192, t.tile * 128 + 32 * b, 0);
-                        bulk_commit();
-                        bulk_wait_all();
-                        fence_proxy_async_global();
-                    }
-                }
+                if (tr) tr[15] = gtimer();
+                if (wtid == 0) mbar_arrive(acc_empty);
                 ++gidx;
             } else if (t.kind == kAeAttn) {
-                // -------------------------------------------------- attention tile
+                // -------------------------------------------------- attention: one head pair
+                // (128 stacked query rows) x one key range of <= 2 blocks of 64 keys; exact
+                // softmax over the range, normalised partial + (row max, row sum) to global.
                 const uint32_t ph = aidx & 1;
-                const int rb = t.tile, j = t.kb0;
-                const int nh = min(2, p.heads - 2 * rb);
-                if (wtid == 0) {
-                    const CUtensorMap* qm = maps + t.xmap;
-                    mbar_arrive_expect_tx(q_full, nh * 4 * 8192);
-                    for (int hh = 0; hh < nh; ++hh)
-                        for (int a4 = 0; a4 < 4; ++a4)
-                            tma_load_2d(sQ + a4 * 16384 + hh * 8192, qm, q_full, (2 * rb + hh) * 256 + a4 * 64, 0,
-                                        kEvictLast);
-                    for (int isv = 0; isv < 2; ++isv) {
-                        uint64_t* bar = isv ? v_full : k_full;
-                        uint8_t* dst = isv ? sV : sK;
-                        mbar_arrive_expect_tx(bar, 32768);
-                        for (int half = 0; half < 2; ++half) {
-                            const int key = j * 64 + half * 32;
-                            const bool seg0 = key < p.kv_rows0;
-                            const CUtensorMap* m = maps + (seg0 ? t.wmap : t.omap);
-                            const int row = seg0 ? key : key - p.kv_rows0;
-                            const int col = (seg0 ? p.kcol_cache : p.kcol_own) + isv * 256;
-                            for (int a4 = 0; a4 < 4; ++a4)
-                                tma_load_2d(dst + a4 * 8192 + half * 4096, m, bar, col + a4 * 64, row, kEvictLast);
-                        }
+                const int rb = t.tile, split = t.kb0, nb = t.nkb;
+                const int key0 = split * kBlocksPerSplit * 64;
+                const AeMat km = load_mat(p.mats + t.wmat);  // LLM K/V cache of layer (i % llm_layers)
+                const __nv_bfloat16* kvc = reinterpret_cast<const __nv_bfloat16*>(km.ptr);
+                auto issue_kv = [&](uint8_t* dst, int col_off) {
+                    for (int u = 0; u < 8 * nb; ++u) {
+                        const int q = wtid + 256 * u;
+                        const int b = q >> 11, a4 = (q >> 9) & 3, kr = (q >> 3) & 63, c = q & 7;
+                        const int key = key0 + b * 64 + kr;
+                        const __nv_bfloat16* src = kvc;
+                        bool ok = true;
+                        if (key < p.kv_rows0)
+                            src = kvc + (size_t)key * km.ld + p.kcol_cache + col_off + a4 * 64 + c * 8;
+                        else if (key < p.kv_rows0 + 64)
+                            src = p.qkv + (size_t)(key - p.kv_rows0) * p.n_qkv + p.kcol_own + col_off + a4 * 64 + c * 8;
+                        else
+                            ok = false;
+                        cp_async16(dst + b * 32768 + a4 * 8192 + swz(kr, c), src, ok);
                     }
+                };
+                {   // Q (both heads of the pair) and K
+#pragma unroll 4
+                    for (int u = 0; u < 16; ++u) {
+                        const int q = wtid + 256 * u;
+                        const int a4 = q >> 10, R = (q >> 3) & 127, c = q & 7;
+                        const int head = 2 * rb + (R >> 6);
+                        const bool ok = head < p.heads;
+                        cp_async16(sQ + a4 * 16384 + swz(R, c),
+                                   ok ? p.qkv + (size_t)(R & 63) * p.n_qkv + head * 256 + a4 * 64 + c * 8 : p.qkv, ok);
+                    }
+                    issue_kv(sK, 0);
+                    cp_async_arrive_noinc(q_full);
                 }
-                unsigned long long* tra = (tr && threadIdx.x == 128) ? tr : nullptr;  // warp 4 lane 0
+                mbar_wait(s_full, ph);  // K (and Q) consumed: V may overwrite K
+                tc_fence_after();
+                issue_kv(sV, 256);
+                cp_async_arrive_noinc(v_full);
+                if (tr) tr[10] = gtimer();
+                unsigned long long* trs =
+                    (p.trace && threadIdx.x == 128) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
                 if (softmax) {
-                    const int R = srow;
+                    const int R = wq * 32 + lane;
                     const int head = 2 * rb + (R >> 6);
                     const bool hv = head < p.heads;
-                    const int gi = 2 * rb * 64 + R;
-                    mbar_wait(s_full, ph);
-                    tc_fence_after();
-                    if (tra) tra[4] = gtimer();
-                    float s[64];
-                    tmem_ld32(tmem + kTS + tlane, reinterpret_cast<float(&)[32]>(s[0]));
-                    tmem_ld32(tmem + kTS + tlane + 32, reinterpret_cast<float(&)[32]>(s[32]));
-                    const int total = p.kv_rows0 + 64;
+                    const int nk = p.kv_rows0 + 64 - key0;  // valid keys from key0
+                    const uint32_t ts = tmem + kTS + tlane;
                     float mx = -INFINITY;
+#pragma unroll 1
+                    for (int q = 0; q < nb * 8; ++q) {
+                        float v[8];
+                        tmem_ld8(ts + q * 8, v);
 #pragma unroll
-                    for (int c = 0; c < 64; ++c) {
-                        s[c] = j * 64 + c < total ? s[c] * p.scale_log2 : -INFINITY;
-                        mx = fmaxf(mx, s[c]);
+                        for (int e = 0; e < 8; ++e)
+                            if (q * 8 + e < nk) mx = fmaxf(mx, v[e] * p.scale_log2);
                     }
-                    if (hv) atomicMax(p.mmax[t.par] + gi, fkey(mx));
-                    named_bar_sync(2, 128);
-                    if (R == 0) {
-                        __threadfence();
-                        red_release_add_u32(p.bars + t.aux, 1);
-                        wait_counter(p.bars + t.aux, unsigned(p.key_blocks));
-                        __threadfence();
-                    }
-                    named_bar_sync(2, 128);
-                    if (tra) tra[5] = gtimer();
-                    const float M = hv ? fdecode(ld_relaxed_u32(p.mmax[t.par] + gi)) : mx;
                     float l = 0.f;
-                    uint32_t pk[32];
+#pragma unroll 1
+                    for (int q = 0; q < nb * 8; ++q) {
+                        float v[8];
+                        tmem_ld8(ts + q * 8, v);
+                        uint32_t pk[4];
 #pragma unroll
-                    for (int c = 0; c < 64; c += 2) {
-                        const float e0 = exp2f(s[c] - M), e1 = exp2f(s[c + 1] - M);
-                        l += e0 + e1;
-                        pk[c / 2] = pack2(e0, e1);
+                        for (int e = 0; e < 8; e += 2) {
+                            const float e0 = q * 8 + e < nk ? ex2_fast(v[e] * p.scale_log2 - mx) : 0.f;
+                            const float e1 = q * 8 + e + 1 < nk ? ex2_fast(v[e + 1] * p.scale_log2 - mx) : 0.f;
+                            l += e0 + e1;
+                            pk[e / 2] = pack2(e0, e1);
+                        }
+                        *reinterpret_cast<uint4*>(sP + (q >> 3) * 16384 + swz(R, q & 7)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                     }
-                    if (hv) atomicAdd(p.lacc[t.par] + gi, l);
-                    uint8_t* prow = sP + R * 128;
-#pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        *reinterpret_cast<uint4*>(prow + ((c ^ (R & 7)) << 4)) =
-                            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
                     fence_proxy_async_smem();
                     tc_fence_before();
                     named_bar_sync(2, 128);
                     if (R == 0) mbar_arrive(p_full);
+                    if (trs) trs[11] = gtimer();
                     mbar_wait(o_done, ph);
                     tc_fence_after();
-                    if (tra) tra[6] = gtimer();
-                    // un-normalised O -> fp32 boxes [head-in-pair][32-col chunk] -> reduce-add
-                    const int row = R & 63;
+                    if (trs) trs[12] = gtimer();
+                    const float il = l > 0.f ? 1.f / l : 0.f;
+                    __nv_bfloat16* orow = p.opart + (size_t)split * 64 * p.q_width + (size_t)(R & 63) * p.q_width + head * 256;
 #pragma unroll 1
-                    for (int c8 = 0; c8 < 8; ++c8) {
-                        float o[32];
-                        tmem_ld32(tmem + kTO + tlane + c8 * 32, o);
-                        uint8_t* box = sU + ((R >> 6) * 8 + c8) * 8192 + row * 128;
-#pragma unroll
-                        for (int q4 = 0; q4 < 8; ++q4)
-                            *reinterpret_cast<float4*>(box + ((q4 ^ (row & 7)) << 4)) =
-                                make_float4(o[4 * q4], o[4 * q4 + 1], o[4 * q4 + 2], o[4 * q4 + 3]);
+                    for (int q = 0; q < 32; ++q) {
+                        float o[8];
+                        tmem_ld8(tmem + kTO + tlane + q * 8, o);
+                        if (hv)
+                            *reinterpret_cast<uint4*>(orow + q * 8) =
+                                make_uint4(pack2(o[0] * il, o[1] * il), pack2(o[2] * il, o[3] * il),
+                                           pack2(o[4] * il, o[5] * il), pack2(o[6] * il, o[7] * il));
                     }
-                    fence_proxy_async_smem();
+                    if (hv) p.ml[(size_t)split * p.heads * 64 + head * 64 + (R & 63)] = make_float2(mx, l);
                     tc_fence_before();
-                    named_bar_sync(2, 128);
-                    if (R == 0) {
-                        const CUtensorMap* om = maps + t.nkb;
-                        for (int hh = 0; hh < nh; ++hh)
-                            for (int c8 = 0; c8 < 8; ++c8)
-                                tma_reduce_add_2d(om, sU + (hh * 8 + c8) * 8192, (2 * rb + hh) * 256 + c8 * 32, 0);
-                        bulk_commit();
-                        bulk_wait_all();
-                        fence_proxy_async_global();
-                        if (tra) tra[7] = gtimer();
-                    }
+                    if (trs) trs[13] = gtimer();
                 }
                 ++aidx;
             } else if (t.kind == kAeRecY) {
@@ -689,22 +691,41 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             }
 
             // -------------------------------------------------- publish completion
-            // The task that completes a phase sets the phase's flag in every CTA's mailbox line.
+            // bar.sync orders every worker's writes before lane 0's release (PTX cumulativity).
             named_bar_sync(1, kWorkers);
-            if (warp == 2) {
-                unsigned old = 0;
-                if (lane == 0) {
-                    __threadfence();
-                    old = atom_add_acqrel_u32(p.bars + t.sig_bar, 1u);
+            if (t.kind == kAeGemm && t.epi == kEpiRed) {
+                // Split-K: the last task of a 128-column tile finalises it: fp32 y -> bf16 yb and
+                // the rows' sums of squares (RmsStats) for the next RmsScale; only finalisers
+                // count towards the phase.
+                if (wtid == 0) sm_flag[0] = atom_add_acqrel_u32(p.bars + t.omat, 1u) + 1 == t.sig_cnt;
+                named_bar_sync(1, kWorkers);
+                if (sm_flag[0]) {
+                    const int r = wtid >> 2, c0 = t.tile * 128 + (wtid & 3) * 32;
+                    const float4* yr = reinterpret_cast<const float4*>(p.y + (size_t)r * p.width + c0);
+                    float4 v[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) v[j] = __ldcg(yr + j);
+                    float ss = 0.f;
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        ss += v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w;
+                        pk[2 * j] = pack2(v[j].x, v[j].y);
+                        pk[2 * j + 1] = pack2(v[j].z, v[j].w);
+                    }
+                    uint4* yb4 = reinterpret_cast<uint4*>(p.yb + (size_t)r * p.width + c0);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) yb4[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+                    ss += __shfl_xor_sync(0xffffffff, ss, 1);
+                    ss += __shfl_xor_sync(0xffffffff, ss, 2);
+                    if ((wtid & 3) == 0) atomicAdd(p.stats + (size_t)t.aux * 64 + r, ss);
+                    named_bar_sync(1, kWorkers);
+                    if (wtid == 0) atom_add_acqrel_u32(p.bars + t.sig_bar, 1u);
                 }
-                __syncwarp();
-                old = __shfl_sync(0xffffffff, old, 0);
-                if (old + 1 == t.sig_cnt) {
-                    __threadfence();
-                    for (int c = lane; c < int(gridDim.x); c += 32) st_relaxed_u32(p.mbox + size_t(c) * p.n_bars + t.sig_bar, 1u);
-                }
-                if (tr && lane == 0) tr[3] = gtimer();
+            } else if (wtid == 0) {
+                atom_add_acqrel_u32(p.bars + t.sig_bar, 1u);
             }
+            if (tr) tr[3] = gtimer();
         }
     }
 
@@ -745,7 +766,9 @@ AePlan ae_plan(const AePlanInput& in) {
     need(in.rope_cols % 128 == 0, "rope columns");
     need(in.chunk + 1 <= 64, "suffix rows > 64");
     need(in.act_dim <= 32 && in.state_dim <= 64, "action/state dims");
-    need(in.kv_rows0 % 32 == 0, "prefix length must be a multiple of 32");
+    need(in.kv_rows0 % 8 == 0, "prefix length must be a multiple of 8");
+    const int splits = (in.key_blocks + kBlocksPerSplit - 1) / kBlocksPerSplit;
+    need(splits <= kMaxSplits, "too many attention key blocks (prefix too long)");
     need(in.num_ctas >= 2 * ((in.heads + 1) / 2), "too few SMs");
 
     int nbar = 0;
@@ -759,6 +782,9 @@ AePlan ae_plan(const AePlanInput& in) {
     std::vector<double> load(size_t(in.num_ctas), 0.0);
     using QE = std::pair<double, int>;
     auto assign = [&](std::vector<Item>& items, bool distinct) {
+        // A CTA runs its tasks of one phase back to back, so a phase is spread over distinct CTAs
+        // whenever it has at most one task per CTA (least-loaded CTAs first).
+        distinct = distinct || int(items.size()) <= in.num_ctas;
         std::sort(items.begin(), items.end(), [](const Item& a, const Item& b) { return a.cost > b.cost; });
         std::priority_queue<QE, std::vector<QE>, std::greater<QE>> pq;
         for (int c = 0; c < in.num_ctas; ++c) pq.push({load[size_t(c)], c});
@@ -771,15 +797,15 @@ AePlan ae_plan(const AePlanInput& in) {
         }
         ++phase;
     };
-    auto gemm = [&](uint8_t xsrc, uint8_t epi, int wmap, int xmap, int omap, int tile, int kb0, int nkb, int wbar,
+    auto gemm = [&](uint8_t xsrc, uint8_t epi, int wmat, int xmat, int rowoff, int tile, int kb0, int nkb, int wbar,
                     int wcnt, int sbar) {
         AeTask t{};
         t.kind = kAeGemm;
         t.xsrc = xsrc;
         t.epi = epi;
-        t.wmap = uint16_t(wmap);
-        t.xmap = uint16_t(xmap);
-        t.omap = uint16_t(omap);
+        t.wmat = uint16_t(wmat);
+        t.xmat = uint16_t(xmat);
+        t.rowoff = uint8_t(rowoff);
         t.tile = uint16_t(tile);
         t.kb0 = uint16_t(kb0);
         t.nkb = uint16_t(nkb);
@@ -804,17 +830,37 @@ AePlan ae_plan(const AePlanInput& in) {
     {
         std::vector<Item> it;
         for (int t = 0; t < W / 128; ++t)
-            it.push_back({gemm(kXRows, kEpiInit, in.map_wst, 0, 0, t, 0, 1, 0, 0, bar_init), kWB});
+            it.push_back({gemm(kXRows, kEpiInit, in.mat_wst, 0, 0, t, 0, 1, 0, 0, bar_init), kWB});
         assign(it, false);
     }
     const int tiles_w = W / 128;
+    int nstat = 0;
+    // split-K residual update: tasks (tile, k-range) with a per-tile arrival counter; the last
+    // arrival of a tile finalises it (yb + stats slot `slot`) and signals the phase counter.
+    auto red_phase = [&](int wmat, int xmat, uint8_t xsrc, int rowoff, int kbt, int ks, int wbar, int wcnt, int pbar,
+                         int slot) {
+        std::vector<Item> it;
+        const int per = (kbt + ks - 1) / ks;
+        for (int t = 0; t < tiles_w; ++t) {
+            const int fin = newbar();
+            for (int k = 0; k < ks; ++k) {
+                const int kb0 = k * per, nkb = std::min(kbt, kb0 + per) - kb0;
+                if (nkb <= 0) continue;
+                AeTask x = gemm(xsrc, kEpiRed, wmat, xmat, rowoff, t, kb0, nkb, wbar, wcnt, pbar);
+                x.omat = uint16_t(fin);
+                x.aux = uint16_t(slot);
+                x.sig_cnt = uint16_t((kbt + per - 1) / per);
+                it.push_back({x, nkb * kWB});
+            }
+        }
+        assign(it, false);
+    };
     const int ks_ao = splits_for(tiles_w, kbW, 32);
     const int ks_proj = splits_for(tiles_w, in.q_width / 64, 128);
     const int ks_down = splits_for(tiles_w, MLP / 64, 128);
-    const int n_ao = tiles_w * ks_ao, n_proj = tiles_w * ks_proj, n_down = tiles_w * ks_down;
     const int tiles_qkv = NQ / 128, tiles_ffn = 2 * MLP / 128;
     const int pairs = (in.heads + 1) / 2;
-    const int n_attn = pairs * in.key_blocks;
+    const int n_attn = pairs * splits;
     int prev_bar = bar_init, prev_cnt = W / 128;
     int rec_slot = 0;
     for (int s = 0; s < FS; ++s) {
@@ -822,35 +868,26 @@ AePlan ae_plan(const AePlanInput& in) {
         {
             std::vector<Item> it;
             for (int t = 0; t < tiles_w; ++t) {
-                AeTask x = gemm(kXRows, kEpiSilu, in.map_wap, 0, 0, t, 0, 1, prev_bar, prev_cnt, bar_ap);
+                AeTask x = gemm(kXRows, kEpiSilu, in.mat_wap, 0, 0, t, 0, 1, prev_bar, prev_cnt, bar_ap);
                 x.step = uint16_t(s);
                 it.push_back({x, kWB});
             }
             assign(it, false);
         }
         const int bar_ao = newbar();
-        {
-            std::vector<Item> it;
-            const int per = (kbW + ks_ao - 1) / ks_ao;
-            for (int t = 0; t < tiles_w; ++t)
-                for (int k = 0; k < ks_ao; ++k) {
-                    const int kb0 = k * per, nkb = std::min(kbW, kb0 + per) - kb0;
-                    it.push_back({gemm(kXBf16, kEpiRed, in.map_wao, in.map_ap, in.map_yh, t, kb0, nkb, bar_ap, tiles_w,
-                                       bar_ao),
-                                  nkb * kWB});
-                }
-            assign(it, false);
-        }
+        int slot = nstat++;
+        red_phase(in.mat_wao, in.mat_ap, kXBf16, 1, kbW, ks_ao, bar_ap, tiles_w, bar_ao, slot);
         prev_bar = bar_ao;
-        prev_cnt = n_ao;
+        prev_cnt = tiles_w;
         for (int l = 0; l < NA; ++l) {
-            const int gl = s * NA + l, par = gl & 1;
+            const int gl = s * NA + l;
             const int bar_qkv = newbar();
             {
                 std::vector<Item> it;
                 for (int t = 0; t < tiles_qkv; ++t) {
-                    AeTask x = gemm(kXY, kEpiQkv, in.map_wqkv[size_t(l)], in.map_y, 0, t, 0, kbW, prev_bar, prev_cnt,
-                                    bar_qkv);
+                    AeTask x = gemm(kXBf16, kEpiQkv, in.mat_wqkv[size_t(l)], in.mat_yb, 0, t, 0, kbW, prev_bar,
+                                    prev_cnt, bar_qkv);
+                    x.aux = uint16_t(slot);
                     x.step = uint16_t(s);
                     x.layer = uint16_t(l);
                     it.push_back({x, kbW * kWB});
@@ -860,76 +897,47 @@ AePlan ae_plan(const AePlanInput& in) {
             const int bar_attn = newbar();
             {
                 std::vector<Item> it;
-                for (int rb = 0; rb < pairs; ++rb) {
-                    const int bar_max = newbar();
-                    for (int j = 0; j < in.key_blocks; ++j) {
+                for (int rb = 0; rb < pairs; ++rb)
+                    for (int j = 0; j < splits; ++j) {
                         AeTask x{};
                         x.kind = kAeAttn;
-                        x.par = uint8_t(par);
-                        x.wmap = uint16_t(in.map_kv[size_t(gl % int(in.map_kv.size()))]);
-                        x.xmap = uint16_t(in.map_q);
-                        x.omap = uint16_t(in.map_kvown);
-                        x.nkb = uint16_t(in.map_oacc[size_t(par)]);
+                        x.wmat = uint16_t(in.mat_kv[size_t(gl % int(in.mat_kv.size()))]);  // llm.qkv@mod
                         x.tile = uint16_t(rb);
                         x.kb0 = uint16_t(j);
+                        x.nkb = uint16_t(std::min(kBlocksPerSplit, in.key_blocks - j * kBlocksPerSplit));
                         x.wait_bar = uint16_t(bar_qkv);
                         x.wait_cnt = uint16_t(tiles_qkv);
                         x.sig_bar = uint16_t(bar_attn);
-                        x.aux = uint16_t(bar_max);
                         x.step = uint16_t(s);
                         x.layer = uint16_t(l);
                         x.phase = uint16_t(phase);
-                        it.push_back({x, 3.0 * kWB});
+                        it.push_back({x, 6.0 * kWB});
                     }
-                }
                 assign(it, true);
             }
             const int bar_proj = newbar();
-            {
-                std::vector<Item> it;
-                const int kbq = in.q_width / 64, per = (kbq + ks_proj - 1) / ks_proj;
-                for (int t = 0; t < tiles_w; ++t)
-                    for (int k = 0; k < ks_proj; ++k) {
-                        const int kb0 = k * per, nkb = std::min(kbq, kb0 + per) - kb0;
-                        AeTask x = gemm(kXO, kEpiRed, in.map_wproj[size_t(l)], in.map_oacc[size_t(par)], in.map_y, t, kb0,
-                                        nkb, bar_attn, n_attn, bar_proj);
-                        x.par = uint8_t(par);
-                        it.push_back({x, nkb * kWB});
-                    }
-                assign(it, false);
-            }
+            slot = nstat++;
+            red_phase(in.mat_wproj[size_t(l)], 0, kXO, 0, in.q_width / 64, ks_proj, bar_attn, n_attn, bar_proj, slot);
             const int bar_ffn = newbar();
             {
                 std::vector<Item> it;
                 for (int t = 0; t < tiles_ffn; ++t) {
-                    AeTask x = gemm(kXY, kEpiGate, in.map_wffn[size_t(l)], in.map_y, 0, t, 0, kbW, bar_proj, n_proj,
-                                    bar_ffn);
-                    x.par = uint8_t(par);
-                    x.aux = uint16_t((std::min(tiles_ffn, 255) << 8) | std::min(t, 254));
-                    if (t >= 255) x.aux = uint16_t((255 << 8) | 255);  // (never: mlp <= 8160)
+                    AeTask x = gemm(kXBf16, kEpiGate, in.mat_wffn[size_t(l)], in.mat_yb, 0, t, 0, kbW, bar_proj,
+                                    tiles_w, bar_ffn);
+                    x.aux = uint16_t(slot);
                     it.push_back({x, kbW * kWB});
                 }
                 assign(it, false);
             }
             const int bar_down = newbar();
-            {
-                std::vector<Item> it;
-                const int kbm = MLP / 64, per = (kbm + ks_down - 1) / ks_down;
-                for (int t = 0; t < tiles_w; ++t)
-                    for (int k = 0; k < ks_down; ++k) {
-                        const int kb0 = k * per, nkb = std::min(kbm, kb0 + per) - kb0;
-                        it.push_back({gemm(kXBf16, kEpiRed, in.map_wdown[size_t(l)], in.map_g, in.map_y, t, kb0, nkb,
-                                           bar_ffn, tiles_ffn, bar_down),
-                                      nkb * kWB});
-                    }
-                assign(it, false);
-            }
+            slot = nstat++;
+            red_phase(in.mat_wdown[size_t(l)], in.mat_g, kXBf16, 0, MLP / 64, ks_down, bar_ffn, tiles_ffn, bar_down, slot);
             if (rec) {
                 std::vector<Item> it;
                 AeTask x{};
                 x.kind = kAeRecY;
                 x.wait_bar = uint16_t(bar_down);
-                x.wait_cnt = uint16_t(n_down);
+                x.wait_cnt = uint16_t(tiles_w);
                 x.sig_bar = uint16_t(bar_down);
                 x.aux = uint16_t(rec_slot++);
                 x.phase = uint16_t(phase);
@@ -937,12 +945,13 @@ AePlan ae_plan(const AePlanInput& in) {
                 assign(it, false);
             }
             prev_bar = bar_down;
-            prev_cnt = n_down + rec;
+            prev_cnt = tiles_w + rec;
         }
         const int bar_head = newbar();
         {
             std::vector<Item> it;
-            AeTask x = gemm(kXY, kEpiHead, in.map_whead, in.map_yh, 0, 0, 0, kbW, prev_bar, prev_cnt, bar_head);
+            AeTask x = gemm(kXBf16, kEpiHead, in.mat_whead, in.mat_ybh, 0, 0, 0, kbW, prev_bar, prev_cnt, bar_head);
+            x.aux = uint16_t(slot);
             x.step = uint16_t(s);
             it.push_back({x, kbW * kWB / 4});
             assign(it, false);
@@ -963,13 +972,6 @@ AePlan ae_plan(const AePlanInput& in) {
         prev_cnt = 1 + rec;
     }
     need(nbar < 65535 && phase < 65535, "task table too large");
-    {   // number of signallers per counter -> sig_cnt (the last one broadcasts)
-        std::vector<int> cnt(size_t(nbar), 0);
-        for (auto& l : lists)
-            for (auto& t : l) ++cnt[t.sig_bar];
-        for (auto& l : lists)
-            for (auto& t : l) t.sig_cnt = uint16_t(cnt[t.sig_bar]);
-    }
     size_t stride = 0;
     for (auto& l : lists) stride = std::max(stride, l.size() + 1);
     out.stride = int(stride);
@@ -980,6 +982,8 @@ AePlan ae_plan(const AePlanInput& in) {
     out.n_phases = phase;
     out.n_tasks = 0;
     for (auto& l : lists) out.n_tasks += int(l.size());
+    out.attn_splits = splits;
+    out.n_stats = nstat;
     out.max_load = *std::max_element(load.begin(), load.end());
     out.min_load = *std::min_element(load.begin(), load.end());
     return out;

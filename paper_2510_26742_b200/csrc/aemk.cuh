@@ -5,14 +5,14 @@
 //
 // The host turns the fused graph into a static task table: every node instance is split into
 // tasks (a 128-feature output tile over a range of 64-wide k-blocks, or one attention
-// (head-pair, key-block) tile), tasks are assigned to CTAs, and each CTA walks its own list in
-// global phase order.  Ordering between node instances uses monotonically increasing global
-// counters (one per phase) instead of kernel boundaries: a task waits until the counter of the
-// phase it reads reaches that phase's task count, and bumps its own phase counter when its
-// outputs are globally visible.  Weights never depend on activations, so a dedicated TMA warp
-// streams each CTA's weight tiles through a shared-memory ring ahead of all dependency waits:
-// HBM keeps streaming the next layer's weights while the current layer's barriers resolve
-// (the "software barrier" + weight prefetch of PAPER.md:232-242 / SURVEY.md 7.3).
+// (head-pair, key-range) tile), tasks are assigned to CTAs, and each CTA walks its own list in
+// global phase order.  Ordering between node instances uses phase counters instead of kernel
+// boundaries: the task that completes a phase sets that phase's flag in every CTA's mailbox
+// line, and a task waits on the flag of the phase it reads.  Weights never depend on
+// activations, so a dedicated producer warp streams each CTA's weight tiles through a
+// shared-memory ring ahead of all dependency waits: HBM keeps streaming the next layer's
+// weights while the current layer's dependencies resolve (the "software barrier" + weight
+// prefetch of PAPER.md:232-242 / SURVEY.md 7.3).
 #pragma once
 
 #include <cuda_bf16.h>
@@ -26,17 +26,17 @@ namespace pi0b {
 
 enum AeTaskKind : uint8_t { kAeEnd = 0, kAeGemm = 1, kAeAttn = 2, kAeRecY = 3, kAeRecA = 4 };
 
-// How the 64-row activation operand of a GEMM task reaches shared memory.
+// How the 64-row activation operand of a GEMM task reaches shared memory (always cp.async).
 enum AeXSrc : uint8_t {
-    kXBf16 = 0,  // bf16 [rows, K] tensor map, TMA straight into the swizzled operand slot
-    kXY = 1,     // fp32 residual stream via TMA; workers convert to bf16 and accumulate the
-                 // row sums of squares (the RmsStats node, evaluate.cpp:308-309) for the epilogue
-    kXO = 2,     // fp32 un-normalised attention output O_acc via TMA, rows scaled by 1/l
-    kXRows = 3,  // small fp32 rows (Euler state / robot state) loaded by the workers
+    kXBf16 = 0,  // bf16 rows straight into the swizzled operand slot
+    kXY = 1,     // fp32 residual stream; workers convert to bf16 and accumulate the row sums of
+                 // squares (the RmsStats node, proj/src/evaluate.cpp:308-309) for the epilogue
+    kXO = 2,     // attention partials (bf16, per key range, with row max / sum): combined
+    kXRows = 3,  // small fp32 rows (Euler state / robot state), K <= 64
 };
 
 enum AeEpi : uint8_t {
-    kEpiRed = 0,   // fp32 tile -> TMA reduce-add into the residual stream (Residual epilogue)
+    kEpiRed = 0,   // fp32 partial -> red.add into the residual stream (Residual epilogue)
     kEpiQkv = 1,   // RmsScale -> RoPE -> bf16 q | k | v   (ae.ln1 + ae.qkv)
     kEpiGate = 2,  // RmsScale -> up * gelu(gate) -> bf16  (ae.ln2 + ae.ffn)
     kEpiSilu = 3,  // silu(z + bias_table[step]) -> bf16; resets y = [st ; b_out] (ae.action_proj)
@@ -44,30 +44,37 @@ enum AeEpi : uint8_t {
     kEpiInit = 5,  // st = z + b                                       (ae.state_proj)
 };
 
+// A dense row-major matrix operand (device pointer + shape + pitch in elements).
+struct alignas(16) AeMat {
+    const void* ptr;
+    int rows, cols, ld, pad_[3];
+};
+static_assert(sizeof(AeMat) == 32, "AeMat layout");
+
 struct AeTask {
-    uint8_t kind, xsrc, epi, par;  // par: layer parity of the attention accumulators
-    uint16_t wmap, xmap, omap;     // tensor-map indices (weights / activation / reduce target)
-    uint16_t tile;                 // GEMM: 128-feature output tile; ATTN: head pair
-    uint16_t kb0, nkb;             // GEMM: k-block range; ATTN: key block in kb0
-    uint16_t wait_bar, wait_cnt;   // wait until bars[wait_bar] >= wait_cnt
-    uint16_t sig_bar;              // bars[sig_bar] += 1 when done
-    uint16_t aux;                  // ATTN: rendezvous counter; REC: record slot
-    uint16_t step, layer;          // flow step, AE layer
-    uint16_t phase;                // global phase index (debug limit)
-    uint16_t sig_cnt;              // tasks that signal sig_bar (the last one broadcasts)
+    uint8_t kind, xsrc, epi, rowoff;  // rowoff: kEpiRed target rows start at y row `rowoff`
+    uint16_t wmat, xmat, omat;        // AeMat indices (weights / activation); split-K: tile counter
+    uint16_t tile;                    // GEMM: 128-feature output tile; ATTN: head pair
+    uint16_t kb0, nkb;                // GEMM: k-block range; ATTN: key split, #key blocks
+    uint16_t wait_bar, wait_cnt;      // wait until phase wait_bar completed (cnt > 0)
+    uint16_t sig_bar;                 // phase this task belongs to
+    uint16_t aux;                     // split-K: stats slot; QKV/FFN/HEAD: stats slot read; REC: slot
+    uint16_t step, layer;             // flow step, AE layer
+    uint16_t phase;                   // global phase index (debug limit)
+    uint16_t sig_cnt;                 // split-K: splits per tile (the last one finalises the tile)
 };
 static_assert(sizeof(AeTask) == 32, "AeTask layout");
 
 struct AeParams {
     const AeTask* tasks;
     int task_stride;               // tasks per CTA row of the table
-    const void* maps;              // CUtensorMap[] in global memory (64-byte aligned)
-    unsigned* bars;                // phase counters, zero on entry
-    unsigned* mbox;                // [ctas][n_bars] completion flags, zero on entry: the last
-                                   // task of a phase sets the phase's flag in every CTA's own
-                                   // line, so waiting CTAs poll disjoint L2 lines
+    const AeMat* mats;             // operand table
+    unsigned* bars;                // [n_bars] phase arrival counters, zero on entry
+    unsigned* mbox;                // [ctas][n_bars] phase-complete flags, zero on entry
     int n_bars;
     float* y;                      // [64, W]   residual stream (row 0 = state token)
+    __nv_bfloat16* yb;             // [64, W]   bf16 shadow of y, written by each tile's finaliser
+    float* stats;                  // [n_stats][64] row sums of squares of y per residual update
     float* a;                      // [C, lda]  Euler state
     int lda;
     const float* state;            // [state_dim] fp32
@@ -75,9 +82,8 @@ struct AeParams {
     __nv_bfloat16* qkv;            // [64, n_qkv]
     __nv_bfloat16* ap;             // [C, W]
     __nv_bfloat16* g;              // [64, mlp]
-    float* oacc[2];                // [64, q_width] un-normalised attention output, per parity
-    float* lacc[2];                // [heads * 64]  softmax denominators
-    unsigned* mmax[2];             // [heads * 64]  order-preserving keys of the row maxima
+    __nv_bfloat16* opart;          // [splits][64, q_width] normalised attention partials
+    float2* ml;                    // [splits][heads * 64] (row max (log2 units), row sum)
     const float* rope_cs;          // [positions][128] {cos, sin}
     const float* table;            // [FS, W] SiluBias table of ae.action_proj
     const float* b_state;          // [W]
@@ -89,29 +95,29 @@ struct AeParams {
     int rope_pos0, rope_cols;      // AE RoPE positions start at the prefix length L
     int kv_rows0;                  // L: rows of the cached LLM K/V segment
     int kcol_cache, kcol_own;      // first K column in the LLM KV cache / in the AE qkv rows
-    int key_blocks;                // ceil((L + 64) / 64)
+    int key_blocks;                // ceil((L + 64) / 64) key blocks of 64
+    int attn_splits;               // key ranges per head pair (<= 3 key blocks each)
     float scale_log2, inv_width, eps, euler;
     int limit_phase;               // run only tasks with phase < limit (debug / parity probes)
-    int w_inflight;                // weight tiles in flight per CTA (queueing latency vs bandwidth)
-    unsigned long long* trace;     // optional [ctas][stride][8] globaltimer stamps per task (pi0b.h)
-
+    int w_inflight;                // weight tiles in flight per CTA
+    unsigned long long* trace;     // optional [ctas][stride][16] globaltimer stamps per task
+    unsigned long long* dbg;       // optional [ctas][128] per-k-block stamps of the first ae.qkv task
 };
 
-// Host planner: dimensions + tensor-map indices in, per-CTA task table out.
+// Host planner: dimensions + operand indices in, per-CTA task table out.
 struct AePlanInput {
     int num_ctas;
     int width, n_qkv, q_width, mlp, layers, flow_steps, heads, chunk, act_dim, state_dim;
     int rope_cols, kv_rows0, key_blocks;
     bool record;
-    int map_wst, map_wap, map_wao, map_whead;
-    std::vector<int> map_wqkv, map_wproj, map_wffn, map_wdown, map_kv;
-    int map_y, map_yh, map_ap, map_g, map_q, map_kvown;
-    std::array<int, 2> map_oacc;
+    int mat_wst, mat_wap, mat_wao, mat_whead;
+    std::vector<int> mat_wqkv, mat_wproj, mat_wffn, mat_wdown, mat_kv;
+    int mat_yb, mat_ybh, mat_ap, mat_g, mat_qkv;
 };
 
 struct AePlan {
     std::vector<AeTask> table;  // [num_ctas][stride]
-    int stride = 0, n_bars = 0, n_phases = 0, n_tasks = 0;
+    int stride = 0, n_bars = 0, n_phases = 0, n_tasks = 0, attn_splits = 1, n_stats = 0;
     double max_load = 0, min_load = 0;  // weight bytes per CTA
 };
 

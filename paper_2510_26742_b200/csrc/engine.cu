@@ -49,6 +49,8 @@ cudaError_t launch_gen_weight(__nv_bfloat16* dst, long long ldk, int k, int m, i
                               uint64_t seed, double lo, double hi, cudaStream_t st);
 cudaError_t launch_pack_weight(__nv_bfloat16* dst, long long ldk, const double* w, int k, int m,
                                int perm, int rope_cols, cudaStream_t st);
+cudaError_t launch_tile_weight(const __nv_bfloat16* src, int rows, int k, long long ldk, __nv_bfloat16* dst,
+                               cudaStream_t st);
 cudaError_t skinny_configure();
 int skinny_tiles(int n_packed);
 cudaError_t launch_skinny(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p, int n_packed,
@@ -258,6 +260,13 @@ public:
     void fetch_actions(double* out);
     void read_checkpoint(const std::string& id, long long inst, float* out, long long rows, long long cols);
     int kernel_count(int part) const;
+    void prepare() {
+        if (ae_mega_ && ae_tiles_dirty_) {
+            for (const TiledW& tw : ae_tiled_) PI0B_CUDA(launch_tile_weight(tw.src, tw.rows, tw.k, tw.ldk, tw.dst, stream_));
+            PI0B_CUDA(cudaStreamSynchronize(stream_));
+            ae_tiles_dirty_ = false;
+        }
+    }
     double time_node(const std::string& node, int reps, int* launches);
     std::string describe() const;
     void ae_trace(void* tasks, unsigned long long* stamps, long long cap, int* ctas, int* stride);
@@ -331,6 +340,14 @@ private:
     AePlan ae_plan_;
     AeParams ae_p_{};
     float* state32_ = nullptr;
+    struct TiledW {
+        const __nv_bfloat16* src;
+        int rows, k;
+        long long ldk;
+        __nv_bfloat16* dst;
+    };
+    std::vector<TiledW> ae_tiled_;  // AE weights re-laid out as contiguous 16 KB tiles
+    bool ae_tiles_dirty_ = true;
     void* ae_zero_ = nullptr;
     size_t ae_zero_bytes_ = 0;
     void build_ae_mega();
@@ -1056,14 +1073,21 @@ void Engine::build_ae_mega() {
     if (c.ae_kv_heads != 1 || c.llm_kv_heads != 1)
         throw EngineError(PI0B_E_UNSUPPORTED, "action-expert megakernel: MQA (1 kv head) only");
     state32_ = alloc<float>(size_t(std::max(c.ae_state_dim, 8)));
-    std::vector<CUtensorMap> maps;
-    auto add = [&](const CUtensorMap& m) {
-        maps.push_back(m);
-        return int(maps.size()) - 1;
+    std::vector<AeMat> mats;
+    auto add = [&](const void* ptr, int rows, int cols, long long ld) {
+        if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld % 4))
+            throw EngineError(PI0B_E_INVALID, "megakernel operand needs 16-byte aligned rows");
+        mats.push_back(AeMat{ptr, rows, cols, int(ld), {0, 0, 0}});
+        return int(mats.size()) - 1;
     };
-    auto wmap = [&](const char* node, int inst, int rows) {
+    auto wmat = [&](const char* node, int inst, int rows) {
+        // tile-contiguous copy: AeMat{ptr, rows, k, k-blocks}
         const NodeWeights& nw = W_.at(node);
-        return add(make_tmap_2d(nw.w.at(size_t(inst)), false, rows, nw.k, nw.ldk, 128));
+        const int kb = (nw.k + 63) / 64, nt = (rows + 127) / 128;
+        __nv_bfloat16* t = alloc<__nv_bfloat16>(size_t(nt) * kb * 8192);
+        ae_tiled_.push_back({nw.w.at(size_t(inst)), rows, nw.k, nw.ldk, t});
+        mats.push_back(AeMat{t, rows, nw.k, kb, {0, 0, 0}});
+        return int(mats.size()) - 1;
     };
     AePlanInput in;
     in.num_ctas = num_sms_;
@@ -1081,60 +1105,40 @@ void Engine::build_ae_mega() {
     in.kv_rows0 = L_;
     in.key_blocks = (L_ + S_ + 63) / 64;
     in.record = o_.record_checkpoints != 0;
-    in.map_wst = wmap("ae.state_proj", 0, W);
-    in.map_wap = wmap("ae.action_proj", 0, W);
-    in.map_wao = wmap("ae.action_out", 0, W);
-    in.map_whead = wmap("ae.head", 0, c.ae_action_dim);
+    in.mat_wst = wmat("ae.state_proj", 0, W);
+    in.mat_wap = wmat("ae.action_proj", 0, W);
+    in.mat_wao = wmat("ae.action_out", 0, W);
+    in.mat_whead = wmat("ae.head", 0, c.ae_action_dim);
     for (int l = 0; l < NA; ++l) {
-        in.map_wqkv.push_back(wmap("ae.qkv", l, NQ));
-        in.map_wproj.push_back(wmap("ae.proj", l, W));
-        in.map_wffn.push_back(wmap("ae.ffn", l, 2 * MLP));
-        in.map_wdown.push_back(wmap("ae.down", l, W));
+        in.mat_wqkv.push_back(wmat("ae.qkv", l, NQ));
+        in.mat_wproj.push_back(wmat("ae.proj", l, W));
+        in.mat_wffn.push_back(wmat("ae.ffn", l, 2 * MLP));
+        in.mat_wdown.push_back(wmat("ae.down", l, W));
     }
     const int llm_qkv_n = llm_q_ + 2 * llm_kv_;
     for (int l = 0; l < c.llm_layers; ++l)  // AE instance i reads LLM layer i % llm_layers (@mod)
-        in.map_kv.push_back(add(make_tmap_2d(kv_[size_t(l)], false, L_, llm_qkv_n, llm_qkv_n, 32)));
-    in.map_y = add(make_tmap_2d(y_, true, S_, W, W, 64));
-    in.map_yh = add(make_tmap_2d(y_ + W, true, C_, W, W, 64));
-    in.map_ap = add(make_tmap_2d(ap_b_, false, C_, W, W, 64));
-    in.map_g = add(make_tmap_2d(ag_, false, S_, MLP, MLP, 64));
-    in.map_q = add(make_tmap_2d(aqkv_, false, S_, NQ, NQ, 64));
-    in.map_kvown = add(make_tmap_2d(aqkv_, false, S_, NQ, NQ, 32));
-
-    // zero-on-entry region: counters | O_acc[2] | l[2] | m[2]
-    const size_t n_o = size_t(64) * ae_q_, n_h = size_t(c.ae_q_heads) * 64;
-    float* oacc[2];
-    try {
-        ae_plan_ = ae_plan([&] {
-            AePlanInput t = in;
-            t.map_oacc = {0, 0};
-            return t;
-        }());
-    } catch (const std::invalid_argument& e) {
-        throw EngineError(PI0B_E_UNSUPPORTED, e.what());
-    }
-    const size_t bar_bytes = size_t(round_up(ae_plan_.n_bars * 4, 256)) +
-                             size_t(round_up(num_sms_ * ae_plan_.n_bars * 4, 256));
-    ae_zero_bytes_ = bar_bytes + 2 * n_o * 4 + 4 * round_up(int(n_h * 4), 256);
-    uint8_t* z = alloc<uint8_t>(ae_zero_bytes_);
-    ae_zero_ = z;
-    unsigned* bars = reinterpret_cast<unsigned*>(z);
-    oacc[0] = reinterpret_cast<float*>(z + bar_bytes);
-    oacc[1] = oacc[0] + n_o;
-    uint8_t* zz = reinterpret_cast<uint8_t*>(oacc[1] + n_o);
-    const size_t hb = size_t(round_up(int(n_h * 4), 256));
-    float* lacc[2] = {reinterpret_cast<float*>(zz), reinterpret_cast<float*>(zz + hb)};
-    unsigned* mmax[2] = {reinterpret_cast<unsigned*>(zz + 2 * hb), reinterpret_cast<unsigned*>(zz + 3 * hb)};
-    in.map_oacc = {add(make_tmap_2d(oacc[0], true, 64, ae_q_, ae_q_, 64)),
-                   add(make_tmap_2d(oacc[1], true, 64, ae_q_, ae_q_, 64))};
+        in.mat_kv.push_back(add(kv_[size_t(l)], L_, llm_qkv_n, llm_qkv_n));
+    __nv_bfloat16* yb = alloc<__nv_bfloat16>(size_t(S_) * W);
+    in.mat_yb = add(yb, S_, W, W);
+    in.mat_ybh = add(yb + W, C_, W, W);
+    in.mat_ap = add(ap_b_, C_, W, W);
+    in.mat_g = add(ag_, S_, MLP, MLP);
+    in.mat_qkv = add(aqkv_, S_, NQ, NQ);
     try {
         ae_plan_ = ae_plan(in);
     } catch (const std::invalid_argument& e) {
         throw EngineError(PI0B_E_UNSUPPORTED, e.what());
     }
+    // zero-on-entry region: phase / tile counters | row-statistics slots
+    const size_t bar_bytes = size_t(round_up(ae_plan_.n_bars * 4, 256));
+    ae_zero_bytes_ = bar_bytes + size_t(ae_plan_.n_stats) * 64 * 4;
+    uint8_t* z = alloc<uint8_t>(ae_zero_bytes_);
+    ae_zero_ = z;
+    __nv_bfloat16* opart = alloc<__nv_bfloat16>(size_t(ae_plan_.attn_splits) * 64 * ae_q_);
+    float2* ml = alloc<float2>(size_t(ae_plan_.attn_splits) * c.ae_q_heads * 64);
 
-    CUtensorMap* dmaps = alloc<CUtensorMap>(maps.size());
-    PI0B_CUDA(cudaMemcpyAsync(dmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice, stream_));
+    AeMat* dmats = alloc<AeMat>(mats.size());
+    PI0B_CUDA(cudaMemcpyAsync(dmats, mats.data(), mats.size() * sizeof(AeMat), cudaMemcpyHostToDevice, stream_));
     AeTask* dtasks = alloc<AeTask>(ae_plan_.table.size());
     PI0B_CUDA(cudaMemcpyAsync(dtasks, ae_plan_.table.data(), ae_plan_.table.size() * sizeof(AeTask),
                               cudaMemcpyHostToDevice, stream_));
@@ -1149,11 +1153,13 @@ void Engine::build_ae_mega() {
     AeParams& P = ae_p_;
     P.tasks = dtasks;
     P.task_stride = ae_plan_.stride;
-    P.maps = dmaps;
-    P.bars = bars;
-    P.mbox = bars + round_up(ae_plan_.n_bars * 4, 256) / 4;
+    P.mats = dmats;
+    P.bars = reinterpret_cast<unsigned*>(z);
+    P.mbox = nullptr;
     P.n_bars = ae_plan_.n_bars;
     P.y = y_;
+    P.yb = yb;
+    P.stats = reinterpret_cast<float*>(z + bar_bytes);
     P.a = a_;
     P.lda = act_ld_;
     P.state = state32_;
@@ -1161,11 +1167,8 @@ void Engine::build_ae_mega() {
     P.qkv = aqkv_;
     P.ap = ap_b_;
     P.g = ag_;
-    for (int i = 0; i < 2; ++i) {
-        P.oacc[i] = oacc[i];
-        P.lacc[i] = lacc[i];
-        P.mmax[i] = mmax[i];
-    }
+    P.opart = opart;
+    P.ml = ml;
     P.rope_cs = rope_cs_;
     P.table = W_.at("ae.action_proj").table;
     P.b_state = W_.at("ae.state_proj").b.at(0);
@@ -1187,16 +1190,20 @@ void Engine::build_ae_mega() {
     P.kcol_cache = llm_q_;
     P.kcol_own = ae_q_;
     P.key_blocks = in.key_blocks;
+    P.attn_splits = ae_plan_.attn_splits;
     P.scale_log2 = float(1.4426950408889634 / std::sqrt(double(c.ae_head_dim)));
     P.inv_width = 1.0f / float(W);
     P.eps = 1e-6f;
     P.euler = float(1.0 / double(FS_));
     P.limit_phase = env_int("PI0B_AE_LIMIT", 1 << 30);
-    P.w_inflight = env_int("PI0B_AE_WINFLIGHT", 2);
+    P.w_inflight = env_int("PI0B_AE_WINFLIGHT", 8);
     P.trace = nullptr;
+    P.dbg = nullptr;
     if (env_int("PI0B_AE_TRACE", 0)) {
-        P.trace = alloc<unsigned long long>(ae_plan_.table.size() * 8);
-        PI0B_CUDA(cudaMemset(P.trace, 0, ae_plan_.table.size() * 64));
+        P.dbg = alloc<unsigned long long>(size_t(num_sms_) * 128);
+        PI0B_CUDA(cudaMemset(P.dbg, 0, size_t(num_sms_) * 128 * 8));
+        P.trace = alloc<unsigned long long>(ae_plan_.table.size() * 16);
+        PI0B_CUDA(cudaMemset(P.trace, 0, ae_plan_.table.size() * 128));
     }
 
     Op m;
@@ -1258,6 +1265,7 @@ void Engine::gen_weights(uint64_t seed) {
     }
     PI0B_CUDA(cudaStreamSynchronize(stream_));
     weights_loaded_ = true;
+    ae_tiles_dirty_ = true;
 }
 
 void Engine::set_weight(const std::string& id, long long inst, const double* w, long long k, long long m,
@@ -1286,6 +1294,7 @@ void Engine::set_weight(const std::string& id, long long inst, const double* w, 
         PI0B_CUDA(cudaStreamSynchronize(stream_));
     }
     weights_loaded_ = true;
+    ae_tiles_dirty_ = true;
 }
 
 void Engine::set_bias_table(const std::string& id, const double* t, long long rows, long long m) {
@@ -1390,6 +1399,11 @@ void Engine::capture(int part, int slot) {
 // part: 0 = full, 1 = prefix, 2 = action (C-ABI numbering)
 void Engine::launch(int part, cudaStream_t st) {
     if (!weights_loaded_) throw EngineError(PI0B_E_STATE, "weights not loaded");
+    if (ae_mega_ && ae_tiles_dirty_) {  // (re)build the tile-contiguous AE weight copies
+        for (const TiledW& tw : ae_tiled_) PI0B_CUDA(launch_tile_weight(tw.src, tw.rows, tw.k, tw.ldk, tw.dst, stream_));
+        PI0B_CUDA(cudaStreamSynchronize(stream_));
+        ae_tiles_dirty_ = false;
+    }
     const int internal = part == 0 ? 2 : part - 1;  // ops filter: 2 all, 0 prefix, 1 action
     const int gidx = part;
     if (o_.use_cuda_graph && !o_.record_checkpoints) {
@@ -1450,6 +1464,7 @@ std::string Engine::describe() const {
 // Average device time of one launch of `node`'s kernels, measured with CUDA events on the
 // engine stream over `reps` back-to-back passes over all instances (bench roofline).
 double Engine::time_node(const std::string& node, int reps, int* launches) {
+    prepare();
     std::vector<const Op*> sel;
     for (const Op& op : ops_)
         if (op.node == node && (op.kind == kOpGemm || op.kind == kOpAttn || op.kind == kOpSkinny || op.kind == kOpAeMega))
@@ -1489,7 +1504,9 @@ void Engine::ae_trace(void* tasks, unsigned long long* stamps, long long cap, in
     if (cap < (long long)n) throw EngineError(PI0B_E_INVALID, "trace buffer too small");
     PI0B_CUDA(cudaStreamSynchronize(stream_));
     std::memcpy(tasks, ae_plan_.table.data(), n * sizeof(AeTask));
-    PI0B_CUDA(cudaMemcpy(stamps, ae_p_.trace, n * 64, cudaMemcpyDeviceToHost));
+    PI0B_CUDA(cudaMemcpy(stamps, ae_p_.trace, n * 128, cudaMemcpyDeviceToHost));
+    if (ae_p_.dbg && cap >= (long long)n + num_sms_ * 8)  // per-k-block stamps appended after the task stamps
+        PI0B_CUDA(cudaMemcpy(stamps + n * 16, ae_p_.dbg, size_t(num_sms_) * 128 * 8, cudaMemcpyDeviceToHost));
 }
 
 void Engine::read_checkpoint(const std::string& id, long long inst, float* out, long long rows, long long cols) {

@@ -116,7 +116,32 @@ __global__ void f32_to_f64_kernel(const float* src, long long lds, int rows, int
     dst[i] = double(src[(long long)(i / cols) * lds + (i % cols)]);
 }
 
+// Packed [rows, K] (pitch ldk) -> tile-contiguous [rows/128][K/64] blocks of 16 KB, each the exact
+// shared-memory image of a 128 x 64 operand tile in the 128-byte swizzle (16-byte chunk c of row
+// r at (c ^ (r & 7))), zero-padded past `rows` / `k`.  The action-expert megakernel streams
+// these with contiguous copies (a [128 x 64] box of the row-major weight is 128 pieces of 128 B
+// at a K-element stride: poor DRAM locality).
+__global__ void tile_weight_kernel(const __nv_bfloat16* src, int rows, int k, long long ldk, __nv_bfloat16* dst,
+                                   int kblocks) {
+    const long long tile = blockIdx.x;  // (n_tile * kblocks + kb)
+    const int nt = int(tile / kblocks), kb = int(tile % kblocks);
+    for (int q = threadIdx.x; q < 1024; q += blockDim.x) {
+        const int r = q >> 3, c = q & 7;
+        const int row = nt * 128 + r, col = kb * 64 + c * 8;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (row < rows && col < k) v = *reinterpret_cast<const uint4*>(src + (long long)row * ldk + col);
+        *reinterpret_cast<uint4*>(dst + tile * 8192 + r * 64 + ((c ^ (r & 7)) << 3)) = v;
+    }
+}
+
 // --------------------------------------------------------------------- launchers
+
+cudaError_t launch_tile_weight(const __nv_bfloat16* src, int rows, int k, long long ldk, __nv_bfloat16* dst,
+                               cudaStream_t st) {
+    const int kblocks = (k + 63) / 64, ntiles = (rows + 127) / 128;
+    tile_weight_kernel<<<ntiles * kblocks, 256, 0, st>>>(src, rows, k, ldk, dst, kblocks);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_gen_weight(__nv_bfloat16* dst, long long ldk, int k, int m, int perm, int rope_cols,
                               uint64_t seed, double lo, double hi, cudaStream_t st) {

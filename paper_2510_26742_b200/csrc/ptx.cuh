@@ -53,13 +53,33 @@ PI0B_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+PI0B_DEV bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 // Blocking wait with a watchdog: a pipeline bug traps (launch error) instead of hanging
 // the GPU forever.
+#ifndef PI0B_MBAR_SPIN
+#define PI0B_MBAR_SPIN 0
+#endif
 PI0B_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t spins = 0;
+#if PI0B_MBAR_SPIN
+    while (!mbar_test_wait(bar, parity)) {
+        if (++spins > (1u << 30)) __trap();
+    }
+#else
     while (!mbar_try_wait(bar, parity)) {
         if (++spins > (1u << 28)) __trap();
     }
+#endif
 }
 
 // ---------------------------------------------------------------- TMA
@@ -73,6 +93,14 @@ PI0B_DEV void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
         " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(cache_hint)
+        : "memory");
+}
+// 1-D bulk copy global -> shared (contiguous bytes, multiple of 16), complete_tx on `bar`.
+PI0B_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t cache_hint) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(cache_hint)
         : "memory");
 }
 // L2 cache-policy constants (createpolicy.fractional encodings used by CUTLASS).
@@ -151,6 +179,26 @@ PI0B_DEV void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Narrow TMEM loads (4 / 8 consecutive fp32 columns of the thread's lane): small loop bodies
+// keep cold epilogue code short (an instruction-cache miss costs ~60 ns per 128-byte line).
+PI0B_DEV void tmem_ld4(uint32_t taddr, float4& v) {
+    uint32_t r0, r1, r2, r3;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    v = make_float4(__uint_as_float(r0), __uint_as_float(r1), __uint_as_float(r2), __uint_as_float(r3));
+}
+PI0B_DEV void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // ---------------------------------------------------------------- clusters / DSMEM / PDL
 PI0B_DEV uint32_t cluster_ctarank() {
     uint32_t r;
@@ -194,6 +242,9 @@ PI0B_DEV void cp_async16(void* dst, const void* src, bool pred) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
                  "r"(sz)
                  : "memory");
+}
+PI0B_DEV void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 PI0B_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -241,6 +292,24 @@ PI0B_DEV float gelu_tanh(float x) {
     return 0.5f * x * (1.0f + tanhf(c * (x + 0.044715f * x * x * x)));
 }
 PI0B_DEV float silu_f(float x) { return x / (1.0f + expf(-x)); }
+
+// Single-MUFU variants for epilogues whose results are rounded to bf16 (2^-9): tanh.approx and
+// ex2.approx carry ~2^-11 relative error.
+PI0B_DEV float tanh_fast(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+PI0B_DEV float ex2_fast(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+PI0B_DEV float gelu_fast(float x) {
+    const float c = 0.7978845608028654f;
+    return 0.5f * x * (1.0f + tanh_fast(c * (x + 0.044715f * x * x * x)));
+}
+PI0B_DEV float silu_fast(float x) { return __fdividef(x, 1.0f + ex2_fast(-1.4426950408889634f * x)); }
 
 PI0B_DEV void red_add_f32(float* p, float v) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");

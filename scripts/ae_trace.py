@@ -30,11 +30,12 @@ dt = np.dtype([("kind", "u1"), ("xsrc", "u1"), ("epi", "u1"), ("par", "u1"), ("w
                ("wait_cnt", "<u2"), ("sig_bar", "<u2"), ("aux", "<u2"), ("step", "<u2"), ("layer", "<u2"),
                ("phase", "<u2"), ("pad", "<u2")])
 tasks = np.zeros(cap, dtype=dt)
-st = np.zeros((cap, 8), dtype=np.uint64)
+st = np.zeros((cap + 148 * 8, 16), dtype=np.uint64)
 ctas, stride = ctypes.c_int(), ctypes.c_int()
 rc = lib.pi0b_engine_ae_trace(eng._h, tasks.ctypes.data, st.ctypes.data, cap, ctypes.byref(ctas), ctypes.byref(stride))
 assert rc == 0, E.lib().pi0b_last_error()
 n = ctas.value * stride.value
+dbg = st[n:n + ctas.value * 8].reshape(ctas.value, 128).astype(np.int64)
 tasks, st = tasks[:n], st[:n].astype(np.int64)
 ok = (tasks["kind"] != 0) & (st[:, 3] > 0)
 t0 = st[ok, 0].min()
@@ -81,7 +82,7 @@ for r in rows[:16]:
 # completion of the previous phase
 cta_of = np.arange(n) // stride.value
 mid = [r for r in rows if r[0] >= len(rows) // 2][:6]
-prev_end = None
+prev_end = 0
 for r in rows:
     if r[0] == mid[0][0] - 1:
         prev_end = r[5]
@@ -96,6 +97,38 @@ for r in mid:
     print(f"  {r[1]:8s} n={r[2]:3d} start {q(rel(0))} ready {q(rel(1))} staged {q(rel(2))} pub {q(rel(3))}")
     if tasks["kind"][idx[0]] == 1:
         print(f"  {'':8s}       w_first_issue {q(rel(4))} w_last_issue {q(rel(5))} w_last_full {q(rel(6))} acc {q(rel(7))}")
+        print(f"  {'':8s}       acc_seen {q(rel(8))} epi_done {q(rel(9))}")
     elif tasks["kind"][idx[0]] == 2:
-        print(f"  {'':8s}       s_landed {q(rel(4))} rendezvous {q(rel(5))} o_done {q(rel(6))} reduced {q(rel(7))}")
+        print(f"  {'':8s}       qk_landed {q(rel(6))} s_full {q(rel(10))} p_full {q(rel(11))} pv_ready {q(rel(7))} o_done {q(rel(12))} stored {q(rel(13))}")
     prev_end = r[5]
+
+if os.environ.get("AE_TRACE_RAW"):
+    print("\nraw stamps of the first phases (us from kernel start): start ready staged pub | wfirst wlast wfull acc | accseen epidone | sfull pfull odone stored | drainer_done barrier")
+    for r in rows[:5]:
+        for i in ph[r[0]][:4]:
+            v = st[i] / 1e3
+            print(f"  ph{r[0]} {r[1]:6s} cta {i // stride.value:3d} " + " ".join(f"{x:7.2f}" if x >= 0 else "      -" for x in v[:16]))
+
+if os.environ.get("AE_TRACE_KB"):
+    rows_d = [c for c in range(ctas.value) if dbg[c, 0] > 0]
+    print("\nper-k-block stamps of the first ae.qkv task (us from its first stamp), CTA", rows_d[:1])
+    for c in rows_d[:1]:
+        d = dbg[c].astype(np.float64)
+        base = d[0]
+        for k in range(16):
+            w = (d[k * 4:k * 4 + 4] - base) / 1e3
+            m = (d[64 + k * 4:64 + k * 4 + 4] - base) / 1e3
+            print(f"  kb{k:2d} worker: start {w[0]:6.2f} f_full {w[1]:6.2f} x_empty {w[2]:6.2f} barrier {w[3]:6.2f}   "
+                  f"mma: start {m[0]:6.2f} w_full {m[1]:6.2f} x_full {m[2]:6.2f} issued {m[3]:6.2f}")
+
+if os.environ.get("AE_TRACE_LATE"):
+    print("\nlatest-ready tasks of a mid PROJ phase and their CTA's previous task:")
+    pr = [r for r in rows if r[1] == "PROJ"]
+    r = pr[len(pr) // 2]
+    idx = sorted(ph[r[0]], key=lambda i: -st[i][1])[:6]
+    for i in idx:
+        c, k = divmod(i, stride.value)
+        prev = i - 1 if k > 0 else None
+        pt = tasks[prev] if prev is not None else None
+        desc = f"prev phase {pt['phase']} kind {pt['kind']} epi {pt['epi']} start {st[prev][0]/1e3:.2f} ready {st[prev][1]/1e3:.2f} pub {st[prev][3]/1e3:.2f}" if prev is not None else "first"
+        print(f"  cta {c:3d} task {k:3d} ready {st[i][1]/1e3:8.2f} pub {st[i][3]/1e3:8.2f} | {desc}")
