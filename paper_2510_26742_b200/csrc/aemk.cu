@@ -178,7 +178,10 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
     float* sm_vec = reinterpret_cast<float*>(smem + kOffAux + 7168);    // [128] epilogue vector
     volatile int* sm_flag = reinterpret_cast<volatile int*>(smem + kOffAux + 768);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warp index through a shuffle: provably warp-uniform, so role branches stay converged and the
+    // MMA issue loop keeps descriptors in uniform registers (tcgen05.mma from divergent single-lane
+    // code costs ~2-3x more issue cycles, scripts/mma_bench.cu)
+    const int warp = __shfl_sync(0xffffffff, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const AeTask* my = p.tasks + size_t(blockIdx.x) * p.task_stride;
 
     if (threadIdx.x == 0) {
@@ -234,7 +237,9 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
         }
     } else if (warp == 1) {
         // ================================================================ MMA issuer
-        if (lane == 0) {
+        // The whole warp walks the task list (warp-uniform control flow); one elected lane issues
+        // each tcgen05.mma / commit.
+        {
             int ws = 0, xs = 0;
             uint32_t wph = 0, xph = 0, gidx = 0, aidx = 0;
             constexpr uint32_t idesc_g = umma_idesc_bf16(128, 128);
@@ -243,9 +248,9 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             for (int i = 0;; ++i) {
                 const AeTask t = load_task(my + i);
                 if (t.kind == kAeEnd || t.phase >= p.limit_phase) break;
-                unsigned long long* tr = p.trace ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
+                unsigned long long* tr = (p.trace && lane == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
                 if (t.kind == kAeGemm) {
-                    unsigned long long* dbg = (p.dbg && t.epi == kEpiQkv && t.step == 0 && t.layer == 0)
+                    unsigned long long* dbg = (p.dbg && lane == 0 && t.epi == kEpiQkv && t.step == 0 && t.layer == 0)
                                                   ? p.dbg + size_t(blockIdx.x) * 128 + 64 : nullptr;
                     mbar_wait(acc_empty, (gidx & 1) ^ 1);
                     for (int k = 0; k < t.nkb; ++k) {
@@ -259,16 +264,20 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         tc_fence_after();
                         const uint64_t ad = umma_desc_sw128(sX + xs * kXTile);
                         const uint64_t bd = umma_desc_sw128(sW + ws * kWTile);
+                        if (elect_one()) {
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            umma_bf16(tmem + kTAcc, ad + 2 * kk, bd + 2 * kk, idesc_g, (k | kk) != 0);
-                        umma_commit(&w_empty[ws]);
-                        umma_commit(&x_empty[xs]);
+                            for (int kk = 0; kk < 4; ++kk)
+                                umma_bf16(tmem + kTAcc, ad + 2 * kk, bd + 2 * kk, idesc_g, (k | kk) != 0);
+                            umma_commit(&w_empty[ws]);
+                            umma_commit(&x_empty[xs]);
+                        }
+                        __syncwarp();
                         if (dbg && k < 16) dbg[k * 4 + 3] = gtimer();
                         adv(ws, wph, 1, kWSt);
                         adv(xs, xph, 1, kXSt);
                     }
-                    umma_commit(acc_full);
+                    if (elect_one()) umma_commit(acc_full);
+                    __syncwarp();
                     if (tr) tr[7] = gtimer();
                     ++gidx;
                 } else if (t.kind == kAeAttn) {
@@ -278,30 +287,37 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     if (tr) tr[6] = gtimer();
                     fence_proxy_async_smem();
                     tc_fence_after();
-                    for (int b = 0; b < nb; ++b) {
-#pragma unroll
-                        for (int kk = 0; kk < 16; ++kk) {
-                            const uint64_t a = umma_desc_sw128(sQ + (kk >> 2) * 16384 + (kk & 3) * 32);
-                            const uint64_t bb = umma_desc_sw128(sK + b * 32768 + (kk >> 2) * 8192 + (kk & 3) * 32);
-                            umma_bf16(tmem + kTS + b * 64, a, bb, idesc_s, kk > 0);
+                    {   // S[b] = Q K_b^T: descriptors advance by (bytes >> 4); compact loop (cold code)
+                        const uint64_t qd = umma_desc_sw128(sQ), kd = umma_desc_sw128(sK);
+#pragma unroll 1
+                        for (int i = 0; i < nb * 16; ++i) {
+                            const int b = i >> 4, kk = i & 15;
+                            if (elect_one())
+                                umma_bf16(tmem + kTS + b * 64, qd + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4),
+                                          kd + ((b * 32768 + (kk >> 2) * 8192 + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
+                            __syncwarp();
                         }
                     }
-                    umma_commit(s_full);
+                    if (elect_one()) umma_commit(s_full);
+                    __syncwarp();
                     mbar_wait(p_full, ph);
                     mbar_wait(v_full, ph);
                     if (tr) tr[7] = gtimer();
                     fence_proxy_async_smem();
                     tc_fence_after();
-                    const uint32_t v0 = smem_u32(sV);
-                    for (int b = 0; b < nb; ++b) {
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            const uint64_t a = umma_desc_sw128(sP + b * 16384 + kk * 32);
-                            const uint64_t bb = desc_mn(v0 + b * 32768 + kk * 2048, 8192);
-                            umma_bf16(tmem + kTO, a, bb, idesc_o, (b | kk) != 0);
+                    {   // O = P V
+                        const uint64_t pd = umma_desc_sw128(sP), vd = desc_mn(smem_u32(sV), 8192);
+#pragma unroll 1
+                        for (int i = 0; i < nb * 4; ++i) {
+                            const int b = i >> 2, kk = i & 3;
+                            if (elect_one())
+                                umma_bf16(tmem + kTO, pd + ((b * 16384 + kk * 32) >> 4), vd + ((b * 32768 + kk * 2048) >> 4),
+                                          idesc_o, i != 0);
+                            __syncwarp();
                         }
                     }
-                    umma_commit(o_done);
+                    if (elect_one()) umma_commit(o_done);
+                    __syncwarp();
                     ++aidx;
                 }
             }
@@ -334,7 +350,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
 
             if (t.kind == kAeGemm) {
                 // RmsScale rows of the residual stream this task reads (its finalisers' stats)
-                if ((t.epi == kEpiQkv || t.epi == kEpiGate || t.epi == kEpiHead) && wtid < 64) {
+                if (t.epi == kEpiHead && wtid < 64) {
                     const int row = min(wtid + (t.epi == kEpiHead ? 1 : 0), 63);
                     sm_rs[wtid] = 1.0f / sqrtf(__ldcg(p.stats + (size_t)t.aux * 64 + row) * p.inv_width + p.eps);
                 }
@@ -473,61 +489,19 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     // short bodies stay hot in the instruction cache after one iteration.
                     const int r = drow;
                     const uint32_t ta = tmem + kTAcc + tlane;
-                    if (t.epi == kEpiRed) {
-                        // split-K partial -> residual stream (red.add, fire-and-forget)
+                    if (t.sig_cnt) {
+                        // split-K partial -> fp32 accumulator (residual stream, or the ae.qkv /
+                        // ae.ffn accumulators finalised by the tile's last task): red.add
+                        float* base = t.epi == kEpiRed ? p.y + (size_t)t.rowoff * p.width
+                                                       : (t.epi == kEpiQkv ? p.qacc : p.facc);
+                        const int ld = t.epi == kEpiRed ? p.width : (t.epi == kEpiQkv ? p.n_qkv : 2 * p.mlp);
                         const bool ok = t.rowoff ? r < p.chunk : true;
-                        float* dst = p.y + (size_t)(r + t.rowoff) * p.width + t.tile * 128 + dhalf * 64;
+                        float* dst = base + (size_t)r * ld + t.tile * 128 + dhalf * 64;
 #pragma unroll 1
                         for (int q = 0; q < 16; ++q) {
                             float4 v;
                             tmem_ld4(ta + dhalf * 64 + q * 4, v);
                             if (ok) red_add_v4_f32(dst + q * 4, v.x, v.y, v.z, v.w);
-                        }
-                    } else if (t.epi == kEpiQkv) {
-                        // RmsScale -> RoPE pairs (c, c+64 in the packed tile = j, j+128 in the head)
-                        const float rs = sm_rs[r];
-                        const int f0 = t.tile * 128;
-                        const bool rope = f0 < p.rope_cols;
-                        const int hd = f0 >> 8, u = (f0 & 255) >> 7;
-                        const int w0 = u * 64 + dhalf * 32;
-                        __nv_bfloat16* orow = p.qkv + (size_t)r * p.n_qkv;
-                        __nv_bfloat16* o1 = rope ? orow + hd * 256 + w0 : orow + f0 + dhalf * 32;
-                        __nv_bfloat16* o2 = rope ? o1 + 128 : o1 + 64;
-                        const float4* csp = reinterpret_cast<const float4*>(p.rope_cs) + ((size_t)(p.rope_pos0 + r) * 128 + w0) / 2;
-                        float4 cs4[16];  // all (cos, sin) pairs of the 32 columns, one round trip
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) cs4[e] = rope ? __ldg(csp + e) : make_float4(1.f, 0.f, 1.f, 0.f);
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            float4 a4, b4;
-                            tmem_ld4(ta + dhalf * 32 + q * 4, a4);
-                            tmem_ld4(ta + 64 + dhalf * 32 + q * 4, b4);
-                            float xa[4] = {a4.x * rs, a4.y * rs, a4.z * rs, a4.w * rs};
-                            float xb[4] = {b4.x * rs, b4.y * rs, b4.z * rs, b4.w * rs};
-                            if (rope) {
-                                const float4 c0 = cs4[2 * q], c1 = cs4[2 * q + 1];
-                                const float cc[4] = {c0.x, c0.z, c1.x, c1.z}, ss[4] = {c0.y, c0.w, c1.y, c1.w};
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    const float x = xa[e], y = xb[e];
-                                    xa[e] = x * cc[e] - y * ss[e];
-                                    xb[e] = x * ss[e] + y * cc[e];
-                                }
-                            }
-                            *reinterpret_cast<uint2*>(o1 + q * 4) = make_uint2(pack2(xa[0], xa[1]), pack2(xa[2], xa[3]));
-                            *reinterpret_cast<uint2*>(o2 + q * 4) = make_uint2(pack2(xb[0], xb[1]), pack2(xb[2], xb[3]));
-                        }
-                    } else if (t.epi == kEpiGate) {
-                        const float rs = sm_rs[r];
-                        __nv_bfloat16* o = p.g + (size_t)r * p.mlp + t.tile * 64 + dhalf * 32;
-#pragma unroll 1
-                        for (int q = 0; q < 8; ++q) {
-                            float4 a4, b4;
-                            tmem_ld4(ta + dhalf * 32 + q * 4, a4);
-                            tmem_ld4(ta + 64 + dhalf * 32 + q * 4, b4);
-                            *reinterpret_cast<uint2*>(o + q * 4) =
-                                make_uint2(pack2((a4.x * rs) * gelu_fast(b4.x * rs), (a4.y * rs) * gelu_fast(b4.y * rs)),
-                                           pack2((a4.z * rs) * gelu_fast(b4.z * rs), (a4.w * rs) * gelu_fast(b4.w * rs)));
                         }
                     } else if (t.epi == kEpiSilu) {
                         // ae.action_proj: silu(a W + T[step]) (the y reset ran during staging)
@@ -625,57 +599,84 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 if (tr) tr[10] = gtimer();
                 unsigned long long* trs =
                     (p.trace && threadIdx.x == 128) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
-                if (softmax) {
+                {
+                    // All 8 worker warps: two per TMEM lane quarter (rows R = 32 wq + lane); warp
+                    // `side` 0 takes key block 0 / output columns 0..127, side 1 block 1 / 128..255.
+                    const int side = (warp >= 6) ? 1 : 0;
                     const int R = wq * 32 + lane;
                     const int head = 2 * rb + (R >> 6);
                     const bool hv = head < p.heads;
                     const int nk = p.kv_rows0 + 64 - key0;  // valid keys from key0
-                    const uint32_t ts = tmem + kTS + tlane;
+                    float* xch = reinterpret_cast<float*>(sm_ml);  // [2 sides][128 rows] exchange
+                    const uint32_t ts = tmem + kTS + tlane + side * 64;
+                    const bool mine = side < nb;
+                    mbar_wait(s_full, ph);
+                    tc_fence_after();
                     float mx = -INFINITY;
 #pragma unroll 1
-                    for (int q = 0; q < nb * 8; ++q) {
+                    for (int q = 0; q < 8; ++q) {
                         float v[8];
-                        tmem_ld8(ts + q * 8, v);
+                        tmem_ld8(ts + q * 8, v);  // warp-uniform
 #pragma unroll
                         for (int e = 0; e < 8; ++e)
-                            if (q * 8 + e < nk) mx = fmaxf(mx, v[e] * p.scale_log2);
+                            if (mine && side * 64 + q * 8 + e < nk) mx = fmaxf(mx, v[e] * p.scale_log2);
                     }
+                    xch[side * 128 + R] = mx;
+                    named_bar_sync(1, kWorkers);
+                    mx = fmaxf(xch[R], xch[128 + R]);
                     float l = 0.f;
+                    if (mine) {
 #pragma unroll 1
-                    for (int q = 0; q < nb * 8; ++q) {
-                        float v[8];
-                        tmem_ld8(ts + q * 8, v);
-                        uint32_t pk[4];
+                        for (int q = 0; q < 8; ++q) {
+                            float v[8];
+                            tmem_ld8(ts + q * 8, v);
+                            uint32_t pk[4];
 #pragma unroll
-                        for (int e = 0; e < 8; e += 2) {
-                            const float e0 = q * 8 + e < nk ? ex2_fast(v[e] * p.scale_log2 - mx) : 0.f;
-                            const float e1 = q * 8 + e + 1 < nk ? ex2_fast(v[e + 1] * p.scale_log2 - mx) : 0.f;
-                            l += e0 + e1;
-                            pk[e / 2] = pack2(e0, e1);
+                            for (int e = 0; e < 8; e += 2) {
+                                const int c = side * 64 + q * 8 + e;
+                                const float e0 = c < nk ? ex2_fast(v[e] * p.scale_log2 - mx) : 0.f;
+                                const float e1 = c + 1 < nk ? ex2_fast(v[e + 1] * p.scale_log2 - mx) : 0.f;
+                                l += e0 + e1;
+                                pk[e / 2] = pack2(e0, e1);
+                            }
+                            *reinterpret_cast<uint4*>(sP + side * 16384 + swz(R, q)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                         }
-                        *reinterpret_cast<uint4*>(sP + (q >> 3) * 16384 + swz(R, q & 7)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                     }
                     fence_proxy_async_smem();
                     tc_fence_before();
-                    named_bar_sync(2, 128);
-                    if (R == 0) mbar_arrive(p_full);
+                    named_bar_sync(1, kWorkers);  // all max reads done before the sums reuse xch
+                    xch[side * 128 + R] = l;
+                    if (wtid == 0) mbar_arrive(p_full);
                     if (trs) trs[11] = gtimer();
                     mbar_wait(o_done, ph);
                     tc_fence_after();
                     if (trs) trs[12] = gtimer();
+                    l = xch[R] + xch[128 + R];
                     const float il = l > 0.f ? 1.f / l : 0.f;
-                    __nv_bfloat16* orow = p.opart + (size_t)split * 64 * p.q_width + (size_t)(R & 63) * p.q_width + head * 256;
+                    // normalised O rows (bf16) -> smem [128 rows][512 B] (Q/K/V/P are free now)
+                    uint8_t* orow_s = sQ + R * 512 + side * 256;
 #pragma unroll 1
-                    for (int q = 0; q < 32; ++q) {
+                    for (int q = 0; q < 16; ++q) {
                         float o[8];
-                        tmem_ld8(tmem + kTO + tlane + q * 8, o);
-                        if (hv)
-                            *reinterpret_cast<uint4*>(orow + q * 8) =
-                                make_uint4(pack2(o[0] * il, o[1] * il), pack2(o[2] * il, o[3] * il),
-                                           pack2(o[4] * il, o[5] * il), pack2(o[6] * il, o[7] * il));
+                        tmem_ld8(tmem + kTO + tlane + side * 128 + q * 8, o);
+                        *reinterpret_cast<uint4*>(orow_s + ((q ^ (R & 15)) << 4)) =
+                            make_uint4(pack2(o[0] * il, o[1] * il), pack2(o[2] * il, o[3] * il),
+                                       pack2(o[4] * il, o[5] * il), pack2(o[6] * il, o[7] * il));
                     }
-                    if (hv) p.ml[(size_t)split * p.heads * 64 + head * 64 + (R & 63)] = make_float2(mx, l);
+                    if (side == 0 && hv) p.ml[(size_t)split * p.heads * 64 + head * 64 + (R & 63)] = make_float2(mx, l);
                     tc_fence_before();
+                    named_bar_sync(1, kWorkers);
+                    // coalesced store: each warp writes whole 512-byte rows
+                    __nv_bfloat16* obase = p.opart + (size_t)split * 64 * p.q_width;
+#pragma unroll 1
+                    for (int e = wtid; e < 128 * 32; e += kWorkers) {
+                        const int rr = e >> 5, cc = e & 31, hd2 = 2 * rb + (rr >> 6);
+                        if (hd2 < p.heads) {
+                            const int half = cc >> 4, q16 = cc & 15;
+                            const uint4 v = *reinterpret_cast<const uint4*>(sQ + rr * 512 + half * 256 + ((q16 ^ (rr & 15)) << 4));
+                            *reinterpret_cast<uint4*>(obase + (size_t)(rr & 63) * p.q_width + hd2 * 256 + cc * 8) = v;
+                        }
+                    }
                     if (trs) trs[13] = gtimer();
                 }
                 ++aidx;
@@ -693,32 +694,96 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             // -------------------------------------------------- publish completion
             // bar.sync orders every worker's writes before lane 0's release (PTX cumulativity).
             named_bar_sync(1, kWorkers);
-            if (t.kind == kAeGemm && t.epi == kEpiRed) {
-                // Split-K: the last task of a 128-column tile finalises it: fp32 y -> bf16 yb and
-                // the rows' sums of squares (RmsStats) for the next RmsScale; only finalisers
-                // count towards the phase.
+            if (t.kind == kAeGemm && t.sig_cnt) {
+                // Split-K: the last task of a 128-column tile finalises it; only finalisers count
+                // towards the phase.  Residual: fp32 y -> bf16 yb + the rows' sums of squares
+                // (RmsStats) for the next RmsScale.  ae.qkv / ae.ffn: RmsScale + RoPE / gated GELU
+                // of the accumulated tile -> bf16, and the accumulator tile is zeroed for reuse.
                 if (wtid == 0) sm_flag[0] = atom_add_acqrel_u32(p.bars + t.omat, 1u) + 1 == t.sig_cnt;
                 named_bar_sync(1, kWorkers);
                 if (sm_flag[0]) {
-                    const int r = wtid >> 2, c0 = t.tile * 128 + (wtid & 3) * 32;
-                    const float4* yr = reinterpret_cast<const float4*>(p.y + (size_t)r * p.width + c0);
-                    float4 v[8];
+                    const int r = wtid >> 2, qd = wtid & 3;
+                    if (t.epi == kEpiRed) {
+                        const int c0 = t.tile * 128 + qd * 32;
+                        const float4* yr = reinterpret_cast<const float4*>(p.y + (size_t)r * p.width + c0);
+                        float4 v[8];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) v[j] = __ldcg(yr + j);
-                    float ss = 0.f;
-                    uint32_t pk[16];
+                        for (int j = 0; j < 8; ++j) v[j] = __ldcg(yr + j);
+                        float ss = 0.f;
+                        uint32_t pk[16];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        ss += v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w;
-                        pk[2 * j] = pack2(v[j].x, v[j].y);
-                        pk[2 * j + 1] = pack2(v[j].z, v[j].w);
+                        for (int j = 0; j < 8; ++j) {
+                            ss += v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w;
+                            pk[2 * j] = pack2(v[j].x, v[j].y);
+                            pk[2 * j + 1] = pack2(v[j].z, v[j].w);
+                        }
+                        uint4* yb4 = reinterpret_cast<uint4*>(p.yb + (size_t)r * p.width + c0);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) yb4[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+                        ss += __shfl_xor_sync(0xffffffff, ss, 1);
+                        ss += __shfl_xor_sync(0xffffffff, ss, 2);
+                        if (qd == 0) atomicAdd(p.stats + (size_t)t.aux * 64 + r, ss);
+                    } else {
+                        // thread: row r, packed pair columns c = 16 qd + j and c + 64 (j < 16)
+                        const bool qkv = t.epi == kEpiQkv;
+                        const int ld = qkv ? p.n_qkv : 2 * p.mlp;
+                        float4* acc = reinterpret_cast<float4*>((qkv ? p.qacc : p.facc) + (size_t)r * ld + t.tile * 128 + qd * 16);
+                        float4 a[4], b[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            a[j] = __ldcg(acc + j);
+                            b[j] = __ldcg(acc + 16 + j);
+                        }
+                        const float rs = 1.0f / sqrtf(__ldcg(p.stats + (size_t)t.aux * 64 + r) * p.inv_width + p.eps);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            __stcg(acc + j, make_float4(0.f, 0.f, 0.f, 0.f));
+                            __stcg(acc + 16 + j, make_float4(0.f, 0.f, 0.f, 0.f));
+                        }
+                        float xa[16], xb[16];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            xa[4 * j] = a[j].x * rs; xa[4 * j + 1] = a[j].y * rs; xa[4 * j + 2] = a[j].z * rs; xa[4 * j + 3] = a[j].w * rs;
+                            xb[4 * j] = b[j].x * rs; xb[4 * j + 1] = b[j].y * rs; xb[4 * j + 2] = b[j].z * rs; xb[4 * j + 3] = b[j].w * rs;
+                        }
+                        if (qkv) {
+                            const int f0 = t.tile * 128;
+                            const bool rope = f0 < p.rope_cols;
+                            const int hd = f0 >> 8, u = (f0 & 255) >> 7;
+                            const int w0 = u * 64 + qd * 16;
+                            __nv_bfloat16* orow = p.qkv + (size_t)r * p.n_qkv;
+                            __nv_bfloat16* o1 = rope ? orow + hd * 256 + w0 : orow + f0 + qd * 16;
+                            __nv_bfloat16* o2 = rope ? o1 + 128 : o1 + 64;
+                            if (rope) {  // pairs (j, j + 128) of the head (proj/src/tensor.cpp:150-178)
+                                const float4* csp = reinterpret_cast<const float4*>(p.rope_cs) + ((size_t)(p.rope_pos0 + r) * 128 + w0) / 2;
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) {
+                                    const float4 cs = __ldg(csp + j);
+                                    const float x0 = xa[2 * j], y0 = xb[2 * j], x1 = xa[2 * j + 1], y1 = xb[2 * j + 1];
+                                    xa[2 * j] = x0 * cs.x - y0 * cs.y;
+                                    xb[2 * j] = x0 * cs.y + y0 * cs.x;
+                                    xa[2 * j + 1] = x1 * cs.z - y1 * cs.w;
+                                    xb[2 * j + 1] = x1 * cs.w + y1 * cs.z;
+                                }
+                            }
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                reinterpret_cast<uint4*>(o1)[h] = make_uint4(pack2(xa[8 * h], xa[8 * h + 1]), pack2(xa[8 * h + 2], xa[8 * h + 3]),
+                                                                            pack2(xa[8 * h + 4], xa[8 * h + 5]), pack2(xa[8 * h + 6], xa[8 * h + 7]));
+                                reinterpret_cast<uint4*>(o2)[h] = make_uint4(pack2(xb[8 * h], xb[8 * h + 1]), pack2(xb[8 * h + 2], xb[8 * h + 3]),
+                                                                            pack2(xb[8 * h + 4], xb[8 * h + 5]), pack2(xb[8 * h + 6], xb[8 * h + 7]));
+                            }
+                        } else {  // gated FFN: up * gelu(gate), packed tile = [up 64 | gate 64]
+                            float gg[16];
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) gg[j] = xa[j] * gelu_fast(xb[j]);
+                            uint4* o = reinterpret_cast<uint4*>(p.g + (size_t)r * p.mlp + t.tile * 64 + qd * 16);
+#pragma unroll
+                            for (int h = 0; h < 2; ++h)
+                                o[h] = make_uint4(pack2(gg[8 * h], gg[8 * h + 1]), pack2(gg[8 * h + 2], gg[8 * h + 3]),
+                                                  pack2(gg[8 * h + 4], gg[8 * h + 5]), pack2(gg[8 * h + 6], gg[8 * h + 7]));
+                        }
                     }
-                    uint4* yb4 = reinterpret_cast<uint4*>(p.yb + (size_t)r * p.width + c0);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) yb4[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-                    ss += __shfl_xor_sync(0xffffffff, ss, 1);
-                    ss += __shfl_xor_sync(0xffffffff, ss, 2);
-                    if ((wtid & 3) == 0) atomicAdd(p.stats + (size_t)t.aux * 64 + r, ss);
                     named_bar_sync(1, kWorkers);
                     if (wtid == 0) atom_add_acqrel_u32(p.bars + t.sig_bar, 1u);
                 }
@@ -837,16 +902,16 @@ AePlan ae_plan(const AePlanInput& in) {
     int nstat = 0;
     // split-K residual update: tasks (tile, k-range) with a per-tile arrival counter; the last
     // arrival of a tile finalises it (yb + stats slot `slot`) and signals the phase counter.
-    auto red_phase = [&](int wmat, int xmat, uint8_t xsrc, int rowoff, int kbt, int ks, int wbar, int wcnt, int pbar,
-                         int slot) {
+    auto split_phase = [&](uint8_t epi, int tiles, int wmat, int xmat, uint8_t xsrc, int rowoff, int kbt, int ks,
+                           int wbar, int wcnt, int pbar, int slot) {
         std::vector<Item> it;
         const int per = (kbt + ks - 1) / ks;
-        for (int t = 0; t < tiles_w; ++t) {
+        for (int t = 0; t < tiles; ++t) {
             const int fin = newbar();
             for (int k = 0; k < ks; ++k) {
                 const int kb0 = k * per, nkb = std::min(kbt, kb0 + per) - kb0;
                 if (nkb <= 0) continue;
-                AeTask x = gemm(xsrc, kEpiRed, wmat, xmat, rowoff, t, kb0, nkb, wbar, wcnt, pbar);
+                AeTask x = gemm(xsrc, epi, wmat, xmat, rowoff, t, kb0, nkb, wbar, wcnt, pbar);
                 x.omat = uint16_t(fin);
                 x.aux = uint16_t(slot);
                 x.sig_cnt = uint16_t((kbt + per - 1) / per);
@@ -855,10 +920,13 @@ AePlan ae_plan(const AePlanInput& in) {
         }
         assign(it, false);
     };
+    auto red_phase = [&](int wmat, int xmat, uint8_t xsrc, int rowoff, int kbt, int ks, int wbar, int wcnt, int pbar,
+                         int slot) { split_phase(kEpiRed, tiles_w, wmat, xmat, xsrc, rowoff, kbt, ks, wbar, wcnt, pbar, slot); };
     const int ks_ao = splits_for(tiles_w, kbW, 32);
     const int ks_proj = splits_for(tiles_w, in.q_width / 64, 128);
     const int ks_down = splits_for(tiles_w, MLP / 64, 128);
     const int tiles_qkv = NQ / 128, tiles_ffn = 2 * MLP / 128;
+    const int ks_qkv = splits_for(tiles_qkv, kbW, in.num_ctas), ks_ffn = splits_for(tiles_ffn, kbW, in.num_ctas);
     const int pairs = (in.heads + 1) / 2;
     const int n_attn = pairs * splits;
     int prev_bar = bar_init, prev_cnt = W / 128;
@@ -882,18 +950,8 @@ AePlan ae_plan(const AePlanInput& in) {
         for (int l = 0; l < NA; ++l) {
             const int gl = s * NA + l;
             const int bar_qkv = newbar();
-            {
-                std::vector<Item> it;
-                for (int t = 0; t < tiles_qkv; ++t) {
-                    AeTask x = gemm(kXBf16, kEpiQkv, in.mat_wqkv[size_t(l)], in.mat_yb, 0, t, 0, kbW, prev_bar,
-                                    prev_cnt, bar_qkv);
-                    x.aux = uint16_t(slot);
-                    x.step = uint16_t(s);
-                    x.layer = uint16_t(l);
-                    it.push_back({x, kbW * kWB});
-                }
-                assign(it, false);
-            }
+            split_phase(kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], in.mat_yb, kXBf16, 0, kbW, ks_qkv, prev_bar, prev_cnt,
+                        bar_qkv, slot);
             const int bar_attn = newbar();
             {
                 std::vector<Item> it;
@@ -919,16 +977,8 @@ AePlan ae_plan(const AePlanInput& in) {
             slot = nstat++;
             red_phase(in.mat_wproj[size_t(l)], 0, kXO, 0, in.q_width / 64, ks_proj, bar_attn, n_attn, bar_proj, slot);
             const int bar_ffn = newbar();
-            {
-                std::vector<Item> it;
-                for (int t = 0; t < tiles_ffn; ++t) {
-                    AeTask x = gemm(kXBf16, kEpiGate, in.mat_wffn[size_t(l)], in.mat_yb, 0, t, 0, kbW, bar_proj,
-                                    tiles_w, bar_ffn);
-                    x.aux = uint16_t(slot);
-                    it.push_back({x, kbW * kWB});
-                }
-                assign(it, false);
-            }
+            split_phase(kEpiGate, tiles_ffn, in.mat_wffn[size_t(l)], in.mat_yb, kXBf16, 0, kbW, ks_ffn, bar_proj, tiles_w,
+                        bar_ffn, slot);
             const int bar_down = newbar();
             slot = nstat++;
             red_phase(in.mat_wdown[size_t(l)], in.mat_g, kXBf16, 0, MLP / 64, ks_down, bar_ffn, tiles_ffn, bar_down, slot);

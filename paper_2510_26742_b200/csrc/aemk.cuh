@@ -80,6 +80,8 @@ struct AeParams {
     const float* state;            // [state_dim] fp32
     float* st;                     // [W] state token (ae.state_proj output)
     __nv_bfloat16* qkv;            // [64, n_qkv]
+    float* qacc;                   // [64, n_qkv]   split-K accumulator of ae.qkv (packed columns)
+    float* facc;                   // [64, 2 * mlp] split-K accumulator of ae.ffn (packed columns)
     __nv_bfloat16* ap;             // [C, W]
     __nv_bfloat16* g;              // [64, mlp]
     __nv_bfloat16* opart;          // [splits][64, q_width] normalised attention partials

@@ -1131,7 +1131,9 @@ void Engine::build_ae_mega() {
     }
     // zero-on-entry region: phase / tile counters | row-statistics slots
     const size_t bar_bytes = size_t(round_up(ae_plan_.n_bars * 4, 256));
-    ae_zero_bytes_ = bar_bytes + size_t(ae_plan_.n_stats) * 64 * 4;
+    const size_t stat_bytes = size_t(round_up(ae_plan_.n_stats * 64 * 4, 256));
+    const size_t qacc_bytes = size_t(64) * NQ * 4, facc_bytes = size_t(64) * 2 * MLP * 4;
+    ae_zero_bytes_ = bar_bytes + stat_bytes + qacc_bytes + facc_bytes;
     uint8_t* z = alloc<uint8_t>(ae_zero_bytes_);
     ae_zero_ = z;
     __nv_bfloat16* opart = alloc<__nv_bfloat16>(size_t(ae_plan_.attn_splits) * 64 * ae_q_);
@@ -1160,6 +1162,8 @@ void Engine::build_ae_mega() {
     P.y = y_;
     P.yb = yb;
     P.stats = reinterpret_cast<float*>(z + bar_bytes);
+    P.qacc = reinterpret_cast<float*>(z + bar_bytes + stat_bytes);
+    P.facc = reinterpret_cast<float*>(z + bar_bytes + stat_bytes + qacc_bytes);
     P.a = a_;
     P.lda = act_ld_;
     P.state = state32_;

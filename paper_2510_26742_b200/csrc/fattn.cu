@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
     uint64_t* o_done = p_full + 1;      // [1]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
 
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = __shfl_sync(0xffffffff, tid >> 5, 0), lane = tid & 31;
     const int qt = blockIdx.x, grp = blockIdx.z;
     const int hpg = p.heads / p.kv_heads;
     const int grows = hpg * p.q_rows;
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
         __syncwarp();
     } else if (warp == 4) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        {  // warp-uniform loop; one elected lane issues (see gemm.cu)
             constexpr uint32_t idesc_qk = umma_idesc_bf16(kFaRows, kFaKeys);
             constexpr uint32_t idesc_pv = umma_idesc_bf16(kFaRows, DV) | (1u << 16);  // B (V) MN-major
             const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK), v0 = smem_u32(sV), p0 = smem_u32(sP);
@@ -194,10 +194,13 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                 for (int kk = 0; kk < DK / 16; ++kk) {
                     const uint64_t a = desc_kmajor(q0 + (kk >> 2) * (kFaRows * 128) + (kk & 3) * 32);
                     const uint64_t b = desc_kmajor(k0 + st * C::K_BYTES + (kk >> 2) * (kFaKeys * 128) + (kk & 3) * 32);
-                    umma_bf16(tmem + C::TMEM_S + sb * 64, a, b, idesc_qk, kk > 0);
+                    if (elect_one()) umma_bf16(tmem + C::TMEM_S + sb * 64, a, b, idesc_qk, kk > 0);
                 }
-                umma_commit(&s_full[sb]);
-                umma_commit(&k_empty[st]);
+                if (elect_one()) {
+                    umma_commit(&s_full[sb]);
+                    umma_commit(&k_empty[st]);
+                }
+                __syncwarp();
             };
             issue_qk(0);
             for (int t = 0; t < ntiles; ++t) {
@@ -210,10 +213,13 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                 for (int kk = 0; kk < kFaKeys / 16; ++kk) {
                     const uint64_t a = desc_kmajor(p0 + kk * 32);
                     const uint64_t b = desc_mnmajor(v0 + sv * C::V_BYTES + kk * 2048, kFaKeys * 128);
-                    umma_bf16(tmem + C::TMEM_O, a, b, idesc_pv, (t | kk) > 0);
+                    if (elect_one()) umma_bf16(tmem + C::TMEM_O, a, b, idesc_pv, (t | kk) > 0);
                 }
-                umma_commit(o_done);
-                umma_commit(&v_empty[sv]);
+                if (elect_one()) {
+                    umma_commit(o_done);
+                    umma_commit(&v_empty[sv]);
+                }
+                __syncwarp();
             }
         }
         __syncwarp();

@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
     float* sm_vec = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::BAR_BYTES);
 
-    const int warp = threadIdx.x >> 5;
+    const int warp = __shfl_sync(0xffffffff, int(threadIdx.x >> 5), 0);  // warp-uniform (see below)
     const int lane = threadIdx.x & 31;
     const int m_tile = blockIdx.x, n_tile = blockIdx.y, split = blockIdx.z;
     const int KB = (p.K + BK - 1) / BK;
@@ -170,7 +170,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        // Warp-uniform loop, one elected lane issues: tcgen05.mma from a divergent single-lane
+        // branch costs ~270 instead of ~128 issue cycles per N=256 MMA (scripts/mma_bench.cu).
+        {
             constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
             for (int i = 0; i < nkb; ++i) {
                 const int s = i % STAGES;
@@ -179,12 +181,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 tc_fence_after();
                 const uint64_t ad = umma_desc_sw128(sA + s * Cfg::A_BYTES);
                 const uint64_t bd = umma_desc_sw128(sB + s * Cfg::B_BYTES);
+                if (elect_one()) {
 #pragma unroll
-                for (int k = 0; k < BK / 16; ++k)
-                    umma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0);
-                umma_commit(&empty[s]);
+                    for (int k = 0; k < BK / 16; ++k)
+                        umma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0);
+                    umma_commit(&empty[s]);
+                }
+                __syncwarp();
             }
-            umma_commit(accum_full);
+            if (elect_one()) umma_commit(accum_full);
         }
         __syncwarp();
     } else {

@@ -42,6 +42,18 @@ __global__ void __launch_bounds__(256, 1) red_kernel(const __grid_constant__ CUt
         for (int j = 0; j < 8; ++j) red_add_v4_f32(dst + 4 * j, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         __threadfence();
         __syncthreads();
+    } else if (mode == 4 || mode == 5) {
+        // coalesced: warp w -> rows 8w..8w+7, lane -> 4 consecutive columns (512 B per row)
+        const int w = tid >> 5, lane = tid & 31;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float* dst = (mode == 4 ? target + (8 * w + i) * 1024 + tile * 128
+                                    : ws + (size_t)blockIdx.x * 8192 + (8 * w + i) * 128) + lane * 4;
+            if (mode == 4) red_add_v4_f32(dst, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            else *reinterpret_cast<float4*>(dst) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+        __threadfence();
+        __syncthreads();
     } else if (mode == 1 || mode == 2) {
         if (mode == 1) {
             uint8_t* box = smem + q * 8192 + r * 128;
@@ -103,8 +115,9 @@ int main() {
     cudaMalloc(&out, 148 * 8);
     int clk;
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-    const char* names[] = {"red.v4 from registers", "TMA reduce 4x8KB SW128", "TMA reduce 1x32KB", "plain st.v4 (no add)"};
-    for (int mode = 0; mode < 4; ++mode)
+    const char* names[] = {"red.v4 from registers", "TMA reduce 4x8KB SW128", "TMA reduce 1x32KB", "plain st.v4 (no add)",
+                           "red.v4 coalesced", "st.v4 coalesced"};
+    for (int mode = 0; mode < 6; ++mode)
         for (int n : {8, 32, 128, 148}) {
             double best = 1e30, med = 0;
             for (int rep = 0; rep < 3; ++rep) {
