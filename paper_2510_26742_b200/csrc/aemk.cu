@@ -46,8 +46,8 @@ constexpr int kXTile = 64 * 128;      // 8 KB: 64 activation rows x 64 k
 constexpr int kFSt = 5;
 constexpr int kFTile = 16384;         // fp32 staging of one k-block: two SW128 boxes of 32 columns
 constexpr int kOSt = 2;
-constexpr int kMaxSplits = 5;         // attention key ranges combined by the ae.proj staging
-constexpr int kOTile = kMaxSplits * 8192;
+constexpr int kMaxSplits = 10;        // attention key ranges combined by the ae.proj staging
+constexpr int kORegion = 81920;       // partial staging: 2 slots of <= 5 ranges, or 1 slot of <= 10
 constexpr int kBlocksPerSplit = 2;    // 64-key blocks per attention task
 constexpr int kOffW = 0;
 constexpr int kOffU = kWSt * kWTile;                // union region (128 KB)
@@ -59,9 +59,9 @@ constexpr int kOffK = kOffU + 65536;                // ATTN: K [2 blocks][64 x 2
 constexpr int kOffP = kOffQ;                        // ATTN: P [128 x 128 keys] (reuses Q)
 constexpr int kOffV = kOffK;                        // ATTN: V (reuses K)
 constexpr int kOffAux = kOffU + kUnion;
-constexpr int kAuxBytes = 8192;
+constexpr int kAuxBytes = 16384;
 constexpr int kAeSmem = kOffAux + kAuxBytes + 1024;
-static_assert(kOffF + kFSt * kFTile <= kOffAux && kOffF + kOSt * kOTile <= kOffAux, "GEMM union overflow");
+static_assert(kOffF + kORegion <= kOffAux, "GEMM union overflow");
 static_assert(kAeSmem <= 232448, "shared memory budget");
 
 constexpr uint32_t kTAcc = 0, kTS = 0, kTO = 256;  // TMEM columns (512 allocated)
@@ -174,8 +174,8 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
     uint64_t* o_done = mb + kBODone;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffAux + 512);
     float* sm_rs = reinterpret_cast<float*>(smem + kOffAux + 1024);     // [64]
-    float2* sm_ml = reinterpret_cast<float2*>(smem + kOffAux + 2048);   // [kOSt][kMaxSplits][64]
-    float* sm_vec = reinterpret_cast<float*>(smem + kOffAux + 7168);    // [128] epilogue vector
+    float2* sm_ml = reinterpret_cast<float2*>(smem + kOffAux + 2048);   // [2][kMaxSplits][64]
+    float* sm_vec = reinterpret_cast<float*>(smem + kOffAux + 12288);   // [128] epilogue vector
     volatile int* sm_flag = reinterpret_cast<volatile int*>(smem + kOffAux + 768);
 
     // warp index through a shuffle: provably warp-uniform, so role branches stay converged and the
@@ -376,9 +376,11 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     // o = sum_j l_j 2^(m_j - M) O_j / sum_j l_j 2^(m_j - M); each thread loads and
                     // combines its own 16 columns of its own row (no block barrier).
                     const int ns = p.attn_splits;
+                    const int oslots = ns <= kMaxSplits / 2 ? 2 : 1;
+                    const int otile = kORegion / oslots;
                     auto issue_o = [&](int k, int slot) {
                         const int kc = (t.kb0 + k) * 64, head = kc >> 8;
-                        uint8_t* base = sF + slot * kOTile;
+                        uint8_t* base = sF + slot * otile;
                         for (int j = 0; j < ns; ++j) {
                             const __nv_bfloat16* ob = p.opart + (size_t)j * 64 * p.q_width + (size_t)sr * p.q_width + kc;
                             cp_async16(base + j * 8192 + swz(sr, 2 * sq), ob + 16 * sq, true);
@@ -389,11 +391,11 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                                 cp_async8(sm_ml + (slot * kMaxSplits + j) * 64 + sr, p.ml + (size_t)j * p.heads * 64 + head * 64 + sr);
                         cp_async_commit();
                     };
-                    const int pre = min(t.nkb, kOSt);
+                    const int pre = min(t.nkb, oslots);
                     for (int k = 0; k < pre; ++k) issue_o(k, k);
                     for (int k = 0; k < t.nkb; ++k) {
-                        const int slot = k % kOSt;
-                        if (min(kOSt, t.nkb - k) == 2) cp_async_wait<1>(); else cp_async_wait<0>();
+                        const int slot = k % oslots;
+                        if (min(oslots, t.nkb - k) == 2) cp_async_wait<1>(); else cp_async_wait<0>();
                         __syncwarp();  // (m, l) were fetched by the row's sq == 0 lane
                         mbar_wait(&x_empty[xs], xph ^ 1);
                         const float2* ml = sm_ml + slot * kMaxSplits * 64;
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                             const float2 mlj = ml[j * 64 + sr];
                             const float w = mlj.y * ex2_fast(mlj.x - M);
                             wsum += w;
-                            const uint8_t* src = sF + slot * kOTile + j * 8192;
+                            const uint8_t* src = sF + slot * otile + j * 8192;
 #pragma unroll
                             for (int h2 = 0; h2 < 2; ++h2) {
                                 const uint4 u4 = *reinterpret_cast<const uint4*>(src + swz(sr, 2 * sq + h2));
@@ -429,7 +431,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         fence_proxy_async_smem();
                         mbar_arrive(&x_full[xs]);
                         __syncwarp();  // the row's (m, l) slot is refilled by lane sq == 0 below
-                        if (k + kOSt < t.nkb) issue_o(k + kOSt, slot);
+                        if (k + oslots < t.nkb) issue_o(k + oslots, slot);
                         adv(xs, xph, 1, kXSt);
                     }
                 } else {  // kXRows: Euler state (ae.action_proj) or robot state (ae.state_proj), K <= 64
