@@ -35,6 +35,9 @@ def build(quiet: bool = True) -> None:
     targets = ["port"]
     if os.path.isdir(REFERENCE_SRC):
         targets.append("ref")
+        # the C++ drop-in demo (include/pi0b_rtvla.hpp over libpi0b.so, reference types)
+        if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_2510_26742_b200", "libpi0b.so")):
+            targets.append("demo")
     out = subprocess.run(["make", "-C", HERE, "-j8", *targets], capture_output=True, text=True)
     if out.returncode != 0:
         raise RuntimeError("oracle build failed:\n" + out.stdout[-4000:] + out.stderr[-4000:])

@@ -132,7 +132,8 @@ EXPORTED_SYMBOLS = [
     "pi0b_default_config", "pi0b_engine_create", "pi0b_engine_destroy", "pi0b_engine_gen_weights",
     "pi0b_engine_set_weight", "pi0b_engine_set_bias_table", "pi0b_engine_run", "pi0b_engine_run_prefix",
     "pi0b_engine_run_action", "pi0b_engine_replay", "pi0b_engine_sync", "pi0b_engine_kernel_count",
-    "pi0b_engine_read_checkpoint", "pi0b_engine_time_node", "pi0b_engine_describe", "pi0b_last_error", "pi0b_gemm", "pi0b_gemm_skinny", "pi0b_attention",
+    "pi0b_engine_read_checkpoint", "pi0b_engine_time_node", "pi0b_engine_describe", "pi0b_engine_ae_trace",
+    "pi0b_last_error", "pi0b_gemm", "pi0b_gemm_skinny", "pi0b_attention",
     "pi0b_attention_ws_floats", "pi0b_random_f64", "pi0b_random_packed_bf16", "pi0b_seed_hash",
 ]
 

@@ -66,3 +66,21 @@ def test_engine_create_fails_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(Exception):
         E.Engine(C.mid_config())
+
+
+
+def test_cpp_dropin_fails_loudly_without_gpu():
+    """The C++ drop-in (include/pi0b_rtvla.hpp) over the reference's types builds and, with no
+    sm_100 device, throws instead of falling back to the CPU."""
+    import subprocess
+    demo = os.path.join(ROOT, "oracle", "_ref", "pi0b_rtvla_demo")
+    if not os.path.exists(demo):
+        pytest.skip("demo not built (needs /root/reference)")
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("GPU present: covered by tests/test_gpu_engine.py::test_rtvla_cpp_dropin")
+    except ImportError:
+        pass
+    r = subprocess.run([demo, "1", "0"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 2 and "pi0b error" in r.stdout, r.stdout + r.stderr

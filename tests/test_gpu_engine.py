@@ -183,3 +183,19 @@ def test_full_scale_actions_match_reference_golden(views):
     rep = _action_report(y, ref)
     print(f"full {views}v actions", rep)
     assert rep["max_abs"] < ACT_MAX_ABS and rep["rel"] < ACT_REL and rep["cos"] > 0.9995, rep
+
+
+DEMO = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "pi0b_rtvla_demo")
+
+
+@pytest.mark.parametrize("views,prompt", [(1, 0), (3, 32)])
+def test_rtvla_cpp_dropin(views, prompt):
+    """include/pi0b_rtvla.hpp with the reference's own C++ types: pi0b::evaluate(g, w, x) and
+    pi0b::Engine vs rtvla::evaluate (fp64, compiled from the reference) on the same graph,
+    WeightStore and Inputs; a non-pi0 graph is rejected with rtvla::ShapeError."""
+    import subprocess
+    if not os.path.exists(DEMO):
+        pytest.skip("oracle/_ref/pi0b_rtvla_demo not built (needs /root/reference at build time)")
+    r = subprocess.run([DEMO, str(views), str(prompt)], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
