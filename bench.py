@@ -109,7 +109,7 @@ def run_ours(args) -> None:
     from paper_2510_26742_b200 import engine as E
     from paper_2510_26742_b200.config import default_config
     from paper_2510_26742_b200.inputs import gen_inputs
-    from paper_2510_26742_b200.roofline import lower_bound_ms, measured_peaks, totals
+    from paper_2510_26742_b200.roofline import ae_weight_bytes, kv_cache_bytes, lower_bound_ms, measured_peaks, totals
 
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
@@ -161,16 +161,22 @@ def run_ours(args) -> None:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         p50, p90, mean, e2e_p50 = [float(v) for v in t.tolist()]
 
-    # dominant kernel: the LLM fused gated FFN GEMM (41% of all FLOPs), timed alone
+    # Dominant kernel: the action-expert megakernel (one launch = all 10 flow steps; HBM-bound on
+    # the weight stream).  Algorithmic bytes per launch = every AE weight byte once per flow step
+    # + the LLM K/V cache it reads; timed alone with CUDA events on the engine stream.
     peaks = measured_peaks()
-    ffn_ms, launches = eng.time_node("llm.ffn", reps=3)
-    L = cfg.prefix_tokens
-    ffn_flops = 2.0 * L * cfg.llm_width * 2 * cfg.llm_mlp
-    achieved = ffn_flops / (ffn_ms * 1e-3) / 1e12
+    ae_ms, _ = eng.time_node("ae.mega", reps=3)
+    ae_bytes = ae_weight_bytes(cfg) * cfg.flow_steps + kv_cache_bytes(cfg) * cfg.flow_steps
+    ae_gbs = ae_bytes / (ae_ms * 1e-3) / 1e9
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_llm_ffn.json")
+    prof = os.path.join(ROOT, "profiles", "ncu_ae_mega.json")
     if os.path.exists(prof):
         traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+    # secondary: the LLM fused gated FFN GEMM (41% of all FLOPs), tensor-bound
+    ffn_ms, _ = eng.time_node("llm.ffn", reps=3)
+    L = cfg.prefix_tokens
+    ffn_flops = 2.0 * L * cfg.llm_width * 2 * cfg.llm_mlp
+    ffn_tf = ffn_flops / (ffn_ms * 1e-3) / 1e12
     lb = lower_bound_ms(cfg)
     tot = totals(cfg)
     n_kernels = eng.kernel_count(0)
@@ -191,11 +197,15 @@ def run_ours(args) -> None:
                 "d2h_bytes_per_step": int(y.nbytes)},
         "gpu_launches": n_kernels * args.steps,
         "gpu_launches_per_step": n_kernels,
-        "roofline": {"bound": "tensor", "kernel": "llm.ffn fused gated GEMM (tcgen05)",
-                     "achieved": round(achieved, 1), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                     "frac": round(achieved / peaks["bf16_tflops"], 4), "traffic": traffic,
-                     "flops_per_launch": ffn_flops, "ms_per_launch": round(ffn_ms, 5),
-                     "peak_source": peaks["source"] + " burst"},
+        "roofline": {"bound": "hbm", "kernel": "action-expert megakernel (aemk_kernel, 1 launch = 10 flow steps)",
+                     "achieved": round(ae_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": round(ae_gbs / peaks["hbm_gbs"], 4), "traffic": traffic,
+                     "bytes_per_launch": ae_bytes, "ms_per_launch": round(ae_ms, 4),
+                     "share_of_step": round(ae_ms / mean, 3), "peak_source": peaks["source"] + " copy bandwidth"},
+        "roofline_prefill_gemm": {"bound": "tensor", "kernel": "llm.ffn fused gated GEMM (tcgen05)",
+                                  "achieved": round(ffn_tf, 1), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                                  "frac": round(ffn_tf / peaks["bf16_tflops"], 4), "flops_per_launch": ffn_flops,
+                                  "ms_per_launch": round(ffn_ms, 5), "peak_source": peaks["source"] + " burst"},
         "step_roofline": {"method": "reference lower bound sum max(2KM/BW, NKM/MAC) (costmodel.cpp:82-92)",
                           "lower_bound_ms": round(lb["total"], 4), "frac": round(lb["total"] / p50, 4),
                           "stages_ms": {k: round(v, 4) for k, v in lb.items() if k != "total"},

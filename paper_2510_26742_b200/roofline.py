@@ -112,3 +112,18 @@ def totals(c: ModelConfig) -> dict:
     unique = sum(g.weight_bytes * (1 if g.node.startswith("ae.") and g.node not in ("ae.qkv", "ae.proj",
                  "ae.ffn", "ae.down") else g.repeat) for g in gemms(c))
     return {"flops": flops, "weight_bytes_streamed": wbytes, "weight_bytes_unique": unique}
+
+
+def ae_weight_bytes(c: ModelConfig) -> int:
+    """bf16 bytes of every action-expert weight the megakernel streams once per flow step:
+    18 x (qkv + proj + ffn + down) + action_proj + action_out + head (state_proj once per launch
+    is included here too; it is 64 KB)."""
+    W, A = c.ae_width, c.ae_action_dim
+    nq = (c.ae_q_heads + 2 * c.ae_kv_heads) * c.ae_head_dim
+    layer = W * nq + c.ae_q_heads * c.ae_head_dim * W + W * 2 * c.ae_mlp + c.ae_mlp * W
+    return 2 * (c.ae_layers * layer + A * W + W * W + W * A)
+
+
+def kv_cache_bytes(c: ModelConfig) -> int:
+    """bf16 bytes of the LLM K and V rows the action expert attends to, per flow step."""
+    return 2 * 2 * c.prefix_tokens * c.llm_kv_heads * c.llm_head_dim * c.ae_layers
