@@ -121,7 +121,8 @@ typedef struct pi0b_gemm_desc {
     const void* w; int64_t ldw;     /* bf16 [N, K] (packed weight)                  */
     int M, N, K;
     int bn;                         /* tile width 64 / 128 / 256                    */
-    int splits;                     /* split-K factor (>= 1)                        */
+    int splits;                     /* split-K factor, clamped to [1, 8]: the splits of
+                                       a tile run as one cluster, reduced over DSMEM  */
     int mode, flags;                /* see paper_2510_26742_b200/csrc/gemm.cuh      */
     const float* row_stats; float inv_width, eps;
     const float* bias;
@@ -132,7 +133,7 @@ typedef struct pi0b_gemm_desc {
     void* outb; int64_t ldob;
     float* out_stats;
     const float* row0_src;
-    float* ws; int* counters;       /* split-K scratch, zero-initialised            */
+    float* ws; int* counters;       /* reserved (ignored; kept for ABI stability)   */
 } pi0b_gemm_desc;
 int pi0b_gemm(const pi0b_gemm_desc* d, void* stream);
 /* Swap-AB small-M GEMM (M <= 64; the action expert's weight-streaming kernel): `w` is the

@@ -703,6 +703,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 // of the accumulated tile -> bf16, and the accumulator tile is zeroed for reuse.
                 if (wtid == 0) sm_flag[0] = atom_add_acqrel_u32(p.bars + t.omat, 1u) + 1 == t.sig_cnt;
                 named_bar_sync(1, kWorkers);
+                if (tr) tr[11] = gtimer();
                 if (sm_flag[0]) {
                     const int r = wtid >> 2, qd = wtid & 3;
                     if (t.epi == kEpiRed) {
@@ -711,6 +712,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         float4 v[8];
 #pragma unroll
                         for (int j = 0; j < 8; ++j) v[j] = __ldcg(yr + j);
+                        if (tr) tr[12] = gtimer() + (unsigned long long)(v[0].x == 12345.f);
                         float ss = 0.f;
                         uint32_t pk[16];
 #pragma unroll
@@ -737,6 +739,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                             b[j] = __ldcg(acc + 16 + j);
                         }
                         const float rs = 1.0f / sqrtf(__ldcg(p.stats + (size_t)t.aux * 64 + r) * p.inv_width + p.eps);
+                        if (tr) tr[12] = gtimer() + (unsigned long long)(a[0].x + b[3].w + rs == 12345.f);
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
                             __stcg(acc + j, make_float4(0.f, 0.f, 0.f, 0.f));
@@ -787,6 +790,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         }
                     }
                     named_bar_sync(1, kWorkers);
+                    if (tr) tr[13] = gtimer();
                     if (wtid == 0) atom_add_acqrel_u32(p.bars + t.sig_bar, 1u);
                 }
             } else if (wtid == 0) {

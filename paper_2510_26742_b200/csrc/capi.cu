@@ -78,8 +78,6 @@ static pi0b::GemmParams params_of(const pi0b_gemm_desc* d) {
     p.ldob = d->ldob;
     p.out_stats = d->out_stats;
     p.row0_src = d->row0_src;
-    p.ws = d->ws;
-    p.counters = d->counters;
     p.splits = 1;
     p.kb_per_split = (d->K + 63) / 64;
     return p;
@@ -109,7 +107,7 @@ int pi0b_gemm(const pi0b_gemm_desc* d, void* stream) {
         p.N = d->N;
         p.K = d->K;
         const int kb = (d->K + 63) / 64;
-        const int s = std::max(1, std::min(d->splits, kb));
+        const int s = std::max(1, std::min({d->splits, kb, kGemmMaxSplits}));
         p.kb_per_split = (kb + s - 1) / s;
         p.splits = (kb + p.kb_per_split - 1) / p.kb_per_split;
         p.mode = d->mode;
@@ -129,8 +127,6 @@ int pi0b_gemm(const pi0b_gemm_desc* d, void* stream) {
         p.ldob = d->ldob;
         p.out_stats = d->out_stats;
         p.row0_src = d->row0_src;
-        p.ws = d->ws;
-        p.counters = d->counters;
         CUtensorMap ta = make_tmap_bf16(d->a, d->M, d->K, d->lda, 128);
         CUtensorMap tb = make_tmap_bf16(d->w, d->N, d->K, d->ldw, d->bn);
         return int(launch_gemm(d->bn, ta, tb, p, static_cast<cudaStream_t>(stream)));

@@ -45,6 +45,7 @@ struct FaMaps {
 cudaError_t fattn_configure();
 FaMaps make_fattn_maps(const AttnParams& p, int head_dim);
 cudaError_t launch_fattn(int head_dim, const FaMaps& maps, const AttnParams& p, cudaStream_t stream);
+void fattn_set_pdl(bool on);
 cudaError_t launch_gen_weight(__nv_bfloat16* dst, long long ldk, int k, int m, int perm, int rope_cols,
                               uint64_t seed, double lo, double hi, cudaStream_t st);
 cudaError_t launch_pack_weight(__nv_bfloat16* dst, long long ldk, const double* w, int k, int m,
@@ -172,14 +173,23 @@ static int env_int(const char* name, int dflt) {
     return v ? atoi(v) : dflt;
 }
 
-static int choose_splits(int m_tiles, int n_tiles, int K, int num_sms) {
+int gemm_max_active_clusters(int bn, int splits);
+void gemm_set_pdl(bool on);
+
+// K-split factor of a prefill GEMM: the splits of a tile run as one cluster (reduced over
+// DSMEM), so all tiles x splits CTAs must be co-resident -- clusters are confined to a GPC,
+// which the occupancy query accounts for.
+static int choose_splits(int m_tiles, int n_tiles, int K, int bn, int num_sms) {
     const int ctas = m_tiles * n_tiles;
     const int kb = (K + 63) / 64;
     if (ctas * 2 > num_sms) return 1;
-    int s = std::max(1, std::min(num_sms / ctas, kb));
-    s = std::min(s, env_int("PI0B_MAX_SPLITS", 1 << 20));
-    const int per = (kb + s - 1) / s;
-    return (kb + per - 1) / per;
+    int s = std::min({num_sms / ctas, kb / 2, kGemmMaxSplits, env_int("PI0B_MAX_SPLITS", kGemmMaxSplits)});
+    for (; s > 1; --s) {
+        const int per = (kb + s - 1) / s;
+        if ((kb + per - 1) / per != s) continue;  // every split must own k-blocks
+        if (gemm_max_active_clusters(bn, s) >= ctas) break;
+    }
+    return std::max(s, 1);
 }
 
 // ------------------------------------------------------------------ plan records
@@ -326,9 +336,6 @@ private:
                   *aqkv_ = nullptr, *ao_ = nullptr, *ag_ = nullptr;
     float *st_ = nullptr, *y_ = nullptr, *a_ = nullptr;
     float* rope_cs_ = nullptr;
-    float* gemm_ws_ = nullptr;
-    int* gemm_ctr_ = nullptr;
-    size_t gemm_ws_floats_ = 0;
     float* stats_[2] = {nullptr, nullptr};
     int stats_rows_ = 0, stats_used_[2] = {0, 0}, stats_cap_[2] = {0, 0};
 
@@ -367,6 +374,8 @@ Engine::Engine(const pi0b_model_config& cfg, const pi0b_engine_options& opt) : c
                                                   std::to_string(prop.major * 10 + prop.minor));
     num_sms_ = prop.multiProcessorCount;
     pdl_ = env_int("PI0B_PDL", 1) != 0;
+    gemm_set_pdl(pdl_);
+    fattn_set_pdl(pdl_);
     PI0B_CUDA(gemm_configure());
     PI0B_CUDA(fattn_configure());
     PI0B_CUDA(skinny_configure());
@@ -571,13 +580,9 @@ void Engine::add_gemm(int part, const std::string& node, int inst, const __nv_bf
     gp.K = K;
     const int m_tiles = (M + 127) / 128, n_tiles = (N + bn - 1) / bn;
     const int kb = (K + 63) / 64;
-    int splits = allow_split ? choose_splits(m_tiles, n_tiles, K, num_sms_) : 1;
+    int splits = allow_split ? choose_splits(m_tiles, n_tiles, K, bn, num_sms_) : 1;
     gp.kb_per_split = (kb + splits - 1) / splits;
     gp.splits = (kb + gp.kb_per_split - 1) / gp.kb_per_split;
-    if (gp.splits > 1 && gp.mode != kModeResid) {
-        gemm_ws_floats_ = std::max(gemm_ws_floats_, size_t(M) * N);
-        gp.ws = nullptr;  // patched after allocation
-    }
     op.gp = gp;
     ops_.push_back(op);
 }
@@ -1050,17 +1055,6 @@ void Engine::build_plan() {
         ops_.push_back(o);
     }
 
-    // scratch shared by all launches (stream-ordered, self-cleaning)
-    gemm_ws_ = alloc<float>(std::max<size_t>(gemm_ws_floats_, 1));
-    PI0B_CUDA(cudaMemsetAsync(gemm_ws_, 0, std::max<size_t>(gemm_ws_floats_, 1) * 4, stream_));
-    gemm_ctr_ = alloc<int>(4096);
-    PI0B_CUDA(cudaMemsetAsync(gemm_ctr_, 0, 4096 * 4, stream_));
-    for (auto& op : ops_) {
-        if (op.kind == kOpGemm) {
-            op.gp.ws = gemm_ws_;
-            op.gp.counters = gemm_ctr_;
-        }
-    }
 }
 
 // ------------------------------------------------------------------ action-expert megakernel

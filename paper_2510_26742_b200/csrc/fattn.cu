@@ -133,6 +133,8 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
         fence_barrier_init();
     }
     if (warp == 4) tmem_alloc(tmem_slot, C::TMEM_COLS);
+    if (tid == 0) pdl_launch_dependents();
+    pdl_wait();  // every input (Q, K, V) is the previous kernel's output
     if (warp < 4) {
         // Q: thread r stages its own stacked row (DK/8 chunks) into the swizzled layout
         const int r = tid, g = qt * kFaRows + r;
@@ -347,21 +349,34 @@ FaMaps make_fattn_maps(const AttnParams& p, int head_dim) {
     return m;
 }
 
+static bool g_fa_pdl = true;
+void fattn_set_pdl(bool on) { g_fa_pdl = on; }
+
+template <int D, int DK, int DV, int KK, int KV>
+static cudaError_t fa_launch_t(const FaMaps& maps, const AttnParams& p, dim3 grid, cudaStream_t stream) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kFaThreads, 1, 1);
+    cfg.dynamicSmemBytes = FaCfg<D, DK, DV, KK, KV>::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_fa_pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, fattn_kernel<D, DK, DV, KK, KV>, maps, p);
+}
+
 // Single pass over all keys; grid = (stacked q tiles of 128, 1, kv groups).
 cudaError_t launch_fattn(int head_dim, const FaMaps& maps, const AttnParams& p, cudaStream_t stream) {
     const int grows = (p.heads / p.kv_heads) * p.q_rows;
     const dim3 grid((grows + kFaRows - 1) / kFaRows, 1, p.kv_heads);
     if ((p.rows0 % 32) || (p.rows1 % 32)) return cudaErrorInvalidValue;
     switch (head_dim) {
-        case 72:
-            fattn_kernel<72, 80, 128, 3, 3><<<grid, kFaThreads, FaCfg<72, 80, 128, 3, 3>::SMEM, stream>>>(maps, p);
-            break;
-        case 256:
-            fattn_kernel<256, 256, 256, 2, 2><<<grid, kFaThreads, FaCfg<256, 256, 256, 2, 2>::SMEM, stream>>>(maps, p);
-            break;
+        case 72: return fa_launch_t<72, 80, 128, 3, 3>(maps, p, grid, stream);
+        case 256: return fa_launch_t<256, 256, 256, 2, 2>(maps, p, grid, stream);
         default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
 }
 
 }  // namespace pi0b

@@ -12,9 +12,12 @@
 //   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> registers -> fused scalar ops ->
 //               global (bf16 rows, or the fp32 residual stream + bf16 shadow + row
 //               sum-of-squares for the next RmsScale).
-// Split-K: partials are reduced with red.global.add.f32 (into the residual stream
-// itself for kModeResid, else into a self-cleaning fp32 workspace); the last CTA of
-// a tile (arrival counter) runs the epilogue.
+// Split-K: grid.z = the K-splits of a tile, launched as ONE thread-block cluster; after the
+// mainloop each CTA parks the fp32 partials of the 32-column chunks it does not own in its own
+// (now idle) pipeline shared memory, and the owner of each chunk pulls the peers' partials over
+// DSMEM and runs the epilogue -- no global workspace, no atomics, no second pass.
+// PDL: the next launch's prologue and first weight tiles overlap this kernel's tail
+// (griddepcontrol.wait guards every read of the previous kernel's outputs).
 #include "gemm.cuh"
 #include "ptx.cuh"
 
@@ -23,6 +26,7 @@ namespace pi0b {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kGemmThreads = 64 + 8 * 32;  // TMA warp, MMA warp, 8 epilogue warps
+static bool g_gemm_pdl = true;             // launch with programmatic stream serialization
 
 template <int BN, int STAGES>
 struct GemmCfg {
@@ -78,28 +82,8 @@ PI0B_DEV void load_f32x32(const float* src, float (&v)[32], int nvalid, bool cg)
     }
 }
 
-// Read 32 fp32 split-K partial sums of one row from the workspace and clear them.
-PI0B_DEV void ws_take32(float* src, float (&v)[32], int nvalid) {
-    load_f32x32(src, v, nvalid, true);
-    if (nvalid >= 32) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) __stcg(reinterpret_cast<float4*>(src + j), make_float4(0.f, 0.f, 0.f, 0.f));
-    } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-            if (j < nvalid) __stcg(src + j, 0.f);
-    }
-}
-
-PI0B_DEV void ws_add32(float* dst, const float (&v)[32], int nvalid) {
-    if (nvalid >= 32) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) red_add_v4_f32(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
-    } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-            if (j < nvalid) red_add_f32(dst + j, v[j]);
-    }
+PI0B_DEV void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
 PI0B_DEV float sumsq32(const float (&v)[32], int nvalid) {
@@ -155,10 +139,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    if (threadIdx.x == 0) pdl_launch_dependents();
+    const int S = p.splits;  // cluster size along K (grid.z)
+
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
-            for (int i = 0; i < nkb; ++i) {
+            // Weight tiles never depend on the previous kernel: issue the first ring's worth
+            // before waiting for it (PDL), then the activation tiles.
+            const int pre = min(STAGES, nkb);
+            for (int i = 0; i < pre; ++i) {
+                mbar_arrive_expect_tx(&full[i], Cfg::STAGE_BYTES);
+                tma_load_2d(sB + i * Cfg::B_BYTES, &tmB, &full[i], (kb0 + i) * BK, n_tile * BN, kEvictNormal);
+            }
+            pdl_wait();
+            for (int i = 0; i < pre; ++i)
+                tma_load_2d(sA + i * Cfg::A_BYTES, &tmA, &full[i], (kb0 + i) * BK, m_tile * BM, kEvictLast);
+            for (int i = pre; i < nkb; ++i) {
                 const int s = i % STAGES;
                 const uint32_t ph = (i / STAGES) & 1;
                 mbar_wait(&empty[s], ph ^ 1);
@@ -167,6 +164,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kc, m_tile * BM, kEvictLast);
                 tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, &full[s], kc, n_tile * BN, kEvictNormal);
             }
+        }
+        __syncwarp();
+        if (S > 1) {
+            cluster_sync_all();
+            cluster_sync_all();
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
@@ -192,6 +194,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (elect_one()) umma_commit(accum_full);
         }
         __syncwarp();
+        if (S > 1) {
+            cluster_sync_all();
+            cluster_sync_all();
+        }
     } else {
         // ------------------------------------------------------------ epilogue (8 warps)
         // Warp w may only touch TMEM lanes [32*(w%4), +32): two warps share each lane
@@ -204,12 +210,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const bool valid = r < p.M;
         const uint32_t trow = tmem + (uint32_t(q * 32) << 16);
         const int n0 = n_tile * BN;
-        const bool split_k = p.splits > 1;
 
         // Stage the per-column vector (bias or SiluBias table row), zero-padded, while the
-        // mainloop runs; prefetch the row scale.
+        // mainloop runs; then wait for the previous kernel (PDL) before reading its outputs.
         const float* vec = MODE == kModeSiluTable ? p.table_row : ((p.flags & kFlagBias) ? p.bias : nullptr);
         for (int c = etid; c < BN; c += 256) sm_vec[c] = (vec && n0 + c < p.N) ? vec[n0 + c] : 0.f;
+        pdl_wait();
         float rs = 1.0f;
         if ((p.flags & kFlagRowScale) && valid) rs = 1.0f / sqrtf(p.row_stats[r] * p.inv_width + p.eps);
         named_bar_sync(1, 256);
@@ -219,60 +225,64 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
         constexpr int NC = BN / 32;                 // 32-column chunks in the tile
         constexpr int NP = NC / 2;                  // (c, c + NP) pairs
-        const int c_begin = kPaired ? hsel * (NP / 2) : hsel * (NC / 2);
-        const int c_end = kPaired ? c_begin + NP / 2 : c_begin + NC / 2;
-        bool from_ws = false;
-
-        if (split_k) {
-            // Partial sums -> global; the last-arriving CTA of the tile finishes.
+        constexpr int NU = kPaired ? NP : NC;       // epilogue units: chunks, or chunk pairs
+        // Split-K: unit u belongs to cluster rank u % S.  Chunk c of row r is parked at
+        // stage + c*16 KB + r*128 B, 16-byte pieces XOR-swizzled by r (conflict-free).
+        const int rank = split;
+        const uint32_t srow = smem_u32(smem) + row_in_tile * 128;
+        const int sw = row_in_tile & 7;
+        if (S > 1) {
 #pragma unroll 1
             for (int c = hsel * (NC / 2); c < (hsel + 1) * (NC / 2); ++c) {
+                if ((kPaired ? c % NP : c) % S == rank) continue;
                 float v[32];
                 tmem_ld32(trow + c * 32, v);
-                const int col0 = n0 + c * 32;
-                const int nv = min(32, p.N - col0);
-                if (!valid || nv <= 0) continue;
-                if (MODE == kModeResid) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        v[j] = p.resid_scale * (v[j] * rs + (split == 0 ? sm_vec[c * 32 + j] : 0.f));
-                    ws_add32(reinterpret_cast<float*>(p.out) + (long long)r * p.ldo + col0, v, nv);
-                } else {
-                    ws_add32(p.ws + (long long)r * p.N + col0, v, nv);
+                for (int j = 0; j < 8; ++j)
+                    st_shared_v4(srow + c * 16384 + ((j ^ sw) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            }
+            cluster_sync_all();
+        }
+        // The full K sum of chunk c for this thread's row: own accumulator + the peers' partials.
+        auto acc32 = [&](int c, float(&v)[32]) {
+            tmem_ld32(trow + c * 32, v);
+            if (S > 1) {
+#pragma unroll 1
+                for (int k = 0; k < S; ++k) {
+                    if (k == rank) continue;
+                    const uint32_t ra = mapa_shared(srow + c * 16384, k);
+                    float4 f[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) f[j] = ld_dsmem_f32x4(ra + ((j ^ sw) << 4));
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        v[4 * j] += f[j].x;
+                        v[4 * j + 1] += f[j].y;
+                        v[4 * j + 2] += f[j].z;
+                        v[4 * j + 3] += f[j].w;
+                    }
                 }
             }
-            __threadfence();
-            named_bar_sync(1, 256);
-            if (etid == 0) {
-                const int tile = m_tile * gridDim.y + n_tile;
-                const int prev = atomicAdd(&p.counters[tile], 1);
-                const int last = prev == p.splits - 1;
-                if (last) atomicExch(&p.counters[tile], 0);
-                *last_flag = last;
-            }
-            named_bar_sync(1, 256);
-            if (!*last_flag) goto epilogue_done;
-            __threadfence();
-            from_ws = true;
-        }
+        };
+        const int u_first = S > 1 ? rank + S * hsel : hsel * (NU / 2);
+        const int u_step = S > 1 ? 2 * S : 1;
+        const int u_end = S > 1 ? NU : u_first + NU / 2;
 
         if constexpr (MODE == kModeResid) {
-            // h += scale*(rs*z + b) in place (already accumulated when split), bf16 shadow, row stats.
+            // h += scale*(rs*z + b) in place, bf16 shadow, row stats.
             float ss = 0.f;
 #pragma unroll 1
-            for (int c = c_begin; c < c_end; ++c) {
+            for (int c = u_first; c < u_end; c += u_step) {
                 float v[32], h[32];
-                if (!from_ws) tmem_ld32(trow + c * 32, v);
+                acc32(c, v);
                 const int col0 = n0 + c * 32;
                 const int nv = min(32, p.N - col0);
                 if (!valid || nv <= 0) continue;
                 float* hp = reinterpret_cast<float*>(p.out) + (long long)r * p.ldo + col0;
-                load_f32x32(hp, h, nv, from_ws);
-                if (!from_ws) {
+                load_f32x32(hp, h, nv, false);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) h[j] += p.resid_scale * (v[j] * rs + sm_vec[c * 32 + j]);
-                    store_f32x32(hp, h, nv);
-                }
+                for (int j = 0; j < 32; ++j) h[j] += p.resid_scale * (v[j] * rs + sm_vec[c * 32 + j]);
+                store_f32x32(hp, h, nv);
                 ss += sumsq32(h, nv);
                 if (p.outb)
                     store_bf16x32(reinterpret_cast<__nv_bfloat16*>(p.outb) + (long long)r * p.ldob + col0, h, nv);
@@ -284,17 +294,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const bool rope = MODE == kModeBf16 && (p.flags & kFlagRope) && n0 < p.rope_cols;
             const float2* cs = reinterpret_cast<const float2*>(p.rope_cs) + (long long)(p.rope_pos0 + r) * 128;
 #pragma unroll 1
-            for (int c = c_begin; c < c_end; ++c) {
+            for (int c = u_first; c < u_end; c += u_step) {
                 float a[32], b[32];
-                if (from_ws) {
-                    if (valid) {
-                        ws_take32(p.ws + (long long)r * p.N + n0 + c * 32, a, 32);
-                        ws_take32(p.ws + (long long)r * p.N + n0 + (c + NP) * 32, b, 32);
-                    }
-                } else {
-                    tmem_ld32(trow + c * 32, a);
-                    tmem_ld32(trow + (c + NP) * 32, b);
-                }
+                acc32(c, a);
+                acc32(c + NP, b);
                 if (!valid) continue;
                 if (MODE == kModeGate) {
 #pragma unroll
@@ -328,15 +331,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             // kModeBf16 (BN < 256) / kModeF32Store / kModeSiluTable, 32 columns at a time.
             float ss = 0.f;
 #pragma unroll 1
-            for (int c = c_begin; c < c_end; ++c) {
+            for (int c = u_first; c < u_end; c += u_step) {
                 float v[32];
                 const int col0 = n0 + c * 32;
                 const int nv = min(32, p.N - col0);
-                if (from_ws) {
-                    if (valid && nv > 0) ws_take32(p.ws + (long long)r * p.N + col0, v, nv);
-                } else {
-                    tmem_ld32(trow + c * 32, v);
-                }
+                acc32(c, v);
                 if (!valid || nv <= 0) continue;
                 if constexpr (MODE == kModeSiluTable) {
 #pragma unroll
@@ -361,12 +360,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if constexpr (MODE == kModeF32Store) {
                 if (valid && p.out_stats) atomicAdd(p.out_stats + r, ss);
                 // Optional extra row -1 (the state token of ae.suffix,
-                // proj/src/builder.cpp:311-312), written by the first tile row.
-                if (p.row0_src && m_tile == 0 && row_in_tile == 0) {
+                // proj/src/builder.cpp:311-312), written by the first tile row of rank 0.
+                if (p.row0_src && m_tile == 0 && row_in_tile == 0 && rank == 0) {
                     float* o = reinterpret_cast<float*>(p.out) - p.ldo;
                     __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(p.outb) - p.ldob;
                     float s0 = 0.f;
-                    for (int j = n0 + c_begin * 32; j < min(n0 + c_end * 32, p.N); ++j) {
+                    for (int j = n0 + hsel * (BN / 2); j < min(n0 + (hsel + 1) * (BN / 2), p.N); ++j) {
                         const float x = p.row0_src[j];
                         o[j] = x;
                         if (p.outb) ob[j] = __float2bfloat16_rn(x);
@@ -376,7 +375,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
             }
         }
-    epilogue_done:;
+        // Peers may still be reading this CTA's parked partials.
+        if (S > 1) cluster_sync_all();
     }
 
     tc_fence_before();
@@ -413,8 +413,28 @@ cudaError_t gemm_configure() {
 template <int BN, int STAGES, int MODE>
 static cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, dim3 grid,
                             cudaStream_t stream) {
-    gemm_tc_kernel<BN, STAGES, MODE><<<grid, kGemmThreads, GemmCfg<BN, STAGES>::SMEM, stream>>>(ta, tb, p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kGemmThreads, 1, 1);
+    cfg.dynamicSmemBytes = GemmCfg<BN, STAGES>::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (p.splits > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = 1;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = p.splits;
+        ++na;
+    }
+    if (g_gemm_pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, MODE>, ta, tb, p);
 }
 
 template <int BN, int STAGES>
@@ -432,9 +452,44 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const
     }
 }
 
+void gemm_set_pdl(bool on) { g_gemm_pdl = on; }
+
+// How many clusters of `splits` CTAs of this GEMM configuration fit on the device at once
+// (clusters are confined to a GPC, so this is below num_sms / splits).
+int gemm_max_active_clusters(int bn, int splits) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1, 1, splits);
+    cfg.blockDim = dim3(kGemmThreads, 1, 1);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = splits;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (bn) {
+        case 256:
+            cfg.dynamicSmemBytes = GemmCfg<256, 4>::SMEM;
+            e = cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<256, 4, kModeBf16>, &cfg);
+            break;
+        case 128:
+            cfg.dynamicSmemBytes = GemmCfg<128, 6>::SMEM;
+            e = cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<128, 6, kModeBf16>, &cfg);
+            break;
+        case 64:
+            cfg.dynamicSmemBytes = GemmCfg<64, 8>::SMEM;
+            e = cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<64, 8, kModeBf16>, &cfg);
+            break;
+    }
+    return e == cudaSuccess ? n : 0;
+}
+
 cudaError_t launch_gemm(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                         cudaStream_t stream) {
     if ((p.flags & kFlagRope) && bn != 256) return cudaErrorInvalidValue;
+    if (p.splits < 1 || p.splits > kGemmMaxSplits) return cudaErrorInvalidValue;
     const dim3 grid((p.M + BM - 1) / BM, (p.N + bn - 1) / bn, p.splits);
     switch (bn) {
         case 256: return launch_bn<256, 4>(ta, tb, p, grid, stream);

@@ -20,6 +20,9 @@ enum GemmMode : int {
     kModeSiluTable = 4, // out(bf16) = silu(z + table_row)
 };
 
+// Split-K factor limit: the splits of a tile form one (portable-size) thread-block cluster.
+constexpr int kGemmMaxSplits = 8;
+
 enum GemmFlags : int {
     kFlagRowScale = 1,  // multiply row r by 1/sqrt(row_stats[r]*inv_width + eps)
     kFlagBias = 2,
@@ -29,7 +32,7 @@ enum GemmFlags : int {
 
 struct GemmParams {
     int M, N, K;
-    int splits;               // split-K factor (grid.z)
+    int splits;               // split-K factor (grid.z = cluster size, 1..kGemmMaxSplits)
     int kb_per_split;         // 64-wide k-blocks per split
     int mode, flags;
     const float* row_stats;   // [M] sum of squares of the A rows (RmsStats node)
@@ -45,8 +48,6 @@ struct GemmParams {
     long long ldob;
     float* out_stats;         // [M] += sum over written columns of out^2
     const float* row0_src;    // kModeF32Store: also write row -1 from this fp32 row
-    float* ws;                // split-K workspace [M, N] fp32, zero on entry and exit
-    int* counters;            // split-K tile arrival counters, zero on entry and exit
 };
 
 }  // namespace pi0b

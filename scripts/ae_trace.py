@@ -28,7 +28,7 @@ cap = 148 * 4096
 dt = np.dtype([("kind", "u1"), ("xsrc", "u1"), ("epi", "u1"), ("par", "u1"), ("wmap", "<u2"), ("xmap", "<u2"),
                ("omap", "<u2"), ("tile", "<u2"), ("kb0", "<u2"), ("nkb", "<u2"), ("wait_bar", "<u2"),
                ("wait_cnt", "<u2"), ("sig_bar", "<u2"), ("aux", "<u2"), ("step", "<u2"), ("layer", "<u2"),
-               ("phase", "<u2"), ("pad", "<u2")])
+               ("phase", "<u2"), ("sig_cnt", "<u2")])
 tasks = np.zeros(cap, dtype=dt)
 st = np.zeros((cap + 148 * 8, 16), dtype=np.uint64)
 ctas, stride = ctypes.c_int(), ctypes.c_int()
@@ -100,6 +100,31 @@ for r in mid:
         print(f"  {'':8s}       acc_seen {q(rel(8))} epi_done {q(rel(9))}")
     elif tasks["kind"][idx[0]] == 2:
         print(f"  {'':8s}       qk_landed {q(rel(6))} s_full {q(rel(10))} p_full {q(rel(11))} pv_ready {q(rel(7))} o_done {q(rel(12))} stored {q(rel(13))}")
+    prev_end = r[5]
+
+# finaliser anatomy of one mid layer: the tile's last split (finaliser) per split-K phase
+print("\nfinalisers of the mid layer (us relative to the previous phase's last publish):")
+prev_end = 0
+for r in rows:
+    if r[0] == mid[0][0] - 1:
+        prev_end = r[5]
+for r in mid:
+    idx = np.array(ph[r[0]])
+    if tasks["kind"][idx[0]] != 1 or tasks["sig_cnt"][idx[0]] == 0:
+        prev_end = r[5]
+        continue
+    s8 = st[idx].astype(np.float64)
+    fin = s8[:, 13] > 0
+    if fin.any():
+        f = s8[fin]
+        rel = lambda v: (v - prev_end) / 1e3
+        def q(v):
+            return "%6.2f/%6.2f/%6.2f" % (np.min(v), np.median(v), np.max(v))
+        print(f"  {r[1]:8s} fin={fin.sum():3d} epi_done {q(rel(f[:, 9]))} tile_atomic {q(rel(f[:, 11]))} loaded {q(rel(f[:, 12]))} "
+              f"stored {q(rel(f[:, 13]))} pub {q(rel(f[:, 3]))}")
+        nf = s8[~fin]
+        if len(nf):
+            print(f"  {'':8s} non-fin={len(nf):3d} epi_done {q(rel(nf[:, 9]))} tile_atomic {q(rel(nf[:, 11]))} pub {q(rel(nf[:, 3]))}")
     prev_end = r[5]
 
 if os.environ.get("AE_TRACE_RAW"):

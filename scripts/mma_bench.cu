@@ -9,7 +9,7 @@
 
 using namespace pi0b;
 
-template <int N>
+template <int N, int NACC>
 __global__ void __launch_bounds__(128, 1) mma_kernel(int n_mma, int per_commit, unsigned long long* out) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int n_mma, int per_commit, 
         fence_barrier_init();
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if ((threadIdx.x >> 5) == 1) tmem_alloc(tslot, 256);
+    if ((threadIdx.x >> 5) == 1) tmem_alloc(tslot, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -37,7 +37,9 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int n_mma, int per_commit, 
         const long long t0 = clock64();
         int c = 0;
         for (int i = 0; i < n_mma; ++i) {
-            if (elect_one()) umma_bf16(tmem, ad + 2 * (i & 3), bd + 2 * (i & 3), idesc, i & 3);
+            // n_acc independent accumulators (TMEM column offsets), round robin
+            const int a = i & (NACC - 1);
+            if (elect_one()) umma_bf16(tmem + a * N, ad + 2 * (i & 3), bd + 2 * (i & 3), idesc, i >= NACC);
             if (++c == per_commit) {
                 c = 0;
                 if (elect_one()) umma_commit(bar);
@@ -50,23 +52,23 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int n_mma, int per_commit, 
     }
     tc_fence_before();
     __syncthreads();
-    if ((threadIdx.x >> 5) == 1) tmem_dealloc(tmem, 256);
+    if ((threadIdx.x >> 5) == 1) tmem_dealloc(tmem, 512);
 }
 
 int main() {
     unsigned long long* out;
     cudaMalloc(&out, 8);
     const int smem = 16384 + 256 * 128 + 1024 + 64;
-    cudaFuncSetAttribute(mma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(mma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(mma_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int per : {1, 4, 32, 1024})
+#define CFG(n, a) cudaFuncSetAttribute(mma_kernel<n, a>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+    CFG(64, 1); CFG(128, 1); CFG(256, 1); CFG(64, 2); CFG(128, 2); CFG(256, 2); CFG(64, 4); CFG(128, 4);
+    for (int nacc : {1, 2, 4})
+    for (int per : {4, 16, 1024})
         for (int n : {64, 128, 256}) {
+            if (n * nacc > 512) continue;
             unsigned long long c = 0;
             for (int rep = 0; rep < 2; ++rep) {
-                if (n == 64) mma_kernel<64><<<1, 128, smem>>>(1024, per, out);
-                if (n == 128) mma_kernel<128><<<1, 128, smem>>>(1024, per, out);
-                if (n == 256) mma_kernel<256><<<1, 128, smem>>>(1024, per, out);
+#define RUN(nn, aa) if (n == nn && nacc == aa) mma_kernel<nn, aa><<<1, 128, smem>>>(1024, per, out)
+                RUN(64, 1); RUN(128, 1); RUN(256, 1); RUN(64, 2); RUN(128, 2); RUN(256, 2); RUN(64, 4); RUN(128, 4);
                 cudaError_t e = cudaDeviceSynchronize();
                 if (e != cudaSuccess) {
                     printf("error %s\n", cudaGetErrorString(e));
@@ -74,7 +76,7 @@ int main() {
                 }
                 cudaMemcpy(&c, out, 8, cudaMemcpyDeviceToHost);
             }
-            printf("N=%3d commit+wait every %4d MMAs: %7.1f cycles per MMA (ideal %d)\n", n, per, c / 1024.0, 128 * n / 256);
+            printf("N=%3d acc=%d commit+wait every %4d MMAs: %7.1f cycles per MMA (ideal %d)\n", n, nacc, per, c / 1024.0, 128 * n / 256);
         }
     return 0;
 }
