@@ -7,23 +7,22 @@
 // (ae.kcat / ae.vcat), the RmsStats nodes, the ae.suffix concat and the ae.act_rows slice.
 //
 // Warp roles (320 threads):
-//   warp 0      weight producer: walks the CTA's task list and TMA-streams every GEMM task's
-//               [128 features x 64 k] bf16 weight tiles into a 6-stage ring.  It never waits
-//               on a dependency, only on free ring slots, so it runs ahead across barriers.
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer.  GEMM: D[128 x 128] +=
-//               X[128 x 64] * W^T, X = the 64 activation rows (rows 64..127 of the A tile are
-//               don't-care and never read back).  Attention: S = Q K^T (N = 64 keys) and
-//               O = P V (N = 256) for one head pair (128 stacked query rows) and one key block.
-//   warps 2..9  workers: dependency waits, activation staging (TMA, or fp32 -> bf16 with the
-//               row sums of squares of the RmsScale), epilogues from TMEM, softmax, the
-//               TMA reduce-add of split-K partials into the fp32 residual stream, signalling.
+//   warp 0      weight producer: walks the CTA's task list and streams every GEMM task's
+//               [64 features x 64 k] bf16 weight tiles (pairs of k-blocks per bulk copy) into a
+//               5-slot ring.  It never waits on a dependency, only on free ring slots, so it runs
+//               ahead across phases.
+//   warp 1      TMEM allocator + tcgen05.mma issuer (warp-uniform loop, one elected lane).
+//               GEMM: D[128 x 64] += X[128 x 64] * W^T, X = the 64 activation rows (rows
+//               64..127 of the A tile are don't-care and never read back).  Attention: S = Q K^T
+//               (N = 64 keys) and O = P V (N = 256) for one head pair and one key range.
+//   warps 2..9  workers: dependency waits, activation staging (bf16 rows, or fp32 residual rows
+//               converted to bf16 with the RmsStats row sums of squares, or the attention-partial
+//               combine), epilogues from TMEM, softmax, red.add of split-K partials into the fp32
+//               residual stream, signalling.
 //
-// All operand traffic is cp.async (LDGSTS): one SM's TMA/bulk engine serialises requests at
-// ~0.4 us each (scripts/ingest_bench.cu), while cp.async sustains ~300 GB/s per SM.  Split-K
-// partials (ae.proj, ae.down, ae.action_out) are added into the fp32 residual stream with
-// red.global.add.v4.f32 straight from the TMEM drain.  Attention runs as independent
-// (head pair, key range) tasks with an exact softmax over the range; the normalised partials and
-// their (row max, row sum) are combined by the ae.proj operand staging.
+// Activation traffic is cp.async (LDGSTS, ~300 GB/s per SM); weights are contiguous bulk copies
+// (the bulk engine's per-request cost, ~0.25 us, is amortised over 16 KB).  No task finalises
+// another's output (aemk.cuh): a phase is complete when all of its tasks have signalled.
 #include "aemk.cuh"
 #include "ptx.cuh"
 
@@ -39,18 +38,18 @@ namespace {
 
 constexpr int kAeThreads = 320;
 constexpr int kWorkers = 256;
+constexpr int kWBlk = 64 * 64 * 2;    // 8 KB: [64 features x 64 k] bf16 SW128 image
+constexpr int kWSlot = 2 * kWBlk;     // ring slot: up to two consecutive k-blocks, one bulk copy
 constexpr int kWSt = 5;
-constexpr int kWTile = 128 * 64 * 2;  // 16 KB: 128 weight rows x 64 k (bf16, SW128 image)
 constexpr int kXSt = 4;
 constexpr int kXTile = 64 * 128;      // 8 KB: 64 activation rows x 64 k
 constexpr int kFSt = 5;
-constexpr int kFTile = 16384;         // fp32 staging of one k-block: two SW128 boxes of 32 columns
-constexpr int kOSt = 2;
+constexpr int kFTile = 16384;         // fp32 staging of one k-block: 64 rows x 64 columns
 constexpr int kMaxSplits = 10;        // attention key ranges combined by the ae.proj staging
 constexpr int kORegion = 81920;       // partial staging: 2 slots of <= 5 ranges, or 1 slot of <= 10
 constexpr int kBlocksPerSplit = 2;    // 64-key blocks per attention task
 constexpr int kOffW = 0;
-constexpr int kOffU = kWSt * kWTile;                // union region (128 KB)
+constexpr int kOffU = kWSt * kWSlot;                // union region (128 KB)
 constexpr int kUnion = 131072;
 constexpr int kOffX = kOffU;                        // GEMM: X ring (+1 pad slot: rows 64..127 of A)
 constexpr int kOffF = kOffU + (kXSt + 1) * kXTile;  // GEMM: fp32 ring (kXY) or partial ring (kXO)
@@ -61,15 +60,15 @@ constexpr int kOffV = kOffK;                        // ATTN: V (reuses K)
 constexpr int kOffAux = kOffU + kUnion;
 constexpr int kAuxBytes = 16384;
 constexpr int kAeSmem = kOffAux + kAuxBytes + 1024;
-static_assert(kOffF + kORegion <= kOffAux, "GEMM union overflow");
+static_assert(kOffF + kORegion <= kOffAux && kOffF + kFSt * kFTile <= kOffAux, "GEMM union overflow");
 static_assert(kAeSmem <= 232448, "shared memory budget");
 
 constexpr uint32_t kTAcc = 0, kTS = 0, kTO = 256;  // TMEM columns (512 allocated)
 
 // mbarrier slots
-constexpr int kBWFull = 0, kBWEmpty = 8, kBXFull = 16, kBXEmpty = 20, kBFFull = 24, kBOFull = 30, kBAccFull = 32,
-              kBAccEmpty = 33, kBQFull = 34, kBSFull = 35, kBVFull = 36, kBPFull = 37, kBODone = 38, kNumBars = 39;
-static_assert(kWSt <= 8 && kXSt <= 4 && kFSt <= 6 && kOSt <= 2, "barrier slots");
+constexpr int kBWFull = 0, kBWEmpty = 8, kBXFull = 16, kBXEmpty = 20, kBAccFull = 32, kBAccEmpty = 33,
+              kBQFull = 34, kBSFull = 35, kBVFull = 36, kBPFull = 37, kBODone = 38, kNumBars = 39;
+static_assert(kWSt <= 8 && kXSt <= 4, "barrier slots");
 
 PI0B_DEV unsigned ld_relaxed_u32(const unsigned* p) {
     unsigned v;
@@ -163,8 +162,6 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
     uint64_t* w_empty = mb + kBWEmpty;
     uint64_t* x_full = mb + kBXFull;
     uint64_t* x_empty = mb + kBXEmpty;
-    uint64_t* f_full = mb + kBFFull;
-    uint64_t* o_full = mb + kBOFull;
     uint64_t* acc_full = mb + kBAccFull;
     uint64_t* acc_empty = mb + kBAccEmpty;
     uint64_t* q_full = mb + kBQFull;
@@ -175,21 +172,18 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffAux + 512);
     float* sm_rs = reinterpret_cast<float*>(smem + kOffAux + 1024);     // [64]
     float2* sm_ml = reinterpret_cast<float2*>(smem + kOffAux + 2048);   // [2][kMaxSplits][64]
-    float* sm_vec = reinterpret_cast<float*>(smem + kOffAux + 12288);   // [128] epilogue vector
-    volatile int* sm_flag = reinterpret_cast<volatile int*>(smem + kOffAux + 768);
+    float* sm_vec = reinterpret_cast<float*>(smem + kOffAux + 12288);   // [64] epilogue vector
 
     // warp index through a shuffle: provably warp-uniform, so role branches stay converged and the
-    // MMA issue loop keeps descriptors in uniform registers (tcgen05.mma from divergent single-lane
-    // code costs ~2-3x more issue cycles, scripts/mma_bench.cu)
+    // MMA issue loop keeps descriptors in uniform registers (tcgen05.mma fed from per-lane
+    // registers costs ~3-4x more issue cycles, scripts/mma_bench.cu)
     const int warp = __shfl_sync(0xffffffff, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const AeTask* my = p.tasks + size_t(blockIdx.x) * p.task_stride;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kNumBars; ++i) {
             uint32_t cnt = 1;
-            if ((i >= kBXFull && i < kBXFull + kXSt) || (i >= kBFFull && i < kBFFull + kFSt) ||
-                (i >= kBOFull && i < kBOFull + kOSt) || i == kBQFull || i == kBVFull)
-                cnt = kWorkers;
+            if ((i >= kBXFull && i < kBXFull + kXSt) || i == kBQFull || i == kBVFull) cnt = kWorkers;
             mbar_init(&mb[i], cnt);
         }
         fence_barrier_init();
@@ -202,36 +196,26 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
 
     if (warp == 0) {
         // ================================================================ weight producer
-        // cp.async of each [128 x 64] weight tile straight into its SW128 operand image; the
-        // tile's w_full barrier completes when all 32 lanes' copies have landed.
+        // Tile-contiguous weights (kernels_misc.cu tile_weight_kernel): the k-blocks of one tile
+        // are consecutive 8 KB swizzled images, so two of them are one 16 KB bulk copy.
         int ws = 0;
         uint32_t wph = 0;
-        unsigned issued = 0;
-        const unsigned cap = unsigned(max(1, min(p.w_inflight, kWSt)));
         for (int i = 0;; ++i) {
             const AeTask t = load_task(my + i);
             if (t.kind == kAeEnd || t.phase >= p.limit_phase) break;
             if (t.kind != kAeGemm) continue;
             unsigned long long* tr = (p.trace && lane == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
             const AeMat wm = load_mat(p.mats + t.wmat);
-            const __nv_bfloat16* wbase = reinterpret_cast<const __nv_bfloat16*>(wm.ptr);
-            for (int k = 0; k < t.nkb; ++k) {
+            const uint8_t* base = reinterpret_cast<const uint8_t*>(wm.ptr) + ((size_t)t.tile * wm.ld + t.kb0) * kWBlk;
+            for (int k = 0; k < t.nkb; k += 2) {
+                const uint32_t bytes = uint32_t(min(2, t.nkb - k)) * kWBlk;
                 mbar_wait(&w_empty[ws], wph ^ 1);
-                if (issued >= cap) {
-                    const unsigned o = issued - cap;
-                    mbar_wait(&w_full[o % kWSt], (o / kWSt) & 1);
-                }
                 if (tr && k == 0) tr[4] = gtimer();
-                // tile-contiguous weights: tile (n_tile, kb) is one 16 KB block, already in the
-                // swizzled smem image (csrc/kernels_misc.cu tile_weight_kernel): one bulk copy on
-                // the TMA engine, off the LSU path the activation cp.asyncs use
-                const uint8_t* src = reinterpret_cast<const uint8_t*>(wbase) + ((size_t)t.tile * wm.ld + t.kb0 + k) * kWTile;
                 if (lane == 0) {
-                    mbar_arrive_expect_tx(&w_full[ws], kWTile);
-                    bulk_g2s(sW + ws * kWTile, src, kWTile, &w_full[ws], kEvictFirst);
+                    mbar_arrive_expect_tx(&w_full[ws], bytes);
+                    bulk_g2s(sW + ws * kWSlot, base + (size_t)k * kWBlk, bytes, &w_full[ws], kEvictFirst);
                 }
                 adv(ws, wph, 1, kWSt);
-                ++issued;
             }
             if (tr) tr[5] = gtimer();
         }
@@ -242,7 +226,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
         {
             int ws = 0, xs = 0;
             uint32_t wph = 0, xph = 0, gidx = 0, aidx = 0;
-            constexpr uint32_t idesc_g = umma_idesc_bf16(128, 128);
+            constexpr uint32_t idesc_g = umma_idesc_bf16(128, 64);
             constexpr uint32_t idesc_s = umma_idesc_bf16(128, 64);
             constexpr uint32_t idesc_o = umma_idesc_bf16(128, 256) | (1u << 16);  // B (V) MN-major
             for (int i = 0;; ++i) {
@@ -250,31 +234,29 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 if (t.kind == kAeEnd || t.phase >= p.limit_phase) break;
                 unsigned long long* tr = (p.trace && lane == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
                 if (t.kind == kAeGemm) {
-                    unsigned long long* dbg = (p.dbg && lane == 0 && t.epi == kEpiQkv && t.step == 0 && t.layer == 0)
-                                                  ? p.dbg + size_t(blockIdx.x) * 128 + 64 : nullptr;
                     mbar_wait(acc_empty, (gidx & 1) ^ 1);
-                    for (int k = 0; k < t.nkb; ++k) {
-                        if (dbg && k < 16) dbg[k * 4] = gtimer();
+                    for (int k = 0; k < t.nkb; k += 2) {
+                        const int n = min(2, t.nkb - k);
                         mbar_wait(&w_full[ws], wph);
-                        if (dbg && k < 16) dbg[k * 4 + 1] = gtimer();
-                        if (tr && k == t.nkb - 1) tr[6] = gtimer();
-                        mbar_wait(&x_full[xs], xph);
-                        if (dbg && k < 16) dbg[k * 4 + 2] = gtimer();
-                        fence_proxy_async_smem();  // cp.async / st.shared data -> tensor-core reads
-                        tc_fence_after();
-                        const uint64_t ad = umma_desc_sw128(sX + xs * kXTile);
-                        const uint64_t bd = umma_desc_sw128(sW + ws * kWTile);
-                        if (elect_one()) {
+                        if (tr && k + n == t.nkb) tr[6] = gtimer();
+                        for (int j = 0; j < n; ++j) {
+                            mbar_wait(&x_full[xs], xph);
+                            fence_proxy_async_smem();  // cp.async / st.shared data -> tensor-core reads
+                            tc_fence_after();
+                            const uint64_t ad = umma_desc_sw128(sX + xs * kXTile);
+                            const uint64_t bd = umma_desc_sw128(sW + ws * kWSlot + j * kWBlk);
+                            if (elect_one()) {
 #pragma unroll
-                            for (int kk = 0; kk < 4; ++kk)
-                                umma_bf16(tmem + kTAcc, ad + 2 * kk, bd + 2 * kk, idesc_g, (k | kk) != 0);
-                            umma_commit(&w_empty[ws]);
-                            umma_commit(&x_empty[xs]);
+                                for (int kk = 0; kk < 4; ++kk)
+                                    umma_bf16(tmem + kTAcc, ad + 2 * kk, bd + 2 * kk, idesc_g, (k + j + kk) != 0);
+                                umma_commit(&x_empty[xs]);
+                            }
+                            __syncwarp();
+                            adv(xs, xph, 1, kXSt);
                         }
+                        if (elect_one()) umma_commit(&w_empty[ws]);
                         __syncwarp();
-                        if (dbg && k < 16) dbg[k * 4 + 3] = gtimer();
                         adv(ws, wph, 1, kWSt);
-                        adv(xs, xph, 1, kXSt);
                     }
                     if (elect_one()) umma_commit(acc_full);
                     __syncwarp();
@@ -330,10 +312,9 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
         const bool drainer = wq < 2;                  // warps 4, 5, 8, 9: TMEM lanes 0..63
         const int drow = wq * 32 + lane;              // drainer: activation row
         const int dhalf = warp >= 8 ? 1 : 0;          // drainer: column half
-        const bool softmax = warp >= 4 && warp < 8;   // TMEM lanes 0..127 (stacked query rows)
         const uint32_t tlane = uint32_t(wq * 32) << 16;
-        int xs = 0, fs = 0, os = 0;
-        uint32_t xph = 0, fph = 0, oph = 0, gidx = 0, aidx = 0;
+        int xs = 0;
+        uint32_t xph = 0, gidx = 0, aidx = 0;
         // staging geometry: thread -> (row sr, 16-column quarter sq) of a 64 x 64 k-block
         const int sr = wtid >> 2, sq = wtid & 3;
 
@@ -349,11 +330,6 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             if (tr) tr[1] = gtimer();
 
             if (t.kind == kAeGemm) {
-                // RmsScale rows of the residual stream this task reads (its finalisers' stats)
-                if (t.epi == kEpiHead && wtid < 64) {
-                    const int row = min(wtid + (t.epi == kEpiHead ? 1 : 0), 63);
-                    sm_rs[wtid] = 1.0f / sqrtf(__ldcg(p.stats + (size_t)t.aux * 64 + row) * p.inv_width + p.eps);
-                }
                 // -------------------------------------------------- activation staging
                 const AeMat xm = load_mat(p.mats + t.xmat);
                 if (t.xsrc == kXBf16) {
@@ -371,6 +347,52 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         cp_async_arrive_noinc(&x_full[xs]);
                         adv(xs, xph, 1, kXSt);
                     }
+                } else if (t.xsrc == kXY) {
+                    // fp32 residual rows over the full K: each thread cp.asyncs its own 64 bytes
+                    // (row sr, columns 16 sq..) of every k-block into a private slice of the fp32
+                    // ring (kFSt - 1 k-blocks in flight), converts them to bf16 into the operand
+                    // slot and accumulates the row's sum of squares (RmsStats).
+                    const float* yf = reinterpret_cast<const float*>(xm.ptr);
+                    const bool okr = sr < xm.rows;
+                    const float* src0 = yf + (size_t)(okr ? sr : 0) * xm.ld + t.kb0 * 64 + sq * 16;
+                    const int rot = (wtid >> 1) & 3;  // 16-byte piece rotation: conflict-free LDS
+                    auto issue = [&](int k) {
+                        if (k < t.nkb) {
+                            uint8_t* dst = sF + (k % kFSt) * kFTile + wtid * 64;
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) cp_async16(dst + ((u ^ rot) << 4), src0 + k * 64 + u * 4, okr);
+                        }
+                        cp_async_commit();
+                    };
+#pragma unroll 1
+                    for (int k = 0; k < kFSt - 1; ++k) issue(k);
+                    float ss = 0.f;
+#pragma unroll 1
+                    for (int k = 0; k < t.nkb; ++k) {
+                        issue(k + kFSt - 1);
+                        cp_async_wait<kFSt - 1>();
+                        const uint8_t* f = sF + (k % kFSt) * kFTile + wtid * 64;
+                        float v[16];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const float4 q4 = *reinterpret_cast<const float4*>(f + ((u ^ rot) << 4));
+                            v[4 * u] = q4.x; v[4 * u + 1] = q4.y; v[4 * u + 2] = q4.z; v[4 * u + 3] = q4.w;
+                        }
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) ss += v[e] * v[e];
+                        mbar_wait(&x_empty[xs], xph ^ 1);
+                        uint8_t* dst = sX + xs * kXTile;
+                        *reinterpret_cast<uint4*>(dst + swz(sr, 2 * sq)) =
+                            make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
+                        *reinterpret_cast<uint4*>(dst + swz(sr, 2 * sq + 1)) =
+                            make_uint4(pack2(v[8], v[9]), pack2(v[10], v[11]), pack2(v[12], v[13]), pack2(v[14], v[15]));
+                        fence_proxy_async_smem();
+                        mbar_arrive(&x_full[xs]);
+                        adv(xs, xph, 1, kXSt);
+                    }
+                    ss += __shfl_xor_sync(0xffffffff, ss, 1);
+                    ss += __shfl_xor_sync(0xffffffff, ss, 2);
+                    if (sq == 0) sm_rs[sr] = 1.0f / sqrtf(ss * p.inv_width + p.eps);
                 } else if (t.xsrc == kXO) {
                     // ae.proj input: combine the attention key-range partials of each row,
                     // o = sum_j l_j 2^(m_j - M) O_j / sum_j l_j 2^(m_j - M); each thread loads and
@@ -458,22 +480,22 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 // Epilogue operands that do not depend on the accumulator: fetched now, while the
                 // MMA runs, so the drain loops touch only TMEM and shared memory.
                 if (t.epi == kEpiSilu || t.epi == kEpiInit || t.epi == kEpiHead) {
-                    const float* vec = t.epi == kEpiSilu ? p.table + (size_t)t.step * p.width + t.tile * 128
-                                                         : (t.epi == kEpiInit ? p.b_state + t.tile * 128 : p.b_head);
-                    const int n = t.epi == kEpiHead ? p.act_dim : 128;
+                    const float* vec = t.epi == kEpiSilu ? p.table + (size_t)t.step * p.width + t.tile * 64
+                                                         : (t.epi == kEpiInit ? p.b_state + t.tile * 64 : p.b_head);
+                    const int n = t.epi == kEpiHead ? p.act_dim : 64;
                     if (wtid < n) sm_vec[wtid] = __ldg(vec + wtid);
                 }
                 if (t.epi == kEpiSilu) {  // ae.suffix: y = [st ; b_out] on this tile's columns
-                    float4 yv[8];
+                    float4 yv[4];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int q = wtid + 256 * u, row = q >> 5, c4 = q & 31;
-                        yv[u] = __ldcg(reinterpret_cast<const float4*>((row == 0 ? p.st : p.b_out) + t.tile * 128) + c4);
+                    for (int u = 0; u < 4; ++u) {
+                        const int q = wtid + 256 * u, row = q >> 4, c4 = q & 15;
+                        yv[u] = __ldcg(reinterpret_cast<const float4*>((row == 0 ? p.st : p.b_out) + t.tile * 64) + c4);
                     }
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int q = wtid + 256 * u, row = q >> 5, c4 = q & 31;
-                        reinterpret_cast<float4*>(p.y + (size_t)row * p.width + t.tile * 128)[c4] = yv[u];
+                    for (int u = 0; u < 4; ++u) {
+                        const int q = wtid + 256 * u, row = q >> 4, c4 = q & 15;
+                        reinterpret_cast<float4*>(p.y + (size_t)row * p.width + t.tile * 64)[c4] = yv[u];
                     }
                 }
                 named_bar_sync(1, kWorkers);  // sm_rs / sm_vec complete
@@ -483,34 +505,78 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 mbar_wait(acc_full, gidx & 1);
                 tc_fence_after();
                 if (tr) tr[8] = gtimer();
-                unsigned long long* trd =
-                    (p.trace && threadIdx.x == 128) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
-                if (trd) trd[10] = gtimer();
                 if (drainer) {
-                    // Compact loops over 4-column quads of the thread's row (TMEM lane):
-                    // short bodies stay hot in the instruction cache after one iteration.
+                    // Compact loops over 4-column quads of the thread's row (TMEM lane): short
+                    // bodies stay hot in the instruction cache after one iteration.
                     const int r = drow;
                     const uint32_t ta = tmem + kTAcc + tlane;
-                    if (t.sig_cnt) {
-                        // split-K partial -> fp32 accumulator (residual stream, or the ae.qkv /
-                        // ae.ffn accumulators finalised by the tile's last task): red.add
-                        float* base = t.epi == kEpiRed ? p.y + (size_t)t.rowoff * p.width
-                                                       : (t.epi == kEpiQkv ? p.qacc : p.facc);
-                        const int ld = t.epi == kEpiRed ? p.width : (t.epi == kEpiQkv ? p.n_qkv : 2 * p.mlp);
+                    if (t.epi == kEpiRed) {
+                        // split-K partial -> the fp32 residual stream (rows from `rowoff`)
                         const bool ok = t.rowoff ? r < p.chunk : true;
-                        float* dst = base + (size_t)r * ld + t.tile * 128 + dhalf * 64;
+                        float* dst = p.y + (size_t)(r + t.rowoff) * p.width + t.tile * 64 + dhalf * 32;
 #pragma unroll 1
-                        for (int q = 0; q < 16; ++q) {
+                        for (int q = 0; q < 8; ++q) {
                             float4 v;
-                            tmem_ld4(ta + dhalf * 64 + q * 4, v);
+                            tmem_ld4(ta + dhalf * 32 + q * 4, v);
                             if (ok) red_add_v4_f32(dst + q * 4, v.x, v.y, v.z, v.w);
+                        }
+                    } else if (t.epi == kEpiQkv || t.epi == kEpiGate) {
+                        // paired tile (aemk.cuh AeTileOrder): column i < 32 and its partner 32 + i;
+                        // this thread: i in [16 dhalf, 16 dhalf + 16)
+                        const float rs = sm_rs[r];
+                        const int T = t.tile >> 1, sub = t.tile & 1, i0 = dhalf * 16;
+                        float xa[16], xb[16];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            float4 a4, b4;
+                            tmem_ld4(ta + i0 + q * 4, a4);
+                            tmem_ld4(ta + 32 + i0 + q * 4, b4);
+                            xa[4 * q] = a4.x * rs; xa[4 * q + 1] = a4.y * rs; xa[4 * q + 2] = a4.z * rs; xa[4 * q + 3] = a4.w * rs;
+                            xb[4 * q] = b4.x * rs; xb[4 * q + 1] = b4.y * rs; xb[4 * q + 2] = b4.z * rs; xb[4 * q + 3] = b4.w * rs;
+                        }
+                        __nv_bfloat16 *o1, *o2;
+                        if (t.epi == kEpiQkv) {
+                            const int f0 = T * 128;
+                            __nv_bfloat16* orow = p.qkv + (size_t)r * p.n_qkv;
+                            if (f0 < p.rope_cols) {
+                                // pairs (j, j + 128) of one head (proj/src/tensor.cpp:150-178)
+                                const int hd = f0 >> 8, j0 = ((f0 & 255) >> 7) * 64 + sub * 32 + i0;
+                                o1 = orow + hd * 256 + j0;
+                                o2 = o1 + 128;
+                                const float4* csp = reinterpret_cast<const float4*>(p.rope_cs) + ((size_t)(p.rope_pos0 + r) * 128 + j0) / 2;
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) {
+                                    const float4 cs = __ldg(csp + j);
+                                    const float x0 = xa[2 * j], y0 = xb[2 * j], x1 = xa[2 * j + 1], y1 = xb[2 * j + 1];
+                                    xa[2 * j] = x0 * cs.x - y0 * cs.y;
+                                    xb[2 * j] = x0 * cs.y + y0 * cs.x;
+                                    xa[2 * j + 1] = x1 * cs.z - y1 * cs.w;
+                                    xb[2 * j + 1] = x1 * cs.w + y1 * cs.z;
+                                }
+                            } else {
+                                o1 = orow + f0 + sub * 32 + i0;
+                                o2 = o1 + 64;
+                            }
+                        } else {  // gated FFN: up * gelu(gate) -> g column 64 T + 32 sub + i
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) xa[j] = xa[j] * gelu_fast(xb[j]);
+                            o1 = p.g + (size_t)r * p.mlp + T * 64 + sub * 32 + i0;
+                            o2 = nullptr;
+                        }
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            reinterpret_cast<uint4*>(o1)[h] = make_uint4(pack2(xa[8 * h], xa[8 * h + 1]), pack2(xa[8 * h + 2], xa[8 * h + 3]),
+                                                                        pack2(xa[8 * h + 4], xa[8 * h + 5]), pack2(xa[8 * h + 6], xa[8 * h + 7]));
+                            if (o2)
+                                reinterpret_cast<uint4*>(o2)[h] = make_uint4(pack2(xb[8 * h], xb[8 * h + 1]), pack2(xb[8 * h + 2], xb[8 * h + 3]),
+                                                                            pack2(xb[8 * h + 4], xb[8 * h + 5]), pack2(xb[8 * h + 6], xb[8 * h + 7]));
                         }
                     } else if (t.epi == kEpiSilu) {
                         // ae.action_proj: silu(a W + T[step]) (the y reset ran during staging)
-                        const int c0 = dhalf * 64;
-                        __nv_bfloat16* o = p.ap + (size_t)r * p.width + t.tile * 128 + c0;
+                        const int c0 = dhalf * 32;
+                        __nv_bfloat16* o = p.ap + (size_t)r * p.width + t.tile * 64 + c0;
 #pragma unroll 1
-                        for (int q = 0; q < 16; ++q) {
+                        for (int q = 0; q < 8; ++q) {
                             float4 v;
                             tmem_ld4(ta + c0 + q * 4, v);
                             const float4 tb = *reinterpret_cast<const float4*>(sm_vec + c0 + q * 4);
@@ -538,22 +604,19 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                                                       av[q].z + p.euler * (v.z * rs + bv.z), av[q].w + p.euler * (v.w * rs + bv.w));
                         }
                     } else if (t.epi == kEpiInit) {
-                        const int col0 = t.tile * 128 + dhalf * 64;
+                        const int col0 = t.tile * 64 + dhalf * 32;
 #pragma unroll 1
-                        for (int q = 0; q < 16; ++q) {
+                        for (int q = 0; q < 8; ++q) {
                             float4 v;
-                            tmem_ld4(ta + dhalf * 64 + q * 4, v);
-                            const float4 bv = *reinterpret_cast<const float4*>(sm_vec + dhalf * 64 + q * 4);
+                            tmem_ld4(ta + dhalf * 32 + q * 4, v);
+                            const float4 bv = *reinterpret_cast<const float4*>(sm_vec + dhalf * 32 + q * 4);
                             if (r == 0) reinterpret_cast<float4*>(p.st + col0)[q] = make_float4(v.x + bv.x, v.y + bv.y, v.z + bv.z, v.w + bv.w);
                         }
                     }
                 }
                 if (tr) tr[9] = gtimer();
-                if (p.trace && threadIdx.x == 128)  // drainer warp 4 lane 0 (row 0)
-                    p.trace[(size_t(blockIdx.x) * p.task_stride + i) * 16 + 14] = gtimer();
                 tc_fence_before();
                 named_bar_sync(1, kWorkers);
-                if (tr) tr[15] = gtimer();
                 if (wtid == 0) mbar_arrive(acc_empty);
                 ++gidx;
             } else if (t.kind == kAeAttn) {
@@ -696,106 +759,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             // -------------------------------------------------- publish completion
             // bar.sync orders every worker's writes before lane 0's release (PTX cumulativity).
             named_bar_sync(1, kWorkers);
-            if (t.kind == kAeGemm && t.sig_cnt) {
-                // Split-K: the last task of a 128-column tile finalises it; only finalisers count
-                // towards the phase.  Residual: fp32 y -> bf16 yb + the rows' sums of squares
-                // (RmsStats) for the next RmsScale.  ae.qkv / ae.ffn: RmsScale + RoPE / gated GELU
-                // of the accumulated tile -> bf16, and the accumulator tile is zeroed for reuse.
-                if (wtid == 0) sm_flag[0] = atom_add_acqrel_u32(p.bars + t.omat, 1u) + 1 == t.sig_cnt;
-                named_bar_sync(1, kWorkers);
-                if (tr) tr[11] = gtimer();
-                if (sm_flag[0]) {
-                    const int r = wtid >> 2, qd = wtid & 3;
-                    if (t.epi == kEpiRed) {
-                        const int c0 = t.tile * 128 + qd * 32;
-                        const float4* yr = reinterpret_cast<const float4*>(p.y + (size_t)r * p.width + c0);
-                        float4 v[8];
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) v[j] = __ldcg(yr + j);
-                        if (tr) tr[12] = gtimer() + (unsigned long long)(v[0].x == 12345.f);
-                        float ss = 0.f;
-                        uint32_t pk[16];
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            ss += v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w;
-                            pk[2 * j] = pack2(v[j].x, v[j].y);
-                            pk[2 * j + 1] = pack2(v[j].z, v[j].w);
-                        }
-                        uint4* yb4 = reinterpret_cast<uint4*>(p.yb + (size_t)r * p.width + c0);
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) yb4[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-                        ss += __shfl_xor_sync(0xffffffff, ss, 1);
-                        ss += __shfl_xor_sync(0xffffffff, ss, 2);
-                        if (qd == 0) atomicAdd(p.stats + (size_t)t.aux * 64 + r, ss);
-                    } else {
-                        // thread: row r, packed pair columns c = 16 qd + j and c + 64 (j < 16)
-                        const bool qkv = t.epi == kEpiQkv;
-                        const int ld = qkv ? p.n_qkv : 2 * p.mlp;
-                        float4* acc = reinterpret_cast<float4*>((qkv ? p.qacc : p.facc) + (size_t)r * ld + t.tile * 128 + qd * 16);
-                        float4 a[4], b[4];
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            a[j] = __ldcg(acc + j);
-                            b[j] = __ldcg(acc + 16 + j);
-                        }
-                        const float rs = 1.0f / sqrtf(__ldcg(p.stats + (size_t)t.aux * 64 + r) * p.inv_width + p.eps);
-                        if (tr) tr[12] = gtimer() + (unsigned long long)(a[0].x + b[3].w + rs == 12345.f);
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            __stcg(acc + j, make_float4(0.f, 0.f, 0.f, 0.f));
-                            __stcg(acc + 16 + j, make_float4(0.f, 0.f, 0.f, 0.f));
-                        }
-                        float xa[16], xb[16];
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            xa[4 * j] = a[j].x * rs; xa[4 * j + 1] = a[j].y * rs; xa[4 * j + 2] = a[j].z * rs; xa[4 * j + 3] = a[j].w * rs;
-                            xb[4 * j] = b[j].x * rs; xb[4 * j + 1] = b[j].y * rs; xb[4 * j + 2] = b[j].z * rs; xb[4 * j + 3] = b[j].w * rs;
-                        }
-                        if (qkv) {
-                            const int f0 = t.tile * 128;
-                            const bool rope = f0 < p.rope_cols;
-                            const int hd = f0 >> 8, u = (f0 & 255) >> 7;
-                            const int w0 = u * 64 + qd * 16;
-                            __nv_bfloat16* orow = p.qkv + (size_t)r * p.n_qkv;
-                            __nv_bfloat16* o1 = rope ? orow + hd * 256 + w0 : orow + f0 + qd * 16;
-                            __nv_bfloat16* o2 = rope ? o1 + 128 : o1 + 64;
-                            if (rope) {  // pairs (j, j + 128) of the head (proj/src/tensor.cpp:150-178)
-                                const float4* csp = reinterpret_cast<const float4*>(p.rope_cs) + ((size_t)(p.rope_pos0 + r) * 128 + w0) / 2;
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) {
-                                    const float4 cs = __ldg(csp + j);
-                                    const float x0 = xa[2 * j], y0 = xb[2 * j], x1 = xa[2 * j + 1], y1 = xb[2 * j + 1];
-                                    xa[2 * j] = x0 * cs.x - y0 * cs.y;
-                                    xb[2 * j] = x0 * cs.y + y0 * cs.x;
-                                    xa[2 * j + 1] = x1 * cs.z - y1 * cs.w;
-                                    xb[2 * j + 1] = x1 * cs.w + y1 * cs.z;
-                                }
-                            }
-#pragma unroll
-                            for (int h = 0; h < 2; ++h) {
-                                reinterpret_cast<uint4*>(o1)[h] = make_uint4(pack2(xa[8 * h], xa[8 * h + 1]), pack2(xa[8 * h + 2], xa[8 * h + 3]),
-                                                                            pack2(xa[8 * h + 4], xa[8 * h + 5]), pack2(xa[8 * h + 6], xa[8 * h + 7]));
-                                reinterpret_cast<uint4*>(o2)[h] = make_uint4(pack2(xb[8 * h], xb[8 * h + 1]), pack2(xb[8 * h + 2], xb[8 * h + 3]),
-                                                                            pack2(xb[8 * h + 4], xb[8 * h + 5]), pack2(xb[8 * h + 6], xb[8 * h + 7]));
-                            }
-                        } else {  // gated FFN: up * gelu(gate), packed tile = [up 64 | gate 64]
-                            float gg[16];
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) gg[j] = xa[j] * gelu_fast(xb[j]);
-                            uint4* o = reinterpret_cast<uint4*>(p.g + (size_t)r * p.mlp + t.tile * 64 + qd * 16);
-#pragma unroll
-                            for (int h = 0; h < 2; ++h)
-                                o[h] = make_uint4(pack2(gg[8 * h], gg[8 * h + 1]), pack2(gg[8 * h + 2], gg[8 * h + 3]),
-                                                  pack2(gg[8 * h + 4], gg[8 * h + 5]), pack2(gg[8 * h + 6], gg[8 * h + 7]));
-                        }
-                    }
-                    named_bar_sync(1, kWorkers);
-                    if (tr) tr[13] = gtimer();
-                    if (wtid == 0) atom_add_acqrel_u32(p.bars + t.sig_bar, 1u);
-                }
-            } else if (wtid == 0) {
-                atom_add_acqrel_u32(p.bars + t.sig_bar, 1u);
-            }
+            if (wtid == 0) atom_add_acqrel_u32(p.bars + t.sig_bar, 1u);
             if (tr) tr[3] = gtimer();
         }
     }
@@ -852,10 +816,10 @@ AePlan ae_plan(const AePlanInput& in) {
     std::vector<std::vector<AeTask>> lists(size_t(in.num_ctas));
     std::vector<double> load(size_t(in.num_ctas), 0.0);
     using QE = std::pair<double, int>;
-    auto assign = [&](std::vector<Item>& items, bool distinct) {
+    auto assign = [&](std::vector<Item>& items) {
         // A CTA runs its tasks of one phase back to back, so a phase is spread over distinct CTAs
         // whenever it has at most one task per CTA (least-loaded CTAs first).
-        distinct = distinct || int(items.size()) <= in.num_ctas;
+        const bool distinct = int(items.size()) <= in.num_ctas;
         std::sort(items.begin(), items.end(), [](const Item& a, const Item& b) { return a.cost > b.cost; });
         std::priority_queue<QE, std::vector<QE>, std::greater<QE>> pq;
         for (int c = 0; c < in.num_ctas; ++c) pq.push({load[size_t(c)], c});
@@ -892,72 +856,59 @@ AePlan ae_plan(const AePlanInput& in) {
         const int per = (kb + s - 1) / s;
         return (kb + per - 1) / per;
     };
-    const double kWB = double(kWTile);
+    // Task cost for placement: its weight bytes, plus the fp32 staging of a full-K task.
+    const double kWB = double(kWBlk);
     const int rec = in.record ? 1 : 0;
     const int kbW = W / 64;
+    const int tiles_w = W / 64, tiles_qkv = NQ / 64, tiles_ffn = 2 * MLP / 64;
 
-    // ae.state_proj -> st
-    const int bar_init = newbar();
-    {
+    // One phase of independent full-K tasks (nonlinear epilogue, no reduction).
+    auto full_phase = [&](uint8_t xsrc, uint8_t epi, int tiles, int wmat, int xmat, int kbt, int wbar, int wcnt,
+                          int sbar, int step) {
         std::vector<Item> it;
-        for (int t = 0; t < W / 128; ++t)
-            it.push_back({gemm(kXRows, kEpiInit, in.mat_wst, 0, 0, t, 0, 1, 0, 0, bar_init), kWB});
-        assign(it, false);
-    }
-    const int tiles_w = W / 128;
-    int nstat = 0;
-    // split-K residual update: tasks (tile, k-range) with a per-tile arrival counter; the last
-    // arrival of a tile finalises it (yb + stats slot `slot`) and signals the phase counter.
-    auto split_phase = [&](uint8_t epi, int tiles, int wmat, int xmat, uint8_t xsrc, int rowoff, int kbt, int ks,
-                           int wbar, int wcnt, int pbar, int slot) {
+        for (int t = 0; t < tiles; ++t) {
+            AeTask x = gemm(xsrc, epi, wmat, xmat, 0, t, 0, kbt, wbar, wcnt, sbar);
+            x.step = uint16_t(step);
+            it.push_back({x, kbt * kWB * (xsrc == kXY ? 3.0 : 1.0)});
+        }
+        assign(it);
+        return int(it.size());
+    };
+    // Split-K residual update: every (tile, k-range) task adds its partial into y.
+    auto red_phase = [&](int wmat, int xmat, uint8_t xsrc, int rowoff, int kbt, int ks, int wbar, int wcnt, int sbar) {
         std::vector<Item> it;
         const int per = (kbt + ks - 1) / ks;
-        for (int t = 0; t < tiles; ++t) {
-            const int fin = newbar();
+        for (int t = 0; t < tiles_w; ++t)
             for (int k = 0; k < ks; ++k) {
                 const int kb0 = k * per, nkb = std::min(kbt, kb0 + per) - kb0;
                 if (nkb <= 0) continue;
-                AeTask x = gemm(xsrc, epi, wmat, xmat, rowoff, t, kb0, nkb, wbar, wcnt, pbar);
-                x.omat = uint16_t(fin);
-                x.aux = uint16_t(slot);
-                x.sig_cnt = uint16_t((kbt + per - 1) / per);
-                it.push_back({x, nkb * kWB});
+                it.push_back({gemm(xsrc, kEpiRed, wmat, xmat, rowoff, t, kb0, nkb, wbar, wcnt, sbar), nkb * kWB});
             }
-        }
-        assign(it, false);
+        assign(it);
+        return int(it.size());
     };
-    auto red_phase = [&](int wmat, int xmat, uint8_t xsrc, int rowoff, int kbt, int ks, int wbar, int wcnt, int pbar,
-                         int slot) { split_phase(kEpiRed, tiles_w, wmat, xmat, xsrc, rowoff, kbt, ks, wbar, wcnt, pbar, slot); };
-    const int ks_ao = splits_for(tiles_w, kbW, 32);
-    const int ks_proj = splits_for(tiles_w, in.q_width / 64, 128);
-    const int ks_down = splits_for(tiles_w, MLP / 64, 128);
-    const int tiles_qkv = NQ / 128, tiles_ffn = 2 * MLP / 128;
-    const int ks_qkv = splits_for(tiles_qkv, kbW, in.num_ctas), ks_ffn = splits_for(tiles_ffn, kbW, in.num_ctas);
+    const int ks_ao = splits_for(tiles_w, kbW, in.ao_tasks);
+    const int ks_proj = splits_for(tiles_w, in.q_width / 64, in.proj_tasks);
+    const int ks_down = splits_for(tiles_w, MLP / 64, in.down_tasks);
     const int pairs = (in.heads + 1) / 2;
     const int n_attn = pairs * splits;
-    int prev_bar = bar_init, prev_cnt = W / 128;
+
+    // ae.state_proj -> st
+    const int bar_init = newbar();
+    int prev_bar = bar_init;
+    int prev_cnt = full_phase(kXRows, kEpiInit, tiles_w, in.mat_wst, 0, 1, 0, 0, bar_init, 0);
     int rec_slot = 0;
     for (int s = 0; s < FS; ++s) {
         const int bar_ap = newbar();
-        {
-            std::vector<Item> it;
-            for (int t = 0; t < tiles_w; ++t) {
-                AeTask x = gemm(kXRows, kEpiSilu, in.mat_wap, 0, 0, t, 0, 1, prev_bar, prev_cnt, bar_ap);
-                x.step = uint16_t(s);
-                it.push_back({x, kWB});
-            }
-            assign(it, false);
-        }
+        const int n_ap = full_phase(kXRows, kEpiSilu, tiles_w, in.mat_wap, 0, 1, prev_bar, prev_cnt, bar_ap, s);
         const int bar_ao = newbar();
-        int slot = nstat++;
-        red_phase(in.mat_wao, in.mat_ap, kXBf16, 1, kbW, ks_ao, bar_ap, tiles_w, bar_ao, slot);
+        prev_cnt = red_phase(in.mat_wao, in.mat_ap, kXBf16, 1, kbW, ks_ao, bar_ap, n_ap, bar_ao);
         prev_bar = bar_ao;
-        prev_cnt = tiles_w;
         for (int l = 0; l < NA; ++l) {
             const int gl = s * NA + l;
             const int bar_qkv = newbar();
-            split_phase(kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], in.mat_yb, kXBf16, 0, kbW, ks_qkv, prev_bar, prev_cnt,
-                        bar_qkv, slot);
+            const int n_qkv = full_phase(kXY, kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], in.mat_y, kbW, prev_bar,
+                                         prev_cnt, bar_qkv, s);
             const int bar_attn = newbar();
             {
                 std::vector<Item> it;
@@ -970,48 +921,47 @@ AePlan ae_plan(const AePlanInput& in) {
                         x.kb0 = uint16_t(j);
                         x.nkb = uint16_t(std::min(kBlocksPerSplit, in.key_blocks - j * kBlocksPerSplit));
                         x.wait_bar = uint16_t(bar_qkv);
-                        x.wait_cnt = uint16_t(tiles_qkv);
+                        x.wait_cnt = uint16_t(n_qkv);
                         x.sig_bar = uint16_t(bar_attn);
                         x.step = uint16_t(s);
                         x.layer = uint16_t(l);
                         x.phase = uint16_t(phase);
-                        it.push_back({x, 6.0 * kWB});
+                        it.push_back({x, 12.0 * kWB});
                     }
-                assign(it, true);
+                assign(it);
             }
             const int bar_proj = newbar();
-            slot = nstat++;
-            red_phase(in.mat_wproj[size_t(l)], 0, kXO, 0, in.q_width / 64, ks_proj, bar_attn, n_attn, bar_proj, slot);
+            const int n_proj = red_phase(in.mat_wproj[size_t(l)], 0, kXO, 0, in.q_width / 64, ks_proj, bar_attn, n_attn,
+                                         bar_proj);
             const int bar_ffn = newbar();
-            split_phase(kEpiGate, tiles_ffn, in.mat_wffn[size_t(l)], in.mat_yb, kXBf16, 0, kbW, ks_ffn, bar_proj, tiles_w,
-                        bar_ffn, slot);
+            const int n_ffn = full_phase(kXY, kEpiGate, tiles_ffn, in.mat_wffn[size_t(l)], in.mat_y, kbW, bar_proj,
+                                         n_proj, bar_ffn, s);
             const int bar_down = newbar();
-            slot = nstat++;
-            red_phase(in.mat_wdown[size_t(l)], in.mat_g, kXBf16, 0, MLP / 64, ks_down, bar_ffn, tiles_ffn, bar_down, slot);
+            prev_cnt = red_phase(in.mat_wdown[size_t(l)], in.mat_g, kXBf16, 0, MLP / 64, ks_down, bar_ffn, n_ffn, bar_down);
             if (rec) {
                 std::vector<Item> it;
                 AeTask x{};
                 x.kind = kAeRecY;
                 x.wait_bar = uint16_t(bar_down);
-                x.wait_cnt = uint16_t(tiles_w);
+                x.wait_cnt = uint16_t(prev_cnt);
                 x.sig_bar = uint16_t(bar_down);
                 x.aux = uint16_t(rec_slot++);
                 x.phase = uint16_t(phase);
                 it.push_back({x, kWB});
-                assign(it, false);
+                assign(it);
+                prev_cnt += 1;
             }
             prev_bar = bar_down;
-            prev_cnt = tiles_w + rec;
         }
         const int bar_head = newbar();
         {
             std::vector<Item> it;
-            AeTask x = gemm(kXBf16, kEpiHead, in.mat_whead, in.mat_ybh, 0, 0, 0, kbW, prev_bar, prev_cnt, bar_head);
-            x.aux = uint16_t(slot);
+            AeTask x = gemm(kXY, kEpiHead, in.mat_whead, in.mat_yh, 0, 0, 0, kbW, prev_bar, prev_cnt, bar_head);
             x.step = uint16_t(s);
-            it.push_back({x, kbW * kWB / 4});
-            assign(it, false);
+            it.push_back({x, 3.0 * kbW * kWB});
+            assign(it);
         }
+        prev_cnt = 1;
         if (rec) {
             std::vector<Item> it;
             AeTask x{};
@@ -1022,10 +972,10 @@ AePlan ae_plan(const AePlanInput& in) {
             x.aux = uint16_t(s);
             x.phase = uint16_t(phase);
             it.push_back({x, kWB});
-            assign(it, false);
+            assign(it);
+            prev_cnt = 2;
         }
         prev_bar = bar_head;
-        prev_cnt = 1 + rec;
     }
     need(nbar < 65535 && phase < 65535, "task table too large");
     size_t stride = 0;
@@ -1039,7 +989,6 @@ AePlan ae_plan(const AePlanInput& in) {
     out.n_tasks = 0;
     for (auto& l : lists) out.n_tasks += int(l.size());
     out.attn_splits = splits;
-    out.n_stats = nstat;
     out.max_load = *std::max_element(load.begin(), load.end());
     out.min_load = *std::min_element(load.begin(), load.end());
     return out;

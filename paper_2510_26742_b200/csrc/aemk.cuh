@@ -4,15 +4,20 @@
 // persistent launch of one CTA per SM.
 //
 // The host turns the fused graph into a static task table: every node instance is split into
-// tasks (a 128-feature output tile over a range of 64-wide k-blocks, or one attention
+// tasks (a 64-feature output tile over a range of 64-wide k-blocks, or one attention
 // (head-pair, key-range) tile), tasks are assigned to CTAs, and each CTA walks its own list in
 // global phase order.  Ordering between node instances uses phase counters instead of kernel
-// boundaries: the task that completes a phase sets that phase's flag in every CTA's mailbox
-// line, and a task waits on the flag of the phase it reads.  Weights never depend on
-// activations, so a dedicated producer warp streams each CTA's weight tiles through a
-// shared-memory ring ahead of all dependency waits: HBM keeps streaming the next layer's
+// boundaries: every task bumps its phase's counter with a release atomic, and a task waits
+// until the counter of the phase it reads reaches that phase's task count.  Weights never
+// depend on activations, so a dedicated producer warp streams each CTA's weight tiles through
+// a shared-memory ring ahead of all dependency waits: HBM keeps streaming the next layer's
 // weights while the current layer's dependencies resolve (the "software barrier" + weight
 // prefetch of PAPER.md:232-242 / SURVEY.md 7.3).
+//
+// No task ever finalises another task's output: the nonlinear GEMMs (ae.qkv, ae.ffn,
+// ae.head) run over the full K and read the fp32 residual stream directly, computing the
+// RmsStats row sums of squares while they stage it; only the residual updates (ae.proj,
+// ae.down, ae.action_out) are split over K, and they add straight into the residual stream.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -29,14 +34,14 @@ enum AeTaskKind : uint8_t { kAeEnd = 0, kAeGemm = 1, kAeAttn = 2, kAeRecY = 3, k
 // How the 64-row activation operand of a GEMM task reaches shared memory (always cp.async).
 enum AeXSrc : uint8_t {
     kXBf16 = 0,  // bf16 rows straight into the swizzled operand slot
-    kXY = 1,     // fp32 residual stream; workers convert to bf16 and accumulate the row sums of
-                 // squares (the RmsStats node, proj/src/evaluate.cpp:308-309) for the epilogue
+    kXY = 1,     // fp32 residual stream (full K); workers convert to bf16 and accumulate the row
+                 // sums of squares (the RmsStats node, proj/src/evaluate.cpp:308-309)
     kXO = 2,     // attention partials (bf16, per key range, with row max / sum): combined
     kXRows = 3,  // small fp32 rows (Euler state / robot state), K <= 64
 };
 
 enum AeEpi : uint8_t {
-    kEpiRed = 0,   // fp32 partial -> red.add into the residual stream (Residual epilogue)
+    kEpiRed = 0,   // fp32 split-K partial -> red.add into the residual stream (Residual epilogue)
     kEpiQkv = 1,   // RmsScale -> RoPE -> bf16 q | k | v   (ae.ln1 + ae.qkv)
     kEpiGate = 2,  // RmsScale -> up * gelu(gate) -> bf16  (ae.ln2 + ae.ffn)
     kEpiSilu = 3,  // silu(z + bias_table[step]) -> bf16; resets y = [st ; b_out] (ae.action_proj)
@@ -53,15 +58,15 @@ static_assert(sizeof(AeMat) == 32, "AeMat layout");
 
 struct AeTask {
     uint8_t kind, xsrc, epi, rowoff;  // rowoff: kEpiRed target rows start at y row `rowoff`
-    uint16_t wmat, xmat, omat;        // AeMat indices (weights / activation); split-K: tile counter
-    uint16_t tile;                    // GEMM: 128-feature output tile; ATTN: head pair
+    uint16_t wmat, xmat, pad0;        // AeMat indices (weights / activation)
+    uint16_t tile;                    // GEMM: 64-feature output tile; ATTN: head pair
     uint16_t kb0, nkb;                // GEMM: k-block range; ATTN: key split, #key blocks
-    uint16_t wait_bar, wait_cnt;      // wait until phase wait_bar completed (cnt > 0)
-    uint16_t sig_bar;                 // phase this task belongs to
-    uint16_t aux;                     // split-K: stats slot; QKV/FFN/HEAD: stats slot read; REC: slot
+    uint16_t wait_bar, wait_cnt;      // wait until counter wait_bar reaches wait_cnt (cnt > 0)
+    uint16_t sig_bar;                 // counter of the phase this task belongs to
+    uint16_t aux;                     // REC: record slot
     uint16_t step, layer;             // flow step, AE layer
     uint16_t phase;                   // global phase index (debug limit)
-    uint16_t sig_cnt;                 // split-K: splits per tile (the last one finalises the tile)
+    uint16_t pad1;
 };
 static_assert(sizeof(AeTask) == 32, "AeTask layout");
 
@@ -70,18 +75,13 @@ struct AeParams {
     int task_stride;               // tasks per CTA row of the table
     const AeMat* mats;             // operand table
     unsigned* bars;                // [n_bars] phase arrival counters, zero on entry
-    unsigned* mbox;                // [ctas][n_bars] phase-complete flags, zero on entry
     int n_bars;
     float* y;                      // [64, W]   residual stream (row 0 = state token)
-    __nv_bfloat16* yb;             // [64, W]   bf16 shadow of y, written by each tile's finaliser
-    float* stats;                  // [n_stats][64] row sums of squares of y per residual update
     float* a;                      // [C, lda]  Euler state
     int lda;
     const float* state;            // [state_dim] fp32
     float* st;                     // [W] state token (ae.state_proj output)
     __nv_bfloat16* qkv;            // [64, n_qkv]
-    float* qacc;                   // [64, n_qkv]   split-K accumulator of ae.qkv (packed columns)
-    float* facc;                   // [64, 2 * mlp] split-K accumulator of ae.ffn (packed columns)
     __nv_bfloat16* ap;             // [C, W]
     __nv_bfloat16* g;              // [64, mlp]
     __nv_bfloat16* opart;          // [splits][64, q_width] normalised attention partials
@@ -101,7 +101,6 @@ struct AeParams {
     int attn_splits;               // key ranges per head pair (<= 3 key blocks each)
     float scale_log2, inv_width, eps, euler;
     int limit_phase;               // run only tasks with phase < limit (debug / parity probes)
-    int w_inflight;                // weight tiles in flight per CTA
     unsigned long long* trace;     // optional [ctas][stride][16] globaltimer stamps per task
     unsigned long long* dbg;       // optional [ctas][128] per-k-block stamps of the first ae.qkv task
 };
@@ -112,14 +111,21 @@ struct AePlanInput {
     int width, n_qkv, q_width, mlp, layers, flow_steps, heads, chunk, act_dim, state_dim;
     int rope_cols, kv_rows0, key_blocks;
     bool record;
+    int ao_tasks = 64, proj_tasks = 128, down_tasks = 128;  // split-K task targets per phase
     int mat_wst, mat_wap, mat_wao, mat_whead;
     std::vector<int> mat_wqkv, mat_wproj, mat_wffn, mat_wdown, mat_kv;
-    int mat_yb, mat_ybh, mat_ap, mat_g, mat_qkv;
+    int mat_y, mat_yh, mat_ap, mat_g, mat_qkv;  // fp32 y rows 0.. / rows 1.. (ae.act_rows)
 };
+
+// Weight row order of one 64-feature tile of a tile-contiguous AE weight copy
+// (kernels_misc.cu tile_weight_kernel): plain, or "paired" — tile 2T + s of a matrix packed in
+// 128-row groups [64 | 64 partners] (kPermRope qkv, kPermGate64 ffn) takes rows
+// 128T + 32s + [0, 32) followed by their partners 128T + 64 + 32s + [0, 32).
+enum AeTileOrder : int { kTilePlain = 0, kTilePaired = 1 };
 
 struct AePlan {
     std::vector<AeTask> table;  // [num_ctas][stride]
-    int stride = 0, n_bars = 0, n_phases = 0, n_tasks = 0, attn_splits = 1, n_stats = 0;
+    int stride = 0, n_bars = 0, n_phases = 0, n_tasks = 0, attn_splits = 1;
     double max_load = 0, min_load = 0;  // weight bytes per CTA
 };
 

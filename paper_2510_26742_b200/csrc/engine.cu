@@ -50,7 +50,7 @@ cudaError_t launch_gen_weight(__nv_bfloat16* dst, long long ldk, int k, int m, i
                               uint64_t seed, double lo, double hi, cudaStream_t st);
 cudaError_t launch_pack_weight(__nv_bfloat16* dst, long long ldk, const double* w, int k, int m,
                                int perm, int rope_cols, cudaStream_t st);
-cudaError_t launch_tile_weight(const __nv_bfloat16* src, int rows, int k, long long ldk, __nv_bfloat16* dst,
+cudaError_t launch_tile_weight(const __nv_bfloat16* src, int rows, int k, long long ldk, __nv_bfloat16* dst, int order,
                                cudaStream_t st);
 cudaError_t skinny_configure();
 int skinny_tiles(int n_packed);
@@ -272,7 +272,7 @@ public:
     int kernel_count(int part) const;
     void prepare() {
         if (ae_mega_ && ae_tiles_dirty_) {
-            for (const TiledW& tw : ae_tiled_) PI0B_CUDA(launch_tile_weight(tw.src, tw.rows, tw.k, tw.ldk, tw.dst, stream_));
+            for (const TiledW& tw : ae_tiled_) PI0B_CUDA(launch_tile_weight(tw.src, tw.rows, tw.k, tw.ldk, tw.dst, tw.order, stream_));
             PI0B_CUDA(cudaStreamSynchronize(stream_));
             ae_tiles_dirty_ = false;
         }
@@ -352,8 +352,9 @@ private:
         int rows, k;
         long long ldk;
         __nv_bfloat16* dst;
+        int order;  // AeTileOrder
     };
-    std::vector<TiledW> ae_tiled_;  // AE weights re-laid out as contiguous 16 KB tiles
+    std::vector<TiledW> ae_tiled_;  // AE weights re-laid out as contiguous 8 KB tiles
     bool ae_tiles_dirty_ = true;
     void* ae_zero_ = nullptr;
     size_t ae_zero_bytes_ = 0;
@@ -1074,12 +1075,12 @@ void Engine::build_ae_mega() {
         mats.push_back(AeMat{ptr, rows, cols, int(ld), {0, 0, 0}});
         return int(mats.size()) - 1;
     };
-    auto wmat = [&](const char* node, int inst, int rows) {
-        // tile-contiguous copy: AeMat{ptr, rows, k, k-blocks}
+    auto wmat = [&](const char* node, int inst, int rows, int order = kTilePlain) {
+        // tile-contiguous copy of 64-row tiles: AeMat{ptr, rows, k, k-blocks}
         const NodeWeights& nw = W_.at(node);
-        const int kb = (nw.k + 63) / 64, nt = (rows + 127) / 128;
-        __nv_bfloat16* t = alloc<__nv_bfloat16>(size_t(nt) * kb * 8192);
-        ae_tiled_.push_back({nw.w.at(size_t(inst)), rows, nw.k, nw.ldk, t});
+        const int kb = (nw.k + 63) / 64, nt = (rows + 63) / 64;
+        __nv_bfloat16* t = alloc<__nv_bfloat16>(size_t(nt) * kb * 4096);
+        ae_tiled_.push_back({nw.w.at(size_t(inst)), rows, nw.k, nw.ldk, t, order});
         mats.push_back(AeMat{t, rows, nw.k, kb, {0, 0, 0}});
         return int(mats.size()) - 1;
     };
@@ -1099,22 +1100,24 @@ void Engine::build_ae_mega() {
     in.kv_rows0 = L_;
     in.key_blocks = (L_ + S_ + 63) / 64;
     in.record = o_.record_checkpoints != 0;
+    in.ao_tasks = env_int("PI0B_AE_AO_TASKS", in.ao_tasks);
+    in.proj_tasks = env_int("PI0B_AE_PROJ_TASKS", in.proj_tasks);
+    in.down_tasks = env_int("PI0B_AE_DOWN_TASKS", in.down_tasks);
     in.mat_wst = wmat("ae.state_proj", 0, W);
     in.mat_wap = wmat("ae.action_proj", 0, W);
     in.mat_wao = wmat("ae.action_out", 0, W);
     in.mat_whead = wmat("ae.head", 0, c.ae_action_dim);
     for (int l = 0; l < NA; ++l) {
-        in.mat_wqkv.push_back(wmat("ae.qkv", l, NQ));
+        in.mat_wqkv.push_back(wmat("ae.qkv", l, NQ, kTilePaired));
         in.mat_wproj.push_back(wmat("ae.proj", l, W));
-        in.mat_wffn.push_back(wmat("ae.ffn", l, 2 * MLP));
+        in.mat_wffn.push_back(wmat("ae.ffn", l, 2 * MLP, kTilePaired));
         in.mat_wdown.push_back(wmat("ae.down", l, W));
     }
     const int llm_qkv_n = llm_q_ + 2 * llm_kv_;
     for (int l = 0; l < c.llm_layers; ++l)  // AE instance i reads LLM layer i % llm_layers (@mod)
         in.mat_kv.push_back(add(kv_[size_t(l)], L_, llm_qkv_n, llm_qkv_n));
-    __nv_bfloat16* yb = alloc<__nv_bfloat16>(size_t(S_) * W);
-    in.mat_yb = add(yb, S_, W, W);
-    in.mat_ybh = add(yb + W, C_, W, W);
+    in.mat_y = add(y_, S_, W, W);
+    in.mat_yh = add(y_ + W, C_, W, W);  // ae.act_rows: rows 1..63
     in.mat_ap = add(ap_b_, C_, W, W);
     in.mat_g = add(ag_, S_, MLP, MLP);
     in.mat_qkv = add(aqkv_, S_, NQ, NQ);
@@ -1123,11 +1126,8 @@ void Engine::build_ae_mega() {
     } catch (const std::invalid_argument& e) {
         throw EngineError(PI0B_E_UNSUPPORTED, e.what());
     }
-    // zero-on-entry region: phase / tile counters | row-statistics slots
-    const size_t bar_bytes = size_t(round_up(ae_plan_.n_bars * 4, 256));
-    const size_t stat_bytes = size_t(round_up(ae_plan_.n_stats * 64 * 4, 256));
-    const size_t qacc_bytes = size_t(64) * NQ * 4, facc_bytes = size_t(64) * 2 * MLP * 4;
-    ae_zero_bytes_ = bar_bytes + stat_bytes + qacc_bytes + facc_bytes;
+    // zero-on-entry region: the phase counters
+    ae_zero_bytes_ = size_t(round_up(ae_plan_.n_bars * 4, 256));
     uint8_t* z = alloc<uint8_t>(ae_zero_bytes_);
     ae_zero_ = z;
     __nv_bfloat16* opart = alloc<__nv_bfloat16>(size_t(ae_plan_.attn_splits) * 64 * ae_q_);
@@ -1151,13 +1151,8 @@ void Engine::build_ae_mega() {
     P.task_stride = ae_plan_.stride;
     P.mats = dmats;
     P.bars = reinterpret_cast<unsigned*>(z);
-    P.mbox = nullptr;
     P.n_bars = ae_plan_.n_bars;
     P.y = y_;
-    P.yb = yb;
-    P.stats = reinterpret_cast<float*>(z + bar_bytes);
-    P.qacc = reinterpret_cast<float*>(z + bar_bytes + stat_bytes);
-    P.facc = reinterpret_cast<float*>(z + bar_bytes + stat_bytes + qacc_bytes);
     P.a = a_;
     P.lda = act_ld_;
     P.state = state32_;
@@ -1194,7 +1189,6 @@ void Engine::build_ae_mega() {
     P.eps = 1e-6f;
     P.euler = float(1.0 / double(FS_));
     P.limit_phase = env_int("PI0B_AE_LIMIT", 1 << 30);
-    P.w_inflight = env_int("PI0B_AE_WINFLIGHT", 8);
     P.trace = nullptr;
     P.dbg = nullptr;
     if (env_int("PI0B_AE_TRACE", 0)) {
@@ -1398,7 +1392,7 @@ void Engine::capture(int part, int slot) {
 void Engine::launch(int part, cudaStream_t st) {
     if (!weights_loaded_) throw EngineError(PI0B_E_STATE, "weights not loaded");
     if (ae_mega_ && ae_tiles_dirty_) {  // (re)build the tile-contiguous AE weight copies
-        for (const TiledW& tw : ae_tiled_) PI0B_CUDA(launch_tile_weight(tw.src, tw.rows, tw.k, tw.ldk, tw.dst, stream_));
+        for (const TiledW& tw : ae_tiled_) PI0B_CUDA(launch_tile_weight(tw.src, tw.rows, tw.k, tw.ldk, tw.dst, tw.order, stream_));
         PI0B_CUDA(cudaStreamSynchronize(stream_));
         ae_tiles_dirty_ = false;
     }

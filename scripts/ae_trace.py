@@ -25,10 +25,10 @@ lib = E.lib()
 lib.pi0b_engine_ae_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
 cap = 148 * 4096
-dt = np.dtype([("kind", "u1"), ("xsrc", "u1"), ("epi", "u1"), ("par", "u1"), ("wmap", "<u2"), ("xmap", "<u2"),
-               ("omap", "<u2"), ("tile", "<u2"), ("kb0", "<u2"), ("nkb", "<u2"), ("wait_bar", "<u2"),
+dt = np.dtype([("kind", "u1"), ("xsrc", "u1"), ("epi", "u1"), ("rowoff", "u1"), ("wmap", "<u2"), ("xmap", "<u2"),
+               ("pad0", "<u2"), ("tile", "<u2"), ("kb0", "<u2"), ("nkb", "<u2"), ("wait_bar", "<u2"),
                ("wait_cnt", "<u2"), ("sig_bar", "<u2"), ("aux", "<u2"), ("step", "<u2"), ("layer", "<u2"),
-               ("phase", "<u2"), ("sig_cnt", "<u2")])
+               ("phase", "<u2"), ("pad1", "<u2")])
 tasks = np.zeros(cap, dtype=dt)
 st = np.zeros((cap + 148 * 8, 16), dtype=np.uint64)
 ctas, stride = ctypes.c_int(), ctypes.c_int()
@@ -53,7 +53,7 @@ for p in sorted(ph):
         nm = "ATTN"
     elif tk["kind"] == 1 and tk["epi"] == 0:
         nm = {0: "AO/DOWN", 2: "PROJ"}.get(int(tk["xsrc"]), "RED")
-        if tk["xsrc"] == 0 and tk["omap"] != tasks[ph[max(ph)][0]]["omap"]:
+        if tk["xsrc"] == 0 and tk["rowoff"] == 1:
             nm = "AO"
     else:
         nm = names.get((int(tk["kind"]), int(tk["epi"])), f"K{tk['kind']}")
@@ -110,7 +110,7 @@ for r in rows:
         prev_end = r[5]
 for r in mid:
     idx = np.array(ph[r[0]])
-    if tasks["kind"][idx[0]] != 1 or tasks["sig_cnt"][idx[0]] == 0:
+    if tasks["kind"][idx[0]] != 1 or True:
         prev_end = r[5]
         continue
     s8 = st[idx].astype(np.float64)
