@@ -40,19 +40,21 @@ constexpr int kAeThreads = 320;
 constexpr int kWorkers = 256;
 constexpr int kWBlk = 64 * 64 * 2;    // 8 KB: [64 features x 64 k] bf16 SW128 image
 constexpr int kWSlot = 2 * kWBlk;     // ring slot: up to two consecutive k-blocks, one bulk copy
-constexpr int kWSt = 5;
+constexpr int kWSt = 3;
+constexpr int kWPrefetch = 0;  // weight bytes a CTA keeps bulk-prefetched into L2 ahead
 constexpr int kXSt = 4;
 constexpr int kXTile = 64 * 128;      // 8 KB: 64 activation rows x 64 k
+constexpr int kXSlot = 2 * kXTile;    // X ring slot: two k-blocks, one handshake
 constexpr int kFSt = 5;
 constexpr int kFTile = 16384;         // fp32 staging of one k-block: 64 rows x 64 columns
 constexpr int kMaxSplits = 10;        // attention key ranges combined by the ae.proj staging
 constexpr int kORegion = 81920;       // partial staging: 2 slots of <= 5 ranges, or 1 slot of <= 10
 constexpr int kBlocksPerSplit = 2;    // 64-key blocks per attention task
 constexpr int kOffW = 0;
-constexpr int kOffU = kWSt * kWSlot;                // union region (128 KB)
-constexpr int kUnion = 131072;
-constexpr int kOffX = kOffU;                        // GEMM: X ring (+1 pad slot: rows 64..127 of A)
-constexpr int kOffF = kOffU + (kXSt + 1) * kXTile;  // GEMM: fp32 ring (kXY) or partial ring (kXO)
+constexpr int kOffU = kWSt * kWSlot;                // union region (160 KB)
+constexpr int kUnion = 163840;
+constexpr int kOffX = kOffU;                        // GEMM: X ring (+8 KB pad: rows 64..127 of A)
+constexpr int kOffF = kOffU + kXSt * kXSlot + kXTile;  // GEMM: fp32 ring (kXY) / partial ring (kXO)
 constexpr int kOffQ = kOffU;                        // ATTN: Q [128 x 256] = 4 x 16 KB
 constexpr int kOffK = kOffU + 65536;                // ATTN: K [2 blocks][64 x 256] = 2 x 32 KB
 constexpr int kOffP = kOffQ;                        // ATTN: P [128 x 128 keys] (reuses Q)
@@ -66,9 +68,9 @@ static_assert(kAeSmem <= 232448, "shared memory budget");
 constexpr uint32_t kTAcc = 0, kTS = 0, kTO = 256;  // TMEM columns (512 allocated)
 
 // mbarrier slots
-constexpr int kBWFull = 0, kBWEmpty = 8, kBXFull = 16, kBXEmpty = 20, kBAccFull = 32, kBAccEmpty = 33,
+constexpr int kBWFull = 0, kBWEmpty = 8, kBXFull = 16, kBXEmpty = 24, kBAccFull = 32, kBAccEmpty = 33,
               kBQFull = 34, kBSFull = 35, kBVFull = 36, kBPFull = 37, kBODone = 38, kNumBars = 39;
-static_assert(kWSt <= 8 && kXSt <= 4, "barrier slots");
+static_assert(kWSt <= 8 && kXSt <= 8, "barrier slots");
 
 PI0B_DEV unsigned ld_relaxed_u32(const unsigned* p) {
     unsigned v;
@@ -184,6 +186,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
         for (int i = 0; i < kNumBars; ++i) {
             uint32_t cnt = 1;
             if ((i >= kBXFull && i < kBXFull + kXSt) || i == kBQFull || i == kBVFull) cnt = kWorkers;
+            if (i >= kBWFull && i < kBWFull + kWSt) cnt = 32;  // producer lanes' cp.async arrivals
             mbar_init(&mb[i], cnt);
         }
         fence_barrier_init();
@@ -197,24 +200,50 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
     if (warp == 0) {
         // ================================================================ weight producer
         // Tile-contiguous weights (kernels_misc.cu tile_weight_kernel): the k-blocks of one tile
-        // are consecutive 8 KB swizzled images, so two of them are one 16 KB bulk copy.
+        // are consecutive 8 KB swizzled images, so two of them are one 16 KB bulk copy.  A
+        // second cursor keeps the next kWPrefetch bytes of this CTA's weights bulk-prefetched
+        // into L2, so ring refills see L2 latency, not HBM latency under load.
         int ws = 0;
         uint32_t wph = 0;
+        int pj = 0;
+        long long ahead = 0;  // prefetched bytes of tasks >= i
+        bool pend = false;
         for (int i = 0;; ++i) {
             const AeTask t = load_task(my + i);
             if (t.kind == kAeEnd || t.phase >= p.limit_phase) break;
+            if (pj <= i) pj = i;
+            while (!pend && ahead < kWPrefetch) {
+                const AeTask u = load_task(my + pj);
+                if (u.kind == kAeEnd || u.phase >= p.limit_phase) {
+                    pend = true;
+                    break;
+                }
+                if (u.kind == kAeGemm) {
+                    const AeMat um = load_mat(p.mats + u.wmat);
+                    const uint8_t* ub = reinterpret_cast<const uint8_t*>(um.ptr) + ((size_t)u.tile * um.ld + u.kb0) * kWBlk;
+                    const uint32_t bytes = uint32_t(u.nkb) * kWBlk;
+                    if (lane == 0)
+                        for (uint32_t o = 0; o < bytes; o += 65536) bulk_prefetch_l2(ub + o, min(65536u, bytes - o));
+                    ahead += bytes;
+                }
+                ++pj;
+            }
             if (t.kind != kAeGemm) continue;
+            if (pj > i) ahead -= (long long)t.nkb * kWBlk;
             unsigned long long* tr = (p.trace && lane == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
             const AeMat wm = load_mat(p.mats + t.wmat);
             const uint8_t* base = reinterpret_cast<const uint8_t*>(wm.ptr) + ((size_t)t.tile * wm.ld + t.kb0) * kWBlk;
             for (int k = 0; k < t.nkb; k += 2) {
-                const uint32_t bytes = uint32_t(min(2, t.nkb - k)) * kWBlk;
+                const int bytes = min(2, t.nkb - k) * kWBlk;
                 mbar_wait(&w_empty[ws], wph ^ 1);
                 if (tr && k == 0) tr[4] = gtimer();
-                if (lane == 0) {
-                    mbar_arrive_expect_tx(&w_full[ws], bytes);
-                    bulk_g2s(sW + ws * kWSlot, base + (size_t)k * kWBlk, bytes, &w_full[ws], kEvictFirst);
-                }
+                // warp-wide cp.async: each instruction moves 512 contiguous bytes; the slot's
+                // w_full completes when all 32 lanes' copies have landed (noinc arrivals)
+                const uint8_t* src = base + (size_t)k * kWBlk + lane * 16;
+                uint8_t* dst = sW + ws * kWSlot + lane * 16;
+#pragma unroll 8
+                for (int o = 0; o < bytes; o += 512) cp_async16_hint(dst + o, src + o, kEvictFirst);
+                cp_async_arrive_noinc(&w_full[ws]);
                 adv(ws, wph, 1, kWSt);
             }
             if (tr) tr[5] = gtimer();
@@ -234,28 +263,32 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 if (t.kind == kAeEnd || t.phase >= p.limit_phase) break;
                 unsigned long long* tr = (p.trace && lane == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
                 if (t.kind == kAeGemm) {
+                    unsigned long long* dbg = (p.dbg && lane == 0 && t.epi == kEpiQkv && t.step == 1 && t.layer == 5)
+                                                  ? p.dbg + size_t(blockIdx.x) * 128 + 64 : nullptr;
                     mbar_wait(acc_empty, (gidx & 1) ^ 1);
+                    // one W chunk and one X slot per step: two k-blocks (8 MMAs) per handshake
                     for (int k = 0; k < t.nkb; k += 2) {
                         const int n = min(2, t.nkb - k);
+                        if (dbg) dbg[k * 4] = gtimer();
                         mbar_wait(&w_full[ws], wph);
+                        if (dbg) dbg[k * 4 + 1] = gtimer();
                         if (tr && k + n == t.nkb) tr[6] = gtimer();
-                        for (int j = 0; j < n; ++j) {
-                            mbar_wait(&x_full[xs], xph);
-                            fence_proxy_async_smem();  // cp.async / st.shared data -> tensor-core reads
-                            tc_fence_after();
-                            const uint64_t ad = umma_desc_sw128(sX + xs * kXTile);
-                            const uint64_t bd = umma_desc_sw128(sW + ws * kWSlot + j * kWBlk);
-                            if (elect_one()) {
-#pragma unroll
-                                for (int kk = 0; kk < 4; ++kk)
-                                    umma_bf16(tmem + kTAcc, ad + 2 * kk, bd + 2 * kk, idesc_g, (k + j + kk) != 0);
-                                umma_commit(&x_empty[xs]);
-                            }
-                            __syncwarp();
-                            adv(xs, xph, 1, kXSt);
+                        mbar_wait(&x_full[xs], xph);
+                        if (dbg) dbg[k * 4 + 2] = gtimer();
+                        fence_proxy_async_smem();  // cp.async / st.shared data -> tensor-core reads
+                        tc_fence_after();
+                        const uint64_t ad = umma_desc_sw128(sX + xs * kXSlot);
+                        const uint64_t bd = umma_desc_sw128(sW + ws * kWSlot);
+                        if (elect_one()) {
+                            for (int q = 0; q < 4 * n; ++q)  // k-block j = q >> 2 is 8 KB (512 desc units) on
+                                umma_bf16(tmem + kTAcc, ad + (q >> 2) * 512 + 2 * (q & 3), bd + (q >> 2) * 512 + 2 * (q & 3),
+                                          idesc_g, (k + q) != 0);
+                            umma_commit(&x_empty[xs]);
+                            umma_commit(&w_empty[ws]);
                         }
-                        if (elect_one()) umma_commit(&w_empty[ws]);
                         __syncwarp();
+                        if (dbg) dbg[k * 4 + 3] = gtimer();
+                        adv(xs, xph, 1, kXSt);
                         adv(ws, wph, 1, kWSt);
                     }
                     if (elect_one()) umma_commit(acc_full);
@@ -334,65 +367,76 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 const AeMat xm = load_mat(p.mats + t.xmat);
                 if (t.xsrc == kXBf16) {
                     const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(xm.ptr);
-                    for (int k = 0; k < t.nkb; ++k) {
+                    for (int k = 0; k < t.nkb; k += 2) {
+                        const int n = min(2, t.nkb - k);
                         mbar_wait(&x_empty[xs], xph ^ 1);
-                        const int kc = (t.kb0 + k) * 64;
+                        for (int j = 0; j < n; ++j) {
+                            const int kc = (t.kb0 + k + j) * 64;
 #pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            const int q = wtid + 256 * u;
-                            const int row = q >> 3, c = q & 7;
-                            const bool ok = row < xm.rows;
-                            cp_async16(sX + xs * kXTile + swz(row, c), ok ? xb + (size_t)row * xm.ld + kc + c * 8 : xb, ok);
+                            for (int u = 0; u < 2; ++u) {
+                                const int q = wtid + 256 * u;
+                                const int row = q >> 3, c = q & 7;
+                                const bool ok = row < xm.rows;
+                                cp_async16(sX + xs * kXSlot + j * kXTile + swz(row, c), ok ? xb + (size_t)row * xm.ld + kc + c * 8 : xb,
+                                           ok);
+                            }
                         }
                         cp_async_arrive_noinc(&x_full[xs]);
                         adv(xs, xph, 1, kXSt);
                     }
                 } else if (t.xsrc == kXY) {
-                    // fp32 residual rows over the full K: each thread cp.asyncs its own 64 bytes
-                    // (row sr, columns 16 sq..) of every k-block into a private slice of the fp32
-                    // ring (kFSt - 1 k-blocks in flight), converts them to bf16 into the operand
-                    // slot and accumulates the row's sum of squares (RmsStats).
+                    // fp32 residual rows over the full K, coalesced: for k-block k, thread
+                    // q = wtid + 256 u (u < 4) cp.asyncs 16 bytes (row q >> 4, columns 4 (q & 15)..)
+                    // into its own slot of the fp32 ring (a half-warp reads one row's 256-byte
+                    // segment), then converts them to bf16 into the operand slot and accumulates
+                    // the row's sum of squares (RmsStats); kFSt - 1 k-blocks in flight.
                     const float* yf = reinterpret_cast<const float*>(xm.ptr);
-                    const bool okr = sr < xm.rows;
-                    const float* src0 = yf + (size_t)(okr ? sr : 0) * xm.ld + t.kb0 * 64 + sq * 16;
-                    const int rot = (wtid >> 1) & 3;  // 16-byte piece rotation: conflict-free LDS
+                    const float* src0 = yf + t.kb0 * 64 + (wtid & 15) * 4;
                     auto issue = [&](int k) {
                         if (k < t.nkb) {
-                            uint8_t* dst = sF + (k % kFSt) * kFTile + wtid * 64;
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) cp_async16(dst + ((u ^ rot) << 4), src0 + k * 64 + u * 4, okr);
+                            for (int u = 0; u < 4; ++u) {
+                                const int row = (wtid >> 4) + 16 * u;
+                                const bool ok = row < xm.rows;
+                                cp_async16(sF + (k % kFSt) * kFTile + (wtid + 256 * u) * 16, src0 + (size_t)(ok ? row : 0) * xm.ld + k * 64, ok);
+                            }
                         }
                         cp_async_commit();
                     };
 #pragma unroll 1
                     for (int k = 0; k < kFSt - 1; ++k) issue(k);
-                    float ss = 0.f;
+                    float ss[4] = {0.f, 0.f, 0.f, 0.f};
+                    const int c = wtid & 15;
 #pragma unroll 1
                     for (int k = 0; k < t.nkb; ++k) {
                         issue(k + kFSt - 1);
                         cp_async_wait<kFSt - 1>();
-                        const uint8_t* f = sF + (k % kFSt) * kFTile + wtid * 64;
-                        float v[16];
+                        if (!(k & 1)) mbar_wait(&x_empty[xs], xph ^ 1);
+                        uint8_t* dst = sX + xs * kXSlot + (k & 1) * kXTile;
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            const float4 q4 = *reinterpret_cast<const float4*>(f + ((u ^ rot) << 4));
-                            v[4 * u] = q4.x; v[4 * u + 1] = q4.y; v[4 * u + 2] = q4.z; v[4 * u + 3] = q4.w;
+                            const int row = (wtid >> 4) + 16 * u;
+                            const float4 f = *reinterpret_cast<const float4*>(sF + (k % kFSt) * kFTile + (wtid + 256 * u) * 16);
+                            ss[u] += f.x * f.x + f.y * f.y + f.z * f.z + f.w * f.w;
+                            *reinterpret_cast<uint2*>(dst + row * 128 + (((c >> 1) ^ (row & 7)) << 4) + (c & 1) * 8) =
+                                make_uint2(pack2(f.x, f.y), pack2(f.z, f.w));
                         }
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) ss += v[e] * v[e];
-                        mbar_wait(&x_empty[xs], xph ^ 1);
-                        uint8_t* dst = sX + xs * kXTile;
-                        *reinterpret_cast<uint4*>(dst + swz(sr, 2 * sq)) =
-                            make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
-                        *reinterpret_cast<uint4*>(dst + swz(sr, 2 * sq + 1)) =
-                            make_uint4(pack2(v[8], v[9]), pack2(v[10], v[11]), pack2(v[12], v[13]), pack2(v[14], v[15]));
-                        fence_proxy_async_smem();
-                        mbar_arrive(&x_full[xs]);
-                        adv(xs, xph, 1, kXSt);
+                        if ((k & 1) || k + 1 == t.nkb) {
+                            fence_proxy_async_smem();
+                            mbar_arrive(&x_full[xs]);
+                            adv(xs, xph, 1, kXSt);
+                        }
                     }
-                    ss += __shfl_xor_sync(0xffffffff, ss, 1);
-                    ss += __shfl_xor_sync(0xffffffff, ss, 2);
-                    if (sq == 0) sm_rs[sr] = 1.0f / sqrtf(ss * p.inv_width + p.eps);
+                    // row sums over the 16 lanes of each half-warp
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        float v = ss[u];
+                        v += __shfl_xor_sync(0xffffffff, v, 1);
+                        v += __shfl_xor_sync(0xffffffff, v, 2);
+                        v += __shfl_xor_sync(0xffffffff, v, 4);
+                        v += __shfl_xor_sync(0xffffffff, v, 8);
+                        if (c == 0) sm_rs[(wtid >> 4) + 16 * u] = 1.0f / sqrtf(v * p.inv_width + p.eps);
+                    }
                 } else if (t.xsrc == kXO) {
                     // ae.proj input: combine the attention key-range partials of each row,
                     // o = sum_j l_j 2^(m_j - M) O_j / sum_j l_j 2^(m_j - M); each thread loads and
@@ -419,7 +463,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         const int slot = k % oslots;
                         if (min(oslots, t.nkb - k) == 2) cp_async_wait<1>(); else cp_async_wait<0>();
                         __syncwarp();  // (m, l) were fetched by the row's sq == 0 lane
-                        mbar_wait(&x_empty[xs], xph ^ 1);
+                        if (!(k & 1)) mbar_wait(&x_empty[xs], xph ^ 1);
                         const float2* ml = sm_ml + slot * kMaxSplits * 64;
                         float M = -INFINITY;
                         for (int j = 0; j < ns; ++j) M = fmaxf(M, ml[j * 64 + sr].x);
@@ -443,18 +487,20 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                             }
                         }
                         const float iw = wsum > 0.f ? 1.f / wsum : 0.f;
-                        uint8_t* dst = sX + xs * kXTile;
+                        uint8_t* dst = sX + xs * kXSlot + (k & 1) * kXTile;
                         *reinterpret_cast<uint4*>(dst + swz(sr, 2 * sq)) =
                             make_uint4(pack2(v[0] * iw, v[1] * iw), pack2(v[2] * iw, v[3] * iw), pack2(v[4] * iw, v[5] * iw),
                                        pack2(v[6] * iw, v[7] * iw));
                         *reinterpret_cast<uint4*>(dst + swz(sr, 2 * sq + 1)) =
                             make_uint4(pack2(v[8] * iw, v[9] * iw), pack2(v[10] * iw, v[11] * iw),
                                        pack2(v[12] * iw, v[13] * iw), pack2(v[14] * iw, v[15] * iw));
-                        fence_proxy_async_smem();
-                        mbar_arrive(&x_full[xs]);
+                        if ((k & 1) || k + 1 == t.nkb) {
+                            fence_proxy_async_smem();
+                            mbar_arrive(&x_full[xs]);
+                            adv(xs, xph, 1, kXSt);
+                        }
                         __syncwarp();  // the row's (m, l) slot is refilled by lane sq == 0 below
                         if (k + oslots < t.nkb) issue_o(k + oslots, slot);
-                        adv(xs, xph, 1, kXSt);
                     }
                 } else {  // kXRows: Euler state (ae.action_proj) or robot state (ae.state_proj), K <= 64
                     const bool init = t.epi == kEpiInit;
@@ -468,7 +514,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         const int c = sq * 16 + j;
                         v[j] = (sr < rows && c < cols) ? __ldcg(src + sr * ld + c) : 0.f;
                     }
-                    uint8_t* dst = sX + xs * kXTile;
+                    uint8_t* dst = sX + xs * kXSlot;
                     *reinterpret_cast<uint4*>(dst + swz(sr, 2 * sq)) =
                         make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
                     *reinterpret_cast<uint4*>(dst + swz(sr, 2 * sq + 1)) =
@@ -864,11 +910,12 @@ AePlan ae_plan(const AePlanInput& in) {
 
     // One phase of independent full-K tasks (nonlinear epilogue, no reduction).
     auto full_phase = [&](uint8_t xsrc, uint8_t epi, int tiles, int wmat, int xmat, int kbt, int wbar, int wcnt,
-                          int sbar, int step) {
+                          int sbar, int step, int layer = 0) {
         std::vector<Item> it;
         for (int t = 0; t < tiles; ++t) {
             AeTask x = gemm(xsrc, epi, wmat, xmat, 0, t, 0, kbt, wbar, wcnt, sbar);
             x.step = uint16_t(step);
+            x.layer = uint16_t(layer);
             it.push_back({x, kbt * kWB * (xsrc == kXY ? 3.0 : 1.0)});
         }
         assign(it);
@@ -908,7 +955,7 @@ AePlan ae_plan(const AePlanInput& in) {
             const int gl = s * NA + l;
             const int bar_qkv = newbar();
             const int n_qkv = full_phase(kXY, kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], in.mat_y, kbW, prev_bar,
-                                         prev_cnt, bar_qkv, s);
+                                         prev_cnt, bar_qkv, s, l);
             const int bar_attn = newbar();
             {
                 std::vector<Item> it;
@@ -935,7 +982,7 @@ AePlan ae_plan(const AePlanInput& in) {
                                          bar_proj);
             const int bar_ffn = newbar();
             const int n_ffn = full_phase(kXY, kEpiGate, tiles_ffn, in.mat_wffn[size_t(l)], in.mat_y, kbW, bar_proj,
-                                         n_proj, bar_ffn, s);
+                                         n_proj, bar_ffn, s, l);
             const int bar_down = newbar();
             prev_cnt = red_phase(in.mat_wdown[size_t(l)], in.mat_g, kXBf16, 0, MLP / 64, ks_down, bar_ffn, n_ffn, bar_down);
             if (rec) {

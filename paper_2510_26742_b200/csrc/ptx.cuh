@@ -104,6 +104,10 @@ PI0B_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar
         : "memory");
 }
 // L2 cache-policy constants (createpolicy.fractional encodings used by CUTLASS).
+// Bulk prefetch of [src, src + bytes) into L2 (no shared-memory destination); bytes % 16 == 0.
+PI0B_DEV void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
 constexpr uint64_t kEvictNormal = 0x1000000000000000ull;
 constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
@@ -241,6 +245,12 @@ PI0B_DEV void cp_async16(void* dst, const void* src, bool pred) {
     const int sz = pred ? 16 : 0;
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
                  "r"(sz)
+                 : "memory");
+}
+// 16-byte cp.async with an L2 cache-policy hint (e.g. kEvictFirst for streamed weights).
+PI0B_DEV void cp_async16_hint(void* dst, const void* src, uint64_t policy) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "l"(policy)
                  : "memory");
 }
 PI0B_DEV void cp_async8(void* dst, const void* src) {

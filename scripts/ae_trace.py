@@ -136,14 +136,14 @@ if os.environ.get("AE_TRACE_RAW"):
 
 if os.environ.get("AE_TRACE_KB"):
     rows_d = [c for c in range(ctas.value) if dbg[c, 0] > 0]
-    print("\nper-k-block stamps of the first ae.qkv task (us from its first stamp), CTA", rows_d[:1])
-    for c in rows_d[:1]:
+    print("\nper-k-block stamps of an ae.qkv task (step 1, layer 5; us from its first stamp), CTAs", rows_d[:3])
+    for c in rows_d[:3]:
         d = dbg[c].astype(np.float64)
         base = d[0]
         for k in range(16):
             w = (d[k * 4:k * 4 + 4] - base) / 1e3
             m = (d[64 + k * 4:64 + k * 4 + 4] - base) / 1e3
-            print(f"  kb{k:2d} worker: start {w[0]:6.2f} f_full {w[1]:6.2f} x_empty {w[2]:6.2f} barrier {w[3]:6.2f}   "
+            print(f"  kb{k:2d} worker: start {w[0]:6.2f} f_landed {w[1]:6.2f} x_empty {w[2]:6.2f} x_full_arrive {w[3]:6.2f}   "
                   f"mma: start {m[0]:6.2f} w_full {m[1]:6.2f} x_full {m[2]:6.2f} issued {m[3]:6.2f}")
 
 if os.environ.get("AE_TRACE_LATE"):

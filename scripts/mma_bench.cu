@@ -9,7 +9,16 @@
 
 using namespace pi0b;
 
-template <int N, int NACC>
+// TS = 1: A operand from TMEM (tcgen05.mma [d], [a_tmem], b_desc, ...), columns 256.. of the
+// allocation hold the A tile (garbage values: only the issue rate is measured).
+PI0B_DEV void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+
+template <int M, int N, int NACC, int TS>
 __global__ void __launch_bounds__(128, 1) mma_kernel(int n_mma, int per_commit, unsigned long long* out) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -31,7 +40,7 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int n_mma, int per_commit, 
     const uint32_t tmem = *tslot;
     const int warp_u = __shfl_sync(0xffffffff, int(threadIdx.x >> 5), 0);  // provably warp-uniform
     if (warp_u == 1) {  // whole warp runs the loop; one elected lane issues
-        constexpr uint32_t idesc = umma_idesc_bf16(128, N);
+        constexpr uint32_t idesc = umma_idesc_bf16(M, N);
         const uint64_t ad = umma_desc_sw128(sA), bd = umma_desc_sw128(sB);
         uint32_t ph = 0;
         const long long t0 = clock64();
@@ -39,7 +48,11 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int n_mma, int per_commit, 
         for (int i = 0; i < n_mma; ++i) {
             // n_acc independent accumulators (TMEM column offsets), round robin
             const int a = i & (NACC - 1);
-            if (elect_one()) umma_bf16(tmem + a * N, ad + 2 * (i & 3), bd + 2 * (i & 3), idesc, i >= NACC);
+            if (TS) {
+                if (elect_one()) umma_bf16_ts(tmem + a * N, tmem + 256 + 8 * (i & 3), bd + 2 * (i & 3), idesc, i >= NACC);
+            } else {
+                if (elect_one()) umma_bf16(tmem + a * N, ad + 2 * (i & 3), bd + 2 * (i & 3), idesc, i >= NACC);
+            }
             if (++c == per_commit) {
                 c = 0;
                 if (elect_one()) umma_commit(bar);
@@ -55,28 +68,32 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int n_mma, int per_commit, 
     if ((threadIdx.x >> 5) == 1) tmem_dealloc(tmem, 512);
 }
 
+template <int M, int N, int TS>
+static void run(int per, void* outp) {
+    unsigned long long* out = (unsigned long long*)outp;
+    const int smem = 16384 + 256 * 128 + 1024 + 64;
+    cudaFuncSetAttribute(mma_kernel<M, N, 1, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    unsigned long long c = 0;
+    for (int rep = 0; rep < 2; ++rep) {
+        mma_kernel<M, N, 1, TS><<<1, 128, smem>>>(1024, per, out);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            printf("error %s\n", cudaGetErrorString(e));
+            exit(1);
+        }
+        cudaMemcpy(&c, out, 8, cudaMemcpyDeviceToHost);
+    }
+    printf("M=%3d N=%3d %s commit+wait every %4d MMAs: %7.1f cycles per MMA\n", M, N, TS ? "A:TMEM" : "A:smem", per, c / 1024.0);
+}
+
 int main() {
     unsigned long long* out;
     cudaMalloc(&out, 8);
-    const int smem = 16384 + 256 * 128 + 1024 + 64;
-#define CFG(n, a) cudaFuncSetAttribute(mma_kernel<n, a>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
-    CFG(64, 1); CFG(128, 1); CFG(256, 1); CFG(64, 2); CFG(128, 2); CFG(256, 2); CFG(64, 4); CFG(128, 4);
-    for (int nacc : {1, 2, 4})
-    for (int per : {4, 16, 1024})
-        for (int n : {64, 128, 256}) {
-            if (n * nacc > 512) continue;
-            unsigned long long c = 0;
-            for (int rep = 0; rep < 2; ++rep) {
-#define RUN(nn, aa) if (n == nn && nacc == aa) mma_kernel<nn, aa><<<1, 128, smem>>>(1024, per, out)
-                RUN(64, 1); RUN(128, 1); RUN(256, 1); RUN(64, 2); RUN(128, 2); RUN(256, 2); RUN(64, 4); RUN(128, 4);
-                cudaError_t e = cudaDeviceSynchronize();
-                if (e != cudaSuccess) {
-                    printf("error %s\n", cudaGetErrorString(e));
-                    return 1;
-                }
-                cudaMemcpy(&c, out, 8, cudaMemcpyDeviceToHost);
-            }
-            printf("N=%3d acc=%d commit+wait every %4d MMAs: %7.1f cycles per MMA (ideal %d)\n", n, nacc, per, c / 1024.0, 128 * n / 256);
-        }
+    for (int per : {4, 1024}) {
+        run<128, 64, 0>(per, out); run<128, 128, 0>(per, out); run<128, 256, 0>(per, out);
+        run<64, 64, 0>(per, out); run<64, 128, 0>(per, out); run<64, 256, 0>(per, out);
+        run<128, 64, 1>(per, out); run<128, 128, 1>(per, out); run<128, 256, 1>(per, out);
+        run<64, 64, 1>(per, out); run<64, 128, 1>(per, out); run<64, 256, 1>(per, out);
+    }
     return 0;
 }
