@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             int ws = 0, xs = 0;
             uint32_t wph = 0, xph = 0, gidx = 0, aidx = 0;
             constexpr uint32_t idesc_g = umma_idesc_bf16(128, 64);
-            constexpr uint32_t idesc_s = umma_idesc_bf16(128, 64);
+            constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128);
             constexpr uint32_t idesc_o = umma_idesc_bf16(128, 256) | (1u << 16);  // B (V) MN-major
             for (int i = 0;; ++i) {
                 const AeTask t = load_task(my + i);
@@ -302,14 +302,13 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     if (tr) tr[6] = gtimer();
                     fence_proxy_async_smem();
                     tc_fence_after();
-                    {   // S[b] = Q K_b^T: descriptors advance by (bytes >> 4); compact loop (cold code)
+                    {   // S = Q K^T over the range's 128 keys (N = 128; absent keys are zero rows):
+                        // descriptors advance by (bytes >> 4); compact loop (cold code)
                         const uint64_t qd = umma_desc_sw128(sQ), kd = umma_desc_sw128(sK);
 #pragma unroll 1
-                        for (int i = 0; i < nb * 16; ++i) {
-                            const int b = i >> 4, kk = i & 15;
-                            if (elect_one())
-                                umma_bf16(tmem + kTS + b * 64, qd + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4),
-                                          kd + ((b * 32768 + (kk >> 2) * 8192 + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
+                        for (int kk = 0; kk < 16; ++kk) {
+                            const uint32_t o = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+                            if (elect_one()) umma_bf16(tmem + kTS, qd + o, kd + o, idesc_s, kk > 0);
                             __syncwarp();
                         }
                     }
@@ -356,6 +355,20 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             if (t.kind == kAeEnd || t.phase >= p.limit_phase) break;
             unsigned long long* tr = (p.trace && wtid == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
             if (tr) tr[0] = gtimer();
+            // Attention over a range of cached LLM keys: K does not depend on this step, so its
+            // copies start before the dependency wait.
+            const bool early_k = t.kind == kAeAttn && (t.kb0 + 1) * kBlocksPerSplit * 64 <= p.kv_rows0;
+            if (early_k) {
+                const AeMat km = load_mat(p.mats + t.wmat);
+                const __nv_bfloat16* kvc = reinterpret_cast<const __nv_bfloat16*>(km.ptr);
+                const int key0 = t.kb0 * kBlocksPerSplit * 64;
+#pragma unroll 4
+                for (int u = 0; u < 16; ++u) {
+                    const int q = wtid + 256 * u;
+                    const int a4 = q >> 10, key = (q >> 3) & 127, c = q & 7;
+                    cp_async16(sK + a4 * 16384 + swz(key, c), kvc + (size_t)(key0 + key) * km.ld + p.kcol_cache + a4 * 64 + c * 8, true);
+                }
+            }
             if (t.wait_cnt) {
                 if (wtid == 0) wait_flag(p.bars + t.wait_bar, t.wait_cnt);
                 named_bar_sync(1, kWorkers);
@@ -674,10 +687,12 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 const int key0 = split * kBlocksPerSplit * 64;
                 const AeMat km = load_mat(p.mats + t.wmat);  // LLM K/V cache of layer (i % llm_layers)
                 const __nv_bfloat16* kvc = reinterpret_cast<const __nv_bfloat16*>(km.ptr);
-                auto issue_kv = [&](uint8_t* dst, int col_off) {
-                    for (int u = 0; u < 8 * nb; ++u) {
+                // K: [4 d-regions][128 keys][128 B] (B operand of the N = 128 score MMA);
+                // V: [2 blocks][4 d-regions][64 keys][128 B] (MN-major B of O = P V)
+                auto issue_kv = [&](uint8_t* dst, int col_off, bool kmaj) {
+                    for (int u = 0; u < (kmaj ? 16 : 8 * nb); ++u) {
                         const int q = wtid + 256 * u;
-                        const int b = q >> 11, a4 = (q >> 9) & 3, kr = (q >> 3) & 63, c = q & 7;
+                        const int b = kmaj ? (q >> 9) & 1 : q >> 11, a4 = kmaj ? q >> 10 : (q >> 9) & 3, kr = (q >> 3) & 63, c = q & 7;
                         const int key = key0 + b * 64 + kr;
                         const __nv_bfloat16* src = kvc;
                         bool ok = true;
@@ -687,7 +702,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                             src = p.qkv + (size_t)(key - p.kv_rows0) * p.n_qkv + p.kcol_own + col_off + a4 * 64 + c * 8;
                         else
                             ok = false;
-                        cp_async16(dst + b * 32768 + a4 * 8192 + swz(kr, c), src, ok);
+                        cp_async16(dst + (kmaj ? a4 * 16384 + swz(b * 64 + kr, c) : b * 32768 + a4 * 8192 + swz(kr, c)), src, ok);
                     }
                 };
                 {   // Q (both heads of the pair) and K
@@ -700,12 +715,12 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         cp_async16(sQ + a4 * 16384 + swz(R, c),
                                    ok ? p.qkv + (size_t)(R & 63) * p.n_qkv + head * 256 + a4 * 64 + c * 8 : p.qkv, ok);
                     }
-                    issue_kv(sK, 0);
+                    if (!early_k) issue_kv(sK, 0, true);
                     cp_async_arrive_noinc(q_full);
                 }
                 mbar_wait(s_full, ph);  // K (and Q) consumed: V may overwrite K
                 tc_fence_after();
-                issue_kv(sV, 256);
+                issue_kv(sV, 256, false);
                 cp_async_arrive_noinc(v_full);
                 if (tr) tr[10] = gtimer();
                 unsigned long long* trs =
