@@ -40,21 +40,21 @@ constexpr int kAeThreads = 320;
 constexpr int kWorkers = 256;
 constexpr int kWBlk = 64 * 64 * 2;    // 8 KB: [64 features x 64 k] bf16 SW128 image
 constexpr int kWSlot = 2 * kWBlk;     // ring slot: up to two consecutive k-blocks, one bulk copy
-constexpr int kWSt = 3;
+constexpr int kWSt = 5;
 constexpr int kWPrefetch = 0;  // weight bytes a CTA keeps bulk-prefetched into L2 ahead
-constexpr int kXSt = 4;
+constexpr int kXSt = 3;
 constexpr int kXTile = 64 * 128;      // 8 KB: 64 activation rows x 64 k
 constexpr int kXSlot = 2 * kXTile;    // X ring slot: two k-blocks, one handshake
-constexpr int kFSt = 5;
+constexpr int kFSt = 3;
 constexpr int kFTile = 16384;         // fp32 staging of one k-block: 64 rows x 64 columns
 constexpr int kMaxSplits = 10;        // attention key ranges combined by the ae.proj staging
-constexpr int kORegion = 81920;       // partial staging: 2 slots of <= 5 ranges, or 1 slot of <= 10
 constexpr int kBlocksPerSplit = 2;    // 64-key blocks per attention task
 constexpr int kOffW = 0;
-constexpr int kOffU = kWSt * kWSlot;                // union region (160 KB)
-constexpr int kUnion = 163840;
+constexpr int kOffU = kWSt * kWSlot;                // union region (128 KB)
+constexpr int kUnion = 131072;
 constexpr int kOffX = kOffU;                        // GEMM: X ring (+8 KB pad: rows 64..127 of A)
 constexpr int kOffF = kOffU + kXSt * kXSlot + kXTile;  // GEMM: fp32 ring (kXY) / partial ring (kXO)
+constexpr int kORegion = kUnion - (kOffF - kOffU);  // kXO partial staging: ranges x 8 KB per slot
 constexpr int kOffQ = kOffU;                        // ATTN: Q [128 x 256] = 4 x 16 KB
 constexpr int kOffK = kOffU + 65536;                // ATTN: K [2 blocks][64 x 256] = 2 x 32 KB
 constexpr int kOffP = kOffQ;                        // ATTN: P [128 x 128 keys] (reuses Q)
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     // o = sum_j l_j 2^(m_j - M) O_j / sum_j l_j 2^(m_j - M); each thread loads and
                     // combines its own 16 columns of its own row (no block barrier).
                     const int ns = p.attn_splits;
-                    const int oslots = ns <= kMaxSplits / 2 ? 2 : 1;
+                    const int oslots = 2 * ns * 8192 <= kORegion ? 2 : 1;
                     const int otile = kORegion / oslots;
                     auto issue_o = [&](int k, int slot) {
                         const int kc = (t.kb0 + k) * 64, head = kc >> 8;
@@ -864,7 +864,7 @@ AePlan ae_plan(const AePlanInput& in) {
     need(in.act_dim <= 32 && in.state_dim <= 64, "action/state dims");
     need(in.kv_rows0 % 8 == 0, "prefix length must be a multiple of 8");
     const int splits = (in.key_blocks + kBlocksPerSplit - 1) / kBlocksPerSplit;
-    need(splits <= kMaxSplits, "too many attention key blocks (prefix too long)");
+    need(splits <= kMaxSplits && splits * 8192 <= kORegion, "too many attention key blocks (prefix too long)");
     need(in.num_ctas >= 2 * ((in.heads + 1) / 2), "too few SMs");
 
     int nbar = 0;
