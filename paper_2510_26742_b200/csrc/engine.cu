@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cctype>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -183,7 +184,9 @@ static int choose_splits(int m_tiles, int n_tiles, int K, int bn, int num_sms) {
     const int ctas = m_tiles * n_tiles;
     const int kb = (K + 63) / 64;
     if (ctas * 2 > num_sms) return 1;
-    int s = std::min({num_sms / ctas, kb / 2, kGemmMaxSplits, env_int("PI0B_MAX_SPLITS", kGemmMaxSplits)});
+    // two-way splits measured best (scripts/gemm_sweep.sh): the DSMEM reduction moves (S-1)/S of
+    // every tile and the cluster barriers grow with S
+    int s = std::min({num_sms / ctas, kb / 2, kGemmMaxSplits, env_int("PI0B_MAX_SPLITS", 2)});
     for (; s > 1; --s) {
         const int per = (kb + s - 1) / s;
         if ((kb + per - 1) / per != s) continue;  // every split must own k-blocks
@@ -568,6 +571,13 @@ void Engine::tag(const std::string& node, int inst, const void* ptr, int rows, i
 void Engine::add_gemm(int part, const std::string& node, int inst, const __nv_bfloat16* A,
                       long long lda, int M, const NodeWeights& W, int widx, int bn, GemmParams gp,
                       bool allow_split) {
+    // Tuning overrides (sweeps): PI0B_BN_<NODE> / PI0B_SPLIT_<NODE>, NODE = id with '.' -> '_',
+    // upper case (e.g. PI0B_BN_VE_PROJ=64).
+    std::string key = node;
+    for (char& ch : key) ch = ch == '.' ? '_' : char(std::toupper(static_cast<unsigned char>(ch)));
+    const int bn_env = env_int(("PI0B_BN_" + key).c_str(), 0);
+    if ((bn_env == 64 || bn_env == 128 || bn_env == 256) && !(gp.flags & kFlagRope) && gp.mode != kModeGate) bn = bn_env;
+    const int split_env = env_int(("PI0B_SPLIT_" + key).c_str(), 0);
     Op op;
     op.kind = kOpGemm;
     op.part = part;
@@ -582,6 +592,7 @@ void Engine::add_gemm(int part, const std::string& node, int inst, const __nv_bf
     const int m_tiles = (M + 127) / 128, n_tiles = (N + bn - 1) / bn;
     const int kb = (K + 63) / 64;
     int splits = allow_split ? choose_splits(m_tiles, n_tiles, K, bn, num_sms_) : 1;
+    if (split_env > 0) splits = std::min({split_env, kb, kGemmMaxSplits});
     gp.kb_per_split = (kb + splits - 1) / splits;
     gp.splits = (kb + gp.kb_per_split - 1) / gp.kb_per_split;
     op.gp = gp;
@@ -715,7 +726,7 @@ void Engine::build_plan() {
             g.outb = ve_hb_;
             g.ldob = ve_w_;
             g.out_stats = st2;
-            add_gemm(0, "ve.proj", i, ve_attn_, ve_w_, T_, Wv["ve.proj"], i, 128, g);
+            add_gemm(0, "ve.proj", i, ve_attn_, ve_w_, T_, Wv["ve.proj"], i, 64, g);
             tag("ve.proj", i, ve_h_, T_, ve_w_, ve_w_, 0);
         }
         {   // ve.ln2 + ve.fc1: gelu((p W) * rms(p) + b)
@@ -745,7 +756,7 @@ void Engine::build_plan() {
             g.outb = ve_hb_;
             g.ldob = ve_w_;
             g.out_stats = st;
-            add_gemm(0, "ve.fc2", i, ve_mlp_, ve_mlp_ld_, T_, Wv["ve.fc2"], i, 128, g);
+            add_gemm(0, "ve.fc2", i, ve_mlp_, ve_mlp_ld_, T_, Wv["ve.fc2"], i, 64, g);
             tag("ve.fc2", i, ve_h_, T_, ve_w_, ve_w_, 0);
         }
     }
@@ -840,7 +851,7 @@ void Engine::build_plan() {
             g.outb = xb_;
             g.ldob = llm_w_;
             g.out_stats = ps;
-            add_gemm(0, "llm.proj", l, llm_attn_, llm_q_, L_, Wv["llm.proj"], l, 256, g);
+            add_gemm(0, "llm.proj", l, llm_attn_, llm_q_, L_, Wv["llm.proj"], l, 64, g);
             tag("llm.proj", l, x_, L_, llm_w_, llm_w_, 0);
         }
         {   // llm.ln2 + fused gated FFN: up * gelu(gate)
@@ -867,7 +878,7 @@ void Engine::build_plan() {
             g.outb = xb_;
             g.ldob = llm_w_;
             g.out_stats = xs;
-            add_gemm(0, "llm.down", l, llm_g_, c.llm_mlp, L_, Wv["llm.down"], l, 256, g);
+            add_gemm(0, "llm.down", l, llm_g_, c.llm_mlp, L_, Wv["llm.down"], l, 128, g);
             tag("llm.down", l, x_, L_, llm_w_, llm_w_, 0);
         }
     }
