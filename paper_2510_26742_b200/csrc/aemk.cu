@@ -82,6 +82,11 @@ PI0B_DEV unsigned atom_add_acqrel_u32(unsigned* p, unsigned v) {
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
     return old;
 }
+// Release-ordered counter bump without a return value: the issuing thread does not wait for the
+// L2 round trip (consumers poll the counter with relaxed loads and an acquire fence).
+PI0B_DEV void red_add_release_u32(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 PI0B_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // Arrive on `bar` when all of this thread's prior cp.async copies have landed.
 PI0B_DEV void cp_async_arrive_noinc(uint64_t* bar) {
@@ -220,8 +225,9 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 }
                 if (u.kind == kAeGemm) {
                     const AeMat um = load_mat(p.mats + u.wmat);
-                    const uint8_t* ub = reinterpret_cast<const uint8_t*>(um.ptr) + ((size_t)u.tile * um.ld + u.kb0) * kWBlk;
-                    const uint32_t bytes = uint32_t(u.nkb) * kWBlk;
+                    const int ublk = (u.ncol == 128 ? 2 : 1) * kWBlk;
+                    const uint8_t* ub = reinterpret_cast<const uint8_t*>(um.ptr) + ((size_t)u.tile * um.ld + u.kb0) * ublk;
+                    const uint32_t bytes = uint32_t(u.nkb) * ublk;
                     if (lane == 0)
                         for (uint32_t o = 0; o < bytes; o += 65536) bulk_prefetch_l2(ub + o, min(65536u, bytes - o));
                     ahead += bytes;
@@ -229,17 +235,19 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 ++pj;
             }
             if (t.kind != kAeGemm) continue;
-            if (pj > i) ahead -= (long long)t.nkb * kWBlk;
+            // k-block image: 8 KB (64-feature tile) or 16 KB (128); a slot takes 16 KB of them
+            const int blk = (t.ncol == 128 ? 2 : 1) * kWBlk, kpc = kWSlot / blk;
+            if (pj > i) ahead -= (long long)t.nkb * blk;
             unsigned long long* tr = (p.trace && lane == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
             const AeMat wm = load_mat(p.mats + t.wmat);
-            const uint8_t* base = reinterpret_cast<const uint8_t*>(wm.ptr) + ((size_t)t.tile * wm.ld + t.kb0) * kWBlk;
-            for (int k = 0; k < t.nkb; k += 2) {
-                const int bytes = min(2, t.nkb - k) * kWBlk;
+            const uint8_t* base = reinterpret_cast<const uint8_t*>(wm.ptr) + ((size_t)t.tile * wm.ld + t.kb0) * blk;
+            for (int k = 0; k < t.nkb; k += kpc) {
+                const int bytes = min(kpc, t.nkb - k) * blk;
                 mbar_wait(&w_empty[ws], wph ^ 1);
                 if (tr && k == 0) tr[4] = gtimer();
                 // warp-wide cp.async: each instruction moves 512 contiguous bytes; the slot's
                 // w_full completes when all 32 lanes' copies have landed (noinc arrivals)
-                const uint8_t* src = base + (size_t)k * kWBlk + lane * 16;
+                const uint8_t* src = base + (size_t)k * blk + lane * 16;
                 uint8_t* dst = sW + ws * kWSlot + lane * 16;
 #pragma unroll 8
                 for (int o = 0; o < bytes; o += 512) cp_async16_hint(dst + o, src + o, kEvictFirst);
@@ -255,7 +263,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
         {
             int ws = 0, xs = 0;
             uint32_t wph = 0, xph = 0, gidx = 0, aidx = 0;
-            constexpr uint32_t idesc_g = umma_idesc_bf16(128, 64);
+            constexpr uint32_t idesc_g = umma_idesc_bf16(128, 64), idesc_w = umma_idesc_bf16(128, 128);
             constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128);
             constexpr uint32_t idesc_o = umma_idesc_bf16(128, 256) | (1u << 16);  // B (V) MN-major
             for (int i = 0;; ++i) {
@@ -266,30 +274,35 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     unsigned long long* dbg = (p.dbg && lane == 0 && t.epi == kEpiQkv && t.step == 1 && t.layer == 5)
                                                   ? p.dbg + size_t(blockIdx.x) * 128 + 64 : nullptr;
                     mbar_wait(acc_empty, (gidx & 1) ^ 1);
-                    // one W chunk and one X slot per step: two k-blocks (8 MMAs) per handshake
+                    // one X slot (two k-blocks) per handshake; a 64-feature task takes one W slot per
+                    // X slot, a 128-feature task one W slot per k-block
+                    const bool wide = t.ncol == 128;
+                    const uint32_t idesc = wide ? idesc_w : idesc_g;
                     for (int k = 0; k < t.nkb; k += 2) {
                         const int n = min(2, t.nkb - k);
                         if (dbg) dbg[k * 4] = gtimer();
-                        mbar_wait(&w_full[ws], wph);
-                        if (dbg) dbg[k * 4 + 1] = gtimer();
-                        if (tr && k + n == t.nkb) tr[6] = gtimer();
                         mbar_wait(&x_full[xs], xph);
                         if (dbg) dbg[k * 4 + 2] = gtimer();
-                        fence_proxy_async_smem();  // cp.async / st.shared data -> tensor-core reads
-                        tc_fence_after();
-                        const uint64_t ad = umma_desc_sw128(sX + xs * kXSlot);
-                        const uint64_t bd = umma_desc_sw128(sW + ws * kWSlot);
-                        if (elect_one()) {
-                            for (int q = 0; q < 4 * n; ++q)  // k-block j = q >> 2 is 8 KB (512 desc units) on
-                                umma_bf16(tmem + kTAcc, ad + (q >> 2) * 512 + 2 * (q & 3), bd + (q >> 2) * 512 + 2 * (q & 3),
-                                          idesc_g, (k + q) != 0);
-                            umma_commit(&x_empty[xs]);
-                            umma_commit(&w_empty[ws]);
+                        for (int j = 0; j < n; ++j) {
+                            if (wide || j == 0) mbar_wait(&w_full[ws], wph);
+                            if (tr && k + n == t.nkb) tr[6] = gtimer();
+                            fence_proxy_async_smem();  // cp.async / st.shared data -> tensor-core reads
+                            tc_fence_after();
+                            const uint64_t ad = umma_desc_sw128(sX + xs * kXSlot + j * kXTile);
+                            const uint64_t bd = umma_desc_sw128(sW + ws * kWSlot + (wide ? 0 : j * kWBlk));
+                            const bool last = wide || j == n - 1;
+                            if (elect_one()) {
+#pragma unroll
+                                for (int q = 0; q < 4; ++q)
+                                    umma_bf16(tmem + kTAcc, ad + 2 * q, bd + 2 * q, idesc, (k + j + q) != 0);
+                                if (last) umma_commit(&w_empty[ws]);
+                                if (j == n - 1) umma_commit(&x_empty[xs]);
+                            }
+                            __syncwarp();
+                            if (last) adv(ws, wph, 1, kWSt);
                         }
-                        __syncwarp();
                         if (dbg) dbg[k * 4 + 3] = gtimer();
                         adv(xs, xph, 1, kXSt);
-                        adv(ws, wph, 1, kWSt);
                     }
                     if (elect_one()) umma_commit(acc_full);
                     __syncwarp();
@@ -572,11 +585,12 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     if (t.epi == kEpiRed) {
                         // split-K partial -> the fp32 residual stream (rows from `rowoff`)
                         const bool ok = t.rowoff ? r < p.chunk : true;
-                        float* dst = p.y + (size_t)(r + t.rowoff) * p.width + t.tile * 64 + dhalf * 32;
+                        const int hw = t.ncol == 128 ? 64 : 32;  // this thread's column half
+                        float* dst = p.y + (size_t)(r + t.rowoff) * p.width + t.tile * 2 * hw + dhalf * hw;
 #pragma unroll 1
-                        for (int q = 0; q < 8; ++q) {
+                        for (int q = 0; q < hw / 4; ++q) {
                             float4 v;
-                            tmem_ld4(ta + dhalf * 32 + q * 4, v);
+                            tmem_ld4(ta + dhalf * hw + q * 4, v);
                             if (ok) red_add_v4_f32(dst + q * 4, v.x, v.y, v.z, v.w);
                         }
                     } else if (t.epi == kEpiQkv || t.epi == kEpiGate) {
@@ -820,7 +834,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             // -------------------------------------------------- publish completion
             // bar.sync orders every worker's writes before lane 0's release (PTX cumulativity).
             named_bar_sync(1, kWorkers);
-            if (wtid == 0) atom_add_acqrel_u32(p.bars + t.sig_bar, 1u);
+            if (wtid == 0) red_add_release_u32(p.bars + t.sig_bar, 1u);
             if (tr) tr[3] = gtimer();
         }
     }
@@ -937,20 +951,23 @@ AePlan ae_plan(const AePlanInput& in) {
         return int(it.size());
     };
     // Split-K residual update: every (tile, k-range) task adds its partial into y.
-    auto red_phase = [&](int wmat, int xmat, uint8_t xsrc, int rowoff, int kbt, int ks, int wbar, int wcnt, int sbar) {
+    auto red_phase = [&](int wmat, int xmat, uint8_t xsrc, int rowoff, int kbt, int ks, int wbar, int wcnt, int sbar,
+                         int ncol = 64) {
         std::vector<Item> it;
         const int per = (kbt + ks - 1) / ks;
-        for (int t = 0; t < tiles_w; ++t)
+        for (int t = 0; t < W / ncol; ++t)
             for (int k = 0; k < ks; ++k) {
                 const int kb0 = k * per, nkb = std::min(kbt, kb0 + per) - kb0;
                 if (nkb <= 0) continue;
-                it.push_back({gemm(xsrc, kEpiRed, wmat, xmat, rowoff, t, kb0, nkb, wbar, wcnt, sbar), nkb * kWB});
+                AeTask x = gemm(xsrc, kEpiRed, wmat, xmat, rowoff, t, kb0, nkb, wbar, wcnt, sbar);
+                x.ncol = uint16_t(ncol);
+                it.push_back({x, nkb * kWB * ncol / 64});
             }
         assign(it);
         return int(it.size());
     };
     const int ks_ao = splits_for(tiles_w, kbW, in.ao_tasks);
-    const int ks_proj = splits_for(tiles_w, in.q_width / 64, in.proj_tasks);
+    const int ks_proj = splits_for(W / in.proj_ncol, in.q_width / 64, in.proj_tasks);
     const int ks_down = splits_for(tiles_w, MLP / 64, in.down_tasks);
     const int pairs = (in.heads + 1) / 2;
     const int n_attn = pairs * splits;
@@ -994,7 +1011,7 @@ AePlan ae_plan(const AePlanInput& in) {
             }
             const int bar_proj = newbar();
             const int n_proj = red_phase(in.mat_wproj[size_t(l)], 0, kXO, 0, in.q_width / 64, ks_proj, bar_attn, n_attn,
-                                         bar_proj);
+                                         bar_proj, in.proj_ncol);
             const int bar_ffn = newbar();
             const int n_ffn = full_phase(kXY, kEpiGate, tiles_ffn, in.mat_wffn[size_t(l)], in.mat_y, kbW, bar_proj,
                                          n_proj, bar_ffn, s, l);

@@ -58,8 +58,9 @@ static_assert(sizeof(AeMat) == 32, "AeMat layout");
 
 struct AeTask {
     uint8_t kind, xsrc, epi, rowoff;  // rowoff: kEpiRed target rows start at y row `rowoff`
-    uint16_t wmat, xmat, pad0;        // AeMat indices (weights / activation)
-    uint16_t tile;                    // GEMM: 64-feature output tile; ATTN: head pair
+    uint16_t wmat, xmat;              // AeMat indices (weights / activation)
+    uint16_t ncol;                    // GEMM: output tile width, 64 or 128 (0 = 64)
+    uint16_t tile;                    // GEMM: output tile (ncol features); ATTN: head pair
     uint16_t kb0, nkb;                // GEMM: k-block range; ATTN: key split, #key blocks
     uint16_t wait_bar, wait_cnt;      // wait until counter wait_bar reaches wait_cnt (cnt > 0)
     uint16_t sig_bar;                 // counter of the phase this task belongs to
@@ -112,16 +113,18 @@ struct AePlanInput {
     int rope_cols, kv_rows0, key_blocks;
     bool record;
     int ao_tasks = 64, proj_tasks = 128, down_tasks = 128;  // split-K task targets per phase
+    int proj_ncol = 128;                                    // ae.proj tile width (64 or 128)
     int mat_wst, mat_wap, mat_wao, mat_whead;
     std::vector<int> mat_wqkv, mat_wproj, mat_wffn, mat_wdown, mat_kv;
     int mat_y, mat_yh, mat_ap, mat_g, mat_qkv;  // fp32 y rows 0.. / rows 1.. (ae.act_rows)
 };
 
-// Weight row order of one 64-feature tile of a tile-contiguous AE weight copy
+// Weight row order of one tile of a tile-contiguous AE weight copy (64-row tiles; ae.proj uses
+// plain 128-row tiles)
 // (kernels_misc.cu tile_weight_kernel): plain, or "paired" — tile 2T + s of a matrix packed in
 // 128-row groups [64 | 64 partners] (kPermRope qkv, kPermGate64 ffn) takes rows
 // 128T + 32s + [0, 32) followed by their partners 128T + 64 + 32s + [0, 32).
-enum AeTileOrder : int { kTilePlain = 0, kTilePaired = 1 };
+enum AeTileOrder : int { kTilePlain = 0, kTilePaired = 1, kTilePlain128 = 2 };
 
 struct AePlan {
     std::vector<AeTask> table;  // [num_ctas][stride]

@@ -1089,8 +1089,9 @@ void Engine::build_ae_mega() {
     auto wmat = [&](const char* node, int inst, int rows, int order = kTilePlain) {
         // tile-contiguous copy of 64-row tiles: AeMat{ptr, rows, k, k-blocks}
         const NodeWeights& nw = W_.at(node);
-        const int kb = (nw.k + 63) / 64, nt = (rows + 63) / 64;
-        __nv_bfloat16* t = alloc<__nv_bfloat16>(size_t(nt) * kb * 4096);
+        const int R = order == kTilePlain128 ? 128 : 64;
+        const int kb = (nw.k + 63) / 64, nt = (rows + R - 1) / R;
+        __nv_bfloat16* t = alloc<__nv_bfloat16>(size_t(nt) * kb * R * 64);
         ae_tiled_.push_back({nw.w.at(size_t(inst)), rows, nw.k, nw.ldk, t, order});
         mats.push_back(AeMat{t, rows, nw.k, kb, {0, 0, 0}});
         return int(mats.size()) - 1;
@@ -1114,13 +1115,14 @@ void Engine::build_ae_mega() {
     in.ao_tasks = env_int("PI0B_AE_AO_TASKS", in.ao_tasks);
     in.proj_tasks = env_int("PI0B_AE_PROJ_TASKS", in.proj_tasks);
     in.down_tasks = env_int("PI0B_AE_DOWN_TASKS", in.down_tasks);
+    in.proj_ncol = env_int("PI0B_AE_PROJ_NCOL", in.proj_ncol) == 64 ? 64 : 128;
     in.mat_wst = wmat("ae.state_proj", 0, W);
     in.mat_wap = wmat("ae.action_proj", 0, W);
     in.mat_wao = wmat("ae.action_out", 0, W);
     in.mat_whead = wmat("ae.head", 0, c.ae_action_dim);
     for (int l = 0; l < NA; ++l) {
         in.mat_wqkv.push_back(wmat("ae.qkv", l, NQ, kTilePaired));
-        in.mat_wproj.push_back(wmat("ae.proj", l, W));
+        in.mat_wproj.push_back(wmat("ae.proj", l, W, in.proj_ncol == 128 ? kTilePlain128 : kTilePlain));
         in.mat_wffn.push_back(wmat("ae.ffn", l, 2 * MLP, kTilePaired));
         in.mat_wdown.push_back(wmat("ae.down", l, W));
     }

@@ -120,20 +120,22 @@ __global__ void f32_to_f64_kernel(const float* src, long long lds, int rows, int
 // Tile-contiguous copy of a packed [rows, k] weight for the action-expert megakernel: block
 // (n_tile, kb) is the shared-memory image of a 64 x 64 operand tile in the 128-byte swizzle
 // (16-byte chunk c of row r at (c ^ (r & 7))), zero-padded past `rows` / `k`.  The megakernel
-// streams these with contiguous bulk copies (a [64 x 64] box of the row-major weight is 64
-// pieces of 128 B at a K-element stride: poor DRAM locality).  order 1 ("paired", aemk.cuh
-// AeTileOrder): tile 2T + s takes rows 128T + 32s + [0, 32) and their partners 64 rows later.
+// streams these with contiguous copies (a [64 x 64] box of the row-major weight is 64 pieces
+// of 128 B at a K-element stride: poor DRAM locality).  order 1 ("paired", aemk.cuh
+// AeTileOrder): tile 2T + s takes rows 128T + 32s + [0, 32) and their partners 64 rows later;
+// order 2: plain 128-row tiles (16 KB blocks).
 __global__ void tile_weight_kernel(const __nv_bfloat16* src, int rows, int k, long long ldk, __nv_bfloat16* dst,
                                    int kblocks, int order) {
     const long long tile = blockIdx.x;  // (n_tile * kblocks + kb)
     const int nt = int(tile / kblocks), kb = int(tile % kblocks);
-    for (int q = threadIdx.x; q < 512; q += blockDim.x) {
+    const int R = order == 2 ? 128 : 64;
+    for (int q = threadIdx.x; q < R * 8; q += blockDim.x) {
         const int r = q >> 3, c = q & 7;
-        const int row = order ? (nt >> 1) * 128 + (r >> 5) * 64 + (nt & 1) * 32 + (r & 31) : nt * 64 + r;
+        const int row = order == 1 ? (nt >> 1) * 128 + (r >> 5) * 64 + (nt & 1) * 32 + (r & 31) : nt * R + r;
         const int col = kb * 64 + c * 8;
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
         if (row < rows && col < k) v = *reinterpret_cast<const uint4*>(src + (long long)row * ldk + col);
-        *reinterpret_cast<uint4*>(dst + tile * 4096 + r * 64 + ((c ^ (r & 7)) << 3)) = v;
+        *reinterpret_cast<uint4*>(dst + tile * (R * 64) + r * 64 + ((c ^ (r & 7)) << 3)) = v;
     }
 }
 
@@ -141,7 +143,8 @@ __global__ void tile_weight_kernel(const __nv_bfloat16* src, int rows, int k, lo
 
 cudaError_t launch_tile_weight(const __nv_bfloat16* src, int rows, int k, long long ldk, __nv_bfloat16* dst,
                                int order, cudaStream_t st) {
-    const int kblocks = (k + 63) / 64, ntiles = (rows + 63) / 64;
+    const int R = order == 2 ? 128 : 64;
+    const int kblocks = (k + 63) / 64, ntiles = (rows + R - 1) / R;
     tile_weight_kernel<<<ntiles * kblocks, 256, 0, st>>>(src, rows, k, ldk, dst, kblocks, order);
     return cudaGetLastError();
 }
