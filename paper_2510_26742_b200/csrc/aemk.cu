@@ -966,9 +966,9 @@ AePlan ae_plan(const AePlanInput& in) {
         assign(it);
         return int(it.size());
     };
-    const int ks_ao = splits_for(tiles_w, kbW, in.ao_tasks);
+    const int ks_ao = splits_for(W / in.ao_ncol, kbW, in.ao_tasks);
     const int ks_proj = splits_for(W / in.proj_ncol, in.q_width / 64, in.proj_tasks);
-    const int ks_down = splits_for(tiles_w, MLP / 64, in.down_tasks);
+    const int ks_down = splits_for(W / in.down_ncol, MLP / 64, in.down_tasks);
     const int pairs = (in.heads + 1) / 2;
     const int n_attn = pairs * splits;
 
@@ -981,7 +981,7 @@ AePlan ae_plan(const AePlanInput& in) {
         const int bar_ap = newbar();
         const int n_ap = full_phase(kXRows, kEpiSilu, tiles_w, in.mat_wap, 0, 1, prev_bar, prev_cnt, bar_ap, s);
         const int bar_ao = newbar();
-        prev_cnt = red_phase(in.mat_wao, in.mat_ap, kXBf16, 1, kbW, ks_ao, bar_ap, n_ap, bar_ao);
+        prev_cnt = red_phase(in.mat_wao, in.mat_ap, kXBf16, 1, kbW, ks_ao, bar_ap, n_ap, bar_ao, in.ao_ncol);
         prev_bar = bar_ao;
         for (int l = 0; l < NA; ++l) {
             const int gl = s * NA + l;
@@ -1016,7 +1016,8 @@ AePlan ae_plan(const AePlanInput& in) {
             const int n_ffn = full_phase(kXY, kEpiGate, tiles_ffn, in.mat_wffn[size_t(l)], in.mat_y, kbW, bar_proj,
                                          n_proj, bar_ffn, s, l);
             const int bar_down = newbar();
-            prev_cnt = red_phase(in.mat_wdown[size_t(l)], in.mat_g, kXBf16, 0, MLP / 64, ks_down, bar_ffn, n_ffn, bar_down);
+            prev_cnt = red_phase(in.mat_wdown[size_t(l)], in.mat_g, kXBf16, 0, MLP / 64, ks_down, bar_ffn, n_ffn, bar_down,
+                                 in.down_ncol);
             if (rec) {
                 std::vector<Item> it;
                 AeTask x{};

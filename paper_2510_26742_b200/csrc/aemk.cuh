@@ -113,7 +113,7 @@ struct AePlanInput {
     int rope_cols, kv_rows0, key_blocks;
     bool record;
     int ao_tasks = 64, proj_tasks = 128, down_tasks = 128;  // split-K task targets per phase
-    int proj_ncol = 128;                                    // ae.proj tile width (64 or 128)
+    int proj_ncol = 128, down_ncol = 64, ao_ncol = 64;     // residual-update tile widths (64 or 128)
     int mat_wst, mat_wap, mat_wao, mat_whead;
     std::vector<int> mat_wqkv, mat_wproj, mat_wffn, mat_wdown, mat_kv;
     int mat_y, mat_yh, mat_ap, mat_g, mat_qkv;  // fp32 y rows 0.. / rows 1.. (ae.act_rows)

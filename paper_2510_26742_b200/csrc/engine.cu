@@ -1116,15 +1116,17 @@ void Engine::build_ae_mega() {
     in.proj_tasks = env_int("PI0B_AE_PROJ_TASKS", in.proj_tasks);
     in.down_tasks = env_int("PI0B_AE_DOWN_TASKS", in.down_tasks);
     in.proj_ncol = env_int("PI0B_AE_PROJ_NCOL", in.proj_ncol) == 64 ? 64 : 128;
+    in.down_ncol = env_int("PI0B_AE_DOWN_NCOL", in.down_ncol) == 128 ? 128 : 64;
+    in.ao_ncol = env_int("PI0B_AE_AO_NCOL", in.ao_ncol) == 128 ? 128 : 64;
     in.mat_wst = wmat("ae.state_proj", 0, W);
     in.mat_wap = wmat("ae.action_proj", 0, W);
-    in.mat_wao = wmat("ae.action_out", 0, W);
+    in.mat_wao = wmat("ae.action_out", 0, W, in.ao_ncol == 128 ? kTilePlain128 : kTilePlain);
     in.mat_whead = wmat("ae.head", 0, c.ae_action_dim);
     for (int l = 0; l < NA; ++l) {
         in.mat_wqkv.push_back(wmat("ae.qkv", l, NQ, kTilePaired));
         in.mat_wproj.push_back(wmat("ae.proj", l, W, in.proj_ncol == 128 ? kTilePlain128 : kTilePlain));
         in.mat_wffn.push_back(wmat("ae.ffn", l, 2 * MLP, kTilePaired));
-        in.mat_wdown.push_back(wmat("ae.down", l, W));
+        in.mat_wdown.push_back(wmat("ae.down", l, W, in.down_ncol == 128 ? kTilePlain128 : kTilePlain));
     }
     const int llm_qkv_n = llm_q_ + 2 * llm_kv_;
     for (int l = 0; l < c.llm_layers; ++l)  // AE instance i reads LLM layer i % llm_layers (@mod)
