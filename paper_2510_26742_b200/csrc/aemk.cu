@@ -752,30 +752,29 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     const bool mine = side < nb;
                     mbar_wait(s_full, ph);
                     tc_fence_after();
+                    // one TMEM pass (64 scores per thread kept in registers): TMEM reads run at
+                    // ~64 B/cycle per SM, so a second pass over S costs ~0.5 us
+                    float sv[64];
+                    tmem_ld32(ts, *reinterpret_cast<float(*)[32]>(sv));  // warp-uniform
+                    tmem_ld32(ts + 32, *reinterpret_cast<float(*)[32]>(sv + 32));
+                    const int nkm = mine ? nk - side * 64 : 0;  // valid keys of this thread's block
                     float mx = -INFINITY;
-#pragma unroll 1
-                    for (int q = 0; q < 8; ++q) {
-                        float v[8];
-                        tmem_ld8(ts + q * 8, v);  // warp-uniform
 #pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            if (mine && side * 64 + q * 8 + e < nk) mx = fmaxf(mx, v[e] * p.scale_log2);
+                    for (int e = 0; e < 64; ++e) {
+                        sv[e] = e < nkm ? sv[e] * p.scale_log2 : -INFINITY;
+                        mx = fmaxf(mx, sv[e]);
                     }
                     xch[side * 128 + R] = mx;
                     named_bar_sync(1, kWorkers);
                     mx = fmaxf(xch[R], xch[128 + R]);
                     float l = 0.f;
                     if (mine) {
-#pragma unroll 1
+#pragma unroll
                         for (int q = 0; q < 8; ++q) {
-                            float v[8];
-                            tmem_ld8(ts + q * 8, v);
                             uint32_t pk[4];
 #pragma unroll
                             for (int e = 0; e < 8; e += 2) {
-                                const int c = side * 64 + q * 8 + e;
-                                const float e0 = c < nk ? ex2_fast(v[e] * p.scale_log2 - mx) : 0.f;
-                                const float e1 = c + 1 < nk ? ex2_fast(v[e + 1] * p.scale_log2 - mx) : 0.f;
+                                const float e0 = ex2_fast(sv[q * 8 + e] - mx), e1 = ex2_fast(sv[q * 8 + e + 1] - mx);
                                 l += e0 + e1;
                                 pk[e / 2] = pack2(e0, e1);
                             }
