@@ -79,8 +79,8 @@ struct FaCfg {
     static constexpr int Q_BYTES = QA * kFaRows * 128;
     static constexpr int K_BYTES = QA * kFaKeys * 128;
     static constexpr int V_BYTES = VA * kFaKeys * 128;
-    static constexpr int P_BYTES = kFaRows * 128;
-    static constexpr int SMEM = Q_BYTES + KK * K_BYTES + KV * V_BYTES + P_BYTES + 256 + 1024;
+    static constexpr int P_BYTES = kFaRows * 128;  // one P buffer; two are allocated
+    static constexpr int SMEM = Q_BYTES + KK * K_BYTES + KV * V_BYTES + 2 * P_BYTES + 256 + 1024;
     static constexpr int TMEM_S = 0;  // two 64-column S buffers
     static constexpr int TMEM_O = 128;
     static constexpr int TMEM_COLS = 128 + DV <= 256 ? 256 : 512;
@@ -96,16 +96,16 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
     uint8_t* sK = sQ + C::Q_BYTES;
     uint8_t* sV = sK + KK * C::K_BYTES;
     uint8_t* sP = sV + KV * C::V_BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::P_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES);
     uint64_t* k_full = bars;            // [KK]
     uint64_t* k_empty = k_full + KK;    // [KK]
     uint64_t* v_full = k_empty + KK;    // [KV]
     uint64_t* v_empty = v_full + KV;    // [KV]
     uint64_t* s_full = v_empty + KV;    // [2]
     uint64_t* s_free = s_full + 2;      // [2]
-    uint64_t* p_full = s_free + 2;      // [1]
-    uint64_t* o_done = p_full + 1;      // [1]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+    uint64_t* p_full = s_free + 2;      // [2] per P buffer
+    uint64_t* o_done = p_full + 2;      // [2] PV of tile t done (buffer t & 1 free again)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
     const int tid = threadIdx.x, warp = __shfl_sync(0xffffffff, tid >> 5, 0), lane = tid & 31;
     const int qt = blockIdx.x, grp = blockIdx.z;
@@ -128,8 +128,10 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             mbar_init(&s_full[s], 1);
             mbar_init(&s_free[s], 128);
         }
-        mbar_init(p_full, 128);
-        mbar_init(o_done, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&p_full[s], 128);
+            mbar_init(&o_done[s], 1);
+        }
         fence_barrier_init();
     }
     if (warp == 4) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -209,16 +211,16 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                 if (t + 1 < ntiles) issue_qk(t + 1);
                 const int sv = t % KV;
                 mbar_wait(&v_full[sv], (t / KV) & 1);
-                mbar_wait(p_full, t & 1);
+                mbar_wait(&p_full[t & 1], (t >> 1) & 1);
                 tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < kFaKeys / 16; ++kk) {
-                    const uint64_t a = desc_kmajor(p0 + kk * 32);
+                    const uint64_t a = desc_kmajor(p0 + (t & 1) * C::P_BYTES + kk * 32);
                     const uint64_t b = desc_mnmajor(v0 + sv * C::V_BYTES + kk * 2048, kFaKeys * 128);
                     if (elect_one()) umma_bf16(tmem + C::TMEM_O, a, b, idesc_pv, (t | kk) > 0);
                 }
                 if (elect_one()) {
-                    umma_commit(o_done);
+                    umma_commit(&o_done[t & 1]);
                     umma_commit(&v_empty[sv]);
                 }
                 __syncwarp();
@@ -249,11 +251,8 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                 s1[j] = kbase + 32 + j < total ? s1[j] * p.scale_log2 : -INFINITY;
                 mx = fmaxf(mx, fmaxf(s0[j], s1[j]));
             }
-            // previous PV done: the P buffer and O are ours
-            if (t > 0) {
-                mbar_wait(o_done, (t - 1) & 1);
-                tc_fence_after();
-            }
+            // P is double-buffered: buffer t & 1 is free once PV(t - 2) is done; O may only be
+            // rescaled once PV(t - 1) is done (rare: lazy rescale)
             float factor = 1.f;
             const bool grow = mx > m_ref + 8.f;
             if (grow) {
@@ -261,7 +260,14 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                 m_ref = mx;
                 l *= factor;
             }
-            if (t > 0 && __any_sync(0xffffffff, grow)) {
+            const bool rescale = t > 0 && __any_sync(0xffffffff, grow);
+            if (rescale) {
+                mbar_wait(&o_done[(t - 1) & 1], ((t - 1) >> 1) & 1);
+                tc_fence_after();
+            } else if (t >= 2) {
+                mbar_wait(&o_done[t & 1], ((t - 2) >> 1) & 1);
+            }
+            if (rescale) {
 #pragma unroll 1
                 for (int c = 0; c < DV / 32; ++c) {
                     float o[32];
@@ -275,24 +281,24 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             uint32_t pk[32];
 #pragma unroll
             for (int j = 0; j < 32; j += 2) {
-                const float a0 = exp2f(s0[j] - m_ref), a1 = exp2f(s0[j + 1] - m_ref);
-                const float b0 = exp2f(s1[j] - m_ref), b1 = exp2f(s1[j + 1] - m_ref);
+                const float a0 = ex2_fast(s0[j] - m_ref), a1 = ex2_fast(s0[j + 1] - m_ref);
+                const float b0 = ex2_fast(s1[j] - m_ref), b1 = ex2_fast(s1[j + 1] - m_ref);
                 ls += a0 + a1 + b0 + b1;
                 pk[j / 2] = pack_bf16(a0, a1);
                 pk[16 + j / 2] = pack_bf16(b0, b1);
             }
             l += ls;
-            uint8_t* prow = sP + r * 128;
+            uint8_t* prow = sP + (t & 1) * C::P_BYTES + r * 128;
 #pragma unroll
             for (int c = 0; c < 8; ++c)
                 *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) =
                     make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
             fence_proxy_async();
             tc_fence_before();
-            mbar_arrive(p_full);
+            mbar_arrive(&p_full[t & 1]);
         }
         // epilogue: O / l -> bf16
-        mbar_wait(o_done, (ntiles - 1) & 1);
+        mbar_wait(&o_done[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
         tc_fence_after();
         const float il = l > 0.f ? 1.f / l : 0.f;
         __nv_bfloat16* orow = p.out;
