@@ -63,13 +63,18 @@ constexpr int kOffAux = kOffU + kUnion;
 constexpr int kAuxBytes = 16384;
 constexpr int kAeSmem = kOffAux + kAuxBytes + 1024;
 static_assert(kOffF + kORegion <= kOffAux && kOffF + kFSt * kFTile <= kOffAux, "GEMM union overflow");
+// Pair (2-CTA split-K) receive buffer in the owner's union tail, past the X and fp32 rings:
+// the helper's [64 x 64] fp32 partial (256-byte rows) + its 64 row sums of squares.
+constexpr int kOffRecv = kOffF + kFSt * kFTile;
+static_assert(kOffRecv + 16384 + 256 <= kOffAux, "pair receive buffer");
 static_assert(kAeSmem <= 232448, "shared memory budget");
 
 constexpr uint32_t kTAcc = 0, kTS = 0, kTO = 256;  // TMEM columns (512 allocated)
 
 // mbarrier slots
 constexpr int kBWFull = 0, kBWEmpty = 8, kBXFull = 16, kBXEmpty = 24, kBAccFull = 32, kBAccEmpty = 33,
-              kBQFull = 34, kBSFull = 35, kBVFull = 36, kBPFull = 37, kBODone = 38, kNumBars = 39;
+              kBQFull = 34, kBSFull = 35, kBVFull = 36, kBPFull = 37, kBODone = 38, kBPairFull = 39,
+              kBPairReady = 40, kNumBars = 41;
 static_assert(kWSt <= 8 && kXSt <= 8, "barrier slots");
 
 PI0B_DEV unsigned ld_relaxed_u32(const unsigned* p) {
@@ -86,6 +91,41 @@ PI0B_DEV unsigned atom_add_acqrel_u32(unsigned* p, unsigned v) {
 // L2 round trip (consumers poll the counter with relaxed loads and an acquire fence).
 PI0B_DEV void red_add_release_u32(unsigned* p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// DSMEM: the same shared-memory offset in the partner CTA of a 2-CTA cluster.
+PI0B_DEV uint32_t partner_addr(const void* p) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(cluster_ctarank() ^ 1u));
+    return r;
+}
+PI0B_DEV void st_cluster_v4(uint32_t addr, float4 v) {
+    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+PI0B_DEV void st_cluster_f32(uint32_t addr, float v) {
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+// Asynchronous remote store that completes `bytes` of the transaction count of a barrier in the
+// destination CTA (no release fence needed: the owner's barrier wait makes the data visible).
+PI0B_DEV void st_async_v4(uint32_t addr, float4 v, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(mbar)
+                 : "memory");
+}
+PI0B_DEV void st_async_f32(uint32_t addr, float v, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(addr), "f"(v), "r"(mbar)
+                 : "memory");
+}
+PI0B_DEV void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+PI0B_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
 }
 PI0B_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // Arrive on `bar` when all of this thread's prior cp.async copies have landed.
@@ -178,6 +218,10 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
     uint64_t* o_done = mb + kBODone;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffAux + 512);
     float* sm_rs = reinterpret_cast<float*>(smem + kOffAux + 1024);     // [64]
+    float* sm_ss = reinterpret_cast<float*>(smem + kOffAux + 1280);     // [64] pair tasks: raw row sums of squares
+    float* recv = reinterpret_cast<float*>(smem + kOffRecv);           // [64][64] helper partial, then [64] sums
+    uint64_t* pair_full = mb + kBPairFull;
+    uint64_t* pair_ready = mb + kBPairReady;
     float2* sm_ml = reinterpret_cast<float2*>(smem + kOffAux + 2048);   // [2][kMaxSplits][64]
     float* sm_vec = reinterpret_cast<float*>(smem + kOffAux + 12288);   // [64] epilogue vector
 
@@ -192,6 +236,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             uint32_t cnt = 1;
             if ((i >= kBXFull && i < kBXFull + kXSt) || i == kBQFull || i == kBVFull) cnt = kWorkers;
             if (i >= kBWFull && i < kBWFull + kWSt) cnt = 32;  // producer lanes' cp.async arrivals
+            // kBPairFull / kBPairReady: one remote arrival each (from the partner CTA)
             mbar_init(&mb[i], cnt);
         }
         fence_barrier_init();
@@ -359,7 +404,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
         const int dhalf = warp >= 8 ? 1 : 0;          // drainer: column half
         const uint32_t tlane = uint32_t(wq * 32) << 16;
         int xs = 0;
-        uint32_t xph = 0, gidx = 0, aidx = 0;
+        uint32_t xph = 0, gidx = 0, aidx = 0, oidx = 0, hidx = 0;  // oidx / hidx: pair owner / helper tasks
         // staging geometry: thread -> (row sr, 16-column quarter sq) of a 64 x 64 k-block
         const int sr = wtid >> 2, sq = wtid & 3;
 
@@ -368,6 +413,11 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             if (t.kind == kAeEnd || t.phase >= p.limit_phase) break;
             unsigned long long* tr = (p.trace && wtid == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
             if (tr) tr[0] = gtimer();
+            // Pair owner: its receive buffer (union tail) is free from here on -- tell the helper.
+            if (t.pair == 1 && wtid == 0) {
+                mbar_arrive_expect_tx(pair_full, 64 * 64 * 4 + 64 * 4);  // the helper's st.async bytes
+                mbar_arrive_remote(partner_addr(pair_ready));
+            }
             // Attention over a range of cached LLM keys: K does not depend on this step, so its
             // copies start before the dependency wait.
             const bool early_k = t.kind == kAeAttn && (t.kb0 + 1) * kBlocksPerSplit * 64 <= p.kv_rows0;
@@ -461,7 +511,10 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         v += __shfl_xor_sync(0xffffffff, v, 2);
                         v += __shfl_xor_sync(0xffffffff, v, 4);
                         v += __shfl_xor_sync(0xffffffff, v, 8);
-                        if (c == 0) sm_rs[(wtid >> 4) + 16 * u] = 1.0f / sqrtf(v * p.inv_width + p.eps);
+                        if (c == 0) {
+                            if (t.pair) sm_ss[(wtid >> 4) + 16 * u] = v;  // half of K: the owner adds both
+                            else sm_rs[(wtid >> 4) + 16 * u] = 1.0f / sqrtf(v * p.inv_width + p.eps);
+                        }
                     }
                 } else if (t.xsrc == kXO) {
                     // ae.proj input: combine the attention key-range partials of each row,
@@ -577,7 +630,35 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 mbar_wait(acc_full, gidx & 1);
                 tc_fence_after();
                 if (tr) tr[8] = gtimer();
-                if (drainer) {
+                if (t.pair == 2) {
+                    // Pair helper: push the fp32 partial + row sums of squares into the owner's
+                    // receive buffer once the owner has started this tile.
+                    mbar_wait_cluster(pair_ready, hidx & 1);
+                    if (tr) tr[10] = gtimer();
+                    // st.async straight from registers into the owner's receive buffer, each store
+                    // completing its bytes on the owner's pair_full barrier (a release fence or a
+                    // releasing remote arrive here costs ~1.3 us: it waits for the SM's
+                    // outstanding global traffic).  Row r's 16-byte chunk c sits at c ^ (r & 7), so
+                    // a warp's 32 rows land in distinct banks.
+                    const uint32_t rbar = partner_addr(pair_full);
+                    if (drainer) {
+                        const uint32_t ta = tmem + kTAcc + tlane;
+                        const uint32_t dst = partner_addr(recv + drow * 64);
+#pragma unroll 1
+                        for (int q = 0; q < 8; ++q) {
+                            float4 v;
+                            tmem_ld4(ta + dhalf * 32 + q * 4, v);
+                            st_async_v4(dst + (((dhalf * 8 + q) ^ (drow & 7)) << 4), v, rbar);
+                        }
+                    }
+                    if (wtid < 64) st_async_f32(partner_addr(recv + 64 * 64 + wtid), sm_ss[wtid], rbar);
+                    if (tr) tr[11] = gtimer();
+                    ++hidx;
+                } else if (t.pair == 1) {
+                    mbar_wait_cluster(pair_full, oidx & 1);
+                    ++oidx;
+                }
+                if (drainer && t.pair != 2) {
                     // Compact loops over 4-column quads of the thread's row (TMEM lane): short
                     // bodies stay hot in the instruction cache after one iteration.
                     const int r = drow;
@@ -596,7 +677,8 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     } else if (t.epi == kEpiQkv || t.epi == kEpiGate) {
                         // paired tile (aemk.cuh AeTileOrder): column i < 32 and its partner 32 + i;
                         // this thread: i in [16 dhalf, 16 dhalf + 16)
-                        const float rs = sm_rs[r];
+                        const bool pr = t.pair == 1;  // add the helper's half-K partial
+                        const float rs = pr ? 1.0f / sqrtf((sm_ss[r] + recv[64 * 64 + r]) * p.inv_width + p.eps) : sm_rs[r];
                         const int T = t.tile >> 1, sub = t.tile & 1, i0 = dhalf * 16;
                         float xa[16], xb[16];
 #pragma unroll
@@ -604,6 +686,12 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                             float4 a4, b4;
                             tmem_ld4(ta + i0 + q * 4, a4);
                             tmem_ld4(ta + 32 + i0 + q * 4, b4);
+                            if (pr) {
+                                const float4 ha = *reinterpret_cast<const float4*>(recv + r * 64 + (((dhalf * 4 + q) ^ (r & 7)) << 2));
+                                const float4 hb = *reinterpret_cast<const float4*>(recv + r * 64 + (((8 + dhalf * 4 + q) ^ (r & 7)) << 2));
+                                a4.x += ha.x; a4.y += ha.y; a4.z += ha.z; a4.w += ha.w;
+                                b4.x += hb.x; b4.y += hb.y; b4.z += hb.z; b4.w += hb.w;
+                            }
                             xa[4 * q] = a4.x * rs; xa[4 * q + 1] = a4.y * rs; xa[4 * q + 2] = a4.z * rs; xa[4 * q + 3] = a4.w * rs;
                             xb[4 * q] = b4.x * rs; xb[4 * q + 1] = b4.y * rs; xb[4 * q + 2] = b4.z * rs; xb[4 * q + 3] = b4.w * rs;
                         }
@@ -840,6 +928,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
 
     tc_fence_before();
     __syncthreads();
+    cluster_sync_all();  // no CTA leaves while its partner may still touch its shared memory
     if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
@@ -855,11 +944,15 @@ cudaError_t aemk_launch(const AeParams& p, int grid, cudaStream_t stream) {
     cfg.blockDim = dim3(kAeThreads, 1, 1);
     cfg.dynamicSmemBytes = kAeSmem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other)
     attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;  // CTA pairs share split-K tiles over DSMEM
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, aemk_kernel, p);
 }
 
@@ -936,6 +1029,30 @@ AePlan ae_plan(const AePlanInput& in) {
     const int kbW = W / 64;
     const int tiles_w = W / 64, tiles_qkv = NQ / 64, tiles_ffn = 2 * MLP / 64;
 
+    // A phase of full-K tiles split over K between the two CTAs of a cluster (CTAs 2c, 2c + 1):
+    // the owner takes the first half of K and runs the epilogue, the helper the second half.
+    auto pair_phase = [&](uint8_t epi, int tiles, int wmat, int xmat, int kbt, int wbar, int wcnt, int sbar, int step,
+                          int layer) {
+        const int nclu = in.num_ctas / 2, h = kbt / 2;
+        std::vector<std::pair<double, int>> order;
+        for (int c = 0; c < nclu; ++c) order.push_back({std::max(load[size_t(2 * c)], load[size_t(2 * c + 1)]), c});
+        std::sort(order.begin(), order.end());
+        for (int t = 0; t < tiles; ++t) {
+            const int c = order[size_t(t % nclu)].second;
+            const int own = 2 * c + ((t / nclu + phase) & 1);
+            for (int r = 0; r < 2; ++r) {
+                AeTask x = gemm(kXY, epi, wmat, xmat, 0, t, r ? h : 0, r ? kbt - h : h, wbar, wcnt, sbar);
+                x.step = uint16_t(step);
+                x.layer = uint16_t(layer);
+                x.pair = uint16_t(r ? 2 : 1);
+                const int cta = r ? own ^ 1 : own;
+                load[size_t(cta)] += (r ? kbt - h : h) * kWB * 3.0;
+                lists[size_t(cta)].push_back(x);
+            }
+        }
+        ++phase;
+        return 2 * tiles;
+    };
     // One phase of independent full-K tasks (nonlinear epilogue, no reduction).
     auto full_phase = [&](uint8_t xsrc, uint8_t epi, int tiles, int wmat, int xmat, int kbt, int wbar, int wcnt,
                           int sbar, int step, int layer = 0) {
@@ -985,8 +1102,11 @@ AePlan ae_plan(const AePlanInput& in) {
         for (int l = 0; l < NA; ++l) {
             const int gl = s * NA + l;
             const int bar_qkv = newbar();
-            const int n_qkv = full_phase(kXY, kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], in.mat_y, kbW, prev_bar,
-                                         prev_cnt, bar_qkv, s, l);
+            const bool pq = in.pair_qkv && 2 * tiles_qkv <= in.num_ctas && (in.num_ctas % 2) == 0;
+            const int n_qkv = pq ? pair_phase(kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], in.mat_y, kbW, prev_bar, prev_cnt,
+                                              bar_qkv, s, l)
+                                 : full_phase(kXY, kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], in.mat_y, kbW, prev_bar,
+                                              prev_cnt, bar_qkv, s, l);
             const int bar_attn = newbar();
             {
                 std::vector<Item> it;

@@ -14,7 +14,10 @@
 // weights while the current layer's dependencies resolve (the "software barrier" + weight
 // prefetch of PAPER.md:232-242 / SURVEY.md 7.3).
 //
-// No task ever finalises another task's output: the nonlinear GEMMs (ae.qkv, ae.ffn,
+// The kernel runs as 2-CTA clusters (cooperative launch): an ae.qkv tile is split over K between
+// the two CTAs of a cluster; the helper pushes its fp32 partial and row sums of squares into the
+// owner's shared memory (DSMEM) and the owner runs the epilogue.  No task ever finalises
+// another task's output through global memory: the nonlinear GEMMs (ae.qkv, ae.ffn,
 // ae.head) run over the full K and read the fp32 residual stream directly, computing the
 // RmsStats row sums of squares while they stage it; only the residual updates (ae.proj,
 // ae.down, ae.action_out) are split over K, and they add straight into the residual stream.
@@ -67,7 +70,7 @@ struct AeTask {
     uint16_t aux;                     // REC: record slot
     uint16_t step, layer;             // flow step, AE layer
     uint16_t phase;                   // global phase index (debug limit)
-    uint16_t pad1;
+    uint16_t pair;                    // full-K tile split over a 2-CTA cluster: 1 owner, 2 helper
 };
 static_assert(sizeof(AeTask) == 32, "AeTask layout");
 
@@ -114,6 +117,7 @@ struct AePlanInput {
     bool record;
     int ao_tasks = 64, proj_tasks = 128, down_tasks = 128;  // split-K task targets per phase
     int proj_ncol = 128, down_ncol = 64, ao_ncol = 64;     // residual-update tile widths (64 or 128)
+    bool pair_qkv = true;  // ae.qkv tiles split over K between the two CTAs of a cluster (DSMEM)
     int mat_wst, mat_wap, mat_wao, mat_whead;
     std::vector<int> mat_wqkv, mat_wproj, mat_wffn, mat_wdown, mat_kv;
     int mat_y, mat_yh, mat_ap, mat_g, mat_qkv;  // fp32 y rows 0.. / rows 1.. (ae.act_rows)

@@ -1118,6 +1118,7 @@ void Engine::build_ae_mega() {
     in.proj_ncol = env_int("PI0B_AE_PROJ_NCOL", in.proj_ncol) == 64 ? 64 : 128;
     in.down_ncol = env_int("PI0B_AE_DOWN_NCOL", in.down_ncol) == 128 ? 128 : 64;
     in.ao_ncol = env_int("PI0B_AE_AO_NCOL", in.ao_ncol) == 128 ? 128 : 64;
+    in.pair_qkv = env_int("PI0B_AE_PAIR", 1) != 0;
     in.mat_wst = wmat("ae.state_proj", 0, W);
     in.mat_wap = wmat("ae.action_proj", 0, W);
     in.mat_wao = wmat("ae.action_out", 0, W, in.ao_ncol == 128 ? kTilePlain128 : kTilePlain);

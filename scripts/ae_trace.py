@@ -102,6 +102,26 @@ for r in mid:
         print(f"  {'':8s}       qk_landed {q(rel(6))} s_full {q(rel(10))} p_full {q(rel(11))} pv_ready {q(rel(7))} o_done {q(rel(12))} stored {q(rel(13))}")
     prev_end = r[5]
 
+# pair (2-CTA split-K) tasks of the mid layer: owner vs helper stamps
+print("\npair tasks of the mid layer (us relative to the previous phase's last publish):")
+prev_end = 0
+for r in rows:
+    if r[0] == mid[0][0] - 1:
+        prev_end = r[5]
+for r in mid:
+    idx = np.array(ph[r[0]])
+    pr = tasks["pad1"][idx]
+    if (pr > 0).any():
+        for role, nm in ((1, "owner"), (2, "helper")):
+            s8 = st[idx[pr == role]].astype(np.float64)
+            rel = lambda c: (s8[:, c] - prev_end) / 1e3
+            q = lambda v: "%6.2f/%6.2f/%6.2f" % (np.min(v), np.median(v), np.max(v))
+            print(f"  {r[1]:6s} {nm:6s} ready {q(rel(1))} staged {q(rel(2))} acc {q(rel(7))} acc_seen {q(rel(8))} "
+                  f"epi_done {q(rel(9))} pub {q(rel(3))}")
+            if role == 2:
+                print(f"  {'':13s} ready_ok {q(rel(10))} stores {q(rel(11))} bar {q(rel(12))} fence {q(rel(13))}")
+    prev_end = r[5]
+
 # finaliser anatomy of one mid layer: the tile's last split (finaliser) per split-K phase
 print("\nfinalisers of the mid layer (us relative to the previous phase's last publish):")
 prev_end = 0
