@@ -25,16 +25,19 @@ def _newer(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, lib: str = LIB, defines: list[str] | None = None) -> str:
+    """Build `lib` (default libpi0b.so); `defines` (-DNAME=V) select an experimental variant,
+    built in its own object directory."""
+    obj = OBJ if not defines else OBJ + "_" + os.path.basename(lib).replace(".so", "")
+    os.makedirs(obj, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(os.path.dirname(PKG), "include", "pi0b.h"))
     jobs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJ, src.replace(".cu", ".o"))
+        o = os.path.join(obj, src.replace(".cu", ".o"))
         if force or _newer(o, [s] + headers):
-            jobs.append([NVCC, *ARCH, *FLAGS, "-c", s, "-o", o])
+            jobs.append([NVCC, *ARCH, *FLAGS, *(defines or []), "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -45,11 +48,16 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=len(jobs) or 1) as ex:
         list(ex.map(run, jobs))
-    objs = [os.path.join(OBJ, s.replace(".cu", ".o")) for s in SOURCES]
-    if force or jobs or _newer(LIB, objs):
-        run([NVCC, *ARCH, "-shared", "-o", LIB, *objs])
-    return LIB
+    objs = [os.path.join(obj, s.replace(".cu", ".o")) for s in SOURCES]
+    if force or jobs or _newer(lib, objs):
+        run([NVCC, *ARCH, "-shared", "-o", lib, *objs])
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    # python build.py [-v] [-f] [out.so -DNAME=V ...]
+    args = [a for a in sys.argv[1:] if a not in ("-v", "-f")]
+    if args:
+        print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, lib=os.path.abspath(args[0]), defines=args[1:]))
+    else:
+        print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

@@ -49,6 +49,16 @@ constexpr int kFSt = 3;
 constexpr int kFTile = 16384;         // fp32 staging of one k-block: 64 rows x 64 columns
 constexpr int kMaxSplits = 10;        // attention key ranges combined by the ae.proj staging
 constexpr int kBlocksPerSplit = 2;    // 64-key blocks per attention task
+#ifndef PI0B_AE_YREG
+#define PI0B_AE_YREG 0
+#endif
+#ifndef PI0B_AE_ROT
+#define PI0B_AE_ROT 0
+#endif
+#ifndef PI0B_AE_OREG
+#define PI0B_AE_OREG 1
+#endif
+constexpr int kOReg = 5;              // ae.proj staging combines up to this many key ranges in registers
 constexpr int kOffW = 0;
 constexpr int kOffU = kWSt * kWSlot;                // union region (128 KB)
 constexpr int kUnion = 131072;
@@ -189,6 +199,17 @@ PI0B_DEV unsigned long long gtimer() {
     return t;
 }
 
+// Full-K tasks that stage the fp32 residual stream start at a tile-dependent k-block, so the
+// CTAs of one phase do not all read the same 16 KB of y at the same time (rotation by an even
+// number of k-blocks keeps the producer's two-k-block copies contiguous).
+PI0B_DEV int ae_rot(const AeTask& t) {
+#if PI0B_AE_ROT
+    return (t.xsrc == kXY && !(t.nkb & 1) && t.nkb >= 4) ? 2 * (int(t.tile) % (t.nkb >> 1)) : 0;
+#else
+    return 0;
+#endif
+}
+
 PI0B_DEV int swz(int row, int chunk) { return row * 128 + ((chunk ^ (row & 7)) << 4); }
 
 }  // namespace
@@ -286,13 +307,16 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             unsigned long long* tr = (p.trace && lane == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
             const AeMat wm = load_mat(p.mats + t.wmat);
             const uint8_t* base = reinterpret_cast<const uint8_t*>(wm.ptr) + ((size_t)t.tile * wm.ld + t.kb0) * blk;
+            const int rot = ae_rot(t);
             for (int k = 0; k < t.nkb; k += kpc) {
                 const int bytes = min(kpc, t.nkb - k) * blk;
                 mbar_wait(&w_empty[ws], wph ^ 1);
                 if (tr && k == 0) tr[4] = gtimer();
                 // warp-wide cp.async: each instruction moves 512 contiguous bytes; the slot's
                 // w_full completes when all 32 lanes' copies have landed (noinc arrivals)
-                const uint8_t* src = base + (size_t)k * blk + lane * 16;
+                int kr = k + rot;
+                if (kr >= t.nkb) kr -= t.nkb;
+                const uint8_t* src = base + (size_t)kr * blk + lane * 16;
                 uint8_t* dst = sW + ws * kWSlot + lane * 16;
 #pragma unroll 8
                 for (int o = 0; o < bytes; o += 512) cp_async16_hint(dst + o, src + o, kEvictFirst);
@@ -466,15 +490,65 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     // into its own slot of the fp32 ring (a half-warp reads one row's 256-byte
                     // segment), then converts them to bf16 into the operand slot and accumulates
                     // the row's sum of squares (RmsStats); kFSt - 1 k-blocks in flight.
+#if PI0B_AE_YREG
+                    // The staging is latency-bound (L2 round trip under the weight stream), so
+                    // kYD k-blocks (kYD x 16 KB per CTA) are kept in flight in registers:
+                    // ld.global.cg -> convert -> st.shared, no fp32 round trip through smem.
+                    const float* yf = reinterpret_cast<const float*>(xm.ptr);
+                    const int c = wtid & 15, r0 = wtid >> 4;
+                    const float* src0 = yf + t.kb0 * 64 + c * 4;
+                    constexpr int kYD = PI0B_AE_YREG;
+                    float4 yb[kYD][4];
+                    auto ldblk = [&](float4(&b)[4], int k) {
+                        if (k < t.nkb) {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int row = r0 + 16 * u;
+                                b[u] = row < xm.rows ? __ldcg(reinterpret_cast<const float4*>(src0 + (size_t)row * xm.ld + k * 64))
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+                            }
+                        }
+                    };
+#pragma unroll
+                    for (int d = 0; d < kYD; ++d) ldblk(yb[d], d);
+                    float ss[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+                    for (int k0 = 0; k0 < t.nkb; k0 += kYD) {
+#pragma unroll
+                        for (int d = 0; d < kYD; ++d) {
+                            const int k = k0 + d;
+                            if (k < t.nkb) {
+                                if (!(k & 1)) mbar_wait(&x_empty[xs], xph ^ 1);
+                                uint8_t* dst = sX + xs * kXSlot + (k & 1) * kXTile;
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    const int row = r0 + 16 * u;
+                                    const float4 f = yb[d][u];
+                                    ss[u] += f.x * f.x + f.y * f.y + f.z * f.z + f.w * f.w;
+                                    *reinterpret_cast<uint2*>(dst + row * 128 + (((c >> 1) ^ (row & 7)) << 4) + (c & 1) * 8) =
+                                        make_uint2(pack2(f.x, f.y), pack2(f.z, f.w));
+                                }
+                                if ((k & 1) || k + 1 == t.nkb) {
+                                    fence_proxy_async_smem();
+                                    mbar_arrive(&x_full[xs]);
+                                    adv(xs, xph, 1, kXSt);
+                                }
+                                ldblk(yb[d], k + kYD);
+                            }
+                        }
+                    }
+#else
                     const float* yf = reinterpret_cast<const float*>(xm.ptr);
                     const float* src0 = yf + t.kb0 * 64 + (wtid & 15) * 4;
+                    const int rot = ae_rot(t);
                     auto issue = [&](int k) {
                         if (k < t.nkb) {
+                            const int kr = k + rot < t.nkb ? k + rot : k + rot - t.nkb;
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
                                 const int row = (wtid >> 4) + 16 * u;
                                 const bool ok = row < xm.rows;
-                                cp_async16(sF + (k % kFSt) * kFTile + (wtid + 256 * u) * 16, src0 + (size_t)(ok ? row : 0) * xm.ld + k * 64, ok);
+                                cp_async16(sF + (k % kFSt) * kFTile + (wtid + 256 * u) * 16, src0 + (size_t)(ok ? row : 0) * xm.ld + kr * 64, ok);
                             }
                         }
                         cp_async_commit();
@@ -503,6 +577,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                             adv(xs, xph, 1, kXSt);
                         }
                     }
+#endif
                     // row sums over the 16 lanes of each half-warp
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
@@ -516,10 +591,79 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                             else sm_rs[(wtid >> 4) + 16 * u] = 1.0f / sqrtf(v * p.inv_width + p.eps);
                         }
                     }
-                } else if (t.xsrc == kXO) {
+#if PI0B_AE_OREG
+                } else if (t.xsrc == kXO && p.attn_splits <= kOReg && t.nkb <= 2 && (t.kb0 & 3) + t.nkb <= 4) {
                     // ae.proj input: combine the attention key-range partials of each row,
                     // o = sum_j l_j 2^(m_j - M) O_j / sum_j l_j 2^(m_j - M); each thread loads and
-                    // combines its own 16 columns of its own row (no block barrier).
+                    // combines its own 16 columns of its own row (no block barrier).  Every
+                    // partial of both k-blocks is loaded into registers at once (the loads are
+                    // latency-bound, so all of them are put in flight together).
+                    const int ns = p.attn_splits;
+                    // both k-blocks lie in one head: one (m, l) per key range
+                    uint4 ov[2][kOReg][2];
+                    float2 mlv[kOReg];
+                    const int head = (t.kb0 * 64) >> 8;
+#pragma unroll
+                    for (int j = 0; j < kOReg; ++j)
+                        mlv[j] = j < ns ? __ldcg(p.ml + (size_t)j * p.heads * 64 + head * 64 + sr) : make_float2(-INFINITY, 0.f);
+#pragma unroll
+                    for (int k = 0; k < 2; ++k) {
+                        const int kc = (t.kb0 + k) * 64;
+#pragma unroll
+                        for (int j = 0; j < kOReg; ++j) {
+                            if (k < t.nkb && j < ns) {
+                                const uint4* ob = reinterpret_cast<const uint4*>(p.opart + (size_t)j * 64 * p.q_width +
+                                                                                 (size_t)sr * p.q_width + kc + 16 * sq);
+                                ov[k][j][0] = __ldcg(ob);
+                                ov[k][j][1] = __ldcg(ob + 1);
+                            } else {
+                                ov[k][j][0] = ov[k][j][1] = make_uint4(0u, 0u, 0u, 0u);
+                            }
+                        }
+                    }
+                    float M = -INFINITY;
+#pragma unroll
+                    for (int j = 0; j < kOReg; ++j) M = fmaxf(M, mlv[j].x);
+                    float cw[kOReg], wsum = 0.f;
+#pragma unroll
+                    for (int j = 0; j < kOReg; ++j) {
+                        cw[j] = j < ns ? mlv[j].y * ex2_fast(mlv[j].x - M) : 0.f;
+                        wsum += cw[j];
+                    }
+                    const float iw = wsum > 0.f ? 1.f / wsum : 0.f;
+                    mbar_wait(&x_empty[xs], xph ^ 1);
+#pragma unroll
+                    for (int k = 0; k < 2; ++k) {
+                        if (k < t.nkb) {
+                            float v[16];
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) v[e] = 0.f;
+#pragma unroll
+                            for (int j = 0; j < kOReg; ++j) {
+                                const float w = cw[j] * iw;
+#pragma unroll
+                                for (int h2 = 0; h2 < 2; ++h2) {
+                                    const uint32_t w4[4] = {ov[k][j][h2].x, ov[k][j][h2].y, ov[k][j][h2].z, ov[k][j][h2].w};
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e) {
+                                        v[h2 * 8 + 2 * e] += w * __uint_as_float(w4[e] << 16);
+                                        v[h2 * 8 + 2 * e + 1] += w * __uint_as_float(w4[e] & 0xffff0000u);
+                                    }
+                                }
+                            }
+                            uint8_t* dst = sX + xs * kXSlot + k * kXTile;
+                            *reinterpret_cast<uint4*>(dst + swz(sr, 2 * sq)) =
+                                make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
+                            *reinterpret_cast<uint4*>(dst + swz(sr, 2 * sq + 1)) =
+                                make_uint4(pack2(v[8], v[9]), pack2(v[10], v[11]), pack2(v[12], v[13]), pack2(v[14], v[15]));
+                        }
+                    }
+                    fence_proxy_async_smem();
+                    mbar_arrive(&x_full[xs]);
+                    adv(xs, xph, 1, kXSt);
+#endif
+                } else if (t.xsrc == kXO) {
+                    // general case (more key ranges): cp.async through the partial staging region
                     const int ns = p.attn_splits;
                     const int oslots = 2 * ns * 8192 <= kORegion ? 2 : 1;
                     const int otile = kORegion / oslots;

@@ -595,6 +595,29 @@ void Engine::add_gemm(int part, const std::string& node, int inst, const __nv_bf
     if (split_env > 0) splits = std::min({split_env, kb, kGemmMaxSplits});
     gp.kb_per_split = (kb + splits - 1) / splits;
     gp.splits = (kb + gp.kb_per_split - 1) / gp.kb_per_split;
+    // More tiles than SMs and no split-K: one persistent CTA per SM with the accumulator
+    // double-buffered in TMEM (epilogue of tile j overlapped with the mainloop of tile j + 1).
+    // PI0B_PERSIST_<NODE>=0/1 overrides.
+    const int persist_env = env_int(("PI0B_PERSIST_" + key).c_str(), -1);
+    // 256 x 256 tiles for the large unsplit bn = 256 GEMMs: a CTA pair on one tcgen05
+    // cta_group::2 MMA (PI0B_CG[_<NODE>]: 0 off, 1 auto, 2 force), or else two m-tiles per CTA
+    // (PI0B_MT[_<NODE>], default off: it halves L2 traffic but not the shared-memory traffic
+    // that bounds a single-CTA MMA).
+    {
+        const bool can = bn == 256 && gp.splits == 1 && M > 128 &&
+                         (gp.mode == kModeGate || gp.mode == kModeBf16 || gp.mode == kModeResid);
+        const int cg_env = env_int(("PI0B_CG_" + key).c_str(), -1), cg_all = env_int("PI0B_CG", 1);
+        const bool want_cg = cg_env >= 0 ? cg_env > 0 : (cg_all == 2 || (cg_all == 1 && m_tiles * n_tiles > num_sms_));
+        gp.cg = can && want_cg ? 2 : 1;
+        const int mt_env = env_int(("PI0B_MT_" + key).c_str(), -1), mt_all = env_int("PI0B_MT", 0);
+        const bool want = mt_env >= 0 ? mt_env > 0 : (mt_all == 2 || (mt_all == 1 && m_tiles * n_tiles > num_sms_));
+        gp.mt = can && want && gp.cg == 1 ? 2 : 1;
+        if (gp.cg == 2) op.tb = make_tmap_bf16(wptr, N, K, W.ldk, bn / 2);
+    }
+    // PI0B_PERSIST: 0 off, 1 (default) when tiles > SMs, 2 every unsplit GEMM (tests).
+    const int persist_all = env_int("PI0B_PERSIST", 1);
+    const bool auto_p = persist_all == 2 || (persist_all == 1 && m_tiles * n_tiles > num_sms_);
+    gp.persist = gp.splits == 1 && (persist_env >= 0 ? persist_env > 0 : auto_p) ? 1 : 0;
     op.gp = gp;
     ops_.push_back(op);
 }
@@ -1447,8 +1470,10 @@ std::string Engine::describe() const {
         char buf[256];
         if (op.kind == kOpGemm) {
             const int mt = (op.gp.M + 127) / 128, nt = (op.gp.N + op.bn - 1) / op.bn;
-            snprintf(buf, sizeof buf, "%d %d gemm %s %d %dx%dx%d M=%d N=%d K=%d bn=%d mode=%d\n", idx, op.part,
-                     op.node.c_str(), op.inst, mt, nt, op.gp.splits, op.gp.M, op.gp.N, op.gp.K, op.bn, op.gp.mode);
+            snprintf(buf, sizeof buf, "%d %d gemm %s %d %dx%dx%d M=%d N=%d K=%d bn=%d mode=%d%s\n", idx, op.part,
+                     op.node.c_str(), op.inst, mt, nt, op.gp.splits, op.gp.M, op.gp.N, op.gp.K, op.bn, op.gp.mode,
+                     op.gp.cg > 1 ? (op.gp.persist ? " persistent cta-pair" : " cta-pair")
+                                  : op.gp.persist ? (op.gp.mt > 1 ? " persistent mt2" : " persistent") : (op.gp.mt > 1 ? " mt2" : ""));
         } else if (op.kind == kOpSkinny) {
             snprintf(buf, sizeof buf, "%d %d skinny %s %d tiles=%d cluster=%d M=%d N=%d K=%d mode=%d\n", idx, op.part,
                      op.node.c_str(), op.inst, skinny_tiles(op.n_packed), op.cluster, op.gp.M, op.gp.N, op.gp.K,

@@ -21,6 +21,10 @@
 #include "gemm.cuh"
 #include "ptx.cuh"
 
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
 namespace pi0b {
 
 constexpr int BM = 128;
@@ -28,10 +32,17 @@ constexpr int BK = 64;
 constexpr int kGemmThreads = 64 + 8 * 32;  // TMA warp, MMA warp, 8 epilogue warps
 static bool g_gemm_pdl = true;             // launch with programmatic stream serialization
 
-template <int BN, int STAGES>
+// MT: 128-row m-tiles per CTA sharing every weight tile (MT = 2: a 256 x BN CTA tile, two
+// accumulators in TMEM, half the L2 -> SM weight traffic per FLOP of MT = 1).
+// CG: CTAs per MMA (CG = 2: a CTA pair runs one 256 x BN tile with tcgen05 cta_group::2; each
+// CTA stages its own 128 A rows and half of the BN weight rows, so the shared-memory operand
+// traffic per MMA halves -- a single-CTA M=128 MMA fed by TMA is shared-memory-bandwidth bound
+// at ~55% of the tensor pipe).
+template <int BN, int STAGES, int MT = 1, int CG = 1>
 struct GemmCfg {
-    static constexpr int A_BYTES = BM * BK * 2;
-    static constexpr int B_BYTES = BN * BK * 2;
+    static constexpr int A_TILE = BM * BK * 2;
+    static constexpr int A_BYTES = MT * A_TILE;
+    static constexpr int B_BYTES = (BN / CG) * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int BAR_BYTES = 256;
     static constexpr int SMEM = STAGES * STAGE_BYTES + BAR_BYTES + BN * 4 + 1024;
@@ -97,11 +108,14 @@ PI0B_DEV float sumsq32(const float (&v)[32], int nvalid) {
 
 // MODE is a GemmMode; each instantiation carries only its own epilogue so the code a
 // CTA executes once (cold instruction cache) stays small.
-template <int BN, int STAGES, int MODE>
+template <int BN, int STAGES, int MODE, int MT = 1, int CG = 1>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmParams p) {
-    using Cfg = GemmCfg<BN, STAGES>;
+    using Cfg = GemmCfg<BN, STAGES, MT, CG>;
+    static_assert(CG == 1 || (MT == 1 && BN == 256), "CTA-pair tiles are 256 x 256");
+    // accumulator buffers: double-buffered when two fit in TMEM's 512 columns
+    constexpr int NBUF = 2 * MT * Cfg::TMEM_COLS <= 512 ? 2 : 1;
     constexpr bool kPaired = MODE == kModeGate || (MODE == kModeBf16 && BN == 256);
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
@@ -110,14 +124,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
     uint64_t* empty = full + STAGES;
-    uint64_t* accum_full = empty + STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_full + 1);
+    uint64_t* accum_full = empty + STAGES;   // [2] (double-buffered accumulator when persistent)
+    uint64_t* accum_empty = accum_full + 2;  // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_empty + 2);
     int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
     float* sm_vec = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::BAR_BYTES);
 
     const int warp = __shfl_sync(0xffffffff, int(threadIdx.x >> 5), 0);  // warp-uniform (see below)
     const int lane = threadIdx.x & 31;
-    const int m_tile = blockIdx.x, n_tile = blockIdx.y, split = blockIdx.z;
+    // Persistent mode (p.persist, no split-K): CTA b walks tiles b, b + grid, ... (m fastest, so
+    // CTAs running together share weight tiles in L2) with the accumulator double-buffered in
+    // TMEM: the epilogue of tile j overlaps the mainloop of tile j + 1.
+    const bool persist = p.persist != 0;
+    // CG = 2: the pair (blockIdx.x / 2) owns a 256-row tile; this CTA its rows rank * 128 + ..
+    const uint32_t crank = CG == 2 ? cluster_ctarank() : 0u;
+    const bool leader = crank == 0;
+    const int gm = (p.M + MT * CG * BM - 1) / (MT * CG * BM);
+    const int n_tiles = persist ? gm * ((p.N + BN - 1) / BN) : 1;
+    const int t_first = persist ? int(blockIdx.x) / CG : 0, t_step = persist ? int(gridDim.x) / CG : 1;
+    auto tile_mn = [&](int t, int& m, int& n) {
+        if (persist) {
+            m = t % gm;
+            n = t / gm;
+        } else {
+            m = blockIdx.x / CG;
+            n = blockIdx.y;
+        }
+    };
+    const int split = blockIdx.z;
     const int KB = (p.K + BK - 1) / BK;
     const int kb0 = split * p.kb_per_split;
     const int kb1 = min(KB, kb0 + p.kb_per_split);
@@ -126,16 +160,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
+        // CG = 2: the leader's full[s] collects both CTAs' TMA bytes (and one arrival each), its
+        // accum_empty[b] both CTAs' epilogue arrivals
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], CG);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(accum_full, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&accum_full[b], 1);
+            mbar_init(&accum_empty[b], CG);
+        }
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+    const int tmem_cols = (persist ? NBUF : 1) * MT * Cfg::TMEM_COLS;
+    if (warp == 1) {
+        if constexpr (CG == 2) tmem_alloc_cg2(tmem_slot, tmem_cols);
+        else tmem_alloc(tmem_slot, tmem_cols);
+    }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote arrive
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -145,24 +189,59 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
-            // Weight tiles never depend on the previous kernel: issue the first ring's worth
-            // before waiting for it (PDL), then the activation tiles.
-            const int pre = min(STAGES, nkb);
-            for (int i = 0; i < pre; ++i) {
-                mbar_arrive_expect_tx(&full[i], Cfg::STAGE_BYTES);
-                tma_load_2d(sB + i * Cfg::B_BYTES, &tmB, &full[i], (kb0 + i) * BK, n_tile * BN, kEvictNormal);
-            }
-            pdl_wait();
-            for (int i = 0; i < pre; ++i)
-                tma_load_2d(sA + i * Cfg::A_BYTES, &tmA, &full[i], (kb0 + i) * BK, m_tile * BM, kEvictLast);
-            for (int i = pre; i < nkb; ++i) {
-                const int s = i % STAGES;
-                const uint32_t ph = (i / STAGES) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
-                mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
-                const int kc = (kb0 + i) * BK;
-                tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kc, m_tile * BM, kEvictLast);
-                tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, &full[s], kc, n_tile * BN, kEvictNormal);
+            int g = 0;  // k-blocks issued by this CTA (ring position across tiles)
+            for (int t = t_first; t < n_tiles; t += t_step) {
+                int m_tile, n_tile;
+                tile_mn(t, m_tile, n_tile);
+                int i0 = 0;
+                // CG = 2: this CTA's A rows / weight rows within the pair tile, and the leader's
+                // full barrier (shared::cluster address) that both CTAs' copies complete on
+                const int arow = CG == 2 ? (m_tile * 2 + int(crank)) * BM : 0;
+                const int brow = n_tile * BN + int(crank) * (BN / CG);
+                auto arm = [&](int s) {
+                    if constexpr (CG == 2) {
+                        if (leader) mbar_arrive_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
+                        else mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&full[s]), 0));
+                    } else {
+                        mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+                    }
+                };
+                auto load_b = [&](int s, int kc) {
+                    if constexpr (CG == 2) tma_load_2d_cg2(sB + s * Cfg::B_BYTES, &tmB, mapa_shared(smem_u32(&full[s]), 0), kc, brow, kEvictNormal);
+                    else tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, &full[s], kc, brow, kEvictNormal);
+                };
+                auto load_a = [&](int s, int kc) {
+                    if constexpr (CG == 2) {
+                        tma_load_2d_cg2(sA + s * Cfg::A_BYTES, &tmA, mapa_shared(smem_u32(&full[s]), 0), kc, arow, kEvictLast);
+                    } else {
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt)
+                            tma_load_2d(sA + s * Cfg::A_BYTES + mt * Cfg::A_TILE, &tmA, &full[s], kc, (m_tile * MT + mt) * BM,
+                                        kEvictLast);
+                    }
+                };
+                if (g == 0) {
+                    // Weight tiles never depend on the previous kernel: issue the first ring's
+                    // worth before waiting for it (PDL), then the activation tiles.
+                    const int pre = min(STAGES, nkb);
+                    for (int i = 0; i < pre; ++i) {
+                        arm(i);
+                        load_b(i, (kb0 + i) * BK);
+                    }
+                    pdl_wait();
+                    for (int i = 0; i < pre; ++i) load_a(i, (kb0 + i) * BK);
+                    i0 = pre;
+                    g = pre;
+                }
+                for (int i = i0; i < nkb; ++i, ++g) {
+                    const int s = g % STAGES;
+                    const uint32_t ph = (g / STAGES) & 1;
+                    if (g >= STAGES) mbar_wait(&empty[s], ph ^ 1);
+                    arm(s);
+                    const int kc = (kb0 + i) * BK;
+                    load_a(s, kc);
+                    load_b(s, kc);
+                }
             }
         }
         __syncwarp();
@@ -174,24 +253,45 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // ------------------------------------------------------------ MMA issuer
         // Warp-uniform loop, one elected lane issues: tcgen05.mma from a divergent single-lane
         // branch costs ~270 instead of ~128 issue cycles per N=256 MMA (scripts/mma_bench.cu).
-        {
-            constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % STAGES;
-                const uint32_t ph = (i / STAGES) & 1;
-                mbar_wait(&full[s], ph);
-                tc_fence_after();
-                const uint64_t ad = umma_desc_sw128(sA + s * Cfg::A_BYTES);
-                const uint64_t bd = umma_desc_sw128(sB + s * Cfg::B_BYTES);
-                if (elect_one()) {
+        if (leader) {  // CG = 2: only the leader CTA issues (for both)
+            constexpr uint32_t idesc = umma_idesc_bf16(BM * CG, BN);
+            int g = 0, j = 0;
+            for (int t = t_first; t < n_tiles; t += t_step, ++j) {
+                const int b = j % NBUF;
+                if (j >= NBUF) {  // the epilogue of tile j - NBUF has drained this accumulator
+                    mbar_wait(&accum_empty[b], ((j / NBUF) & 1) ^ 1);
+                    tc_fence_after();
+                }
+                const uint32_t dt = tmem + uint32_t(b * MT * BN);
+                for (int i = 0; i < nkb; ++i, ++g) {
+                    const int s = g % STAGES;
+                    const uint32_t ph = (g / STAGES) & 1;
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint64_t ad = umma_desc_sw128(sA + s * Cfg::A_BYTES);
+                    const uint64_t bd = umma_desc_sw128(sB + s * Cfg::B_BYTES);
+                    if (elect_one()) {
+                        if constexpr (CG == 2) {
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)
-                        umma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0);
-                    umma_commit(&empty[s]);
+                            for (int k = 0; k < BK / 16; ++k) umma_bf16_cg2(dt, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0);
+                            umma_commit_cg2(&empty[s]);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < BK / 16; ++k)
+#pragma unroll
+                                for (int mt = 0; mt < MT; ++mt)
+                                    umma_bf16(dt + mt * BN, ad + ((mt * Cfg::A_TILE) >> 4) + 2 * k, bd + 2 * k, idesc, (i | k) != 0);
+                            umma_commit(&empty[s]);
+                        }
+                    }
+                    __syncwarp();
+                }
+                if (elect_one()) {
+                    if constexpr (CG == 2) umma_commit_cg2(&accum_full[b]);
+                    else umma_commit(&accum_full[b]);
                 }
                 __syncwarp();
             }
-            if (elect_one()) umma_commit(accum_full);
         }
         __syncwarp();
         if (S > 1) {
@@ -206,9 +306,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int hsel = (warp - 2) >> 2;
         const int etid = threadIdx.x - 64;  // 0..255
         const int row_in_tile = q * 32 + lane;
+        int j = 0;
+        for (int t = t_first; t < n_tiles; t += t_step, ++j) {
+        int m_big, n_tile;
+        tile_mn(t, m_big, n_tile);
+        const uint32_t acc_base = uint32_t((j % NBUF) * MT * BN);
+        if (MT > 1) mbar_wait(&accum_full[j % NBUF], (j / NBUF) & 1);
+#pragma unroll 1
+        for (int mt = 0; mt < MT; ++mt) {
+        const int m_tile = CG == 2 ? m_big * 2 + int(crank) : m_big * MT + mt;
         const int r = m_tile * BM + row_in_tile;
         const bool valid = r < p.M;
-        const uint32_t trow = tmem + (uint32_t(q * 32) << 16);
+        const uint32_t trow = tmem + (uint32_t(q * 32) << 16) + acc_base + uint32_t(mt * BN);
         const int n0 = n_tile * BN;
 
         // Stage the per-column vector (bias or SiluBias table row), zero-padded, while the
@@ -220,7 +329,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if ((p.flags & kFlagRowScale) && valid) rs = 1.0f / sqrtf(p.row_stats[r] * p.inv_width + p.eps);
         named_bar_sync(1, 256);
 
-        mbar_wait(accum_full, 0);
+        if (MT == 1) mbar_wait(&accum_full[j % NBUF], (j / NBUF) & 1);
         tc_fence_after();
 
         constexpr int NC = BN / 32;                 // 32-column chunks in the tile
@@ -377,19 +486,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         // Peers may still be reading this CTA's parked partials.
         if (S > 1) cluster_sync_all();
+        named_bar_sync(1, 256);  // sm_vec free for the next (sub-)tile
+        }
+        // accumulator drained (CG = 2: both CTAs arrive on the leader's barrier)
+        tc_fence_before();
+        named_bar_sync(1, 256);
+        if (etid == 0) {
+            if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&accum_empty[j % NBUF]), 0));
+            else mbar_arrive(&accum_empty[j % NBUF]);
+        }
+        }
     }
 
     tc_fence_before();
-    __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, Cfg::TMEM_COLS);
+    if constexpr (CG == 2) {
+        cluster_sync_all();  // the leader's MMAs into the peer's TMEM are complete
+        if (warp == 1) tmem_dealloc_cg2(tmem, tmem_cols);
+    } else {
+        __syncthreads();
+        if (warp == 1) tmem_dealloc(tmem, tmem_cols);
+    }
 }
 
 // ------------------------------------------------------------------ host side
 
-template <int BN, int STAGES, int MODE>
+template <int BN, int STAGES, int MODE, int MT = 1, int CG = 1>
 static cudaError_t configure_t() {
-    return cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                GemmCfg<BN, STAGES>::SMEM);
+    return cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, MODE, MT, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                GemmCfg<BN, STAGES, MT, CG>::SMEM);
 }
 
 template <int BN, int STAGES>
@@ -405,24 +529,30 @@ static cudaError_t configure_bn() {
 cudaError_t gemm_configure() {
     cudaError_t e = configure_bn<256, 4>();
     if (e == cudaSuccess) e = configure_t<256, 4, kModeGate>();
+    if (e == cudaSuccess) e = configure_t<256, 3, kModeGate, 2>();
+    if (e == cudaSuccess) e = configure_t<256, 3, kModeBf16, 2>();
+    if (e == cudaSuccess) e = configure_t<256, 3, kModeResid, 2>();
+    if (e == cudaSuccess) e = configure_t<256, 6, kModeGate, 1, 2>();
+    if (e == cudaSuccess) e = configure_t<256, 6, kModeBf16, 1, 2>();
+    if (e == cudaSuccess) e = configure_t<256, 6, kModeResid, 1, 2>();
     if (e == cudaSuccess) e = configure_bn<128, 6>();
     if (e == cudaSuccess) e = configure_bn<64, 8>();
     return e;
 }
 
-template <int BN, int STAGES, int MODE>
+template <int BN, int STAGES, int MODE, int MT = 1, int CG = 1>
 static cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, dim3 grid,
                             cudaStream_t stream) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(kGemmThreads, 1, 1);
-    cfg.dynamicSmemBytes = GemmCfg<BN, STAGES>::SMEM;
+    cfg.dynamicSmemBytes = GemmCfg<BN, STAGES, MT, CG>::SMEM;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     int na = 0;
-    if (p.splits > 1) {
+    if (p.splits > 1 || CG > 1) {
         attr[na].id = cudaLaunchAttributeClusterDimension;
-        attr[na].val.clusterDim.x = 1;
+        attr[na].val.clusterDim.x = CG;
         attr[na].val.clusterDim.y = 1;
         attr[na].val.clusterDim.z = p.splits;
         ++na;
@@ -434,7 +564,7 @@ static cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const 
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, MODE>, ta, tb, p);
+    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, MODE, MT, CG>, ta, tb, p);
 }
 
 template <int BN, int STAGES>
@@ -490,7 +620,59 @@ cudaError_t launch_gemm(int bn, const CUtensorMap& ta, const CUtensorMap& tb, co
                         cudaStream_t stream) {
     if ((p.flags & kFlagRope) && bn != 256) return cudaErrorInvalidValue;
     if (p.splits < 1 || p.splits > kGemmMaxSplits) return cudaErrorInvalidValue;
-    const dim3 grid((p.M + BM - 1) / BM, (p.N + bn - 1) / bn, p.splits);
+    const int mt = p.mt > 1 ? p.mt : 1, cg = p.cg > 1 ? p.cg : 1;
+    if (p.persist && p.splits != 1) return cudaErrorInvalidValue;
+    if (mt > 1 && (mt != 2 || bn != 256 || p.splits != 1)) return cudaErrorInvalidValue;
+    if (cg > 1 && (cg != 2 || mt != 1 || bn != 256 || p.splits != 1)) return cudaErrorInvalidValue;
+    dim3 grid((p.M + mt * cg * BM - 1) / (mt * cg * BM), (p.N + bn - 1) / bn, p.splits);
+    if (p.persist) {
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        unsigned slots = unsigned(sms / cg);
+        if (cg == 2) {  // co-resident CTA pairs (clusters are placed within a GPC)
+            static int pairs = -1;
+            if (pairs < 0) {
+                cudaLaunchConfig_t c{};
+                c.gridDim = dim3(2, 1, 1);
+                c.blockDim = dim3(kGemmThreads, 1, 1);
+                c.dynamicSmemBytes = GemmCfg<256, 6, 1, 2>::SMEM;
+                cudaLaunchAttribute a[1];
+                a[0].id = cudaLaunchAttributeClusterDimension;
+                a[0].val.clusterDim.x = 2;
+                a[0].val.clusterDim.y = 1;
+                a[0].val.clusterDim.z = 1;
+                c.attrs = a;
+                c.numAttrs = 1;
+                int n = 0;
+                if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<256, 6, kModeGate, 1, 2>, &c) != cudaSuccess) n = 0;
+                pairs = n;
+                if (getenv("PI0B_GEMM_DEBUG")) fprintf(stderr, "pi0b: %d co-resident GEMM CTA pairs\n", n);
+            }
+            if (pairs > 0) slots = std::min(slots, unsigned(pairs));
+        }
+        grid = dim3(std::min<unsigned>(grid.x * grid.y, slots), 1, 1);
+    }
+    grid.x *= cg;  // CTA pairs: cluster (2, 1, 1)
+    if (cg == 2) {
+        switch (p.mode) {
+            case kModeGate: return launch_t<256, 6, kModeGate, 1, 2>(ta, tb, p, grid, stream);
+            case kModeBf16: return launch_t<256, 6, kModeBf16, 1, 2>(ta, tb, p, grid, stream);
+            case kModeResid: return launch_t<256, 6, kModeResid, 1, 2>(ta, tb, p, grid, stream);
+            default: return cudaErrorInvalidValue;
+        }
+    }
+    if (mt == 2) {
+        switch (p.mode) {
+            case kModeGate: return launch_t<256, 3, kModeGate, 2>(ta, tb, p, grid, stream);
+            case kModeBf16: return launch_t<256, 3, kModeBf16, 2>(ta, tb, p, grid, stream);
+            case kModeResid: return launch_t<256, 3, kModeResid, 2>(ta, tb, p, grid, stream);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     switch (bn) {
         case 256: return launch_bn<256, 4>(ta, tb, p, grid, stream);
         case 128: return launch_bn<128, 6>(ta, tb, p, grid, stream);

@@ -48,6 +48,10 @@ struct GemmParams {
     long long ldob;
     float* out_stats;         // [M] += sum over written columns of out^2
     const float* row0_src;    // kModeF32Store: also write row -1 from this fp32 row
+    int persist;              // 1: one CTA per SM walks the tiles (splits == 1), TMEM double buffer
+    int mt;                   // 128-row m-tiles per CTA (1, or 2 with bn = 256 and splits == 1)
+    int cg;                   // 2: CTA-pair tcgen05 (cta_group::2) 256 x 256 tiles (bn = 256, splits == 1,
+                              //    weight tensor map box = 128 rows)
 };
 
 }  // namespace pi0b

@@ -330,4 +330,50 @@ PI0B_DEV void red_add_v4_f32(float* p, float a, float b, float c, float d) {
                  : "memory");
 }
 
+// ---------------------------------------------------------------- CTA pair (cta_group::2)
+// A kernel that uses cta_group::2 must use it for every tcgen05 alloc / mma / commit.
+PI0B_DEV void tmem_alloc_cg2(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)), "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+PI0B_DEV void tmem_dealloc_cg2(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+// D[256 x N] over the pair: A rows 0..127 / B rows 0..N/2-1 from the issuing (leader) CTA's
+// shared memory, rows 128..255 / N/2..N-1 from the peer's at the same offsets; D rows
+// 0..127 land in the leader's TMEM, 128..255 in the peer's, same TMEM address.
+PI0B_DEV void umma_bf16_cg2(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// Arrive on the barrier at the same offset in both CTAs of the pair (mask 0b11) once the
+// previously issued cta_group::2 MMAs complete.
+PI0B_DEV void umma_commit_cg2(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(uint16_t(3))
+        : "memory");
+}
+// 2-D TMA tile load into this CTA's shared memory, completing bytes on a barrier that may live
+// in the peer CTA (`mbar_cluster` = shared::cluster address, e.g. the leader's).
+PI0B_DEV void tma_load_2d_cg2(void* dst, const CUtensorMap* m, uint32_t mbar_cluster, int c0, int c1, uint64_t cache_hint) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(mbar_cluster), "r"(c0), "r"(c1), "l"(cache_hint)
+        : "memory");
+}
+PI0B_DEV void mbar_arrive_cluster(uint32_t mbar_cluster) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mbar_cluster) : "memory");
+}
+// Relaxed remote arrive (no fence: a release here compiles to MEMBAR.GPU, ~1 us per call under
+// load); for arrivals whose data travels by TMA complete_tx, not by this thread's stores.
+PI0B_DEV void mbar_arrive_cluster_relaxed(uint32_t mbar_cluster) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(mbar_cluster) : "memory");
+}
+
 }  // namespace pi0b

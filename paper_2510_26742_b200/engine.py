@@ -20,7 +20,8 @@ import numpy as np
 
 from .config import ModelConfig
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpi0b.so")
+# PI0B_LIB: an alternative build of the same library (A/B experiments, scripts/variants.sh)
+LIB_PATH = os.environ.get("PI0B_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpi0b.so")
 
 PI0B_E_INVALID = -1
 PI0B_E_UNSUPPORTED = -2

@@ -76,8 +76,20 @@ def _action_report(y, ref):
             "rms_ref": float(np.sqrt(np.mean(ref * ref))), "rel": rel_err(y, ref, 0.1), "cos": cosine(y, ref)}
 
 
-@pytest.mark.parametrize("views,prompt", [(1, 0), (2, 0), (3, 32)])
-def test_engine_mid_config_matches_oracle(views, prompt):
+# GEMM variants forced onto every eligible prefill GEMM (default: chosen by size)
+GEMM_VARIANTS = {
+    "auto": {},
+    "persist+pair": {"PI0B_PERSIST": "2", "PI0B_CG": "2"},       # persistent CTA-pair tcgen05
+    "pair": {"PI0B_PERSIST": "0", "PI0B_CG": "2"},               # one CTA-pair tile per cluster
+    "persist+mt2": {"PI0B_PERSIST": "2", "PI0B_CG": "0", "PI0B_MT": "2"},
+}
+
+
+@pytest.mark.parametrize("views,prompt,variant", [(1, 0, "auto"), (2, 0, "auto"), (3, 32, "auto"),
+                                                  (2, 0, "persist+pair"), (2, 0, "pair"), (2, 0, "persist+mt2")])
+def test_engine_mid_config_matches_oracle(views, prompt, variant, monkeypatch):
+    for k, v in GEMM_VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
     cfg = mid_config(views=views, prompt_tokens=prompt)
     x = O.gen_inputs(cfg, 1)
     ref, recs = O.port_forward(cfg, x, record=_record_list(cfg))
