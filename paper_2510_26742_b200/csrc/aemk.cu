@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             unsigned long long* tr = (p.trace && wtid == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
             if (tr) tr[0] = gtimer();
             // Pair owner: its receive buffer (union tail) is free from here on -- tell the helper.
-            if (t.pair == 1 && wtid == 0) {
+            if ((t.pair == 1 || t.pair >= 3) && wtid == 0) {
                 mbar_arrive_expect_tx(pair_full, 64 * 64 * 4 + 64 * 4);  // the helper's st.async bytes
                 mbar_arrive_remote(partner_addr(pair_ready));
             }
@@ -801,6 +801,27 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 } else if (t.pair == 1) {
                     mbar_wait_cluster(pair_full, oidx & 1);
                     ++oidx;
+                } else if (t.pair >= 3) {
+                    // Symmetric pair (ae.ffn, 128-wide tile = 64 up | 64 gate, K split in two):
+                    // each CTA finalises 32 up + their 32 gate columns (half hf) and pushes its
+                    // partial of the other half's columns into the partner's receive buffer.
+                    const int hf = t.pair - 3;
+                    mbar_wait_cluster(pair_ready, hidx & 1);
+                    ++hidx;
+                    const uint32_t rbar = partner_addr(pair_full);
+                    if (drainer) {
+                        const uint32_t ta = tmem + kTAcc + tlane + dhalf * 64 + (1 - hf) * 32;
+                        const uint32_t dst = partner_addr(recv + drow * 64);
+#pragma unroll 1
+                        for (int q = 0; q < 8; ++q) {
+                            float4 v;
+                            tmem_ld4(ta + q * 4, v);
+                            st_async_v4(dst + (((dhalf * 8 + q) ^ (drow & 7)) << 4), v, rbar);
+                        }
+                    }
+                    if (wtid < 64) st_async_f32(partner_addr(recv + 64 * 64 + wtid), sm_ss[wtid], rbar);
+                    mbar_wait_cluster(pair_full, oidx & 1);
+                    ++oidx;
                 }
                 if (drainer && t.pair != 2) {
                     // Compact loops over 4-column quads of the thread's row (TMEM lane): short
@@ -821,15 +842,19 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     } else if (t.epi == kEpiQkv || t.epi == kEpiGate) {
                         // paired tile (aemk.cuh AeTileOrder): column i < 32 and its partner 32 + i;
                         // this thread: i in [16 dhalf, 16 dhalf + 16)
-                        const bool pr = t.pair == 1;  // add the helper's half-K partial
+                        const bool pr = t.pair == 1 || t.pair >= 3;  // add the partner's half-K partial
                         const float rs = pr ? 1.0f / sqrtf((sm_ss[r] + recv[64 * 64 + r]) * p.inv_width + p.eps) : sm_rs[r];
-                        const int T = t.tile >> 1, sub = t.tile & 1, i0 = dhalf * 16;
+                        // 64-wide paired tile T = tile / 2, sub-tile tile & 1; symmetric 128-wide
+                        // pair: tile T, this CTA's half
+                        const bool sym = t.pair >= 3;
+                        const int T = sym ? int(t.tile) : t.tile >> 1, sub = sym ? t.pair - 3 : t.tile & 1, i0 = dhalf * 16;
+                        const int ca = sym ? sub * 32 : 0, cb = sym ? 64 + sub * 32 : 32;  // TMEM columns
                         float xa[16], xb[16];
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
                             float4 a4, b4;
-                            tmem_ld4(ta + i0 + q * 4, a4);
-                            tmem_ld4(ta + 32 + i0 + q * 4, b4);
+                            tmem_ld4(ta + ca + i0 + q * 4, a4);
+                            tmem_ld4(ta + cb + i0 + q * 4, b4);
                             if (pr) {
                                 const float4 ha = *reinterpret_cast<const float4*>(recv + r * 64 + (((dhalf * 4 + q) ^ (r & 7)) << 2));
                                 const float4 hb = *reinterpret_cast<const float4*>(recv + r * 64 + (((8 + dhalf * 4 + q) ^ (r & 7)) << 2));
@@ -1176,8 +1201,9 @@ AePlan ae_plan(const AePlanInput& in) {
     // A phase of full-K tiles split over K between the two CTAs of a cluster (CTAs 2c, 2c + 1):
     // the owner takes the first half of K and runs the epilogue, the helper the second half.
     auto pair_phase = [&](uint8_t epi, int tiles, int wmat, int xmat, int kbt, int wbar, int wcnt, int sbar, int step,
-                          int layer) {
+                          int layer, bool sym = false) {
         const int nclu = in.num_ctas / 2, h = kbt / 2;
+        const double wscale = sym ? 2.0 : 1.0;  // sym tiles are 128 wide (16 KB k-blocks)
         std::vector<std::pair<double, int>> order;
         for (int c = 0; c < nclu; ++c) order.push_back({std::max(load[size_t(2 * c)], load[size_t(2 * c + 1)]), c});
         std::sort(order.begin(), order.end());
@@ -1188,9 +1214,10 @@ AePlan ae_plan(const AePlanInput& in) {
                 AeTask x = gemm(kXY, epi, wmat, xmat, 0, t, r ? h : 0, r ? kbt - h : h, wbar, wcnt, sbar);
                 x.step = uint16_t(step);
                 x.layer = uint16_t(layer);
-                x.pair = uint16_t(r ? 2 : 1);
+                x.pair = uint16_t(sym ? (r ? 4 : 3) : (r ? 2 : 1));
+                if (sym) x.ncol = 128;
                 const int cta = r ? own ^ 1 : own;
-                load[size_t(cta)] += (r ? kbt - h : h) * kWB * 3.0;
+                load[size_t(cta)] += (r ? kbt - h : h) * kWB * (2.0 + wscale);
                 lists[size_t(cta)].push_back(x);
             }
         }
@@ -1276,8 +1303,12 @@ AePlan ae_plan(const AePlanInput& in) {
             const int n_proj = red_phase(in.mat_wproj[size_t(l)], 0, kXO, 0, in.q_width / 64, ks_proj, bar_attn, n_attn,
                                          bar_proj, in.proj_ncol);
             const int bar_ffn = newbar();
-            const int n_ffn = full_phase(kXY, kEpiGate, tiles_ffn, in.mat_wffn[size_t(l)], in.mat_y, kbW, bar_proj,
-                                         n_proj, bar_ffn, s, l);
+            const bool pf = in.pair_ffn;  // the caller tiled mat_wffn for it (128-wide tiles)
+            need(!pf || ((2 * MLP) % 128 == 0 && 2 * (2 * MLP / 128) <= in.num_ctas && in.num_ctas % 2 == 0), "ae.ffn pairs");
+            const int n_ffn = pf ? pair_phase(kEpiGate, 2 * MLP / 128, in.mat_wffn[size_t(l)], in.mat_y, kbW, bar_proj, n_proj,
+                                              bar_ffn, s, l, true)
+                                 : full_phase(kXY, kEpiGate, tiles_ffn, in.mat_wffn[size_t(l)], in.mat_y, kbW, bar_proj,
+                                              n_proj, bar_ffn, s, l);
             const int bar_down = newbar();
             prev_cnt = red_phase(in.mat_wdown[size_t(l)], in.mat_g, kXBf16, 0, MLP / 64, ks_down, bar_ffn, n_ffn, bar_down,
                                  in.down_ncol);

@@ -1142,6 +1142,8 @@ void Engine::build_ae_mega() {
     in.down_ncol = env_int("PI0B_AE_DOWN_NCOL", in.down_ncol) == 128 ? 128 : 64;
     in.ao_ncol = env_int("PI0B_AE_AO_NCOL", in.ao_ncol) == 128 ? 128 : 64;
     in.pair_qkv = env_int("PI0B_AE_PAIR", 1) != 0;
+    in.pair_ffn = env_int("PI0B_AE_PAIR_FFN", 1) != 0 && (2 * MLP) % 128 == 0 && 2 * (2 * MLP / 128) <= num_sms_ &&
+                  num_sms_ % 2 == 0;
     in.mat_wst = wmat("ae.state_proj", 0, W);
     in.mat_wap = wmat("ae.action_proj", 0, W);
     in.mat_wao = wmat("ae.action_out", 0, W, in.ao_ncol == 128 ? kTilePlain128 : kTilePlain);
@@ -1149,7 +1151,7 @@ void Engine::build_ae_mega() {
     for (int l = 0; l < NA; ++l) {
         in.mat_wqkv.push_back(wmat("ae.qkv", l, NQ, kTilePaired));
         in.mat_wproj.push_back(wmat("ae.proj", l, W, in.proj_ncol == 128 ? kTilePlain128 : kTilePlain));
-        in.mat_wffn.push_back(wmat("ae.ffn", l, 2 * MLP, kTilePaired));
+        in.mat_wffn.push_back(wmat("ae.ffn", l, 2 * MLP, in.pair_ffn ? kTilePlain128 : kTilePaired));
         in.mat_wdown.push_back(wmat("ae.down", l, W, in.down_ncol == 128 ? kTilePlain128 : kTilePlain));
     }
     const int llm_qkv_n = llm_q_ + 2 * llm_kv_;
