@@ -42,10 +42,22 @@ constexpr int kWBlk = 64 * 64 * 2;    // 8 KB: [64 features x 64 k] bf16 SW128 i
 constexpr int kWSlot = 2 * kWBlk;     // ring slot: up to two consecutive k-blocks, one bulk copy
 constexpr int kWSt = 5;
 constexpr int kWPrefetch = 0;  // weight bytes a CTA keeps bulk-prefetched into L2 ahead
-constexpr int kXSt = 3;
+#ifndef PI0B_AE_XST
+#define PI0B_AE_XST 3
+#endif
+#ifndef PI0B_AE_FST
+#define PI0B_AE_FST 4
+#endif
+#ifndef PI0B_AE_XPAD
+#define PI0B_AE_XPAD 0
+#endif
+// X ring: bf16 operand slots of two k-blocks.  Rows 64..127 of an M=128 A operand are don't-care
+// (only the 64 activation rows are read back), so the last slot's overhang may read whatever
+// follows (the fp32 ring) instead of a pad.
+constexpr int kXSt = PI0B_AE_XST;
 constexpr int kXTile = 64 * 128;      // 8 KB: 64 activation rows x 64 k
 constexpr int kXSlot = 2 * kXTile;    // X ring slot: two k-blocks, one handshake
-constexpr int kFSt = 3;
+constexpr int kFSt = PI0B_AE_FST;  // fp32 staging ring: kFSt - 1 k-blocks in flight (latency-bound)
 constexpr int kFTile = 16384;         // fp32 staging of one k-block: 64 rows x 64 columns
 constexpr int kMaxSplits = 10;        // attention key ranges combined by the ae.proj staging
 constexpr int kBlocksPerSplit = 2;    // 64-key blocks per attention task
@@ -63,7 +75,7 @@ constexpr int kOffW = 0;
 constexpr int kOffU = kWSt * kWSlot;                // union region (128 KB)
 constexpr int kUnion = 131072;
 constexpr int kOffX = kOffU;                        // GEMM: X ring (+8 KB pad: rows 64..127 of A)
-constexpr int kOffF = kOffU + kXSt * kXSlot + kXTile;  // GEMM: fp32 ring (kXY) / partial ring (kXO)
+constexpr int kOffF = kOffU + kXSt * kXSlot + PI0B_AE_XPAD * kXTile;  // GEMM: fp32 ring (kXY) / partial ring (kXO)
 constexpr int kORegion = kUnion - (kOffF - kOffU);  // kXO partial staging: ranges x 8 KB per slot
 constexpr int kOffQ = kOffU;                        // ATTN: Q [128 x 256] = 4 x 16 KB
 constexpr int kOffK = kOffU + 65536;                // ATTN: K [2 blocks][64 x 256] = 2 x 32 KB
@@ -76,7 +88,7 @@ static_assert(kOffF + kORegion <= kOffAux && kOffF + kFSt * kFTile <= kOffAux, "
 // Pair (2-CTA split-K) receive buffer in the owner's union tail, past the X and fp32 rings:
 // the helper's [64 x 64] fp32 partial (256-byte rows) + its 64 row sums of squares.
 constexpr int kOffRecv = kOffF + kFSt * kFTile;
-static_assert(kOffRecv + 16384 + 256 <= kOffAux, "pair receive buffer");
+static_assert(kOffRecv + 16384 <= kOffAux, "pair receive buffer");
 static_assert(kAeSmem <= 232448, "shared memory budget");
 
 constexpr uint32_t kTAcc = 0, kTS = 0, kTO = 256;  // TMEM columns (512 allocated)
@@ -240,7 +252,8 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffAux + 512);
     float* sm_rs = reinterpret_cast<float*>(smem + kOffAux + 1024);     // [64]
     float* sm_ss = reinterpret_cast<float*>(smem + kOffAux + 1280);     // [64] pair tasks: raw row sums of squares
-    float* recv = reinterpret_cast<float*>(smem + kOffRecv);           // [64][64] helper partial, then [64] sums
+    float* recv = reinterpret_cast<float*>(smem + kOffRecv);           // [64][64] partner's partial
+    float* recv_ss = reinterpret_cast<float*>(smem + kOffAux + 1536);  // [64] partner's row sums of squares
     uint64_t* pair_full = mb + kBPairFull;
     uint64_t* pair_ready = mb + kBPairReady;
     float2* sm_ml = reinterpret_cast<float2*>(smem + kOffAux + 2048);   // [2][kMaxSplits][64]
@@ -795,7 +808,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                             st_async_v4(dst + (((dhalf * 8 + q) ^ (drow & 7)) << 4), v, rbar);
                         }
                     }
-                    if (wtid < 64) st_async_f32(partner_addr(recv + 64 * 64 + wtid), sm_ss[wtid], rbar);
+                    if (wtid < 64) st_async_f32(partner_addr(recv_ss + wtid), sm_ss[wtid], rbar);
                     if (tr) tr[11] = gtimer();
                     ++hidx;
                 } else if (t.pair == 1) {
@@ -819,7 +832,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                             st_async_v4(dst + (((dhalf * 8 + q) ^ (drow & 7)) << 4), v, rbar);
                         }
                     }
-                    if (wtid < 64) st_async_f32(partner_addr(recv + 64 * 64 + wtid), sm_ss[wtid], rbar);
+                    if (wtid < 64) st_async_f32(partner_addr(recv_ss + wtid), sm_ss[wtid], rbar);
                     mbar_wait_cluster(pair_full, oidx & 1);
                     ++oidx;
                 }
@@ -843,7 +856,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         // paired tile (aemk.cuh AeTileOrder): column i < 32 and its partner 32 + i;
                         // this thread: i in [16 dhalf, 16 dhalf + 16)
                         const bool pr = t.pair == 1 || t.pair >= 3;  // add the partner's half-K partial
-                        const float rs = pr ? 1.0f / sqrtf((sm_ss[r] + recv[64 * 64 + r]) * p.inv_width + p.eps) : sm_rs[r];
+                        const float rs = pr ? 1.0f / sqrtf((sm_ss[r] + recv_ss[r]) * p.inv_width + p.eps) : sm_rs[r];
                         // 64-wide paired tile T = tile / 2, sub-tile tile & 1; symmetric 128-wide
                         // pair: tile T, this CTA's half
                         const bool sym = t.pair >= 3;

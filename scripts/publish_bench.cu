@@ -30,7 +30,7 @@ constexpr int kSlots = 5, kSlot = 16384;
 
 __global__ void __launch_bounds__(288, 1) pp_kernel(const uint8_t* w, long long wbytes, int stream, int pub,
                                                     unsigned* flags, uint4* data, int rounds, unsigned long long* out,
-                                                    volatile int* stop) {
+                                                    volatile int* stop, int dmode) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -98,15 +98,19 @@ __global__ void __launch_bounds__(288, 1) pp_kernel(const uint8_t* w, long long 
                 asm volatile("fence.acq_rel.gpu;" ::: "memory");
             }
             named_bar_sync(1, 256);
-            const uint4 v = __ldcg(pdata + tid * 2);
-            if (v.x != target) ++bad;
+            if (dmode == 0) {
+                const uint4 v = __ldcg(pdata + tid * 2);
+                if (v.x != target) ++bad;
+            }
         }
         if (initiator && r == 1 && tid == 0) {
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
         }
         const unsigned tag = initiator ? unsigned(r + 1) : unsigned(r + 1);
-        mydata[tid * 2] = make_uint4(tag, tag, tag, tag);
-        mydata[tid * 2 + 1] = make_uint4(tag, tag, tag, tag);
+        if (dmode != 1) {
+            mydata[tid * 2] = make_uint4(tag, tag, tag, tag);
+            mydata[tid * 2 + 1] = make_uint4(tag, tag, tag, tag);
+        }
         named_bar_sync(1, 256);
         if (tid == 0) {
             if (pub == 0) {
@@ -154,8 +158,10 @@ int main(int argc, char** argv) {
     const char* sn[] = {"none", "cp.async", "bulk"};
     const char* pn[] = {"red.release", "fence+red", "st.release"};
     const int rounds = 200;
+    const char* dn[] = {"write+read 8KB", "flag only", "write only"};
+    for (int dmode = 0; dmode < 3; ++dmode)
     for (int stream = s_lo; stream <= s_hi; ++stream)
-        for (int pub = 0; pub < 3; ++pub) {
+        for (int pub = 0; pub < 1; ++pub) {
             for (int rep = 0; rep < 2; ++rep) {
                 cudaMemset(flags, 0, G * 32 * 4);
                 cudaMemset(data, 0, (size_t)G * 512 * 16);
@@ -164,7 +170,7 @@ int main(int argc, char** argv) {
                 cudaEventCreate(&a);
                 cudaEventCreate(&b);
                 cudaEventRecord(a);
-                pp_kernel<<<G, 288, smem>>>(w, wbytes, stream, pub, flags, data, rounds, out, stop);
+                pp_kernel<<<G, 288, smem>>>(w, wbytes, stream, pub, flags, data, rounds, out, stop, dmode);
                 cudaEventRecord(b);
                 cudaError_t e = cudaDeviceSynchronize();
                 float ms = 0;
@@ -180,8 +186,8 @@ int main(int argc, char** argv) {
                 }
                 m /= (G / 2);
                 if (rep == 1)
-                    printf("stream=%-8s publish=%-12s one-way %6.3f us (max pair %6.3f)  kernel %.3f ms  HBM %.0f GB/s  bad=%llu %s\n",
-                           sn[stream], pn[pub], m * 1e-3, mx * 1e-3, ms, 0.0, bad, e == cudaSuccess ? "" : cudaGetErrorString(e));
+                    printf("%-15s stream=%-8s publish=%-12s one-way %6.3f us (max pair %6.3f)  kernel %.3f ms  HBM %.0f GB/s  bad=%llu %s\n",
+                           dn[dmode], sn[stream], pn[pub], m * 1e-3, mx * 1e-3, ms, 0.0, bad, e == cudaSuccess ? "" : cudaGetErrorString(e));
             }
         }
     return 0;
