@@ -1120,7 +1120,7 @@ cudaError_t aemk_configure() {
     return cudaFuncSetAttribute(aemk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAeSmem);
 }
 
-cudaError_t aemk_launch(const AeParams& p, int grid, cudaStream_t stream) {
+cudaError_t aemk_launch(const AeParams& p, int grid, cudaStream_t stream, bool cluster) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid, 1, 1);
     cfg.blockDim = dim3(kAeThreads, 1, 1);
@@ -1134,7 +1134,7 @@ cudaError_t aemk_launch(const AeParams& p, int grid, cudaStream_t stream) {
     attr[1].val.clusterDim.y = 1;
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = cluster ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, aemk_kernel, p);
 }
 

@@ -140,6 +140,9 @@ struct AePlan {
 
 AePlan ae_plan(const AePlanInput& in);
 cudaError_t aemk_configure();
-cudaError_t aemk_launch(const AeParams& p, int grid, cudaStream_t stream);
+// cluster: launch as 2-CTA clusters (required when the plan has pair tasks); without pair tasks
+// the kernel also runs as a plain cooperative launch (e.g. under ncu, which cannot replay the
+// cooperative + cluster launch).
+cudaError_t aemk_launch(const AeParams& p, int grid, cudaStream_t stream, bool cluster = true);
 
 }  // namespace pi0b

@@ -348,6 +348,7 @@ private:
     // action-expert megakernel (aemk.cu)
     bool ae_mega_ = true;
     AePlan ae_plan_;
+    bool ae_cluster_ = true;
     AeParams ae_p_{};
     float* state32_ = nullptr;
     struct TiledW {
@@ -1144,6 +1145,7 @@ void Engine::build_ae_mega() {
     in.pair_qkv = env_int("PI0B_AE_PAIR", 1) != 0;
     in.pair_ffn = env_int("PI0B_AE_PAIR_FFN", 1) != 0 && (2 * MLP) % 128 == 0 && 2 * (2 * MLP / 128) <= num_sms_ &&
                   num_sms_ % 2 == 0;
+    ae_cluster_ = in.pair_qkv || in.pair_ffn;  // pair tasks need the 2-CTA cluster launch
     in.mat_wst = wmat("ae.state_proj", 0, W);
     in.mat_wap = wmat("ae.action_proj", 0, W);
     in.mat_wao = wmat("ae.action_out", 0, W, in.ao_ncol == 128 ? kTilePlain128 : kTilePlain);
@@ -1383,7 +1385,7 @@ void Engine::run_ops(int part, cudaStream_t st) {
                 break;
             case kOpF32F64: PI0B_CUDA(launch_f32_to_f64(op.src32, op.ld32, op.rows, op.cols, op.dst64, st)); break;
             case kOpMemset: PI0B_CUDA(cudaMemsetAsync(op.mptr, 0, op.mbytes, st)); break;
-            case kOpAeMega: PI0B_CUDA(aemk_launch(ae_p_, num_sms_, st)); break;
+            case kOpAeMega: PI0B_CUDA(aemk_launch(ae_p_, num_sms_, st, ae_cluster_)); break;
         }
         if (o_.record_checkpoints)
             for (const CkTag& tg : op.extra_ck) {
@@ -1510,7 +1512,7 @@ double Engine::time_node(const std::string& node, int reps, int* launches) {
         else if (op.kind == kOpSkinny) PI0B_CUDA(launch_skinny(op.ta, op.tb, op.gp, op.n_packed, op.cluster, pdl_, stream_));
         else if (op.kind == kOpAeMega) {
             PI0B_CUDA(cudaMemsetAsync(ae_zero_, 0, ae_zero_bytes_, stream_));
-            PI0B_CUDA(aemk_launch(ae_p_, num_sms_, stream_));
+            PI0B_CUDA(aemk_launch(ae_p_, num_sms_, stream_, ae_cluster_));
         }
         else PI0B_CUDA(launch_fattn(op.hd, op.fm, op.ap, stream_));
     };
