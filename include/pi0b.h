@@ -148,8 +148,8 @@ typedef struct pi0b_attn_desc {
     const void* k0; const void* v0; int64_t ld0; int rows0;
     const void* k1; const void* v1; int64_t ld1; int rows1;
     void* out; int64_t ldo;
-    int kv_splits;                  /* 0 = choose                                   */
-    float* ws; int* counters;       /* scratch for kv_splits > 1                    */
+    int kv_splits;                  /* 0/1: one pass; 2, 4, 8: key splits (cluster) */
+    float* ws; int* counters;       /* unused (DSMEM combine); kept for ABI layout  */
 } pi0b_attn_desc;
 int pi0b_attention(const pi0b_attn_desc* d, void* stream);
 /* Workspace floats / counters an attention launch with these dims needs. */

@@ -26,11 +26,9 @@ struct AttnParams {
     float scale_log2;         // log2(e) / sqrt(d)
     __nv_bfloat16* out;       // [q_rows, heads*d]
     long long ldo;
-    int kv_splits;            // grid.y; > 1 -> partials in ws, last CTA combines
-    int kv_per_split;         // keys per split (multiple of the key tile)
-    float* ws_o;              // [splits][grid.z][q_tiles*64][d] fp32
-    float* ws_ml;             // [splits][grid.z][q_tiles*64][2]
-    int* counters;            // [grid.z * q_tiles], zero on entry and exit
+    int kv_splits;            // grid.y = key splits (1, 2, 4, 8): a (1, S, 1) cluster per q tile,
+                              // partials combined over DSMEM (no workspace)
+    int kv_per_split;         // informational: keys per split
 };
 
 }  // namespace pi0b

@@ -161,7 +161,7 @@ int pi0b_attention(const pi0b_attn_desc* d, void* stream) {
     p.out = static_cast<__nv_bfloat16*>(d->out);
     p.ldo = d->ldo;
     p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(d->head_dim)));
-    p.kv_splits = 1;
+    p.kv_splits = d->kv_splits > 1 ? d->kv_splits : 1;  // 2, 4, 8: key splits combined over DSMEM
     p.kv_per_split = d->rows0 + d->rows1;
     try {
         const FaMaps m = make_fattn_maps(p, d->head_dim);

@@ -652,7 +652,20 @@ void Engine::add_attn(int part, const std::string& node, int inst, int hd, AttnP
     op.kind = kOpAttn;
     op.part = part;
     op.hd = hd;
-    ap.kv_splits = 1;
+    // Key splits (a (1, S, 1) cluster per q tile, DSMEM combine): as many as keep the grid
+    // within one wave, at least two 64-key tiles per split.  PI0B_ATTN_SPLITS[_<NODE>] override.
+    {
+        std::string key = node;
+        for (char& ch : key) ch = ch == '.' ? '_' : char(std::toupper(static_cast<unsigned char>(ch)));
+        const int base = ((ap.heads / ap.kv_heads) * ap.q_rows + 127) / 128 * ap.kv_heads;
+        const int tiles = (ap.rows0 + ap.rows1 + 63) / 64;
+        int S = 1;
+        // measured: splits pay only for grids below half the SMs, and clusters of 8 are slow
+        // (llm.attn 2v: 15.9 -> 13.8 us at S = 4, 37.8 us at S = 8; ve.attn slower at S = 2)
+        while (S < 4 && 2 * base <= num_sms_ / 2 && base * S * 2 <= num_sms_ && tiles >= S * 4) S *= 2;
+        S = env_int(("PI0B_ATTN_SPLITS_" + key).c_str(), env_int("PI0B_ATTN_SPLITS", S));
+        ap.kv_splits = (S == 2 || S == 4 || S == 8) ? S : 1;
+    }
     ap.kv_per_split = ap.rows0 + ap.rows1;
     ap.scale_log2 = float(1.4426950408889634 / std::sqrt(double(hd)));
     if ((ap.rows0 % 32) || (ap.rows1 % 32))

@@ -113,7 +113,13 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
     const int grows = hpg * p.q_rows;
     const int kvh = grp;
     const int total = p.rows0 + p.rows1;
-    const int ntiles = (total + kFaKeys - 1) / kFaKeys;
+    // Key split (grid.y = S, launched as a (1, S, 1) cluster): this CTA takes key tiles
+    // [t0, t0 + ntiles); the partial outputs are combined over DSMEM at the end.
+    const int S = gridDim.y;
+    const int ntiles_all = (total + kFaKeys - 1) / kFaKeys;
+    const int tps = (ntiles_all + S - 1) / S;
+    const int t0 = int(blockIdx.y) * tps;
+    const int ntiles = max(0, min(ntiles_all, t0 + tps) - t0);
 
     if (tid == 0) {
         for (int s = 0; s < KK; ++s) {
@@ -164,7 +170,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             auto load_rows = [&](bool is_v, uint8_t* dst_tile, int t, int regions) {
                 // two 32-key boxes per region; each box lies in one key segment (or fully OOB -> zeros)
                 for (int half = 0; half < 2; ++half) {
-                    const int j = t * kFaKeys + half * 32;
+                    const int j = (t0 + t) * kFaKeys + half * 32;
                     const bool seg0 = j < p.rows0;
                     const CUtensorMap* m = seg0 ? (is_v ? &maps.v0 : &maps.k0) : (is_v ? &maps.v1 : &maps.k1);
                     const int row = seg0 ? j : j - p.rows0;
@@ -206,7 +212,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                 }
                 __syncwarp();
             };
-            issue_qk(0);
+            if (ntiles > 0) issue_qk(0);
             for (int t = 0; t < ntiles; ++t) {
                 if (t + 1 < ntiles) issue_qk(t + 1);
                 const int sv = t % KV;
@@ -243,7 +249,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             tmem_ld32(trow + C::TMEM_S + sb * 64 + 32, s1);
             tc_fence_before();
             mbar_arrive(&s_free[sb]);
-            const int kbase = t * kFaKeys;
+            const int kbase = (t0 + t) * kFaKeys;
             float mx = -INFINITY;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -298,13 +304,36 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             mbar_arrive(&p_full[t & 1]);
         }
         // epilogue: O / l -> bf16
-        mbar_wait(&o_done[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
+        if (ntiles > 0) mbar_wait(&o_done[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
         tc_fence_after();
         const float il = l > 0.f ? 1.f / l : 0.f;
+        if (S > 1) {
+            // park this split's normalised partial (bf16, row r at r * DV * 2, 16-byte chunks
+            // swizzled by r & 7) in the now idle K ring, (m, l) in the P buffers
+            uint8_t* prow = sK + r * (DV * 2);
+#pragma unroll 1
+            for (int c = 0; c < DV / 32; ++c) {
+                float o[32];
+                if (ntiles > 0) tmem_ld32(trow + C::TMEM_O + c * 32, o);
+                else
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) o[j] = 0.f;
+#pragma unroll
+                for (int j = 0; j < 32; j += 8) {
+                    uint4 u;
+                    u.x = pack_bf16(o[j] * il, o[j + 1] * il);
+                    u.y = pack_bf16(o[j + 2] * il, o[j + 3] * il);
+                    u.z = pack_bf16(o[j + 4] * il, o[j + 5] * il);
+                    u.w = pack_bf16(o[j + 6] * il, o[j + 7] * il);
+                    *reinterpret_cast<uint4*>(prow + ((((c * 32 + j) >> 3) ^ (r & 7)) << 4)) = u;
+                }
+            }
+            reinterpret_cast<float2*>(sP)[r] = make_float2(l > 0.f ? m_ref : -INFINITY, l);
+        }
         __nv_bfloat16* orow = p.out;
         if (row_ok) orow = p.out + (long long)(g % p.q_rows) * p.ldo + (kvh + p.kv_heads * (g / p.q_rows)) * D;
 #pragma unroll 1
-        for (int c = 0; c < DV / 32; ++c) {
+        for (int c = 0; c < (S > 1 ? 0 : DV / 32); ++c) {
             float o[32];
             tmem_ld32(trow + C::TMEM_O + c * 32, o);
             if (row_ok) {
@@ -321,6 +350,57 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                 }
             }
         }
+    }
+    if (S > 1) {
+        // Combine the S key splits of this q tile: CTA y of the cluster finalises rows
+        // [y * 128 / S, (y + 1) * 128 / S): o = sum_j w_j O_j / sum_j w_j, w_j = l_j 2^(m_j - M),
+        // reading the peers' parked partials over DSMEM.
+        cluster_sync_all();
+        const int rows = kFaRows / S, r0 = int(blockIdx.y) * rows;
+        float* wts = reinterpret_cast<float*>(sQ);  // [rows][S] normalised weights (Q is idle)
+        for (int i = tid; i < rows; i += kFaThreads) {
+            const int r = r0 + i;
+            float m[8], l[8], M = -INFINITY, den = 0.f;
+            for (int j = 0; j < S; ++j) {
+                const float4 v = ld_dsmem_f32x4(mapa_shared(smem_u32(sP) + (r & ~1) * 8, j));
+                m[j] = (r & 1) ? v.z : v.x;
+                l[j] = (r & 1) ? v.w : v.y;
+                M = fmaxf(M, m[j]);
+            }
+            for (int j = 0; j < S; ++j) {
+                const float w = l[j] > 0.f ? l[j] * exp2f(m[j] - M) : 0.f;
+                m[j] = w;
+                den += w;
+            }
+            for (int j = 0; j < S; ++j) wts[i * S + j] = den > 0.f ? m[j] / den : 0.f;
+        }
+        __syncthreads();
+        constexpr int CH = DV / 8;  // 16-byte chunks per row
+        for (int it = tid; it < rows * CH; it += kFaThreads) {
+            const int i = it / CH, c = it % CH, r = r0 + i;
+            const int g = qt * kFaRows + r;
+            if (g >= grows || c * 8 >= D) continue;
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            const uint32_t off = smem_u32(sK) + r * (DV * 2) + ((c ^ (r & 7)) << 4);
+            for (int j = 0; j < S; ++j) {
+                const float w = wts[i * S + j];
+                const float4 v = ld_dsmem_f32x4(mapa_shared(off, j));
+                const uint32_t u[4] = {__float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z), __float_as_uint(v.w)};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    acc[2 * e] += w * __uint_as_float(u[e] << 16);
+                    acc[2 * e + 1] += w * __uint_as_float(u[e] & 0xffff0000u);
+                }
+            }
+            __nv_bfloat16* orow = p.out + (long long)(g % p.q_rows) * p.ldo + (kvh + p.kv_heads * (g / p.q_rows)) * D;
+            uint4 o;
+            o.x = pack_bf16(acc[0], acc[1]);
+            o.y = pack_bf16(acc[2], acc[3]);
+            o.z = pack_bf16(acc[4], acc[5]);
+            o.w = pack_bf16(acc[6], acc[7]);
+            *reinterpret_cast<uint4*>(orow + c * 8) = o;
+        }
+        cluster_sync_all();  // peers are done reading this CTA's parked partial
     }
     tc_fence_before();
     __syncthreads();
@@ -365,18 +445,31 @@ static cudaError_t fa_launch_t(const FaMaps& maps, const AttnParams& p, dim3 gri
     cfg.blockDim = dim3(kFaThreads, 1, 1);
     cfg.dynamicSmemBytes = FaCfg<D, DK, DV, KK, KV>::SMEM;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (g_fa_pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (grid.y > 1) {  // key splits of one q tile form a cluster (DSMEM combine)
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = 1;
+        attr[na].val.clusterDim.y = grid.y;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = g_fa_pdl ? 1 : 0;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, fattn_kernel<D, DK, DV, KK, KV>, maps, p);
 }
 
-// Single pass over all keys; grid = (stacked q tiles of 128, 1, kv groups).
+// grid = (stacked q tiles of 128, key splits (p.kv_splits: 1, 2, 4 or 8), kv groups).
 cudaError_t launch_fattn(int head_dim, const FaMaps& maps, const AttnParams& p, cudaStream_t stream) {
     const int grows = (p.heads / p.kv_heads) * p.q_rows;
-    const dim3 grid((grows + kFaRows - 1) / kFaRows, 1, p.kv_heads);
+    const int S = p.kv_splits > 1 ? p.kv_splits : 1;
+    if (S != 1 && S != 2 && S != 4 && S != 8) return cudaErrorInvalidValue;
+    const dim3 grid((grows + kFaRows - 1) / kFaRows, S, p.kv_heads);
     if ((p.rows0 % 32) || (p.rows1 % 32)) return cudaErrorInvalidValue;
     switch (head_dim) {
         case 72: return fa_launch_t<72, 80, 128, 3, 3>(maps, p, grid, stream);

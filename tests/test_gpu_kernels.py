@@ -201,7 +201,9 @@ def _attn_ref(q, k, v, heads, kv_heads, hd):
 @pytest.mark.parametrize("hd,heads,kv_heads,q_rows,rows0,rows1,splits", [
     (72, 16, 16, 512, 512, 0, 0), (72, 16, 16, 768, 768, 0, 0), (72, 4, 4, 256, 256, 0, 2),
     (256, 8, 1, 512, 512, 0, 0), (256, 8, 1, 800, 800, 0, 0), (256, 8, 1, 512, 512, 0, 1),
-    (256, 8, 1, 64, 512, 64, 0), (256, 8, 1, 64, 800, 64, 0), (256, 2, 1, 64, 256, 64, 3),
+    (256, 8, 1, 64, 512, 64, 0), (256, 8, 1, 64, 800, 64, 0), (256, 2, 1, 64, 256, 64, 4),
+    (72, 16, 16, 512, 512, 0, 2), (256, 8, 1, 512, 512, 0, 4), (256, 8, 1, 800, 800, 0, 8),
+    (72, 16, 16, 768, 768, 0, 8),
 ])
 def test_attention(hd, heads, kv_heads, q_rows, rows0, rows1, splits):
     # q/k/v live in one qkv-style buffer like the engine's (row stride = q + 2 kv)
