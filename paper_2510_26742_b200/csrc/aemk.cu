@@ -968,6 +968,10 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 // softmax over the range, normalised partial + (row max, row sum) to global.
                 const uint32_t ph = aidx & 1;
                 const int rb = t.tile, split = t.kb0, nb = t.nkb;
+                // one = single-head task (tile = head): 64 query rows in A rows 0..63 of the M=128
+                // MMAs (rows 64..127 don't-care), half the Q load / O readout / O store of a pair
+                const bool one = t.ncol == 1;
+                const int hrow = one ? 64 : 128;  // valid stacked query rows
                 const int key0 = split * kBlocksPerSplit * 64;
                 const AeMat km = load_mat(p.mats + t.wmat);  // LLM K/V cache of layer (i % llm_layers)
                 const __nv_bfloat16* kvc = reinterpret_cast<const __nv_bfloat16*>(km.ptr);
@@ -989,12 +993,12 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         cp_async16(dst + (kmaj ? a4 * 16384 + swz(b * 64 + kr, c) : b * 32768 + a4 * 8192 + swz(kr, c)), src, ok);
                     }
                 };
-                {   // Q (both heads of the pair) and K
+                {   // Q (both heads of the pair, or the one head) and K
 #pragma unroll 4
-                    for (int u = 0; u < 16; ++u) {
+                    for (int u = 0; u < (one ? 8 : 16); ++u) {
                         const int q = wtid + 256 * u;
-                        const int a4 = q >> 10, R = (q >> 3) & 127, c = q & 7;
-                        const int head = 2 * rb + (R >> 6);
+                        const int a4 = one ? q >> 9 : q >> 10, R = (q >> 3) & (hrow - 1), c = q & 7;
+                        const int head = one ? rb : 2 * rb + (R >> 6);
                         const bool ok = head < p.heads;
                         cp_async16(sQ + a4 * 16384 + swz(R, c),
                                    ok ? p.qkv + (size_t)(R & 63) * p.n_qkv + head * 256 + a4 * 64 + c * 8 : p.qkv, ok);
@@ -1014,8 +1018,9 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     // `side` 0 takes key block 0 / output columns 0..127, side 1 block 1 / 128..255.
                     const int side = (warp >= 6) ? 1 : 0;
                     const int R = wq * 32 + lane;
-                    const int head = 2 * rb + (R >> 6);
+                    const int head = one ? rb : 2 * rb + (R >> 6);
                     const bool hv = head < p.heads;
+                    const bool act = R < hrow;  // warp-uniform: single-head tasks use lanes 0..63
                     const int nk = p.kv_rows0 + 64 - key0;  // valid keys from key0
                     float* xch = reinterpret_cast<float*>(sm_ml);  // [2 sides][128 rows] exchange
                     const uint32_t ts = tmem + kTS + tlane + side * 64;
@@ -1025,9 +1030,11 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     // one TMEM pass (64 scores per thread kept in registers): TMEM reads run at
                     // ~64 B/cycle per SM, so a second pass over S costs ~0.5 us
                     float sv[64];
-                    tmem_ld32(ts, *reinterpret_cast<float(*)[32]>(sv));  // warp-uniform
-                    tmem_ld32(ts + 32, *reinterpret_cast<float(*)[32]>(sv + 32));
-                    const int nkm = mine ? nk - side * 64 : 0;  // valid keys of this thread's block
+                    if (act) {
+                        tmem_ld32(ts, *reinterpret_cast<float(*)[32]>(sv));  // warp-uniform
+                        tmem_ld32(ts + 32, *reinterpret_cast<float(*)[32]>(sv + 32));
+                    }
+                    const int nkm = mine && act ? nk - side * 64 : 0;  // valid keys of this thread's block
                     float mx = -INFINITY;
 #pragma unroll
                     for (int e = 0; e < 64; ++e) {
@@ -1038,7 +1045,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     named_bar_sync(1, kWorkers);
                     mx = fmaxf(xch[R], xch[128 + R]);
                     float l = 0.f;
-                    if (mine) {
+                    if (mine && act) {
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
                             uint32_t pk[4];
@@ -1065,21 +1072,21 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     // normalised O rows (bf16) -> smem [128 rows][512 B] (Q/K/V/P are free now)
                     uint8_t* orow_s = sQ + R * 512 + side * 256;
 #pragma unroll 1
-                    for (int q = 0; q < 16; ++q) {
+                    for (int q = 0; q < (act ? 16 : 0); ++q) {
                         float o[8];
                         tmem_ld8(tmem + kTO + tlane + side * 128 + q * 8, o);
                         *reinterpret_cast<uint4*>(orow_s + ((q ^ (R & 15)) << 4)) =
                             make_uint4(pack2(o[0] * il, o[1] * il), pack2(o[2] * il, o[3] * il),
                                        pack2(o[4] * il, o[5] * il), pack2(o[6] * il, o[7] * il));
                     }
-                    if (side == 0 && hv) p.ml[(size_t)split * p.heads * 64 + head * 64 + (R & 63)] = make_float2(mx, l);
+                    if (side == 0 && hv && act) p.ml[(size_t)split * p.heads * 64 + head * 64 + (R & 63)] = make_float2(mx, l);
                     tc_fence_before();
                     named_bar_sync(1, kWorkers);
                     // coalesced store: each warp writes whole 512-byte rows
                     __nv_bfloat16* obase = p.opart + (size_t)split * 64 * p.q_width;
 #pragma unroll 1
-                    for (int e = wtid; e < 128 * 32; e += kWorkers) {
-                        const int rr = e >> 5, cc = e & 31, hd2 = 2 * rb + (rr >> 6);
+                    for (int e = wtid; e < hrow * 32; e += kWorkers) {
+                        const int rr = e >> 5, cc = e & 31, hd2 = one ? rb : 2 * rb + (rr >> 6);
                         if (hd2 < p.heads) {
                             const int half = cc >> 4, q16 = cc & 15;
                             const uint4 v = *reinterpret_cast<const uint4*>(sQ + rr * 512 + half * 256 + ((q16 ^ (rr & 15)) << 4));
@@ -1270,7 +1277,7 @@ AePlan ae_plan(const AePlanInput& in) {
     const int ks_proj = splits_for(W / in.proj_ncol, in.q_width / 64, in.proj_tasks);
     const int ks_down = splits_for(W / in.down_ncol, MLP / 64, in.down_tasks);
     const int pairs = (in.heads + 1) / 2;
-    const int n_attn = pairs * splits;
+    const int n_attn = (in.attn_single ? in.heads : pairs) * splits;
 
     // ae.state_proj -> st
     const int bar_init = newbar();
@@ -1294,10 +1301,11 @@ AePlan ae_plan(const AePlanInput& in) {
             const int bar_attn = newbar();
             {
                 std::vector<Item> it;
-                for (int rb = 0; rb < pairs; ++rb)
+                for (int rb = 0; rb < (in.attn_single ? in.heads : pairs); ++rb)
                     for (int j = 0; j < splits; ++j) {
                         AeTask x{};
                         x.kind = kAeAttn;
+                        x.ncol = uint16_t(in.attn_single ? 1 : 0);  // 1: single-head task (tile = head)
                         x.wmat = uint16_t(in.mat_kv[size_t(gl % int(in.mat_kv.size()))]);  // llm.qkv@mod
                         x.tile = uint16_t(rb);
                         x.kb0 = uint16_t(j);

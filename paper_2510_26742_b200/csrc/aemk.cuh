@@ -62,7 +62,7 @@ static_assert(sizeof(AeMat) == 32, "AeMat layout");
 struct AeTask {
     uint8_t kind, xsrc, epi, rowoff;  // rowoff: kEpiRed target rows start at y row `rowoff`
     uint16_t wmat, xmat;              // AeMat indices (weights / activation)
-    uint16_t ncol;                    // GEMM: output tile width, 64 or 128 (0 = 64)
+    uint16_t ncol;                    // GEMM: output tile width, 64 or 128 (0 = 64); ATTN: 1 = one head
     uint16_t tile;                    // GEMM: output tile (ncol features); ATTN: head pair
     uint16_t kb0, nkb;                // GEMM: k-block range; ATTN: key split, #key blocks
     uint16_t wait_bar, wait_cnt;      // wait until counter wait_bar reaches wait_cnt (cnt > 0)
@@ -119,6 +119,7 @@ struct AePlanInput {
     int ao_tasks = 64, proj_tasks = 128, down_tasks = 128;  // split-K task targets per phase
     int proj_ncol = 128, down_ncol = 64, ao_ncol = 64;     // residual-update tile widths (64 or 128)
     bool pair_qkv = true;  // ae.qkv tiles split over K between the two CTAs of a cluster (DSMEM)
+    bool attn_single = true;  // one attention task per (head, key range) instead of (head pair, range)
     bool pair_ffn = true;  // ae.ffn as 128-wide tiles split over K, symmetric exchange (mat_wffn kTilePlain128)
     int mat_wst, mat_wap, mat_wao, mat_whead;
     std::vector<int> mat_wqkv, mat_wproj, mat_wffn, mat_wdown, mat_kv;
