@@ -20,6 +20,11 @@ using namespace pi0b;
 PI0B_DEV void cp_async_arrive_noinc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+PI0B_DEV unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 PI0B_DEV unsigned ld_relaxed(const unsigned* p) {
     unsigned v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -93,9 +98,14 @@ __global__ void __launch_bounds__(288, 1) pp_kernel(const uint8_t* w, long long 
             // wait for the partner's round r (initiator: r-1 answered)
             const unsigned target = initiator ? unsigned(r) : unsigned(r + 1);
             if (tid == 0) {
-                while (ld_relaxed(pflag) < target) {
+                if (pub >= 10) {
+                    while (ld_acquire(pflag) < target) {
+                    }
+                } else {
+                    while (ld_relaxed(pflag) < target) {
+                    }
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
                 }
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
             }
             named_bar_sync(1, 256);
             if (dmode == 0) {
@@ -113,7 +123,7 @@ __global__ void __launch_bounds__(288, 1) pp_kernel(const uint8_t* w, long long 
         }
         named_bar_sync(1, 256);
         if (tid == 0) {
-            if (pub == 0) {
+            if (pub == 0 || pub == 10) {
                 asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(myflag) : "memory");
             } else if (pub == 1) {
                 asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -161,7 +171,7 @@ int main(int argc, char** argv) {
     const char* dn[] = {"write+read 8KB", "flag only", "write only"};
     for (int dmode = 0; dmode < 3; ++dmode)
     for (int stream = s_lo; stream <= s_hi; ++stream)
-        for (int pub = 0; pub < 1; ++pub) {
+        for (int pub : {0, 10}) {
             for (int rep = 0; rep < 2; ++rep) {
                 cudaMemset(flags, 0, G * 32 * 4);
                 cudaMemset(data, 0, (size_t)G * 512 * 16);
@@ -187,7 +197,7 @@ int main(int argc, char** argv) {
                 m /= (G / 2);
                 if (rep == 1)
                     printf("%-15s stream=%-8s publish=%-12s one-way %6.3f us (max pair %6.3f)  kernel %.3f ms  HBM %.0f GB/s  bad=%llu %s\n",
-                           dn[dmode], sn[stream], pn[pub], m * 1e-3, mx * 1e-3, ms, 0.0, bad, e == cudaSuccess ? "" : cudaGetErrorString(e));
+                           dn[dmode], sn[stream], pub == 10 ? "red.rel/ld.acq" : pn[pub], m * 1e-3, mx * 1e-3, ms, 0.0, bad, e == cudaSuccess ? "" : cudaGetErrorString(e));
             }
         }
     return 0;
