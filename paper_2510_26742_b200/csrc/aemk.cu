@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <queue>
+#include <type_traits>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -458,7 +459,8 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             if (tr) tr[0] = gtimer();
             // Pair owner: its receive buffer (union tail) is free from here on -- tell the helper.
             if ((t.pair == 1 || t.pair >= 3) && wtid == 0) {
-                mbar_arrive_expect_tx(pair_full, 64 * 64 * 4 + 64 * 4);  // the helper's st.async bytes
+                // the partner's st.async bytes: its partial of this CTA's columns + 64 row sums
+                mbar_arrive_expect_tx(pair_full, (t.pair >= 5 ? 64 * 32 * 4 : 64 * 64 * 4) + 64 * 4);
                 mbar_arrive_remote(partner_addr(pair_ready));
             }
             // Attention over a range of cached LLM keys: K does not depend on this step, so its
@@ -821,21 +823,27 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     mbar_wait_cluster(pair_full, oidx & 1);
                     ++oidx;
                 } else if (t.pair >= 3) {
-                    // Symmetric pair (ae.ffn, 128-wide tile = 64 up | 64 gate, K split in two):
-                    // each CTA finalises 32 up + their 32 gate columns (half hf) and pushes its
-                    // partial of the other half's columns into the partner's receive buffer.
-                    const int hf = t.pair - 3;
+                    // Symmetric pair, K split in two, each CTA finalising half of the tile's
+                    // columns and pushing its partial of the other half into the partner's receive
+                    // buffer:  3 / 4 = ae.ffn 128-wide tile (64 up | 64 gate; 32 + 32 per CTA),
+                    //          5 / 6 = ae.qkv 64-wide paired tile (32 | 32 RoPE partners; 16 + 16).
+                    const bool wide = t.pair <= 4;
+                    const int hf = wide ? t.pair - 3 : t.pair - 5;
+                    const int hw = wide ? 32 : 16;         // columns per half and part
+                    const int pb = wide ? 64 : 32;         // first partner column
+                    const int rsf = wide ? 64 : 32;        // receive row stride (floats)
                     mbar_wait_cluster(pair_ready, hidx & 1);
                     ++hidx;
                     const uint32_t rbar = partner_addr(pair_full);
                     if (drainer) {
-                        const uint32_t ta = tmem + kTAcc + tlane + dhalf * 64 + (1 - hf) * 32;
-                        const uint32_t dst = partner_addr(recv + drow * 64);
+                        // dhalf 0: the other half's features, dhalf 1: their partners
+                        const uint32_t ta = tmem + kTAcc + tlane + dhalf * pb + (1 - hf) * hw;
+                        const uint32_t dst = partner_addr(recv + drow * rsf);
 #pragma unroll 1
-                        for (int q = 0; q < 8; ++q) {
+                        for (int q = 0; q < hw / 4; ++q) {
                             float4 v;
                             tmem_ld4(ta + q * 4, v);
-                            st_async_v4(dst + (((dhalf * 8 + q) ^ (drow & 7)) << 4), v, rbar);
+                            st_async_v4(dst + (((dhalf * (hw / 4) + q) ^ (drow & 7)) << 4), v, rbar);
                         }
                     }
                     if (wtid < 64) st_async_f32(partner_addr(recv_ss + wtid), sm_ss[wtid], rbar);
@@ -859,67 +867,78 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                             if (ok) red_add_v4_f32(dst + q * 4, v.x, v.y, v.z, v.w);
                         }
                     } else if (t.epi == kEpiQkv || t.epi == kEpiGate) {
-                        // paired tile (aemk.cuh AeTileOrder): column i < 32 and its partner 32 + i;
-                        // this thread: i in [16 dhalf, 16 dhalf + 16)
+                        // paired tile (aemk.cuh AeTileOrder): feature column i and its partner
+                        // (RoPE pair / gate); NI columns per thread: i in [NI dhalf, NI dhalf + NI)
+                        // of this CTA's features
                         const bool pr = t.pair == 1 || t.pair >= 3;  // add the partner's half-K partial
                         const float rs = pr ? 1.0f / sqrtf((sm_ss[r] + recv_ss[r]) * p.inv_width + p.eps) : sm_rs[r];
-                        // 64-wide paired tile T = tile / 2, sub-tile tile & 1; symmetric 128-wide
-                        // pair: tile T, this CTA's half
-                        const bool sym = t.pair >= 3;
-                        const int T = sym ? int(t.tile) : t.tile >> 1, sub = sym ? t.pair - 3 : t.tile & 1, i0 = dhalf * 16;
-                        const int ca = sym ? sub * 32 : 0, cb = sym ? 64 + sub * 32 : 32;  // TMEM columns
-                        float xa[16], xb[16];
+                        const bool sym128 = t.pair == 3 || t.pair == 4, sym64 = t.pair >= 5;
+                        const int hf = sym128 ? t.pair - 3 : (sym64 ? t.pair - 5 : 0);
+                        auto body = [&](auto ni_c) {
+                            constexpr int NI = decltype(ni_c)::value;
+                            // 64-wide paired tile T = tile / 2, sub-tile tile & 1; symmetric 128-wide
+                            // pair: tile T, sub = this CTA's half
+                            const int T = sym128 ? int(t.tile) : t.tile >> 1, sub = sym128 ? hf : t.tile & 1;
+                            const int i0 = dhalf * NI;
+                            const int ca = sym128 ? hf * 32 : (sym64 ? hf * 16 : 0);         // TMEM feature columns
+                            const int cb = sym128 ? 64 + hf * 32 : (sym64 ? 32 + hf * 16 : 32);  // partners
+                            const int fo = sub * 32 + (sym64 ? hf * 16 : 0) + i0;            // output feature offset
+                            const int rsf = sym64 ? 32 : 64, pch = rsf / 8;                   // receive stride, partner chunk base
+                            float xa[NI], xb[NI];
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            float4 a4, b4;
-                            tmem_ld4(ta + ca + i0 + q * 4, a4);
-                            tmem_ld4(ta + cb + i0 + q * 4, b4);
-                            if (pr) {
-                                const float4 ha = *reinterpret_cast<const float4*>(recv + r * 64 + (((dhalf * 4 + q) ^ (r & 7)) << 2));
-                                const float4 hb = *reinterpret_cast<const float4*>(recv + r * 64 + (((8 + dhalf * 4 + q) ^ (r & 7)) << 2));
-                                a4.x += ha.x; a4.y += ha.y; a4.z += ha.z; a4.w += ha.w;
-                                b4.x += hb.x; b4.y += hb.y; b4.z += hb.z; b4.w += hb.w;
-                            }
-                            xa[4 * q] = a4.x * rs; xa[4 * q + 1] = a4.y * rs; xa[4 * q + 2] = a4.z * rs; xa[4 * q + 3] = a4.w * rs;
-                            xb[4 * q] = b4.x * rs; xb[4 * q + 1] = b4.y * rs; xb[4 * q + 2] = b4.z * rs; xb[4 * q + 3] = b4.w * rs;
-                        }
-                        __nv_bfloat16 *o1, *o2;
-                        if (t.epi == kEpiQkv) {
-                            const int f0 = T * 128;
-                            __nv_bfloat16* orow = p.qkv + (size_t)r * p.n_qkv;
-                            if (f0 < p.rope_cols) {
-                                // pairs (j, j + 128) of one head (proj/src/tensor.cpp:150-178)
-                                const int hd = f0 >> 8, j0 = ((f0 & 255) >> 7) * 64 + sub * 32 + i0;
-                                o1 = orow + hd * 256 + j0;
-                                o2 = o1 + 128;
-                                const float4* csp = reinterpret_cast<const float4*>(p.rope_cs) + ((size_t)(p.rope_pos0 + r) * 128 + j0) / 2;
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) {
-                                    const float4 cs = __ldg(csp + j);
-                                    const float x0 = xa[2 * j], y0 = xb[2 * j], x1 = xa[2 * j + 1], y1 = xb[2 * j + 1];
-                                    xa[2 * j] = x0 * cs.x - y0 * cs.y;
-                                    xb[2 * j] = x0 * cs.y + y0 * cs.x;
-                                    xa[2 * j + 1] = x1 * cs.z - y1 * cs.w;
-                                    xb[2 * j + 1] = x1 * cs.w + y1 * cs.z;
+                            for (int q = 0; q < NI / 4; ++q) {
+                                float4 a4, b4;
+                                tmem_ld4(ta + ca + i0 + q * 4, a4);
+                                tmem_ld4(ta + cb + i0 + q * 4, b4);
+                                if (pr) {
+                                    const float4 ha = *reinterpret_cast<const float4*>(recv + r * rsf + (((dhalf * (NI / 4) + q) ^ (r & 7)) << 2));
+                                    const float4 hb = *reinterpret_cast<const float4*>(recv + r * rsf + (((pch + dhalf * (NI / 4) + q) ^ (r & 7)) << 2));
+                                    a4.x += ha.x; a4.y += ha.y; a4.z += ha.z; a4.w += ha.w;
+                                    b4.x += hb.x; b4.y += hb.y; b4.z += hb.z; b4.w += hb.w;
                                 }
-                            } else {
-                                o1 = orow + f0 + sub * 32 + i0;
-                                o2 = o1 + 64;
+                                xa[4 * q] = a4.x * rs; xa[4 * q + 1] = a4.y * rs; xa[4 * q + 2] = a4.z * rs; xa[4 * q + 3] = a4.w * rs;
+                                xb[4 * q] = b4.x * rs; xb[4 * q + 1] = b4.y * rs; xb[4 * q + 2] = b4.z * rs; xb[4 * q + 3] = b4.w * rs;
                             }
-                        } else {  // gated FFN: up * gelu(gate) -> g column 64 T + 32 sub + i
+                            __nv_bfloat16 *o1, *o2;
+                            if (t.epi == kEpiQkv) {
+                                const int f0 = T * 128;
+                                __nv_bfloat16* orow = p.qkv + (size_t)r * p.n_qkv;
+                                if (f0 < p.rope_cols) {
+                                    // pairs (j, j + 128) of one head (proj/src/tensor.cpp:150-178)
+                                    const int hd = f0 >> 8, j0 = ((f0 & 255) >> 7) * 64 + fo;
+                                    o1 = orow + hd * 256 + j0;
+                                    o2 = o1 + 128;
+                                    const float4* csp = reinterpret_cast<const float4*>(p.rope_cs) + ((size_t)(p.rope_pos0 + r) * 128 + j0) / 2;
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) xa[j] = xa[j] * gelu_fast(xb[j]);
-                            o1 = p.g + (size_t)r * p.mlp + T * 64 + sub * 32 + i0;
-                            o2 = nullptr;
-                        }
+                                    for (int j = 0; j < NI / 2; ++j) {
+                                        const float4 cs = __ldg(csp + j);
+                                        const float x0 = xa[2 * j], y0 = xb[2 * j], x1 = xa[2 * j + 1], y1 = xb[2 * j + 1];
+                                        xa[2 * j] = x0 * cs.x - y0 * cs.y;
+                                        xb[2 * j] = x0 * cs.y + y0 * cs.x;
+                                        xa[2 * j + 1] = x1 * cs.z - y1 * cs.w;
+                                        xb[2 * j + 1] = x1 * cs.w + y1 * cs.z;
+                                    }
+                                } else {
+                                    o1 = orow + f0 + fo;
+                                    o2 = o1 + 64;
+                                }
+                            } else {  // gated FFN: up * gelu(gate) -> g column 64 T + 32 sub + i
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            reinterpret_cast<uint4*>(o1)[h] = make_uint4(pack2(xa[8 * h], xa[8 * h + 1]), pack2(xa[8 * h + 2], xa[8 * h + 3]),
-                                                                        pack2(xa[8 * h + 4], xa[8 * h + 5]), pack2(xa[8 * h + 6], xa[8 * h + 7]));
-                            if (o2)
-                                reinterpret_cast<uint4*>(o2)[h] = make_uint4(pack2(xb[8 * h], xb[8 * h + 1]), pack2(xb[8 * h + 2], xb[8 * h + 3]),
-                                                                            pack2(xb[8 * h + 4], xb[8 * h + 5]), pack2(xb[8 * h + 6], xb[8 * h + 7]));
-                        }
+                                for (int j = 0; j < NI; ++j) xa[j] = xa[j] * gelu_fast(xb[j]);
+                                o1 = p.g + (size_t)r * p.mlp + T * 64 + fo;
+                                o2 = nullptr;
+                            }
+#pragma unroll
+                            for (int h = 0; h < NI / 8; ++h) {
+                                reinterpret_cast<uint4*>(o1)[h] = make_uint4(pack2(xa[8 * h], xa[8 * h + 1]), pack2(xa[8 * h + 2], xa[8 * h + 3]),
+                                                                            pack2(xa[8 * h + 4], xa[8 * h + 5]), pack2(xa[8 * h + 6], xa[8 * h + 7]));
+                                if (o2)
+                                    reinterpret_cast<uint4*>(o2)[h] = make_uint4(pack2(xb[8 * h], xb[8 * h + 1]), pack2(xb[8 * h + 2], xb[8 * h + 3]),
+                                                                                pack2(xb[8 * h + 4], xb[8 * h + 5]), pack2(xb[8 * h + 6], xb[8 * h + 7]));
+                            }
+                        };
+                        if (sym64) body(std::integral_constant<int, 8>{});
+                        else body(std::integral_constant<int, 16>{});
                     } else if (t.epi == kEpiSilu) {
                         // ae.action_proj: silu(a W + T[step]) (the y reset ran during staging)
                         const int c0 = dhalf * 32;
@@ -1240,7 +1259,7 @@ AePlan ae_plan(const AePlanInput& in) {
                 AeTask x = gemm(kXY, epi, wmat, xmat, 0, t, r ? h : 0, r ? kbt - h : h, wbar, wcnt, sbar);
                 x.step = uint16_t(step);
                 x.layer = uint16_t(layer);
-                x.pair = uint16_t(sym ? (r ? 4 : 3) : (r ? 2 : 1));
+                x.pair = uint16_t(sym ? (r ? 4 : 3) : (in.sym_qkv ? (r ? 6 : 5) : (r ? 2 : 1)));
                 if (sym) x.ncol = 128;
                 const int cta = r ? own ^ 1 : own;
                 load[size_t(cta)] += (r ? kbt - h : h) * kWB * (2.0 + wscale);

@@ -71,7 +71,8 @@ struct AeTask {
     uint16_t step, layer;             // flow step, AE layer
     uint16_t phase;                   // global phase index (debug limit)
     uint16_t pair;                    // full-K tile split over K in a 2-CTA cluster: 1 owner / 2 helper
-                                      // (owner finalises), or 3 / 4 symmetric (each finalises half)
+                                      // (owner finalises), or symmetric (each finalises half):
+                                      // 3 / 4 128-wide ae.ffn tiles, 5 / 6 64-wide ae.qkv tiles
 };
 static_assert(sizeof(AeTask) == 32, "AeTask layout");
 
@@ -119,6 +120,7 @@ struct AePlanInput {
     int ao_tasks = 64, proj_tasks = 128, down_tasks = 128;  // split-K task targets per phase
     int proj_ncol = 128, down_ncol = 64, ao_ncol = 64;     // residual-update tile widths (64 or 128)
     bool pair_qkv = true;  // ae.qkv tiles split over K between the two CTAs of a cluster (DSMEM)
+    bool sym_qkv = true;      // ae.qkv pairs exchange symmetrically (each CTA finalises half)
     bool attn_single = true;  // one attention task per (head, key range) instead of (head pair, range)
     bool pair_ffn = true;  // ae.ffn as 128-wide tiles split over K, symmetric exchange (mat_wffn kTilePlain128)
     int mat_wst, mat_wap, mat_wao, mat_whead;
