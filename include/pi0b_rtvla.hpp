@@ -17,6 +17,10 @@
 //     rtvla::Tensor a2 = eng.run(x);                       // one CUDA-graph replay
 //     eng.run_prefix(x); rtvla::Tensor a3 = eng.run_action(x);  // streaming split
 //
+//     // unfused checkpoint layout (rtvla::build_pi0_graph_naive): fused on the host by the
+//     // reference's own passes + weight rules, then run on the GPU
+//     rtvla::Tensor a4 = pi0b::evaluate_naive(gn, wn, xn);
+//
 // Error convention follows the reference (proj/src/evaluate.cpp:98-99,265,352-354): malformed
 // graphs / shapes throw rtvla::ShapeError, non-finite outputs rtvla::NumericError, device errors
 // std::runtime_error.  There is no CPU fallback: without an sm_100 GPU the Engine constructor
@@ -30,6 +34,7 @@
 #include "rtvla/passes.hpp"
 #include "rtvla/tensor.hpp"
 
+#include <algorithm>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -85,22 +90,31 @@ public:
     // Weights from a reference WeightStore (fp64 -> bf16 once, on the device).
     Engine(const rtvla::Graph& g, const rtvla::WeightStore& w, EngineOptions opt = {}) : cfg_(g.config) {
         create(g, opt);
-        for (const rtvla::Node& n : g.nodes) {
+        // isomorphism is positional and ignores node names (a graph fused from the naive one
+        // by the reference's passes keeps the naive names): weights go to the engine under the
+        // name of the node at the same position in build_pi0_graph
+        const rtvla::Graph canon = rtvla::build_pi0_graph(g.config);
+        for (size_t k = 0; k < g.nodes.size(); ++k) {
+            const rtvla::Node& n = g.nodes[k];
+            const std::string& cid = canon.nodes[k].id;
             auto it = w.by_node.find(n.id);
             if (it == w.by_node.end()) continue;
             const rtvla::WeightSet& ws = it->second;
-            for (size_t i = 0; i < ws.w.size(); ++i) {
+            // instances beyond the node's own count (e.g. carried over from an unpruned graph by
+            // rtvla::apply_weight_rules) are never read by the reference either
+            const size_t n_inst = std::min(ws.w.size(), size_t(std::max<int64_t>(0, n.weight_instances())));
+            for (size_t i = 0; i < n_inst; ++i) {
                 const rtvla::Tensor& t = ws.w[i];
                 const bool has_bias = i < ws.bias.size() && !ws.bias[i].empty();
-                check(pi0b_engine_set_weight(h_.get(), n.id.c_str(), int64_t(i), t.data.data(), t.rows, t.cols,
+                check(pi0b_engine_set_weight(h_.get(), cid.c_str(), int64_t(i), t.data.data(), t.rows, t.cols,
                                              has_bias ? ws.bias[i].data() : nullptr,
                                              has_bias ? int64_t(ws.bias[i].size()) : 0),
-                      ("set_weight " + n.id).c_str());
+                      ("set_weight " + cid).c_str());
             }
             if (ws.bias_table.rows > 0)
-                check(pi0b_engine_set_bias_table(h_.get(), n.id.c_str(), ws.bias_table.data.data(), ws.bias_table.rows,
+                check(pi0b_engine_set_bias_table(h_.get(), cid.c_str(), ws.bias_table.data.data(), ws.bias_table.rows,
                                                  ws.bias_table.cols),
-                      ("set_bias_table " + n.id).c_str());
+                      ("set_bias_table " + cid).c_str());
         }
     }
     // Weights generated on the device: bit-identical bf16 rounding of rtvla::gen_weights(g, seed).
@@ -157,6 +171,33 @@ private:
 inline rtvla::Tensor evaluate(const rtvla::Graph& g, const rtvla::WeightStore& w, const rtvla::Inputs& x) {
     Engine e(g, w);
     return e.run(x);
+}
+
+// Unfused graphs: rtvla::build_pi0_graph_naive — one node per framework-level op
+// (separate q/k/v, RMSNorm with gamma, the action time-embedding MLP) — which is what a real pi0
+// checkpoint maps onto.  The reference's own rewrite passes, in its standard order
+// (rtvla::pass_registry, proj/src/passes.cpp), and weight rules (rtvla::apply_weight_rules,
+// proj/src/passes.cpp:692-790: PremultiplyDiag gamma into W, ConcatCols q|k|v and up|gate,
+// ComposeTimeFold of the time MLP into the ae.action_proj bias table) turn the naive graph and
+// its WeightStore into the fused graph and weights once on the host; the engine runs those.
+struct Fused {
+    rtvla::Graph graph;
+    rtvla::WeightStore weights;
+};
+inline Fused fuse(const rtvla::Graph& naive, const rtvla::WeightStore& w) {
+    Fused f{naive, w};
+    for (const auto& [name, fn] : rtvla::pass_registry()) {
+        rtvla::PassResult r = fn(f.graph);
+        f.weights = rtvla::apply_weight_rules(f.graph, r.graph, r.rules, f.weights, f.graph.config.flow_steps);
+        f.graph = std::move(r.graph);
+        (void)name;
+    }
+    return f;
+}
+// rtvla::evaluate on a naive-graph WeightStore (same Inputs: the source nodes are shared).
+inline rtvla::Tensor evaluate_naive(const rtvla::Graph& naive, const rtvla::WeightStore& w, const rtvla::Inputs& x) {
+    const Fused f = fuse(naive, w);
+    return pi0b::evaluate(f.graph, f.weights, x);
 }
 
 }  // namespace pi0b

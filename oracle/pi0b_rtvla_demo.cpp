@@ -4,14 +4,23 @@
 // libpi0b.so), and the result is compared with rtvla::evaluate (the fp64 oracle) on a reduced-width
 // twin with full-scale head geometry (paper_2510_26742_b200/config.py mid_config).
 //   usage: pi0b_rtvla_demo [views] [prompt]      exit 0 when max |gpu - fp64| < 0.05
+//          pi0b_rtvla_demo naive [views] [prompt] : the unfused graph (build_pi0_graph_naive) and its
+//          WeightStore through pi0b::evaluate_naive (host-side fusion by the reference's passes)
+//          vs rtvla::evaluate on the naive graph
 #include "pi0b_rtvla.hpp"
 #include "rtvla/builder.hpp"
 
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 int main(int argc, char** argv) {
+    const bool naive = argc > 1 && std::string(argv[1]) == "naive";
+    if (naive) {
+        --argc;
+        ++argv;
+    }
     rtvla::ModelConfig c;
     c.views = argc > 1 ? std::atoi(argv[1]) : 1;
     c.prompt_tokens = argc > 2 ? std::atoi(argv[2]) : 0;
@@ -21,6 +30,26 @@ int main(int argc, char** argv) {
     c.ve = rtvla::VisionConfig{2, 288, 4, 72, 1076, 588};
     c.llm = rtvla::LlmConfig{3, 512, 2, 256, 1, 1024};
     c.ae = rtvla::ActionConfig{2, 256, 2, 256, 1, 512, 32, 32};
+    if (naive) {
+        const rtvla::Graph gn = rtvla::build_pi0_graph_naive(c);
+        const rtvla::WeightStore wn = rtvla::gen_weights(gn, 1);
+        const rtvla::Inputs xn = rtvla::gen_inputs(gn, 1);
+        const rtvla::Tensor refn = rtvla::evaluate(gn, wn, xn);
+        try {
+            const rtvla::Tensor an = pi0b::evaluate_naive(gn, wn, xn);
+            double d = 0, rms = 0;
+            for (size_t i = 0; i < refn.data.size(); ++i) {
+                d = std::fmax(d, std::fabs(an.data[i] - refn.data[i]));
+                rms += refn.data[i] * refn.data[i];
+            }
+            std::printf("pi0b::evaluate_naive vs rtvla::evaluate(naive graph) max|d| = %.3e (rms %.3f)\n", d,
+                        std::sqrt(rms / refn.data.size()));
+            return d < 0.05 ? 0 : 1;
+        } catch (const std::exception& e) {
+            std::printf("pi0b error: %s\n", e.what());
+            return 2;
+        }
+    }
     const rtvla::Graph g = rtvla::build_pi0_graph(c);
     const rtvla::WeightStore w = rtvla::gen_weights(g, 1);
     const rtvla::Inputs x = rtvla::gen_inputs(g, 1);

@@ -211,3 +211,16 @@ def test_rtvla_cpp_dropin(views, prompt):
     r = subprocess.run([DEMO, str(views), str(prompt)], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("views,prompt", [(1, 0), (3, 32)])
+def test_rtvla_cpp_naive_graph(views, prompt):
+    """SURVEY 8(f) f1: an unfused graph (rtvla::build_pi0_graph_naive: separate q/k/v, RMSNorm gamma,
+    time MLP) and its WeightStore through pi0b::evaluate_naive -- fused on the host by the
+    reference's own passes and weight rules -- vs rtvla::evaluate on the naive graph."""
+    import subprocess
+    if not os.path.exists(DEMO):
+        pytest.skip("oracle/_ref/pi0b_rtvla_demo not built (needs /root/reference at build time)")
+    r = subprocess.run([DEMO, "naive", str(views), str(prompt)], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
