@@ -38,6 +38,7 @@ def build(quiet: bool = True) -> None:
         # the reference's stream simulator + driver (scripts/streamsim_b200.py)
         targets.append("streamsim")
         targets.append("naive")
+        targets.append("analyze")
         # the C++ drop-in demo (include/pi0b_rtvla.hpp over libpi0b.so, reference types)
         if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_2510_26742_b200", "libpi0b.so")):
             targets.append("demo")
