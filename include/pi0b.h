@@ -77,6 +77,17 @@ int pi0b_engine_set_bias_table(pi0b_engine* e, const char* node_id, const double
 int pi0b_engine_run(pi0b_engine* e, const double* patches, const double* state, const double* noise,
                     const double* prompt, double* actions_out);
 
+/* run() from camera frames instead of patches: images [views][height][width*3]
+ * fp64, channels interleaved; resized on the device to the patch grid (half-pixel-centre bilinear,
+ * bit-identical to rtvla::bilinear_resize, proj/src/tensor.cpp:180-212) and cut into the
+ * ve.embed patches (row view*g*g + (y/P)*g + x/P, feature ((y%P)*P + x%P)*3 + c). */
+int pi0b_engine_run_images(pi0b_engine* e, const double* images, int height, int width, const double* state,
+                           const double* noise, const double* prompt, double* actions_out);
+/* The same resize + img2col as a device op: images (device) -> patches (device) [views*(side/patch)^2,
+ * patch*patch*channels]. */
+int pi0b_image_patches(const double* images, int views, int height, int width, int channels, int side,
+                       int patch, double* patches, void* stream);
+
 /* Streaming split of run(): the prefix (VE + LLM, fills the KV cache) and the action
  * expert (all flow steps against the cached prefix KV). */
 int pi0b_engine_run_prefix(pi0b_engine* e, const double* patches, const double* prompt);

@@ -89,6 +89,7 @@ def ref_lib():
         lib.ref_matmul.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, _dp, ctypes.c_int64, _dp]
         lib.ref_rms_scales.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, _dp]
         lib.ref_softmax_rows.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, _dp]
+        lib.ref_bilinear_resize.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]
         lib.ref_rope.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _dp]
         lib.ref_rope_table.argtypes = [ctypes.c_int, ctypes.c_int, _dp, _dp]
         lib.ref_time_embedding.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]

@@ -223,6 +223,14 @@ int ref_rms_scales(const double* x, int64_t rows, int64_t cols, double eps, doub
         std::memcpy(out, s.data.data(), size_t(rows) * 8);
     });
 }
+int ref_bilinear_resize(const double* img, int64_t h, int64_t w, int channels, int out_h, int out_w, double* out) {
+    return guarded([&] {
+        rtvla::Tensor t(h, w * channels);
+        std::memcpy(t.data.data(), img, size_t(h * w * channels) * 8);
+        const rtvla::Tensor r = rtvla::bilinear_resize(t, channels, out_h, out_w);
+        std::memcpy(out, r.data.data(), r.data.size() * 8);
+    });
+}
 int ref_softmax_rows(const double* x, int64_t rows, int64_t cols, double* out) {
     return guarded([&] {
         rtvla::Tensor t(rows, cols);

@@ -64,6 +64,8 @@ cudaError_t launch_rows_to_f32(const double* src, int rows, int cols, float* dst
                                __nv_bfloat16* dstb, long long lddb, float* stats, cudaStream_t st);
 cudaError_t launch_f64_to_bf16_rows(const double* src, int rows, int cols, __nv_bfloat16* dst,
                                     long long ldd, cudaStream_t st);
+cudaError_t launch_image_patches(const double* img, int views, int H, int W, int C, int side, int P, double* patches,
+                                 cudaStream_t st);
 cudaError_t launch_f32_to_f64(const float* src, long long lds, int rows, int cols, double* dst,
                               cudaStream_t st);
 
@@ -269,6 +271,9 @@ public:
     void set_bias_table(const std::string& id, const double* t, long long rows, long long m);
     void upload_inputs(const double* patches, const double* state, const double* noise,
                        const double* prompt, int which);
+    // camera frames [views][height][width*3] (fp64) -> resize + img2col on the device into the
+    // patch input (kernels_misc.cu image_patches_kernel), instead of host patches
+    void upload_images(const double* images, int height, int width);
     void launch(int part, cudaStream_t st);
     void fetch_actions(double* out);
     void read_checkpoint(const std::string& id, long long inst, float* out, long long rows, long long cols);
@@ -326,6 +331,8 @@ private:
     double *d_patches_ = nullptr, *d_state_ = nullptr, *d_noise_ = nullptr, *d_prompt_ = nullptr,
            *d_out_ = nullptr;
     double *h_in_ = nullptr, *h_out_ = nullptr;
+    double *h_img_ = nullptr, *d_img_ = nullptr;  // image front-end staging (grown on demand)
+    size_t n_img_ = 0;
     size_t n_patches_ = 0, n_state_ = 0, n_noise_ = 0, n_prompt_ = 0, n_out_ = 0;
 
     // activations
@@ -399,6 +406,8 @@ Engine::~Engine() {
     for (auto& kv : ck_) cudaFree(kv.second.dev);
     for (void* p : allocs_) cudaFree(p);
     if (h_in_) cudaFreeHost(h_in_);
+    if (h_img_) cudaFreeHost(h_img_);
+    if (d_img_) cudaFree(d_img_);
     if (h_out_) cudaFreeHost(h_out_);
     if (stream_) cudaStreamDestroy(stream_);
 }
@@ -1362,7 +1371,7 @@ void Engine::set_bias_table(const std::string& id, const double* t, long long ro
 
 void Engine::upload_inputs(const double* patches, const double* state, const double* noise,
                            const double* prompt, int which) {
-    // which: 0 = all, 1 = prefix inputs, 2 = action inputs. Copies go through pinned
+    // which: 0 = all, 1 = prefix inputs, 2 = action inputs, 3 = all but the patches. Copies go through pinned
     // staging so the H2D transfers are asynchronous DMA on the engine stream.
     double* h = h_in_;
     auto stage = [&](const double* src, size_t n, double* dev) {
@@ -1376,10 +1385,37 @@ void Engine::upload_inputs(const double* patches, const double* state, const dou
         stage(patches, n_patches_, d_patches_);
         if (P_ > 0) stage(prompt, n_prompt_, d_prompt_);
     }
+    if (which == 3) {  // everything but the patches (image front-end)
+        if (P_ > 0) stage(prompt, n_prompt_, d_prompt_);
+        stage(state, n_state_, d_state_);
+        stage(noise, n_noise_, d_noise_);
+    }
     if (which == 0 || which == 2) {
         stage(state, n_state_, d_state_);
         stage(noise, n_noise_, d_noise_);
     }
+}
+
+void Engine::upload_images(const double* images, int height, int width) {
+    const auto& c = c_;
+    const int C = 3;
+    const int P = int(std::lround(std::sqrt(double(c.ve_patch_in / C))));
+    const int g = int(std::lround(std::sqrt(double(c.tokens_per_view))));
+    if (P * P * C != c.ve_patch_in || g * g != c.tokens_per_view)
+        throw EngineError(PI0B_E_UNSUPPORTED, "image front-end: patch_in must be P*P*3 and tokens_per_view g*g");
+    if (!images || height < 2 || width < 2) throw EngineError(PI0B_E_INVALID, "image front-end: images of at least 2x2");
+    const size_t n = size_t(c.views) * height * width * C;
+    if (n > n_img_) {
+        if (h_img_) cudaFreeHost(h_img_);
+        if (d_img_) cudaFree(d_img_);
+        PI0B_CUDA(cudaMallocHost(&h_img_, n * 8));
+        PI0B_CUDA(cudaMalloc(&d_img_, n * 8));
+        n_img_ = n;
+    }
+    PI0B_CUDA(cudaStreamSynchronize(stream_));  // the staging buffer may still feed the last copy
+    std::memcpy(h_img_, images, n * 8);
+    PI0B_CUDA(cudaMemcpyAsync(d_img_, h_img_, n * 8, cudaMemcpyHostToDevice, stream_));
+    PI0B_CUDA(launch_image_patches(d_img_, c.views, height, width, C, g * P, P, d_patches_, stream_));
 }
 
 void Engine::run_ops(int part, cudaStream_t st) {
@@ -1641,6 +1677,22 @@ int pi0b_engine_run(pi0b_engine* e, const double* patches, const double* state, 
         e->impl->launch(0, e->impl->stream());
         e->impl->fetch_actions(out);
     })
+}
+
+int pi0b_engine_run_images(pi0b_engine* e, const double* images, int height, int width, const double* state,
+                           const double* noise, const double* prompt, double* out) {
+    PI0B_TRY({
+        e->impl->upload_images(images, height, width);
+        e->impl->upload_inputs(nullptr, state, noise, prompt, 3);
+        e->impl->launch(0, e->impl->stream());
+        e->impl->fetch_actions(out);
+    })
+}
+
+int pi0b_image_patches(const double* images, int views, int height, int width, int channels, int side, int patch,
+                       double* patches, void* stream) {
+    return int(pi0b::launch_image_patches(images, views, height, width, channels, side, patch, patches,
+                                          static_cast<cudaStream_t>(stream)));
 }
 
 int pi0b_engine_run_prefix(pi0b_engine* e, const double* patches, const double* prompt) {

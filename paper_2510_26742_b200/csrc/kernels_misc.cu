@@ -139,6 +139,40 @@ __global__ void tile_weight_kernel(const __nv_bfloat16* src, int rows, int k, lo
     }
 }
 
+
+// Image front-end: camera frames [views][H][W*C] (fp64, channels interleaved)
+// -> half-pixel-centre bilinear resize to side x side (the reference's rtvla::bilinear_resize,
+// proj/src/tensor.cpp:180-212, same fp64 operation order with FMA contraction disabled, so the
+// resized values are bit-identical) -> img2col into the ve.embed input patches [views*g*g][P*P*C]
+// (the reference draws `patches` at random and leaves the flattening unspecified; this engine's
+// order: patch row t = view*g*g + (y / P)*g + (x / P), feature ((y % P)*P + (x % P))*C + c).
+__global__ void image_patches_kernel(const double* img, int views, int H, int W, int C, int side, int P,
+                                     double* patches) {
+    const long long n = (long long)views * side * side * C;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int c = int(i % C);
+    const int ox = int((i / C) % side);
+    const int oy = int((i / ((long long)C * side)) % side);
+    const int v = int(i / ((long long)C * side * side));
+    auto clampd = [](double x, double lo, double hi) { return x < lo ? lo : (x > hi ? hi : x); };
+    const double sy = clampd(__dsub_rn(__ddiv_rn(__dmul_rn(oy + 0.5, double(H)), double(side)), 0.5), 0.0, double(H - 1));
+    const double sx = clampd(__dsub_rn(__ddiv_rn(__dmul_rn(ox + 0.5, double(W)), double(side)), 0.5), 0.0, double(W - 1));
+    const int y0 = int(sy), x0 = int(sx);
+    const int y1 = min(y0 + 1, H - 1), x1 = min(x0 + 1, W - 1);
+    const double ty = __dsub_rn(sy, double(y0)), tx = __dsub_rn(sx, double(x0));
+    const double* im = img + (long long)v * H * W * C;
+    const double v00 = im[((long long)y0 * W + x0) * C + c], v01 = im[((long long)y0 * W + x1) * C + c];
+    const double v10 = im[((long long)y1 * W + x0) * C + c], v11 = im[((long long)y1 * W + x1) * C + c];
+    const double top = __dadd_rn(v00, __dmul_rn(__dsub_rn(v01, v00), tx));
+    const double bot = __dadd_rn(v10, __dmul_rn(__dsub_rn(v11, v10), tx));
+    const double out = __dadd_rn(top, __dmul_rn(__dsub_rn(bot, top), ty));
+    const int g = side / P;
+    const long long t = (long long)v * g * g + (oy / P) * g + (ox / P);
+    const int f = ((oy % P) * P + (ox % P)) * C + c;
+    patches[t * (P * P * C) + f] = out;
+}
+
 // --------------------------------------------------------------------- launchers
 
 cudaError_t launch_tile_weight(const __nv_bfloat16* src, int rows, int k, long long ldk, __nv_bfloat16* dst,
@@ -183,6 +217,14 @@ cudaError_t launch_f64_to_bf16_rows(const double* src, int rows, int cols, __nv_
 cudaError_t launch_f32_to_f64(const float* src, long long lds, int rows, int cols, double* dst,
                               cudaStream_t st) {
     f32_to_f64_kernel<<<(rows * cols + 255) / 256, 256, 0, st>>>(src, lds, rows, cols, dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_image_patches(const double* img, int views, int H, int W, int C, int side, int P, double* patches,
+                                 cudaStream_t st) {
+    if (views < 1 || H < 2 || W < 2 || C < 1 || side < P || side % P) return cudaErrorInvalidValue;
+    const long long n = (long long)views * side * side * C;
+    image_patches_kernel<<<int((n + 255) / 256), 256, 0, st>>>(img, views, H, W, C, side, P, patches);
     return cudaGetLastError();
 }
 

@@ -106,6 +106,9 @@ def lib():
         L.pi0b_engine_set_bias_table.argtypes = [vp, ctypes.c_char_p, _dp, ctypes.c_int64, ctypes.c_int64]
         L.pi0b_engine_run.argtypes = [vp, _dp, _dp, _dp, _dp, _dp]
         L.pi0b_engine_run_prefix.argtypes = [vp, _dp, _dp]
+        L.pi0b_engine_run_images.argtypes = [vp, _dp, ctypes.c_int, ctypes.c_int, _dp, _dp, _dp, _dp]
+        L.pi0b_image_patches.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, vp, vp]
         L.pi0b_engine_run_action.argtypes = [vp, _dp, _dp, _dp]
         L.pi0b_engine_replay.argtypes = [vp, ctypes.c_int, vp]
         L.pi0b_engine_sync.argtypes = [vp]
@@ -136,6 +139,7 @@ EXPORTED_SYMBOLS = [
     "pi0b_engine_read_checkpoint", "pi0b_engine_time_node", "pi0b_engine_describe", "pi0b_engine_ae_trace",
     "pi0b_last_error", "pi0b_gemm", "pi0b_gemm_skinny", "pi0b_attention",
     "pi0b_attention_ws_floats", "pi0b_random_f64", "pi0b_random_packed_bf16", "pi0b_seed_hash",
+    "pi0b_engine_run_images", "pi0b_image_patches",
 ]
 
 
@@ -227,6 +231,18 @@ class Engine:
         y = np.zeros((self.cfg.chunk_len, self.cfg.ae_action_dim), dtype=np.float64)
         _raise(lib().pi0b_engine_run(self._h, self._p(x["patches"]), self._p(x["state"]), self._p(x["noise"]),
                                      self._p(x.get("prompt")), self._p(y)), "run")
+        return y
+
+    def run_images(self, images, state, noise, prompt=None) -> np.ndarray:
+        """run() from camera frames [views, height, width, 3] (any size >= 2x2): resize + img2col on
+        the device (include/pi0b.h pi0b_engine_run_images)."""
+        img = np.ascontiguousarray(images, dtype=np.float64)
+        if img.ndim != 4 or img.shape[0] != self.cfg.views or img.shape[3] != 3:
+            raise ShapeError(f"images must be [views={self.cfg.views}, h, w, 3], got {img.shape}")
+        x = self._inputs(state=state, noise=noise, prompt=prompt)
+        y = np.zeros((self.cfg.chunk_len, self.cfg.ae_action_dim), dtype=np.float64)
+        _raise(lib().pi0b_engine_run_images(self._h, self._p(img), img.shape[1], img.shape[2], self._p(x["state"]),
+                                            self._p(x["noise"]), self._p(x.get("prompt")), self._p(y)), "run_images")
         return y
 
     def run_prefix(self, patches, prompt=None) -> None:
