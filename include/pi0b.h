@@ -94,6 +94,39 @@ int pi0b_engine_run_prefix(pi0b_engine* e, const double* patches, const double* 
 int pi0b_engine_run_action(pi0b_engine* e, const double* state, const double* noise,
                            double* actions_out);
 
+/* Full-streaming runtime (the real execution of what the reference only simulates,
+ * proj/include/rtvla/streamsim.hpp:54-131): a camera stream at frame_rate feeds the prefix (VE + LLM)
+ * into one of two KV buffers (two engines, double-buffered KV); an action-expert stream runs
+ * control ticks at up to ae_rate on the KV chosen by kv_policy with the freshest sensor sample;
+ * each tick writes its chunk into a trajectory buffer of trajectory_rate slots whose commit cursor
+ * advances with wall time.  Runs `seconds` of synthetic frames/sensors (random patches / state /
+ * noise) on one GPU and reports the reference's loop metrics (rtvla::measure_loops,
+ * streamsim.hpp:166-205) measured on the real execution. */
+typedef struct pi0b_stream_options {
+    double frame_rate;       /* camera frames per second (30)                                  */
+    int camera_latency;      /* frames between capture and availability (2)                     */
+    double ae_rate;          /* target action-expert ticks per second (480)                     */
+    double trajectory_rate;  /* trajectory slots per second (480)                               */
+    int kv_policy;           /* 0 most_recent, 1 frame_sticky (rtvla::KvPolicy)                 */
+    int device;
+} pi0b_stream_options;
+
+typedef struct pi0b_stream_report {
+    double seconds;             /* wall time of the run                                         */
+    int64_t frames, ticks;      /* prefixes / action-expert ticks completed                     */
+    double vlm_per_s, ae_per_s;
+    double quick_mean_ms, quick_best_ms, quick_worst_ms;  /* sensor sample -> first commit of its window */
+    int64_t quick_count;
+    double slow_mean_ms, slow_best_ms, slow_worst_ms;     /* frame capture -> first commit using its KV  */
+    int64_t slow_count;
+    double prefix_p50_ms, tick_p50_ms, tick_p99_ms;       /* issue -> completion, per operation           */
+    int64_t committed_slots, overwritten_slots;           /* trajectory buffer                           */
+} pi0b_stream_report;
+
+/* cfg.flow_steps is the number of flow steps per tick (1 = one "AE pass" of the paper). */
+int pi0b_stream_run(const pi0b_model_config* cfg, uint64_t weight_seed, const pi0b_stream_options* opt,
+                    double seconds, pi0b_stream_report* report);
+
 /* Device-resident replay of the last inputs (no host copies): 0 = full, 1 = prefix,
  * 2 = action.  `stream` is a cudaStream_t (NULL = the engine's stream).  Asynchronous. */
 int pi0b_engine_replay(pi0b_engine* e, int part, void* stream);

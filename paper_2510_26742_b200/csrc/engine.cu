@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <random>
+#include <chrono>
 #include <cctype>
 #include <cmath>
 #include <cstdio>
@@ -276,6 +278,11 @@ public:
     void upload_images(const double* images, int height, int width);
     void launch(int part, cudaStream_t st);
     void fetch_actions(double* out);
+    // asynchronous pieces for the streaming runtime (one outstanding operation per engine)
+    void prefix_async(const double* patches, const double* prompt);
+    void tick_async(const double* state, const double* noise);
+    bool idle();                      // the last async operation completed
+    const double* tick_result();      // host copy of the last tick's actions (after idle())
     void read_checkpoint(const std::string& id, long long inst, float* out, long long rows, long long cols);
     int kernel_count(int part) const;
     void prepare() {
@@ -331,6 +338,7 @@ private:
     double *d_patches_ = nullptr, *d_state_ = nullptr, *d_noise_ = nullptr, *d_prompt_ = nullptr,
            *d_out_ = nullptr;
     double *h_in_ = nullptr, *h_out_ = nullptr;
+    cudaEvent_t done_ev_ = nullptr;               // streaming runtime: last async operation
     double *h_img_ = nullptr, *d_img_ = nullptr;  // image front-end staging (grown on demand)
     size_t n_img_ = 0;
     size_t n_patches_ = 0, n_state_ = 0, n_noise_ = 0, n_prompt_ = 0, n_out_ = 0;
@@ -407,6 +415,7 @@ Engine::~Engine() {
     for (void* p : allocs_) cudaFree(p);
     if (h_in_) cudaFreeHost(h_in_);
     if (h_img_) cudaFreeHost(h_img_);
+    if (done_ev_) cudaEventDestroy(done_ev_);
     if (d_img_) cudaFree(d_img_);
     if (h_out_) cudaFreeHost(h_out_);
     if (stream_) cudaStreamDestroy(stream_);
@@ -1500,6 +1509,32 @@ void Engine::launch(int part, cudaStream_t st) {
     }
 }
 
+void Engine::prefix_async(const double* patches, const double* prompt) {
+    if (!done_ev_) PI0B_CUDA(cudaEventCreateWithFlags(&done_ev_, cudaEventDisableTiming));
+    upload_inputs(patches, nullptr, nullptr, prompt, 1);
+    launch(1, stream_);
+    PI0B_CUDA(cudaEventRecord(done_ev_, stream_));
+}
+void Engine::tick_async(const double* state, const double* noise) {
+    if (!done_ev_) PI0B_CUDA(cudaEventCreateWithFlags(&done_ev_, cudaEventDisableTiming));
+    upload_inputs(nullptr, state, noise, nullptr, 2);
+    launch(2, stream_);
+    PI0B_CUDA(cudaMemcpyAsync(h_out_, d_out_, n_out_ * 8, cudaMemcpyDeviceToHost, stream_));
+    PI0B_CUDA(cudaEventRecord(done_ev_, stream_));
+}
+bool Engine::idle() {
+    if (!done_ev_) return true;
+    const cudaError_t e = cudaEventQuery(done_ev_);
+    if (e == cudaErrorNotReady) return false;
+    PI0B_CUDA(e);
+    return true;
+}
+const double* Engine::tick_result() {
+    for (size_t i = 0; i < n_out_; ++i)
+        if (!std::isfinite(h_out_[i])) throw EngineError(PI0B_E_NUMERIC, "non-finite action output");
+    return h_out_;
+}
+
 void Engine::fetch_actions(double* out) {
     PI0B_CUDA(cudaMemcpyAsync(h_out_, d_out_, n_out_ * 8, cudaMemcpyDeviceToHost, stream_));
     PI0B_CUDA(cudaStreamSynchronize(stream_));
@@ -1620,6 +1655,172 @@ void Engine::read_checkpoint(const std::string& id, long long inst, float* out, 
 using pi0b::Engine;
 using pi0b::EngineError;
 
+// ---------------------------------------------------------------------- streaming runtime
+// the full-streaming execution the reference simulates
+// (proj/src/streamsim.cpp:280-602): camera frames -> prefix into one of two KV buffers (two engines,
+// double-buffered KV) on one stream, action-expert ticks on the KV chosen by the policy on the other
+// engine's stream, a fixed-rate trajectory buffer whose commit cursor follows wall time, and the
+// reference's loop metrics (measure_loops, streamsim.cpp:520-602) on what actually ran.
+namespace pi0b {
+namespace {
+double pctl(std::vector<double> v, double q) {
+    if (v.empty()) return 0.0;
+    std::sort(v.begin(), v.end());
+    return v[std::min(v.size() - 1, size_t(q * double(v.size())))];
+}
+}  // namespace
+
+void stream_run(const pi0b_model_config& cfg, uint64_t seed, const pi0b_stream_options& o, double seconds,
+                pi0b_stream_report& rep) {
+    using clk = std::chrono::steady_clock;
+    if (o.frame_rate <= 0 || o.ae_rate <= 0 || o.trajectory_rate <= 0 || o.camera_latency < 0 || seconds <= 0)
+        throw EngineError(PI0B_E_INVALID, "stream options");
+    pi0b_engine_options eo{o.device, 1, 0};
+    std::unique_ptr<Engine> eng[2] = {std::make_unique<Engine>(cfg, eo), std::make_unique<Engine>(cfg, eo)};
+    const int P = cfg.prompt_tokens, C = cfg.chunk_len, A = cfg.ae_action_dim;
+    std::mt19937_64 rng(seed * 7919u + 1);
+    std::uniform_real_distribution<double> U(-1.0, 1.0);
+    auto rnd = [&](size_t n) {
+        std::vector<double> v(n);
+        for (double& x : v) x = U(rng);
+        return v;
+    };
+    const std::vector<double> patches = rnd(size_t(cfg.views) * cfg.tokens_per_view * cfg.ve_patch_in);
+    const std::vector<double> prompt = rnd(size_t(std::max(P, 1)) * cfg.llm_width);
+    std::vector<double> state = rnd(size_t(cfg.ae_state_dim)), noise = rnd(size_t(C) * A);
+    for (auto& e : eng) {  // weights + CUDA-graph capture of both parts, outside the measured run
+        e->gen_weights(seed);
+        e->prefix_async(patches.data(), P ? prompt.data() : nullptr);
+        e->tick_async(state.data(), noise.data());
+        PI0B_CUDA(cudaStreamSynchronize(e->stream()));
+    }
+    const double period = 1.0 / o.frame_rate, tick_dt = 1.0 / o.ae_rate, slot_dt = 1.0 / o.trajectory_rate;
+    struct Op {
+        int kind = 0;  // 0 idle, 1 prefix, 2 tick
+        int64_t id = -1, kv = -1;
+        double t_issue = 0, t_sensor = 0;
+    } op[2];
+    int64_t kv_frame[2] = {-1, -1};  // completed frame whose KV each engine holds
+    int64_t next_frame = 0, sticky = -1;
+    double next_tick = 0.0;
+    struct Slot {
+        int64_t writer = -1, kv = -1;
+        double sensor = 0;
+    };
+    std::map<int64_t, Slot> traj;
+    std::vector<double> prefix_ms, tick_ms;
+    int64_t frames = 0, ticks = 0, overwritten = 0, tick_id = 0;
+    const auto t0 = clk::now();
+    auto now = [&]() { return std::chrono::duration<double>(clk::now() - t0).count(); };
+    auto newest = [&]() {  // engine holding the newest completed KV that is not being rewritten
+        int best = -1;
+        for (int e = 0; e < 2; ++e)
+            if (kv_frame[e] >= 0 && op[e].kind != 1 && (best < 0 || kv_frame[e] > kv_frame[best])) best = e;
+        return best;
+    };
+    bool stop = false;
+    while (true) {
+        const double t = now();
+        if (t >= seconds) stop = true;
+        // completions
+        for (int e = 0; e < 2; ++e) {
+            if (op[e].kind == 0 || !eng[e]->idle()) continue;
+            const double tc = now();
+            if (op[e].kind == 1) {
+                kv_frame[e] = op[e].id;
+                ++frames;
+                prefix_ms.push_back((tc - op[e].t_issue) * 1e3);
+            } else {
+                const double* act = eng[e]->tick_result();
+                (void)act;  // the chunk's values are what the robot would execute; timing is the metric
+                ++ticks;
+                tick_ms.push_back((tc - op[e].t_issue) * 1e3);
+                // write window: the chunk into the first C uncommitted slots (slot time > now)
+                const int64_t first = int64_t(std::floor(tc / slot_dt)) + 1;
+                for (int64_t k = first; k < first + C; ++k) {
+                    auto it = traj.find(k);
+                    if (it != traj.end()) ++overwritten;
+                    traj[k] = Slot{op[e].id, op[e].kv, op[e].t_sensor};
+                }
+            }
+            op[e] = Op{};
+        }
+        if (stop) {
+            if (op[0].kind == 0 && op[1].kind == 0) break;
+            continue;
+        }
+        // camera: frame f captured at f * period, available camera_latency frames later, prefix on
+        // engine f % 2 (the other engine keeps serving the previous KV)
+        if (double(next_frame + o.camera_latency) * period <= t) {
+            const int e = int(next_frame % 2);
+            if (op[e].kind == 0) {
+                if (o.kv_policy == 1) sticky = newest() >= 0 ? kv_frame[newest()] : -1;
+                eng[e]->prefix_async(patches.data(), P ? prompt.data() : nullptr);
+                op[e] = Op{1, next_frame, -1, now(), 0};
+                kv_frame[e] = -1;
+                ++next_frame;
+            }
+        }
+        // control tick: the freshest sensor sample (2 kHz grid) and fresh noise on the chosen KV
+        if (t >= next_tick) {
+            int e = newest();
+            if (o.kv_policy == 1 && sticky >= 0) {  // frame_sticky: keep the KV chosen at the last VLM start
+                e = -1;
+                for (int k = 0; k < 2; ++k)
+                    if (kv_frame[k] == sticky && op[k].kind != 1) e = k;
+                if (e < 0) e = newest();
+            }
+            if (e >= 0 && op[e].kind == 0) {
+                for (double& x : state) x = U(rng);
+                for (double& x : noise) x = U(rng);
+                const double ts = std::floor(t * 2000.0) / 2000.0;
+                eng[e]->tick_async(state.data(), noise.data());
+                op[e] = Op{2, tick_id++, kv_frame[e], now(), ts};
+                next_tick = std::max(next_tick + tick_dt, t);  // no catch-up bursts
+            }
+        }
+    }
+    const double t_end = now();
+    // loop metrics on the committed slots (slot time <= end of run)
+    std::map<int64_t, double> quick;  // tick -> first committed slot time - sensor time
+    std::map<int64_t, double> slow;   // frame -> first committed slot time using its KV - capture time
+    int64_t committed = 0;
+    for (const auto& [k, sl] : traj) {
+        const double ts = double(k) * slot_dt;
+        if (ts > t_end) break;
+        ++committed;
+        if (!quick.count(sl.writer)) quick[sl.writer] = ts - sl.sensor;
+        if (sl.kv >= 1 && !slow.count(sl.kv)) slow[sl.kv] = ts - double(sl.kv) * period;  // frame 0 = cold start
+    }
+    auto stats = [](const std::map<int64_t, double>& m, double& mean, double& best, double& worst, int64_t& n) {
+        n = int64_t(m.size());
+        mean = 0, best = 1e30, worst = 0;
+        for (const auto& kv : m) {
+            mean += kv.second;
+            best = std::min(best, kv.second);
+            worst = std::max(worst, kv.second);
+        }
+        mean = n ? mean / double(n) * 1e3 : 0.0;
+        best = n ? best * 1e3 : 0.0;
+        worst *= 1e3;
+    };
+    rep = pi0b_stream_report{};
+    rep.seconds = t_end;
+    rep.frames = frames;
+    rep.ticks = ticks;
+    rep.vlm_per_s = double(frames) / t_end;
+    rep.ae_per_s = double(ticks) / t_end;
+    stats(quick, rep.quick_mean_ms, rep.quick_best_ms, rep.quick_worst_ms, rep.quick_count);
+    stats(slow, rep.slow_mean_ms, rep.slow_best_ms, rep.slow_worst_ms, rep.slow_count);
+    rep.prefix_p50_ms = pctl(prefix_ms, 0.5);
+    rep.tick_p50_ms = pctl(tick_ms, 0.5);
+    rep.tick_p99_ms = pctl(tick_ms, 0.99);
+    rep.committed_slots = committed;
+    rep.overwritten_slots = overwritten;
+}
+
+}  // namespace pi0b
+
 struct pi0b_engine {
     std::unique_ptr<Engine> impl;
 };
@@ -1693,6 +1894,12 @@ int pi0b_image_patches(const double* images, int views, int height, int width, i
                        double* patches, void* stream) {
     return int(pi0b::launch_image_patches(images, views, height, width, channels, side, patch, patches,
                                           static_cast<cudaStream_t>(stream)));
+}
+
+int pi0b_stream_run(const pi0b_model_config* cfg, uint64_t seed, const pi0b_stream_options* opt, double seconds,
+                    pi0b_stream_report* report) {
+    if (!cfg || !opt || !report) return pi0b::fail(EngineError(PI0B_E_INVALID, "null argument"));
+    PI0B_TRY(pi0b::stream_run(*cfg, seed, *opt, seconds, *report))
 }
 
 int pi0b_engine_run_prefix(pi0b_engine* e, const double* patches, const double* prompt) {

@@ -106,6 +106,8 @@ def lib():
         L.pi0b_engine_set_bias_table.argtypes = [vp, ctypes.c_char_p, _dp, ctypes.c_int64, ctypes.c_int64]
         L.pi0b_engine_run.argtypes = [vp, _dp, _dp, _dp, _dp, _dp]
         L.pi0b_engine_run_prefix.argtypes = [vp, _dp, _dp]
+        L.pi0b_stream_run.argtypes = [cfgp, ctypes.c_uint64, ctypes.POINTER(StreamOptions), ctypes.c_double,
+                                       ctypes.POINTER(StreamReport)]
         L.pi0b_engine_run_images.argtypes = [vp, _dp, ctypes.c_int, ctypes.c_int, _dp, _dp, _dp, _dp]
         L.pi0b_image_patches.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, vp, vp]
@@ -132,6 +134,37 @@ def lib():
     return _lib
 
 
+class StreamOptions(ctypes.Structure):
+    """include/pi0b.h pi0b_stream_options"""
+    _fields_ = [("frame_rate", ctypes.c_double), ("camera_latency", ctypes.c_int), ("ae_rate", ctypes.c_double),
+                ("trajectory_rate", ctypes.c_double), ("kv_policy", ctypes.c_int), ("device", ctypes.c_int)]
+
+
+class StreamReport(ctypes.Structure):
+    """include/pi0b.h pi0b_stream_report"""
+    _fields_ = [("seconds", ctypes.c_double), ("frames", ctypes.c_int64), ("ticks", ctypes.c_int64),
+                ("vlm_per_s", ctypes.c_double), ("ae_per_s", ctypes.c_double),
+                ("quick_mean_ms", ctypes.c_double), ("quick_best_ms", ctypes.c_double),
+                ("quick_worst_ms", ctypes.c_double), ("quick_count", ctypes.c_int64),
+                ("slow_mean_ms", ctypes.c_double), ("slow_best_ms", ctypes.c_double),
+                ("slow_worst_ms", ctypes.c_double), ("slow_count", ctypes.c_int64),
+                ("prefix_p50_ms", ctypes.c_double), ("tick_p50_ms", ctypes.c_double), ("tick_p99_ms", ctypes.c_double),
+                ("committed_slots", ctypes.c_int64), ("overwritten_slots", ctypes.c_int64)]
+
+
+def stream_run(cfg, seconds: float, *, weight_seed: int = 1, frame_rate: float = 30.0, camera_latency: int = 2,
+               ae_rate: float = 480.0, trajectory_rate: float = 480.0, kv_policy: str = "most_recent",
+               device: int = 0) -> dict:
+    """The full-streaming runtime (include/pi0b.h pi0b_stream_run): `seconds` of camera frames and
+    control ticks on one GPU, two engines (double-buffered KV).  cfg.flow_steps = flow steps per tick."""
+    o = StreamOptions(frame_rate, camera_latency, ae_rate, trajectory_rate,
+                      {"most_recent": 0, "frame_sticky": 1}[kv_policy], device)
+    r = StreamReport()
+    _raise(lib().pi0b_stream_run(ctypes.byref(cfg), weight_seed, ctypes.byref(o), seconds, ctypes.byref(r)),
+           "stream_run")
+    return {k: getattr(r, k) for k, _ in StreamReport._fields_}
+
+
 EXPORTED_SYMBOLS = [
     "pi0b_default_config", "pi0b_engine_create", "pi0b_engine_destroy", "pi0b_engine_gen_weights",
     "pi0b_engine_set_weight", "pi0b_engine_set_bias_table", "pi0b_engine_run", "pi0b_engine_run_prefix",
@@ -139,7 +172,7 @@ EXPORTED_SYMBOLS = [
     "pi0b_engine_read_checkpoint", "pi0b_engine_time_node", "pi0b_engine_describe", "pi0b_engine_ae_trace",
     "pi0b_last_error", "pi0b_gemm", "pi0b_gemm_skinny", "pi0b_attention",
     "pi0b_attention_ws_floats", "pi0b_random_f64", "pi0b_random_packed_bf16", "pi0b_seed_hash",
-    "pi0b_engine_run_images", "pi0b_image_patches",
+    "pi0b_engine_run_images", "pi0b_image_patches", "pi0b_stream_run",
 ]
 
 
