@@ -41,7 +41,10 @@ constexpr int kAeThreads = 320;
 constexpr int kWorkers = 256;
 constexpr int kWBlk = 64 * 64 * 2;    // 8 KB: [64 features x 64 k] bf16 SW128 image
 constexpr int kWSlot = 2 * kWBlk;     // ring slot: up to two consecutive k-blocks, one bulk copy
-constexpr int kWSt = 5;
+#ifndef PI0B_AE_WST
+#define PI0B_AE_WST 5
+#endif
+constexpr int kWSt = PI0B_AE_WST;
 constexpr int kWPrefetch = 0;  // weight bytes a CTA keeps bulk-prefetched into L2 ahead
 #ifndef PI0B_AE_XST
 #define PI0B_AE_XST 3
