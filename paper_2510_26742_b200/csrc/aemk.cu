@@ -74,6 +74,10 @@ constexpr int kBlocksPerSplit = 2;    // 64-key blocks per attention task
 #ifndef PI0B_AE_OREG
 #define PI0B_AE_OREG 1
 #endif
+#ifndef PI0B_AE_ADUP
+#define PI0B_AE_ADUP 1
+#endif
+constexpr bool kAttnDup = PI0B_AE_ADUP != 0;  // single-head attention with duplicated query rows
 constexpr int kOReg = 5;              // ae.proj staging combines up to this many key ranges in registers
 constexpr int kOffW = 0;
 constexpr int kOffU = kWSt * kWSlot;                // union region (128 KB)
@@ -1028,8 +1032,12 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         const int a4 = one ? q >> 9 : q >> 10, R = (q >> 3) & (hrow - 1), c = q & 7;
                         const int head = one ? rb : 2 * rb + (R >> 6);
                         const bool ok = head < p.heads;
-                        cp_async16(sQ + a4 * 16384 + swz(R, c),
-                                   ok ? p.qkv + (size_t)(R & 63) * p.n_qkv + head * 256 + a4 * 64 + c * 8 : p.qkv, ok);
+                        const __nv_bfloat16* qsrc = ok ? p.qkv + (size_t)(R & 63) * p.n_qkv + head * 256 + a4 * 64 + c * 8 : p.qkv;
+                        cp_async16(sQ + a4 * 16384 + swz(R, c), qsrc, ok);
+                        // single head: the 64 query rows also fill A rows 64..127, so S (and P, O)
+                        // come out twice and all four TMEM lane quarters (= SM sub-partitions) can
+                        // share the softmax and the O readout
+                        if (one && kAttnDup) cp_async16(sQ + a4 * 16384 + swz(R + 64, c), qsrc, ok);
                     }
                     if (!early_k) issue_kv(sK, 0, true);
                     cp_async_arrive_noinc(q_full);
@@ -1041,6 +1049,77 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 if (tr) tr[10] = gtimer();
                 unsigned long long* trs =
                     (p.trace && threadIdx.x == 128) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
+                if (one && kAttnDup) {
+                    // Single head, duplicated rows: TMEM lane L holds query row R = L & 63; lane half
+                    // kh = L >> 6 takes key block kh and, for O, output columns [128 kh, 128 kh + 128);
+                    // warp side splits those into two halves.  4 partial (max, sum) per row.
+                    const int side = (warp >= 6) ? 1 : 0;
+                    const int L = wq * 32 + lane, R = L & 63, kh = L >> 6;
+                    const int nk = p.kv_rows0 + 64 - key0;  // valid keys from key0
+                    float* xch = reinterpret_cast<float*>(sm_ml);  // [4 parts][64 rows]
+                    const int part = kh * 2 + side;
+                    mbar_wait(s_full, ph);
+                    tc_fence_after();
+                    float sv[32];
+                    tmem_ld32(tmem + kTS + tlane + kh * 64 + side * 32, sv);  // warp-uniform
+                    const int nkm = kh < nb ? min(32, max(0, nk - (kh * 64 + side * 32))) : 0;
+                    float mx = -INFINITY;
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        sv[e] = e < nkm ? sv[e] * p.scale_log2 : -INFINITY;
+                        mx = fmaxf(mx, sv[e]);
+                    }
+                    xch[part * 64 + R] = mx;
+                    named_bar_sync(1, kWorkers);
+                    mx = fmaxf(fmaxf(xch[R], xch[64 + R]), fmaxf(xch[128 + R], xch[192 + R]));
+                    float l = 0.f;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint32_t pk[4];
+#pragma unroll
+                        for (int e = 0; e < 8; e += 2) {
+                            const float e0 = ex2_fast(sv[q * 8 + e] - mx), e1 = ex2_fast(sv[q * 8 + e + 1] - mx);
+                            l += e0 + e1;
+                            pk[e / 2] = pack2(e0, e1);
+                        }
+                        const uint4 v = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                        *reinterpret_cast<uint4*>(sP + kh * 16384 + swz(R, side * 4 + q)) = v;
+                        *reinterpret_cast<uint4*>(sP + kh * 16384 + swz(R + 64, side * 4 + q)) = v;
+                    }
+                    fence_proxy_async_smem();
+                    tc_fence_before();
+                    named_bar_sync(1, kWorkers);  // all max reads done before the sums reuse xch
+                    xch[part * 64 + R] = l;
+                    if (wtid == 0) mbar_arrive(p_full);
+                    if (trs) trs[11] = gtimer();
+                    mbar_wait(o_done, ph);
+                    tc_fence_after();
+                    if (trs) trs[12] = gtimer();
+                    l = (xch[R] + xch[64 + R]) + (xch[128 + R] + xch[192 + R]);
+                    const float il = l > 0.f ? 1.f / l : 0.f;
+                    // normalised O (bf16) -> smem [64 rows][512 B]; this thread: columns
+                    // [128 kh + 64 side, +64) of row R
+                    uint8_t* orow_s = sQ + R * 512 + kh * 256;
+#pragma unroll 1
+                    for (int q = 0; q < 8; ++q) {
+                        float o[8];
+                        tmem_ld8(tmem + kTO + tlane + kh * 128 + side * 64 + q * 8, o);
+                        *reinterpret_cast<uint4*>(orow_s + (((side * 8 + q) ^ (R & 15)) << 4)) =
+                            make_uint4(pack2(o[0] * il, o[1] * il), pack2(o[2] * il, o[3] * il),
+                                       pack2(o[4] * il, o[5] * il), pack2(o[6] * il, o[7] * il));
+                    }
+                    if (part == 0 && rb < p.heads) p.ml[(size_t)split * p.heads * 64 + rb * 64 + R] = make_float2(mx, l);
+                    tc_fence_before();
+                    named_bar_sync(1, kWorkers);
+                    __nv_bfloat16* obase = p.opart + (size_t)split * 64 * p.q_width;
+#pragma unroll 1
+                    for (int e = wtid; e < 64 * 32; e += kWorkers) {
+                        const int rr = e >> 5, cc = e & 31;
+                        const int half = cc >> 4, q16 = cc & 15;
+                        const uint4 v = *reinterpret_cast<const uint4*>(sQ + rr * 512 + half * 256 + ((q16 ^ (rr & 15)) << 4));
+                        *reinterpret_cast<uint4*>(obase + (size_t)rr * p.q_width + rb * 256 + cc * 8) = v;
+                    }
+                } else
                 {
                     // All 8 worker warps: two per TMEM lane quarter (rows R = 32 wq + lane); warp
                     // `side` 0 takes key block 0 / output columns 0..127, side 1 block 1 / 128..255.
