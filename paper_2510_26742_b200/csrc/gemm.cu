@@ -28,6 +28,10 @@
 namespace pi0b {
 
 constexpr int BM = 128;
+#ifndef PI0B_PAIR_STAGES
+#define PI0B_PAIR_STAGES 7
+#endif
+constexpr int kPairStages = PI0B_PAIR_STAGES;  // smem ring depth of the CTA-pair GEMM (32 KB stages)
 constexpr int BK = 64;
 constexpr int kGemmThreads = 64 + 8 * 32;  // TMA warp, MMA warp, 8 epilogue warps
 static bool g_gemm_pdl = true;             // launch with programmatic stream serialization
@@ -532,9 +536,9 @@ cudaError_t gemm_configure() {
     if (e == cudaSuccess) e = configure_t<256, 3, kModeGate, 2>();
     if (e == cudaSuccess) e = configure_t<256, 3, kModeBf16, 2>();
     if (e == cudaSuccess) e = configure_t<256, 3, kModeResid, 2>();
-    if (e == cudaSuccess) e = configure_t<256, 6, kModeGate, 1, 2>();
-    if (e == cudaSuccess) e = configure_t<256, 6, kModeBf16, 1, 2>();
-    if (e == cudaSuccess) e = configure_t<256, 6, kModeResid, 1, 2>();
+    if (e == cudaSuccess) e = configure_t<256, kPairStages, kModeGate, 1, 2>();
+    if (e == cudaSuccess) e = configure_t<256, kPairStages, kModeBf16, 1, 2>();
+    if (e == cudaSuccess) e = configure_t<256, kPairStages, kModeResid, 1, 2>();
     if (e == cudaSuccess) e = configure_bn<128, 6>();
     if (e == cudaSuccess) e = configure_bn<64, 8>();
     return e;
@@ -639,7 +643,7 @@ cudaError_t launch_gemm(int bn, const CUtensorMap& ta, const CUtensorMap& tb, co
                 cudaLaunchConfig_t c{};
                 c.gridDim = dim3(2, 1, 1);
                 c.blockDim = dim3(kGemmThreads, 1, 1);
-                c.dynamicSmemBytes = GemmCfg<256, 6, 1, 2>::SMEM;
+                c.dynamicSmemBytes = GemmCfg<256, kPairStages, 1, 2>::SMEM;
                 cudaLaunchAttribute a[1];
                 a[0].id = cudaLaunchAttributeClusterDimension;
                 a[0].val.clusterDim.x = 2;
@@ -648,7 +652,7 @@ cudaError_t launch_gemm(int bn, const CUtensorMap& ta, const CUtensorMap& tb, co
                 c.attrs = a;
                 c.numAttrs = 1;
                 int n = 0;
-                if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<256, 6, kModeGate, 1, 2>, &c) != cudaSuccess) n = 0;
+                if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<256, kPairStages, kModeGate, 1, 2>, &c) != cudaSuccess) n = 0;
                 pairs = n;
                 if (getenv("PI0B_GEMM_DEBUG")) fprintf(stderr, "pi0b: %d co-resident GEMM CTA pairs\n", n);
             }
@@ -659,9 +663,9 @@ cudaError_t launch_gemm(int bn, const CUtensorMap& ta, const CUtensorMap& tb, co
     grid.x *= cg;  // CTA pairs: cluster (2, 1, 1)
     if (cg == 2) {
         switch (p.mode) {
-            case kModeGate: return launch_t<256, 6, kModeGate, 1, 2>(ta, tb, p, grid, stream);
-            case kModeBf16: return launch_t<256, 6, kModeBf16, 1, 2>(ta, tb, p, grid, stream);
-            case kModeResid: return launch_t<256, 6, kModeResid, 1, 2>(ta, tb, p, grid, stream);
+            case kModeGate: return launch_t<256, kPairStages, kModeGate, 1, 2>(ta, tb, p, grid, stream);
+            case kModeBf16: return launch_t<256, kPairStages, kModeBf16, 1, 2>(ta, tb, p, grid, stream);
+            case kModeResid: return launch_t<256, kPairStages, kModeResid, 1, 2>(ta, tb, p, grid, stream);
             default: return cudaErrorInvalidValue;
         }
     }
