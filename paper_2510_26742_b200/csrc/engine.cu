@@ -1383,11 +1383,17 @@ void Engine::upload_inputs(const double* patches, const double* state, const dou
     // which: 0 = all, 1 = prefix inputs, 2 = action inputs, 3 = all but the patches. Copies go through pinned
     // staging so the H2D transfers are asynchronous DMA on the engine stream.
     double* h = h_in_;
+    // Large tensors go in 256 KB pieces so that the host copy of piece i + 1 into the pinned
+    // staging overlaps the DMA of piece i.
     auto stage = [&](const double* src, size_t n, double* dev) {
         if (!n) return;
         if (!src) throw EngineError(PI0B_E_INVALID, "missing input tensor");
-        std::memcpy(h, src, n * 8);
-        PI0B_CUDA(cudaMemcpyAsync(dev, h, n * 8, cudaMemcpyHostToDevice, stream_));
+        constexpr size_t kPiece = 32768;  // doubles (256 KB)
+        for (size_t o = 0; o < n; o += kPiece) {
+            const size_t m = std::min(kPiece, n - o);
+            std::memcpy(h + o, src + o, m * 8);
+            PI0B_CUDA(cudaMemcpyAsync(dev + o, h + o, m * 8, cudaMemcpyHostToDevice, stream_));
+        }
         h += n;
     };
     if (which == 0 || which == 1) {
