@@ -35,6 +35,19 @@ sys.path.insert(0, ROOT)
 METRIC = "p50 π0 inference latency (ms) at 1/2/3 views, chunk 63, 10 flow steps"
 
 
+def reduce_over_ranks(values, device=None):
+    """Max over ranks of per-rank timings (the contract: every multi-GPU number is the max over
+    ranks).  No-op at world size 1; `device` = where the collective's tensor lives (cuda for
+    NCCL, None = cpu for gloo)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return [float(v) for v in values]
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -156,10 +169,7 @@ def run_ours(args) -> None:
             e2e.append((time.perf_counter() - t0) * 1e3)
     e2e_p50 = float(np.median(e2e))
 
-    if ws > 1:
-        t = torch.tensor([p50, p90, mean, e2e_p50], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        p50, p90, mean, e2e_p50 = [float(v) for v in t.tolist()]
+    p50, p90, mean, e2e_p50 = reduce_over_ranks([p50, p90, mean, e2e_p50], device="cuda")
 
     # Dominant kernel: the action-expert megakernel (one launch = all 10 flow steps; HBM-bound on
     # the weight stream).  Algorithmic bytes per launch = every AE weight byte once per flow step

@@ -1,0 +1,64 @@
+"""Multi-process host logic of bench.py's N > 1 path on CPU (gloo, world size 2): the timing
+reduction is the max over ranks, the reported throughput aggregates the replicas, and the
+reference arm runs on rank 0 only (the other ranks exit 0 without work)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, ws, port, out):
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    import bench
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    try:
+        # rank r reports [p50, p90, mean, e2e] = [10 + r, 11 + r, 10.5 + 2 r, 12 - r]
+        vals = bench.reduce_over_ranks([10 + rank, 11 + rank, 10.5 + 2 * rank, 12 - rank])
+        out.put((rank, vals))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_reduce_over_ranks_is_max_gloo():
+    ws, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_worker, args=(r, ws, port, q)) for r in range(ws)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(ws))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(ws):
+        assert res[r] == [11.0, 12.0, 12.5, 12.0]
+
+
+def test_reduce_single_process_is_identity():
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.reduce_over_ranks([1, 2.5]) == [1.0, 2.5]
+
+
+def test_reference_arm_rank1_exits_without_work():
+    env = dict(os.environ, WORLD_SIZE="2", RANK="1", LOCAL_RANK="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=120, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.strip() == ""
