@@ -475,7 +475,12 @@ void Engine::alloc_weights() {
     add("ve.fc1", ve_w, c.ve_mlp, c.ve_layers, true);
     add("ve.fc2", c.ve_mlp, ve_w, c.ve_layers, true);
     add("llm.proj_in", ve_w, llm_w, 1, true);
-    add("llm.qkv", llm_w, llm_qkv, c.llm_layers, false);
+    // llm.qkv on 128-wide tiles needs each tile to hold 64 columns of a head and their RoPE
+    // partners: the kPermRope packing (PI0B_LLM_QKV_BN128=0: 256-wide head tiles, natural order)
+    if (env_int("PI0B_LLM_QKV_BN128", 1))
+        add("llm.qkv", llm_w, llm_qkv, c.llm_layers, false, kPermRope, false, llm_q + c.llm_kv_heads * c.llm_head_dim);
+    else
+        add("llm.qkv", llm_w, llm_qkv, c.llm_layers, false);
     add("llm.proj", llm_q, llm_w, c.llm_layers - 1, false);
     add("llm.ffn", llm_w, 2 * c.llm_mlp, c.llm_layers - 1, false, kPermGate128);
     add("llm.down", c.llm_mlp, llm_w, c.llm_layers - 1, false);
@@ -862,11 +867,14 @@ void Engine::build_plan() {
             g.rope_cs = rope_cs_;
             g.rope_pos0 = 0;
             g.ldo = llm_qkv_n;
+            const bool bn128 = Wv["llm.qkv"].perm == kPermRope;
+            const int qkv_bn = bn128 ? 128 : 256;
+            if (bn128) g.flags |= kFlagRopePacked;
             if (l < NL - 1) {
                 g.N = llm_qkv_n;
                 g.rope_cols = llm_q_ + llm_kv_;
                 g.out = kv_[l];
-                add_gemm(0, "llm.qkv", l, xb_, llm_w_, L_, Wv["llm.qkv"], l, 256, g);
+                add_gemm(0, "llm.qkv", l, xb_, llm_w_, L_, Wv["llm.qkv"], l, qkv_bn, g);
             } else {
                 // Last layer: only K/V feed the action expert; its Q is dead.
                 NodeWeights sub = Wv["llm.qkv"];
@@ -874,7 +882,7 @@ void Engine::build_plan() {
                 g.N = 2 * llm_kv_;
                 g.rope_cols = llm_kv_;
                 g.out = kv_[l] + llm_q_;
-                add_gemm(0, "llm.qkv", l, xb_, llm_w_, L_, sub, l, 256, g);
+                add_gemm(0, "llm.qkv", l, xb_, llm_w_, L_, sub, l, qkv_bn, g);
             }
             tag("llm.qkv", l, kv_[l], L_, llm_qkv_n, llm_qkv_n, 1);
         }

@@ -120,7 +120,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     static_assert(CG == 1 || (MT == 1 && BN == 256), "CTA-pair tiles are 256 x 256");
     // accumulator buffers: double-buffered when two fit in TMEM's 512 columns
     constexpr int NBUF = 2 * MT * Cfg::TMEM_COLS <= 512 ? 2 : 1;
-    constexpr bool kPaired = MODE == kModeGate || (MODE == kModeBf16 && BN == 256);
+    // chunk pairs (c, c + NP): gated FFN (up | gate), RoPE heads (bn 256, or bn 128 over
+    // kPermRope-packed weights); bn 256 bf16 GEMMs without RoPE take the same path and simply
+    // write both chunks in place
+    const bool kPaired = MODE == kModeGate || (MODE == kModeBf16 && (BN == 256 || (BN == 128 && (p.flags & kFlagRopePacked))));
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
         constexpr int NC = BN / 32;                 // 32-column chunks in the tile
         constexpr int NP = NC / 2;                  // (c, c + NP) pairs
-        constexpr int NU = kPaired ? NP : NC;       // epilogue units: chunks, or chunk pairs
+        const int NU = kPaired ? NP : NC;           // epilogue units: chunks, or chunk pairs
         // Split-K: unit u belongs to cluster rank u % S.  Chunk c of row r is parked at
         // stage + c*16 KB + r*128 B, 16-byte pieces XOR-swizzled by r (conflict-free).
         const int rank = split;
@@ -401,7 +404,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     store_bf16x32(reinterpret_cast<__nv_bfloat16*>(p.outb) + (long long)r * p.ldob + col0, h, nv);
             }
             if (valid && p.out_stats) atomicAdd(p.out_stats + r, ss);
-        } else if constexpr (kPaired) {
+        } else if (kPaired) {
             // Gate: tile columns [0, BN/2) are up, [BN/2, BN) the matching gate columns.
             // RoPE (BN == 256, one head per tile): pairs (j, j+128), proj/src/tensor.cpp:150-178.
             const bool rope = MODE == kModeBf16 && (p.flags & kFlagRope) && n0 < p.rope_cols;
@@ -424,10 +427,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         a[j] = a[j] * rs + sm_vec[c * 32 + j];
                         b[j] = b[j] * rs + sm_vec[(c + NP) * 32 + j];
                     }
+                    if (p.flags & kFlagGelu) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            a[j] = gelu_tanh(a[j]);
+                            b[j] = gelu_tanh(b[j]);
+                        }
+                    }
+                    // packed bn = 128 head tile: features at head * 256 + 64 * half + 32 c + j,
+                    // partners 128 further (kernels_misc.cu packed_row, kPermRope)
+                    const bool packed = BN == 128 && rope && (p.flags & kFlagRopePacked);
+                    const int j0 = packed ? ((n0 >> 7) & 1) * 64 + c * 32 : c * 32;  // rope table column
                     if (rope) {
 #pragma unroll
                         for (int j = 0; j < 32; j += 2) {
-                            const float4 t = *reinterpret_cast<const float4*>(cs + c * 32 + j);
+                            const float4 t = *reinterpret_cast<const float4*>(cs + j0 + j);
                             const float x0 = a[j], y0 = b[j], x1 = a[j + 1], y1 = b[j + 1];
                             a[j] = x0 * t.x - y0 * t.y;
                             b[j] = x0 * t.y + y0 * t.x;
@@ -435,9 +449,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             b[j + 1] = x1 * t.w + y1 * t.z;
                         }
                     }
-                    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)r * p.ldo + n0;
-                    store_bf16x32(o + c * 32, a, min(32, p.N - (n0 + c * 32)));
-                    store_bf16x32(o + (c + NP) * 32, b, min(32, p.N - (n0 + (c + NP) * 32)));
+                    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)r * p.ldo;
+                    if (packed) {
+                        const int f = (n0 >> 8) * 256 + j0;
+                        store_bf16x32(o + f, a, 32);
+                        store_bf16x32(o + f + 128, b, 32);
+                    } else {
+                        store_bf16x32(o + n0 + c * 32, a, min(32, p.N - (n0 + c * 32)));
+                        store_bf16x32(o + n0 + (c + NP) * 32, b, min(32, p.N - (n0 + (c + NP) * 32)));
+                    }
                 }
             }
         } else {
@@ -622,7 +642,7 @@ int gemm_max_active_clusters(int bn, int splits) {
 
 cudaError_t launch_gemm(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                         cudaStream_t stream) {
-    if ((p.flags & kFlagRope) && bn != 256) return cudaErrorInvalidValue;
+    if ((p.flags & kFlagRope) && bn != 256 && !(bn == 128 && (p.flags & kFlagRopePacked))) return cudaErrorInvalidValue;
     if (p.splits < 1 || p.splits > kGemmMaxSplits) return cudaErrorInvalidValue;
     const int mt = p.mt > 1 ? p.mt : 1, cg = p.cg > 1 ? p.cg : 1;
     if (p.persist && p.splits != 1) return cudaErrorInvalidValue;
