@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
     if (threadIdx.x == 0) {
         for (int i = 0; i < kNumBars; ++i) {
             uint32_t cnt = 1;
-            if ((i >= kBXFull && i < kBXFull + kXSt) || i == kBQFull || i == kBVFull) cnt = kWorkers;
+            if ((i >= kBXFull && i < kBXFull + kXSt) || i == kBQFull) cnt = kWorkers;  // v_full: one TMA arm
             if (i >= kBWFull && i < kBWFull + kWSt) cnt = 32;  // producer lanes' cp.async arrivals
             // kBPairFull / kBPairReady: one remote arrival each (from the partner CTA)
             mbar_init(&mb[i], cnt);
@@ -1042,10 +1042,26 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     if (!early_k) issue_kv(sK, 0, true);
                     cp_async_arrive_noinc(q_full);
                 }
-                mbar_wait(s_full, ph);  // K (and Q) consumed: V may overwrite K
-                tc_fence_after();
-                issue_kv(sV, 256, false);
-                cp_async_arrive_noinc(v_full);
+                // V overwrites K once the score MMA has consumed it: one thread issues the V tiles as
+                // TMA boxes of 32 keys x 64 columns (LLM cache rows, then the expert's own rows;
+                // rows past the own 64 are zero-filled), everybody else goes straight to the softmax
+                if (wtid == 0) {
+                    mbar_wait(s_full, ph);
+                    tc_fence_after();
+                    mbar_arrive_expect_tx(v_full, uint32_t(nb) * 32768u);
+                    const CUtensorMap* cm = p.vmaps + t.aux;
+                    const CUtensorMap* om = p.vmaps + (p.n_vmaps - 1);
+                    for (int b = 0; b < nb; ++b)
+                        for (int a4 = 0; a4 < 4; ++a4)
+                            for (int h2 = 0; h2 < 2; ++h2) {
+                                const int key = key0 + b * 64 + h2 * 32;
+                                uint8_t* dst = sV + b * 32768 + a4 * 8192 + h2 * 4096;
+                                if (key < p.kv_rows0)
+                                    tma_load_2d(dst, cm, v_full, p.kcol_cache + 256 + a4 * 64, key, kEvictLast);
+                                else
+                                    tma_load_2d(dst, om, v_full, p.kcol_own + 256 + a4 * 64, key - p.kv_rows0, kEvictNormal);
+                            }
+                }
                 if (tr) tr[10] = gtimer();
                 unsigned long long* trs =
                     (p.trace && threadIdx.x == 128) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
@@ -1264,7 +1280,7 @@ AePlan ae_plan(const AePlanInput& in) {
     need(in.rope_cols % 128 == 0, "rope columns");
     need(in.chunk + 1 <= 64, "suffix rows > 64");
     need(in.act_dim <= 32 && in.state_dim <= 64, "action/state dims");
-    need(in.kv_rows0 % 8 == 0, "prefix length must be a multiple of 8");
+    need(in.kv_rows0 % 32 == 0, "prefix length must be a multiple of 32 (32-key TMA boxes)");
     const int splits = (in.key_blocks + kBlocksPerSplit - 1) / kBlocksPerSplit;
     need(splits <= kMaxSplits && splits * 8192 <= kORegion, "too many attention key blocks (prefix too long)");
     need(in.num_ctas >= 2 * ((in.heads + 1) / 2), "too few SMs");
@@ -1414,6 +1430,7 @@ AePlan ae_plan(const AePlanInput& in) {
                         x.kind = kAeAttn;
                         x.ncol = uint16_t(in.attn_single ? 1 : 0);  // 1: single-head task (tile = head)
                         x.wmat = uint16_t(in.mat_kv[size_t(gl % int(in.mat_kv.size()))]);  // llm.qkv@mod
+                        x.aux = uint16_t(gl % int(in.mat_kv.size()));  // V tensor map (AeParams::vmaps)
                         x.tile = uint16_t(rb);
                         x.kb0 = uint16_t(j);
                         x.nkb = uint16_t(std::min(kBlocksPerSplit, in.key_blocks - j * kBlocksPerSplit));

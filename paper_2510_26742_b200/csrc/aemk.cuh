@@ -23,6 +23,7 @@
 // ae.down, ae.action_out) are split over K, and they add straight into the residual stream.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -109,6 +110,10 @@ struct AeParams {
     int limit_phase;               // run only tasks with phase < limit (debug / parity probes)
     unsigned long long* trace;     // optional [ctas][stride][16] globaltimer stamps per task
     unsigned long long* dbg;       // optional [ctas][128] per-k-block stamps of the first ae.qkv task
+    // attention V tiles by TMA (32-row boxes of 64 columns, 128-byte swizzle): [0, n) = the LLM KV
+    // caches (attention task aux = index), [n] = the action expert's own q|k|v rows
+    const CUtensorMap* vmaps;
+    int n_vmaps;
 };
 
 // Host planner: dimensions + operand indices in, per-CTA task table out.

@@ -1230,6 +1230,16 @@ void Engine::build_ae_mega() {
     }
     PI0B_CUDA(cudaStreamSynchronize(stream_));
 
+    // V tensor maps for the attention tasks: every LLM KV cache, then the expert's q|k|v rows
+    {
+        std::vector<CUtensorMap> vm;
+        for (int l = 0; l < c.llm_layers; ++l) vm.push_back(make_tmap_bf16(kv_[size_t(l)], L_, llm_qkv_n, llm_qkv_n, 32));
+        vm.push_back(make_tmap_bf16(aqkv_, S_, NQ, NQ, 32));
+        CUtensorMap* dvm = alloc<CUtensorMap>(vm.size());
+        PI0B_CUDA(cudaMemcpy(dvm, vm.data(), vm.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+        ae_p_.vmaps = dvm;
+        ae_p_.n_vmaps = int(vm.size());
+    }
     AeParams& P = ae_p_;
     P.tasks = dtasks;
     P.task_stride = ae_plan_.stride;
