@@ -282,7 +282,8 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
     if (threadIdx.x == 0) {
         for (int i = 0; i < kNumBars; ++i) {
             uint32_t cnt = 1;
-            if ((i >= kBXFull && i < kBXFull + kXSt) || i == kBQFull) cnt = kWorkers;  // v_full: one TMA arm
+            if (i >= kBXFull && i < kBXFull + kXSt) cnt = kWorkers;
+            if (i == kBQFull) cnt = kWorkers + 1;  // workers' cp.async arrivals + one (TMA) arm; v_full: one arm
             if (i >= kBWFull && i < kBWFull + kWSt) cnt = 32;  // producer lanes' cp.async arrivals
             // kBPairFull / kBPairReady: one remote arrival each (from the partner CTA)
             mbar_init(&mb[i], cnt);
@@ -1026,18 +1027,31 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     }
                 };
                 {   // Q (both heads of the pair, or the one head) and K
+                    // single head: the 64 query rows also fill A rows 64..127, so S (and P, O)
+                    // come out twice and all four TMEM lane quarters (= SM sub-partitions) can
+                    // share the softmax and the O readout.  Those Q tiles come by TMA (one thread,
+                    // 8 boxes of 64 rows x 64 columns); q_full also takes that thread's arm.
+                    const bool qtma = one && kAttnDup;
+                    if (wtid == 0) {
+                        if (qtma) {
+                            mbar_arrive_expect_tx(q_full, 65536u);
+                            const CUtensorMap* qm = p.vmaps + (p.n_vmaps - 1);
+                            for (int a4 = 0; a4 < 4; ++a4) {
+                                tma_load_2d(sQ + a4 * 16384, qm, q_full, rb * 256 + a4 * 64, 0, kEvictNormal);
+                                tma_load_2d(sQ + a4 * 16384 + 8192, qm, q_full, rb * 256 + a4 * 64, 0, kEvictNormal);
+                            }
+                        } else {
+                            mbar_arrive(q_full);
+                        }
+                    }
 #pragma unroll 4
-                    for (int u = 0; u < (one ? 8 : 16); ++u) {
+                    for (int u = 0; u < (qtma ? 0 : one ? 8 : 16); ++u) {
                         const int q = wtid + 256 * u;
                         const int a4 = one ? q >> 9 : q >> 10, R = (q >> 3) & (hrow - 1), c = q & 7;
                         const int head = one ? rb : 2 * rb + (R >> 6);
                         const bool ok = head < p.heads;
                         const __nv_bfloat16* qsrc = ok ? p.qkv + (size_t)(R & 63) * p.n_qkv + head * 256 + a4 * 64 + c * 8 : p.qkv;
                         cp_async16(sQ + a4 * 16384 + swz(R, c), qsrc, ok);
-                        // single head: the 64 query rows also fill A rows 64..127, so S (and P, O)
-                        // come out twice and all four TMEM lane quarters (= SM sub-partitions) can
-                        // share the softmax and the O readout
-                        if (one && kAttnDup) cp_async16(sQ + a4 * 16384 + swz(R + 64, c), qsrc, ok);
                     }
                     if (!early_k) issue_kv(sK, 0, true);
                     cp_async_arrive_noinc(q_full);
@@ -1050,7 +1064,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     tc_fence_after();
                     mbar_arrive_expect_tx(v_full, uint32_t(nb) * 32768u);
                     const CUtensorMap* cm = p.vmaps + t.aux;
-                    const CUtensorMap* om = p.vmaps + (p.n_vmaps - 1);
+                    const CUtensorMap* om = p.vmaps + (p.n_vmaps - 2);
                     for (int b = 0; b < nb; ++b)
                         for (int a4 = 0; a4 < 4; ++a4)
                             for (int h2 = 0; h2 < 2; ++h2) {

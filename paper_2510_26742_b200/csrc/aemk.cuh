@@ -111,7 +111,8 @@ struct AeParams {
     unsigned long long* trace;     // optional [ctas][stride][16] globaltimer stamps per task
     unsigned long long* dbg;       // optional [ctas][128] per-k-block stamps of the first ae.qkv task
     // attention V tiles by TMA (32-row boxes of 64 columns, 128-byte swizzle): [0, n) = the LLM KV
-    // caches (attention task aux = index), [n] = the action expert's own q|k|v rows
+    // caches (attention task aux = index), [n] = the action expert's own q|k|v rows (32-row
+    // boxes), [n + 1] = the same with 64-row boxes (Q tiles)
     const CUtensorMap* vmaps;
     int n_vmaps;
 };

@@ -1234,7 +1234,8 @@ void Engine::build_ae_mega() {
     {
         std::vector<CUtensorMap> vm;
         for (int l = 0; l < c.llm_layers; ++l) vm.push_back(make_tmap_bf16(kv_[size_t(l)], L_, llm_qkv_n, llm_qkv_n, 32));
-        vm.push_back(make_tmap_bf16(aqkv_, S_, NQ, NQ, 32));
+        vm.push_back(make_tmap_bf16(aqkv_, S_, NQ, NQ, 32));  // own K / V rows, 32-key boxes
+        vm.push_back(make_tmap_bf16(aqkv_, S_, NQ, NQ, 64));  // own Q rows, 64-row boxes
         CUtensorMap* dvm = alloc<CUtensorMap>(vm.size());
         PI0B_CUDA(cudaMemcpy(dvm, vm.data(), vm.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
         ae_p_.vmaps = dvm;
