@@ -24,6 +24,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <random>
 #include <chrono>
 #include <cctype>
@@ -65,7 +70,8 @@ cudaError_t launch_f64_to_f32(float* dst, const double* src, int n, cudaStream_t
 cudaError_t launch_rows_to_f32(const double* src, int rows, int cols, float* dst, long long ldd,
                                __nv_bfloat16* dstb, long long lddb, float* stats, cudaStream_t st);
 cudaError_t launch_f64_to_bf16_rows(const double* src, int rows, int cols, __nv_bfloat16* dst,
-                                    long long ldd, cudaStream_t st);
+                                    long long ldd, cudaStream_t st,
+                                    const int* host_bf16 = nullptr, const __nv_bfloat16* srcb = nullptr);
 cudaError_t launch_image_patches(const double* img, int views, int H, int W, int C, int side, int P, double* patches,
                                  cudaStream_t st);
 cudaError_t launch_f32_to_f64(const float* src, long long lds, int rows, int cols, double* dst,
@@ -234,6 +240,8 @@ struct Op {
     float* stats = nullptr;
     const float* src32 = nullptr;
     double* dst64 = nullptr;
+    const int* skip = nullptr;  // kOpF64Bf16: device flag, nonzero = the rows came as bf16 in srcb
+    const __nv_bfloat16* srcb = nullptr;
     void* mptr = nullptr;
     size_t mbytes = 0;
     // checkpoint tag (record mode)
@@ -262,6 +270,112 @@ struct Checkpoint {
     int rows = 0, cols = 0, bf16 = 0;
 };
 
+// Host side of the end-to-end call: the patches (2.4 MB of fp64 at 2 views) are converted to
+// bf16 into pinned staging before their DMA, and one core (~10 GB/s of memory traffic) bounds
+// that.  A few helper threads convert row pieces in parallel; the calling thread works too and
+// issues each piece's DMA, in order, as soon as the piece is ready.
+class StagingPool {
+public:
+    explicit StagingPool(int helpers) {
+        for (int i = 0; i < helpers; ++i) th_.emplace_back([this] { loop(); });
+    }
+    ~StagingPool() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    // work(k) for k in [0, np) on the helpers and the calling thread; issue(k) on the calling
+    // thread, in order, once work(k) has finished.
+    template <class Work, class Issue>
+    void run(size_t np, Work&& work, Issue&& issue) {
+        if (th_.empty() || np < 2) {
+            for (size_t k = 0; k < np; ++k) {
+                work(k);
+                issue(k);
+            }
+            return;
+        }
+        // helpers of the previous job must have left it before its fields change
+        while (acks_.load(std::memory_order_acquire) != int(th_.size())) std::this_thread::yield();
+        if (np > cap_) {
+            done_.reset(new std::atomic<uint8_t>[np]);
+            cap_ = np;
+        }
+        for (size_t k = 0; k < np; ++k) done_[k].store(0, std::memory_order_relaxed);
+        work_ = std::function<void(size_t)>(work);
+        np_ = np;
+        next_.store(0, std::memory_order_relaxed);
+        acks_.store(0, std::memory_order_relaxed);
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            ++gen_;
+        }
+        cv_.notify_all();
+        size_t issued = 0;
+        try {
+            while (issued < np) {
+                if (done_[issued].load(std::memory_order_acquire)) {
+                    issue(issued);
+                    ++issued;
+                    continue;
+                }
+                const size_t k = next_.fetch_add(1, std::memory_order_relaxed);
+                if (k < np) do_piece(k);
+            }
+        } catch (...) {  // the caller's buffer must outlive every helper's work
+            next_.store(np, std::memory_order_relaxed);
+            while (acks_.load(std::memory_order_acquire) != int(th_.size())) std::this_thread::yield();
+            throw;
+        }
+    }
+
+private:
+    void do_piece(size_t k) {
+        work_(k);
+        done_[k].store(1, std::memory_order_release);
+    }
+    void loop() {
+        unsigned long long seen = 0;
+        acks_.fetch_add(1, std::memory_order_release);  // idle
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+            }
+            for (;;) {
+                const size_t k = next_.fetch_add(1, std::memory_order_relaxed);
+                if (k >= np_) break;
+                do_piece(k);
+            }
+            acks_.fetch_add(1, std::memory_order_release);
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_;
+    unsigned long long gen_ = 0;
+    bool stop_ = false;
+    std::atomic<size_t> next_{0};
+    std::atomic<int> acks_{0};
+    std::unique_ptr<std::atomic<uint8_t>[]> done_;
+    size_t cap_ = 0;
+    std::function<void(size_t)> work_;
+    size_t np_ = 0;
+};
+
+static int staging_helpers() {
+    const char* e = std::getenv("PI0B_STAGING_THREADS");
+    const int hw = int(std::thread::hardware_concurrency());
+    const int want = e ? std::atoi(e) : 3;
+    return std::max(0, std::min(want, hw - 1));
+}
+
 class Engine {
 public:
     Engine(const pi0b_model_config& cfg, const pi0b_engine_options& opt);
@@ -276,6 +390,7 @@ public:
     // camera frames [views][height][width*3] (fp64) -> resize + img2col on the device into the
     // patch input (kernels_misc.cu image_patches_kernel), instead of host patches
     void upload_images(const double* images, int height, int width);
+    void stage_patches_bf16(const double* patches);
     void launch(int part, cudaStream_t st);
     void fetch_actions(double* out);
     // asynchronous pieces for the streaming runtime (one outstanding operation per engine)
@@ -338,6 +453,13 @@ private:
     double *d_patches_ = nullptr, *d_state_ = nullptr, *d_noise_ = nullptr, *d_prompt_ = nullptr,
            *d_out_ = nullptr;
     double *h_in_ = nullptr, *h_out_ = nullptr;
+    std::unique_ptr<StagingPool> staging_{new StagingPool(staging_helpers())};
+    // patches converted to bf16 on the host (pinned staging) + the device flag that tells the
+    // graph's conversion op to skip; h_flag_[0] = 0, h_flag_[1] = 1 (pinned sources of the flag)
+    uint16_t* h_pb_ = nullptr;
+    int* h_flag_ = nullptr;
+    int* d_patch_host_bf16_ = nullptr;
+    __nv_bfloat16* d_pb_ = nullptr;  // the host-converted patches, packed
     cudaEvent_t done_ev_ = nullptr;               // streaming runtime: last async operation
     double *h_img_ = nullptr, *d_img_ = nullptr;  // image front-end staging (grown on demand)
     size_t n_img_ = 0;
@@ -418,6 +540,8 @@ Engine::~Engine() {
     if (done_ev_) cudaEventDestroy(done_ev_);
     if (d_img_) cudaFree(d_img_);
     if (h_out_) cudaFreeHost(h_out_);
+    if (h_pb_) cudaFreeHost(h_pb_);
+    if (h_flag_) cudaFreeHost(h_flag_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -526,6 +650,13 @@ void Engine::alloc_activations() {
     d_out_ = alloc<double>(n_out_);
     PI0B_CUDA(cudaMallocHost(&h_in_, (n_patches_ + n_state_ + n_noise_ + n_prompt_) * sizeof(double)));
     PI0B_CUDA(cudaMallocHost(&h_out_, n_out_ * sizeof(double)));
+    PI0B_CUDA(cudaMallocHost(&h_pb_, n_patches_ * sizeof(uint16_t)));
+    PI0B_CUDA(cudaMallocHost(&h_flag_, 2 * sizeof(int)));
+    h_flag_[0] = 0;
+    h_flag_[1] = 1;
+    d_patch_host_bf16_ = alloc<int>(1);
+    d_pb_ = alloc<__nv_bfloat16>(n_patches_);
+    PI0B_CUDA(cudaMemsetAsync(d_patch_host_bf16_, 0, sizeof(int), stream_));
 
     patches_b_ = alloc<__nv_bfloat16>(size_t(T_) * patch_ld_);
     PI0B_CUDA(cudaMemsetAsync(patches_b_, 0, size_t(T_) * patch_ld_ * 2, stream_));
@@ -723,6 +854,8 @@ void Engine::build_plan() {
         cv.cols = c.ve_patch_in;
         cv.dstb = patches_b_;
         cv.ldb = patch_ld_;
+        cv.skip = d_patch_host_bf16_;
+        cv.srcb = d_pb_;
         ops_.push_back(cv);
     }
     // --- vision encoder (proj/src/builder.cpp:205-240)
@@ -1416,7 +1549,7 @@ void Engine::upload_inputs(const double* patches, const double* state, const dou
         h += n;
     };
     if (which == 0 || which == 1) {
-        stage(patches, n_patches_, d_patches_);
+        stage_patches_bf16(patches);
         if (P_ > 0) stage(prompt, n_prompt_, d_prompt_);
     }
     if (which == 3) {  // everything but the patches (image front-end)
@@ -1428,6 +1561,44 @@ void Engine::upload_inputs(const double* patches, const double* state, const dou
         stage(state, n_state_, d_state_);
         stage(noise, n_noise_, d_noise_);
     }
+}
+
+// bf16(float(x)) with float -> bf16 round-to-nearest-even: bit-identical to the device conversion
+// (kernels_misc.cu f64_to_bf16_rows_kernel, __float2bfloat16_rn(float(x))).
+static inline uint16_t host_bf16(double x) {
+    const float f = float(x);
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return uint16_t(0x7fffu);  // canonical NaN, as cvt.rn.bf16.f32
+    return uint16_t((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+}
+
+void Engine::stage_patches_bf16(const double* patches) {
+    // The patches are the one large input (2.4 MB of fp64 at 2 views): converted on the host in
+    // row pieces into pinned bf16 staging, each piece's (contiguous) DMA issued as soon as it is
+    // converted; the graph's conversion op then only pads them into the GEMM operand.
+    if (!patches) throw EngineError(PI0B_E_INVALID, "missing input tensor");
+    const int cols = c_.ve_patch_in;
+    constexpr int kRowsPerPiece = 32;
+    const size_t np = size_t((T_ + kRowsPerPiece - 1) / kRowsPerPiece);
+    constexpr size_t kDmas = 4;
+    const size_t per_dma = std::max<size_t>(1, (np + kDmas - 1) / kDmas);
+    uint16_t* hb = h_pb_;
+    const size_t T = size_t(T_);
+    staging_->run(
+        np,
+        [=](size_t k) {
+            const size_t r0 = k * kRowsPerPiece, nr = std::min<size_t>(kRowsPerPiece, T - r0);
+            const double* src = patches + r0 * cols;
+            uint16_t* dst = hb + r0 * cols;
+            for (size_t i = 0, n = nr * cols; i < n; ++i) dst[i] = host_bf16(src[i]);
+        },
+        [&](size_t k) {  // a few large DMAs: each costs ~10 us of fixed latency on the B200 boxes
+            if ((k + 1) % per_dma && k + 1 != np) return;
+            const size_t r0 = (k / per_dma) * per_dma * kRowsPerPiece, r1 = std::min<size_t>((k + 1) * kRowsPerPiece, T);
+            PI0B_CUDA(cudaMemcpyAsync(d_pb_ + r0 * cols, hb + r0 * cols, (r1 - r0) * cols * 2, cudaMemcpyHostToDevice, stream_));
+        });
+    PI0B_CUDA(cudaMemcpyAsync(d_patch_host_bf16_, h_flag_ + 1, sizeof(int), cudaMemcpyHostToDevice, stream_));
 }
 
 void Engine::upload_images(const double* images, int height, int width) {
@@ -1450,6 +1621,7 @@ void Engine::upload_images(const double* images, int height, int width) {
     std::memcpy(h_img_, images, n * 8);
     PI0B_CUDA(cudaMemcpyAsync(d_img_, h_img_, n * 8, cudaMemcpyHostToDevice, stream_));
     PI0B_CUDA(launch_image_patches(d_img_, c.views, height, width, C, g * P, P, d_patches_, stream_));
+    PI0B_CUDA(cudaMemcpyAsync(d_patch_host_bf16_, h_flag_ + 0, sizeof(int), cudaMemcpyHostToDevice, stream_));
 }
 
 void Engine::run_ops(int part, cudaStream_t st) {
@@ -1466,7 +1638,7 @@ void Engine::run_ops(int part, cudaStream_t st) {
                                              op.stats, st));
                 break;
             case kOpF64Bf16:
-                PI0B_CUDA(launch_f64_to_bf16_rows(op.src64, op.rows, op.cols, op.dstb, op.ldb, st));
+                PI0B_CUDA(launch_f64_to_bf16_rows(op.src64, op.rows, op.cols, op.dstb, op.ldb, st, op.skip, op.srcb));
                 break;
             case kOpF32F64: PI0B_CUDA(launch_f32_to_f64(op.src32, op.ld32, op.rows, op.cols, op.dst64, st)); break;
             case kOpMemset: PI0B_CUDA(cudaMemsetAsync(op.mptr, 0, op.mbytes, st)); break;

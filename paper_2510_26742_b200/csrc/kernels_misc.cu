@@ -102,12 +102,15 @@ __global__ void rows_to_f32_kernel(const double* src, int rows, int cols, float*
     if (stats && lane == 0) stats[row] = ss;
 }
 
+// `host_bf16` (nullable): a device flag set when the host delivered the rows already converted,
+// packed in `srcb` (Engine::stage_patches_bf16: a quarter of the bytes cross PCIe); then this is
+// only the copy into the padded operand.
 __global__ void f64_to_bf16_rows_kernel(const double* src, int rows, int cols, __nv_bfloat16* dst,
-                                        long long ldd) {
+                                        long long ldd, const int* host_bf16, const __nv_bfloat16* srcb) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (long long)rows * cols) return;
     const int r = int(i / cols), c = int(i % cols);
-    dst[(long long)r * ldd + c] = __float2bfloat16_rn(float(src[i]));
+    dst[(long long)r * ldd + c] = (host_bf16 && *host_bf16) ? srcb[i] : __float2bfloat16_rn(float(src[i]));
 }
 
 __global__ void f32_to_f64_kernel(const float* src, long long lds, int rows, int cols, double* dst) {
@@ -209,9 +212,10 @@ cudaError_t launch_rows_to_f32(const double* src, int rows, int cols, float* dst
     return cudaGetLastError();
 }
 cudaError_t launch_f64_to_bf16_rows(const double* src, int rows, int cols, __nv_bfloat16* dst,
-                                    long long ldd, cudaStream_t st) {
+                                    long long ldd, cudaStream_t st, const int* host_bf16,
+                                    const __nv_bfloat16* srcb) {
     const long long n = (long long)rows * cols;
-    f64_to_bf16_rows_kernel<<<int((n + 255) / 256), 256, 0, st>>>(src, rows, cols, dst, ldd);
+    f64_to_bf16_rows_kernel<<<int((n + 255) / 256), 256, 0, st>>>(src, rows, cols, dst, ldd, host_bf16, srcb);
     return cudaGetLastError();
 }
 cudaError_t launch_f32_to_f64(const float* src, long long lds, int rows, int cols, double* dst,
