@@ -14,7 +14,10 @@ from paper_2510_26742_b200.config import default_config  # noqa: E402
 seconds = float(sys.argv[1]) if len(sys.argv) > 1 else 3.0
 cfg = default_config(views=2).replace(flow_steps=1)
 out = {"views": 2, "flow_steps_per_tick": 1, "seconds": seconds, "runs": []}
-for rate, policy in ((480.0, "most_recent"), (480.0, "frame_sticky"), (1290.0, "most_recent")):
+# the maximum comes from the reference simulator on this engine's stream numbers
+# (profiles/r01_streamsim_2v.json b200_max_feasible_rate_hz; 1440 Hz at the time of writing)
+max_rate = float(os.environ.get("PI0B_STREAM_MAX_HZ", "1440"))
+for rate, policy in ((480.0, "most_recent"), (480.0, "frame_sticky"), (max_rate, "most_recent")):
     r = E.stream_run(cfg, seconds, ae_rate=rate, kv_policy=policy)
     r.update({"ae_rate_target": rate, "kv_policy": policy})
     out["runs"].append(r)
