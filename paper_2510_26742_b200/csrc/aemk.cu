@@ -1395,15 +1395,19 @@ AePlan ae_plan(const AePlanInput& in) {
         return int(it.size());
     };
     // Split-K residual update: every (tile, k-range) task adds its partial into y.
+    // head_div > 0: per-head dependency -- the task waits on counter wbar + head / head_div
+    // (head = its first k-block / 4, 256-column heads) for head_cnt arrivals
     auto red_phase = [&](int wmat, int xmat, uint8_t xsrc, int rowoff, int kbt, int ks, int wbar, int wcnt, int sbar,
-                         int ncol = 64) {
+                         int ncol = 64, int head_div = 0, int head_cnt = 0) {
         std::vector<Item> it;
         const int per = (kbt + ks - 1) / ks;
         for (int t = 0; t < W / ncol; ++t)
             for (int k = 0; k < ks; ++k) {
                 const int kb0 = k * per, nkb = std::min(kbt, kb0 + per) - kb0;
                 if (nkb <= 0) continue;
-                AeTask x = gemm(xsrc, kEpiRed, wmat, xmat, rowoff, t, kb0, nkb, wbar, wcnt, sbar);
+                AeTask x = head_div ? gemm(xsrc, kEpiRed, wmat, xmat, rowoff, t, kb0, nkb, wbar + (kb0 / 4) / head_div,
+                                           head_cnt, sbar)
+                                    : gemm(xsrc, kEpiRed, wmat, xmat, rowoff, t, kb0, nkb, wbar, wcnt, sbar);
                 x.ncol = uint16_t(ncol);
                 it.push_back({x, nkb * kWB * ncol / 64});
             }
@@ -1435,7 +1439,14 @@ AePlan ae_plan(const AePlanInput& in) {
                                               bar_qkv, s, l)
                                  : full_phase(kXY, kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], in.mat_y, kbW, prev_bar,
                                               prev_cnt, bar_qkv, s, l);
+            // Attention signals one counter per head (pair) and each ae.proj task waits only for the
+            // key ranges of the head its k-blocks belong to (no extra release: one signal per task).
+            const int n_rb = in.attn_single ? in.heads : pairs;
+            const bool per_head = in.per_head_proj && (in.q_width / 64) % ks_proj == 0 &&
+                                  ((in.q_width / 64) / ks_proj) <= 4 && 4 % ((in.q_width / 64) / ks_proj) == 0;
             const int bar_attn = newbar();
+            if (per_head)
+                for (int h = 1; h < n_rb; ++h) newbar();  // bar_attn + rb
             {
                 std::vector<Item> it;
                 for (int rb = 0; rb < (in.attn_single ? in.heads : pairs); ++rb)
@@ -1450,7 +1461,7 @@ AePlan ae_plan(const AePlanInput& in) {
                         x.nkb = uint16_t(std::min(kBlocksPerSplit, in.key_blocks - j * kBlocksPerSplit));
                         x.wait_bar = uint16_t(bar_qkv);
                         x.wait_cnt = uint16_t(n_qkv);
-                        x.sig_bar = uint16_t(bar_attn);
+                        x.sig_bar = uint16_t(per_head ? bar_attn + rb : bar_attn);
                         x.step = uint16_t(s);
                         x.layer = uint16_t(l);
                         x.phase = uint16_t(phase);
@@ -1460,7 +1471,7 @@ AePlan ae_plan(const AePlanInput& in) {
             }
             const int bar_proj = newbar();
             const int n_proj = red_phase(in.mat_wproj[size_t(l)], 0, kXO, 0, in.q_width / 64, ks_proj, bar_attn, n_attn,
-                                         bar_proj, in.proj_ncol);
+                                         bar_proj, in.proj_ncol, per_head ? (in.attn_single ? 1 : 2) : 0, splits);
             const int bar_ffn = newbar();
             const bool pf = in.pair_ffn;  // the caller tiled mat_wffn for it (128-wide tiles)
             need(!pf || ((2 * MLP) % 128 == 0 && 2 * (2 * MLP / 128) <= in.num_ctas && in.num_ctas % 2 == 0), "ae.ffn pairs");
