@@ -1358,7 +1358,7 @@ AePlan ae_plan(const AePlanInput& in) {
     // A phase of full-K tiles split over K between the two CTAs of a cluster (CTAs 2c, 2c + 1):
     // the owner takes the first half of K and runs the epilogue, the helper the second half.
     auto pair_phase = [&](uint8_t epi, int tiles, int wmat, int xmat, int kbt, int wbar, int wcnt, int sbar, int step,
-                          int layer, bool sym = false) {
+                          int layer, bool sym = false, int sig_group = 0) {
         const int nclu = in.num_ctas / 2, h = kbt / 2;
         const double wscale = sym ? 2.0 : 1.0;  // sym tiles are 128 wide (16 KB k-blocks)
         std::vector<std::pair<double, int>> order;
@@ -1368,7 +1368,8 @@ AePlan ae_plan(const AePlanInput& in) {
             const int c = order[size_t(t % nclu)].second;
             const int own = 2 * c + ((t / nclu + phase) & 1);
             for (int r = 0; r < 2; ++r) {
-                AeTask x = gemm(kXY, epi, wmat, xmat, 0, t, r ? h : 0, r ? kbt - h : h, wbar, wcnt, sbar);
+                AeTask x = gemm(kXY, epi, wmat, xmat, 0, t, r ? h : 0, r ? kbt - h : h, wbar, wcnt,
+                                sig_group ? sbar + t / sig_group : sbar);
                 x.step = uint16_t(step);
                 x.layer = uint16_t(layer);
                 x.pair = uint16_t(sym ? (r ? 4 : 3) : (in.sym_qkv ? (r ? 6 : 5) : (r ? 2 : 1)));
@@ -1395,18 +1396,17 @@ AePlan ae_plan(const AePlanInput& in) {
         return int(it.size());
     };
     // Split-K residual update: every (tile, k-range) task adds its partial into y.
-    // head_div > 0: per-head dependency -- the task waits on counter wbar + head / head_div
-    // (head = its first k-block / 4, 256-column heads) for head_cnt arrivals
+    // group_kb > 0: grouped dependency -- the task waits on counter wbar + kb0 / group_kb (the
+    // producers of its k-blocks) for group_cnt arrivals instead of the whole producer phase
     auto red_phase = [&](int wmat, int xmat, uint8_t xsrc, int rowoff, int kbt, int ks, int wbar, int wcnt, int sbar,
-                         int ncol = 64, int head_div = 0, int head_cnt = 0) {
+                         int ncol = 64, int group_kb = 0, int group_cnt = 0) {
         std::vector<Item> it;
         const int per = (kbt + ks - 1) / ks;
         for (int t = 0; t < W / ncol; ++t)
             for (int k = 0; k < ks; ++k) {
                 const int kb0 = k * per, nkb = std::min(kbt, kb0 + per) - kb0;
                 if (nkb <= 0) continue;
-                AeTask x = head_div ? gemm(xsrc, kEpiRed, wmat, xmat, rowoff, t, kb0, nkb, wbar + (kb0 / 4) / head_div,
-                                           head_cnt, sbar)
+                AeTask x = group_kb ? gemm(xsrc, kEpiRed, wmat, xmat, rowoff, t, kb0, nkb, wbar + kb0 / group_kb, group_cnt, sbar)
                                     : gemm(xsrc, kEpiRed, wmat, xmat, rowoff, t, kb0, nkb, wbar, wcnt, sbar);
                 x.ncol = uint16_t(ncol);
                 it.push_back({x, nkb * kWB * ncol / 64});
@@ -1471,17 +1471,23 @@ AePlan ae_plan(const AePlanInput& in) {
             }
             const int bar_proj = newbar();
             const int n_proj = red_phase(in.mat_wproj[size_t(l)], 0, kXO, 0, in.q_width / 64, ks_proj, bar_attn, n_attn,
-                                         bar_proj, in.proj_ncol, per_head ? (in.attn_single ? 1 : 2) : 0, splits);
-            const int bar_ffn = newbar();
+                                         bar_proj, in.proj_ncol, per_head ? (in.attn_single ? 4 : 8) : 0, splits);
             const bool pf = in.pair_ffn;  // the caller tiled mat_wffn for it (128-wide tiles)
+            // ae.down tasks wait only for the ae.ffn tiles that produce their k-blocks (a 128-wide
+            // ffn tile T yields g columns [64 T, 64 T + 64) = down k-block T)
+            const int per_down = (MLP / 64) / std::max(1, ks_down);
+            const bool grp_down = pf && in.group_down && (MLP / 64) % ks_down == 0;
+            const int bar_ffn = newbar();
+            if (grp_down)
+                for (int g = 1; g < ks_down; ++g) newbar();  // bar_ffn + k-range
             need(!pf || ((2 * MLP) % 128 == 0 && 2 * (2 * MLP / 128) <= in.num_ctas && in.num_ctas % 2 == 0), "ae.ffn pairs");
             const int n_ffn = pf ? pair_phase(kEpiGate, 2 * MLP / 128, in.mat_wffn[size_t(l)], in.mat_y, kbW, bar_proj, n_proj,
-                                              bar_ffn, s, l, true)
+                                              bar_ffn, s, l, true, grp_down ? per_down : 0)
                                  : full_phase(kXY, kEpiGate, tiles_ffn, in.mat_wffn[size_t(l)], in.mat_y, kbW, bar_proj,
                                               n_proj, bar_ffn, s, l);
             const int bar_down = newbar();
             prev_cnt = red_phase(in.mat_wdown[size_t(l)], in.mat_g, kXBf16, 0, MLP / 64, ks_down, bar_ffn, n_ffn, bar_down,
-                                 in.down_ncol);
+                                 in.down_ncol, grp_down ? per_down : 0, 2 * per_down);
             if (rec) {
                 std::vector<Item> it;
                 AeTask x{};
