@@ -1358,7 +1358,7 @@ AePlan ae_plan(const AePlanInput& in) {
     // A phase of full-K tiles split over K between the two CTAs of a cluster (CTAs 2c, 2c + 1):
     // the owner takes the first half of K and runs the epilogue, the helper the second half.
     auto pair_phase = [&](uint8_t epi, int tiles, int wmat, int xmat, int kbt, int wbar, int wcnt, int sbar, int step,
-                          int layer, bool sym = false, int sig_group = 0) {
+                          int layer, bool sym = false) {
         const int nclu = in.num_ctas / 2, h = kbt / 2;
         const double wscale = sym ? 2.0 : 1.0;  // sym tiles are 128 wide (16 KB k-blocks)
         std::vector<std::pair<double, int>> order;
@@ -1368,8 +1368,7 @@ AePlan ae_plan(const AePlanInput& in) {
             const int c = order[size_t(t % nclu)].second;
             const int own = 2 * c + ((t / nclu + phase) & 1);
             for (int r = 0; r < 2; ++r) {
-                AeTask x = gemm(kXY, epi, wmat, xmat, 0, t, r ? h : 0, r ? kbt - h : h, wbar, wcnt,
-                                sig_group ? sbar + t / sig_group : sbar);
+                AeTask x = gemm(kXY, epi, wmat, xmat, 0, t, r ? h : 0, r ? kbt - h : h, wbar, wcnt, sbar);
                 x.step = uint16_t(step);
                 x.layer = uint16_t(layer);
                 x.pair = uint16_t(sym ? (r ? 4 : 3) : (in.sym_qkv ? (r ? 6 : 5) : (r ? 2 : 1)));
@@ -1441,6 +1440,8 @@ AePlan ae_plan(const AePlanInput& in) {
                                               prev_cnt, bar_qkv, s, l);
             // Attention signals one counter per head (pair) and each ae.proj task waits only for the
             // key ranges of the head its k-blocks belong to (no extra release: one signal per task).
+            // Safe for y: its readers before ae.proj's red.add (the ae.qkv tasks) all finished
+            // before any attention task started.
             const int n_rb = in.attn_single ? in.heads : pairs;
             const bool per_head = in.per_head_proj && (in.q_width / 64) % ks_proj == 0 &&
                                   ((in.q_width / 64) / ks_proj) <= 4 && 4 % ((in.q_width / 64) / ks_proj) == 0;
@@ -1473,21 +1474,17 @@ AePlan ae_plan(const AePlanInput& in) {
             const int n_proj = red_phase(in.mat_wproj[size_t(l)], 0, kXO, 0, in.q_width / 64, ks_proj, bar_attn, n_attn,
                                          bar_proj, in.proj_ncol, per_head ? (in.attn_single ? 4 : 8) : 0, splits);
             const bool pf = in.pair_ffn;  // the caller tiled mat_wffn for it (128-wide tiles)
-            // ae.down tasks wait only for the ae.ffn tiles that produce their k-blocks (a 128-wide
-            // ffn tile T yields g columns [64 T, 64 T + 64) = down k-block T)
-            const int per_down = (MLP / 64) / std::max(1, ks_down);
-            const bool grp_down = pf && in.group_down && (MLP / 64) % ks_down == 0;
+            // (ae.down waits for the whole ae.ffn phase: its red.add into y must not overtake any
+            // ae.ffn task still staging y)
             const int bar_ffn = newbar();
-            if (grp_down)
-                for (int g = 1; g < ks_down; ++g) newbar();  // bar_ffn + k-range
             need(!pf || ((2 * MLP) % 128 == 0 && 2 * (2 * MLP / 128) <= in.num_ctas && in.num_ctas % 2 == 0), "ae.ffn pairs");
             const int n_ffn = pf ? pair_phase(kEpiGate, 2 * MLP / 128, in.mat_wffn[size_t(l)], in.mat_y, kbW, bar_proj, n_proj,
-                                              bar_ffn, s, l, true, grp_down ? per_down : 0)
+                                              bar_ffn, s, l, true)
                                  : full_phase(kXY, kEpiGate, tiles_ffn, in.mat_wffn[size_t(l)], in.mat_y, kbW, bar_proj,
                                               n_proj, bar_ffn, s, l);
             const int bar_down = newbar();
             prev_cnt = red_phase(in.mat_wdown[size_t(l)], in.mat_g, kXBf16, 0, MLP / 64, ks_down, bar_ffn, n_ffn, bar_down,
-                                 in.down_ncol, grp_down ? per_down : 0, 2 * per_down);
+                                 in.down_ncol);
             if (rec) {
                 std::vector<Item> it;
                 AeTask x{};

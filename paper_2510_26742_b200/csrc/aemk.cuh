@@ -129,7 +129,6 @@ struct AePlanInput {
     bool sym_qkv = true;      // ae.qkv pairs exchange symmetrically (each CTA finalises half)
     bool attn_single = true;  // one attention task per (head, key range) instead of (head pair, range)
     bool per_head_proj = true;  // ae.proj tasks wait only for their head's attention key ranges
-    bool group_down = true;     // ae.down tasks wait only for the ae.ffn tiles of their k-blocks
     bool pair_ffn = true;  // ae.ffn as 128-wide tiles split over K, symmetric exchange (mat_wffn kTilePlain128)
     int mat_wst, mat_wap, mat_wao, mat_whead;
     std::vector<int> mat_wqkv, mat_wproj, mat_wffn, mat_wdown, mat_kv;

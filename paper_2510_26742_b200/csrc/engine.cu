@@ -1318,7 +1318,6 @@ void Engine::build_ae_mega() {
     in.attn_single = env_int("PI0B_AE_ATTN_SINGLE", 1) != 0;
     in.sym_qkv = env_int("PI0B_AE_SYM_QKV", 1) != 0;
     in.per_head_proj = env_int("PI0B_AE_HEAD_DEP", 1) != 0;
-    in.group_down = env_int("PI0B_AE_GROUP_DOWN", 1) != 0;
     in.pair_ffn = env_int("PI0B_AE_PAIR_FFN", 1) != 0 && (2 * MLP) % 128 == 0 && 2 * (2 * MLP / 128) <= num_sms_ &&
                   num_sms_ % 2 == 0;
     ae_cluster_ = in.pair_qkv || in.pair_ffn;  // pair tasks need the 2-CTA cluster launch
