@@ -87,6 +87,10 @@ int pi0b_engine_run_images(pi0b_engine* e, const double* images, int height, int
  * patch*patch*channels]. */
 int pi0b_image_patches(const double* images, int views, int height, int width, int channels, int side,
                        int patch, double* patches, void* stream);
+/* The host-side conversion run() applies to the patches before their DMA (host memory in and
+ * out, no GPU needed): dst[i] = bf16(float(src[i])), round-to-nearest-even at both steps, NaN ->
+ * 0x7fff -- bit-identical to the device conversion (__float2bfloat16_rn(float(x))). */
+int pi0b_f64_to_bf16_host(const double* src, long long n, uint16_t* dst);
 
 /* Streaming split of run(): the prefix (VE + LLM, fills the KV cache) and the action
  * expert (all flow steps against the cached prefix KV). */

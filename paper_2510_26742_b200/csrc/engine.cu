@@ -2094,6 +2094,12 @@ int pi0b_image_patches(const double* images, int views, int height, int width, i
                                           static_cast<cudaStream_t>(stream)));
 }
 
+int pi0b_f64_to_bf16_host(const double* src, long long n, uint16_t* dst) {
+    if ((!src || !dst) && n > 0) return pi0b::fail(EngineError(PI0B_E_INVALID, "null argument"));
+    for (long long i = 0; i < n; ++i) dst[i] = pi0b::host_bf16(src[i]);
+    return PI0B_OK;
+}
+
 int pi0b_stream_run(const pi0b_model_config* cfg, uint64_t seed, const pi0b_stream_options* opt, double seconds,
                     pi0b_stream_report* report) {
     if (!cfg || !opt || !report) return pi0b::fail(EngineError(PI0B_E_INVALID, "null argument"));

@@ -84,3 +84,35 @@ def test_cpp_dropin_fails_loudly_without_gpu():
         pass
     r = subprocess.run([demo, "1", "0"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 2 and "pi0b error" in r.stdout, r.stdout + r.stderr
+
+
+def _bf16_of_f32_rne(x64):
+    """numpy restatement of bf16(float(x)): fp64 -> fp32 round-to-nearest-even (numpy's cast),
+    then fp32 -> bf16 round-to-nearest-even on the bit pattern, NaN -> 0x7fff (cvt.rn.bf16.f32)."""
+    import numpy as np
+    u = x64.astype(np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    nan = (u & 0x7FFFFFFF) > 0x7F800000
+    r[nan] = 0x7FFF
+    return r
+
+
+def test_host_patch_conversion_matches_device_rounding():
+    """pi0b_f64_to_bf16_host (the conversion run() applies to the patches before their DMA) is
+    bf16(float(x)) with round-to-nearest-even at both steps: ties, values that round differently
+    via fp32 than directly, subnormals, infinities and NaN."""
+    import numpy as np
+    rng = np.random.default_rng(5)
+    x = np.concatenate([
+        rng.normal(size=20000), rng.uniform(-1, 1, 20000) * 1e-40, rng.normal(size=2000) * 1e30,
+        # exact bf16 ties (odd and even lower halves) and ties broken only by the fp64 tail
+        np.array([1.0 + 2.0 ** -8, 1.0 + 3 * 2.0 ** -8, 1.0 + 2.0 ** -8 + 2.0 ** -40, -(1.0 + 2.0 ** -8 - 2.0 ** -40),
+                  3.3895313892515355e38, 3.4e38, 1e39, -1e39, 0.0, -0.0, np.inf, -np.inf, np.nan, 1e-46]),
+    ])
+    out = np.empty(x.size, dtype=np.uint16)
+    rc = E.lib().pi0b_f64_to_bf16_host(x.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), x.size,
+                                       out.ctypes.data_as(ctypes.c_void_p))
+    assert rc == 0
+    with np.errstate(over="ignore"):
+        ref = _bf16_of_f32_rne(x)
+    assert np.array_equal(out, ref)
