@@ -92,6 +92,22 @@ int pi0b_image_patches(const double* images, int views, int height, int width, i
  * 0x7fff -- bit-identical to the device conversion (__float2bfloat16_rn(float(x))). */
 int pi0b_f64_to_bf16_host(const double* src, long long n, uint16_t* dst);
 
+/* ------------------------------------------------------------------ unfused checkpoints
+ * Weight rules for the naive graph (rtvla::build_pi0_graph_naive, proj/src/builder.cpp:369-541),
+ * host memory in and out, no GPU needed; bit-identical to rtvla::apply_weight_rules
+ * (proj/src/passes.cpp:692-790).  include/pi0b_rtvla.hpp fuse_naive() applies them to a whole
+ * naive WeightStore (the concatenations are plain copies there). */
+/* rtvla::time_embedding(step, dim, flow_steps) (proj/src/evaluate.cpp:23-36) -> out[dim]. */
+int pi0b_time_embedding(int step, int dim, int flow_steps, double* out);
+/* PremultiplyDiag (passes.cpp:706-721): w[k, m] row r *= gamma[r], in place. */
+int pi0b_premultiply_rows(double* w, int64_t k, int64_t m, const double* gamma);
+/* ComposeTimeFold (passes.cpp:754-785): the action time MLP (ae.act_in: w_act [act, width],
+ * b_act; ae.mlp_in: w_mix [t_dim + width, mix_cols], b_mix) folded into ae.action_proj:
+ * w_out [act, mix_cols] and its per-flow-step bias table table_out [flow_steps, mix_cols]. */
+int pi0b_fold_time_mlp(const double* w_act, int64_t act, int64_t width, const double* b_act, const double* w_mix,
+                       int64_t t_dim, int64_t mix_cols, const double* b_mix, int flow_steps, double* w_out,
+                       double* table_out);
+
 /* Streaming split of run(): the prefix (VE + LLM, fills the KV cache) and the action
  * expert (all flow steps against the cached prefix KV). */
 int pi0b_engine_run_prefix(pi0b_engine* e, const double* patches, const double* prompt);

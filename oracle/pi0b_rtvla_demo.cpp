@@ -77,7 +77,22 @@ int main(int argc, char** argv) {
             threw = true;
         }
         std::printf("non-pi0 graph rejected with rtvla::ShapeError: %s\n", threw ? "yes" : "no");
-        return (da < 0.05 && db < 0.05 && ds < 0.02 && threw) ? 0 : 1;
+        // a WeightStore missing a node / an instance / the bias table is refused with
+        // rtvla::NumericError, as rtvla::evaluate refuses it (proj/src/evaluate.cpp:96-99)
+        int refused = 0;
+        for (int v = 0; v < 3; ++v) {
+            rtvla::WeightStore bad = w;
+            if (v == 0) bad.by_node.erase("ae.ffn");
+            if (v == 1) bad.by_node.at("llm.down").w.pop_back();
+            if (v == 2) bad.by_node.at("ae.action_proj").bias_table = rtvla::Tensor();
+            try {
+                pi0b::Engine e3(g, bad);
+            } catch (const rtvla::NumericError&) {
+                ++refused;
+            }
+        }
+        std::printf("incomplete WeightStores refused with rtvla::NumericError: %d of 3\n", refused);
+        return (da < 0.05 && db < 0.05 && ds < 0.02 && threw && refused == 3) ? 0 : 1;
     } catch (const std::exception& e) {
         std::printf("pi0b error: %s\n", e.what());
         return 2;

@@ -15,7 +15,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr"] + os.environ.get("PI0B_NVCC_EXTRA", "").split()
-SOURCES = ["gemm.cu", "skinny.cu", "fattn.cu", "aemk.cu", "kernels_misc.cu", "engine.cu", "capi.cu"]
+SOURCES = ["gemm.cu", "skinny.cu", "fattn.cu", "aemk.cu", "kernels_misc.cu", "engine.cu", "capi.cu", "naive.cu"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:

@@ -263,6 +263,11 @@ struct NodeWeights {
     std::vector<__nv_bfloat16*> w;
     std::vector<float*> b;
     float* table = nullptr;
+    // what has been loaded (per instance; the bias table): launch() refuses to run on any
+    // entry never written, as the reference throws NumericError("no weights for node ...")
+    // (proj/src/evaluate.cpp:96-99) instead of reading zeroed / uninitialised memory
+    std::vector<char> loaded;
+    bool table_loaded = false;
 };
 
 struct Checkpoint {
@@ -411,7 +416,8 @@ public:
     std::string describe() const;
     void ae_trace(void* tasks, unsigned long long* stamps, long long cap, int* ctas, int* stride);
     cudaStream_t stream() const { return stream_; }
-    bool weights_ready() const { return weights_loaded_; }
+    bool weights_ready() const { return missing_weights().empty(); }
+    std::string missing_weights() const;
 
 private:
     template <typename T>
@@ -442,7 +448,7 @@ private:
     cudaStream_t stream_ = nullptr;
     std::vector<void*> allocs_;
     std::map<std::string, NodeWeights> W_;
-    bool weights_loaded_ = false;
+    bool weights_checked_ = false;
 
     // dims
     int T_ = 0, P_ = 0, L_ = 0, S_ = 0, C_ = 0, FS_ = 0;
@@ -1485,8 +1491,22 @@ void Engine::gen_weights(uint64_t seed) {
                                             seed_hash(seed, id, uint64_t(s), 4), -lim, lim, stream_));
     }
     PI0B_CUDA(cudaStreamSynchronize(stream_));
-    weights_loaded_ = true;
+    for (auto& kv : W_) {
+        kv.second.loaded.assign(size_t(kv.second.instances), 1);
+        kv.second.table_loaded = kv.second.has_table;
+    }
     ae_tiles_dirty_ = true;
+}
+
+std::string Engine::missing_weights() const {
+    for (const auto& kv : W_) {
+        const NodeWeights& nw = kv.second;
+        for (int i = 0; i < nw.instances; ++i)
+            if (size_t(i) >= nw.loaded.size() || !nw.loaded[size_t(i)])
+                return "no weights for node '" + kv.first + "' instance " + std::to_string(i);
+        if (nw.has_table && !nw.table_loaded) return "no bias table for node '" + kv.first + "'";
+    }
+    return {};
 }
 
 void Engine::set_weight(const std::string& id, long long inst, const double* w, long long k, long long m,
@@ -1514,7 +1534,8 @@ void Engine::set_weight(const std::string& id, long long inst, const double* w, 
         PI0B_CUDA(cudaMemcpyAsync(nw.b[size_t(inst)], b.data(), size_t(m) * 4, cudaMemcpyHostToDevice, stream_));
         PI0B_CUDA(cudaStreamSynchronize(stream_));
     }
-    weights_loaded_ = true;
+    if (nw.loaded.size() != size_t(nw.instances)) nw.loaded.assign(size_t(nw.instances), 0);
+    nw.loaded[size_t(inst)] = 1;
     ae_tiles_dirty_ = true;
 }
 
@@ -1527,6 +1548,7 @@ void Engine::set_bias_table(const std::string& id, const double* t, long long ro
     for (size_t i = 0; i < f.size(); ++i) f[i] = float(t[i]);
     PI0B_CUDA(cudaMemcpyAsync(it->second.table, f.data(), f.size() * 4, cudaMemcpyHostToDevice, stream_));
     PI0B_CUDA(cudaStreamSynchronize(stream_));
+    it->second.table_loaded = true;
 }
 
 // ------------------------------------------------------------------ execution
@@ -1691,7 +1713,11 @@ void Engine::capture(int part, int slot) {
 
 // part: 0 = full, 1 = prefix, 2 = action (C-ABI numbering)
 void Engine::launch(int part, cudaStream_t st) {
-    if (!weights_loaded_) throw EngineError(PI0B_E_STATE, "weights not loaded");
+    if (!weights_checked_) {  // every (node, instance, bias table) written at least once
+        const std::string miss = missing_weights();
+        if (!miss.empty()) throw EngineError(PI0B_E_STATE, "weights not loaded: " + miss);
+        weights_checked_ = true;
+    }
     if (ae_mega_ && ae_tiles_dirty_) {  // (re)build the tile-contiguous AE weight copies
         for (const TiledW& tw : ae_tiled_) PI0B_CUDA(launch_tile_weight(tw.src, tw.rows, tw.k, tw.ldk, tw.dst, tw.order, stream_));
         PI0B_CUDA(cudaStreamSynchronize(stream_));

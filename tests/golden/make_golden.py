@@ -2,13 +2,21 @@
 
 * tiny_1v.json, mid_{1v,2v,3v32p}.json — actions from the compiled UNMODIFIED reference
   (``rtvla::evaluate`` via oracle/_ref/librtvla_ref.so), seed 1 for weights and inputs.
+* sketch_{1v,2v,3v32p}.npz — full-scale per-layer hidden-state "sketches": a fixed subset of
+  rows (tests/_util.py sketch_rows) of every SURVEY.md 8(c) checkpoint, in fp32, from the
+  bitwise-equal restatement: ve.fc2[0..26], llm.proj_in, llm.qkv[l] K|V columns [2048,2560)
+  (the KV cache), llm.down[l], ae.down at every layer of flow steps 0 and 9 and the last
+  layer of every step, ae.head[s].  The GPU tests assert cosine >= 0.999 on each.
 * full_1v.json, full_2v.json — full-scale actions from the fp64 restatement
   (oracle/pi0_oracle.cpp, bitwise equal to the reference on every config the tests can
   afford to run through the reference), cross-checked against the reference's own
   full-scale run recorded in SURVEY.md 8(c) / BASELINE.md 3 (y[0], y[1], y[last], sum,
   sum|y| at 17 significant digits); generation aborts if they disagree.
 
-Usage:  PYTHONPATH=. python tests/golden/make_golden.py [tiny mid full1 full2 full3]
+* full_3v32p.json — restatement actions, checked element for element against the reference's
+  own full-scale run (ref_full_3v32p.json from ref_full_run.py, ~40 min single-threaded).
+
+Usage:  PYTHONPATH=. python tests/golden/make_golden.py [tiny mid full1 full2 full3 sketch1 sketch2 sketch3]
 """
 import json
 import os
@@ -22,6 +30,9 @@ sys.path.insert(0, ROOT)
 
 from oracle import oracle as O  # noqa: E402
 from paper_2510_26742_b200.config import default_config, mid_config, tiny_config  # noqa: E402
+
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from _util import sketch_checkpoints, sketch_take  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
@@ -73,8 +84,37 @@ def main(which):
     if "full3" in which:
         cfg = default_config(views=3, prompt_tokens=32)
         x = O.gen_inputs(cfg, 1)
+        t = time.time()
         y, _ = O.port_forward(cfg, x)
-        dump("full_3v32p.json", cfg, y, "pi0_oracle restatement")
+        dt = time.time() - t
+        ref_path = os.path.join(HERE, "ref_full_3v32p.json")
+        ref = json.load(open(ref_path))
+        r = np.array(ref["actions"]).reshape(y.shape)
+        if not np.array_equal(r, y):
+            raise SystemExit(f"full 3v32p: restatement != reference, max |d| {np.abs(r - y).max():.3e}")
+        dump("full_3v32p.json", cfg, y, "pi0_oracle restatement (bitwise == reference rtvla::evaluate, "
+             "ref_full_3v32p.json)", {"restatement_seconds": dt,
+                                      "reference_evaluate_seconds": ref["evaluate_seconds"]})
+    for views, prompt, key in [(1, 0, "sketch1"), (2, 0, "sketch2"), (3, 32, "sketch3")]:
+        if key not in which:
+            continue
+        cfg = default_config(views=views, prompt_tokens=prompt)
+        x = O.gen_inputs(cfg, 1)
+        cks = sketch_checkpoints(cfg)
+        t = time.time()
+        y, recs = O.port_forward(cfg, x, record=[(n, i, shape) for (n, i, shape, _) in cks])
+        dt = time.time() - t
+        arrays = {"actions": y.astype(np.float64)}
+        for (node, inst, shape, cols) in cks:
+            arrays[f"{node}[{inst}]"] = sketch_take(recs[(node, inst)], cols).astype(np.float32)
+        tag = f"{views}v" + (f"{prompt}p" if prompt else "")
+        gold = os.path.join(HERE, f"full_{tag}.json")
+        if os.path.exists(gold):   # the sketch's forward must be the golden forward
+            g = np.array(json.load(open(gold))["actions"]).reshape(y.shape)
+            if not np.array_equal(g, y):
+                raise SystemExit(f"sketch {tag}: actions differ from {gold}")
+        np.savez_compressed(os.path.join(HERE, f"sketch_{tag}.npz"), **arrays)
+        print(f"wrote sketch_{tag}.npz ({len(arrays) - 1} checkpoints, {dt:.0f} s)")
 
 
 if __name__ == "__main__":

@@ -1,6 +1,8 @@
 """Multi-process host logic of bench.py's N > 1 path on CPU (gloo, world size 2): the timing
-reduction is the max over ranks, the reported throughput aggregates the replicas, and the
-reference arm runs on rank 0 only (the other ranks exit 0 without work)."""
+reduction is the max over ranks, `bench.py --gpus N` outside torchrun re-launches itself with N
+ranks through the same launcher the driver uses, WORLD_SIZE != --gpus is refused, no NCCL
+communicator is created, and the reference arm runs on rank 0 only (the other ranks exit 0
+without work)."""
 import json
 import os
 import socket
@@ -62,3 +64,27 @@ def test_reference_arm_rank1_exits_without_work():
                         "--warmup", "3"], capture_output=True, text=True, timeout=120, env=env, cwd=ROOT)
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip() == ""
+
+
+def test_bench_gpus_n_spawns_replicas_over_gloo():
+    """The real launcher path: no WORLD_SIZE in the environment, --gpus 2 -> torch.distributed.run
+    with 2 ranks -> gloo group -> max/min over ranks printed by rank 0 only."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launch-check"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    doc = json.loads(lines[0])
+    assert doc["world_size"] == 2
+    assert doc["max"] == [1.0, 11.0] and doc["min"] == [0.0]
+    assert doc["nccl_initialized"] is False
+    assert doc["staging_threads"] >= 0
+
+
+def test_bench_world_size_must_match_gpus():
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--launch-check"],
+                       capture_output=True, text=True, timeout=120, env=env, cwd=ROOT)
+    assert r.returncode != 0
+    assert "WORLD_SIZE=2 but --gpus 4" in (r.stderr + r.stdout)

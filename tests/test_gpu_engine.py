@@ -13,7 +13,7 @@ import os
 import numpy as np
 import pytest
 
-from _util import bf16_bits_from_f64, cosine, rel_err
+from _util import bf16_bits_from_f64, cosine, rel_err, sketch_checkpoints, sketch_take
 from oracle import oracle as O
 from paper_2510_26742_b200 import engine as E
 from paper_2510_26742_b200.config import default_config, mid_config
@@ -180,21 +180,61 @@ def test_engine_rejects_bad_inputs():
         eng.set_weight("ve.qkv", 99, np.zeros((cfg.ve_width, 3 * cfg.ve_width)), np.zeros(3 * cfg.ve_width))
 
 
-@pytest.mark.parametrize("views", [1, 2])
-def test_full_scale_actions_match_reference_golden(views):
-    """Full-scale pi0 (seed 1) vs the reference's fp64 output (tests/golden/full_{v}v.json,
-    generated by tests/golden/make_golden.py through the compiled reference)."""
-    path = os.path.join(GOLDEN, f"full_{views}v.json")
-    gold = json.load(open(path))
+def _record_parity(tag, doc):
+    """Measured errors go to $PI0B_PARITY_OUT/<tag>.json (copied under profiles/ per round)."""
+    out = os.environ.get("PI0B_PARITY_OUT")
+    if out:
+        os.makedirs(out, exist_ok=True)
+        with open(os.path.join(out, f"{tag}.json"), "w") as f:
+            json.dump(doc, f, indent=1)
+
+
+FULL_CONFIGS = [(1, 0, "1v"), (2, 0, "2v"), (3, 32, "3v32p")]
+
+
+@pytest.mark.parametrize("views,prompt,tag", FULL_CONFIGS)
+def test_full_scale_actions_match_reference_golden(views, prompt, tag):
+    """Full-scale pi0 (seed 1) vs the reference's fp64 output (tests/golden/full_<tag>.json,
+    generated by tests/golden/make_golden.py and pinned to the compiled reference's own
+    full-scale run), through the default (graph-replay) engine."""
+    gold = json.load(open(os.path.join(GOLDEN, f"full_{tag}.json")))
     ref = np.array(gold["actions"], dtype=np.float64).reshape(63, 32)
-    cfg = default_config(views=views)
+    cfg = default_config(views=views, prompt_tokens=prompt)
     x = O.gen_inputs(cfg, 1)
     eng = E.Engine(cfg)
     eng.gen_weights(1)
-    y = eng.run(x["patches"], x["state"], x["noise"])
+    y = eng.run(x["patches"], x["state"], x["noise"], x.get("prompt"))
     rep = _action_report(y, ref)
-    print(f"full {views}v actions", rep)
+    print(f"full {tag} actions", rep)
+    _record_parity(f"actions_{tag}", rep)
     assert rep["max_abs"] < ACT_MAX_ABS and rep["rel"] < ACT_REL and rep["cos"] > 0.9995, rep
+
+
+@pytest.mark.parametrize("views,prompt,tag", FULL_CONFIGS)
+def test_full_scale_per_layer_cosine(views, prompt, tag):
+    """North star: per-layer hidden-state cosine >= 0.999 at FULL scale, across all 225 serial
+    layers' checkpoints of SURVEY.md 8(c) (ve.fc2[0..26], llm.proj_in, the KV cache
+    llm.qkv[l][:, 2048:2560], llm.down[l], ae.down of flow steps 0 and 9 and the last layer of
+    every step, ae.head[s]) against the committed fp64 sketches (tests/golden/sketch_<tag>.npz:
+    fixed row subsets of the bitwise-equal restatement's hidden states)."""
+    sk = np.load(os.path.join(GOLDEN, f"sketch_{tag}.npz"))
+    cfg = default_config(views=views, prompt_tokens=prompt)
+    x = O.gen_inputs(cfg, 1)
+    eng = E.Engine(cfg, record_checkpoints=True)
+    eng.gen_weights(1)
+    y = eng.run(x["patches"], x["state"], x["noise"], x.get("prompt"))
+    cos = {}
+    for node, inst, shape, cols in sketch_checkpoints(cfg):
+        key = f"{node}[{inst}]"
+        cos[key] = cosine(sketch_take(eng.checkpoint(node, inst, *shape), cols), sk[key])
+    rep = _action_report(y, sk["actions"])
+    worst = sorted(cos.items(), key=lambda kv: kv[1])[:8]
+    print(f"full {tag}: {len(cos)} checkpoints, worst {worst}, actions {rep}")
+    _record_parity(f"layers_{tag}", {"checkpoints": len(cos), "min_cos": min(cos.values()), "worst": worst,
+                                     "cos": cos, "actions": rep})
+    assert len(cos) == len(sk.files) - 1
+    bad = {k: v for k, v in cos.items() if v < LAYER_COS}
+    assert not bad, bad
 
 
 DEMO = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "pi0b_rtvla_demo")
@@ -216,8 +256,9 @@ def test_rtvla_cpp_dropin(views, prompt):
 @pytest.mark.parametrize("views,prompt", [(1, 0), (3, 32)])
 def test_rtvla_cpp_naive_graph(views, prompt):
     """SURVEY 8(f) f1: an unfused graph (rtvla::build_pi0_graph_naive: separate q/k/v, RMSNorm gamma,
-    time MLP) and its WeightStore through pi0b::evaluate_naive -- fused on the host by the
-    reference's own passes and weight rules -- vs rtvla::evaluate on the naive graph."""
+    time MLP) and its WeightStore through pi0b::evaluate_naive -- fused on the host by the engine's
+    own weight rules (pi0b::fuse_naive; bitwise == rtvla::apply_weight_rules, test_adaptor_cpu.py)
+    -- vs rtvla::evaluate on the naive graph."""
     import subprocess
     if not os.path.exists(DEMO):
         pytest.skip("oracle/_ref/pi0b_rtvla_demo not built (needs /root/reference at build time)")
