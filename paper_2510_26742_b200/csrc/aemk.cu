@@ -135,27 +135,8 @@ PI0B_DEV void st_cluster_v4(uint32_t addr, float4 v) {
 PI0B_DEV void st_cluster_f32(uint32_t addr, float v) {
     asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
-// Asynchronous remote store that completes `bytes` of the transaction count of a barrier in the
-// destination CTA (no release fence needed: the owner's barrier wait makes the data visible).
-PI0B_DEV void st_async_v4(uint32_t addr, float4 v, uint32_t mbar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
-                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(mbar)
-                 : "memory");
-}
-PI0B_DEV void st_async_f32(uint32_t addr, float v, uint32_t mbar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(addr), "f"(v), "r"(mbar)
-                 : "memory");
-}
 PI0B_DEV void mbar_arrive_remote(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-PI0B_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
 }
 PI0B_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // Arrive on `bar` when all of this thread's prior cp.async copies have landed.

@@ -6,6 +6,7 @@
 // `ae.vcat` (proj/src/builder.cpp:321-329) are consumed without materialising the concat.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
 
@@ -29,6 +30,14 @@ struct AttnParams {
     int kv_splits;            // grid.y = key splits (1, 2, 4, 8): a (1, S, 1) cluster per q tile,
                               // partials combined over DSMEM (no workspace)
     int kv_per_split;         // informational: keys per split
+};
+
+// Tensor maps of one attention launch (fattn.cu make_fattn_maps): Q [q_rows, heads*d] and the two
+// key / value segments [rows, kv_heads*d], bf16, boxes of 64 columns x 32 (Q; K/V of two segments)
+// or 64 rows (K/V of one segment), 128-byte swizzle.
+struct FaMaps {
+    CUtensorMap q, k0, v0, k1, v1;
+    int kv_box;  // key rows per K/V box: 64 (one key segment) or 32 (a tile may straddle two)
 };
 
 }  // namespace pi0b

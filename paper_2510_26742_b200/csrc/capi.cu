@@ -18,9 +18,6 @@ namespace pi0b {
 cudaError_t gemm_configure();
 cudaError_t launch_gemm(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                         cudaStream_t stream);
-struct FaMaps {
-    CUtensorMap k0, v0, k1, v1;
-};
 cudaError_t fattn_configure();
 FaMaps make_fattn_maps(const AttnParams& p, int head_dim);
 cudaError_t launch_fattn(int head_dim, const FaMaps& maps, const AttnParams& p, cudaStream_t stream);

@@ -47,9 +47,6 @@ namespace pi0b {
 cudaError_t gemm_configure();
 cudaError_t launch_gemm(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                         cudaStream_t stream);
-struct FaMaps {
-    CUtensorMap k0, v0, k1, v1;
-};
 cudaError_t fattn_configure();
 FaMaps make_fattn_maps(const AttnParams& p, int head_dim);
 cudaError_t launch_fattn(int head_dim, const FaMaps& maps, const AttnParams& p, cudaStream_t stream);
@@ -819,10 +816,12 @@ void Engine::add_attn(int part, const std::string& node, int inst, int hd, AttnP
         for (char& ch : key) ch = ch == '.' ? '_' : char(std::toupper(static_cast<unsigned char>(ch)));
         const int base = ((ap.heads / ap.kv_heads) * ap.q_rows + 127) / 128 * ap.kv_heads;
         const int tiles = (ap.rows0 + ap.rows1 + 63) / 64;
+        // measured (scripts/fa_trace.py, 2 views): the split combine (DSMEM) costs more than the
+        // key tiles it saves -- ve.attn 10.5 us at S = 1 vs 11.0 at S = 2, llm.attn 13.6 vs 14.6 /
+        // 14.9 at S = 2 / 4 -- so one CTA per q tile unless PI0B_ATTN_SPLITS says otherwise
         int S = 1;
-        // measured: splits pay only for grids below half the SMs, and clusters of 8 are slow
-        // (llm.attn 2v: 15.9 -> 13.8 us at S = 4, 37.8 us at S = 8; ve.attn slower at S = 2)
-        while (S < 4 && 2 * base <= num_sms_ / 2 && base * S * 2 <= num_sms_ && tiles >= S * 4) S *= 2;
+        (void)base;
+        (void)tiles;
         S = env_int(("PI0B_ATTN_SPLITS_" + key).c_str(), env_int("PI0B_ATTN_SPLITS", S));
         ap.kv_splits = (S == 2 || S == 4 || S == 8) ? S : 1;
     }

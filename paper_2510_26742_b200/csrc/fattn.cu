@@ -1,6 +1,7 @@
 // tcgen05 flash attention: S = Q K^T and O += P V on the 5th-gen tensor cores with both
-// accumulators in TMEM; the online softmax runs one query row per thread straight out of
-// TMEM (no shuffles), and P goes back through shared memory as the A operand of the PV MMA.
+// accumulators in TMEM; the online softmax runs out of TMEM with two threads per query row (eight
+// softmax warps: warps w and w + 4 share TMEM lane quarter w % 4 and split each 64-key tile), and
+// P goes back through shared memory as the A operand of the PV MMA.
 //
 // Semantics are the reference `Evaluator::attention` (proj/src/evaluate.cpp:225-252): per head
 // softmax(Q_h K_{h%kvh}^T / sqrt(d)) V, no mask, keys = rows of [segment 0 ; segment 1]
@@ -8,15 +9,19 @@
 // as query rows; a CTA owns 128 stacked rows.  The running maximum is only moved (and O in
 // TMEM rescaled) when it grows by more than 2^8, so O is almost never touched between tiles.
 //
-// Warps 0-3: softmax + epilogue, thread t = query row t = TMEM lane t (they also stage Q).
-// Warp 4: TMEM allocator + single-thread MMA issuer.  Warp 5: TMA producer for K and V.
+// Warps 0-7: softmax + epilogue (row R = 32 (w % 4) + lane, key half / O column half w / 4).
+// Warp 8: TMEM allocator + single-thread MMA issuer.  Warp 9: TMA producer for Q, K and V.
 // Shared-memory operand layouts are the 128-byte-swizzle UMMA layouts (1024-byte aligned
 // regions, 16-byte chunk c of row r at (c ^ (r & 7))):
-//   Q  [128 rows x DK]   K-major, one 16 KB region per 64 columns of d      (cp.async)
+//   Q  [128 rows x DK]   K-major, one 16 KB region per 64 columns of d      (TMA, 32-row boxes)
 //   K  [64 keys  x DK]   K-major B operand of QK^T (N = keys), 8 KB per 64 d (TMA)
 //   V  [64 keys  x DV]   same bytes, consumed MN-major as B of PV (N = d)    (TMA)
 //   P  [128 rows x 64]   K-major A operand of PV                             (st.shared)
 // Key tiles are fetched as 32-row TMA boxes so a tile may straddle the two key segments.
+// Key splits (grid.y = S, one (1, S, 1) cluster per q tile): split y owns rows [y 128/S, +128/S)
+// of the tile; the other splits push their normalised partials and (max, sum) into its drained
+// K ring with st.async (complete_tx on its receive barrier), and it combines them.
+// The output tile is staged in shared memory and written with coalesced 16-byte stores.
 #include "attention.cuh"
 #include "ptx.cuh"
 
@@ -28,7 +33,7 @@ namespace {
 
 constexpr int kFaRows = 128;
 constexpr int kFaKeys = 64;
-constexpr int kFaThreads = 192;
+constexpr int kFaThreads = 320;  // 8 softmax warps, MMA warp, TMA warp
 
 PI0B_DEV uint64_t desc_kmajor(uint32_t saddr) {
     uint64_t d = 0;
@@ -66,9 +71,26 @@ PI0B_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;
 
 }  // namespace
 
-struct FaMaps {
-    CUtensorMap k0, v0, k1, v1;  // [rows, kv_heads*D] bf16, box {64 cols, 32 rows}, 128B swizzle
-};
+// Timeline instrumentation (variant builds only, -DPI0B_FA_TRACE; scripts/fa_trace.py): 16
+// globaltimer stamps per CTA into the buffer set by pi0b_fa_trace_buffer().
+#ifdef PI0B_FA_TRACE
+__device__ unsigned long long* g_fa_trace;
+#define FA_STAMP(i)                                                                                      \
+    do {                                                                                                 \
+        if (g_fa_trace) {                                                                                \
+            unsigned long long t_;                                                                       \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                       \
+            g_fa_trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16 + (i)] = t_; \
+        }                                                                                                \
+    } while (0)
+extern "C" int pi0b_fa_trace_buffer(unsigned long long* p) {
+    return int(cudaMemcpyToSymbol(g_fa_trace, &p, sizeof(p)));
+}
+#else
+#define FA_STAMP(i) \
+    do {            \
+    } while (0)
+#endif
 
 // D = real head dim, DK = QK contraction (D padded to 16), DV = PV width (D padded to 64),
 // KK / KV = key / value ring depths.
@@ -80,23 +102,25 @@ struct FaCfg {
     static constexpr int K_BYTES = QA * kFaKeys * 128;
     static constexpr int V_BYTES = VA * kFaKeys * 128;
     static constexpr int P_BYTES = kFaRows * 128;  // one P buffer; two are allocated
-    static constexpr int SMEM = Q_BYTES + KK * K_BYTES + KV * V_BYTES + 2 * P_BYTES + 256 + 1024;
+    static constexpr int XCH_BYTES = 2 * 2 * kFaRows * 4;  // [2 tiles][2 halves][128 rows] row maxima
+    static constexpr int SMEM = Q_BYTES + KK * K_BYTES + KV * V_BYTES + 2 * P_BYTES + XCH_BYTES + 256;
     static constexpr int TMEM_S = 0;  // two 64-column S buffers
     static constexpr int TMEM_O = 128;
     static constexpr int TMEM_COLS = 128 + DV <= 256 ? 256 : 512;
+    static constexpr int ROW_BYTES = DV * 2;  // staged bf16 output row
+    static_assert(Q_BYTES >= kFaRows * ROW_BYTES, "output staging fits the Q region");
 };
 
 template <int D, int DK, int DV, int KK, int KV>
 __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_constant__ FaMaps maps, const AttnParams p) {
     using C = FaCfg<D, DK, DV, KK, KV>;
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t raw = smem_u32(smem_raw);
-    uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sQ = smem;
     uint8_t* sK = sQ + C::Q_BYTES;
     uint8_t* sV = sK + KK * C::K_BYTES;
     uint8_t* sP = sV + KV * C::V_BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES);
+    float* xch = reinterpret_cast<float*>(sP + 2 * C::P_BYTES);  // [2][2][128]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES + C::XCH_BYTES);
     uint64_t* k_full = bars;            // [KK]
     uint64_t* k_empty = k_full + KK;    // [KK]
     uint64_t* v_full = k_empty + KK;    // [KV]
@@ -105,23 +129,30 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
     uint64_t* s_free = s_full + 2;      // [2]
     uint64_t* p_full = s_free + 2;      // [2] per P buffer
     uint64_t* o_done = p_full + 2;      // [2] PV of tile t done (buffer t & 1 free again)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+    uint64_t* q_full = o_done + 2;      // Q tiles landed (TMA)
+    uint64_t* q_ready = q_full + 1;     // Q padding columns cleared (D % 16 != 0)
+    uint64_t* peers_free = q_ready + 1; // key splits: every peer's K ring drained and armed
+    uint64_t* recv_full = peers_free + 1;  // key splits: the peers' partials of this CTA's rows landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_full + 1);
 
     const int tid = threadIdx.x, warp = __shfl_sync(0xffffffff, tid >> 5, 0), lane = tid & 31;
+    if (tid == 0) FA_STAMP(0);
     const int qt = blockIdx.x, grp = blockIdx.z;
     const int hpg = p.heads / p.kv_heads;
     const int grows = hpg * p.q_rows;
     const int kvh = grp;
     const int total = p.rows0 + p.rows1;
     // Key split (grid.y = S, launched as a (1, S, 1) cluster): this CTA takes key tiles
-    // [t0, t0 + ntiles); the partial outputs are combined over DSMEM at the end.
-    const int S = gridDim.y;
+    // [t0, t0 + ntiles) and finalises rows [y * 128 / S, (y + 1) * 128 / S) of the q tile.
+    const int S = gridDim.y, y = int(blockIdx.y);
     const int ntiles_all = (total + kFaKeys - 1) / kFaKeys;
     const int tps = (ntiles_all + S - 1) / S;
-    const int t0 = int(blockIdx.y) * tps;
+    const int t0 = y * tps;
     const int ntiles = max(0, min(ntiles_all, t0 + tps) - t0);
+    const int own_rows = kFaRows / S;
 
     if (tid == 0) {
+        if (smem_u32(smem) & 1023u) __trap();  // SW128 operand regions need 1024-byte alignment
         for (int s = 0; s < KK; ++s) {
             mbar_init(&k_full[s], 1);
             mbar_init(&k_empty[s], 1);
@@ -132,42 +163,54 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&s_full[s], 1);
-            mbar_init(&s_free[s], 128);
-        }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&p_full[s], 128);
+            mbar_init(&s_free[s], 256);
+            mbar_init(&p_full[s], 256);
             mbar_init(&o_done[s], 1);
         }
+        mbar_init(q_full, 1);
+        mbar_init(q_ready, 128);
+        mbar_init(peers_free, S > 1 ? S - 1 : 1);
+        mbar_init(recv_full, 1);
         fence_barrier_init();
     }
-    if (warp == 4) tmem_alloc(tmem_slot, C::TMEM_COLS);
+    if (warp == 8) tmem_alloc(tmem_slot, C::TMEM_COLS);
     if (tid == 0) pdl_launch_dependents();
-    pdl_wait();  // every input (Q, K, V) is the previous kernel's output
-    if (warp < 4) {
-        // Q: thread r stages its own stacked row (DK/8 chunks) into the swizzled layout
-        const int r = tid, g = qt * kFaRows + r;
-        const __nv_bfloat16* qrow = p.q;
-        const bool row_ok = g < grows;
-        if (row_ok) qrow = p.q + (long long)(g % p.q_rows) * p.ldq + (kvh + p.kv_heads * (g / p.q_rows)) * D;
-#pragma unroll
-        for (int c = 0; c < DK / 8; ++c) {
-            const bool ok = row_ok && c * 8 < D;
-            cp_async16(sQ + (c >> 3) * (kFaRows * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4), ok ? qrow + c * 8 : p.q,
-                       ok);
-        }
-        cp_async_commit();
-        cp_async_wait<0>();
-        fence_proxy_async();
-    }
     tc_fence_before();
-    __syncthreads();
+    if (S > 1) cluster_sync_all();  // peers' barriers initialised before any remote arrive
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (tid == 0) FA_STAMP(2);
 
-    if (warp == 5) {
+    if (warp == 9) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
+            pdl_wait();  // Q, K, V are the previous kernel's outputs
+            FA_STAMP(1);
+            // Q: 32-row boxes (q_rows % 32 == 0, so a box never straddles two stacked heads)
+            int qbytes = 0;
+            for (int b = 0; b < kFaRows / 32; ++b)
+                if (qt * kFaRows + b * 32 < grows) qbytes += 32 * 128 * C::QA;
+            mbar_arrive_expect_tx(q_full, uint32_t(qbytes));
+            for (int b = 0; b < kFaRows / 32; ++b) {
+                const int g0 = qt * kFaRows + b * 32;
+                if (g0 >= grows) break;
+                const int head = kvh + p.kv_heads * (g0 / p.q_rows), row0 = g0 % p.q_rows;
+                for (int a = 0; a < C::QA; ++a)
+                    tma_load_2d(sQ + a * (kFaRows * 128) + b * 32 * 128, &maps.q, q_full, head * D + a * 64, row0,
+                                kEvictNormal);
+            }
             auto load_rows = [&](bool is_v, uint8_t* dst_tile, int t, int regions) {
+                uint64_t* bar = is_v ? &v_full[t % KV] : &k_full[t % KK];
+                if (maps.kv_box == 64) {
+                    // one key segment: the whole 64-key tile is one box per region (8 KB boxes:
+                    // ~85 GB/s of TMA ingest per SM against ~60 for 32-row boxes; rows past the
+                    // segment are zero-filled)
+                    const CUtensorMap* m = is_v ? &maps.v0 : &maps.k0;
+                    for (int a = 0; a < regions; ++a)
+                        tma_load_2d(dst_tile + a * (kFaKeys * 128), m, bar, kvh * D + a * 64, (t0 + t) * kFaKeys, kEvictLast);
+                    return;
+                }
                 // two 32-key boxes per region; each box lies in one key segment (or fully OOB -> zeros)
                 for (int half = 0; half < 2; ++half) {
                     const int j = (t0 + t) * kFaKeys + half * 32;
@@ -175,10 +218,10 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                     const CUtensorMap* m = seg0 ? (is_v ? &maps.v0 : &maps.k0) : (is_v ? &maps.v1 : &maps.k1);
                     const int row = seg0 ? j : j - p.rows0;
                     for (int a = 0; a < regions; ++a)
-                        tma_load_2d(dst_tile + a * (kFaKeys * 128) + half * 32 * 128, m,
-                                    is_v ? &v_full[t % KV] : &k_full[t % KK], kvh * D + a * 64, row, kEvictLast);
+                        tma_load_2d(dst_tile + a * (kFaKeys * 128) + half * 32 * 128, m, bar, kvh * D + a * 64, row, kEvictLast);
                 }
             };
+            FA_STAMP(10);
             for (int t = 0; t < ntiles; ++t) {
                 mbar_wait(&k_empty[t % KK], ((t / KK) & 1) ^ 1);
                 mbar_arrive_expect_tx(&k_full[t % KK], C::K_BYTES);
@@ -189,12 +232,13 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             }
         }
         __syncwarp();
-    } else if (warp == 4) {
+    } else if (warp == 8) {
         // ------------------------------------------------------------ MMA issuer
         {  // warp-uniform loop; one elected lane issues (see gemm.cu)
             constexpr uint32_t idesc_qk = umma_idesc_bf16(kFaRows, kFaKeys);
             constexpr uint32_t idesc_pv = umma_idesc_bf16(kFaRows, DV) | (1u << 16);  // B (V) MN-major
             const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK), v0 = smem_u32(sV), p0 = smem_u32(sP);
+            mbar_wait(q_ready, 0);
             auto issue_qk = [&](int t) {
                 const int st = t % KK, sb = t & 1;
                 mbar_wait(&k_full[st], (t / KK) & 1);
@@ -213,6 +257,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                 __syncwarp();
             };
             if (ntiles > 0) issue_qk(0);
+            if (lane == 0) FA_STAMP(11);
             for (int t = 0; t < ntiles; ++t) {
                 if (t + 1 < ntiles) issue_qk(t + 1);
                 const int sv = t % KV;
@@ -235,30 +280,49 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
         __syncwarp();
     } else {
         // ------------------------------------------------------------ softmax + epilogue
-        const int r = tid;
+        const int qd = warp & 3, hf = warp >> 2;  // TMEM lane quarter, key / O-column half
+        const int r = qd * 32 + lane;
         const int g = qt * kFaRows + r;
         const bool row_ok = g < grows;
-        const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
+        const uint32_t trow = tmem + (uint32_t(qd * 32) << 16);
+        const uint32_t pair_bar = 1 + qd;  // named barrier of warps qd and qd + 4 (64 threads)
+        mbar_wait(q_full, 0);  // (also orders every thread after the producer's pdl_wait)
+        if (hf == 0) {
+            // Q columns D..DK of the last region belong to the next head (or are OOB zeros): clear
+            // them so the QK contraction over DK = D rounded up to 16 sees only this head.
+            if constexpr (D % 64 != 0 && D < DK) {
+                constexpr int a = D / 64, c0 = (D % 64) / 8, c1 = (DK - 64 * a + 7) / 8;
+#pragma unroll
+                for (int c = c0; c < c1; ++c)
+                    *reinterpret_cast<uint4*>(sQ + a * (kFaRows * 128) + r * 128 + ((c ^ (r & 7)) << 4)) = make_uint4(0u, 0u, 0u, 0u);
+                fence_proxy_async();
+            }
+            mbar_arrive(q_ready);
+        }
         float m_ref = -INFINITY, l = 0.f;
         for (int t = 0; t < ntiles; ++t) {
             const int sb = t & 1;
             mbar_wait(&s_full[sb], (t >> 1) & 1);
+            if (tid == 0 && t == 0) FA_STAMP(3);
             tc_fence_after();
-            float s0[32], s1[32];
-            tmem_ld32(trow + C::TMEM_S + sb * 64, s0);
-            tmem_ld32(trow + C::TMEM_S + sb * 64 + 32, s1);
+            float sv[32];
+            tmem_ld32(trow + C::TMEM_S + sb * 64 + hf * 32, sv);
             tc_fence_before();
             mbar_arrive(&s_free[sb]);
-            const int kbase = (t0 + t) * kFaKeys;
+            const int kbase = (t0 + t) * kFaKeys + hf * 32;
             float mx = -INFINITY;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                s0[j] = kbase + j < total ? s0[j] * p.scale_log2 : -INFINITY;
-                s1[j] = kbase + 32 + j < total ? s1[j] * p.scale_log2 : -INFINITY;
-                mx = fmaxf(mx, fmaxf(s0[j], s1[j]));
+                sv[j] = kbase + j < total ? sv[j] * p.scale_log2 : -INFINITY;
+                mx = fmaxf(mx, sv[j]);
             }
+            // row max over both key halves (the partner thread is in warp w ^ 4)
+            xch[(sb * 2 + hf) * kFaRows + r] = mx;
+            named_bar_sync(pair_bar, 64);
+            mx = fmaxf(xch[(sb * 2) * kFaRows + r], xch[(sb * 2 + 1) * kFaRows + r]);
             // P is double-buffered: buffer t & 1 is free once PV(t - 2) is done; O may only be
-            // rescaled once PV(t - 1) is done (rare: lazy rescale)
+            // rescaled once PV(t - 1) is done (rare: lazy rescale).  Both threads of a row make
+            // the same decisions (same maxima).
             float factor = 1.f;
             const bool grow = mx > m_ref + 8.f;
             if (grow) {
@@ -275,136 +339,195 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             }
             if (rescale) {
 #pragma unroll 1
-                for (int c = 0; c < DV / 32; ++c) {
+                for (int c = 0; c < DV / 64; ++c) {
                     float o[32];
-                    tmem_ld32(trow + C::TMEM_O + c * 32, o);
+                    tmem_ld32(trow + C::TMEM_O + hf * (DV / 2) + c * 32, o);
 #pragma unroll
                     for (int j = 0; j < 32; ++j) o[j] *= factor;
-                    tmem_st32(trow + C::TMEM_O + c * 32, o);
+                    tmem_st32(trow + C::TMEM_O + hf * (DV / 2) + c * 32, o);
                 }
             }
             float ls = 0.f;
-            uint32_t pk[32];
+            uint32_t pk[16];
 #pragma unroll
             for (int j = 0; j < 32; j += 2) {
-                const float a0 = ex2_fast(s0[j] - m_ref), a1 = ex2_fast(s0[j + 1] - m_ref);
-                const float b0 = ex2_fast(s1[j] - m_ref), b1 = ex2_fast(s1[j + 1] - m_ref);
-                ls += a0 + a1 + b0 + b1;
+                const float a0 = ex2_fast(sv[j] - m_ref), a1 = ex2_fast(sv[j + 1] - m_ref);
+                ls += a0 + a1;
                 pk[j / 2] = pack_bf16(a0, a1);
-                pk[16 + j / 2] = pack_bf16(b0, b1);
             }
             l += ls;
-            uint8_t* prow = sP + (t & 1) * C::P_BYTES + r * 128;
+            uint8_t* prow = sP + sb * C::P_BYTES + r * 128;
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-                *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) =
+            for (int c = 0; c < 4; ++c)
+                *reinterpret_cast<uint4*>(prow + (((hf * 4 + c) ^ (r & 7)) << 4)) =
                     make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
             fence_proxy_async();
             tc_fence_before();
-            mbar_arrive(&p_full[t & 1]);
+            mbar_arrive(&p_full[sb]);
         }
-        // epilogue: O / l -> bf16
+        if (tid == 0) FA_STAMP(4);
+        // row sum over both halves (exchange slot of a tile two back: free, see the max exchange)
+        {
+            const int xb = ntiles & 1;
+            xch[(xb * 2 + hf) * kFaRows + r] = l;
+            named_bar_sync(pair_bar, 64);
+            l = xch[(xb * 2) * kFaRows + r] + xch[(xb * 2 + 1) * kFaRows + r];
+        }
         if (ntiles > 0) mbar_wait(&o_done[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
         tc_fence_after();
-        const float il = l > 0.f ? 1.f / l : 0.f;
-        if (S > 1) {
-            // park this split's normalised partial (bf16, row r at r * DV * 2, 16-byte chunks
-            // swizzled by r & 7) in the now idle K ring, (m, l) in the P buffers
-            uint8_t* prow = sK + r * (DV * 2);
+        if (tid == 0) FA_STAMP(5);
+        // This thread's output columns: [hf * DV / 2, (hf + 1) * DV / 2) of row r, as 16-byte
+        // chunks q of the staged row (bf16, row r at r * ROW_BYTES, chunk q at (q ^ (r & 7))).
+        constexpr int HC = DV / 2 / 8;  // chunks per half row
+        auto stage_row = [&](int row, const float* o, int c32, float scale) {
+            uint8_t* srow = sQ + row * C::ROW_BYTES;
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+                const int q = hf * HC + (c32 * 32 + j) / 8;
+                *reinterpret_cast<uint4*>(srow + ((q ^ (row & 7)) << 4)) =
+                    make_uint4(pack_bf16(o[j] * scale, o[j + 1] * scale), pack_bf16(o[j + 2] * scale, o[j + 3] * scale),
+                               pack_bf16(o[j + 4] * scale, o[j + 5] * scale), pack_bf16(o[j + 6] * scale, o[j + 7] * scale));
+            }
+        };
+        int row_lo = 0, row_hi = kFaRows;  // rows this CTA writes out
+        if (S == 1) {
+            const float il = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll 1
-            for (int c = 0; c < DV / 32; ++c) {
+            for (int c = 0; c < DV / 64; ++c) {
                 float o[32];
-                if (ntiles > 0) tmem_ld32(trow + C::TMEM_O + c * 32, o);
+                if (ntiles > 0) tmem_ld32(trow + C::TMEM_O + hf * (DV / 2) + c * 32, o);
                 else
 #pragma unroll
                     for (int j = 0; j < 32; ++j) o[j] = 0.f;
+                stage_row(r, o, c, il);
+            }
+        } else {
+            // ---------------- key-split combine (push form)
+            // Every split stages the normalised partial rows it does not own (bf16) and their
+            // (max, sum) in its drained V ring, one contiguous block per owner; one thread then
+            // bulk-copies each block into the owner's drained K ring (DSMEM, complete_tx on the
+            // owner's recv_full).  Block = own_rows rows of ROW_BYTES (16-byte chunk q of local
+            // row i at q ^ (i & 7)) followed by own_rows (max, sum) pairs.
+            row_lo = y * own_rows;
+            row_hi = row_lo + own_rows;
+            const int blk = own_rows * (C::ROW_BYTES + 8);
+            auto slot_of = [&](int sender, int owner_rank) { return sender < owner_rank ? sender : sender - 1; };
+            if (tid == 0) {
+                // this CTA's K ring is drained (all MMAs done): arm the receive barrier, then
+                // let the peers push
+                mbar_arrive_expect_tx(recv_full, uint32_t((S - 1) * blk));
+                for (int k = 0; k < S; ++k)
+                    if (k != y) mbar_arrive_cluster(mapa_shared(smem_u32(peers_free), uint32_t(k)));
+            }
+            const int owner = r / own_rows, lrow = r - owner * own_rows;
+            // TMEM reads stay warp-converged (tcgen05.ld is .sync.aligned; with 8+ splits a warp
+            // spans two owners): every thread stages its normalised partial, into the outgoing
+            // block of its row's owner or, for its own rows, into the idle half of the Q region.
+            const float il = l > 0.f ? 1.f / l : 0.f;
+            uint8_t* ob = owner != y ? sV + slot_of(owner, y) * blk                              // outgoing
+                                     : sQ + (row_lo < kFaRows / 2 ? kFaRows / 2 : 0) * C::ROW_BYTES;  // own
+#pragma unroll 1
+            for (int c = 0; c < DV / 64; ++c) {
+                float o[32];
+                if (ntiles > 0) tmem_ld32(trow + C::TMEM_O + hf * (DV / 2) + c * 32, o);
+                else
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) o[j] = 0.f;  // a split without keys never reads TMEM
 #pragma unroll
                 for (int j = 0; j < 32; j += 8) {
-                    uint4 u;
-                    u.x = pack_bf16(o[j] * il, o[j + 1] * il);
-                    u.y = pack_bf16(o[j + 2] * il, o[j + 3] * il);
-                    u.z = pack_bf16(o[j + 4] * il, o[j + 5] * il);
-                    u.w = pack_bf16(o[j + 6] * il, o[j + 7] * il);
-                    *reinterpret_cast<uint4*>(prow + ((((c * 32 + j) >> 3) ^ (r & 7)) << 4)) = u;
+                    const int q = hf * HC + (c * 32 + j) / 8;
+                    *reinterpret_cast<uint4*>(ob + lrow * C::ROW_BYTES + ((q ^ (lrow & 7)) << 4)) =
+                        make_uint4(pack_bf16(o[j] * il, o[j + 1] * il), pack_bf16(o[j + 2] * il, o[j + 3] * il),
+                                   pack_bf16(o[j + 4] * il, o[j + 5] * il), pack_bf16(o[j + 6] * il, o[j + 7] * il));
                 }
             }
-            reinterpret_cast<float2*>(sP)[r] = make_float2(l > 0.f ? m_ref : -INFINITY, l);
-        }
-        __nv_bfloat16* orow = p.out;
-        if (row_ok) orow = p.out + (long long)(g % p.q_rows) * p.ldo + (kvh + p.kv_heads * (g / p.q_rows)) * D;
-#pragma unroll 1
-        for (int c = 0; c < (S > 1 ? 0 : DV / 32); ++c) {
-            float o[32];
-            tmem_ld32(trow + C::TMEM_O + c * 32, o);
-            if (row_ok) {
+            if (owner != y && hf == 0)
+                reinterpret_cast<float2*>(ob + own_rows * C::ROW_BYTES)[lrow] = make_float2(l > 0.f ? m_ref : -INFINITY, l);
+            fence_proxy_async();  // generic-proxy stores -> the bulk copy engine
+            named_bar_sync(6, 256);
+            if (tid == 0) {
+                mbar_wait_cluster(peers_free, 0);
+                for (int k = 0; k < S; ++k) {
+                    if (k == y) continue;
+                    const uint32_t dst = mapa_shared(smem_u32(sK + slot_of(y, k) * blk), uint32_t(k));
+                    const uint32_t bar = mapa_shared(smem_u32(recv_full), uint32_t(k));
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                        "r"(smem_u32(sV + slot_of(k, y) * blk)), "r"(uint32_t(blk)), "r"(bar)
+                        : "memory");
+                }
+                FA_STAMP(7);
+            }
+            if (owner == y) {
+                mbar_wait_cluster(recv_full, 0);
+                // o = sum_j w_j O_j / sum_j w_j over the S normalised partials, w_j = l_j 2^(m_j - M)
+                const float m_own = l > 0.f ? m_ref : -INFINITY;
+                auto ml_of = [&](int k) {
+                    return k == y ? make_float2(m_own, l)
+                                  : reinterpret_cast<const float2*>(sK + slot_of(k, y) * blk + own_rows * C::ROW_BYTES)[lrow];
+                };
+                float M = -INFINITY;
+                for (int k = 0; k < S; ++k) M = fmaxf(M, ml_of(k).x);
+                float wk[8], den = 0.f;
 #pragma unroll
-                for (int j = 0; j < 32; j += 8) {
-                    if (c * 32 + j < D) {
-                        uint4 u;
-                        u.x = pack_bf16(o[j] * il, o[j + 1] * il);
-                        u.y = pack_bf16(o[j + 2] * il, o[j + 3] * il);
-                        u.z = pack_bf16(o[j + 4] * il, o[j + 5] * il);
-                        u.w = pack_bf16(o[j + 6] * il, o[j + 7] * il);
-                        *reinterpret_cast<uint4*>(orow + c * 32 + j) = u;
+                for (int k = 0; k < 8; ++k) {
+                    wk[k] = 0.f;
+                    if (k < S) {
+                        const float2 v = ml_of(k);
+                        wk[k] = v.y > 0.f ? v.y * exp2f(v.x - M) : 0.f;
+                        den += wk[k];
                     }
                 }
-            }
-        }
-    }
-    if (S > 1) {
-        // Combine the S key splits of this q tile: CTA y of the cluster finalises rows
-        // [y * 128 / S, (y + 1) * 128 / S): o = sum_j w_j O_j / sum_j w_j, w_j = l_j 2^(m_j - M),
-        // reading the peers' parked partials over DSMEM.
-        cluster_sync_all();
-        const int rows = kFaRows / S, r0 = int(blockIdx.y) * rows;
-        float* wts = reinterpret_cast<float*>(sQ);  // [rows][S] normalised weights (Q is idle)
-        for (int i = tid; i < rows; i += kFaThreads) {
-            const int r = r0 + i;
-            float m[8], l[8], M = -INFINITY, den = 0.f;
-            for (int j = 0; j < S; ++j) {
-                const float4 v = ld_dsmem_f32x4(mapa_shared(smem_u32(sP) + (r & ~1) * 8, j));
-                m[j] = (r & 1) ? v.z : v.x;
-                l[j] = (r & 1) ? v.w : v.y;
-                M = fmaxf(M, m[j]);
-            }
-            for (int j = 0; j < S; ++j) {
-                const float w = l[j] > 0.f ? l[j] * exp2f(m[j] - M) : 0.f;
-                m[j] = w;
-                den += w;
-            }
-            for (int j = 0; j < S; ++j) wts[i * S + j] = den > 0.f ? m[j] / den : 0.f;
-        }
-        __syncthreads();
-        constexpr int CH = DV / 8;  // 16-byte chunks per row
-        for (int it = tid; it < rows * CH; it += kFaThreads) {
-            const int i = it / CH, c = it % CH, r = r0 + i;
-            const int g = qt * kFaRows + r;
-            if (g >= grows || c * 8 >= D) continue;
-            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            const uint32_t off = smem_u32(sK) + r * (DV * 2) + ((c ^ (r & 7)) << 4);
-            for (int j = 0; j < S; ++j) {
-                const float w = wts[i * S + j];
-                const float4 v = ld_dsmem_f32x4(mapa_shared(off, j));
-                const uint32_t u[4] = {__float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z), __float_as_uint(v.w)};
+                const float iden = den > 0.f ? 1.f / den : 0.f;
+#pragma unroll 1
+                for (int c = 0; c < DV / 64; ++c) {
+                    float o[32];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    acc[2 * e] += w * __uint_as_float(u[e] << 16);
-                    acc[2 * e + 1] += w * __uint_as_float(u[e] & 0xffff0000u);
+                    for (int j = 0; j < 32; ++j) o[j] = 0.f;
+#pragma unroll 1
+                    for (int k = 0; k < S; ++k) {
+                        const uint8_t* src = (k == y ? ob : sK + slot_of(k, y) * blk) + lrow * C::ROW_BYTES;
+#pragma unroll
+                        for (int j = 0; j < 32; j += 8) {
+                            const int q = hf * HC + (c * 32 + j) / 8;
+                            const uint4 u = *reinterpret_cast<const uint4*>(src + ((q ^ (lrow & 7)) << 4));
+                            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                o[j + 2 * e] += wk[k] * __uint_as_float(w4[e] << 16);
+                                o[j + 2 * e + 1] += wk[k] * __uint_as_float(w4[e] & 0xffff0000u);
+                            }
+                        }
+                    }
+                    stage_row(r, o, c, iden);
                 }
+                if (tid == y * own_rows) FA_STAMP(8);
             }
-            __nv_bfloat16* orow = p.out + (long long)(g % p.q_rows) * p.ldo + (kvh + p.kv_heads * (g / p.q_rows)) * D;
-            uint4 o;
-            o.x = pack_bf16(acc[0], acc[1]);
-            o.y = pack_bf16(acc[2], acc[3]);
-            o.z = pack_bf16(acc[4], acc[5]);
-            o.w = pack_bf16(acc[6], acc[7]);
-            *reinterpret_cast<uint4*>(orow + c * 8) = o;
         }
-        cluster_sync_all();  // peers are done reading this CTA's parked partial
+        if (tid == 0) FA_STAMP(6);
+        // coalesced copy-out of the staged rows [row_lo, row_hi): D bf16 of each row
+        named_bar_sync(5, 256);
+        if (tid == 0) FA_STAMP(12);
+        constexpr int CPR = (D * 2 + 15) / 16;  // 16-byte chunks per output row
+        const int n = (row_hi - row_lo) * CPR;
+        for (int e = tid; e < n; e += 256) {
+            const int rr = row_lo + e / CPR, q = e % CPR;
+            const int gg = qt * kFaRows + rr;
+            if (gg >= grows) continue;
+            const uint4 v = *reinterpret_cast<const uint4*>(sQ + rr * C::ROW_BYTES + ((q ^ (rr & 7)) << 4));
+            __nv_bfloat16* orow = p.out + (long long)(gg % p.q_rows) * p.ldo + (kvh + p.kv_heads * (gg / p.q_rows)) * D;
+            *reinterpret_cast<uint4*>(orow + q * 8) = v;
+        }
+        if (tid == 0) FA_STAMP(13);
+        (void)row_ok;
     }
+    // Key splits: the bulk copies read this CTA's V ring after its softmax threads moved on; the
+    // cluster barrier (every owner has seen its recv_full) keeps all sources alive until then.
     tc_fence_before();
-    __syncthreads();
-    if (warp == 4) tmem_dealloc(tmem, C::TMEM_COLS);
+    if (S > 1) cluster_sync_all();
+    else __syncthreads();
+    if (tid == 0) FA_STAMP(9);
+    if (warp == 8) tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
 CUtensorMap make_tmap_bf16(const void* base, long long rows, long long cols, long long ld, int box_rows);
@@ -426,9 +549,12 @@ cudaError_t fattn_configure() {
 // Tensor maps for one attention launch (built once at plan time).
 FaMaps make_fattn_maps(const AttnParams& p, int head_dim) {
     FaMaps m;
+    m.q = make_tmap_bf16(p.q, p.q_rows, (long long)p.heads * head_dim, p.ldq, 32);
     const long long width = (long long)p.kv_heads * head_dim;
-    m.k0 = make_tmap_bf16(p.k0, p.rows0, width, p.ld0, 32);
-    m.v0 = make_tmap_bf16(p.v0, p.rows0, width, p.ld0, 32);
+    const bool one_seg = p.rows1 == 0 || !p.k1;
+    m.kv_box = one_seg ? 64 : 32;
+    m.k0 = make_tmap_bf16(p.k0, p.rows0, width, p.ld0, m.kv_box);
+    m.v0 = make_tmap_bf16(p.v0, p.rows0, width, p.ld0, m.kv_box);
     const bool has1 = p.rows1 > 0 && p.k1;
     m.k1 = make_tmap_bf16(has1 ? p.k1 : p.k0, has1 ? p.rows1 : p.rows0, width, has1 ? p.ld1 : p.ld0, 32);
     m.v1 = make_tmap_bf16(has1 ? p.v1 : p.v0, has1 ? p.rows1 : p.rows0, width, has1 ? p.ld1 : p.ld0, 32);
@@ -470,7 +596,7 @@ cudaError_t launch_fattn(int head_dim, const FaMaps& maps, const AttnParams& p, 
     const int S = p.kv_splits > 1 ? p.kv_splits : 1;
     if (S != 1 && S != 2 && S != 4 && S != 8) return cudaErrorInvalidValue;
     const dim3 grid((grows + kFaRows - 1) / kFaRows, S, p.kv_heads);
-    if ((p.rows0 % 32) || (p.rows1 % 32)) return cudaErrorInvalidValue;
+    if ((p.rows0 % 32) || (p.rows1 % 32) || (p.q_rows % 32)) return cudaErrorInvalidValue;
     switch (head_dim) {
         case 72: return fa_launch_t<72, 80, 128, 3, 3>(maps, p, grid, stream);
         case 256: return fa_launch_t<256, 256, 256, 2, 2>(maps, p, grid, stream);

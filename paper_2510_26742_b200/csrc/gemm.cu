@@ -27,6 +27,27 @@
 
 namespace pi0b {
 
+// Timeline instrumentation (variant builds only, -DPI0B_GEMM_TRACE; scripts/gemm_trace.py): 16
+// globaltimer stamps per CTA into the buffer set by pi0b_gemm_trace_buffer().
+#ifdef PI0B_GEMM_TRACE
+__device__ unsigned long long* g_gm_trace;
+#define GM_STAMP(i)                                                                                      \
+    do {                                                                                                 \
+        if (g_gm_trace) {                                                                                \
+            unsigned long long t_;                                                                       \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                       \
+            g_gm_trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16 + (i)] = t_; \
+        }                                                                                                \
+    } while (0)
+extern "C" int pi0b_gemm_trace_buffer(unsigned long long* p) {
+    return int(cudaMemcpyToSymbol(g_gm_trace, &p, sizeof(p)));
+}
+#else
+#define GM_STAMP(i) \
+    do {            \
+    } while (0)
+#endif
+
 constexpr int BM = 128;
 #ifndef PI0B_PAIR_STAGES
 #define PI0B_PAIR_STAGES 7
@@ -133,12 +154,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint64_t* empty = full + STAGES;
     uint64_t* accum_full = empty + STAGES;   // [2] (double-buffered accumulator when persistent)
     uint64_t* accum_empty = accum_full + 2;  // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_empty + 2);
+    // split-K push combine: peers_free completes when every peer's pipeline smem is drained (and its
+    // recv_full armed); recv_full when the peers' partials of this CTA's chunks have landed
+    uint64_t* peers_free = accum_empty + 2;
+    uint64_t* recv_full = peers_free + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_full + 1);
     int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
     float* sm_vec = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::BAR_BYTES);
 
     const int warp = __shfl_sync(0xffffffff, int(threadIdx.x >> 5), 0);  // warp-uniform (see below)
     const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) GM_STAMP(0);
     // Persistent mode (p.persist, no split-K): CTA b walks tiles b, b + grid, ... (m fastest, so
     // CTAs running together share weight tiles in L2) with the accumulator double-buffered in
     // TMEM: the epilogue of tile j overlaps the mainloop of tile j + 1.
@@ -177,6 +203,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             mbar_init(&accum_full[b], 1);
             mbar_init(&accum_empty[b], CG);
         }
+        mbar_init(peers_free, p.splits > 1 ? p.splits - 1 : 1);
+        mbar_init(recv_full, 1);
         fence_barrier_init();
     }
     const int tmem_cols = (persist ? NBUF : 1) * MT * Cfg::TMEM_COLS;
@@ -189,9 +217,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) GM_STAMP(1);
 
     if (threadIdx.x == 0) pdl_launch_dependents();
     const int S = p.splits;  // cluster size along K (grid.z)
+    // split-K combine by st.async pushes into the peers' drained pipeline smem (see the epilogue)
+    const bool push = S > 1 && S * (BN / 32) * 16384 <= STAGES * Cfg::STAGE_BYTES;
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
@@ -236,6 +267,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         load_b(i, (kb0 + i) * BK);
                     }
                     pdl_wait();
+                    GM_STAMP(2);
                     for (int i = 0; i < pre; ++i) load_a(i, (kb0 + i) * BK);
                     i0 = pre;
                     g = pre;
@@ -252,7 +284,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
         }
         __syncwarp();
-        if (S > 1) {
+        if (S > 1 && !push) {
             cluster_sync_all();
             cluster_sync_all();
         }
@@ -274,6 +306,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     const int s = g % STAGES;
                     const uint32_t ph = (g / STAGES) & 1;
                     mbar_wait(&full[s], ph);
+                    if (lane == 0 && i == 0 && j == 0) GM_STAMP(3);
                     tc_fence_after();
                     const uint64_t ad = umma_desc_sw128(sA + s * Cfg::A_BYTES);
                     const uint64_t bd = umma_desc_sw128(sB + s * Cfg::B_BYTES);
@@ -301,7 +334,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
         }
         __syncwarp();
-        if (S > 1) {
+        if (S > 1 && !push) {
             cluster_sync_all();
             cluster_sync_all();
         }
@@ -334,30 +367,76 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         pdl_wait();
         float rs = 1.0f;
         if ((p.flags & kFlagRowScale) && valid) rs = 1.0f / sqrtf(p.row_stats[r] * p.inv_width + p.eps);
+        constexpr int NC = BN / 32;                 // 32-column chunks in the tile
+        constexpr int NP = NC / 2;                  // (c, c + NP) pairs
+        const int NU = kPaired ? NP : NC;           // epilogue units: chunks, or chunk pairs
+        // Split-K: unit u belongs to cluster rank u % S.
+        const int rank = split;
+        const int u_first = S > 1 ? rank + S * hsel : hsel * (NU / 2);
+        const int u_step = S > 1 ? 2 * S : 1;
+        const int u_end = S > 1 ? NU : u_first + NU / 2;
+        // Residual base of this thread's first unit (the previous kernel's output, independent
+        // of the accumulator): loaded now so its L2 latency overlaps the mainloop.
+        float hpre[32];
+        if constexpr (MODE == kModeResid) {
+            const int col0 = n0 + u_first * 32;
+            if (valid && u_first < u_end && col0 < p.N)
+                load_f32x32(reinterpret_cast<const float*>(p.out) + (long long)r * p.ldo + col0, hpre, min(32, p.N - col0),
+                            false);
+        }
         named_bar_sync(1, 256);
 
         if (MT == 1) mbar_wait(&accum_full[j % NBUF], (j / NBUF) & 1);
         tc_fence_after();
+        if (etid == 0 && j == 0) GM_STAMP(4);
 
-        constexpr int NC = BN / 32;                 // 32-column chunks in the tile
-        constexpr int NP = NC / 2;                  // (c, c + NP) pairs
-        const int NU = kPaired ? NP : NC;           // epilogue units: chunks, or chunk pairs
-        // Split-K: unit u belongs to cluster rank u % S.  Chunk c of row r is parked at
-        // stage + c*16 KB + r*128 B, 16-byte pieces XOR-swizzled by r (conflict-free).
-        const int rank = split;
+        // Split-K combine, push form (S * NC chunks of 16 KB fit in the drained pipeline smem):
+        // as soon as its own MMAs are done a CTA arms its receive barrier and tells the peers its
+        // pipeline smem is free; once all peers are free it st.asyncs the partials of the chunks
+        // it does not own straight from TMEM into the owners' smem (slot [sender rank][chunk],
+        // 128 B per row, 16-byte pieces XOR-swizzled by row), then waits for its own chunks'
+        // partials -- no cluster-wide barrier and no remote loads on the critical path.
+        // Otherwise (larger splits) the chunks are parked locally and pulled over DSMEM.
         const uint32_t srow = smem_u32(smem) + row_in_tile * 128;
         const int sw = row_in_tile & 7;
-        if (S > 1) {
+        auto owner_of = [&](int c) { return (kPaired ? c % NP : c) % S; };
+        if (S > 1 && push) {
+            if (etid == 0) {
+                int owned = 0;
+                for (int c = 0; c < NC; ++c) owned += owner_of(c) == rank;
+                mbar_arrive_expect_tx(recv_full, uint32_t((S - 1) * owned * 16384));
+                for (int k = 0; k < S; ++k)
+                    if (k != rank) mbar_arrive_cluster(mapa_shared(smem_u32(peers_free), uint32_t(k)));
+            }
+            mbar_wait_cluster(peers_free, 0);
 #pragma unroll 1
             for (int c = hsel * (NC / 2); c < (hsel + 1) * (NC / 2); ++c) {
-                if ((kPaired ? c % NP : c) % S == rank) continue;
+                const int own = owner_of(c);
+                if (own == rank) continue;
+                float v[32];
+                tmem_ld32(trow + c * 32, v);
+                const uint32_t dst = mapa_shared(srow + uint32_t((rank * NC + c) * 16384), uint32_t(own));
+                const uint32_t bar = mapa_shared(smem_u32(recv_full), uint32_t(own));
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    st_async_v4(dst + ((j ^ sw) << 4), make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]), bar);
+            }
+            if (etid == 0 && j == 0) GM_STAMP(5);
+            mbar_wait_cluster(recv_full, 0);
+            if (etid == 0 && j == 0) GM_STAMP(6);
+        } else if (S > 1) {
+#pragma unroll 1
+            for (int c = hsel * (NC / 2); c < (hsel + 1) * (NC / 2); ++c) {
+                if (owner_of(c) == rank) continue;
                 float v[32];
                 tmem_ld32(trow + c * 32, v);
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
                     st_shared_v4(srow + c * 16384 + ((j ^ sw) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             }
+            if (etid == 0 && j == 0) GM_STAMP(5);
             cluster_sync_all();
+            if (etid == 0 && j == 0) GM_STAMP(6);
         }
         // The full K sum of chunk c for this thread's row: own accumulator + the peers' partials.
         auto acc32 = [&](int c, float(&v)[32]) {
@@ -366,10 +445,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll 1
                 for (int k = 0; k < S; ++k) {
                     if (k == rank) continue;
-                    const uint32_t ra = mapa_shared(srow + c * 16384, k);
                     float4 f[8];
+                    if (push) {
+                        const float4* src = reinterpret_cast<const float4*>(smem + (k * NC + c) * 16384 + row_in_tile * 128);
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) f[j] = ld_dsmem_f32x4(ra + ((j ^ sw) << 4));
+                        for (int j = 0; j < 8; ++j) f[j] = src[j ^ sw];
+                    } else {
+                        const uint32_t ra = mapa_shared(srow + c * 16384, k);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) f[j] = ld_dsmem_f32x4(ra + ((j ^ sw) << 4));
+                    }
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         v[4 * j] += f[j].x;
@@ -380,10 +465,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
             }
         };
-        const int u_first = S > 1 ? rank + S * hsel : hsel * (NU / 2);
-        const int u_step = S > 1 ? 2 * S : 1;
-        const int u_end = S > 1 ? NU : u_first + NU / 2;
-
         if constexpr (MODE == kModeResid) {
             // h += scale*(rs*z + b) in place, bf16 shadow, row stats.
             float ss = 0.f;
@@ -395,7 +476,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const int nv = min(32, p.N - col0);
                 if (!valid || nv <= 0) continue;
                 float* hp = reinterpret_cast<float*>(p.out) + (long long)r * p.ldo + col0;
-                load_f32x32(hp, h, nv, false);
+                if (c == u_first) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) h[j] = hpre[j];
+                } else {
+                    load_f32x32(hp, h, nv, false);
+                }
 #pragma unroll
                 for (int j = 0; j < 32; ++j) h[j] += p.resid_scale * (v[j] * rs + sm_vec[c * 32 + j]);
                 store_f32x32(hp, h, nv);
@@ -417,7 +503,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 if (!valid) continue;
                 if (MODE == kModeGate) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) a[j] = (a[j] * rs) * gelu_tanh(b[j] * rs);
+                    for (int j = 0; j < 32; ++j) a[j] = (a[j] * rs) * gelu_fast(b[j] * rs);
                     const int ocol0 = n_tile * (BN / 2) + c * 32;
                     store_bf16x32(reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)r * p.ldo + ocol0, a,
                                   min(32, p.N / 2 - ocol0));
@@ -430,8 +516,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     if (p.flags & kFlagGelu) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
-                            a[j] = gelu_tanh(a[j]);
-                            b[j] = gelu_tanh(b[j]);
+                            a[j] = gelu_fast(a[j]);
+                            b[j] = gelu_fast(b[j]);
                         }
                     }
                     // packed bn = 128 head tile: features at head * 256 + 64 * half + 32 c + j,
@@ -478,7 +564,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     for (int j = 0; j < 32; ++j) v[j] = v[j] * rs + sm_vec[c * 32 + j];
                     if (MODE == kModeBf16 && (p.flags & kFlagGelu)) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+                        for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
                     }
                 }
                 if constexpr (MODE == kModeF32Store) {
@@ -508,8 +594,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
             }
         }
-        // Peers may still be reading this CTA's parked partials.
-        if (S > 1) cluster_sync_all();
+        if (etid == 0 && j == 0) GM_STAMP(7);
+        // Pull form: peers may still be reading this CTA's parked partials.  Push form: every
+        // st.async into this CTA has landed (recv_full); the exit barrier below keeps senders alive.
+        if (S > 1 && !push) cluster_sync_all();
+        if (etid == 0 && j == 0) GM_STAMP(8);
         named_bar_sync(1, 256);  // sm_vec free for the next (sub-)tile
         }
         // accumulator drained (CG = 2: both CTAs arrive on the leader's barrier)
@@ -527,9 +616,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         cluster_sync_all();  // the leader's MMAs into the peer's TMEM are complete
         if (warp == 1) tmem_dealloc_cg2(tmem, tmem_cols);
     } else {
+        // Push form needs no exit barrier: every CTA waited for all pushes into its own smem
+        // (recv_full) before its epilogue, and nothing ever reads a peer's smem.
         __syncthreads();
         if (warp == 1) tmem_dealloc(tmem, tmem_cols);
     }
+    if (threadIdx.x == 0) GM_STAMP(9);
 }
 
 // ------------------------------------------------------------------ host side

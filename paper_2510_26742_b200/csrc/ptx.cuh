@@ -376,4 +376,40 @@ PI0B_DEV void mbar_arrive_cluster_relaxed(uint32_t mbar_cluster) {
     asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(mbar_cluster) : "memory");
 }
 
+
+// Asynchronous remote store into a peer CTA's shared memory (cluster address) that completes its
+// bytes on a barrier in the destination CTA (mbarrier::complete_tx): no fence on the sender, the
+// receiver's barrier wait makes the data visible.
+PI0B_DEV void st_async_v4(uint32_t addr, float4 v, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(mbar)
+                 : "memory");
+}
+PI0B_DEV void st_async_f32(uint32_t addr, float v, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(addr), "f"(v), "r"(mbar)
+                 : "memory");
+}
+// Wait on a local barrier whose phase completes through remote (cluster-scope) arrivals / st.async.
+PI0B_DEV bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// (with the same watchdog as mbar_wait: a broken handshake traps instead of hanging the GPU)
+PI0B_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t spins = 0;
+    while (!mbar_try_wait_cluster(bar, parity)) {
+        if (++spins > (1u << 28)) __trap();
+    }
+}
+// Split cluster barrier: arrive (release) early, wait (acquire) later.
+PI0B_DEV void cluster_arrive_release() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+PI0B_DEV void cluster_wait_acquire() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
 }  // namespace pi0b

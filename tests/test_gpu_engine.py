@@ -27,6 +27,11 @@ ACT_MAX_ABS = 0.05      # of actions whose rms is ~1
 ACT_REL = 0.25          # max |d| / max(|ref|, 0.1*rms(ref))
 LAYER_COS = 0.999
 RUN_TO_RUN = 0.02      # fp32 atomic (split-K / row-stat) ordering differs between runs
+# full scale (r02 measurements, profiles/r02_parity_*.json: max-abs 0.011-0.013, rel 0.13-0.16,
+# rms error 0.0047-0.0048 on actions of rms 0.80; per-layer cosine >= 0.99995): ~2x margins
+FULL_MAX_ABS = 0.025
+FULL_REL = 0.2
+FULL_RMS_ERR = 0.01
 
 
 def test_device_weight_stream_bitexact():
@@ -207,7 +212,8 @@ def test_full_scale_actions_match_reference_golden(views, prompt, tag):
     rep = _action_report(y, ref)
     print(f"full {tag} actions", rep)
     _record_parity(f"actions_{tag}", rep)
-    assert rep["max_abs"] < ACT_MAX_ABS and rep["rel"] < ACT_REL and rep["cos"] > 0.9995, rep
+    assert rep["max_abs"] < FULL_MAX_ABS and rep["rel"] < FULL_REL and rep["rms_err"] < FULL_RMS_ERR, rep
+    assert rep["cos"] > 0.9999, rep
 
 
 @pytest.mark.parametrize("views,prompt,tag", FULL_CONFIGS)
