@@ -174,6 +174,7 @@ EXPORTED_SYMBOLS = [
     "pi0b_last_error", "pi0b_gemm", "pi0b_gemm_skinny", "pi0b_attention",
     "pi0b_attention_ws_floats", "pi0b_random_f64", "pi0b_random_packed_bf16", "pi0b_seed_hash",
     "pi0b_engine_run_images", "pi0b_image_patches", "pi0b_stream_run", "pi0b_f64_to_bf16_host",
+    "pi0b_premultiply_rows", "pi0b_fold_time_mlp", "pi0b_time_embedding",
 ]
 
 
