@@ -464,6 +464,7 @@ private:
     int* d_patch_host_bf16_ = nullptr;
     __nv_bfloat16* d_pb_ = nullptr;  // the host-converted patches, packed
     cudaEvent_t done_ev_ = nullptr;               // streaming runtime: last async operation
+    cudaEvent_t h2d_ev_ = nullptr;                // after the last H2D copy out of h_in_ / h_pb_
     double *h_img_ = nullptr, *d_img_ = nullptr;  // image front-end staging (grown on demand)
     size_t n_img_ = 0;
     size_t n_patches_ = 0, n_state_ = 0, n_noise_ = 0, n_prompt_ = 0, n_out_ = 0;
@@ -541,6 +542,7 @@ Engine::~Engine() {
     if (h_in_) cudaFreeHost(h_in_);
     if (h_img_) cudaFreeHost(h_img_);
     if (done_ev_) cudaEventDestroy(done_ev_);
+    if (h2d_ev_) cudaEventDestroy(h2d_ev_);
     if (d_img_) cudaFree(d_img_);
     if (h_out_) cudaFreeHost(h_out_);
     if (h_pb_) cudaFreeHost(h_pb_);
@@ -1555,11 +1557,15 @@ void Engine::set_bias_table(const std::string& id, const double* t, long long ro
 void Engine::upload_inputs(const double* patches, const double* state, const double* noise,
                            const double* prompt, int which) {
     // which: 0 = all, 1 = prefix inputs, 2 = action inputs, 3 = all but the patches. Copies go through pinned
-    // staging so the H2D transfers are asynchronous DMA on the engine stream.
-    double* h = h_in_;
+    // staging so the H2D transfers are asynchronous DMA on the engine stream.  Each input owns a
+    // fixed region of h_in_ (prompt | state | noise), and no staging buffer is rewritten before
+    // the DMAs of the previous upload have read it (h2d_ev_): a prefix upload followed at once by
+    // an action upload (the streaming runtime) cannot overwrite bytes still queued for a DMA.
+    if (!h2d_ev_) PI0B_CUDA(cudaEventCreateWithFlags(&h2d_ev_, cudaEventDisableTiming));
+    PI0B_CUDA(cudaEventSynchronize(h2d_ev_));
     // Large tensors go in 256 KB pieces so that the host copy of piece i + 1 into the pinned
     // staging overlaps the DMA of piece i.
-    auto stage = [&](const double* src, size_t n, double* dev) {
+    auto stage = [&](const double* src, size_t n, double* dev, double* h) {
         if (!n) return;
         if (!src) throw EngineError(PI0B_E_INVALID, "missing input tensor");
         constexpr size_t kPiece = 32768;  // doubles (256 KB)
@@ -1568,21 +1574,20 @@ void Engine::upload_inputs(const double* patches, const double* state, const dou
             std::memcpy(h + o, src + o, m * 8);
             PI0B_CUDA(cudaMemcpyAsync(dev + o, h + o, m * 8, cudaMemcpyHostToDevice, stream_));
         }
-        h += n;
     };
+    double* h_prompt = h_in_;
+    double* h_state = h_prompt + n_prompt_;
+    double* h_noise = h_state + n_state_;
     if (which == 0 || which == 1) {
         stage_patches_bf16(patches);
-        if (P_ > 0) stage(prompt, n_prompt_, d_prompt_);
+        if (P_ > 0) stage(prompt, n_prompt_, d_prompt_, h_prompt);
     }
-    if (which == 3) {  // everything but the patches (image front-end)
-        if (P_ > 0) stage(prompt, n_prompt_, d_prompt_);
-        stage(state, n_state_, d_state_);
-        stage(noise, n_noise_, d_noise_);
+    if (which == 3 && P_ > 0) stage(prompt, n_prompt_, d_prompt_, h_prompt);  // image front-end: no patches
+    if (which == 0 || which == 2 || which == 3) {
+        stage(state, n_state_, d_state_, h_state);
+        stage(noise, n_noise_, d_noise_, h_noise);
     }
-    if (which == 0 || which == 2) {
-        stage(state, n_state_, d_state_);
-        stage(noise, n_noise_, d_noise_);
-    }
+    PI0B_CUDA(cudaEventRecord(h2d_ev_, stream_));
 }
 
 // bf16(float(x)) with float -> bf16 round-to-nearest-even: bit-identical to the device conversion

@@ -2,7 +2,13 @@
 // (proj/src/tensor.cpp:7-47): SplitMix64, FNV-1a seed hashing, and the uniform
 // draw lo + (hi - lo) * u with u = (x >> 11) * 2^-53, all evaluated in IEEE fp64
 // without contraction so the device reproduces the host stream bit for bit.
-// Plus the one rounding rule used for every fp64 -> bf16 conversion in the engine.
+// Plus the single-RNE fp64 -> bf16 rule used for every WEIGHT (gen_weights on the device and
+// set_weight from a host WeightStore).  Activation inputs go through fp32 instead, because
+// that is the engine's activation format: the prompt rows enter the fp32 residual stream
+// (kernels_misc.cu rows_to_f32_kernel) and the image patches are converted as
+// bf16(float(x)) (host: pi0b_f64_to_bf16_host / engine.cu host_bf16; device:
+// f64_to_bf16_rows_kernel; bit-identical to each other).  bf16(float(x)) differs from the
+// single-RNE rule only when x lies within 2^-29 relative of a bf16 rounding tie.
 #pragma once
 
 #include <math.h>

@@ -4,7 +4,7 @@ cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 { nvidia-smi -L; nproc; lscpu | grep -E "Model name|^CPU\(s\)"; free -g | head -2; ldd --version | head -1; } > gpurun_out/env.txt 2>&1
 if [ -z "$NOTEST" ]; then
-  timeout ${T_TESTS:-900} python -m pytest tests -m gpu -x -q --timeout=300 ${TSEL:+-k "$TSEL"} > gpurun_out/tests.log 2>&1
+  timeout ${T_TESTS:-900} python -m pytest tests -m gpu -x -q -s -rA --timeout=300 ${TSEL:+-k "$TSEL"} > gpurun_out/tests.log 2>&1
   tail -15 gpurun_out/tests.log
 fi
 if [ -n "$BENCH" ]; then
