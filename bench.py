@@ -66,8 +66,11 @@ def init_replicas(gpus: int):
     if ws != gpus:
         raise SystemExit(f"bench.py: WORLD_SIZE={ws} but --gpus {gpus}")
     if ws > 1:
+        import datetime
+
         import torch.distributed as dist
-        dist.init_process_group("gloo")
+        # bounded: a rank that dies must not leave the others in a barrier for the default 30 min
+        dist.init_process_group("gloo", timeout=datetime.timedelta(seconds=600))
     return ws, rank, local
 
 
@@ -108,6 +111,105 @@ def golden_parity(cfg, y) -> dict | None:
             "rms_err": float(np.sqrt(np.mean(d * d))), "rms_ref": float(np.sqrt(np.mean(ref * ref))),
             "rel": float(np.max(np.abs(d) / np.maximum(np.abs(ref), floor))),
             "cos": float((y.ravel() @ ref.ravel()) / (np.linalg.norm(y) * np.linalg.norm(ref)))}
+
+
+def ve_shard_bench(cfg, ws: int, rank: int, local: int, steps: int, warmup: int, single_p50: float) -> dict | None:
+    """SURVEY.md 8(e) / north_star: the view-sharded SigLIP stage at G = views GPUs (ranks < G):
+    each rank encodes its own view(s) and the layers' q|k|v rows plus the final llm.proj_in rows
+    are exchanged over NVLink peer memory (CUDA IPC mappings, the engine's fused push + release
+    kernel, kernels_misc.cu); rank 0 runs the LLM and the action expert.  Latency = rank 0's
+    device-timed full inference (CUDA events around its replay, the peers replaying their prefix
+    at the same time after a host rendezvous).  Reported beside the single-GPU p50 so the
+    "only where it lowers latency" question is answered by the measurement.  Every rank takes
+    part in the same sequence of gloo collectives; any failure aborts the experiment on all ranks
+    and is reported, never raised."""
+    import torch
+    import torch.distributed as dist
+    from paper_2510_26742_b200 import engine as E
+    from paper_2510_26742_b200.inputs import gen_inputs
+    G = cfg.views
+    if ws < G or G < 2:
+        return None
+    part = rank < G
+    eng, opened, err = None, [], None
+
+    def agree(ok: bool) -> bool:
+        flags = [None] * ws
+        dist.all_gather_object(flags, ok)
+        return all(flags)
+
+    try:
+        if part:
+            eng = E.Engine(cfg, device=local, ve_shards=G, ve_shard=rank)
+            eng.gen_weights(1)
+            mine = [E.ipc_export(p) for p in eng.ve_buffers().as_list()]
+        else:
+            mine = None
+    except Exception as e:  # noqa: BLE001
+        err, mine = f"rank {rank} setup: {e}"[:300], None
+    handles = [None] * ws
+    dist.all_gather_object(handles, mine)
+    ok = err is None
+    if part and ok:
+        try:
+            peers = []
+            for g in range(G):
+                if g == rank:
+                    peers.append(eng.ve_buffers())
+                else:
+                    ptrs = [E.ipc_open(h) for h in handles[g]]
+                    opened += ptrs
+                    peers.append(E.VeBuffers.from_list(ptrs))
+            eng.set_ve_peers(peers)
+        except Exception as e:  # noqa: BLE001
+            err, ok = f"rank {rank} peers: {e}"[:300], False
+    if not agree(ok and all(h is not None for h in handles[:G])):
+        res = {"gpus": G, "error": err or "setup failed on another rank"}
+    else:
+        x = gen_inputs(cfg, 1)
+        times, y = [], None
+        stream = torch.cuda.Stream() if part else None
+        for i in range(warmup + steps):
+            if not agree(ok):
+                break
+            try:
+                if rank == 0:
+                    if y is None:   # first call: uploads the inputs and captures the graph
+                        y = eng.run(x["patches"], x["state"], x["noise"], x.get("prompt"))
+                        continue
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    eng.replay(0, stream.cuda_stream)
+                    b.record(stream)
+                    b.synchronize()
+                    if i >= warmup:
+                        times.append(a.elapsed_time(b))
+                elif part:
+                    if i == 0:
+                        eng.run_prefix(x["patches"], x.get("prompt"))
+                    else:
+                        eng.replay(1, stream.cuda_stream)
+                        stream.synchronize()
+            except Exception as e:  # noqa: BLE001
+                err, ok = f"rank {rank} run: {e}"[:300], False
+        agree(ok)
+        if rank == 0 and times:
+            p50 = float(np.median(times))
+            res = {"gpus": G, "p50_ms": round(p50, 4), "p90_ms": round(float(np.percentile(times, 90)), 4),
+                   "steps": len(times), "single_gpu_p50_ms": round(single_p50, 4),
+                   "lowers_latency": bool(p50 < single_p50), "parity": golden_parity(cfg, y),
+                   "method": "rank 0 device-timed replay (CUDA events); peers replay their VE prefix after the same "
+                             "gloo rendezvous; K/V rows + proj_in rows over CUDA-IPC peer memory"}
+        else:
+            res = {"gpus": G, "error": err or "no timed steps"}
+    for ptr in opened:
+        try:
+            E.ipc_close(ptr)
+        except Exception:  # noqa: BLE001
+            pass
+    if eng is not None:
+        eng.close()
+    return res if rank == 0 else None
 
 
 def _dist():
@@ -188,6 +290,9 @@ def run_ours(args) -> None:
 
     ws, rank, local = init_replicas(args.gpus)
     os.environ["PI0B_STAGING_THREADS"] = str(staging_threads(ws))
+    # one GPU per rank; more ranks than GPUs (a functional run of the multi-rank path on a
+    # 1-GPU box) share devices round-robin
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     cfg = default_config(views=args.views, prompt_tokens=args.prompt)
     eng = E.Engine(cfg, device=local)
@@ -257,6 +362,10 @@ def run_ours(args) -> None:
     lb = lower_bound_ms(cfg)
     tot = totals(cfg)
     n_kernels = eng.kernel_count(0)
+    ve_shard = None
+    if ws > 1 and not args.no_ve_shard:
+        eng.close()          # frees this replica's HBM for the shard engine
+        ve_shard = ve_shard_bench(cfg, ws, rank, local, min(args.steps, 100), args.warmup, p50)
     if rank != 0:
         return
     # bytes that cross PCIe per call: the patches go as bf16 (converted on the host, engine.cu
@@ -293,6 +402,8 @@ def run_ours(args) -> None:
         "parity": par,
         "paper_4090_ms": {1: 20.0, 2: 27.3, 3: 36.8}.get(cfg.views),
     }
+    if ve_shard is not None:
+        line["ve_shard"] = ve_shard
     if ws == 1 and not args.no_cpu:
         try:
             line["cpu_baseline"] = cpu_baseline_port(cfg, os.cpu_count() or 1)
@@ -352,6 +463,7 @@ def main():
     ap.add_argument("--views", type=int, default=2)
     ap.add_argument("--prompt", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ve-shard", action="store_true", help="skip the view-sharded VE measurement at N > 1")
     ap.add_argument("--launch-check", action="store_true",
                     help="exercise the replica launcher + gloo reduction only (no GPU; tests/test_dist_cpu.py)")
     args = ap.parse_args()

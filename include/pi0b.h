@@ -46,6 +46,13 @@ typedef struct pi0b_engine_options {
     int device;             /* CUDA ordinal                                              */
     int use_cuda_graph;     /* 1: capture the whole forward as one CUDA graph (default)   */
     int record_checkpoints; /* 1: keep every node instance's output for parity checks    */
+    /* View-sharded vision encoder: ve_shards > 1 engines (one per GPU) each run
+     * the VE for views [ve_shard*V/ve_shards, (ve_shard+1)*V/ve_shards); every layer's q|k|v rows
+     * are all-gathered over peer memory before the joint attention (proj/src/builder.cpp:219-222)
+     * and the llm.proj_in rows are gathered into shard 0, which runs the LLM and the action
+     * expert.  Shards other than 0 serve run_prefix only.  0 or 1: no sharding. */
+    int ve_shards;
+    int ve_shard;
 } pi0b_engine_options;
 
 typedef struct pi0b_engine pi0b_engine;
@@ -107,6 +114,24 @@ int pi0b_premultiply_rows(double* w, int64_t k, int64_t m, const double* gamma);
 int pi0b_fold_time_mlp(const double* w_act, int64_t act, int64_t width, const double* b_act, const double* w_mix,
                        int64_t t_dim, int64_t mix_cols, const double* b_mix, int flow_steps, double* w_out,
                        double* table_out);
+
+/* View-sharded VE plumbing (see pi0b_engine_options): the device buffers a shard exposes to its
+ * peers, and the peers' buffers mapped into this process (same process: the pointers themselves;
+ * across processes: pi0b_ipc_export / pi0b_ipc_open of each buffer).  set_ve_peers must be called
+ * before the first run; peers[ve_shard] is ignored. */
+typedef struct pi0b_ve_buffers {
+    void* qkv[2]; /* gathered ve.qkv rows, double-buffered by layer parity [T, 3 ve_width] bf16 */
+    void* x;      /* llm.proj_in output rows [L, llm_width] fp32                                  */
+    void* xb;     /* the same, bf16                                                               */
+    void* stats;  /* prefix row-statistics arena (fp32)                                           */
+    void* sync;   /* flags [8] (one per source shard) + inference counter + arrival counter       */
+} pi0b_ve_buffers;
+int pi0b_engine_ve_buffers(pi0b_engine* e, pi0b_ve_buffers* out);
+int pi0b_engine_set_ve_peers(pi0b_engine* e, const pi0b_ve_buffers* peers, int n);
+/* cudaIpcGetMemHandle / cudaIpcOpenMemHandle of a device allocation (64-byte handle). */
+int pi0b_ipc_export(const void* dptr, uint8_t* handle64);
+int pi0b_ipc_open(const uint8_t* handle64, void** dptr);
+int pi0b_ipc_close(void* dptr);
 
 /* Streaming split of run(): the prefix (VE + LLM, fills the KV cache) and the action
  * expert (all flow steps against the cached prefix KV). */

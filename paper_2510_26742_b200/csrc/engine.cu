@@ -16,6 +16,7 @@
 // epilogue of the kernel that produced the residual stream.
 #include "../../include/pi0b.h"
 #include "aemk.cuh"
+#include "veshard.cuh"
 #include "attention.cuh"
 #include "gemm.cuh"
 #include "numerics.cuh"
@@ -29,6 +30,8 @@
 #include <functional>
 #include <mutex>
 #include <thread>
+#include <tuple>
+#include <initializer_list>
 #include <random>
 #include <chrono>
 #include <cctype>
@@ -204,7 +207,8 @@ static int choose_splits(int m_tiles, int n_tiles, int K, int bn, int num_sms) {
 
 // ------------------------------------------------------------------ plan records
 
-enum OpKind { kOpGemm, kOpAttn, kOpRowsF32, kOpF64Bf16, kOpF32F64, kOpMemset, kOpSkinny, kOpAeMega };
+enum OpKind { kOpGemm, kOpAttn, kOpRowsF32, kOpF64Bf16, kOpF32F64, kOpMemset, kOpSkinny, kOpAeMega,
+              kOpVeEpoch, kOpVePush, kOpVeWait };
 
 // A checkpoint the megakernel leaves in a record buffer (record mode).
 struct CkTag {
@@ -249,6 +253,14 @@ struct Op {
     long long ck_ld = 0;
     int ck_bf16 = 0;
     std::vector<CkTag> extra_ck;
+    // view-sharded VE: push own rows (segments: source, peer buffer, byte offset, bytes) to the
+    // peers (or to shard 0 only) and signal step `ve_step`; or wait for `ve_step` from ve_mask
+    int ve_step = 0, ve_nseg = 0;
+    bool ve_root_only = false;
+    unsigned ve_mask = 0;
+    const void* ve_src[3] = {nullptr, nullptr, nullptr};
+    int ve_buf[3] = {0, 0, 0};  // 0/1 qkv[parity], 2 x, 3 xb, 4 stats
+    size_t ve_off[3] = {0, 0, 0}, ve_bytes[3] = {0, 0, 0};
     bool is_kernel() const { return kind != kOpMemset; }
 };
 
@@ -506,6 +518,22 @@ private:
     void build_ae_mega();
     std::map<std::pair<std::string, int>, Checkpoint> ck_;
     bool pdl_ = true;
+
+    // view-sharded VE (pi0b_engine_options::ve_shards)
+public:
+    int ve_shards() const { return G_; }
+    int ve_shard() const { return g_; }
+    void ve_buffers(pi0b_ve_buffers* out) const;
+    void set_ve_peers(const pi0b_ve_buffers* peers, int n);
+private:
+    int G_ = 1, g_ = 0, ve_r0_ = 0, ve_rows_ = 0;
+    __nv_bfloat16* ve_qkv2_ = nullptr;  // second gathered q|k|v buffer (odd layers)
+    unsigned* ve_sync_ = nullptr;
+    std::vector<pi0b_ve_buffers> ve_peers_;
+    bool ve_peers_set_ = false;
+    void add_ve_push(int step, bool root_only, std::initializer_list<std::tuple<const void*, int, size_t, size_t>> segs);
+    void add_ve_wait(int step, unsigned mask);
+    __nv_bfloat16* ve_qkv_buf(int layer) const { return (G_ > 1 && (layer & 1)) ? ve_qkv2_ : ve_qkv_; }
 };
 
 // ------------------------------------------------------------------ construction
@@ -668,6 +696,18 @@ void Engine::alloc_activations() {
     ve_h_ = alloc<float>(size_t(T_) * ve_w_);
     ve_hb_ = alloc<__nv_bfloat16>(size_t(T_) * ve_w_);
     ve_qkv_ = alloc<__nv_bfloat16>(size_t(T_) * 3 * ve_w_);
+    G_ = std::max(1, o_.ve_shards);
+    g_ = G_ > 1 ? o_.ve_shard : 0;
+    if (G_ > kVeMaxShards || g_ < 0 || g_ >= G_ || c.views % G_)
+        throw EngineError(PI0B_E_UNSUPPORTED, "ve_shards must divide views (<= 8 shards), 0 <= ve_shard < ve_shards");
+    ve_rows_ = T_ / G_;
+    ve_r0_ = g_ * ve_rows_;
+    if (G_ > 1) {
+        ve_qkv2_ = alloc<__nv_bfloat16>(size_t(T_) * 3 * ve_w_);
+        ve_sync_ = alloc<unsigned>(kVeSyncWords);
+        PI0B_CUDA(cudaMemsetAsync(ve_sync_, 0, kVeSyncWords * sizeof(unsigned), stream_));
+        ve_peers_.resize(size_t(G_));
+    }
     ve_attn_ = alloc<__nv_bfloat16>(size_t(T_) * ve_w_);
     ve_mlp_ = alloc<__nv_bfloat16>(size_t(T_) * ve_mlp_ld_);
     PI0B_CUDA(cudaMemsetAsync(ve_mlp_, 0, size_t(T_) * ve_mlp_ld_ * 2, stream_));
@@ -709,6 +749,63 @@ void Engine::alloc_activations() {
     stats_cap_[0] = 2 + 2 * c.ve_layers + 2 * c.llm_layers;
     stats_cap_[1] = FS_ * (2 + 2 * c.ae_layers) + 2;
     for (int p = 0; p < 2; ++p) stats_[p] = alloc<float>(size_t(stats_cap_[p]) * stats_rows_);
+}
+
+void Engine::add_ve_push(int step, bool root_only,
+                         std::initializer_list<std::tuple<const void*, int, size_t, size_t>> segs) {
+    Op op;
+    op.kind = kOpVePush;
+    op.part = 0;
+    op.ve_step = step;
+    op.ve_root_only = root_only;
+    for (const auto& sg : segs) {
+        if (op.ve_nseg == 3) throw EngineError(PI0B_E_STATE, "ve push: too many segments");
+        if ((std::get<3>(sg) % 16) || (std::get<2>(sg) % 16) || (reinterpret_cast<uintptr_t>(std::get<0>(sg)) % 16))
+            throw EngineError(PI0B_E_UNSUPPORTED, "ve push: rows must be 16-byte aligned");
+        op.ve_src[op.ve_nseg] = std::get<0>(sg);
+        op.ve_buf[op.ve_nseg] = std::get<1>(sg);
+        op.ve_off[op.ve_nseg] = std::get<2>(sg);
+        op.ve_bytes[op.ve_nseg] = std::get<3>(sg);
+        ++op.ve_nseg;
+    }
+    ops_.push_back(op);
+}
+
+void Engine::add_ve_wait(int step, unsigned mask) {
+    Op op;
+    op.kind = kOpVeWait;
+    op.part = 0;
+    op.ve_step = step;
+    op.ve_mask = mask;
+    ops_.push_back(op);
+}
+
+void Engine::ve_buffers(pi0b_ve_buffers* out) const {
+    if (G_ < 2) throw EngineError(PI0B_E_STATE, "engine is not view-sharded (ve_shards < 2)");
+    out->qkv[0] = ve_qkv_;
+    out->qkv[1] = ve_qkv2_;
+    out->x = x_;
+    out->xb = xb_;
+    out->stats = stats_[0];
+    out->sync = ve_sync_;
+}
+
+void Engine::set_ve_peers(const pi0b_ve_buffers* peers, int n) {
+    if (G_ < 2) throw EngineError(PI0B_E_STATE, "engine is not view-sharded (ve_shards < 2)");
+    if (!peers || n != G_) throw EngineError(PI0B_E_INVALID, "set_ve_peers: one entry per shard");
+    for (int p = 0; p < G_; ++p) {
+        if (p == g_) continue;
+        const pi0b_ve_buffers& b = peers[p];
+        if (!b.qkv[0] || !b.qkv[1] || !b.sync || (p == 0 && (!b.x || !b.xb || !b.stats)))
+            throw EngineError(PI0B_E_INVALID, "set_ve_peers: missing peer buffer");
+        ve_peers_[size_t(p)] = b;
+    }
+    for (auto& g : graph_)  // captured with the old peers
+        if (g) {
+            cudaGraphExecDestroy(g);
+            g = nullptr;
+        }
+    ve_peers_set_ = true;
 }
 
 float* Engine::stats_slot(int part) {
@@ -865,7 +962,17 @@ void Engine::build_plan() {
         cv.srcb = d_pb_;
         ops_.push_back(cv);
     }
-    // --- vision encoder (proj/src/builder.cpp:205-240)
+    // --- vision encoder (proj/src/builder.cpp:205-240).  View-sharded (G_ > 1): this engine runs
+    // the rows [r0, r0 + Tg) of its own views; the joint attention reads every shard's rows,
+    // all-gathered after each ve.qkv (double-buffered by layer parity: a shard can only be one
+    // layer ahead of a peer, because it waits for that peer's rows of the next layer).
+    const int r0 = ve_r0_, Tg = ve_rows_;
+    if (G_ > 1) {
+        Op e;
+        e.kind = kOpVeEpoch;
+        e.part = 0;
+        ops_.insert(ops_.begin(), e);
+    }
     float* st = stats_slot(0);
     {
         GemmParams g{};
@@ -873,12 +980,12 @@ void Engine::build_plan() {
         g.mode = kModeF32Store;
         g.flags = kFlagBias;
         g.bias = Wv["ve.embed"].b[0];
-        g.out = ve_h_;
+        g.out = ve_h_ + size_t(r0) * ve_w_;
         g.ldo = ve_w_;
-        g.outb = ve_hb_;
+        g.outb = ve_hb_ + size_t(r0) * ve_w_;
         g.ldob = ve_w_;
-        g.out_stats = st;
-        add_gemm(0, "ve.embed", 0, patches_b_, patch_ld_, T_, Wv["ve.embed"], 0, 128, g);
+        g.out_stats = st + r0;
+        add_gemm(0, "ve.embed", 0, patches_b_ + size_t(r0) * patch_ld_, patch_ld_, Tg, Wv["ve.embed"], 0, 128, g);
         tag("ve.embed", 0, ve_h_, T_, ve_w_, ve_w_, 0);
     }
     const float inv_ve = 1.0f / float(ve_w_);
@@ -888,27 +995,33 @@ void Engine::build_plan() {
             g.N = ve_qkv_n;
             g.mode = kModeBf16;
             g.flags = kFlagRowScale | kFlagBias;
-            g.row_stats = st;
+            g.row_stats = st + r0;
             g.inv_width = inv_ve;
             g.eps = 1e-6f;
             g.bias = Wv["ve.qkv"].b[i];
-            g.out = ve_qkv_;
+            g.out = ve_qkv_buf(i) + size_t(r0) * ve_qkv_n;
             g.ldo = ve_qkv_n;
-            add_gemm(0, "ve.qkv", i, ve_hb_, ve_w_, T_, Wv["ve.qkv"], i, 128, g);
-            tag("ve.qkv", i, ve_qkv_, T_, ve_qkv_n, ve_qkv_n, 1);
+            add_gemm(0, "ve.qkv", i, ve_hb_ + size_t(r0) * ve_w_, ve_w_, Tg, Wv["ve.qkv"], i, 128, g);
+            tag("ve.qkv", i, ve_qkv_buf(i), T_, ve_qkv_n, ve_qkv_n, 1);
+        }
+        if (G_ > 1) {   // all-gather this layer's q|k|v rows (own rows -> every peer), then wait
+            const size_t row_bytes = size_t(ve_qkv_n) * 2;
+            add_ve_push(i, false, {std::make_tuple((const void*)(ve_qkv_buf(i) + size_t(r0) * ve_qkv_n), i & 1,
+                                                   size_t(r0) * row_bytes, size_t(Tg) * row_bytes)});
+            add_ve_wait(i, ((1u << G_) - 1u) & ~(1u << g_));
         }
         {   // ve.attn: joint over all views' tokens, no mask
             AttnParams a{};
-            a.q = ve_qkv_;
+            a.q = ve_qkv_buf(i) + size_t(r0) * ve_qkv_n;
             a.ldq = ve_qkv_n;
-            a.q_rows = T_;
+            a.q_rows = Tg;
             a.heads = c.ve_heads;
             a.kv_heads = c.ve_heads;
-            a.k0 = ve_qkv_ + ve_w_;
-            a.v0 = ve_qkv_ + 2 * ve_w_;
+            a.k0 = ve_qkv_buf(i) + ve_w_;
+            a.v0 = ve_qkv_buf(i) + 2 * ve_w_;
             a.ld0 = ve_qkv_n;
             a.rows0 = T_;
-            a.out = ve_attn_;
+            a.out = ve_attn_ + size_t(r0) * ve_w_;
             a.ldo = ve_w_;
             add_attn(0, "ve.attn", i, c.ve_head_dim, a);
             tag("ve.attn", i, ve_attn_, T_, ve_w_, ve_w_, 1);
@@ -921,12 +1034,12 @@ void Engine::build_plan() {
             g.flags = kFlagBias;
             g.bias = Wv["ve.proj"].b[i];
             g.resid_scale = 1.0f;
-            g.out = ve_h_;
+            g.out = ve_h_ + size_t(r0) * ve_w_;
             g.ldo = ve_w_;
-            g.outb = ve_hb_;
+            g.outb = ve_hb_ + size_t(r0) * ve_w_;
             g.ldob = ve_w_;
-            g.out_stats = st2;
-            add_gemm(0, "ve.proj", i, ve_attn_, ve_w_, T_, Wv["ve.proj"], i, 64, g);
+            g.out_stats = st2 + r0;
+            add_gemm(0, "ve.proj", i, ve_attn_ + size_t(r0) * ve_w_, ve_w_, Tg, Wv["ve.proj"], i, 64, g);
             tag("ve.proj", i, ve_h_, T_, ve_w_, ve_w_, 0);
         }
         {   // ve.ln2 + ve.fc1: gelu((p W) * rms(p) + b)
@@ -934,13 +1047,13 @@ void Engine::build_plan() {
             g.N = c.ve_mlp;
             g.mode = kModeBf16;
             g.flags = kFlagRowScale | kFlagBias | kFlagGelu;
-            g.row_stats = st2;
+            g.row_stats = st2 + r0;
             g.inv_width = inv_ve;
             g.eps = 1e-6f;
             g.bias = Wv["ve.fc1"].b[i];
-            g.out = ve_mlp_;
+            g.out = ve_mlp_ + size_t(r0) * ve_mlp_ld_;
             g.ldo = ve_mlp_ld_;
-            add_gemm(0, "ve.fc1", i, ve_hb_, ve_w_, T_, Wv["ve.fc1"], i, 128, g);
+            add_gemm(0, "ve.fc1", i, ve_hb_ + size_t(r0) * ve_w_, ve_w_, Tg, Wv["ve.fc1"], i, 128, g);
             tag("ve.fc1", i, ve_mlp_, T_, c.ve_mlp, ve_mlp_ld_, 1);
         }
         st = stats_slot(0);
@@ -951,12 +1064,12 @@ void Engine::build_plan() {
             g.flags = kFlagBias;
             g.bias = Wv["ve.fc2"].b[i];
             g.resid_scale = 1.0f;
-            g.out = ve_h_;
+            g.out = ve_h_ + size_t(r0) * ve_w_;
             g.ldo = ve_w_;
-            g.outb = ve_hb_;
+            g.outb = ve_hb_ + size_t(r0) * ve_w_;
             g.ldob = ve_w_;
-            g.out_stats = st;
-            add_gemm(0, "ve.fc2", i, ve_mlp_, ve_mlp_ld_, T_, Wv["ve.fc2"], i, 64, g);
+            g.out_stats = st + r0;
+            add_gemm(0, "ve.fc2", i, ve_mlp_ + size_t(r0) * ve_mlp_ld_, ve_mlp_ld_, Tg, Wv["ve.fc2"], i, 64, g);
             tag("ve.fc2", i, ve_h_, T_, ve_w_, ve_w_, 0);
         }
     }
@@ -967,17 +1080,35 @@ void Engine::build_plan() {
         g.N = llm_w_;
         g.mode = kModeF32Store;
         g.flags = kFlagRowScale | kFlagBias;
-        g.row_stats = st;
+        g.row_stats = st + r0;
         g.inv_width = inv_ve;
         g.eps = 1e-6f;
         g.bias = Wv["llm.proj_in"].b[0];
-        g.out = x_;
+        g.out = x_ + size_t(r0) * llm_w_;
         g.ldo = llm_w_;
-        g.outb = xb_;
+        g.outb = xb_ + size_t(r0) * llm_w_;
         g.ldob = llm_w_;
-        g.out_stats = xs;
-        add_gemm(0, "llm.proj_in", 0, ve_hb_, ve_w_, T_, Wv["llm.proj_in"], 0, 256, g);
+        g.out_stats = xs + r0;
+        add_gemm(0, "llm.proj_in", 0, ve_hb_ + size_t(r0) * ve_w_, ve_w_, Tg, Wv["llm.proj_in"], 0, 256, g);
         tag("llm.proj_in", 0, x_, T_, llm_w_, llm_w_, 0);
+    }
+    if (G_ > 1) {
+        // gather the llm.proj_in rows (fp32, bf16 shadow, row sums of squares) into shard 0, then
+        // an end-of-VE barrier: shard 0 releases every peer once all rows have arrived, so no
+        // shard starts the next inference's layer-0 exchange while a peer still reads layer 26
+        const int kGather = c.ve_layers, kRelease = c.ve_layers + 1;
+        const unsigned peers = ((1u << G_) - 1u) & ~1u;
+        if (g_ != 0) {
+            add_ve_push(kGather, true,
+                        {std::make_tuple((const void*)(x_ + size_t(r0) * llm_w_), 2, size_t(r0) * llm_w_ * 4, size_t(Tg) * llm_w_ * 4),
+                         std::make_tuple((const void*)(xb_ + size_t(r0) * llm_w_), 3, size_t(r0) * llm_w_ * 2, size_t(Tg) * llm_w_ * 2),
+                         std::make_tuple((const void*)(xs + r0), 4, size_t((xs + r0) - stats_[0]) * 4, size_t(Tg) * 4)});
+            add_ve_wait(kRelease, 1u);
+            // shards other than 0 serve run_prefix only: no LLM, no action expert
+            return;
+        }
+        add_ve_wait(kGather, peers);
+        add_ve_push(kRelease, false, {});
     }
     if (P_ > 0) {   // llm.tokens = concat_rows(proj_in, prompt)
         Op cv;
@@ -1670,6 +1801,32 @@ void Engine::run_ops(int part, cudaStream_t st) {
             case kOpF32F64: PI0B_CUDA(launch_f32_to_f64(op.src32, op.ld32, op.rows, op.cols, op.dst64, st)); break;
             case kOpMemset: PI0B_CUDA(cudaMemsetAsync(op.mptr, 0, op.mbytes, st)); break;
             case kOpAeMega: PI0B_CUDA(aemk_launch(ae_p_, num_sms_, st, ae_cluster_)); break;
+            case kOpVeEpoch: PI0B_CUDA(launch_ve_epoch(ve_sync_ + kVeEpoch, st)); break;
+            case kOpVeWait: PI0B_CUDA(launch_ve_wait(ve_sync_, op.ve_mask, ve_sync_ + kVeEpoch, unsigned(op.ve_step), st)); break;
+            case kOpVePush: {
+                VePushArgs a{};
+                a.nseg = op.ve_nseg;
+                for (int sg = 0; sg < op.ve_nseg; ++sg) {
+                    a.src[sg] = static_cast<const uint4*>(op.ve_src[sg]);
+                    a.n16[sg] = (long long)(op.ve_bytes[sg] / 16);
+                }
+                for (int p = 0; p < G_; ++p) {
+                    if (p == g_ || (op.ve_root_only && p != 0)) continue;
+                    const pi0b_ve_buffers& b = ve_peers_[size_t(p)];
+                    for (int sg = 0; sg < op.ve_nseg; ++sg) {
+                        void* base = op.ve_buf[sg] < 2 ? b.qkv[op.ve_buf[sg]]
+                                                       : (op.ve_buf[sg] == 2 ? b.x : (op.ve_buf[sg] == 3 ? b.xb : b.stats));
+                        a.dst[a.npeer][sg] = reinterpret_cast<uint4*>(static_cast<uint8_t*>(base) + op.ve_off[sg]);
+                    }
+                    a.flag[a.npeer] = static_cast<unsigned*>(b.sync) + g_;
+                    ++a.npeer;
+                }
+                a.epoch = ve_sync_ + kVeEpoch;
+                a.done = ve_sync_ + kVeDone;
+                a.step = unsigned(op.ve_step);
+                PI0B_CUDA(launch_ve_push(a, st));
+                break;
+            }
         }
         if (o_.record_checkpoints)
             for (const CkTag& tg : op.extra_ck) {
@@ -1717,6 +1874,9 @@ void Engine::capture(int part, int slot) {
 
 // part: 0 = full, 1 = prefix, 2 = action (C-ABI numbering)
 void Engine::launch(int part, cudaStream_t st) {
+    if (G_ > 1 && !ve_peers_set_) throw EngineError(PI0B_E_STATE, "view-sharded engine: set_ve_peers first");
+    if (G_ > 1 && g_ != 0 && part != 1)
+        throw EngineError(PI0B_E_STATE, "view-sharded engine: shards other than 0 run the prefix only");
     if (!weights_checked_) {  // every (node, instance, bias table) written at least once
         const std::string miss = missing_weights();
         if (!miss.empty()) throw EngineError(PI0B_E_STATE, "weights not loaded: " + miss);
@@ -2072,7 +2232,7 @@ void pi0b_default_config(pi0b_model_config* c) {
 
 int pi0b_engine_create(const pi0b_model_config* cfg, const pi0b_engine_options* opt, pi0b_engine** out) {
     if (!cfg || !out) return pi0b::fail(EngineError(PI0B_E_INVALID, "null argument"));
-    pi0b_engine_options o{0, 1, 0};
+    pi0b_engine_options o{0, 1, 0, 0, 0};
     if (opt) o = *opt;
     PI0B_TRY({
         auto* e = new pi0b_engine;
@@ -2151,6 +2311,34 @@ int pi0b_engine_run_action(pi0b_engine* e, const double* state, const double* no
         e->impl->fetch_actions(out);
     })
 }
+
+int pi0b_engine_ve_buffers(pi0b_engine* e, pi0b_ve_buffers* out) {
+    if (!out) return pi0b::fail(EngineError(PI0B_E_INVALID, "null argument"));
+    PI0B_TRY(e->impl->ve_buffers(out))
+}
+
+int pi0b_engine_set_ve_peers(pi0b_engine* e, const pi0b_ve_buffers* peers, int n) {
+    PI0B_TRY(e->impl->set_ve_peers(peers, n))
+}
+
+int pi0b_ipc_export(const void* dptr, uint8_t* handle64) {
+    if (!dptr || !handle64) return pi0b::fail(EngineError(PI0B_E_INVALID, "null argument"));
+    cudaIpcMemHandle_t h;
+    PI0B_TRY({
+        PI0B_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)));
+        static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+        std::memcpy(handle64, &h, 64);
+    })
+}
+
+int pi0b_ipc_open(const uint8_t* handle64, void** dptr) {
+    if (!dptr || !handle64) return pi0b::fail(EngineError(PI0B_E_INVALID, "null argument"));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    PI0B_TRY(PI0B_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess)))
+}
+
+int pi0b_ipc_close(void* dptr) { PI0B_TRY(PI0B_CUDA(cudaIpcCloseMemHandle(dptr))) }
 
 int pi0b_engine_replay(pi0b_engine* e, int part, void* stream) {
     PI0B_TRY({

@@ -11,6 +11,9 @@
 //   * f32_to_f64_kernel   - the [63, 32] action chunk back to fp64.
 #include "numerics.cuh"
 #include "ptx.cuh"
+#include "veshard.cuh"
+
+#include <algorithm>
 
 namespace pi0b {
 
@@ -229,6 +232,75 @@ cudaError_t launch_image_patches(const double* img, int views, int H, int W, int
     if (views < 1 || H < 2 || W < 2 || C < 1 || side < P || side % P) return cudaErrorInvalidValue;
     const long long n = (long long)views * side * side * C;
     image_patches_kernel<<<int((n + 255) / 256), 256, 0, st>>>(img, views, H, W, C, side, P, patches);
+    return cudaGetLastError();
+}
+
+}  // namespace pi0b
+
+// ------------------------------------------------------------------ view-sharded vision encoder
+// the VE attention is joint over every view's tokens (proj/src/builder.cpp:
+// 219-222), so a view-sharded VE must all-gather each layer's q|k|v rows before the attention.
+// One engine per shard (one per GPU); each pushes its own rows straight into every peer's
+// gathered buffer (P2P stores over NVLink; peers' buffers mapped by CUDA IPC), then publishes a
+// sequence number into each peer's flag slot with a system-scope release.  The receiving side's
+// wait kernel polls its own flags with system-scope acquire loads.  Sequence number of step s of
+// inference e: 64 e + s + 1 (monotone, so nothing is ever reset).
+namespace pi0b {
+
+__global__ void ve_push_kernel(const VePushArgs a) {
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
+    for (int s = 0; s < a.nseg; ++s)
+        for (long long i = tid; i < a.n16[s]; i += nth) {
+            const uint4 v = __ldcg(a.src[s] + i);
+            for (int p = 0; p < a.npeer; ++p) a.dst[p][s][i] = v;
+        }
+    __threadfence_system();  // this CTA's peer stores are visible system-wide
+    __syncthreads();
+    __shared__ unsigned last;
+    if (threadIdx.x == 0) last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last && threadIdx.x < a.npeer) {
+        __threadfence_system();
+        const unsigned v = 64u * *a.epoch + a.step + 1u;
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.flag[threadIdx.x]), "r"(v) : "memory");
+        if (threadIdx.x == 0) *a.done = 0u;  // every CTA has arrived: ready for the next launch
+    }
+}
+
+// Lane p waits until flags[p] (written by peer p) reaches this inference's sequence number for
+// `step`; traps after ~10 s (a peer that never arrives) instead of hanging the GPU.
+__global__ void ve_wait_kernel(const unsigned* flags, unsigned mask, const unsigned* epoch, unsigned step) {
+    const int p = threadIdx.x;
+    if (p >= 32 || !((mask >> p) & 1u)) return;
+    const unsigned target = 64u * *epoch + step + 1u;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        unsigned v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + p) : "memory");
+        if (int(v - target) >= 0) break;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 10000000000ull) __trap();
+        __nanosleep(200);
+    }
+}
+
+__global__ void ve_epoch_kernel(unsigned* epoch) { *epoch += 1u; }
+
+cudaError_t launch_ve_push(const VePushArgs& a, cudaStream_t st) {
+    long long n = 0;
+    for (int s = 0; s < a.nseg; ++s) n = n > a.n16[s] ? n : a.n16[s];
+    const int blocks = int(std::min<long long>(64, (n + 255) / 256 + 1));
+    ve_push_kernel<<<blocks, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_ve_wait(const unsigned* flags, unsigned mask, const unsigned* epoch, unsigned step, cudaStream_t st) {
+    ve_wait_kernel<<<1, 32, 0, st>>>(flags, mask, epoch, step);
+    return cudaGetLastError();
+}
+cudaError_t launch_ve_epoch(unsigned* epoch, cudaStream_t st) {
+    ve_epoch_kernel<<<1, 1, 0, st>>>(epoch);
     return cudaGetLastError();
 }
 

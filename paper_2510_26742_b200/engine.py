@@ -46,7 +46,25 @@ class UnsupportedConfig(ShapeError):
 
 
 class EngineOptions(ctypes.Structure):
-    _fields_ = [("device", ctypes.c_int), ("use_cuda_graph", ctypes.c_int), ("record_checkpoints", ctypes.c_int)]
+    _fields_ = [("device", ctypes.c_int), ("use_cuda_graph", ctypes.c_int), ("record_checkpoints", ctypes.c_int),
+                ("ve_shards", ctypes.c_int), ("ve_shard", ctypes.c_int)]
+
+
+class VeBuffers(ctypes.Structure):
+    """pi0b_ve_buffers: device buffers a view-sharded VE engine exposes to its peers."""
+    _fields_ = [("qkv", ctypes.c_void_p * 2), ("x", ctypes.c_void_p), ("xb", ctypes.c_void_p),
+                ("stats", ctypes.c_void_p), ("sync", ctypes.c_void_p)]
+
+    FIELDS = ("qkv0", "qkv1", "x", "xb", "stats", "sync")
+
+    def as_list(self):
+        return [self.qkv[0], self.qkv[1], self.x, self.xb, self.stats, self.sync]
+
+    @classmethod
+    def from_list(cls, v):
+        b = cls()
+        b.qkv[0], b.qkv[1], b.x, b.xb, b.stats, b.sync = v
+        return b
 
 
 class GemmDesc(ctypes.Structure):
@@ -131,6 +149,11 @@ def lib():
                                               ctypes.c_int, ctypes.c_uint64, ctypes.c_double, ctypes.c_double, vp]
         L.pi0b_seed_hash.argtypes = [ctypes.c_uint64, ctypes.c_char_p, ctypes.c_uint64, ctypes.c_uint64]
         L.pi0b_seed_hash.restype = ctypes.c_uint64
+        L.pi0b_engine_ve_buffers.argtypes = [vp, ctypes.POINTER(VeBuffers)]
+        L.pi0b_engine_set_ve_peers.argtypes = [vp, ctypes.POINTER(VeBuffers), ctypes.c_int]
+        L.pi0b_ipc_export.argtypes = [vp, ctypes.c_char_p]
+        L.pi0b_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
+        L.pi0b_ipc_close.argtypes = [vp]
         _lib = L
     return _lib
 
@@ -175,6 +198,7 @@ EXPORTED_SYMBOLS = [
     "pi0b_attention_ws_floats", "pi0b_random_f64", "pi0b_random_packed_bf16", "pi0b_seed_hash",
     "pi0b_engine_run_images", "pi0b_image_patches", "pi0b_stream_run", "pi0b_f64_to_bf16_host",
     "pi0b_premultiply_rows", "pi0b_fold_time_mlp", "pi0b_time_embedding",
+    "pi0b_engine_ve_buffers", "pi0b_engine_set_ve_peers", "pi0b_ipc_export", "pi0b_ipc_open", "pi0b_ipc_close",
 ]
 
 
@@ -206,10 +230,10 @@ class Engine:
     """One pi0 engine on one B200 (weights, activations, KV cache, captured CUDA graphs)."""
 
     def __init__(self, cfg: ModelConfig, device: int = 0, use_cuda_graph: bool = True,
-                 record_checkpoints: bool = False):
+                 record_checkpoints: bool = False, ve_shards: int = 0, ve_shard: int = 0):
         self.cfg = cfg
         self._h = ctypes.c_void_p()
-        opt = EngineOptions(device, int(use_cuda_graph), int(record_checkpoints))
+        opt = EngineOptions(device, int(use_cuda_graph), int(record_checkpoints), ve_shards, ve_shard)
         _raise(lib().pi0b_engine_create(ctypes.byref(cfg), ctypes.byref(opt), ctypes.byref(self._h)),
                "pi0b_engine_create")
 
@@ -292,6 +316,17 @@ class Engine:
                "run_action")
         return y
 
+    # ---- view-sharded vision encoder (include/pi0b.h pi0b_ve_buffers)
+    def ve_buffers(self) -> VeBuffers:
+        b = VeBuffers()
+        _raise(lib().pi0b_engine_ve_buffers(self._h, ctypes.byref(b)), "ve_buffers")
+        return b
+
+    def set_ve_peers(self, peers: list) -> None:
+        """peers[i] = VeBuffers of shard i (this shard's own entry is ignored)."""
+        arr = (VeBuffers * len(peers))(*peers)
+        _raise(lib().pi0b_engine_set_ve_peers(self._h, arr, len(peers)), "set_ve_peers")
+
     def replay(self, part: int = 0, stream: int | None = None) -> None:
         _raise(lib().pi0b_engine_replay(self._h, part, stream), "replay")
 
@@ -318,6 +353,24 @@ class Engine:
                                                  out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), rows, cols),
                f"checkpoint {node}[{inst}]")
         return out
+
+
+def ipc_export(dptr: int) -> bytes:
+    """64-byte CUDA IPC handle of a device allocation (cudaIpcGetMemHandle)."""
+    buf = ctypes.create_string_buffer(64)
+    _raise(lib().pi0b_ipc_export(dptr, buf), "ipc_export")
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map another process's allocation into this one (cudaIpcOpenMemHandle); returns the pointer."""
+    p = ctypes.c_void_p()
+    _raise(lib().pi0b_ipc_open(handle, ctypes.byref(p)), "ipc_open")
+    return p.value
+
+
+def ipc_close(dptr: int) -> None:
+    _raise(lib().pi0b_ipc_close(dptr), "ipc_close")
 
 
 def evaluate(cfg: ModelConfig, weight_seed: int, inputs: dict) -> np.ndarray:

@@ -9,6 +9,9 @@ import ctypes
 import os
 import sys
 
+# the production (clustered) megakernel without the cooperative attribute, which ncu cannot replay
+os.environ.setdefault("PI0B_AE_COOP", "0")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2510_26742_b200 import engine as E  # noqa: E402
