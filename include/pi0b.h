@@ -64,6 +64,12 @@ void pi0b_default_config(pi0b_model_config* cfg);
 int pi0b_engine_create(const pi0b_model_config* cfg, const pi0b_engine_options* opt,
                        pi0b_engine** out);
 void pi0b_engine_destroy(pi0b_engine* e);
+/* An engine that reads `donor`'s weight arena instead of allocating its own (same config and
+ * device): several KV caches / input sets over one copy of the 5.2 GB of weights, e.g. the
+ * streaming runtime's double-buffered KV.  Weights are loaded through the donor only
+ * (gen_weights / set_weight on this engine return PI0B_E_STATE); destroy it before the donor. */
+int pi0b_engine_create_shared(const pi0b_model_config* cfg, const pi0b_engine_options* opt, pi0b_engine* donor,
+                              pi0b_engine** out);
 
 /* Device-side rtvla::gen_weights(build_pi0_graph(cfg), seed): the same SplitMix64 /
  * FNV-1a streams, rounded once to bf16 (proj/src/evaluate.cpp:38-75). */
@@ -141,7 +147,7 @@ int pi0b_engine_run_action(pi0b_engine* e, const double* state, const double* no
 
 /* Full-streaming runtime (the real execution of what the reference only simulates,
  * proj/include/rtvla/streamsim.hpp:54-131): a camera stream at frame_rate feeds the prefix (VE + LLM)
- * into one of two KV buffers (two engines, double-buffered KV); an action-expert stream runs
+ * into one of two KV buffers (two engines over one shared weight arena); an action-expert stream runs
  * control ticks at up to ae_rate on the KV chosen by kv_policy with the freshest sensor sample;
  * each tick writes its chunk into a trajectory buffer of trajectory_rate slots whose commit cursor
  * advances with wall time.  Runs `seconds` of synthetic frames/sensors (random patches / state /

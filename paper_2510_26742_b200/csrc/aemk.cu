@@ -1075,11 +1075,21 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     float sv[32];
                     tmem_ld32(tmem + kTS + tlane + kh * 64 + side * 32, sv);  // warp-uniform
                     const int nkm = kh < nb ? min(32, max(0, nk - (kh * 64 + side * 32))) : 0;
+                    // padding keys of the cached prefix [kv_valid0, kv_rows0), relative to this chunk
+                    const int kc = key0 + kh * 64 + side * 32, pad_lo = p.kv_valid0 - kc, pad_hi = p.kv_rows0 - kc;
                     float mx = -INFINITY;
+                    if (nkm == 32 && (pad_lo >= 32 || pad_hi <= 0)) {  // no masked key in this chunk
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        sv[e] = e < nkm ? sv[e] * p.scale_log2 : -INFINITY;
-                        mx = fmaxf(mx, sv[e]);
+                        for (int e = 0; e < 32; ++e) {
+                            sv[e] *= p.scale_log2;
+                            mx = fmaxf(mx, sv[e]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) {
+                            sv[e] = e < nkm && (e < pad_lo || e >= pad_hi) ? sv[e] * p.scale_log2 : -INFINITY;
+                            mx = fmaxf(mx, sv[e]);
+                        }
                     }
                     xch[part * 64 + R] = mx;
                     named_bar_sync(1, kWorkers);
@@ -1157,10 +1167,11 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         tmem_ld32(ts + 32, *reinterpret_cast<float(*)[32]>(sv + 32));
                     }
                     const int nkm = mine && act ? nk - side * 64 : 0;  // valid keys of this thread's block
+                    const int kc = key0 + side * 64, pad_lo = p.kv_valid0 - kc, pad_hi = p.kv_rows0 - kc;  // padding keys
                     float mx = -INFINITY;
 #pragma unroll
                     for (int e = 0; e < 64; ++e) {
-                        sv[e] = e < nkm ? sv[e] * p.scale_log2 : -INFINITY;
+                        sv[e] = e < nkm && (e < pad_lo || e >= pad_hi) ? sv[e] * p.scale_log2 : -INFINITY;
                         mx = fmaxf(mx, sv[e]);
                     }
                     xch[side * 128 + R] = mx;

@@ -102,7 +102,8 @@ struct AeParams {
     float* rec_a;                  // record mode: [slots][C, lda]
     int width, n_qkv, q_width, mlp, act_dim, state_dim, chunk, heads;
     int rope_pos0, rope_cols;      // AE RoPE positions start at the prefix length L
-    int kv_rows0;                  // L: rows of the cached LLM K/V segment
+    int kv_rows0;                  // Lp = L rounded up to 32: first key index of the expert's own rows
+    int kv_valid0;                 // L: cached keys [kv_valid0, kv_rows0) are padding (masked)
     int kcol_cache, kcol_own;      // first K column in the LLM KV cache / in the AE qkv rows
     int key_blocks;                // ceil((L + 64) / 64) key blocks of 64
     int attn_splits;               // key ranges per head pair (<= 3 key blocks each)

@@ -20,6 +20,8 @@ struct AttnParams {
     const __nv_bfloat16* v0;
     long long ld0;
     int rows0;
+    int rows0_valid;          // keys [rows0_valid, rows0) of segment 0 are padding and masked (<= 0: none):
+                              // a prefix padded to a 32-row multiple ahead of a second segment
     const __nv_bfloat16* k1;  // segment 1 (rows1 may be 0)
     const __nv_bfloat16* v1;
     long long ld1;

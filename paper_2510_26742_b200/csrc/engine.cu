@@ -392,7 +392,10 @@ static int staging_helpers() {
 
 class Engine {
 public:
-    Engine(const pi0b_model_config& cfg, const pi0b_engine_options& opt);
+    // donor != nullptr: this engine reads the donor's weights (one weight arena for several
+    // engines, e.g. the streaming runtime's double-buffered KV): only activations and the KV cache
+    // are allocated; weights can be written only through the donor, which must outlive it.
+    Engine(const pi0b_model_config& cfg, const pi0b_engine_options& opt, Engine* donor = nullptr);
     ~Engine();
 
     void gen_weights(uint64_t seed);
@@ -460,7 +463,7 @@ private:
     bool weights_checked_ = false;
 
     // dims
-    int T_ = 0, P_ = 0, L_ = 0, S_ = 0, C_ = 0, FS_ = 0;
+    int T_ = 0, P_ = 0, L_ = 0, Lp_ = 0, S_ = 0, C_ = 0, FS_ = 0;  // Lp_: L_ rounded up to 32 rows
     int ve_w_ = 0, llm_w_ = 0, ae_w_ = 0, llm_q_ = 0, llm_kv_ = 0, ae_q_ = 0, ae_kv_ = 0;
     int patch_ld_ = 0, act_ld_ = 0, state_ld_ = 0, ve_mlp_ld_ = 0;
 
@@ -518,6 +521,12 @@ private:
     void build_ae_mega();
     std::map<std::pair<std::string, int>, Checkpoint> ck_;
     bool pdl_ = true;
+    Engine* donor_ = nullptr;  // weights borrowed from this engine (nullptr: own arena)
+    std::string ae_fallback_;  // why the per-node action expert runs instead of the megakernel
+public:
+    const std::string& ae_fallback() const { return ae_fallback_; }
+    bool ae_megakernel() const { return ae_mega_; }
+private:
 
     // view-sharded VE (pi0b_engine_options::ve_shards)
 public:
@@ -538,7 +547,13 @@ private:
 
 // ------------------------------------------------------------------ construction
 
-Engine::Engine(const pi0b_model_config& cfg, const pi0b_engine_options& opt) : c_(cfg), o_(opt) {
+Engine::Engine(const pi0b_model_config& cfg, const pi0b_engine_options& opt, Engine* donor)
+    : c_(cfg), o_(opt), donor_(donor) {
+    if (donor_) {
+        const pi0b_model_config& d = donor_->c_;
+        if (std::memcmp(&d, &cfg, sizeof cfg) != 0 || donor_->o_.device != opt.device)
+            throw EngineError(PI0B_E_INVALID, "shared weights: the donor engine has another config or device");
+    }
     validate_config();
     PI0B_CUDA(cudaSetDevice(o_.device));
     cudaDeviceProp prop;
@@ -599,6 +614,10 @@ void Engine::validate_config() {
 
 void Engine::alloc_weights() {
     const auto& c = c_;
+    if (donor_) {  // same config: the same node list, pointers into the donor's arena
+        W_ = donor_->W_;
+        return;
+    }
     auto add = [&](const std::string& id, int k, int m, int inst, bool bias, int perm = kPermNone,
                    bool table = false, int rope_cols = 0) {
         NodeWeights nw;
@@ -656,6 +675,7 @@ void Engine::alloc_activations() {
     T_ = c.views * c.tokens_per_view;
     P_ = c.prompt_tokens;
     L_ = T_ + P_;
+    Lp_ = round_up(L_, 32);
     C_ = c.chunk_len;
     S_ = C_ + 1;
     FS_ = c.flow_steps;
@@ -711,11 +731,19 @@ void Engine::alloc_activations() {
     ve_attn_ = alloc<__nv_bfloat16>(size_t(T_) * ve_w_);
     ve_mlp_ = alloc<__nv_bfloat16>(size_t(T_) * ve_mlp_ld_);
     PI0B_CUDA(cudaMemsetAsync(ve_mlp_, 0, size_t(T_) * ve_mlp_ld_ * 2, stream_));
-    x_ = alloc<float>(size_t(L_) * llm_w_);
-    xb_ = alloc<__nv_bfloat16>(size_t(L_) * llm_w_);
-    llm_attn_ = alloc<__nv_bfloat16>(size_t(L_) * llm_q_);
-    llm_g_ = alloc<__nv_bfloat16>(size_t(L_) * c.llm_mlp);
-    for (int l = 0; l < c.llm_layers; ++l) kv_.push_back(alloc<__nv_bfloat16>(size_t(L_) * (llm_q_ + 2 * llm_kv_)));
+    // The prefix is processed in Lp_ = round_up(L_, 32) rows (any prompt length the reference
+    // accepts, proj/include/rtvla/graph.hpp:156-158): rows [L_, Lp_) start as zeros, stay finite
+    // and row-local through every GEMM, and are masked out of every attention as keys.
+    x_ = alloc<float>(size_t(Lp_) * llm_w_);
+    xb_ = alloc<__nv_bfloat16>(size_t(Lp_) * llm_w_);
+    PI0B_CUDA(cudaMemsetAsync(x_, 0, size_t(Lp_) * llm_w_ * 4, stream_));
+    PI0B_CUDA(cudaMemsetAsync(xb_, 0, size_t(Lp_) * llm_w_ * 2, stream_));
+    llm_attn_ = alloc<__nv_bfloat16>(size_t(Lp_) * llm_q_);
+    llm_g_ = alloc<__nv_bfloat16>(size_t(Lp_) * c.llm_mlp);
+    for (int l = 0; l < c.llm_layers; ++l) {
+        kv_.push_back(alloc<__nv_bfloat16>(size_t(Lp_) * (llm_q_ + 2 * llm_kv_)));
+        PI0B_CUDA(cudaMemsetAsync(kv_.back(), 0, size_t(Lp_) * (llm_q_ + 2 * llm_kv_) * 2, stream_));
+    }
     state_b_ = alloc<__nv_bfloat16>(size_t(state_ld_));
     PI0B_CUDA(cudaMemsetAsync(state_b_, 0, size_t(state_ld_) * 2, stream_));
     ab_ = alloc<__nv_bfloat16>(size_t(C_) * act_ld_);
@@ -731,7 +759,7 @@ void Engine::alloc_activations() {
 
     // RoPE table: cos/sin of p * 10000^(-2j/256), evaluated in fp64 as make_rope_table
     // (proj/src/tensor.cpp:133-148) and rounded to fp32. Positions [0, L+S).
-    const int npos = L_ + S_;
+    const int npos = Lp_ + S_;
     std::vector<float> cs(size_t(npos) * 128 * 2);
     for (int p = 0; p < npos; ++p)
         for (int j = 0; j < 128; ++j) {
@@ -745,7 +773,7 @@ void Engine::alloc_activations() {
     PI0B_CUDA(cudaStreamSynchronize(stream_));
 
     // Row-stat slots: one per residual-stream producer instance, zeroed per replay.
-    stats_rows_ = round_up(std::max(L_, S_), 64);
+    stats_rows_ = round_up(std::max(Lp_, S_), 64);
     stats_cap_[0] = 2 + 2 * c.ve_layers + 2 * c.llm_layers;
     stats_cap_[1] = FS_ * (2 + 2 * c.ae_layers) + 2;
     for (int p = 0; p < 2; ++p) stats_[p] = alloc<float>(size_t(stats_cap_[p]) * stats_rows_);
@@ -926,8 +954,8 @@ void Engine::add_attn(int part, const std::string& node, int inst, int hd, AttnP
     }
     ap.kv_per_split = ap.rows0 + ap.rows1;
     ap.scale_log2 = float(1.4426950408889634 / std::sqrt(double(hd)));
-    if ((ap.rows0 % 32) || (ap.rows1 % 32))
-        throw EngineError(PI0B_E_UNSUPPORTED, "attention key segments must be multiples of 32 rows");
+    if ((ap.rows1 > 0 && (ap.rows0 % 32)) || (ap.rows1 % 32) || (ap.q_rows % 32))
+        throw EngineError(PI0B_E_UNSUPPORTED, "attention: two key segments need 32-row multiples");
     op.fm = make_fattn_maps(ap, hd);
     op.ap = ap;
     ops_.push_back(op);
@@ -1110,6 +1138,17 @@ void Engine::build_plan() {
         add_ve_wait(kGather, peers);
         add_ve_push(kRelease, false, {});
     }
+    if (Lp_ > L_) {  // padding rows of the prefix start each inference as zeros (engine.cu alloc_activations)
+        Op m;
+        m.kind = kOpMemset;
+        m.part = 0;
+        m.mptr = x_ + size_t(L_) * llm_w_;
+        m.mbytes = size_t(Lp_ - L_) * llm_w_ * 4;
+        ops_.push_back(m);
+        m.mptr = xb_ + size_t(L_) * llm_w_;
+        m.mbytes = size_t(Lp_ - L_) * llm_w_ * 2;
+        ops_.push_back(m);
+    }
     if (P_ > 0) {   // llm.tokens = concat_rows(proj_in, prompt)
         Op cv;
         cv.kind = kOpRowsF32;
@@ -1145,7 +1184,7 @@ void Engine::build_plan() {
                 g.N = llm_qkv_n;
                 g.rope_cols = llm_q_ + llm_kv_;
                 g.out = kv_[l];
-                add_gemm(0, "llm.qkv", l, xb_, llm_w_, L_, Wv["llm.qkv"], l, qkv_bn, g);
+                add_gemm(0, "llm.qkv", l, xb_, llm_w_, Lp_, Wv["llm.qkv"], l, qkv_bn, g);
             } else {
                 // Last layer: only K/V feed the action expert; its Q is dead.
                 NodeWeights sub = Wv["llm.qkv"];
@@ -1153,7 +1192,7 @@ void Engine::build_plan() {
                 g.N = 2 * llm_kv_;
                 g.rope_cols = llm_kv_;
                 g.out = kv_[l] + llm_q_;
-                add_gemm(0, "llm.qkv", l, xb_, llm_w_, L_, sub, l, qkv_bn, g);
+                add_gemm(0, "llm.qkv", l, xb_, llm_w_, Lp_, sub, l, qkv_bn, g);
             }
             tag("llm.qkv", l, kv_[l], L_, llm_qkv_n, llm_qkv_n, 1);
         }
@@ -1162,7 +1201,7 @@ void Engine::build_plan() {
             AttnParams a{};
             a.q = kv_[l];
             a.ldq = llm_qkv_n;
-            a.q_rows = L_;
+            a.q_rows = Lp_;
             a.heads = c.llm_q_heads;
             a.kv_heads = c.llm_kv_heads;
             a.k0 = kv_[l] + llm_q_;
@@ -1185,7 +1224,7 @@ void Engine::build_plan() {
             g.outb = xb_;
             g.ldob = llm_w_;
             g.out_stats = ps;
-            add_gemm(0, "llm.proj", l, llm_attn_, llm_q_, L_, Wv["llm.proj"], l, 64, g);
+            add_gemm(0, "llm.proj", l, llm_attn_, llm_q_, Lp_, Wv["llm.proj"], l, 64, g);
             tag("llm.proj", l, x_, L_, llm_w_, llm_w_, 0);
         }
         {   // llm.ln2 + fused gated FFN: up * gelu(gate)
@@ -1198,7 +1237,7 @@ void Engine::build_plan() {
             g.eps = 1e-6f;
             g.out = llm_g_;
             g.ldo = c.llm_mlp;
-            add_gemm(0, "llm.ffn", l, xb_, llm_w_, L_, Wv["llm.ffn"], l, 256, g);
+            add_gemm(0, "llm.ffn", l, xb_, llm_w_, Lp_, Wv["llm.ffn"], l, 256, g);
             tag("llm.ffn", l, llm_g_, L_, c.llm_mlp, c.llm_mlp, 1);
         }
         xs = stats_slot(0);
@@ -1212,15 +1251,26 @@ void Engine::build_plan() {
             g.outb = xb_;
             g.ldob = llm_w_;
             g.out_stats = xs;
-            add_gemm(0, "llm.down", l, llm_g_, c.llm_mlp, L_, Wv["llm.down"], l, 128, g);
+            add_gemm(0, "llm.down", l, llm_g_, c.llm_mlp, Lp_, Wv["llm.down"], l, 128, g);
             tag("llm.down", l, x_, L_, llm_w_, llm_w_, 0);
         }
     }
 
     // ================================================================ action expert (part 1)
     if (ae_mega_) {
-        build_ae_mega();
-    } else {
+        // the megakernel's planner covers prefixes of up to ~1200 rows (its combine of the
+        // attention key ranges is bounded); any longer prefix the reference accepts runs on the
+        // per-node action expert (same kernels as the prefill) instead of failing
+        try {
+            build_ae_mega();
+        } catch (const EngineError& e) {
+            if (e.code != PI0B_E_UNSUPPORTED || env_int("PI0B_AE_MEGA", 1) > 1) throw;  // 2: megakernel or fail
+            ae_mega_ = false;
+            ae_tiled_.clear();
+            ae_fallback_ = e.what();
+        }
+    }
+    if (!ae_mega_) {
     // (proj/src/builder.cpp:291-363)
     {
         Op m;
@@ -1318,7 +1368,8 @@ void Engine::build_plan() {
                 a.k0 = kv_[i % NL] + llm_q_;  // llm.qkv@mod (instance i % R)
                 a.v0 = kv_[i % NL] + llm_q_ + llm_kv_;
                 a.ld0 = llm_qkv_n;
-                a.rows0 = L_;
+                a.rows0 = Lp_;          // 32-row aligned segment boundary ...
+                a.rows0_valid = L_;     // ... cached keys [L_, Lp_) masked
                 a.k1 = aqkv_ + ae_q_;
                 a.v1 = aqkv_ + ae_q_ + ae_kv_;
                 a.ld1 = ae_qkv_n;
@@ -1425,8 +1476,15 @@ void Engine::build_ae_mega() {
         const NodeWeights& nw = W_.at(node);
         const int R = order == kTilePlain128 ? 128 : 64;
         const int kb = (nw.k + 63) / 64, nt = (rows + R - 1) / R;
-        __nv_bfloat16* t = alloc<__nv_bfloat16>(size_t(nt) * kb * R * 64);
-        ae_tiled_.push_back({nw.w.at(size_t(inst)), rows, nw.k, nw.ldk, t, order});
+        __nv_bfloat16* t = nullptr;
+        if (donor_) {  // the donor's tiled copy of the same weight instance
+            for (const TiledW& tw : donor_->ae_tiled_)
+                if (tw.src == nw.w.at(size_t(inst)) && tw.order == order && tw.rows == rows) t = tw.dst;
+            if (!t) throw EngineError(PI0B_E_STATE, "shared weights: the donor has no tiled copy of " + std::string(node));
+        } else {
+            t = alloc<__nv_bfloat16>(size_t(nt) * kb * R * 64);
+            ae_tiled_.push_back({nw.w.at(size_t(inst)), rows, nw.k, nw.ldk, t, order});
+        }
         mats.push_back(AeMat{t, rows, nw.k, kb, {0, 0, 0}});
         return int(mats.size()) - 1;
     };
@@ -1443,8 +1501,8 @@ void Engine::build_ae_mega() {
     in.act_dim = c.ae_action_dim;
     in.state_dim = c.ae_state_dim;
     in.rope_cols = ae_q_ + ae_kv_;
-    in.kv_rows0 = L_;
-    in.key_blocks = (L_ + S_ + 63) / 64;
+    in.kv_rows0 = Lp_;  // own keys start at the 32-aligned Lp_; cached keys [L_, Lp_) are masked
+    in.key_blocks = (Lp_ + S_ + 63) / 64;
     in.record = o_.record_checkpoints != 0;
     in.ao_tasks = env_int("PI0B_AE_AO_TASKS", in.ao_tasks);
     in.proj_tasks = env_int("PI0B_AE_PROJ_TASKS", in.proj_tasks);
@@ -1471,7 +1529,7 @@ void Engine::build_ae_mega() {
     }
     const int llm_qkv_n = llm_q_ + 2 * llm_kv_;
     for (int l = 0; l < c.llm_layers; ++l)  // AE instance i reads LLM layer i % llm_layers (@mod)
-        in.mat_kv.push_back(add(kv_[size_t(l)], L_, llm_qkv_n, llm_qkv_n));
+        in.mat_kv.push_back(add(kv_[size_t(l)], Lp_, llm_qkv_n, llm_qkv_n));
     in.mat_y = add(y_, S_, W, W);
     in.mat_yh = add(y_ + W, C_, W, W);  // ae.act_rows: rows 1..63
     in.mat_ap = add(ap_b_, C_, W, W);
@@ -1546,7 +1604,8 @@ void Engine::build_ae_mega() {
     P.heads = c.ae_q_heads;
     P.rope_pos0 = L_;
     P.rope_cols = ae_q_ + ae_kv_;
-    P.kv_rows0 = L_;
+    P.kv_rows0 = Lp_;
+    P.kv_valid0 = L_;
     P.kcol_cache = llm_q_;
     P.kcol_own = ae_q_;
     P.key_blocks = in.key_blocks;
@@ -1605,6 +1664,7 @@ void Engine::build_ae_mega() {
 // ------------------------------------------------------------------ weights
 
 void Engine::gen_weights(uint64_t seed) {
+    if (donor_) throw EngineError(PI0B_E_STATE, "weights are shared from another engine: load them there");
     // rtvla::gen_weights (proj/src/evaluate.cpp:38-75): W ~ U(+-1/sqrt(k)) seeded by
     // (seed, node id, instance, 1); bias role 2; bias_table row s role 4.
     for (auto& kv : W_) {
@@ -1631,6 +1691,7 @@ void Engine::gen_weights(uint64_t seed) {
 }
 
 std::string Engine::missing_weights() const {
+    if (donor_) return donor_->missing_weights();
     for (const auto& kv : W_) {
         const NodeWeights& nw = kv.second;
         for (int i = 0; i < nw.instances; ++i)
@@ -1643,6 +1704,7 @@ std::string Engine::missing_weights() const {
 
 void Engine::set_weight(const std::string& id, long long inst, const double* w, long long k, long long m,
                         const double* bias, long long blen) {
+    if (donor_) throw EngineError(PI0B_E_STATE, "weights are shared from another engine: load them there");
     auto it = W_.find(id);
     if (it == W_.end()) throw EngineError(PI0B_E_INVALID, "no weight-bearing node '" + id + "'");
     NodeWeights& nw = it->second;
@@ -1672,6 +1734,7 @@ void Engine::set_weight(const std::string& id, long long inst, const double* w, 
 }
 
 void Engine::set_bias_table(const std::string& id, const double* t, long long rows, long long m) {
+    if (donor_) throw EngineError(PI0B_E_STATE, "weights are shared from another engine: load them there");
     auto it = W_.find(id);
     if (it == W_.end() || !it->second.has_table)
         throw EngineError(PI0B_E_INVALID, "node '" + id + "' has no bias table");
@@ -1887,6 +1950,7 @@ void Engine::launch(int part, cudaStream_t st) {
         PI0B_CUDA(cudaStreamSynchronize(stream_));
         ae_tiles_dirty_ = false;
     }
+    if (donor_) donor_->prepare();  // the shared tiled AE copies are the donor's
     const int internal = part == 0 ? 2 : part - 1;  // ops filter: 2 all, 0 prefix, 1 action
     const int gidx = part;
     if (o_.use_cuda_graph && !o_.record_checkpoints) {
@@ -1941,7 +2005,8 @@ int Engine::kernel_count(int part) const {
 
 // One line per planned op: "<index> <part> <kind> <node> <inst> <grid> <detail>".
 std::string Engine::describe() const {
-    static const char* kinds[] = {"gemm", "attn", "rows_f32", "f64_bf16", "f32_f64", "memset", "skinny", "ae_mega"};
+    static const char* kinds[] = {"gemm", "attn", "rows_f32", "f64_bf16", "f32_f64", "memset", "skinny", "ae_mega",
+                                  "ve_epoch", "ve_push", "ve_wait"};
     std::string s;
     int idx = 0;
     for (const Op& op : ops_) {
@@ -1969,6 +2034,7 @@ std::string Engine::describe() const {
         s += buf;
         ++idx;
     }
+    if (!ae_fallback_.empty()) s += "# action expert on per-node kernels: " + ae_fallback_ + "\n";
     return s;
 }
 
@@ -2045,8 +2111,8 @@ using pi0b::EngineError;
 
 // ---------------------------------------------------------------------- streaming runtime
 // the full-streaming execution the reference simulates
-// (proj/src/streamsim.cpp:280-602): camera frames -> prefix into one of two KV buffers (two engines,
-// double-buffered KV) on one stream, action-expert ticks on the KV chosen by the policy on the other
+// (proj/src/streamsim.cpp:280-602): camera frames -> prefix into one of two KV buffers (two engines over
+// one weight arena, double-buffered KV) on one stream, action-expert ticks on the KV chosen by the policy on the other
 // engine's stream, a fixed-rate trajectory buffer whose commit cursor follows wall time, and the
 // reference's loop metrics (measure_loops, streamsim.cpp:520-602) on what actually ran.
 namespace pi0b {
@@ -2063,8 +2129,12 @@ void stream_run(const pi0b_model_config& cfg, uint64_t seed, const pi0b_stream_o
     using clk = std::chrono::steady_clock;
     if (o.frame_rate <= 0 || o.ae_rate <= 0 || o.trajectory_rate <= 0 || o.camera_latency < 0 || seconds <= 0)
         throw EngineError(PI0B_E_INVALID, "stream options");
-    pi0b_engine_options eo{o.device, 1, 0};
-    std::unique_ptr<Engine> eng[2] = {std::make_unique<Engine>(cfg, eo), std::make_unique<Engine>(cfg, eo)};
+    pi0b_engine_options eo{o.device, 1, 0, 0, 0};
+    // two KV buffers over ONE weight arena: the second engine borrows the first one's weights
+    std::unique_ptr<Engine> eng[2];
+    eng[0] = std::make_unique<Engine>(cfg, eo);
+    eng[1] = std::make_unique<Engine>(cfg, eo, eng[0].get());
+    eng[0]->gen_weights(seed);
     const int P = cfg.prompt_tokens, C = cfg.chunk_len, A = cfg.ae_action_dim;
     std::mt19937_64 rng(seed * 7919u + 1);
     std::uniform_real_distribution<double> U(-1.0, 1.0);
@@ -2076,9 +2146,9 @@ void stream_run(const pi0b_model_config& cfg, uint64_t seed, const pi0b_stream_o
     const std::vector<double> patches = rnd(size_t(cfg.views) * cfg.tokens_per_view * cfg.ve_patch_in);
     const std::vector<double> prompt = rnd(size_t(std::max(P, 1)) * cfg.llm_width);
     std::vector<double> state = rnd(size_t(cfg.ae_state_dim)), noise = rnd(size_t(C) * A);
-    for (auto& e : eng) {  // weights + CUDA-graph capture of both parts, outside the measured run
-        e->gen_weights(seed);
+    for (auto& e : eng) {  // CUDA-graph capture of both parts, outside the measured run
         e->prefix_async(patches.data(), P ? prompt.data() : nullptr);
+        PI0B_CUDA(cudaStreamSynchronize(e->stream()));
         e->tick_async(state.data(), noise.data());
         PI0B_CUDA(cudaStreamSynchronize(e->stream()));
     }
@@ -2088,8 +2158,12 @@ void stream_run(const pi0b_model_config& cfg, uint64_t seed, const pi0b_stream_o
         int64_t id = -1, kv = -1;
         double t_issue = 0, t_sensor = 0;
     } op[2];
-    int64_t kv_frame[2] = {-1, -1};  // completed frame whose KV each engine holds
-    int64_t next_frame = 0, sticky = -1;
+    // completed frame whose KV each engine holds (kNoKv: none).  Engine 1 starts with a pre-roll
+    // frame (-1, the warm-up prefix above) so control ticks run from t = 0, as in the reference's
+    // simulator (its AE passes start with the run); loop metrics exclude frames < 1.
+    constexpr int64_t kNoKv = -2;
+    int64_t kv_frame[2] = {kNoKv, -1};
+    int64_t next_frame = 0, sticky = kNoKv;
     double next_tick = 0.0;
     struct Slot {
         int64_t writer = -1, kv = -1;
@@ -2103,7 +2177,7 @@ void stream_run(const pi0b_model_config& cfg, uint64_t seed, const pi0b_stream_o
     auto newest = [&]() {  // engine holding the newest completed KV that is not being rewritten
         int best = -1;
         for (int e = 0; e < 2; ++e)
-            if (kv_frame[e] >= 0 && op[e].kind != 1 && (best < 0 || kv_frame[e] > kv_frame[best])) best = e;
+            if (kv_frame[e] != kNoKv && op[e].kind != 1 && (best < 0 || kv_frame[e] > kv_frame[best])) best = e;
         return best;
     };
     bool stop = false;
@@ -2142,17 +2216,17 @@ void stream_run(const pi0b_model_config& cfg, uint64_t seed, const pi0b_stream_o
         if (double(next_frame + o.camera_latency) * period <= t) {
             const int e = int(next_frame % 2);
             if (op[e].kind == 0) {
-                if (o.kv_policy == 1) sticky = newest() >= 0 ? kv_frame[newest()] : -1;
+                if (o.kv_policy == 1) sticky = newest() >= 0 ? kv_frame[newest()] : kNoKv;
                 eng[e]->prefix_async(patches.data(), P ? prompt.data() : nullptr);
                 op[e] = Op{1, next_frame, -1, now(), 0};
-                kv_frame[e] = -1;
+                kv_frame[e] = kNoKv;
                 ++next_frame;
             }
         }
         // control tick: the freshest sensor sample (2 kHz grid) and fresh noise on the chosen KV
         if (t >= next_tick) {
             int e = newest();
-            if (o.kv_policy == 1 && sticky >= 0) {  // frame_sticky: keep the KV chosen at the last VLM start
+            if (o.kv_policy == 1 && sticky != kNoKv) {  // frame_sticky: keep the KV chosen at the last VLM start
                 e = -1;
                 for (int k = 0; k < 2; ++k)
                     if (kv_frame[k] == sticky && op[k].kind != 1) e = k;
@@ -2164,7 +2238,11 @@ void stream_run(const pi0b_model_config& cfg, uint64_t seed, const pi0b_stream_o
                 const double ts = std::floor(t * 2000.0) / 2000.0;
                 eng[e]->tick_async(state.data(), noise.data());
                 op[e] = Op{2, tick_id++, kv_frame[e], now(), ts};
-                next_tick = std::max(next_tick + tick_dt, t);  // no catch-up bursts
+                // fixed-rate schedule: a tick issued late does not shift the ones after it (the
+                // average rate stays at the target); only a stall of more than 4 periods is
+                // dropped instead of being caught up in a burst
+                next_tick += tick_dt;
+                if (next_tick < t - 4.0 * tick_dt) next_tick = t;
             }
         }
     }
@@ -2228,6 +2306,23 @@ extern "C" {
 void pi0b_default_config(pi0b_model_config* c) {
     *c = pi0b_model_config{2, 0, 256, 63, 10, 27, 1152, 16, 72, 4304, 588, 18, 2048, 8, 256, 1, 16384,
                            18, 1024, 8, 256, 1, 4096, 32, 32};
+}
+
+int pi0b_engine_create_shared(const pi0b_model_config* cfg, const pi0b_engine_options* opt, pi0b_engine* donor,
+                              pi0b_engine** out) {
+    if (!cfg || !out || !donor) return pi0b::fail(EngineError(PI0B_E_INVALID, "null argument"));
+    pi0b_engine_options o{0, 1, 0, 0, 0};
+    if (opt) o = *opt;
+    PI0B_TRY({
+        auto* e = new pi0b_engine;
+        try {
+            e->impl.reset(new Engine(*cfg, o, donor->impl.get()));
+        } catch (...) {
+            delete e;
+            throw;
+        }
+        *out = e;
+    })
 }
 
 int pi0b_engine_create(const pi0b_model_config* cfg, const pi0b_engine_options* opt, pi0b_engine** out) {

@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
     const int grows = hpg * p.q_rows;
     const int kvh = grp;
     const int total = p.rows0 + p.rows1;
+    const int pad0 = p.rows0_valid > 0 ? p.rows0_valid : p.rows0;  // first padding key of segment 0
     // Key split (grid.y = S, launched as a (1, S, 1) cluster): this CTA takes key tiles
     // [t0, t0 + ntiles) and finalises rows [y * 128 / S, (y + 1) * 128 / S) of the q tile.
     const int S = gridDim.y, y = int(blockIdx.y);
@@ -311,10 +312,21 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             mbar_arrive(&s_free[sb]);
             const int kbase = (t0 + t) * kFaKeys + hf * 32;
             float mx = -INFINITY;
+            // keys past the end, and the padding keys [pad0, rows0) of segment 0, are masked; a
+            // tile that has neither (the common case) takes the unmasked loop
+            if (kbase + 32 <= total && (kbase + 32 <= pad0 || kbase >= p.rows0)) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                sv[j] = kbase + j < total ? sv[j] * p.scale_log2 : -INFINITY;
-                mx = fmaxf(mx, sv[j]);
+                for (int j = 0; j < 32; ++j) {
+                    sv[j] *= p.scale_log2;
+                    mx = fmaxf(mx, sv[j]);
+                }
+            } else {
+                const int end = total - kbase, lo = pad0 - kbase, hi = p.rows0 - kbase;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    sv[j] = j < end && (j < lo || j >= hi) ? sv[j] * p.scale_log2 : -INFINITY;
+                    mx = fmaxf(mx, sv[j]);
+                }
             }
             // row max over both key halves (the partner thread is in warp w ^ 4)
             xch[(sb * 2 + hf) * kFaRows + r] = mx;
@@ -596,7 +608,9 @@ cudaError_t launch_fattn(int head_dim, const FaMaps& maps, const AttnParams& p, 
     const int S = p.kv_splits > 1 ? p.kv_splits : 1;
     if (S != 1 && S != 2 && S != 4 && S != 8) return cudaErrorInvalidValue;
     const dim3 grid((grows + kFaRows - 1) / kFaRows, S, p.kv_heads);
-    if ((p.rows0 % 32) || (p.rows1 % 32) || (p.q_rows % 32)) return cudaErrorInvalidValue;
+    // 32-key boxes may not straddle the two key segments; one segment is read in 64-row boxes
+    // whose rows past the segment are zero-filled (and masked), so its length is free
+    if ((p.rows1 > 0 && (p.rows0 % 32)) || (p.rows1 % 32) || (p.q_rows % 32)) return cudaErrorInvalidValue;
     switch (head_dim) {
         case 72: return fa_launch_t<72, 80, 128, 3, 3>(maps, p, grid, stream);
         case 256: return fa_launch_t<256, 256, 256, 2, 2>(maps, p, grid, stream);

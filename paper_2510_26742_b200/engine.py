@@ -116,6 +116,8 @@ def lib():
         L.pi0b_last_error.restype = ctypes.c_char_p
         L.pi0b_default_config.argtypes = [cfgp]
         L.pi0b_engine_create.argtypes = [cfgp, ctypes.POINTER(EngineOptions), ctypes.POINTER(vp)]
+        if hasattr(L, "pi0b_engine_create_shared"):
+            L.pi0b_engine_create_shared.argtypes = [cfgp, ctypes.POINTER(EngineOptions), vp, ctypes.POINTER(vp)]
         L.pi0b_engine_destroy.argtypes = [vp]
         L.pi0b_engine_destroy.restype = None
         L.pi0b_engine_gen_weights.argtypes = [vp, ctypes.c_uint64]
@@ -149,11 +151,14 @@ def lib():
                                               ctypes.c_int, ctypes.c_uint64, ctypes.c_double, ctypes.c_double, vp]
         L.pi0b_seed_hash.argtypes = [ctypes.c_uint64, ctypes.c_char_p, ctypes.c_uint64, ctypes.c_uint64]
         L.pi0b_seed_hash.restype = ctypes.c_uint64
-        L.pi0b_engine_ve_buffers.argtypes = [vp, ctypes.POINTER(VeBuffers)]
-        L.pi0b_engine_set_ve_peers.argtypes = [vp, ctypes.POINTER(VeBuffers), ctypes.c_int]
-        L.pi0b_ipc_export.argtypes = [vp, ctypes.c_char_p]
-        L.pi0b_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
-        L.pi0b_ipc_close.argtypes = [vp]
+        # (entry points an older build may lack: PI0B_LIB A/B runs against earlier libraries)
+        for name, args in (("pi0b_engine_ve_buffers", [vp, ctypes.POINTER(VeBuffers)]),
+                           ("pi0b_engine_set_ve_peers", [vp, ctypes.POINTER(VeBuffers), ctypes.c_int]),
+                           ("pi0b_ipc_export", [vp, ctypes.c_char_p]),
+                           ("pi0b_ipc_open", [ctypes.c_char_p, ctypes.POINTER(vp)]),
+                           ("pi0b_ipc_close", [vp])):
+            if hasattr(L, name):
+                getattr(L, name).argtypes = args
         _lib = L
     return _lib
 
@@ -198,7 +203,7 @@ EXPORTED_SYMBOLS = [
     "pi0b_attention_ws_floats", "pi0b_random_f64", "pi0b_random_packed_bf16", "pi0b_seed_hash",
     "pi0b_engine_run_images", "pi0b_image_patches", "pi0b_stream_run", "pi0b_f64_to_bf16_host",
     "pi0b_premultiply_rows", "pi0b_fold_time_mlp", "pi0b_time_embedding",
-    "pi0b_engine_ve_buffers", "pi0b_engine_set_ve_peers", "pi0b_ipc_export", "pi0b_ipc_open", "pi0b_ipc_close",
+    "pi0b_engine_create_shared", "pi0b_engine_ve_buffers", "pi0b_engine_set_ve_peers", "pi0b_ipc_export", "pi0b_ipc_open", "pi0b_ipc_close",
 ]
 
 
@@ -230,12 +235,20 @@ class Engine:
     """One pi0 engine on one B200 (weights, activations, KV cache, captured CUDA graphs)."""
 
     def __init__(self, cfg: ModelConfig, device: int = 0, use_cuda_graph: bool = True,
-                 record_checkpoints: bool = False, ve_shards: int = 0, ve_shard: int = 0):
+                 record_checkpoints: bool = False, ve_shards: int = 0, ve_shard: int = 0,
+                 share_weights_with: "Engine | None" = None):
+        """share_weights_with: read that engine's weight arena (include/pi0b.h
+        pi0b_engine_create_shared); it must stay alive as long as this one."""
         self.cfg = cfg
         self._h = ctypes.c_void_p()
+        self._donor = share_weights_with
         opt = EngineOptions(device, int(use_cuda_graph), int(record_checkpoints), ve_shards, ve_shard)
-        _raise(lib().pi0b_engine_create(ctypes.byref(cfg), ctypes.byref(opt), ctypes.byref(self._h)),
-               "pi0b_engine_create")
+        if share_weights_with is None:
+            _raise(lib().pi0b_engine_create(ctypes.byref(cfg), ctypes.byref(opt), ctypes.byref(self._h)),
+                   "pi0b_engine_create")
+        else:
+            _raise(lib().pi0b_engine_create_shared(ctypes.byref(cfg), ctypes.byref(opt), share_weights_with._h,
+                                                   ctypes.byref(self._h)), "pi0b_engine_create_shared")
 
     def close(self):
         if self._h:

@@ -4,7 +4,7 @@ reference's loop metrics (rtvla::measure_loops semantics) on what actually ran."
 import pytest
 
 from paper_2510_26742_b200 import engine as E
-from paper_2510_26742_b200.config import mid_config
+from paper_2510_26742_b200.config import default_config, mid_config
 
 pytestmark = pytest.mark.gpu
 
@@ -19,3 +19,55 @@ def test_stream_runtime_mid(policy):
     assert r["quick_count"] > 100 and 0.0 < r["quick_mean_ms"] < 10.0
     assert r["slow_count"] >= 20 and r["slow_mean_ms"] > 2 * 1000.0 / 30.0  # includes 2 frames of camera latency
     assert r["committed_slots"] > 400
+
+
+def test_shared_weight_engines():
+    """pi0b_engine_create_shared: a second engine over the first one's weight arena (the streaming
+    runtime's second KV buffer) computes the same actions and refuses its own weight loads."""
+    import numpy as np
+
+    from oracle import oracle as O
+    cfg = mid_config(views=2)
+    e0 = E.Engine(cfg)
+    e0.gen_weights(1)
+    e1 = E.Engine(cfg, share_weights_with=e0)
+    x = O.gen_inputs(cfg, 3)
+    y1 = e1.run(x["patches"], x["state"], x["noise"])
+    y0 = e0.run(x["patches"], x["state"], x["noise"])
+    assert np.abs(y1 - y0).max() < 0.02
+    with pytest.raises(RuntimeError):
+        e1.gen_weights(1)
+    e1.close()
+
+
+def test_stream_runtime_vs_reference_simulator():
+    """the runtime sustains the paper's 480 Hz (>= 0.99 x target) on the full
+    2-view model, and its measured quick / slow loops agree with the reference's own event
+    simulator (proj/src/streamsim.cpp simulate + measure_loops, compiled unmodified into
+    oracle/_ref/streamsim_driver) fed this run's measured prefix and 1-step AE times."""
+    import json
+    import os
+    import subprocess
+
+    driver = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                          "streamsim_driver")
+    cfg = default_config(views=2).replace(flow_steps=1)
+    r = E.stream_run(cfg, 3.0, ae_rate=480.0, kv_policy="most_recent")
+    sim = json.loads(subprocess.run([driver, repr(r["prefix_p50_ms"] / 1e3), repr(r["tick_p50_ms"] / 1e3), "480.0",
+                                     "3.0", "most_recent"], check=True, capture_output=True, text=True).stdout)
+    loops = sim["loops"]
+    doc = {"measured": r, "simulated": {"quick_mean_ms": loops["quick_loop"]["mean"] * 1e3,
+                                        "slow_mean_ms": loops["slow_loop"]["mean"] * 1e3,
+                                        "ae_per_s": loops["ae_per_s"], "vlm_per_s": loops["vlm_per_s"],
+                                        "eta": sim["eta"]}}
+    print(json.dumps(doc, indent=1))
+    out = os.environ.get("PI0B_PARITY_OUT")
+    if out:
+        os.makedirs(out, exist_ok=True)
+        json.dump(doc, open(os.path.join(out, "stream_vs_sim_2v.json"), "w"), indent=1)
+    assert r["ae_per_s"] >= 0.99 * 480.0, r
+    assert abs(r["vlm_per_s"] - 30.0) < 1.5, r
+    q, qs = r["quick_mean_ms"], doc["simulated"]["quick_mean_ms"]
+    s_, ss = r["slow_mean_ms"], doc["simulated"]["slow_mean_ms"]
+    assert abs(q - qs) / qs < 0.25, doc
+    assert abs(s_ - ss) / ss < 0.10, doc
