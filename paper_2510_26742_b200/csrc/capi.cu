@@ -151,6 +151,7 @@ int pi0b_attention(const pi0b_attn_desc* d, void* stream) {
     p.v0 = static_cast<const __nv_bfloat16*>(d->v0);
     p.ld0 = d->ld0;
     p.rows0 = d->rows0;
+    p.rows0_valid = d->rows0_valid;
     p.k1 = static_cast<const __nv_bfloat16*>(d->k1);
     p.v1 = static_cast<const __nv_bfloat16*>(d->v1);
     p.ld1 = d->ld1;

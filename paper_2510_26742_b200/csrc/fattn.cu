@@ -517,18 +517,34 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             }
         }
         if (tid == 0) FA_STAMP(6);
-        // coalesced copy-out of the staged rows [row_lo, row_hi): D bf16 of each row
+        // coalesced copy-out of the staged rows [row_lo, row_hi): D bf16 of each row.  Each row's
+        // global address (stacked head -> head, row) is computed once, into a table in the P
+        // buffers (free: every PV MMA is done), so the copy loop has no integer divisions.
+        __nv_bfloat16** rowptr = reinterpret_cast<__nv_bfloat16**>(sP);
+        if (tid < kFaRows) {
+            const int gg = qt * kFaRows + tid;
+            rowptr[tid] = gg < grows ? p.out + (long long)(gg % p.q_rows) * p.ldo + (kvh + p.kv_heads * (gg / p.q_rows)) * D
+                                     : nullptr;
+        }
         named_bar_sync(5, 256);
         if (tid == 0) FA_STAMP(12);
         constexpr int CPR = (D * 2 + 15) / 16;  // 16-byte chunks per output row
-        const int n = (row_hi - row_lo) * CPR;
-        for (int e = tid; e < n; e += 256) {
-            const int rr = row_lo + e / CPR, q = e % CPR;
-            const int gg = qt * kFaRows + rr;
-            if (gg >= grows) continue;
-            const uint4 v = *reinterpret_cast<const uint4*>(sQ + rr * C::ROW_BYTES + ((q ^ (rr & 7)) << 4));
-            __nv_bfloat16* orow = p.out + (long long)(gg % p.q_rows) * p.ldo + (kvh + p.kv_heads * (gg / p.q_rows)) * D;
-            *reinterpret_cast<uint4*>(orow + q * 8) = v;
+        if constexpr (CPR == 32) {  // D = 256: one row per warp and iteration, lane = chunk
+            for (int rr = row_lo + warp; rr < row_hi; rr += 8) {
+                __nv_bfloat16* orow = rowptr[rr];
+                if (!orow) continue;
+                const uint4 v = *reinterpret_cast<const uint4*>(sQ + rr * C::ROW_BYTES + ((lane ^ (rr & 7)) << 4));
+                *reinterpret_cast<uint4*>(orow + lane * 8) = v;
+            }
+        } else {
+            const int n = (row_hi - row_lo) * CPR;
+            for (int e = tid; e < n; e += 256) {
+                const int rr = row_lo + e / CPR, q = e - (e / CPR) * CPR;
+                __nv_bfloat16* orow = rowptr[rr];
+                if (!orow) continue;
+                const uint4 v = *reinterpret_cast<const uint4*>(sQ + rr * C::ROW_BYTES + ((q ^ (rr & 7)) << 4));
+                *reinterpret_cast<uint4*>(orow + q * 8) = v;
+            }
         }
         if (tid == 0) FA_STAMP(13);
         (void)row_ok;

@@ -97,6 +97,7 @@ class AttnDesc(ctypes.Structure):
         ("out", ctypes.c_void_p), ("ldo", ctypes.c_int64),
         ("kv_splits", ctypes.c_int),
         ("ws", ctypes.c_void_p), ("counters", ctypes.c_void_p),
+        ("rows0_valid", ctypes.c_int),
     ]
 
 

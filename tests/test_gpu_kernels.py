@@ -198,14 +198,19 @@ def _attn_ref(q, k, v, heads, kv_heads, hd):
     return out
 
 
-@pytest.mark.parametrize("hd,heads,kv_heads,q_rows,rows0,rows1,splits", [
-    (72, 16, 16, 512, 512, 0, 0), (72, 16, 16, 768, 768, 0, 0), (72, 4, 4, 256, 256, 0, 2),
-    (256, 8, 1, 512, 512, 0, 0), (256, 8, 1, 800, 800, 0, 0), (256, 8, 1, 512, 512, 0, 1),
-    (256, 8, 1, 64, 512, 64, 0), (256, 8, 1, 64, 800, 64, 0), (256, 2, 1, 64, 256, 64, 4),
-    (72, 16, 16, 512, 512, 0, 2), (256, 8, 1, 512, 512, 0, 4), (256, 8, 1, 800, 800, 0, 8),
-    (72, 16, 16, 768, 768, 0, 8),
+@pytest.mark.parametrize("hd,heads,kv_heads,q_rows,rows0,rows1,splits,rows0_valid", [
+    (72, 16, 16, 512, 512, 0, 0, 0), (72, 16, 16, 768, 768, 0, 0, 0), (72, 4, 4, 256, 256, 0, 2, 0),
+    (256, 8, 1, 512, 512, 0, 0, 0), (256, 8, 1, 800, 800, 0, 0, 0), (256, 8, 1, 512, 512, 0, 1, 0),
+    (256, 8, 1, 64, 512, 64, 0, 0), (256, 8, 1, 64, 800, 64, 0, 0), (256, 2, 1, 64, 256, 64, 4, 0),
+    (72, 16, 16, 512, 512, 0, 2, 0), (256, 8, 1, 512, 512, 0, 4, 0), (256, 8, 1, 800, 800, 0, 8, 0),
+    (72, 16, 16, 768, 768, 0, 8, 0),
+    # unaligned prefixes (any prompt length): one segment of 557 keys read in 64-row boxes with the
+    # rows past it zero-filled and masked; and a 32-aligned segment of 576 rows whose last 19 are
+    # padding (rows0_valid) ahead of the action expert's own 64 keys
+    (256, 8, 1, 576, 557, 0, 0, 0), (256, 8, 1, 576, 557, 0, 4, 0), (72, 16, 16, 288, 275, 0, 0, 0),
+    (256, 8, 1, 64, 576, 64, 0, 557), (256, 2, 1, 64, 800, 64, 2, 775),
 ])
-def test_attention(hd, heads, kv_heads, q_rows, rows0, rows1, splits):
+def test_attention(hd, heads, kv_heads, q_rows, rows0, rows1, splits, rows0_valid):
     # q/k/v live in one qkv-style buffer like the engine's (row stride = q + 2 kv)
     qw, kvw = heads * hd, kv_heads * hd
     ld = qw + 2 * kvw
@@ -225,17 +230,19 @@ def test_attention(hd, heads, kv_heads, q_rows, rows0, rows1, splits):
         d.k1, d.v1, d.ld1, d.rows1 = Y[:, qw:qw + kvw].data_ptr(), Y[:, qw + kvw:].data_ptr(), ld, rows1
     d.out, d.ldo = out.data_ptr(), qw
     d.kv_splits = splits
+    d.rows0_valid = rows0_valid
     n_ws = E.attention_ws_floats(d)
     ws = torch.zeros(max(1, n_ws), device=dev)
     ctr = torch.zeros(4096, dtype=torch.int32, device=dev)
     d.ws, d.counters = ws.data_ptr(), ctr.data_ptr()
     E.attention(d)
     torch.cuda.synchronize()
+    n0 = rows0_valid or rows0  # padding keys of segment 0 take no part
     if rows1:
-        kk = torch.cat([k0, Y[:, qw:qw + kvw]], 0)
-        vv = torch.cat([v0, Y[:, qw + kvw:]], 0)
+        kk = torch.cat([k0[:n0], Y[:, qw:qw + kvw]], 0)
+        vv = torch.cat([v0[:n0], Y[:, qw + kvw:]], 0)
     else:
-        kk, vv = k0, v0
+        kk, vv = k0[:n0], v0[:n0]
     ref = _attn_ref(q, kk, vv, heads, kv_heads, hd)
     _close(out, ref, 2e-2)
     assert int(ctr.abs().max()) == 0
