@@ -223,6 +223,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int S = p.splits;  // cluster size along K (grid.z)
     // split-K combine by st.async pushes into the peers' drained pipeline smem (see the epilogue)
     const bool push = S > 1 && S * (BN / 32) * 16384 <= STAGES * Cfg::STAGE_BYTES;
+    // Staged epilogue: a single-tile CTA (no persistence, no CTA pair / multi-tile) writes its
+    // finished 32-column chunks as fp32 into the drained pipeline smem (past the split-K receive
+    // slots) and then copies them out with whole-warp, row-contiguous stores -- per-thread row
+    // stores (32 rows x 16 B per warp instruction) cost ~1.5 us per 32 KB tile
+    // (DESIGN.md 5).  Chunk c of the tile lives at stage_off + c * 16 KB, [128 rows][128 B],
+    // 16-byte pieces XOR-swizzled by row.
+    constexpr int NCH = BN / 32;
+    const int stage_off = S > 1 ? S * NCH * 16384 : 0;
+    const bool staged = !kPaired && !persist && MT == 1 && CG == 1 && (S == 1 || push) &&
+                        stage_off + NCH * 16384 <= STAGES * Cfg::STAGE_BYTES &&
+                        MODE == kModeResid;  // (bf16-output tiles measured slower staged: 8.3 -> 8.8 us ve.qkv)
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
@@ -465,6 +476,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
             }
         };
+        const uint32_t sstage = smem_u32(smem) + uint32_t(stage_off) + row_in_tile * 128;
+        auto stage32 = [&](int c, const float(&v)[32]) {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj)
+                st_shared_v4(sstage + c * 16384 + ((jj ^ sw) << 4), v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
+        };
         if constexpr (MODE == kModeResid) {
             // h += scale*(rs*z + b) in place, bf16 shadow, row stats.
             float ss = 0.f;
@@ -484,8 +501,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
 #pragma unroll
                 for (int j = 0; j < 32; ++j) h[j] += p.resid_scale * (v[j] * rs + sm_vec[c * 32 + j]);
-                store_f32x32(hp, h, nv);
                 ss += sumsq32(h, nv);
+                if (staged) {
+                    stage32(c, h);
+                    continue;
+                }
+                store_f32x32(hp, h, nv);
                 if (p.outb)
                     store_bf16x32(reinterpret_cast<__nv_bfloat16*>(p.outb) + (long long)r * p.ldob + col0, h, nv);
             }
@@ -572,6 +593,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     ss += sumsq32(v, nv);
                     if (p.outb)
                         store_bf16x32(reinterpret_cast<__nv_bfloat16*>(p.outb) + (long long)r * p.ldob + col0, v, nv);
+                } else if (staged) {
+                    stage32(c, v);
                 } else {
                     store_bf16x32(reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)r * p.ldo + col0, v, nv);
                 }
@@ -591,6 +614,43 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         s0 += x * x;
                     }
                     if (p.out_stats) atomicAdd(p.out_stats - 1, s0);
+                }
+            }
+        }
+        if (staged) {
+            // coalesced copy-out of the staged chunks this CTA owns (split-K: c % S == rank):
+            // piece e = (row, 16-byte piece q) of chunk c; a warp writes 4 rows x 128 B (fp32) /
+            // 4 rows x 64 B (bf16), each row segment contiguous in global memory
+            named_bar_sync(1, 256);
+            const uint8_t* sbase = smem + stage_off;
+#pragma unroll 1
+            for (int c = S > 1 ? rank : 0; c < NCH; c += S > 1 ? S : 1) {
+                const int colc = n0 + c * 32;
+#pragma unroll 2
+                for (int e = etid; e < 128 * 8; e += 256) {
+                    const int row = e >> 3, qq = e & 7;
+                    const int gr = m_tile * BM + row, col = colc + qq * 4;
+                    if (gr >= p.M || col >= p.N) continue;
+                    const float4 f = *reinterpret_cast<const float4*>(sbase + c * 16384 + row * 128 + ((qq ^ (row & 7)) << 4));
+                    const uint2 b = make_uint2(pack_bf16(f.x, f.y), pack_bf16(f.z, f.w));
+                    if (col + 4 <= p.N) {
+                        if constexpr (MODE == kModeResid) {
+                            *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + (long long)gr * p.ldo + col) = f;
+                            if (p.outb) *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.outb) + (long long)gr * p.ldob + col) = b;
+                        } else {
+                            *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)gr * p.ldo + col) = b;
+                        }
+                    } else {
+                        const float fv[4] = {f.x, f.y, f.z, f.w};
+                        for (int k = 0; k < 4 && col + k < p.N; ++k) {
+                            if constexpr (MODE == kModeResid) {
+                                reinterpret_cast<float*>(p.out)[(long long)gr * p.ldo + col + k] = fv[k];
+                                if (p.outb) reinterpret_cast<__nv_bfloat16*>(p.outb)[(long long)gr * p.ldob + col + k] = __float2bfloat16_rn(fv[k]);
+                            } else {
+                                reinterpret_cast<__nv_bfloat16*>(p.out)[(long long)gr * p.ldo + col + k] = __float2bfloat16_rn(fv[k]);
+                            }
+                        }
+                    }
                 }
             }
         }
