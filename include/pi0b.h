@@ -244,7 +244,8 @@ typedef struct pi0b_attn_desc {
     const void* k1; const void* v1; int64_t ld1; int rows1;
     void* out; int64_t ldo;
     int kv_splits;                  /* 0/1: one pass; 2, 4, 8: key splits (cluster) */
-    float* ws; int* counters;       /* unused (DSMEM combine); kept for ABI layout  */
+    float* ws; int* counters;       /* ws: key-split workspace, pi0b_attention_ws_floats() floats
+                                       (kv_splits > 1); counters: unused, kept for ABI layout */
     int rows0_valid;                /* > 0: keys [rows0_valid, rows0) of segment 0 are padding (masked) */
 } pi0b_attn_desc;
 int pi0b_attention(const pi0b_attn_desc* d, void* stream);

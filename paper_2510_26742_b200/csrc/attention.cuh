@@ -30,13 +30,25 @@ struct AttnParams {
     __nv_bfloat16* out;       // [q_rows, heads*d]
     long long ldo;
     int kv_splits;            // grid.y = key splits (1, 2, 4, 8): a (1, S, 1) cluster per q tile,
-                              // partials combined over DSMEM (no workspace)
+                              // partials exchanged through `ws` (attention_ws_bytes) + a cluster barrier
+    void* ws;                 // key-split workspace (kv_splits > 1)
     int kv_per_split;         // informational: keys per split
 };
 
 // Tensor maps of one attention launch (fattn.cu make_fattn_maps): Q [q_rows, heads*d] and the two
 // key / value segments [rows, kv_heads*d], bf16, boxes of 64 columns x 32 (Q; K/V of two segments)
 // or 64 rows (K/V of one segment), 128-byte swizzle.
+// Bytes of the key-split workspace of one launch (0 when kv_splits <= 1).
+inline long long attention_ws_bytes(const AttnParams& p, int head_dim) {
+    const int S = p.kv_splits > 1 ? p.kv_splits : 1;
+    if (S == 1) return 0;
+    const int dv = head_dim == 72 ? 128 : head_dim;  // fattn.cu DV (PV width)
+    const long long grows = (long long)(p.heads / p.kv_heads) * p.q_rows;
+    const long long tiles = (grows + 127) / 128 * p.kv_heads;
+    const long long blk = (128 / S) * (2LL * dv + 8);
+    return tiles * S * S * blk;
+}
+
 struct FaMaps {
     CUtensorMap q, k0, v0, k1, v1;
     int kv_box;  // key rows per K/V box: 64 (one key segment) or 32 (a tile may straddle two)

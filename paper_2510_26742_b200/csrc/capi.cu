@@ -133,8 +133,13 @@ int pi0b_gemm(const pi0b_gemm_desc* d, void* stream) {
 }
 
 int64_t pi0b_attention_ws_floats(const pi0b_attn_desc* d) {
-    (void)d;
-    return 0;  // single-pass tcgen05 attention needs no workspace
+    // key splits (kv_splits > 1) exchange their partial rows through this workspace
+    pi0b::AttnParams p{};
+    p.q_rows = d->q_rows;
+    p.heads = d->heads;
+    p.kv_heads = d->kv_heads;
+    p.kv_splits = d->kv_splits;
+    return (pi0b::attention_ws_bytes(p, d->head_dim) + 3) / 4;
 }
 
 int pi0b_attention(const pi0b_attn_desc* d, void* stream) {
@@ -161,6 +166,8 @@ int pi0b_attention(const pi0b_attn_desc* d, void* stream) {
     p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(d->head_dim)));
     p.kv_splits = d->kv_splits > 1 ? d->kv_splits : 1;  // 2, 4, 8: key splits combined over DSMEM
     p.kv_per_split = d->rows0 + d->rows1;
+    p.ws = d->ws;
+    if (p.kv_splits > 1 && !p.ws) return PI0B_E_INVALID;  // see pi0b_attention_ws_floats
     try {
         const FaMaps m = make_fattn_maps(p, d->head_dim);
         return int(launch_fattn(d->head_dim, m, p, static_cast<cudaStream_t>(stream)));

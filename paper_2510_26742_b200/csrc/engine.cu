@@ -956,6 +956,7 @@ void Engine::add_attn(int part, const std::string& node, int inst, int hd, AttnP
     ap.scale_log2 = float(1.4426950408889634 / std::sqrt(double(hd)));
     if ((ap.rows1 > 0 && (ap.rows0 % 32)) || (ap.rows1 % 32) || (ap.q_rows % 32))
         throw EngineError(PI0B_E_UNSUPPORTED, "attention: two key segments need 32-row multiples");
+    if (ap.kv_splits > 1) ap.ws = alloc<uint8_t>(size_t(attention_ws_bytes(ap, hd)));
     op.fm = make_fattn_maps(ap, hd);
     op.ap = ap;
     ops_.push_back(op);

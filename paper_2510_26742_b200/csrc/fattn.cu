@@ -414,23 +414,20 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                 stage_row(r, o, c, il);
             }
         } else {
-            // ---------------- key-split combine (push form)
+            // ---------------- key-split combine through L2
             // Every split stages the normalised partial rows it does not own (bf16) and their
-            // (max, sum) in its drained V ring, one contiguous block per owner; one thread then
-            // bulk-copies each block into the owner's drained K ring (DSMEM, complete_tx on the
-            // owner's recv_full).  Block = own_rows rows of ROW_BYTES (16-byte chunk q of local
-            // row i at q ^ (i & 7)) followed by own_rows (max, sum) pairs.
+            // (max, sum) in its drained V ring, one contiguous block per owner, and writes the
+            // blocks to the global workspace with coalesced stores; after one cluster barrier
+            // (release / acquire: the blocks are visible) each split copies the blocks of its own
+            // rows into its drained K ring and combines them.  Block = own_rows rows of ROW_BYTES
+            // (16-byte chunk q of local row i at q ^ (i & 7)) followed by own_rows (max, sum)
+            // pairs.  (Pushing the same blocks into the owners' smem with DSMEM bulk copies took
+            // ~4.6 us at S = 4 -- scripts/fa_trace.py, round 2 -- against ~1 us through L2.)
             row_lo = y * own_rows;
             row_hi = row_lo + own_rows;
             const int blk = own_rows * (C::ROW_BYTES + 8);
             auto slot_of = [&](int sender, int owner_rank) { return sender < owner_rank ? sender : sender - 1; };
-            if (tid == 0) {
-                // this CTA's K ring is drained (all MMAs done): arm the receive barrier, then
-                // let the peers push
-                mbar_arrive_expect_tx(recv_full, uint32_t((S - 1) * blk));
-                for (int k = 0; k < S; ++k)
-                    if (k != y) mbar_arrive_cluster(mapa_shared(smem_u32(peers_free), uint32_t(k)));
-            }
+            uint8_t* wsb = static_cast<uint8_t*>(p.ws) + size_t(blockIdx.z * gridDim.x + blockIdx.x) * S * S * blk;
             const int owner = r / own_rows, lrow = r - owner * own_rows;
             // TMEM reads stay warp-converged (tcgen05.ld is .sync.aligned; with 8+ splits a warp
             // spans two owners): every thread stages its normalised partial, into the outgoing
@@ -453,30 +450,42 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                                    pack_bf16(o[j + 4] * il, o[j + 5] * il), pack_bf16(o[j + 6] * il, o[j + 7] * il));
                 }
             }
-            if (owner != y && hf == 0)
-                reinterpret_cast<float2*>(ob + own_rows * C::ROW_BYTES)[lrow] = make_float2(l > 0.f ? m_ref : -INFINITY, l);
-            fence_proxy_async();  // generic-proxy stores -> the bulk copy engine
+            if (hf == 0)  // (max, sum) of every row: into the outgoing block, or for own rows into sP + 2 KB
+                (owner != y ? reinterpret_cast<float2*>(ob + own_rows * C::ROW_BYTES) : reinterpret_cast<float2*>(sP + 2048))[lrow] =
+                    make_float2(l > 0.f ? m_ref : -INFINITY, l);
             named_bar_sync(6, 256);
-            if (tid == 0) {
-                mbar_wait_cluster(peers_free, 0);
-                for (int k = 0; k < S; ++k) {
-                    if (k == y) continue;
-                    const uint32_t dst = mapa_shared(smem_u32(sK + slot_of(y, k) * blk), uint32_t(k));
-                    const uint32_t bar = mapa_shared(smem_u32(recv_full), uint32_t(k));
-                    asm volatile(
-                        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                        "r"(smem_u32(sV + slot_of(k, y) * blk)), "r"(uint32_t(blk)), "r"(bar)
-                        : "memory");
-                }
-                FA_STAMP(7);
+            if (tid == 0) FA_STAMP(14);
+            // outgoing blocks -> workspace [tile][sender][owner]
+            for (int k = 0; k < S; ++k) {
+                if (k == y) continue;
+                const uint4* src = reinterpret_cast<const uint4*>(sV + slot_of(k, y) * blk);
+                uint4* dst = reinterpret_cast<uint4*>(wsb + size_t(y * S + k) * blk);
+                for (int e = tid; e < blk / 16; e += 256) dst[e] = src[e];
             }
-            if (owner == y) {
-                mbar_wait_cluster(recv_full, 0);
-                // o = sum_j w_j O_j / sum_j w_j over the S normalised partials, w_j = l_j 2^(m_j - M)
-                const float m_own = l > 0.f ? m_ref : -INFINITY;
+            if (tid == 0) FA_STAMP(7);
+            cluster_sync_all();  // (warps 8 and 9 arrive at the end of their roles)
+            if (tid == 0) FA_STAMP(15);
+            // incoming blocks of this split's rows -> the drained K ring
+            for (int k = 0; k < S; ++k) {
+                if (k == y) continue;
+                const uint8_t* src = wsb + size_t(k * S + y) * blk;
+                uint8_t* dst = sK + slot_of(k, y) * blk;
+                for (int e = tid; e < blk / 16; e += 256) cp_async16(dst + e * 16, src + e * 16, true);
+            }
+            cp_async_commit();
+            cp_async_wait<0>();
+            named_bar_sync(6, 256);
+            // o = sum_j w_j O_j / sum_j w_j over the S normalised partials, w_j = l_j 2^(m_j - M),
+            // spread over all 256 threads (own_rows rows x DV columns; a per-row-thread combine
+            // leaves the work to the two warps of one sub-partition)
+            {
+                constexpr int DVC = DV / 8;                 // 16-byte chunks per row
+                const int segs = 256 / own_rows;             // threads per row
+                const int cps = DVC / segs;                  // chunks per thread (>= 1: own_rows >= 16)
+                const int lr = tid / segs, c0 = (tid % segs) * cps;
+                const float2* ml_own = reinterpret_cast<const float2*>(sP + 2048);
                 auto ml_of = [&](int k) {
-                    return k == y ? make_float2(m_own, l)
-                                  : reinterpret_cast<const float2*>(sK + slot_of(k, y) * blk + own_rows * C::ROW_BYTES)[lrow];
+                    return k == y ? ml_own[lr] : reinterpret_cast<const float2*>(sK + slot_of(k, y) * blk + own_rows * C::ROW_BYTES)[lr];
                 };
                 float M = -INFINITY;
                 for (int k = 0; k < S; ++k) M = fmaxf(M, ml_of(k).x);
@@ -491,29 +500,30 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                     }
                 }
                 const float iden = den > 0.f ? 1.f / den : 0.f;
+                const uint8_t* own_src = sQ + (row_lo < kFaRows / 2 ? kFaRows / 2 : 0) * C::ROW_BYTES;
+                const int rr = row_lo + lr;  // tile row of the output
 #pragma unroll 1
-                for (int c = 0; c < DV / 64; ++c) {
-                    float o[32];
+                for (int cc = 0; cc < cps; ++cc) {
+                    const int q = c0 + cc;
+                    float o[8];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) o[j] = 0.f;
+                    for (int e = 0; e < 8; ++e) o[e] = 0.f;
 #pragma unroll 1
                     for (int k = 0; k < S; ++k) {
-                        const uint8_t* src = (k == y ? ob : sK + slot_of(k, y) * blk) + lrow * C::ROW_BYTES;
+                        const uint8_t* src = (k == y ? own_src : sK + slot_of(k, y) * blk) + lr * C::ROW_BYTES;
+                        const uint4 u = *reinterpret_cast<const uint4*>(src + ((q ^ (lr & 7)) << 4));
+                        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-                        for (int j = 0; j < 32; j += 8) {
-                            const int q = hf * HC + (c * 32 + j) / 8;
-                            const uint4 u = *reinterpret_cast<const uint4*>(src + ((q ^ (lrow & 7)) << 4));
-                            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                o[j + 2 * e] += wk[k] * __uint_as_float(w4[e] << 16);
-                                o[j + 2 * e + 1] += wk[k] * __uint_as_float(w4[e] & 0xffff0000u);
-                            }
+                        for (int e = 0; e < 4; ++e) {
+                            o[2 * e] += wk[k] * __uint_as_float(w4[e] << 16);
+                            o[2 * e + 1] += wk[k] * __uint_as_float(w4[e] & 0xffff0000u);
                         }
                     }
-                    stage_row(r, o, c, iden);
+                    *reinterpret_cast<uint4*>(sQ + rr * C::ROW_BYTES + ((q ^ (rr & 7)) << 4)) =
+                        make_uint4(pack_bf16(o[0] * iden, o[1] * iden), pack_bf16(o[2] * iden, o[3] * iden),
+                                   pack_bf16(o[4] * iden, o[5] * iden), pack_bf16(o[6] * iden, o[7] * iden));
                 }
-                if (tid == y * own_rows) FA_STAMP(8);
+                if (tid == 0) FA_STAMP(8);
             }
         }
         if (tid == 0) FA_STAMP(6);
@@ -549,11 +559,11 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
         if (tid == 0) FA_STAMP(13);
         (void)row_ok;
     }
-    // Key splits: the bulk copies read this CTA's V ring after its softmax threads moved on; the
-    // cluster barrier (every owner has seen its recv_full) keeps all sources alive until then.
+    // Key splits: the MMA and TMA warps take part in the softmax warps' cluster barrier (the
+    // workspace exchange above); nothing crosses CTAs after it.
     tc_fence_before();
-    if (S > 1) cluster_sync_all();
-    else __syncthreads();
+    if (S > 1 && warp >= 8) cluster_sync_all();
+    __syncthreads();
     if (tid == 0) FA_STAMP(9);
     if (warp == 8) tmem_dealloc(tmem, C::TMEM_COLS);
 }

@@ -18,7 +18,7 @@ from paper_2510_26742_b200 import engine as E  # noqa: E402
 views = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 T = 256 * views
 STAMPS = ["start", "pdl", "setup", "s_full0", "softmax_end", "o_done", "staged", "copies_issued", "combined", "exit",
-          "tma_go", "mma_qk0", "bar5", "stored"]
+          "tma_go", "mma_qk0", "bar5", "stored", "split_staged", "cluster_bar"]
 
 
 def run(name, hd, q_rows, heads, kv_heads, rows0, splits, reps=20):
@@ -33,6 +33,8 @@ def run(name, hd, q_rows, heads, kv_heads, rows0, splits, reps=20):
     d.k0, d.v0, d.ld0, d.rows0 = X[:, qw:].data_ptr(), X[:, qw + kvw:].data_ptr(), ld, rows0
     d.out, d.ldo = out.data_ptr(), qw
     d.kv_splits = splits
+    ws = torch.zeros(max(1, E.attention_ws_floats(d)), device=dev)  # key-split workspace
+    d.ws = ws.data_ptr()
     grows = heads // kv_heads * q_rows
     ctas = ((grows + 127) // 128) * max(1, splits) * kv_heads
     buf = torch.zeros(ctas * 16, dtype=torch.int64, device=dev)
