@@ -27,6 +27,8 @@
 
 #include <math.h>
 
+#include <cstdlib>
+
 namespace pi0b {
 
 namespace {
@@ -94,26 +96,29 @@ extern "C" int pi0b_fa_trace_buffer(unsigned long long* p) {
 
 // D = real head dim, DK = QK contraction (D padded to 16), DV = PV width (D padded to 64),
 // KK / KV = key / value ring depths.
-template <int D, int DK, int DV, int KK, int KV>
+template <int D, int DK, int DV, int KK, int KV, int KEYS>
 struct FaCfg {
     static constexpr int QA = (DK + 63) / 64;  // 64-col regions of Q / K
     static constexpr int VA = DV / 64;         // 64-col regions of V
     static constexpr int Q_BYTES = QA * kFaRows * 128;
-    static constexpr int K_BYTES = QA * kFaKeys * 128;
-    static constexpr int V_BYTES = VA * kFaKeys * 128;
-    static constexpr int P_BYTES = kFaRows * 128;  // one P buffer; two are allocated
+    static constexpr int K_BYTES = QA * KEYS * 128;
+    static constexpr int V_BYTES = VA * KEYS * 128;
+    static constexpr int PR = KEYS / 64;                // 64-key regions of a P buffer
+    static constexpr int P_BYTES = PR * kFaRows * 128;  // one P buffer; two are allocated
     static constexpr int XCH_BYTES = 2 * 2 * kFaRows * 4;  // [2 tiles][2 halves][128 rows] row maxima
     static constexpr int SMEM = Q_BYTES + KK * K_BYTES + KV * V_BYTES + 2 * P_BYTES + XCH_BYTES + 256;
-    static constexpr int TMEM_S = 0;  // two 64-column S buffers
-    static constexpr int TMEM_O = 128;
-    static constexpr int TMEM_COLS = 128 + DV <= 256 ? 256 : 512;
+    static constexpr int TMEM_S = 0;  // two KEYS-column S buffers
+    static constexpr int TMEM_O = 2 * KEYS;
+    static constexpr int TMEM_COLS = 2 * KEYS + DV <= 256 ? 256 : 512;
+    static_assert(2 * KEYS + DV <= 512, "TMEM columns");
+    static_assert(KEYS == 64 || KEYS == 128, "key tile");
     static constexpr int ROW_BYTES = DV * 2;  // staged bf16 output row
     static_assert(Q_BYTES >= kFaRows * ROW_BYTES, "output staging fits the Q region");
 };
 
-template <int D, int DK, int DV, int KK, int KV>
+template <int D, int DK, int DV, int KK, int KV, int KEYS>
 __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_constant__ FaMaps maps, const AttnParams p) {
-    using C = FaCfg<D, DK, DV, KK, KV>;
+    using C = FaCfg<D, DK, DV, KK, KV, KEYS>;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sQ = smem;
     uint8_t* sK = sQ + C::Q_BYTES;
@@ -146,7 +151,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
     // Key split (grid.y = S, launched as a (1, S, 1) cluster): this CTA takes key tiles
     // [t0, t0 + ntiles) and finalises rows [y * 128 / S, (y + 1) * 128 / S) of the q tile.
     const int S = gridDim.y, y = int(blockIdx.y);
-    const int ntiles_all = (total + kFaKeys - 1) / kFaKeys;
+    const int ntiles_all = (total + KEYS - 1) / KEYS;
     const int tps = (ntiles_all + S - 1) / S;
     const int t0 = y * tps;
     const int ntiles = max(0, min(ntiles_all, t0 + tps) - t0);
@@ -204,22 +209,23 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             auto load_rows = [&](bool is_v, uint8_t* dst_tile, int t, int regions) {
                 uint64_t* bar = is_v ? &v_full[t % KV] : &k_full[t % KK];
                 if (maps.kv_box == 64) {
-                    // one key segment: the whole 64-key tile is one box per region (8 KB boxes:
-                    // ~85 GB/s of TMA ingest per SM against ~60 for 32-row boxes; rows past the
-                    // segment are zero-filled)
+                    // one key segment: 64-key boxes per region (8 KB boxes: ~85 GB/s of TMA ingest
+                    // per SM against ~60 for 32-row boxes; rows past the segment are zero-filled)
                     const CUtensorMap* m = is_v ? &maps.v0 : &maps.k0;
-                    for (int a = 0; a < regions; ++a)
-                        tma_load_2d(dst_tile + a * (kFaKeys * 128), m, bar, kvh * D + a * 64, (t0 + t) * kFaKeys, kEvictLast);
+                    for (int b = 0; b < KEYS / 64; ++b)
+                        for (int a = 0; a < regions; ++a)
+                            tma_load_2d(dst_tile + a * (KEYS * 128) + b * 64 * 128, m, bar, kvh * D + a * 64,
+                                        (t0 + t) * KEYS + b * 64, kEvictLast);
                     return;
                 }
-                // two 32-key boxes per region; each box lies in one key segment (or fully OOB -> zeros)
-                for (int half = 0; half < 2; ++half) {
-                    const int j = (t0 + t) * kFaKeys + half * 32;
+                // 32-key boxes; each box lies in one key segment (or fully OOB -> zeros)
+                for (int half = 0; half < KEYS / 32; ++half) {
+                    const int j = (t0 + t) * KEYS + half * 32;
                     const bool seg0 = j < p.rows0;
                     const CUtensorMap* m = seg0 ? (is_v ? &maps.v0 : &maps.k0) : (is_v ? &maps.v1 : &maps.k1);
                     const int row = seg0 ? j : j - p.rows0;
                     for (int a = 0; a < regions; ++a)
-                        tma_load_2d(dst_tile + a * (kFaKeys * 128) + half * 32 * 128, m, bar, kvh * D + a * 64, row, kEvictLast);
+                        tma_load_2d(dst_tile + a * (KEYS * 128) + half * 32 * 128, m, bar, kvh * D + a * 64, row, kEvictLast);
                 }
             };
             FA_STAMP(10);
@@ -236,7 +242,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
     } else if (warp == 8) {
         // ------------------------------------------------------------ MMA issuer
         {  // warp-uniform loop; one elected lane issues (see gemm.cu)
-            constexpr uint32_t idesc_qk = umma_idesc_bf16(kFaRows, kFaKeys);
+            constexpr uint32_t idesc_qk = umma_idesc_bf16(kFaRows, KEYS);
             constexpr uint32_t idesc_pv = umma_idesc_bf16(kFaRows, DV) | (1u << 16);  // B (V) MN-major
             const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK), v0 = smem_u32(sV), p0 = smem_u32(sP);
             mbar_wait(q_ready, 0);
@@ -248,8 +254,8 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
 #pragma unroll
                 for (int kk = 0; kk < DK / 16; ++kk) {
                     const uint64_t a = desc_kmajor(q0 + (kk >> 2) * (kFaRows * 128) + (kk & 3) * 32);
-                    const uint64_t b = desc_kmajor(k0 + st * C::K_BYTES + (kk >> 2) * (kFaKeys * 128) + (kk & 3) * 32);
-                    if (elect_one()) umma_bf16(tmem + C::TMEM_S + sb * 64, a, b, idesc_qk, kk > 0);
+                    const uint64_t b = desc_kmajor(k0 + st * C::K_BYTES + (kk >> 2) * (KEYS * 128) + (kk & 3) * 32);
+                    if (elect_one()) umma_bf16(tmem + C::TMEM_S + sb * KEYS, a, b, idesc_qk, kk > 0);
                 }
                 if (elect_one()) {
                     umma_commit(&s_full[sb]);
@@ -266,9 +272,9 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                 mbar_wait(&p_full[t & 1], (t >> 1) & 1);
                 tc_fence_after();
 #pragma unroll
-                for (int kk = 0; kk < kFaKeys / 16; ++kk) {
-                    const uint64_t a = desc_kmajor(p0 + (t & 1) * C::P_BYTES + kk * 32);
-                    const uint64_t b = desc_mnmajor(v0 + sv * C::V_BYTES + kk * 2048, kFaKeys * 128);
+                for (int kk = 0; kk < KEYS / 16; ++kk) {
+                    const uint64_t a = desc_kmajor(p0 + (t & 1) * C::P_BYTES + (kk >> 2) * (kFaRows * 128) + (kk & 3) * 32);
+                    const uint64_t b = desc_mnmajor(v0 + sv * C::V_BYTES + kk * 2048, KEYS * 128);
                     if (elect_one()) umma_bf16(tmem + C::TMEM_O, a, b, idesc_pv, (t | kk) > 0);
                 }
                 if (elect_one()) {
@@ -306,24 +312,27 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             mbar_wait(&s_full[sb], (t >> 1) & 1);
             if (tid == 0 && t == 0) FA_STAMP(3);
             tc_fence_after();
-            float sv[32];
-            tmem_ld32(trow + C::TMEM_S + sb * 64 + hf * 32, sv);
+            constexpr int KH = KEYS / 2;  // keys of this thread's half of the tile
+            float sv[KH];
+#pragma unroll
+            for (int i = 0; i < KH / 32; ++i)
+                tmem_ld32(trow + C::TMEM_S + sb * KEYS + hf * KH + i * 32, *reinterpret_cast<float(*)[32]>(sv + i * 32));
             tc_fence_before();
             mbar_arrive(&s_free[sb]);
-            const int kbase = (t0 + t) * kFaKeys + hf * 32;
+            const int kbase = (t0 + t) * KEYS + hf * KH;
             float mx = -INFINITY;
             // keys past the end, and the padding keys [pad0, rows0) of segment 0, are masked; a
             // tile that has neither (the common case) takes the unmasked loop
-            if (kbase + 32 <= total && (kbase + 32 <= pad0 || kbase >= p.rows0)) {
+            if (kbase + KH <= total && (kbase + KH <= pad0 || kbase >= p.rows0)) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
+                for (int j = 0; j < KH; ++j) {
                     sv[j] *= p.scale_log2;
                     mx = fmaxf(mx, sv[j]);
                 }
             } else {
                 const int end = total - kbase, lo = pad0 - kbase, hi = p.rows0 - kbase;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
+                for (int j = 0; j < KH; ++j) {
                     sv[j] = j < end && (j < lo || j >= hi) ? sv[j] * p.scale_log2 : -INFINITY;
                     mx = fmaxf(mx, sv[j]);
                 }
@@ -360,19 +369,22 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                 }
             }
             float ls = 0.f;
-            uint32_t pk[16];
+            uint32_t pk[KH / 2];
 #pragma unroll
-            for (int j = 0; j < 32; j += 2) {
+            for (int j = 0; j < KH; j += 2) {
                 const float a0 = ex2_fast(sv[j] - m_ref), a1 = ex2_fast(sv[j + 1] - m_ref);
                 ls += a0 + a1;
                 pk[j / 2] = pack_bf16(a0, a1);
             }
             l += ls;
-            uint8_t* prow = sP + sb * C::P_BYTES + r * 128;
+            // P [128 rows x KEYS] as KEYS / 64 regions of [128 rows x 128 B]; this thread's keys
+            // [hf KH, +KH) are 16-byte chunks kq = hf KH / 8 + c (region kq / 8, chunk kq % 8)
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-                *reinterpret_cast<uint4*>(prow + (((hf * 4 + c) ^ (r & 7)) << 4)) =
+            for (int c = 0; c < KH / 8; ++c) {
+                const int kq = hf * (KH / 8) + c;
+                *reinterpret_cast<uint4*>(sP + sb * C::P_BYTES + (kq >> 3) * (kFaRows * 128) + r * 128 + (((kq & 7) ^ (r & 7)) << 4)) =
                     make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+            }
             fence_proxy_async();
             tc_fence_before();
             mbar_arrive(&p_full[sb]);
@@ -571,17 +583,30 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
 CUtensorMap make_tmap_bf16(const void* base, long long rows, long long cols, long long ld, int box_rows);
 
 namespace {
-template <int D, int DK, int DV, int KK, int KV>
+template <int D, int DK, int DV, int KK, int KV, int KEYS>
 cudaError_t fa_configure_t() {
-    return cudaFuncSetAttribute(fattn_kernel<D, DK, DV, KK, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                FaCfg<D, DK, DV, KK, KV>::SMEM);
+    return cudaFuncSetAttribute(fattn_kernel<D, DK, DV, KK, KV, KEYS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                FaCfg<D, DK, DV, KK, KV, KEYS>::SMEM);
 }
 }  // namespace
 
 cudaError_t fattn_configure() {
-    cudaError_t e = fa_configure_t<72, 80, 128, 3, 3>();
-    if (e == cudaSuccess) e = fa_configure_t<256, 256, 256, 2, 2>();
+    cudaError_t e = fa_configure_t<72, 80, 128, 3, 3, 64>();
+    if (e == cudaSuccess) e = fa_configure_t<72, 80, 128, 2, 2, 128>();
+    if (e == cudaSuccess) e = fa_configure_t<256, 256, 256, 2, 2, 64>();
     return e;
+}
+
+// d = 72 (SigLIP): 128-key tiles by default -- the QK^T MMA costs the same ~86 cycles at N = 64
+// and N = 128, so a 128-key tile halves its issue time per key and the per-tile softmax
+// exchanges (PI0B_FA72_KEYS=64: the 64-key tiles with 3-deep rings).  d = 256 keeps 64-key tiles
+// (a 128-key tile does not fit shared memory next to its 64 KB Q tile).
+static int fa72_keys() {
+    static const int k = [] {
+        const char* e = std::getenv("PI0B_FA72_KEYS");
+        return e && std::atoi(e) == 64 ? 64 : 128;
+    }();
+    return k;
 }
 
 // Tensor maps for one attention launch (built once at plan time).
@@ -602,12 +627,12 @@ FaMaps make_fattn_maps(const AttnParams& p, int head_dim) {
 static bool g_fa_pdl = true;
 void fattn_set_pdl(bool on) { g_fa_pdl = on; }
 
-template <int D, int DK, int DV, int KK, int KV>
+template <int D, int DK, int DV, int KK, int KV, int KEYS>
 static cudaError_t fa_launch_t(const FaMaps& maps, const AttnParams& p, dim3 grid, cudaStream_t stream) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(kFaThreads, 1, 1);
-    cfg.dynamicSmemBytes = FaCfg<D, DK, DV, KK, KV>::SMEM;
+    cfg.dynamicSmemBytes = FaCfg<D, DK, DV, KK, KV, KEYS>::SMEM;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     int na = 0;
@@ -616,7 +641,7 @@ static cudaError_t fa_launch_t(const FaMaps& maps, const AttnParams& p, dim3 gri
         attr[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
     }
-    if (grid.y > 1) {  // key splits of one q tile form a cluster (DSMEM combine)
+    if (grid.y > 1) {  // key splits of one q tile form a cluster (co-scheduled; one cluster barrier)
         attr[na].id = cudaLaunchAttributeClusterDimension;
         attr[na].val.clusterDim.x = 1;
         attr[na].val.clusterDim.y = grid.y;
@@ -625,7 +650,7 @@ static cudaError_t fa_launch_t(const FaMaps& maps, const AttnParams& p, dim3 gri
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, fattn_kernel<D, DK, DV, KK, KV>, maps, p);
+    return cudaLaunchKernelEx(&cfg, fattn_kernel<D, DK, DV, KK, KV, KEYS>, maps, p);
 }
 
 // grid = (stacked q tiles of 128, key splits (p.kv_splits: 1, 2, 4 or 8), kv groups).
@@ -638,8 +663,10 @@ cudaError_t launch_fattn(int head_dim, const FaMaps& maps, const AttnParams& p, 
     // whose rows past the segment are zero-filled (and masked), so its length is free
     if ((p.rows1 > 0 && (p.rows0 % 32)) || (p.rows1 % 32) || (p.q_rows % 32)) return cudaErrorInvalidValue;
     switch (head_dim) {
-        case 72: return fa_launch_t<72, 80, 128, 3, 3>(maps, p, grid, stream);
-        case 256: return fa_launch_t<256, 256, 256, 2, 2>(maps, p, grid, stream);
+        case 72:
+            return fa72_keys() == 128 ? fa_launch_t<72, 80, 128, 2, 2, 128>(maps, p, grid, stream)
+                                      : fa_launch_t<72, 80, 128, 3, 3, 64>(maps, p, grid, stream);
+        case 256: return fa_launch_t<256, 256, 256, 2, 2, 64>(maps, p, grid, stream);
         default: return cudaErrorInvalidValue;
     }
 }
