@@ -82,7 +82,10 @@ constexpr bool kAttnDup = PI0B_AE_ADUP != 0;  // single-head attention with dupl
 constexpr int kOReg = 5;              // ae.proj staging combines up to this many key ranges in registers
 constexpr int kOffW = 0;
 constexpr int kOffU = kWSt * kWSlot;                // union region (128 KB)
-constexpr int kUnion = 131072;
+#ifndef PI0B_AE_UNION_KB
+#define PI0B_AE_UNION_KB 128
+#endif
+constexpr int kUnion = PI0B_AE_UNION_KB * 1024;
 constexpr int kOffX = kOffU;                        // GEMM: X ring (+8 KB pad: rows 64..127 of A)
 constexpr int kOffF = kOffU + kXSt * kXSlot + PI0B_AE_XPAD * kXTile;  // GEMM: fp32 ring (kXY) / partial ring (kXO)
 constexpr int kORegion = kUnion - (kOffF - kOffU);  // kXO partial staging: ranges x 8 KB per slot

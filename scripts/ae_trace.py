@@ -112,7 +112,8 @@ for r in mid:
     idx = np.array(ph[r[0]])
     pr = tasks["pad1"][idx]
     if (pr > 0).any():
-        for role, nm in ((1, "owner"), (2, "helper")):
+        for role in sorted(set(int(v) for v in pr if v > 0)):
+            nm = {1: "owner", 2: "helper", 3: "ffn-a", 4: "ffn-b", 5: "qkv-a", 6: "qkv-b"}.get(role, str(role))
             s8 = st[idx[pr == role]].astype(np.float64)
             rel = lambda c: (s8[:, c] - prev_end) / 1e3
             q = lambda v: "%6.2f/%6.2f/%6.2f" % (np.min(v), np.median(v), np.max(v))
