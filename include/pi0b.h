@@ -53,6 +53,9 @@ typedef struct pi0b_engine_options {
      * expert.  Shards other than 0 serve run_prefix only.  0 or 1: no sharding. */
     int ve_shards;
     int ve_shard;
+    /* CTAs of the action-expert megakernel (one per SM): 0 = every SM.  Fewer leaves SMs to work
+     * running concurrently on other streams (the streaming runtime's prefix). */
+    int ae_ctas;
 } pi0b_engine_options;
 
 typedef struct pi0b_engine pi0b_engine;
@@ -160,6 +163,8 @@ typedef struct pi0b_stream_options {
     double trajectory_rate;  /* trajectory slots per second (480)                               */
     int kv_policy;           /* 0 most_recent, 1 frame_sticky (rtvla::KvPolicy)                 */
     int device;
+    int prefix_sms;          /* SMs the action-expert ticks leave to the concurrent prefix
+                                (0: 20; < 0: none -- the megakernel takes every SM)             */
 } pi0b_stream_options;
 
 typedef struct pi0b_stream_report {

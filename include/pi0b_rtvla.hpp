@@ -161,7 +161,7 @@ private:
         if (!rtvla::graphs_isomorphic(g, rtvla::build_pi0_graph(g.config), &why))
             throw rtvla::ShapeError("pi0b: graph is not build_pi0_graph(config): " + why);
         const pi0b_model_config c = to_c(cfg_);
-        pi0b_engine_options o{opt.device, opt.use_cuda_graph ? 1 : 0, 0, 0, 0};
+        pi0b_engine_options o{opt.device, opt.use_cuda_graph ? 1 : 0, 0, 0, 0, 0};
         pi0b_engine* e = nullptr;
         check(pi0b_engine_create(&c, &o, &e), "engine_create");
         h_.reset(e);

@@ -457,6 +457,7 @@ private:
     pi0b_model_config c_;
     pi0b_engine_options o_;
     int num_sms_ = 148;
+    int ae_ctas_ = 148;  // megakernel grid (PI0B_AE_CTAS: fewer leaves SMs to a concurrent prefix)
     cudaStream_t stream_ = nullptr;
     std::vector<void*> allocs_;
     std::map<std::string, NodeWeights> W_;
@@ -562,6 +563,9 @@ Engine::Engine(const pi0b_model_config& cfg, const pi0b_engine_options& opt, Eng
         throw EngineError(PI0B_E_UNSUPPORTED, "pi0b kernels are built for sm_100a (B200); found sm_" +
                                                   std::to_string(prop.major * 10 + prop.minor));
     num_sms_ = prop.multiProcessorCount;
+    ae_ctas_ = num_sms_;
+    if (const int want = env_int("PI0B_AE_CTAS", o_.ae_ctas); want > 0)
+        ae_ctas_ = std::max(16, std::min(num_sms_, want & ~1));  // even: CTA pairs
     pdl_ = env_int("PI0B_PDL", 1) != 0;
     gemm_set_pdl(pdl_);
     fattn_set_pdl(pdl_);
@@ -1490,7 +1494,7 @@ void Engine::build_ae_mega() {
         return int(mats.size()) - 1;
     };
     AePlanInput in;
-    in.num_ctas = num_sms_;
+    in.num_ctas = ae_ctas_;
     in.width = W;
     in.n_qkv = NQ;
     in.q_width = ae_q_;
@@ -1515,8 +1519,8 @@ void Engine::build_ae_mega() {
     in.attn_single = env_int("PI0B_AE_ATTN_SINGLE", 1) != 0;
     in.sym_qkv = env_int("PI0B_AE_SYM_QKV", 1) != 0;
     in.per_head_proj = env_int("PI0B_AE_HEAD_DEP", 1) != 0;
-    in.pair_ffn = env_int("PI0B_AE_PAIR_FFN", 1) != 0 && (2 * MLP) % 128 == 0 && 2 * (2 * MLP / 128) <= num_sms_ &&
-                  num_sms_ % 2 == 0;
+    in.pair_ffn = env_int("PI0B_AE_PAIR_FFN", 1) != 0 && (2 * MLP) % 128 == 0 && 2 * (2 * MLP / 128) <= ae_ctas_ &&
+                  ae_ctas_ % 2 == 0;
     ae_cluster_ = in.pair_qkv || in.pair_ffn;  // pair tasks need the 2-CTA cluster launch
     in.mat_wst = wmat("ae.state_proj", 0, W);
     in.mat_wap = wmat("ae.action_proj", 0, W);
@@ -1619,8 +1623,8 @@ void Engine::build_ae_mega() {
     P.trace = nullptr;
     P.dbg = nullptr;
     if (env_int("PI0B_AE_TRACE", 0)) {
-        P.dbg = alloc<unsigned long long>(size_t(num_sms_) * 128);
-        PI0B_CUDA(cudaMemset(P.dbg, 0, size_t(num_sms_) * 128 * 8));
+        P.dbg = alloc<unsigned long long>(size_t(ae_ctas_) * 128);
+        PI0B_CUDA(cudaMemset(P.dbg, 0, size_t(ae_ctas_) * 128 * 8));
         P.trace = alloc<unsigned long long>(ae_plan_.table.size() * 16);
         PI0B_CUDA(cudaMemset(P.trace, 0, ae_plan_.table.size() * 128));
     }
@@ -1864,7 +1868,7 @@ void Engine::run_ops(int part, cudaStream_t st) {
                 break;
             case kOpF32F64: PI0B_CUDA(launch_f32_to_f64(op.src32, op.ld32, op.rows, op.cols, op.dst64, st)); break;
             case kOpMemset: PI0B_CUDA(cudaMemsetAsync(op.mptr, 0, op.mbytes, st)); break;
-            case kOpAeMega: PI0B_CUDA(aemk_launch(ae_p_, num_sms_, st, ae_cluster_)); break;
+            case kOpAeMega: PI0B_CUDA(aemk_launch(ae_p_, ae_ctas_, st, ae_cluster_)); break;
             case kOpVeEpoch: PI0B_CUDA(launch_ve_epoch(ve_sync_ + kVeEpoch, st)); break;
             case kOpVeWait: PI0B_CUDA(launch_ve_wait(ve_sync_, op.ve_mask, ve_sync_ + kVeEpoch, unsigned(op.ve_step), st)); break;
             case kOpVePush: {
@@ -2024,7 +2028,7 @@ std::string Engine::describe() const {
                      op.gp.mode);
         } else if (op.kind == kOpAeMega) {
             snprintf(buf, sizeof buf, "%d %d ae_mega %s 0 ctas=%d tasks=%d phases=%d counters=%d stride=%d wload=%.0f..%.0fKB\n",
-                     idx, op.part, op.node.c_str(), num_sms_, ae_plan_.n_tasks, ae_plan_.n_phases, ae_plan_.n_bars,
+                     idx, op.part, op.node.c_str(), ae_ctas_, ae_plan_.n_tasks, ae_plan_.n_phases, ae_plan_.n_bars,
                      ae_plan_.stride, ae_plan_.min_load / 1024, ae_plan_.max_load / 1024);
         } else if (op.kind == kOpAttn) {
             snprintf(buf, sizeof buf, "%d %d attn %s %d splits=%d q=%d kv=%d hd=%d\n", idx, op.part, op.node.c_str(),
@@ -2053,7 +2057,7 @@ double Engine::time_node(const std::string& node, int reps, int* launches) {
         else if (op.kind == kOpSkinny) PI0B_CUDA(launch_skinny(op.ta, op.tb, op.gp, op.n_packed, op.cluster, pdl_, stream_));
         else if (op.kind == kOpAeMega) {
             PI0B_CUDA(cudaMemsetAsync(ae_zero_, 0, ae_zero_bytes_, stream_));
-            PI0B_CUDA(aemk_launch(ae_p_, num_sms_, stream_, ae_cluster_));
+            PI0B_CUDA(aemk_launch(ae_p_, ae_ctas_, stream_, ae_cluster_));
         }
         else PI0B_CUDA(launch_fattn(op.hd, op.fm, op.ap, stream_));
     };
@@ -2076,15 +2080,15 @@ double Engine::time_node(const std::string& node, int reps, int* launches) {
 
 void Engine::ae_trace(void* tasks, unsigned long long* stamps, long long cap, int* ctas, int* stride) {
     if (!ae_mega_ || !ae_p_.trace) throw EngineError(PI0B_E_STATE, "no megakernel trace (set PI0B_AE_TRACE=1)");
-    *ctas = num_sms_;
+    *ctas = ae_ctas_;
     *stride = ae_plan_.stride;
     const size_t n = ae_plan_.table.size();
     if (cap < (long long)n) throw EngineError(PI0B_E_INVALID, "trace buffer too small");
     PI0B_CUDA(cudaStreamSynchronize(stream_));
     std::memcpy(tasks, ae_plan_.table.data(), n * sizeof(AeTask));
     PI0B_CUDA(cudaMemcpy(stamps, ae_p_.trace, n * 128, cudaMemcpyDeviceToHost));
-    if (ae_p_.dbg && cap >= (long long)n + num_sms_ * 8)  // per-k-block stamps appended after the task stamps
-        PI0B_CUDA(cudaMemcpy(stamps + n * 16, ae_p_.dbg, size_t(num_sms_) * 128 * 8, cudaMemcpyDeviceToHost));
+    if (ae_p_.dbg && cap >= (long long)n + ae_ctas_ * 8)  // per-k-block stamps appended after the task stamps
+        PI0B_CUDA(cudaMemcpy(stamps + n * 16, ae_p_.dbg, size_t(ae_ctas_) * 128 * 8, cudaMemcpyDeviceToHost));
 }
 
 void Engine::read_checkpoint(const std::string& id, long long inst, float* out, long long rows, long long cols) {
@@ -2130,7 +2134,19 @@ void stream_run(const pi0b_model_config& cfg, uint64_t seed, const pi0b_stream_o
     using clk = std::chrono::steady_clock;
     if (o.frame_rate <= 0 || o.ae_rate <= 0 || o.trajectory_rate <= 0 || o.camera_latency < 0 || seconds <= 0)
         throw EngineError(PI0B_E_INVALID, "stream options");
-    pi0b_engine_options eo{o.device, 1, 0, 0, 0};
+    // The ticks' megakernel leaves `prefix_sms` SMs to the concurrent prefix (measured at 1440 Hz
+    // 1-step ticks, 2 views: 128 of 148 SMs -> prefix p50 19.8 -> 11.3 ms, slow loop 89 -> 81 ms,
+    // the megakernel itself 0.4% slower; its gated-FFN phase needs 2 x 64 CTAs, so no fewer)
+    int sms = 148;
+    {
+        cudaDeviceProp prop;
+        PI0B_CUDA(cudaGetDeviceProperties(&prop, o.device));
+        sms = prop.multiProcessorCount;
+    }
+    const int reserve = o.prefix_sms == 0 ? 20 : std::max(0, o.prefix_sms);
+    const int ffn_ctas = 2 * (2 * cfg.ae_mlp / 128);
+    const int ae_ctas = reserve > 0 ? std::max(std::min(sms, ffn_ctas), (sms - reserve) & ~1) : 0;
+    pi0b_engine_options eo{o.device, 1, 0, 0, 0, ae_ctas};
     // two KV buffers over ONE weight arena: the second engine borrows the first one's weights
     std::unique_ptr<Engine> eng[2];
     eng[0] = std::make_unique<Engine>(cfg, eo);
@@ -2312,7 +2328,7 @@ void pi0b_default_config(pi0b_model_config* c) {
 int pi0b_engine_create_shared(const pi0b_model_config* cfg, const pi0b_engine_options* opt, pi0b_engine* donor,
                               pi0b_engine** out) {
     if (!cfg || !out || !donor) return pi0b::fail(EngineError(PI0B_E_INVALID, "null argument"));
-    pi0b_engine_options o{0, 1, 0, 0, 0};
+    pi0b_engine_options o{0, 1, 0, 0, 0, 0};
     if (opt) o = *opt;
     PI0B_TRY({
         auto* e = new pi0b_engine;
@@ -2328,7 +2344,7 @@ int pi0b_engine_create_shared(const pi0b_model_config* cfg, const pi0b_engine_op
 
 int pi0b_engine_create(const pi0b_model_config* cfg, const pi0b_engine_options* opt, pi0b_engine** out) {
     if (!cfg || !out) return pi0b::fail(EngineError(PI0B_E_INVALID, "null argument"));
-    pi0b_engine_options o{0, 1, 0, 0, 0};
+    pi0b_engine_options o{0, 1, 0, 0, 0, 0};
     if (opt) o = *opt;
     PI0B_TRY({
         auto* e = new pi0b_engine;

@@ -47,7 +47,7 @@ class UnsupportedConfig(ShapeError):
 
 class EngineOptions(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("use_cuda_graph", ctypes.c_int), ("record_checkpoints", ctypes.c_int),
-                ("ve_shards", ctypes.c_int), ("ve_shard", ctypes.c_int)]
+                ("ve_shards", ctypes.c_int), ("ve_shard", ctypes.c_int), ("ae_ctas", ctypes.c_int)]
 
 
 class VeBuffers(ctypes.Structure):
@@ -167,7 +167,8 @@ def lib():
 class StreamOptions(ctypes.Structure):
     """include/pi0b.h pi0b_stream_options"""
     _fields_ = [("frame_rate", ctypes.c_double), ("camera_latency", ctypes.c_int), ("ae_rate", ctypes.c_double),
-                ("trajectory_rate", ctypes.c_double), ("kv_policy", ctypes.c_int), ("device", ctypes.c_int)]
+                ("trajectory_rate", ctypes.c_double), ("kv_policy", ctypes.c_int), ("device", ctypes.c_int),
+                ("prefix_sms", ctypes.c_int)]
 
 
 class StreamReport(ctypes.Structure):
@@ -184,11 +185,12 @@ class StreamReport(ctypes.Structure):
 
 def stream_run(cfg, seconds: float, *, weight_seed: int = 1, frame_rate: float = 30.0, camera_latency: int = 2,
                ae_rate: float = 480.0, trajectory_rate: float = 480.0, kv_policy: str = "most_recent",
-               device: int = 0) -> dict:
+               device: int = 0, prefix_sms: int = 0) -> dict:
     """The full-streaming runtime (include/pi0b.h pi0b_stream_run): `seconds` of camera frames and
-    control ticks on one GPU, two engines (double-buffered KV).  cfg.flow_steps = flow steps per tick."""
+    control ticks on one GPU, two engines over one weight arena (double-buffered KV).
+    cfg.flow_steps = flow steps per tick; prefix_sms = SMs the ticks leave to the prefix (0: 20)."""
     o = StreamOptions(frame_rate, camera_latency, ae_rate, trajectory_rate,
-                      {"most_recent": 0, "frame_sticky": 1}[kv_policy], device)
+                      {"most_recent": 0, "frame_sticky": 1}[kv_policy], device, prefix_sms)
     r = StreamReport()
     _raise(lib().pi0b_stream_run(ctypes.byref(cfg), weight_seed, ctypes.byref(o), seconds, ctypes.byref(r)),
            "stream_run")
@@ -237,13 +239,13 @@ class Engine:
 
     def __init__(self, cfg: ModelConfig, device: int = 0, use_cuda_graph: bool = True,
                  record_checkpoints: bool = False, ve_shards: int = 0, ve_shard: int = 0,
-                 share_weights_with: "Engine | None" = None):
+                 share_weights_with: "Engine | None" = None, ae_ctas: int = 0):
         """share_weights_with: read that engine's weight arena (include/pi0b.h
         pi0b_engine_create_shared); it must stay alive as long as this one."""
         self.cfg = cfg
         self._h = ctypes.c_void_p()
         self._donor = share_weights_with
-        opt = EngineOptions(device, int(use_cuda_graph), int(record_checkpoints), ve_shards, ve_shard)
+        opt = EngineOptions(device, int(use_cuda_graph), int(record_checkpoints), ve_shards, ve_shard, ae_ctas)
         if share_weights_with is None:
             _raise(lib().pi0b_engine_create(ctypes.byref(cfg), ctypes.byref(opt), ctypes.byref(self._h)),
                    "pi0b_engine_create")
