@@ -107,6 +107,10 @@ int pi0b_image_patches(const double* images, int views, int height, int width, i
  * out, no GPU needed): dst[i] = bf16(float(src[i])), round-to-nearest-even at both steps, NaN ->
  * 0x7fff -- bit-identical to the device conversion (__float2bfloat16_rn(float(x))). */
 int pi0b_f64_to_bf16_host(const double* src, long long n, uint16_t* dst);
+/* The RoPE table the engine uploads (host memory, no GPU): out[(p * head_dim/2 + j) * 2 + {0, 1}] =
+ * fp32 {cos, sin} of p * 10000^(-2j/head_dim), computed in fp64 exactly as rtvla::make_rope_table
+ * (proj/src/tensor.cpp:133-148), for positions [0, positions). */
+int pi0b_rope_table_host(int positions, int head_dim, float* out);
 
 /* ------------------------------------------------------------------ unfused checkpoints
  * Weight rules for the naive graph (rtvla::build_pi0_graph_naive, proj/src/builder.cpp:369-541),

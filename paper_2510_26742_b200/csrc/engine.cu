@@ -205,6 +205,21 @@ static int choose_splits(int m_tiles, int n_tiles, int K, int bn, int num_sms) {
     return std::max(s, 1);
 }
 
+// The RoPE table the engine uploads: {cos, sin} of p * 10000^(-2j/d) interleaved, [positions][d/2][2],
+// evaluated in fp64 with make_rope_table's operation order (proj/src/tensor.cpp:133-148) and
+// rounded once to fp32 (pi0b_rope_table_host; bit-exact test against the reference in
+// tests/test_capi.py).
+static void rope_table_f32(int positions, int head_dim, float* out) {
+    const int half = head_dim / 2;
+    for (int p = 0; p < positions; ++p)
+        for (int j = 0; j < half; ++j) {
+            const double freq = std::pow(10000.0, -2.0 * double(j) / double(head_dim));
+            const double ang = double(p) * freq;
+            out[(size_t(p) * half + j) * 2 + 0] = float(std::cos(ang));
+            out[(size_t(p) * half + j) * 2 + 1] = float(std::sin(ang));
+        }
+}
+
 // ------------------------------------------------------------------ plan records
 
 enum OpKind { kOpGemm, kOpAttn, kOpRowsF32, kOpF64Bf16, kOpF32F64, kOpMemset, kOpSkinny, kOpAeMega,
@@ -765,13 +780,7 @@ void Engine::alloc_activations() {
     // (proj/src/tensor.cpp:133-148) and rounded to fp32. Positions [0, L+S).
     const int npos = Lp_ + S_;
     std::vector<float> cs(size_t(npos) * 128 * 2);
-    for (int p = 0; p < npos; ++p)
-        for (int j = 0; j < 128; ++j) {
-            const double freq = std::pow(10000.0, -2.0 * double(j) / 256.0);
-            const double ang = double(p) * freq;
-            cs[(size_t(p) * 128 + j) * 2 + 0] = float(std::cos(ang));
-            cs[(size_t(p) * 128 + j) * 2 + 1] = float(std::sin(ang));
-        }
+    rope_table_f32(npos, 256, cs.data());
     rope_cs_ = alloc<float>(cs.size());
     PI0B_CUDA(cudaMemcpyAsync(rope_cs_, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, stream_));
     PI0B_CUDA(cudaStreamSynchronize(stream_));
@@ -2394,6 +2403,13 @@ int pi0b_image_patches(const double* images, int views, int height, int width, i
                        double* patches, void* stream) {
     return int(pi0b::launch_image_patches(images, views, height, width, channels, side, patch, patches,
                                           static_cast<cudaStream_t>(stream)));
+}
+
+int pi0b_rope_table_host(int positions, int head_dim, float* out) {
+    if (!out || positions <= 0 || head_dim <= 0 || head_dim % 2)
+        return pi0b::fail(EngineError(PI0B_E_INVALID, "rope table: positions > 0, even head_dim"));
+    pi0b::rope_table_f32(positions, head_dim, out);
+    return PI0B_OK;
 }
 
 int pi0b_f64_to_bf16_host(const double* src, long long n, uint16_t* dst) {

@@ -134,6 +134,7 @@ def lib():
                                          ctypes.c_int, vp, vp]
         L.pi0b_engine_run_action.argtypes = [vp, _dp, _dp, _dp]
         L.pi0b_f64_to_bf16_host.argtypes = [_dp, ctypes.c_longlong, vp]
+        L.pi0b_rope_table_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_float)]
         L.pi0b_engine_replay.argtypes = [vp, ctypes.c_int, vp]
         L.pi0b_engine_sync.argtypes = [vp]
         L.pi0b_engine_kernel_count.argtypes = [vp, ctypes.c_int]
@@ -204,7 +205,7 @@ EXPORTED_SYMBOLS = [
     "pi0b_engine_read_checkpoint", "pi0b_engine_time_node", "pi0b_engine_describe", "pi0b_engine_ae_trace",
     "pi0b_last_error", "pi0b_gemm", "pi0b_gemm_skinny", "pi0b_attention",
     "pi0b_attention_ws_floats", "pi0b_random_f64", "pi0b_random_packed_bf16", "pi0b_seed_hash",
-    "pi0b_engine_run_images", "pi0b_image_patches", "pi0b_stream_run", "pi0b_f64_to_bf16_host",
+    "pi0b_engine_run_images", "pi0b_image_patches", "pi0b_stream_run", "pi0b_f64_to_bf16_host", "pi0b_rope_table_host",
     "pi0b_premultiply_rows", "pi0b_fold_time_mlp", "pi0b_time_embedding",
     "pi0b_engine_create_shared", "pi0b_engine_ve_buffers", "pi0b_engine_set_ve_peers", "pi0b_ipc_export", "pi0b_ipc_open", "pi0b_ipc_close",
 ]

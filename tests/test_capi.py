@@ -116,3 +116,20 @@ def test_host_patch_conversion_matches_device_rounding():
     with np.errstate(over="ignore"):
         ref = _bf16_of_f32_rne(x)
     assert np.array_equal(out, ref)
+
+
+def test_rope_table_bitexact_vs_reference():
+    """The engine's RoPE table (pi0b_rope_table_host: what Engine uploads) is the reference's
+    make_rope_table (proj/src/tensor.cpp:133-148) rounded once to fp32, bit for bit, over every
+    position an engine uses (prefix rows and the action expert's L..L+63)."""
+    import numpy as np
+    from oracle import oracle as O
+    npos, d = 1400, 256
+    got = np.zeros(npos * d, dtype=np.float32)
+    assert E.lib().pi0b_rope_table_host(npos, d, got.ctypes.data_as(ctypes.POINTER(ctypes.c_float))) == 0
+    got = got.reshape(npos, d // 2, 2)
+    c = np.zeros(npos * d // 2)
+    s = np.zeros(npos * d // 2)
+    O.ref_lib().ref_rope_table(npos, d, c.ctypes.data_as(O._dp), s.ctypes.data_as(O._dp))
+    assert np.array_equal(got[:, :, 0].view(np.uint32), c.reshape(npos, d // 2).astype(np.float32).view(np.uint32))
+    assert np.array_equal(got[:, :, 1].view(np.uint32), s.reshape(npos, d // 2).astype(np.float32).view(np.uint32))
