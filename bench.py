@@ -123,7 +123,6 @@ def ve_shard_bench(cfg, ws: int, rank: int, local: int, steps: int, warmup: int,
     "only where it lowers latency" question is answered by the measurement.  Every rank takes
     part in the same sequence of gloo collectives; any failure aborts the experiment on all ranks
     and is reported, never raised."""
-    import torch
     import torch.distributed as dist
     from paper_2510_26742_b200 import engine as E
     from paper_2510_26742_b200.inputs import gen_inputs
@@ -133,10 +132,15 @@ def ve_shard_bench(cfg, ws: int, rank: int, local: int, steps: int, warmup: int,
     part = rank < G
     eng, opened, err = None, [], None
 
+    first_err = [None]  # the first failure reported by any rank (for rank 0's line)
+
     def agree(ok: bool) -> bool:
         flags = [None] * ws
-        dist.all_gather_object(flags, ok)
-        return all(flags)
+        dist.all_gather_object(flags, (ok, err))
+        for f_ok, f_err in flags:
+            if not f_ok and first_err[0] is None:
+                first_err[0] = f_err
+        return all(f[0] for f in flags)
 
     try:
         if part:
@@ -149,7 +153,7 @@ def ve_shard_bench(cfg, ws: int, rank: int, local: int, steps: int, warmup: int,
         err, mine = f"rank {rank} setup: {e}"[:300], None
     handles = [None] * ws
     dist.all_gather_object(handles, mine)
-    ok = err is None
+    ok = err is None and all(h is not None for h in handles[:G])
     if part and ok:
         try:
             peers = []
@@ -163,37 +167,33 @@ def ve_shard_bench(cfg, ws: int, rank: int, local: int, steps: int, warmup: int,
             eng.set_ve_peers(peers)
         except Exception as e:  # noqa: BLE001
             err, ok = f"rank {rank} peers: {e}"[:300], False
-    if not agree(ok and all(h is not None for h in handles[:G])):
-        res = {"gpus": G, "error": err or "setup failed on another rank"}
+    if not agree(ok):
+        res = {"gpus": G, "error": first_err[0] or err or "setup failed on another rank"}
     else:
         x = gen_inputs(cfg, 1)
-        times, y = [], None
-        stream = torch.cuda.Stream() if part else None
+        times, y, all_ok = [], None, True
+        timer = DeviceTimer() if part else None
         for i in range(warmup + steps):
-            if not agree(ok):
+            all_ok = agree(ok)   # one collective per iteration on every rank: a failure anywhere stops all
+            if not all_ok:
                 break
             try:
                 if rank == 0:
                     if y is None:   # first call: uploads the inputs and captures the graph
                         y = eng.run(x["patches"], x["state"], x["noise"], x.get("prompt"))
                         continue
-                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a.record(stream)
-                    eng.replay(0, stream.cuda_stream)
-                    b.record(stream)
-                    b.synchronize()
+                    ms = timer.time(lambda st: eng.replay(0, st))
                     if i >= warmup:
-                        times.append(a.elapsed_time(b))
+                        times.append(ms)
                 elif part:
                     if i == 0:
                         eng.run_prefix(x["patches"], x.get("prompt"))
                     else:
-                        eng.replay(1, stream.cuda_stream)
-                        stream.synchronize()
+                        timer.time(lambda st: eng.replay(1, st))
             except Exception as e:  # noqa: BLE001
                 err, ok = f"rank {rank} run: {e}"[:300], False
-        agree(ok)
-        if rank == 0 and times:
+        all_ok = agree(ok) and all_ok
+        if rank == 0 and all_ok and times:
             p50 = float(np.median(times))
             res = {"gpus": G, "p50_ms": round(p50, 4), "p90_ms": round(float(np.percentile(times, 90)), 4),
                    "steps": len(times), "single_gpu_p50_ms": round(single_p50, 4),
@@ -201,7 +201,7 @@ def ve_shard_bench(cfg, ws: int, rank: int, local: int, steps: int, warmup: int,
                    "method": "rank 0 device-timed replay (CUDA events); peers replay their VE prefix after the same "
                              "gloo rendezvous; K/V rows + proj_in rows over CUDA-IPC peer memory"}
         else:
-            res = {"gpus": G, "error": err or "no timed steps"}
+            res = {"gpus": G, "error": first_err[0] or err or "no timed steps"}
     for ptr in opened:
         try:
             E.ipc_close(ptr)
@@ -210,6 +210,24 @@ def ve_shard_bench(cfg, ws: int, rank: int, local: int, steps: int, warmup: int,
     if eng is not None:
         eng.close()
     return res if rank == 0 else None
+
+
+class DeviceTimer:
+    """CUDA events around fn(stream handle) on a dedicated (non-legacy) stream; returns ms."""
+
+    def __init__(self):
+        import torch
+        self._torch = torch
+        self.stream = torch.cuda.Stream()
+
+    def time(self, fn) -> float:
+        t = self._torch
+        a, b = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+        a.record(self.stream)
+        fn(self.stream.cuda_stream)
+        b.record(self.stream)
+        b.synchronize()
+        return a.elapsed_time(b)
 
 
 def _dist():

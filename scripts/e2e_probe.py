@@ -34,3 +34,10 @@ t = []
 for i in range(60):
     t0 = time.perf_counter(); eng.run_action(x["state"], x["noise"]); t.append(time.perf_counter() - t0)
 print("run_action %.1f us" % (np.median(t[10:]) * 1e6))
+# CPU cost of the graph launch call itself (no sync)
+t = []
+for i in range(30):
+    eng.sync()
+    t0 = time.perf_counter(); eng.replay(0); t.append(time.perf_counter() - t0)
+eng.sync()
+print("cudaGraphLaunch (replay call, CPU side) %.1f us" % (np.median(t[5:]) * 1e6))
