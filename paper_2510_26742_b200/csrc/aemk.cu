@@ -1486,6 +1486,8 @@ AePlan ae_plan(const AePlanInput& in) {
                 assign(it);
             }
             const int bar_proj = newbar();
+            std::vector<size_t> proj_from(lists.size());  // the ae.proj tasks are appended after these
+            for (size_t c = 0; c < lists.size(); ++c) proj_from[c] = lists[c].size();
             const int n_proj = red_phase(in.mat_wproj[size_t(l)], 0, kXO, 0, in.q_width / 64, ks_proj, bar_attn, n_attn,
                                          bar_proj, in.proj_ncol, per_head ? (in.attn_single ? 4 : 8) : 0, splits);
             if (per_head) {
@@ -1493,13 +1495,14 @@ AePlan ae_plan(const AePlanInput& in) {
                 // qkv only because ae.ffn waits for every ae.proj task and, together, the ae.proj
                 // tasks wait for every head's counter: check that they do.
                 std::vector<char> seen(size_t(n_rb), 0);
-                for (auto& cl : lists)
-                    for (auto& x : cl)
-                        if (x.phase == uint16_t(phase - 1) && x.sig_bar == uint16_t(bar_proj)) {
-                            const int rb = int(x.wait_bar) - bar_attn;
-                            need(rb >= 0 && rb < n_rb && x.wait_cnt == uint16_t(splits), "ae.proj grouped wait target");
-                            seen[size_t(rb)] = 1;
-                        }
+                for (size_t c = 0; c < lists.size(); ++c)
+                    for (size_t k = proj_from[c]; k < lists[c].size(); ++k) {
+                        const AeTask& x = lists[c][k];
+                        const int rb = int(x.wait_bar) - bar_attn;
+                        need(x.sig_bar == uint16_t(bar_proj) && rb >= 0 && rb < n_rb && x.wait_cnt == uint16_t(splits),
+                             "ae.proj grouped wait target");
+                        seen[size_t(rb)] = 1;
+                    }
                 need(std::all_of(seen.begin(), seen.end(), [](char c) { return c != 0; }),
                      "ae.proj tasks must wait, together, for every head's attention counter");
             }
