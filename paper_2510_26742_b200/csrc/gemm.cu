@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_init(recv_full, 1);
         fence_barrier_init();
     }
+    __syncwarp();  // warp 0 reconverged before the (.aligned) block barrier
     const int tmem_cols = (persist ? NBUF : 1) * MT * Cfg::TMEM_COLS;
     if (warp == 1) {
         if constexpr (CG == 2) tmem_alloc_cg2(tmem_slot, tmem_cols);

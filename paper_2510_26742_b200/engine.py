@@ -134,7 +134,6 @@ def lib():
                                          ctypes.c_int, vp, vp]
         L.pi0b_engine_run_action.argtypes = [vp, _dp, _dp, _dp]
         L.pi0b_f64_to_bf16_host.argtypes = [_dp, ctypes.c_longlong, vp]
-        L.pi0b_rope_table_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_float)]
         L.pi0b_engine_replay.argtypes = [vp, ctypes.c_int, vp]
         L.pi0b_engine_sync.argtypes = [vp]
         L.pi0b_engine_kernel_count.argtypes = [vp, ctypes.c_int]
@@ -158,7 +157,8 @@ def lib():
                            ("pi0b_engine_set_ve_peers", [vp, ctypes.POINTER(VeBuffers), ctypes.c_int]),
                            ("pi0b_ipc_export", [vp, ctypes.c_char_p]),
                            ("pi0b_ipc_open", [ctypes.c_char_p, ctypes.POINTER(vp)]),
-                           ("pi0b_ipc_close", [vp])):
+                           ("pi0b_ipc_close", [vp]),
+                           ("pi0b_rope_table_host", [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_float)])):
             if hasattr(L, name):
                 getattr(L, name).argtypes = args
         _lib = L

@@ -15,8 +15,10 @@
 
 * full_3v32p.json — restatement actions, checked element for element against the reference's
   own full-scale run (ref_full_3v32p.json from ref_full_run.py, ~40 min single-threaded).
+* full_1v17p.json — the same for 1 view + a 17-token prompt (L = 273, not a multiple of 32: the
+  engine's padded-prefix path at full scale), against ref_full_1v17p.json.
 
-Usage:  PYTHONPATH=. python tests/golden/make_golden.py [tiny mid full1 full2 full3 sketch1 sketch2 sketch3]
+Usage:  PYTHONPATH=. python tests/golden/make_golden.py [tiny mid full1 full2 full3 full1p17 sketch1 sketch2 sketch3]
 """
 import json
 import os
@@ -81,6 +83,18 @@ def main(which):
                 raise SystemExit(f"full {views}v: {k} = {got[k]!r} != reference {v!r}")
         dump(f"full_{views}v.json", cfg, y, "pi0_oracle restatement (bitwise == reference spot values)",
              {"restatement_seconds": dt})
+    if "full1p17" in which:   # unaligned prompt at full scale: L = 273 (the engine pads to 288 rows)
+        cfg = default_config(views=1, prompt_tokens=17)
+        x = O.gen_inputs(cfg, 1)
+        t = time.time()
+        y, _ = O.port_forward(cfg, x)
+        dt = time.time() - t
+        ref = json.load(open(os.path.join(HERE, "ref_full_1v17p.json")))
+        r = np.array(ref["actions"]).reshape(y.shape)
+        if not np.array_equal(r, y):
+            raise SystemExit(f"full 1v17p: restatement != reference, max |d| {np.abs(r - y).max():.3e}")
+        dump("full_1v17p.json", cfg, y, "pi0_oracle restatement (bitwise == reference rtvla::evaluate, "
+             "ref_full_1v17p.json)", {"restatement_seconds": dt, "reference_evaluate_seconds": ref["evaluate_seconds"]})
     if "full3" in which:
         cfg = default_config(views=3, prompt_tokens=32)
         x = O.gen_inputs(cfg, 1)

@@ -195,9 +195,11 @@ def _record_parity(tag, doc):
 
 
 FULL_CONFIGS = [(1, 0, "1v"), (2, 0, "2v"), (3, 32, "3v32p")]
+# + an unaligned prompt (L = 273): the padded-prefix path (32-row Lp, masked padding keys) at full scale
+FULL_ACTION_CONFIGS = FULL_CONFIGS + [(1, 17, "1v17p")]
 
 
-@pytest.mark.parametrize("views,prompt,tag", FULL_CONFIGS)
+@pytest.mark.parametrize("views,prompt,tag", FULL_ACTION_CONFIGS)
 def test_full_scale_actions_match_reference_golden(views, prompt, tag):
     """Full-scale pi0 (seed 1) vs the reference's fp64 output (tests/golden/full_<tag>.json,
     generated by tests/golden/make_golden.py and pinned to the compiled reference's own
