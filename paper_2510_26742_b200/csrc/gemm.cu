@@ -214,8 +214,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         else tmem_alloc(tmem_slot, tmem_cols);
     }
     tc_fence_before();
-    if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote arrive
-    else __syncthreads();
+    // Peer barriers initialised before any remote arrive.  CTA pair (CG = 2): a full cluster
+    // barrier.  Split-K cluster (grid.z = p.splits > 1): the arrive (release) here, the matching
+    // wait (acquire) just before each thread's first cluster access (split_wait below), so the
+    // barrier costs nothing on the critical path.
+    if constexpr (CG == 2) {
+        cluster_sync_all();
+    } else {
+        // (fence_barrier_init above is the release of the inits; the arrive itself can be relaxed)
+        if (p.splits > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+        __syncthreads();
+    }
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) GM_STAMP(1);
@@ -224,6 +233,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int S = p.splits;  // cluster size along K (grid.z)
     // split-K combine by st.async pushes into the peers' drained pipeline smem (see the epilogue)
     const bool push = S > 1 && S * (BN / 32) * 16384 <= STAGES * Cfg::STAGE_BYTES;
+    // the other half of the split-K init barrier: exactly once per thread, before its first
+    // remote mbarrier arrive / DSMEM access / cluster barrier
+    auto split_wait = [&]() {
+        if (CG == 1 && S > 1) cluster_wait_acquire();
+    };
     // Staged epilogue: a single-tile CTA (no persistence, no CTA pair / multi-tile) writes its
     // finished 32-column chunks as fp32 into the drained pipeline smem (past the split-K receive
     // slots) and then copies them out with whole-warp, row-contiguous stores -- per-thread row
@@ -296,6 +310,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
         }
         __syncwarp();
+        split_wait();
         if (S > 1 && !push) {
             cluster_sync_all();
             cluster_sync_all();
@@ -346,6 +361,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
         }
         __syncwarp();
+        split_wait();
         if (S > 1 && !push) {
             cluster_sync_all();
             cluster_sync_all();
@@ -402,6 +418,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_after();
         if (etid == 0 && j == 0) GM_STAMP(4);
 
+        split_wait();  // (S > 1 implies one tile per CTA: once)
         // Split-K combine, push form (S * NC chunks of 16 KB fit in the drained pipeline smem):
         // as soon as its own MMAs are done a CTA arms its receive barrier and tells the peers its
         // pipeline smem is free; once all peers are free it st.asyncs the partials of the chunks
