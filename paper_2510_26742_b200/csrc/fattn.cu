@@ -182,8 +182,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
     if (warp == 8) tmem_alloc(tmem_slot, C::TMEM_COLS);
     if (tid == 0) pdl_launch_dependents();
     tc_fence_before();
-    if (S > 1) cluster_sync_all();  // peers' barriers initialised before any remote arrive
-    else __syncthreads();
+    __syncthreads();  // (key splits touch no peer barrier or shared memory: one cluster barrier in the combine)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (tid == 0) FA_STAMP(2);

@@ -18,7 +18,7 @@
 * full_1v17p.json — the same for 1 view + a 17-token prompt (L = 273, not a multiple of 32: the
   engine's padded-prefix path at full scale), against ref_full_1v17p.json.
 
-Usage:  PYTHONPATH=. python tests/golden/make_golden.py [tiny mid full1 full2 full3 full1p17 sketch1 sketch2 sketch3]
+Usage:  PYTHONPATH=. python tests/golden/make_golden.py [tiny mid full1 full2 full3 full1p17 sketch1 sketch2 sketch3 sketch1p17]
 """
 import json
 import os
@@ -109,7 +109,7 @@ def main(which):
         dump("full_3v32p.json", cfg, y, "pi0_oracle restatement (bitwise == reference rtvla::evaluate, "
              "ref_full_3v32p.json)", {"restatement_seconds": dt,
                                       "reference_evaluate_seconds": ref["evaluate_seconds"]})
-    for views, prompt, key in [(1, 0, "sketch1"), (2, 0, "sketch2"), (3, 32, "sketch3")]:
+    for views, prompt, key in [(1, 0, "sketch1"), (2, 0, "sketch2"), (3, 32, "sketch3"), (1, 17, "sketch1p17")]:
         if key not in which:
             continue
         cfg = default_config(views=views, prompt_tokens=prompt)

@@ -218,7 +218,7 @@ def test_full_scale_actions_match_reference_golden(views, prompt, tag):
     assert rep["cos"] > 0.9999, rep
 
 
-@pytest.mark.parametrize("views,prompt,tag", FULL_CONFIGS)
+@pytest.mark.parametrize("views,prompt,tag", FULL_ACTION_CONFIGS)
 def test_full_scale_per_layer_cosine(views, prompt, tag):
     """North star: per-layer hidden-state cosine >= 0.999 at FULL scale, across all 225 serial
     layers' checkpoints of SURVEY.md 8(c) (ve.fc2[0..26], llm.proj_in, the KV cache
