@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             // Pair owner: its receive buffer (union tail) is free from here on -- tell the helper.
             if ((t.pair == 1 || t.pair >= 3) && wtid == 0) {
                 // the partner's st.async bytes: its partial of this CTA's columns + 64 row sums
-                mbar_arrive_expect_tx(pair_full, (t.pair >= 5 ? 64 * 32 * 4 : 64 * 64 * 4) + 64 * 4);
+                mbar_arrive_expect_tx(pair_full, (t.pair >= 7 ? 64 * 16 * 4 : t.pair >= 5 ? 64 * 32 * 4 : 64 * 64 * 4) + 64 * 4);
                 mbar_arrive_remote(partner_addr(pair_ready));
             }
             // Attention over a range of cached LLM keys: K does not depend on this step, so its
@@ -815,6 +815,27 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 } else if (t.pair == 1) {
                     mbar_wait_cluster(pair_full, oidx & 1);
                     ++oidx;
+                } else if (t.pair >= 7) {
+                    // ae.head split over K in a CTA pair (7 / 8): each CTA finalises 16 of the 32
+                    // action columns; it pushes its partial of the other 16 (drainer warp dhalf
+                    // takes 8 of them) and its row sums of squares into the partner
+                    const int hf = t.pair - 7;
+                    mbar_wait_cluster(pair_ready, hidx & 1);
+                    ++hidx;
+                    const uint32_t rbar = partner_addr(pair_full);
+                    if (drainer) {
+                        const uint32_t ta = tmem + kTAcc + tlane + (1 - hf) * 16 + dhalf * 8;
+                        const uint32_t dst = partner_addr(recv + drow * 32);
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            float4 v;
+                            tmem_ld4(ta + q * 4, v);
+                            st_async_v4(dst + (((dhalf * 2 + q) ^ (drow & 7)) << 4), v, rbar);
+                        }
+                    }
+                    if (wtid < 64) st_async_f32(partner_addr(recv_ss + wtid), sm_ss[wtid], rbar);
+                    mbar_wait_cluster(pair_full, oidx & 1);
+                    ++oidx;
                 } else if (t.pair >= 3) {
                     // Symmetric pair, K split in two, each CTA finalising half of the tile's
                     // columns and pushing its partial of the other half into the partner's receive
@@ -947,18 +968,27 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                                                pack2(silu_fast(v.z + tb.z), silu_fast(v.w + tb.w)));
                         }
                     } else if (t.epi == kEpiHead) {
-                        // Euler: a += (RmsScale z + b) / FS on rows 1..63 (ae.act_rows)
+                        // Euler: a += (RmsScale z + b) / FS on rows 1..63 (ae.act_rows).  CTA pair
+                        // (7 / 8): this CTA's 16 columns, the partner's half-K partial added from
+                        // the receive buffer, RmsScale over both halves' row sums of squares.
+                        const bool hp = t.pair >= 7;
+                        const int q0 = hp ? (t.pair - 7) * 4 : 0, q1 = hp ? q0 + 4 : 8;
                         const bool ok = dhalf == 0 && r < p.chunk;
-                        const float rs = sm_rs[r];
+                        const float rs = hp ? 1.0f / sqrtf((sm_ss[r] + recv_ss[r]) * p.inv_width + p.eps) : sm_rs[r];
                         float4* arow = reinterpret_cast<float4*>(p.a + (size_t)r * p.lda);
                         float4 av[8];
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) av[q] = ok && q * 4 < p.act_dim ? __ldcg(arow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        for (int q = 0; q < 8; ++q)
+                            av[q] = ok && q >= q0 && q < q1 && q * 4 < p.act_dim ? __ldcg(arow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
-                            if (q * 4 >= p.act_dim) break;
+                            if (q < q0 || q >= q1 || q * 4 >= p.act_dim) continue;
                             float4 v;
                             tmem_ld4(ta + q * 4, v);  // warp-uniform: tcgen05.ld is .sync.aligned
+                            if (hp) {
+                                const float4 h = *reinterpret_cast<const float4*>(recv + r * 32 + (((q - q0) ^ (r & 7)) << 2));
+                                v.x += h.x; v.y += h.y; v.z += h.z; v.w += h.w;
+                            }
                             const float4 bv = *reinterpret_cast<const float4*>(sm_vec + q * 4);
                             if (ok)
                                 arow[q] = make_float4(av[q].x + p.euler * (v.x * rs + bv.x), av[q].y + p.euler * (v.y * rs + bv.y),
@@ -1373,7 +1403,7 @@ AePlan ae_plan(const AePlanInput& in) {
     // A phase of full-K tiles split over K between the two CTAs of a cluster (CTAs 2c, 2c + 1):
     // the owner takes the first half of K and runs the epilogue, the helper the second half.
     auto pair_phase = [&](uint8_t epi, int tiles, int wmat, int xmat, int kbt, int wbar, int wcnt, int sbar, int step,
-                          int layer, bool sym = false) {
+                          int layer, bool sym = false, int pair_code = 0) {
         const int nclu = in.num_ctas / 2, h = kbt / 2;
         const double wscale = sym ? 2.0 : 1.0;  // sym tiles are 128 wide (16 KB k-blocks)
         std::vector<std::pair<double, int>> order;
@@ -1386,7 +1416,7 @@ AePlan ae_plan(const AePlanInput& in) {
                 AeTask x = gemm(kXY, epi, wmat, xmat, 0, t, r ? h : 0, r ? kbt - h : h, wbar, wcnt, sbar);
                 x.step = uint16_t(step);
                 x.layer = uint16_t(layer);
-                x.pair = uint16_t(sym ? (r ? 4 : 3) : (in.sym_qkv ? (r ? 6 : 5) : (r ? 2 : 1)));
+                x.pair = uint16_t(pair_code ? pair_code + r : sym ? (r ? 4 : 3) : (in.sym_qkv ? (r ? 6 : 5) : (r ? 2 : 1)));
                 if (sym) x.ncol = 128;
                 const int cta = r ? own ^ 1 : own;
                 load[size_t(cta)] += (r ? kbt - h : h) * kWB * (2.0 + wscale);
@@ -1534,26 +1564,29 @@ AePlan ae_plan(const AePlanInput& in) {
             prev_bar = bar_down;
         }
         const int bar_head = newbar();
-        {
+        if (in.pair_head && in.act_dim == 32 && kbW % 2 == 0 && in.num_ctas % 2 == 0) {
+            // ae.head split over K in one CTA pair (codes 7 / 8): half the fp32 staging each
+            prev_cnt = pair_phase(kEpiHead, 1, in.mat_whead, in.mat_yh, kbW, prev_bar, prev_cnt, bar_head, s, 0, false, 7);
+        } else {
             std::vector<Item> it;
             AeTask x = gemm(kXY, kEpiHead, in.mat_whead, in.mat_yh, 0, 0, 0, kbW, prev_bar, prev_cnt, bar_head);
             x.step = uint16_t(s);
             it.push_back({x, 3.0 * kbW * kWB});
             assign(it);
+            prev_cnt = 1;
         }
-        prev_cnt = 1;
         if (rec) {
             std::vector<Item> it;
             AeTask x{};
             x.kind = kAeRecA;
             x.wait_bar = uint16_t(bar_head);
-            x.wait_cnt = 1;
+            x.wait_cnt = uint16_t(prev_cnt);
             x.sig_bar = uint16_t(bar_head);
             x.aux = uint16_t(s);
             x.phase = uint16_t(phase);
             it.push_back({x, kWB});
             assign(it);
-            prev_cnt = 2;
+            prev_cnt += 1;
         }
         prev_bar = bar_head;
     }

@@ -73,7 +73,8 @@ struct AeTask {
     uint16_t phase;                   // global phase index (debug limit)
     uint16_t pair;                    // full-K tile split over K in a 2-CTA cluster: 1 owner / 2 helper
                                       // (owner finalises), or symmetric (each finalises half):
-                                      // 3 / 4 128-wide ae.ffn tiles, 5 / 6 64-wide ae.qkv tiles
+                                      // 3 / 4 128-wide ae.ffn tiles, 5 / 6 64-wide ae.qkv tiles,
+                                      // 7 / 8 ae.head (16 of the 32 action columns each)
 };
 static_assert(sizeof(AeTask) == 32, "AeTask layout");
 
@@ -131,6 +132,7 @@ struct AePlanInput {
     bool attn_single = true;  // one attention task per (head, key range) instead of (head pair, range)
     bool per_head_proj = true;  // ae.proj tasks wait only for their head's attention key ranges
     bool pair_ffn = true;  // ae.ffn as 128-wide tiles split over K, symmetric exchange (mat_wffn kTilePlain128)
+    bool pair_head = true;  // ae.head split over K in one CTA pair (each CTA finalises 16 action columns)
     int mat_wst, mat_wap, mat_wao, mat_whead;
     std::vector<int> mat_wqkv, mat_wproj, mat_wffn, mat_wdown, mat_kv;
     int mat_y, mat_yh, mat_ap, mat_g, mat_qkv;  // fp32 y rows 0.. / rows 1.. (ae.act_rows)

@@ -1530,7 +1530,8 @@ void Engine::build_ae_mega() {
     in.per_head_proj = env_int("PI0B_AE_HEAD_DEP", 1) != 0;
     in.pair_ffn = env_int("PI0B_AE_PAIR_FFN", 1) != 0 && (2 * MLP) % 128 == 0 && 2 * (2 * MLP / 128) <= ae_ctas_ &&
                   ae_ctas_ % 2 == 0;
-    ae_cluster_ = in.pair_qkv || in.pair_ffn;  // pair tasks need the 2-CTA cluster launch
+    in.pair_head = env_int("PI0B_AE_PAIR_HEAD", 1) != 0;
+    ae_cluster_ = in.pair_qkv || in.pair_ffn || in.pair_head;  // pair tasks need the 2-CTA cluster launch
     in.mat_wst = wmat("ae.state_proj", 0, W);
     in.mat_wap = wmat("ae.action_proj", 0, W);
     in.mat_wao = wmat("ae.action_out", 0, W, in.ao_ncol == 128 ? kTilePlain128 : kTilePlain);
