@@ -768,7 +768,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     const int n = t.epi == kEpiHead ? p.act_dim : 64;
                     if (wtid < n) sm_vec[wtid] = __ldg(vec + wtid);
                 }
-                if (t.epi == kEpiSilu) {  // ae.suffix: y = [st ; b_out] on this tile's columns
+                if (t.epi == kEpiSilu && !p.ydouble) {  // ae.suffix: y = [st ; b_out] on this tile's columns
                     float4 yv[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
@@ -873,7 +873,8 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         // split-K partial -> the fp32 residual stream (rows from `rowoff`)
                         const bool ok = t.rowoff ? r < p.chunk : true;
                         const int hw = t.ncol == 128 ? 64 : 32;  // this thread's column half
-                        float* dst = p.y + (size_t)(r + t.rowoff) * p.width + t.tile * 2 * hw + dhalf * hw;
+                        float* dst = (p.ydouble && (t.step & 1) ? p.y1 : p.y) + (size_t)(r + t.rowoff) * p.width +
+                                     t.tile * 2 * hw + dhalf * hw;
 #pragma unroll 1
                         for (int q = 0; q < hw / 4; ++q) {
                             float4 v;
@@ -1001,7 +1002,12 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                             float4 v;
                             tmem_ld4(ta + dhalf * 32 + q * 4, v);
                             const float4 bv = *reinterpret_cast<const float4*>(sm_vec + dhalf * 32 + q * 4);
-                            if (r == 0) reinterpret_cast<float4*>(p.st + col0)[q] = make_float4(v.x + bv.x, v.y + bv.y, v.z + bv.z, v.w + bv.w);
+                            const float4 sv = make_float4(v.x + bv.x, v.y + bv.y, v.z + bv.z, v.w + bv.w);
+                            if (r == 0) reinterpret_cast<float4*>(p.st + col0)[q] = sv;
+                            // double-buffered y: flow step 0's buffer = [st ; b_out] (ae.suffix)
+                            if (p.ydouble)
+                                reinterpret_cast<float4*>(p.y + (size_t)r * p.width + col0)[q] =
+                                    r == 0 ? sv : __ldg(reinterpret_cast<const float4*>(p.b_out + col0) + q);
                         }
                     }
                 }
@@ -1262,9 +1268,19 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     if (trs) trs[13] = gtimer();
                 }
                 ++aidx;
+            } else if (t.kind == kAeYReset) {
+                // ae.suffix of the NEXT flow step, one step ahead: its buffer = [st ; b_out] on this
+                // task's 64 columns (the buffer's last reader, ae.head of the step before, is done)
+                float* yb = (t.step & 1) ? p.y1 : p.y;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int q = wtid + 256 * u, row = q >> 4, c4 = q & 15;
+                    const float4 v = __ldcg(reinterpret_cast<const float4*>((row == 0 ? p.st : p.b_out) + t.tile * 64) + c4);
+                    reinterpret_cast<float4*>(yb + (size_t)row * p.width + t.tile * 64)[c4] = v;
+                }
             } else if (t.kind == kAeRecY) {
                 const int n4 = 64 * p.width / 4;
-                const float4* s4 = reinterpret_cast<const float4*>(p.y);
+                const float4* s4 = reinterpret_cast<const float4*>(p.ydouble && (t.step & 1) ? p.y1 : p.y);
                 float4* d4 = reinterpret_cast<float4*>(p.rec_y + (size_t)t.aux * 64 * p.width);
                 for (int q = wtid; q < n4; q += kWorkers) d4[q] = __ldcg(s4 + q);
             } else if (t.kind == kAeRecA) {
@@ -1443,7 +1459,7 @@ AePlan ae_plan(const AePlanInput& in) {
     // group_kb > 0: grouped dependency -- the task waits on counter wbar + kb0 / group_kb (the
     // producers of its k-blocks) for group_cnt arrivals instead of the whole producer phase
     auto red_phase = [&](int wmat, int xmat, uint8_t xsrc, int rowoff, int kbt, int ks, int wbar, int wcnt, int sbar,
-                         int ncol = 64, int group_kb = 0, int group_cnt = 0) {
+                         int ncol = 64, int group_kb = 0, int group_cnt = 0, int step = 0) {
         std::vector<Item> it;
         const int per = (kbt + ks - 1) / ks;
         for (int t = 0; t < W / ncol; ++t)
@@ -1453,6 +1469,7 @@ AePlan ae_plan(const AePlanInput& in) {
                 AeTask x = group_kb ? gemm(xsrc, kEpiRed, wmat, xmat, rowoff, t, kb0, nkb, wbar + kb0 / group_kb, group_cnt, sbar)
                                     : gemm(xsrc, kEpiRed, wmat, xmat, rowoff, t, kb0, nkb, wbar, wcnt, sbar);
                 x.ncol = uint16_t(ncol);
+                x.step = uint16_t(step);  // (double-buffered y: the step's buffer)
                 it.push_back({x, nkb * kWB * ncol / 64});
             }
         assign(it);
@@ -1469,20 +1486,50 @@ AePlan ae_plan(const AePlanInput& in) {
     int prev_bar = bar_init;
     int prev_cnt = full_phase(kXRows, kEpiInit, tiles_w, in.mat_wst, 0, 1, 0, 0, bar_init, 0);
     int rec_slot = 0;
+    const bool yd = in.mat_y1 >= 0 && in.mat_yh1 >= 0;  // double-buffered residual stream
     for (int s = 0; s < FS; ++s) {
+        const int mat_y = yd && (s & 1) ? in.mat_y1 : in.mat_y, mat_yh = yd && (s & 1) ? in.mat_yh1 : in.mat_yh;
         const int bar_ap = newbar();
-        const int n_ap = full_phase(kXRows, kEpiSilu, tiles_w, in.mat_wap, 0, 1, prev_bar, prev_cnt, bar_ap, s);
+        int n_ap = full_phase(kXRows, kEpiSilu, tiles_w, in.mat_wap, 0, 1, prev_bar, prev_cnt, bar_ap, s);
+        if (yd && s + 1 < FS) {
+            // The NEXT flow step's residual buffer = [st ; b_out] (its last reader, ae.head of the
+            // step before this one, is done: this phase waits for it), on CTAs without an
+            // ae.action_proj task; counted in this phase, so ae.action_out waits for it.
+            std::vector<char> busy(size_t(in.num_ctas), 0);
+            for (int c = 0; c < in.num_ctas; ++c)
+                busy[size_t(c)] = !lists[size_t(c)].empty() && lists[size_t(c)].back().phase == uint16_t(phase - 1);
+            std::vector<QE> cand;
+            for (int c = 0; c < in.num_ctas; ++c)
+                if (!busy[size_t(c)]) cand.push_back({load[size_t(c)], c});
+            std::sort(cand.begin(), cand.end());
+            need(int(cand.size()) >= tiles_w, "idle CTAs for the residual-buffer reset");
+            for (int t = 0; t < tiles_w; ++t) {
+                AeTask x{};
+                x.kind = kAeYReset;
+                x.tile = uint16_t(t);
+                x.step = uint16_t(s + 1);
+                x.wait_bar = uint16_t(prev_bar);
+                x.wait_cnt = uint16_t(prev_cnt);
+                x.sig_bar = uint16_t(bar_ap);
+                x.phase = uint16_t(phase);
+                const int c = cand[size_t(t)].second;
+                lists[size_t(c)].push_back(x);
+                load[size_t(c)] += kWB;
+            }
+            ++phase;
+            n_ap += tiles_w;
+        }
         const int bar_ao = newbar();
-        prev_cnt = red_phase(in.mat_wao, in.mat_ap, kXBf16, 1, kbW, ks_ao, bar_ap, n_ap, bar_ao, in.ao_ncol);
+        prev_cnt = red_phase(in.mat_wao, in.mat_ap, kXBf16, 1, kbW, ks_ao, bar_ap, n_ap, bar_ao, in.ao_ncol, 0, 0, s);
         prev_bar = bar_ao;
         for (int l = 0; l < NA; ++l) {
             const int gl = s * NA + l;
             const int bar_qkv = newbar();
             const bool pq = in.pair_qkv && 2 * tiles_qkv <= in.num_ctas && (in.num_ctas % 2) == 0;
-            const int n_qkv = pq ? pair_phase(kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], in.mat_y, kbW, prev_bar, prev_cnt,
-                                              bar_qkv, s, l)
-                                 : full_phase(kXY, kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], in.mat_y, kbW, prev_bar,
-                                              prev_cnt, bar_qkv, s, l);
+            int n_qkv = pq ? pair_phase(kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], mat_y, kbW, prev_bar, prev_cnt,
+                                        bar_qkv, s, l)
+                           : full_phase(kXY, kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], mat_y, kbW, prev_bar,
+                                        prev_cnt, bar_qkv, s, l);
             // Attention signals one counter per head (pair) and each ae.proj task waits only for the
             // key ranges of the head its k-blocks belong to (no extra release: one signal per task).
             // Safe for y: its readers before ae.proj's red.add (the ae.qkv tasks) all finished
@@ -1519,7 +1566,7 @@ AePlan ae_plan(const AePlanInput& in) {
             std::vector<size_t> proj_from(lists.size());  // the ae.proj tasks are appended after these
             for (size_t c = 0; c < lists.size(); ++c) proj_from[c] = lists[c].size();
             const int n_proj = red_phase(in.mat_wproj[size_t(l)], 0, kXO, 0, in.q_width / 64, ks_proj, bar_attn, n_attn,
-                                         bar_proj, in.proj_ncol, per_head ? (in.attn_single ? 4 : 8) : 0, splits);
+                                         bar_proj, in.proj_ncol, per_head ? (in.attn_single ? 4 : 8) : 0, splits, s);
             if (per_head) {
                 // The grouped ae.proj waits are safe for the NEXT layer's writes of opart / ml /
                 // qkv only because ae.ffn waits for every ae.proj task and, together, the ae.proj
@@ -1541,17 +1588,18 @@ AePlan ae_plan(const AePlanInput& in) {
             // ae.ffn task still staging y)
             const int bar_ffn = newbar();
             need(!pf || ((2 * MLP) % 128 == 0 && 2 * (2 * MLP / 128) <= in.num_ctas && in.num_ctas % 2 == 0), "ae.ffn pairs");
-            const int n_ffn = pf ? pair_phase(kEpiGate, 2 * MLP / 128, in.mat_wffn[size_t(l)], in.mat_y, kbW, bar_proj, n_proj,
+            const int n_ffn = pf ? pair_phase(kEpiGate, 2 * MLP / 128, in.mat_wffn[size_t(l)], mat_y, kbW, bar_proj, n_proj,
                                               bar_ffn, s, l, true)
-                                 : full_phase(kXY, kEpiGate, tiles_ffn, in.mat_wffn[size_t(l)], in.mat_y, kbW, bar_proj,
+                                 : full_phase(kXY, kEpiGate, tiles_ffn, in.mat_wffn[size_t(l)], mat_y, kbW, bar_proj,
                                               n_proj, bar_ffn, s, l);
             const int bar_down = newbar();
             prev_cnt = red_phase(in.mat_wdown[size_t(l)], in.mat_g, kXBf16, 0, MLP / 64, ks_down, bar_ffn, n_ffn, bar_down,
-                                 in.down_ncol);
+                                 in.down_ncol, 0, 0, s);
             if (rec) {
                 std::vector<Item> it;
                 AeTask x{};
                 x.kind = kAeRecY;
+                x.step = uint16_t(s);
                 x.wait_bar = uint16_t(bar_down);
                 x.wait_cnt = uint16_t(prev_cnt);
                 x.sig_bar = uint16_t(bar_down);
@@ -1566,10 +1614,10 @@ AePlan ae_plan(const AePlanInput& in) {
         const int bar_head = newbar();
         if (in.pair_head && in.act_dim == 32 && kbW % 2 == 0 && in.num_ctas % 2 == 0) {
             // ae.head split over K in one CTA pair (codes 7 / 8): half the fp32 staging each
-            prev_cnt = pair_phase(kEpiHead, 1, in.mat_whead, in.mat_yh, kbW, prev_bar, prev_cnt, bar_head, s, 0, false, 7);
+            prev_cnt = pair_phase(kEpiHead, 1, in.mat_whead, mat_yh, kbW, prev_bar, prev_cnt, bar_head, s, 0, false, 7);
         } else {
             std::vector<Item> it;
-            AeTask x = gemm(kXY, kEpiHead, in.mat_whead, in.mat_yh, 0, 0, 0, kbW, prev_bar, prev_cnt, bar_head);
+            AeTask x = gemm(kXY, kEpiHead, in.mat_whead, mat_yh, 0, 0, 0, kbW, prev_bar, prev_cnt, bar_head);
             x.step = uint16_t(s);
             it.push_back({x, 3.0 * kbW * kWB});
             assign(it);

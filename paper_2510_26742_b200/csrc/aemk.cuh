@@ -33,7 +33,7 @@
 
 namespace pi0b {
 
-enum AeTaskKind : uint8_t { kAeEnd = 0, kAeGemm = 1, kAeAttn = 2, kAeRecY = 3, kAeRecA = 4 };
+enum AeTaskKind : uint8_t { kAeEnd = 0, kAeGemm = 1, kAeAttn = 2, kAeRecY = 3, kAeRecA = 4, kAeYReset = 5 };
 
 // How the 64-row activation operand of a GEMM task reaches shared memory (always cp.async).
 enum AeXSrc : uint8_t {
@@ -84,7 +84,10 @@ struct AeParams {
     const AeMat* mats;             // operand table
     unsigned* bars;                // [n_bars] phase arrival counters, zero on entry
     int n_bars;
-    float* y;                      // [64, W]   residual stream (row 0 = state token)
+    float* y;                      // [64, W]   residual stream (row 0 = state token); even flow steps
+    float* y1;                     // [64, W]   the residual stream of odd flow steps (ydouble)
+    int ydouble;                   // 1: flow step s uses y / y1 by parity, each re-initialised to
+                                   // [st ; b_out] one step ahead by kAeYReset tasks (INIT for step 0)
     float* a;                      // [C, lda]  Euler state
     int lda;
     const float* state;            // [state_dim] fp32
@@ -136,6 +139,7 @@ struct AePlanInput {
     int mat_wst, mat_wap, mat_wao, mat_whead;
     std::vector<int> mat_wqkv, mat_wproj, mat_wffn, mat_wdown, mat_kv;
     int mat_y, mat_yh, mat_ap, mat_g, mat_qkv;  // fp32 y rows 0.. / rows 1.. (ae.act_rows)
+    int mat_y1 = -1, mat_yh1 = -1;                // the odd-step buffer (-1: one buffer, AP resets y)
 };
 
 // Weight row order of one tile of a tile-contiguous AE weight copy (64-row tiles; ae.proj uses
