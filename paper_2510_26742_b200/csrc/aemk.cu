@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             // Pair owner: its receive buffer (union tail) is free from here on -- tell the helper.
             if ((t.pair == 1 || t.pair >= 3) && wtid == 0) {
                 // the partner's st.async bytes: its partial of this CTA's columns + 64 row sums
-                mbar_arrive_expect_tx(pair_full, (t.pair >= 7 ? 64 * 16 * 4 : t.pair >= 5 ? 64 * 32 * 4 : 64 * 64 * 4) + 64 * 4);
+                mbar_arrive_expect_tx(pair_full, (t.pair >= 5 ? 64 * 32 * 4 : 64 * 64 * 4) + 64 * 4);
                 mbar_arrive_remote(partner_addr(pair_ready));
             }
             // Attention over a range of cached LLM keys: K does not depend on this step, so its
@@ -768,7 +768,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     const int n = t.epi == kEpiHead ? p.act_dim : 64;
                     if (wtid < n) sm_vec[wtid] = __ldg(vec + wtid);
                 }
-                if (t.epi == kEpiSilu && !p.ydouble) {  // ae.suffix: y = [st ; b_out] on this tile's columns
+                if (t.epi == kEpiSilu) {  // ae.suffix: y = [st ; b_out] on this tile's columns
                     float4 yv[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
@@ -815,27 +815,6 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 } else if (t.pair == 1) {
                     mbar_wait_cluster(pair_full, oidx & 1);
                     ++oidx;
-                } else if (t.pair >= 7) {
-                    // ae.head split over K in a CTA pair (7 / 8): each CTA finalises 16 of the 32
-                    // action columns; it pushes its partial of the other 16 (drainer warp dhalf
-                    // takes 8 of them) and its row sums of squares into the partner
-                    const int hf = t.pair - 7;
-                    mbar_wait_cluster(pair_ready, hidx & 1);
-                    ++hidx;
-                    const uint32_t rbar = partner_addr(pair_full);
-                    if (drainer) {
-                        const uint32_t ta = tmem + kTAcc + tlane + (1 - hf) * 16 + dhalf * 8;
-                        const uint32_t dst = partner_addr(recv + drow * 32);
-#pragma unroll
-                        for (int q = 0; q < 2; ++q) {
-                            float4 v;
-                            tmem_ld4(ta + q * 4, v);
-                            st_async_v4(dst + (((dhalf * 2 + q) ^ (drow & 7)) << 4), v, rbar);
-                        }
-                    }
-                    if (wtid < 64) st_async_f32(partner_addr(recv_ss + wtid), sm_ss[wtid], rbar);
-                    mbar_wait_cluster(pair_full, oidx & 1);
-                    ++oidx;
                 } else if (t.pair >= 3) {
                     // Symmetric pair, K split in two, each CTA finalising half of the tile's
                     // columns and pushing its partial of the other half into the partner's receive
@@ -873,8 +852,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         // split-K partial -> the fp32 residual stream (rows from `rowoff`)
                         const bool ok = t.rowoff ? r < p.chunk : true;
                         const int hw = t.ncol == 128 ? 64 : 32;  // this thread's column half
-                        float* dst = (p.ydouble && (t.step & 1) ? p.y1 : p.y) + (size_t)(r + t.rowoff) * p.width +
-                                     t.tile * 2 * hw + dhalf * hw;
+                        float* dst = p.y + (size_t)(r + t.rowoff) * p.width + t.tile * 2 * hw + dhalf * hw;
 #pragma unroll 1
                         for (int q = 0; q < hw / 4; ++q) {
                             float4 v;
@@ -969,27 +947,18 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                                                pack2(silu_fast(v.z + tb.z), silu_fast(v.w + tb.w)));
                         }
                     } else if (t.epi == kEpiHead) {
-                        // Euler: a += (RmsScale z + b) / FS on rows 1..63 (ae.act_rows).  CTA pair
-                        // (7 / 8): this CTA's 16 columns, the partner's half-K partial added from
-                        // the receive buffer, RmsScale over both halves' row sums of squares.
-                        const bool hp = t.pair >= 7;
-                        const int q0 = hp ? (t.pair - 7) * 4 : 0, q1 = hp ? q0 + 4 : 8;
+                        // Euler: a += (RmsScale z + b) / FS on rows 1..63 (ae.act_rows)
                         const bool ok = dhalf == 0 && r < p.chunk;
-                        const float rs = hp ? 1.0f / sqrtf((sm_ss[r] + recv_ss[r]) * p.inv_width + p.eps) : sm_rs[r];
+                        const float rs = sm_rs[r];
                         float4* arow = reinterpret_cast<float4*>(p.a + (size_t)r * p.lda);
                         float4 av[8];
 #pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            av[q] = ok && q >= q0 && q < q1 && q * 4 < p.act_dim ? __ldcg(arow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        for (int q = 0; q < 8; ++q) av[q] = ok && q * 4 < p.act_dim ? __ldcg(arow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
-                            if (q < q0 || q >= q1 || q * 4 >= p.act_dim) continue;
+                            if (q * 4 >= p.act_dim) break;
                             float4 v;
                             tmem_ld4(ta + q * 4, v);  // warp-uniform: tcgen05.ld is .sync.aligned
-                            if (hp) {
-                                const float4 h = *reinterpret_cast<const float4*>(recv + r * 32 + (((q - q0) ^ (r & 7)) << 2));
-                                v.x += h.x; v.y += h.y; v.z += h.z; v.w += h.w;
-                            }
                             const float4 bv = *reinterpret_cast<const float4*>(sm_vec + q * 4);
                             if (ok)
                                 arow[q] = make_float4(av[q].x + p.euler * (v.x * rs + bv.x), av[q].y + p.euler * (v.y * rs + bv.y),
@@ -1002,12 +971,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                             float4 v;
                             tmem_ld4(ta + dhalf * 32 + q * 4, v);
                             const float4 bv = *reinterpret_cast<const float4*>(sm_vec + dhalf * 32 + q * 4);
-                            const float4 sv = make_float4(v.x + bv.x, v.y + bv.y, v.z + bv.z, v.w + bv.w);
-                            if (r == 0) reinterpret_cast<float4*>(p.st + col0)[q] = sv;
-                            // double-buffered y: flow step 0's buffer = [st ; b_out] (ae.suffix)
-                            if (p.ydouble)
-                                reinterpret_cast<float4*>(p.y + (size_t)r * p.width + col0)[q] =
-                                    r == 0 ? sv : __ldg(reinterpret_cast<const float4*>(p.b_out + col0) + q);
+                            if (r == 0) reinterpret_cast<float4*>(p.st + col0)[q] = make_float4(v.x + bv.x, v.y + bv.y, v.z + bv.z, v.w + bv.w);
                         }
                     }
                 }
@@ -1268,19 +1232,9 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     if (trs) trs[13] = gtimer();
                 }
                 ++aidx;
-            } else if (t.kind == kAeYReset) {
-                // ae.suffix of the NEXT flow step, one step ahead: its buffer = [st ; b_out] on this
-                // task's 64 columns (the buffer's last reader, ae.head of the step before, is done)
-                float* yb = (t.step & 1) ? p.y1 : p.y;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int q = wtid + 256 * u, row = q >> 4, c4 = q & 15;
-                    const float4 v = __ldcg(reinterpret_cast<const float4*>((row == 0 ? p.st : p.b_out) + t.tile * 64) + c4);
-                    reinterpret_cast<float4*>(yb + (size_t)row * p.width + t.tile * 64)[c4] = v;
-                }
             } else if (t.kind == kAeRecY) {
                 const int n4 = 64 * p.width / 4;
-                const float4* s4 = reinterpret_cast<const float4*>(p.ydouble && (t.step & 1) ? p.y1 : p.y);
+                const float4* s4 = reinterpret_cast<const float4*>(p.y);
                 float4* d4 = reinterpret_cast<float4*>(p.rec_y + (size_t)t.aux * 64 * p.width);
                 for (int q = wtid; q < n4; q += kWorkers) d4[q] = __ldcg(s4 + q);
             } else if (t.kind == kAeRecA) {
@@ -1419,7 +1373,7 @@ AePlan ae_plan(const AePlanInput& in) {
     // A phase of full-K tiles split over K between the two CTAs of a cluster (CTAs 2c, 2c + 1):
     // the owner takes the first half of K and runs the epilogue, the helper the second half.
     auto pair_phase = [&](uint8_t epi, int tiles, int wmat, int xmat, int kbt, int wbar, int wcnt, int sbar, int step,
-                          int layer, bool sym = false, int pair_code = 0) {
+                          int layer, bool sym = false) {
         const int nclu = in.num_ctas / 2, h = kbt / 2;
         const double wscale = sym ? 2.0 : 1.0;  // sym tiles are 128 wide (16 KB k-blocks)
         std::vector<std::pair<double, int>> order;
@@ -1432,7 +1386,7 @@ AePlan ae_plan(const AePlanInput& in) {
                 AeTask x = gemm(kXY, epi, wmat, xmat, 0, t, r ? h : 0, r ? kbt - h : h, wbar, wcnt, sbar);
                 x.step = uint16_t(step);
                 x.layer = uint16_t(layer);
-                x.pair = uint16_t(pair_code ? pair_code + r : sym ? (r ? 4 : 3) : (in.sym_qkv ? (r ? 6 : 5) : (r ? 2 : 1)));
+                x.pair = uint16_t(sym ? (r ? 4 : 3) : (in.sym_qkv ? (r ? 6 : 5) : (r ? 2 : 1)));
                 if (sym) x.ncol = 128;
                 const int cta = r ? own ^ 1 : own;
                 load[size_t(cta)] += (r ? kbt - h : h) * kWB * (2.0 + wscale);
@@ -1459,7 +1413,7 @@ AePlan ae_plan(const AePlanInput& in) {
     // group_kb > 0: grouped dependency -- the task waits on counter wbar + kb0 / group_kb (the
     // producers of its k-blocks) for group_cnt arrivals instead of the whole producer phase
     auto red_phase = [&](int wmat, int xmat, uint8_t xsrc, int rowoff, int kbt, int ks, int wbar, int wcnt, int sbar,
-                         int ncol = 64, int group_kb = 0, int group_cnt = 0, int step = 0) {
+                         int ncol = 64, int group_kb = 0, int group_cnt = 0) {
         std::vector<Item> it;
         const int per = (kbt + ks - 1) / ks;
         for (int t = 0; t < W / ncol; ++t)
@@ -1469,7 +1423,6 @@ AePlan ae_plan(const AePlanInput& in) {
                 AeTask x = group_kb ? gemm(xsrc, kEpiRed, wmat, xmat, rowoff, t, kb0, nkb, wbar + kb0 / group_kb, group_cnt, sbar)
                                     : gemm(xsrc, kEpiRed, wmat, xmat, rowoff, t, kb0, nkb, wbar, wcnt, sbar);
                 x.ncol = uint16_t(ncol);
-                x.step = uint16_t(step);  // (double-buffered y: the step's buffer)
                 it.push_back({x, nkb * kWB * ncol / 64});
             }
         assign(it);
@@ -1486,50 +1439,20 @@ AePlan ae_plan(const AePlanInput& in) {
     int prev_bar = bar_init;
     int prev_cnt = full_phase(kXRows, kEpiInit, tiles_w, in.mat_wst, 0, 1, 0, 0, bar_init, 0);
     int rec_slot = 0;
-    const bool yd = in.mat_y1 >= 0 && in.mat_yh1 >= 0;  // double-buffered residual stream
     for (int s = 0; s < FS; ++s) {
-        const int mat_y = yd && (s & 1) ? in.mat_y1 : in.mat_y, mat_yh = yd && (s & 1) ? in.mat_yh1 : in.mat_yh;
         const int bar_ap = newbar();
-        int n_ap = full_phase(kXRows, kEpiSilu, tiles_w, in.mat_wap, 0, 1, prev_bar, prev_cnt, bar_ap, s);
-        if (yd && s + 1 < FS) {
-            // The NEXT flow step's residual buffer = [st ; b_out] (its last reader, ae.head of the
-            // step before this one, is done: this phase waits for it), on CTAs without an
-            // ae.action_proj task; counted in this phase, so ae.action_out waits for it.
-            std::vector<char> busy(size_t(in.num_ctas), 0);
-            for (int c = 0; c < in.num_ctas; ++c)
-                busy[size_t(c)] = !lists[size_t(c)].empty() && lists[size_t(c)].back().phase == uint16_t(phase - 1);
-            std::vector<QE> cand;
-            for (int c = 0; c < in.num_ctas; ++c)
-                if (!busy[size_t(c)]) cand.push_back({load[size_t(c)], c});
-            std::sort(cand.begin(), cand.end());
-            need(int(cand.size()) >= tiles_w, "idle CTAs for the residual-buffer reset");
-            for (int t = 0; t < tiles_w; ++t) {
-                AeTask x{};
-                x.kind = kAeYReset;
-                x.tile = uint16_t(t);
-                x.step = uint16_t(s + 1);
-                x.wait_bar = uint16_t(prev_bar);
-                x.wait_cnt = uint16_t(prev_cnt);
-                x.sig_bar = uint16_t(bar_ap);
-                x.phase = uint16_t(phase);
-                const int c = cand[size_t(t)].second;
-                lists[size_t(c)].push_back(x);
-                load[size_t(c)] += kWB;
-            }
-            ++phase;
-            n_ap += tiles_w;
-        }
+        const int n_ap = full_phase(kXRows, kEpiSilu, tiles_w, in.mat_wap, 0, 1, prev_bar, prev_cnt, bar_ap, s);
         const int bar_ao = newbar();
-        prev_cnt = red_phase(in.mat_wao, in.mat_ap, kXBf16, 1, kbW, ks_ao, bar_ap, n_ap, bar_ao, in.ao_ncol, 0, 0, s);
+        prev_cnt = red_phase(in.mat_wao, in.mat_ap, kXBf16, 1, kbW, ks_ao, bar_ap, n_ap, bar_ao, in.ao_ncol);
         prev_bar = bar_ao;
         for (int l = 0; l < NA; ++l) {
             const int gl = s * NA + l;
             const int bar_qkv = newbar();
             const bool pq = in.pair_qkv && 2 * tiles_qkv <= in.num_ctas && (in.num_ctas % 2) == 0;
-            int n_qkv = pq ? pair_phase(kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], mat_y, kbW, prev_bar, prev_cnt,
-                                        bar_qkv, s, l)
-                           : full_phase(kXY, kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], mat_y, kbW, prev_bar,
-                                        prev_cnt, bar_qkv, s, l);
+            const int n_qkv = pq ? pair_phase(kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], in.mat_y, kbW, prev_bar, prev_cnt,
+                                              bar_qkv, s, l)
+                                 : full_phase(kXY, kEpiQkv, tiles_qkv, in.mat_wqkv[size_t(l)], in.mat_y, kbW, prev_bar,
+                                              prev_cnt, bar_qkv, s, l);
             // Attention signals one counter per head (pair) and each ae.proj task waits only for the
             // key ranges of the head its k-blocks belong to (no extra release: one signal per task).
             // Safe for y: its readers before ae.proj's red.add (the ae.qkv tasks) all finished
@@ -1566,7 +1489,7 @@ AePlan ae_plan(const AePlanInput& in) {
             std::vector<size_t> proj_from(lists.size());  // the ae.proj tasks are appended after these
             for (size_t c = 0; c < lists.size(); ++c) proj_from[c] = lists[c].size();
             const int n_proj = red_phase(in.mat_wproj[size_t(l)], 0, kXO, 0, in.q_width / 64, ks_proj, bar_attn, n_attn,
-                                         bar_proj, in.proj_ncol, per_head ? (in.attn_single ? 4 : 8) : 0, splits, s);
+                                         bar_proj, in.proj_ncol, per_head ? (in.attn_single ? 4 : 8) : 0, splits);
             if (per_head) {
                 // The grouped ae.proj waits are safe for the NEXT layer's writes of opart / ml /
                 // qkv only because ae.ffn waits for every ae.proj task and, together, the ae.proj
@@ -1588,18 +1511,17 @@ AePlan ae_plan(const AePlanInput& in) {
             // ae.ffn task still staging y)
             const int bar_ffn = newbar();
             need(!pf || ((2 * MLP) % 128 == 0 && 2 * (2 * MLP / 128) <= in.num_ctas && in.num_ctas % 2 == 0), "ae.ffn pairs");
-            const int n_ffn = pf ? pair_phase(kEpiGate, 2 * MLP / 128, in.mat_wffn[size_t(l)], mat_y, kbW, bar_proj, n_proj,
+            const int n_ffn = pf ? pair_phase(kEpiGate, 2 * MLP / 128, in.mat_wffn[size_t(l)], in.mat_y, kbW, bar_proj, n_proj,
                                               bar_ffn, s, l, true)
-                                 : full_phase(kXY, kEpiGate, tiles_ffn, in.mat_wffn[size_t(l)], mat_y, kbW, bar_proj,
+                                 : full_phase(kXY, kEpiGate, tiles_ffn, in.mat_wffn[size_t(l)], in.mat_y, kbW, bar_proj,
                                               n_proj, bar_ffn, s, l);
             const int bar_down = newbar();
             prev_cnt = red_phase(in.mat_wdown[size_t(l)], in.mat_g, kXBf16, 0, MLP / 64, ks_down, bar_ffn, n_ffn, bar_down,
-                                 in.down_ncol, 0, 0, s);
+                                 in.down_ncol);
             if (rec) {
                 std::vector<Item> it;
                 AeTask x{};
                 x.kind = kAeRecY;
-                x.step = uint16_t(s);
                 x.wait_bar = uint16_t(bar_down);
                 x.wait_cnt = uint16_t(prev_cnt);
                 x.sig_bar = uint16_t(bar_down);
@@ -1612,29 +1534,26 @@ AePlan ae_plan(const AePlanInput& in) {
             prev_bar = bar_down;
         }
         const int bar_head = newbar();
-        if (in.pair_head && in.act_dim == 32 && kbW % 2 == 0 && in.num_ctas % 2 == 0) {
-            // ae.head split over K in one CTA pair (codes 7 / 8): half the fp32 staging each
-            prev_cnt = pair_phase(kEpiHead, 1, in.mat_whead, mat_yh, kbW, prev_bar, prev_cnt, bar_head, s, 0, false, 7);
-        } else {
+        {
             std::vector<Item> it;
-            AeTask x = gemm(kXY, kEpiHead, in.mat_whead, mat_yh, 0, 0, 0, kbW, prev_bar, prev_cnt, bar_head);
+            AeTask x = gemm(kXY, kEpiHead, in.mat_whead, in.mat_yh, 0, 0, 0, kbW, prev_bar, prev_cnt, bar_head);
             x.step = uint16_t(s);
             it.push_back({x, 3.0 * kbW * kWB});
             assign(it);
-            prev_cnt = 1;
         }
+        prev_cnt = 1;
         if (rec) {
             std::vector<Item> it;
             AeTask x{};
             x.kind = kAeRecA;
             x.wait_bar = uint16_t(bar_head);
-            x.wait_cnt = uint16_t(prev_cnt);
+            x.wait_cnt = 1;
             x.sig_bar = uint16_t(bar_head);
             x.aux = uint16_t(s);
             x.phase = uint16_t(phase);
             it.push_back({x, kWB});
             assign(it);
-            prev_cnt += 1;
+            prev_cnt = 2;
         }
         prev_bar = bar_head;
     }

@@ -33,7 +33,7 @@
 
 namespace pi0b {
 
-enum AeTaskKind : uint8_t { kAeEnd = 0, kAeGemm = 1, kAeAttn = 2, kAeRecY = 3, kAeRecA = 4, kAeYReset = 5 };
+enum AeTaskKind : uint8_t { kAeEnd = 0, kAeGemm = 1, kAeAttn = 2, kAeRecY = 3, kAeRecA = 4 };
 
 // How the 64-row activation operand of a GEMM task reaches shared memory (always cp.async).
 enum AeXSrc : uint8_t {
@@ -73,8 +73,7 @@ struct AeTask {
     uint16_t phase;                   // global phase index (debug limit)
     uint16_t pair;                    // full-K tile split over K in a 2-CTA cluster: 1 owner / 2 helper
                                       // (owner finalises), or symmetric (each finalises half):
-                                      // 3 / 4 128-wide ae.ffn tiles, 5 / 6 64-wide ae.qkv tiles,
-                                      // 7 / 8 ae.head (16 of the 32 action columns each)
+                                      // 3 / 4 128-wide ae.ffn tiles, 5 / 6 64-wide ae.qkv tiles
 };
 static_assert(sizeof(AeTask) == 32, "AeTask layout");
 
@@ -84,10 +83,7 @@ struct AeParams {
     const AeMat* mats;             // operand table
     unsigned* bars;                // [n_bars] phase arrival counters, zero on entry
     int n_bars;
-    float* y;                      // [64, W]   residual stream (row 0 = state token); even flow steps
-    float* y1;                     // [64, W]   the residual stream of odd flow steps (ydouble)
-    int ydouble;                   // 1: flow step s uses y / y1 by parity, each re-initialised to
-                                   // [st ; b_out] one step ahead by kAeYReset tasks (INIT for step 0)
+    float* y;                      // [64, W]   residual stream (row 0 = state token)
     float* a;                      // [C, lda]  Euler state
     int lda;
     const float* state;            // [state_dim] fp32
@@ -135,11 +131,9 @@ struct AePlanInput {
     bool attn_single = true;  // one attention task per (head, key range) instead of (head pair, range)
     bool per_head_proj = true;  // ae.proj tasks wait only for their head's attention key ranges
     bool pair_ffn = true;  // ae.ffn as 128-wide tiles split over K, symmetric exchange (mat_wffn kTilePlain128)
-    bool pair_head = true;  // ae.head split over K in one CTA pair (each CTA finalises 16 action columns)
     int mat_wst, mat_wap, mat_wao, mat_whead;
     std::vector<int> mat_wqkv, mat_wproj, mat_wffn, mat_wdown, mat_kv;
     int mat_y, mat_yh, mat_ap, mat_g, mat_qkv;  // fp32 y rows 0.. / rows 1.. (ae.act_rows)
-    int mat_y1 = -1, mat_yh1 = -1;                // the odd-step buffer (-1: one buffer, AP resets y)
 };
 
 // Weight row order of one tile of a tile-contiguous AE weight copy (64-row tiles; ae.proj uses

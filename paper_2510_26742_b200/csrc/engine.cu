@@ -509,7 +509,7 @@ private:
     std::vector<__nv_bfloat16*> kv_;  // per LLM layer [L, q+2kv]
     __nv_bfloat16 *state_b_ = nullptr, *ab_ = nullptr, *ap_b_ = nullptr, *yb_ = nullptr,
                   *aqkv_ = nullptr, *ao_ = nullptr, *ag_ = nullptr;
-    float *st_ = nullptr, *y_ = nullptr, *y1_ = nullptr, *a_ = nullptr;
+    float *st_ = nullptr, *y_ = nullptr, *a_ = nullptr;
     float* rope_cs_ = nullptr;
     float* stats_[2] = {nullptr, nullptr};
     int stats_rows_ = 0, stats_used_[2] = {0, 0}, stats_cap_[2] = {0, 0};
@@ -1530,8 +1530,7 @@ void Engine::build_ae_mega() {
     in.per_head_proj = env_int("PI0B_AE_HEAD_DEP", 1) != 0;
     in.pair_ffn = env_int("PI0B_AE_PAIR_FFN", 1) != 0 && (2 * MLP) % 128 == 0 && 2 * (2 * MLP / 128) <= ae_ctas_ &&
                   ae_ctas_ % 2 == 0;
-    in.pair_head = env_int("PI0B_AE_PAIR_HEAD", 1) != 0;
-    ae_cluster_ = in.pair_qkv || in.pair_ffn || in.pair_head;  // pair tasks need the 2-CTA cluster launch
+    ae_cluster_ = in.pair_qkv || in.pair_ffn;  // pair tasks need the 2-CTA cluster launch
     in.mat_wst = wmat("ae.state_proj", 0, W);
     in.mat_wap = wmat("ae.action_proj", 0, W);
     in.mat_wao = wmat("ae.action_out", 0, W, in.ao_ncol == 128 ? kTilePlain128 : kTilePlain);
@@ -1547,15 +1546,6 @@ void Engine::build_ae_mega() {
         in.mat_kv.push_back(add(kv_[size_t(l)], Lp_, llm_qkv_n, llm_qkv_n));
     in.mat_y = add(y_, S_, W, W);
     in.mat_yh = add(y_ + W, C_, W, W);  // ae.act_rows: rows 1..63
-    // Double-buffered residual stream (PI0B_AE_YDOUBLE, default on): odd flow steps use y1, and
-    // each step's buffer is set to [st ; b_out] one step ahead by idle CTAs instead of by the
-    // ae.action_proj tasks on the critical path
-    const bool ydouble = env_int("PI0B_AE_YDOUBLE", 1) != 0;
-    if (ydouble) {
-        y1_ = alloc<float>(size_t(S_) * W);
-        in.mat_y1 = add(y1_, S_, W, W);
-        in.mat_yh1 = add(y1_ + W, C_, W, W);
-    }
     in.mat_ap = add(ap_b_, C_, W, W);
     in.mat_g = add(ag_, S_, MLP, MLP);
     in.mat_qkv = add(aqkv_, S_, NQ, NQ);
@@ -1602,8 +1592,6 @@ void Engine::build_ae_mega() {
     P.bars = reinterpret_cast<unsigned*>(z);
     P.n_bars = ae_plan_.n_bars;
     P.y = y_;
-    P.y1 = y1_;
-    P.ydouble = ydouble ? 1 : 0;
     P.a = a_;
     P.lda = act_ld_;
     P.state = state32_;

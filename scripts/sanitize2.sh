@@ -11,7 +11,7 @@ for tool in memcheck racecheck synccheck; do
 done
 # (the one-device view-shard test cannot run under the sanitizer: it serialises kernels, so a shard
 # engine's wait kernel spins on a peer stream that never runs and traps after 10 s)
-export PI0B_AE_PAIR=0 PI0B_AE_PAIR_FFN=0 PI0B_AE_SYM_QKV=0 PI0B_AE_PAIR_HEAD=0
+export PI0B_AE_PAIR=0 PI0B_AE_PAIR_FFN=0 PI0B_AE_SYM_QKV=0
 for tool in memcheck racecheck; do
   timeout ${T_SAN:-900} $CS --tool $tool python scripts/sanitize_run.py 1 17 > gpurun_out/sanitize2_prompt17_$tool.log 2>&1
   echo "engine 1v+17p $tool rc=$?: $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|max \|engine' gpurun_out/sanitize2_prompt17_$tool.log | tr '\n' ' ')"
