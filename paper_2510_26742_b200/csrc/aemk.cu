@@ -1078,21 +1078,17 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     float sv[32];
                     tmem_ld32(tmem + kTS + tlane + kh * 64 + side * 32, sv);  // warp-uniform
                     const int nkm = kh < nb ? min(32, max(0, nk - (kh * 64 + side * 32))) : 0;
-                    // padding keys of the cached prefix [kv_valid0, kv_rows0), relative to this chunk
-                    const int kc = key0 + kh * 64 + side * 32, pad_lo = p.kv_valid0 - kc, pad_hi = p.kv_rows0 - kc;
+                    // valid keys of this 32-key chunk as a bit mask: the first nkm, minus the padding
+                    // keys of the cached prefix [kv_valid0, kv_rows0) (one loop, one bit test per key)
+                    const int kc = key0 + kh * 64 + side * 32;
+                    const int plo = min(32, max(0, p.kv_valid0 - kc)), phi = min(32, max(0, p.kv_rows0 - kc));
+                    const uint32_t vmask = (nkm >= 32 ? 0xffffffffu : (1u << nkm) - 1u) &
+                                           ~((phi >= 32 ? 0xffffffffu : (1u << phi) - 1u) & ~((1u << plo) - 1u));
                     float mx = -INFINITY;
-                    if (nkm == 32 && (pad_lo >= 32 || pad_hi <= 0)) {  // no masked key in this chunk
 #pragma unroll
-                        for (int e = 0; e < 32; ++e) {
-                            sv[e] *= p.scale_log2;
-                            mx = fmaxf(mx, sv[e]);
-                        }
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) {
-                            sv[e] = e < nkm && (e < pad_lo || e >= pad_hi) ? sv[e] * p.scale_log2 : -INFINITY;
-                            mx = fmaxf(mx, sv[e]);
-                        }
+                    for (int e = 0; e < 32; ++e) {
+                        sv[e] = (vmask >> e) & 1u ? sv[e] * p.scale_log2 : -INFINITY;
+                        mx = fmaxf(mx, sv[e]);
                     }
                     xch[part * 64 + R] = mx;
                     named_bar_sync(1, kWorkers);
