@@ -1166,11 +1166,15 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         tmem_ld32(ts + 32, *reinterpret_cast<float(*)[32]>(sv + 32));
                     }
                     const int nkm = mine && act ? nk - side * 64 : 0;  // valid keys of this thread's block
-                    const int kc = key0 + side * 64, pad_lo = p.kv_valid0 - kc, pad_hi = p.kv_rows0 - kc;  // padding keys
+                    // valid-key bitmask: keys below nkm minus the padding keys [kv_valid0, kv_rows0)
+                    const int kc = key0 + side * 64;
+                    const int plo = min(64, max(0, p.kv_valid0 - kc)), phi = min(64, max(0, p.kv_rows0 - kc));
+                    const auto lowbits = [](int n) { return n >= 64 ? ~0ull : (1ull << n) - 1ull; };
+                    const uint64_t vmask = lowbits(nkm) & ~(lowbits(phi) & ~lowbits(plo));
                     float mx = -INFINITY;
 #pragma unroll
                     for (int e = 0; e < 64; ++e) {
-                        sv[e] = e < nkm && (e < pad_lo || e >= pad_hi) ? sv[e] * p.scale_log2 : -INFINITY;
+                        sv[e] = (vmask >> e) & 1ull ? sv[e] * p.scale_log2 : -INFINITY;
                         mx = fmaxf(mx, sv[e]);
                     }
                     xch[side * 128 + R] = mx;
