@@ -30,6 +30,7 @@ enum GemmFlags : int {
     kFlagRope = 8,      // rotate pairs (j, j+128) of every 256-wide head in cols < rope_cols
     kFlagRopePacked = 16,  // bn = 128 over kPermRope-packed weights: a tile = 64 columns of one head
                            // followed by their 64 RoPE partners (written back to j and j + 128)
+    kFlagWarmEpi = 32,     // set by launch_gemm: run the epilogue once "dry" during the mainloop
 };
 
 struct GemmParams {

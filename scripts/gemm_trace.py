@@ -18,7 +18,8 @@ from paper_2510_26742_b200.inputs import gen_inputs  # noqa: E402
 
 views = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 nodes = sys.argv[2:] or ["ve.qkv", "ve.proj", "ve.fc1", "ve.fc2", "llm.qkv", "llm.proj", "llm.down", "llm.ffn"]
-STAMPS = ["start", "setup", "pdl(tma)", "full0(mma)", "acc_full", "parked", "cl_sync", "epi_end", "cl_sync2", "exit"]
+STAMPS = ["start", "setup", "pdl(tma)", "full0(mma)", "acc_full", "parked", "cl_sync", "epi_end", "cl_sync2", "exit",
+          "acc32#0", "chunk0", "loop_end"]
 cfg = default_config(views=views)
 eng = E.Engine(cfg, use_cuda_graph=False)
 eng.gen_weights(1)
