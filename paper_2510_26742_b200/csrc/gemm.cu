@@ -248,7 +248,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int stage_off = S > 1 ? S * NCH * 16384 : 0;
     const bool staged = !kPaired && !persist && MT == 1 && CG == 1 && (S == 1 || push) &&
                         stage_off + NCH * 16384 <= STAGES * Cfg::STAGE_BYTES &&
-                        MODE == kModeResid;  // (bf16-output tiles measured slower staged: 8.3 -> 8.8 us ve.qkv)
+                        MODE == kModeResid;
+    // bf16-output tiles (ve.qkv, ve.fc1): staged as bf16 in the drained pipeline smem, then written
+    // as whole rows (a warp = 2 rows x 256 B at bn 128): per-thread row pieces (32 rows per warp
+    // store) cost ~2 us per 32 KB tile inside the GEMM, a third of a small GEMM's time.
+    constexpr int PR = BN / 8;                       // 16-byte pieces per staged bf16 row
+    constexpr int PSW = PR < 16 ? PR - 1 : 15;       // piece swizzle mask (by row)
+    const bool staged16 = MODE == kModeBf16 && !kPaired && !persist && MT == 1 && CG == 1 && S == 1 &&
+                          (p.flags & kFlagStageBf16) && 128 * PR * 16 <= STAGES * Cfg::STAGE_BYTES;
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
@@ -631,6 +638,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         store_bf16x32(reinterpret_cast<__nv_bfloat16*>(p.outb) + (long long)r * p.ldob + col0, v, nv);
                 } else if (staged) {
                     stage32(c, v);
+                } else if (staged16) {
+                    const uint32_t srow16 = smem_u32(smem) + row_in_tile * (PR * 16);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int pc = c * 4 + q;
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(srow16 + ((pc ^ (row_in_tile & PSW)) << 4)),
+                                     "r"(pack_bf16(v[8 * q], v[8 * q + 1])), "r"(pack_bf16(v[8 * q + 2], v[8 * q + 3])),
+                                     "r"(pack_bf16(v[8 * q + 4], v[8 * q + 5])), "r"(pack_bf16(v[8 * q + 6], v[8 * q + 7]))
+                                     : "memory");
+                    }
                 } else {
                     store_bf16x32(reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)r * p.ldo + col0, v, nv);
                 }
@@ -652,6 +669,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         s0 += x * x;
                     }
                     if (p.out_stats) atomicAdd(p.out_stats - 1, s0);
+                }
+            }
+        }
+        if (staged16) {
+            named_bar_sync(1, 256);
+            __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(p.out);
+#pragma unroll 2
+            for (int e = etid; e < 128 * PR; e += 256) {
+                const int row = e / PR, pc = e % PR;
+                const int gr = m_tile * BM + row, col = n0 + pc * 8;
+                if (gr >= p.M || col >= p.N || dry) continue;
+                const uint4 u = *reinterpret_cast<const uint4*>(smem + row * (PR * 16) + ((pc ^ (row & PSW)) << 4));
+                if (col + 8 <= p.N) {
+                    *reinterpret_cast<uint4*>(ob + (long long)gr * p.ldo + col) = u;
+                } else {
+                    const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&u);
+                    for (int k = 0; k < 8 && col + k < p.N; ++k) ob[(long long)gr * p.ldo + col + k] = hv[k];
                 }
             }
         }
@@ -840,6 +874,8 @@ cudaError_t launch_gemm(int bn, const CUtensorMap& ta, const CUtensorMap& tb, co
     static const int warm = [] { const char* e = getenv("PI0B_GEMM_WARM"); return e ? atoi(e) : 1; }();
     GemmParams q = p;
     if (warm) q.flags |= kFlagWarmEpi;
+    static const int stage16 = [] { const char* e = getenv("PI0B_GEMM_STAGE_BF16"); return e ? atoi(e) : 1; }();
+    if (stage16) q.flags |= kFlagStageBf16;
     if (mt > 1 && (mt != 2 || bn != 256 || p.splits != 1)) return cudaErrorInvalidValue;
     if (cg > 1 && (cg != 2 || mt != 1 || bn != 256 || p.splits != 1)) return cudaErrorInvalidValue;
     dim3 grid((p.M + mt * cg * BM - 1) / (mt * cg * BM), (p.N + bn - 1) / bn, p.splits);

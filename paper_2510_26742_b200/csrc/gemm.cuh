@@ -31,6 +31,7 @@ enum GemmFlags : int {
     kFlagRopePacked = 16,  // bn = 128 over kPermRope-packed weights: a tile = 64 columns of one head
                            // followed by their 64 RoPE partners (written back to j and j + 128)
     kFlagWarmEpi = 32,     // set by launch_gemm: run the epilogue once "dry" during the mainloop
+    kFlagStageBf16 = 64,   // set by launch_gemm: bf16 tiles staged in smem, written as whole rows
 };
 
 struct GemmParams {

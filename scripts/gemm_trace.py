@@ -8,7 +8,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["PI0B_LIB"] = os.path.join(ROOT, "variants", "libpi0b_gmtrace.so")
+os.environ["PI0B_LIB"] = os.environ.get("GM_LIB", os.path.join(ROOT, "variants", "libpi0b_gmtrace.so"))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
