@@ -313,6 +313,7 @@ public:
             std::lock_guard<std::mutex> lk(m_);
             stop_ = true;
             ++gen_;
+            gen_seen_.store(gen_, std::memory_order_release);
         }
         cv_.notify_all();
         for (auto& t : th_) t.join();
@@ -342,6 +343,7 @@ public:
         {
             std::lock_guard<std::mutex> lk(m_);
             ++gen_;
+            gen_seen_.store(gen_, std::memory_order_release);
         }
         cv_.notify_all();
         size_t issued = 0;
@@ -371,6 +373,14 @@ private:
         unsigned long long seen = 0;
         acks_.fetch_add(1, std::memory_order_release);  // idle
         for (;;) {
+            // Optional spin before sleeping (PI0B_STAGING_SPIN_US): a condition-variable wake-up
+            // costs tens of microseconds, which a back-to-back serving loop pays on every call.
+            if (spin_us_ > 0) {
+                const auto t0 = std::chrono::steady_clock::now();
+                while (gen_seen_.load(std::memory_order_acquire) == seen &&
+                       std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(spin_us_))
+                    std::this_thread::yield();
+            }
             {
                 std::unique_lock<std::mutex> lk(m_);
                 cv_.wait(lk, [&] { return gen_ != seen; });
@@ -392,6 +402,8 @@ private:
     bool stop_ = false;
     std::atomic<size_t> next_{0};
     std::atomic<int> acks_{0};
+    std::atomic<unsigned long long> gen_seen_{0};  // gen_, readable without the mutex (spinning helpers)
+    const long spin_us_ = [] { const char* e = std::getenv("PI0B_STAGING_SPIN_US"); return e ? std::atol(e) : 0L; }();
     std::unique_ptr<std::atomic<uint8_t>[]> done_;
     size_t cap_ = 0;
     std::function<void(size_t)> work_;

@@ -115,37 +115,15 @@ for r in mid:
         for role in sorted(set(int(v) for v in pr if v > 0)):
             nm = {1: "owner", 2: "helper", 3: "ffn-a", 4: "ffn-b", 5: "qkv-a", 6: "qkv-b"}.get(role, str(role))
             s8 = st[idx[pr == role]].astype(np.float64)
-            rel = lambda c: (s8[:, c] - prev_end) / 1e3
-            q = lambda v: "%6.2f/%6.2f/%6.2f" % (np.min(v), np.median(v), np.max(v))
+            rel = lambda c: np.where(s8[:, c] > 0, (s8[:, c] - prev_end) / 1e3, np.nan) if len(s8) else np.zeros(0)
+
+            def q(v):
+                v = v[np.isfinite(v)]
+                return "%6.2f/%6.2f/%6.2f" % (np.min(v), np.median(v), np.max(v)) if len(v) else "     -"
             print(f"  {r[1]:6s} {nm:6s} ready {q(rel(1))} staged {q(rel(2))} acc {q(rel(7))} acc_seen {q(rel(8))} "
                   f"epi_done {q(rel(9))} pub {q(rel(3))}")
             if role == 2:
                 print(f"  {'':13s} ready_ok {q(rel(10))} stores {q(rel(11))} bar {q(rel(12))} fence {q(rel(13))}")
-    prev_end = r[5]
-
-# finaliser anatomy of one mid layer: the tile's last split (finaliser) per split-K phase
-print("\nfinalisers of the mid layer (us relative to the previous phase's last publish):")
-prev_end = 0
-for r in rows:
-    if r[0] == mid[0][0] - 1:
-        prev_end = r[5]
-for r in mid:
-    idx = np.array(ph[r[0]])
-    if tasks["kind"][idx[0]] != 1 or True:
-        prev_end = r[5]
-        continue
-    s8 = st[idx].astype(np.float64)
-    fin = s8[:, 13] > 0
-    if fin.any():
-        f = s8[fin]
-        rel = lambda v: (v - prev_end) / 1e3
-        def q(v):
-            return "%6.2f/%6.2f/%6.2f" % (np.min(v), np.median(v), np.max(v))
-        print(f"  {r[1]:8s} fin={fin.sum():3d} epi_done {q(rel(f[:, 9]))} tile_atomic {q(rel(f[:, 11]))} loaded {q(rel(f[:, 12]))} "
-              f"stored {q(rel(f[:, 13]))} pub {q(rel(f[:, 3]))}")
-        nf = s8[~fin]
-        if len(nf):
-            print(f"  {'':8s} non-fin={len(nf):3d} epi_done {q(rel(nf[:, 9]))} tile_atomic {q(rel(nf[:, 11]))} pub {q(rel(nf[:, 3]))}")
     prev_end = r[5]
 
 if os.environ.get("AE_TRACE_RAW"):
