@@ -24,6 +24,7 @@
 // (the bulk engine's per-request cost, ~0.25 us, is amortised over 16 KB).  No task finalises
 // another's output (aemk.cuh): a phase is complete when all of its tasks have signalled.
 #include "aemk.cuh"
+#include "ktrace.cuh"
 #include "ptx.cuh"
 
 #include <algorithm>
@@ -226,6 +227,8 @@ PI0B_DEV int swz(int row, int chunk) { return row * 128 + ((chunk ^ (row & 7)) <
 }  // namespace
 
 __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
+    KT_SMEM;
+    KT_START();
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -1254,6 +1257,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
     tc_fence_before();
     __syncthreads();
     cluster_sync_all();  // no CTA leaves while its partner may still touch its shared memory
+    KT_END(3ull << 62);
     if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
@@ -1573,5 +1577,7 @@ AePlan ae_plan(const AePlanInput& in) {
     out.min_load = *std::min_element(load.begin(), load.end());
     return out;
 }
+
+KT_SETTER(ktrace_set_aemk)
 
 }  // namespace pi0b

@@ -193,3 +193,15 @@ uint64_t pi0b_seed_hash(uint64_t seed, const char* label, uint64_t a, uint64_t b
 }
 
 }  // extern "C"
+
+#ifdef PI0B_KTRACE
+// Whole-graph timeline (variant builds only; ktrace.cuh, scripts/graph_timeline.py).
+namespace pi0b {
+int ktrace_set_gemm(unsigned long long*);
+int ktrace_set_fattn(unsigned long long*);
+int ktrace_set_aemk(unsigned long long*);
+}  // namespace pi0b
+extern "C" int pi0b_ktrace_buffer(unsigned long long* p) {
+    return pi0b::ktrace_set_gemm(p) | pi0b::ktrace_set_fattn(p) | pi0b::ktrace_set_aemk(p);
+}
+#endif

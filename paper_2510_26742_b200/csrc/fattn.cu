@@ -23,6 +23,7 @@
 // K ring with st.async (complete_tx on its receive barrier), and it combines them.
 // The output tile is staged in shared memory and written with coalesced 16-byte stores.
 #include "attention.cuh"
+#include "ktrace.cuh"
 #include "ptx.cuh"
 
 #include <math.h>
@@ -141,6 +142,8 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_full + 1);
 
     const int tid = threadIdx.x, warp = __shfl_sync(0xffffffff, tid >> 5, 0), lane = tid & 31;
+    KT_SMEM;
+    KT_START();
     if (tid == 0) FA_STAMP(0);
     const int qt = blockIdx.x, grp = blockIdx.z;
     const int hpg = p.heads / p.kv_heads;
@@ -191,6 +194,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
             pdl_wait();  // Q, K, V are the previous kernel's outputs
+            KT_DEP();
             FA_STAMP(1);
             // Q: 32-row boxes (q_rows % 32 == 0, so a box never straddles two stacked heads)
             int qbytes = 0;
@@ -576,6 +580,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
     if (S > 1 && warp >= 8) cluster_sync_all();
     __syncthreads();
     if (tid == 0) FA_STAMP(9);
+    KT_END((2ull << 62) | (static_cast<unsigned long long>(D) << 40) | (reinterpret_cast<uintptr_t>(p.out) >> 4 & 0xffffff));
     if (warp == 8) tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
@@ -669,5 +674,7 @@ cudaError_t launch_fattn(int head_dim, const FaMaps& maps, const AttnParams& p, 
         default: return cudaErrorInvalidValue;
     }
 }
+
+KT_SETTER(ktrace_set_fattn)
 
 }  // namespace pi0b

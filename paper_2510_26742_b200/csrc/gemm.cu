@@ -19,6 +19,7 @@
 // PDL: the next launch's prologue and first weight tiles overlap this kernel's tail
 // (griddepcontrol.wait guards every read of the previous kernel's outputs).
 #include "gemm.cuh"
+#include "ktrace.cuh"
 #include "ptx.cuh"
 
 #include <algorithm>
@@ -164,6 +165,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
     const int warp = __shfl_sync(0xffffffff, int(threadIdx.x >> 5), 0);  // warp-uniform (see below)
     const int lane = threadIdx.x & 31;
+    KT_SMEM;
+    KT_START();
     if (threadIdx.x == 0) GM_STAMP(0);
     // Persistent mode (p.persist, no split-K): CTA b walks tiles b, b + grid, ... (m fastest, so
     // CTAs running together share weight tiles in L2) with the accumulator double-buffered in
@@ -300,6 +303,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         load_b(i, (kb0 + i) * BK);
                     }
                     pdl_wait();
+                    KT_DEP();
                     GM_STAMP(2);
                     for (int i = 0; i < pre; ++i) load_a(i, (kb0 + i) * BK);
                     i0 = pre;
@@ -754,6 +758,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         __syncthreads();
         if (warp == 1) tmem_dealloc(tmem, tmem_cols);
     }
+    KT_END((1ull << 62) | (static_cast<unsigned long long>(p.N & 0xffff) << 40) |
+           (static_cast<unsigned long long>(p.K & 0xffff) << 24) |
+           ((reinterpret_cast<uintptr_t>(p.out_stats) ^ reinterpret_cast<uintptr_t>(p.row_stats) ^
+             reinterpret_cast<uintptr_t>(p.out)) >> 4 & 0xffffff));
     if (threadIdx.x == 0) GM_STAMP(9);
 }
 
@@ -832,6 +840,7 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const
 }
 
 void gemm_set_pdl(bool on) { g_gemm_pdl = on; }
+KT_SETTER(ktrace_set_gemm)
 
 // How many clusters of `splits` CTAs of this GEMM configuration fit on the device at once
 // (clusters are confined to a GPC, so this is below num_sms / splits).
