@@ -971,12 +971,10 @@ void Engine::add_attn(int part, const std::string& node, int inst, int hd, AttnP
         for (char& ch : key) ch = ch == '.' ? '_' : char(std::toupper(static_cast<unsigned char>(ch)));
         const int base = ((ap.heads / ap.kv_heads) * ap.q_rows + 127) / 128 * ap.kv_heads;
         const int tiles = (ap.rows0 + ap.rows1 + 63) / 64;
-        // measured (scripts/fa_trace.py, 2 views): the split combine (DSMEM) costs more than the
-        // key tiles it saves -- ve.attn 10.5 us at S = 1 vs 11.0 at S = 2, llm.attn 13.6 vs 14.6 /
-        // 14.9 at S = 2 / 4 -- so one CTA per q tile unless PI0B_ATTN_SPLITS says otherwise
-        int S = 1;
-        (void)base;
-        (void)tiles;
+        // Measured in graph replays (scripts/ab_env.sh, 2 views): d 256 (llm.attn, 32 q tiles) at
+        // S = 4 saves ~5 us per inference (S = 2: +14 us); d 72 (ve.attn) is best unsplit.  S = 4 only
+        // when the split grid fits one wave and every split keeps two 64-key tiles.
+        int S = node == "llm.attn" && base * 4 <= num_sms_ && tiles >= 8 ? 4 : 1;
         S = env_int(("PI0B_ATTN_SPLITS_" + key).c_str(), env_int("PI0B_ATTN_SPLITS", S));
         ap.kv_splits = (S == 2 || S == 4 || S == 8) ? S : 1;
     }
@@ -1096,7 +1094,9 @@ void Engine::build_plan() {
             g.outb = ve_hb_ + size_t(r0) * ve_w_;
             g.ldob = ve_w_;
             g.out_stats = st2 + r0;
-            add_gemm(0, "ve.proj", i, ve_attn_ + size_t(r0) * ve_w_, ve_w_, Tg, Wv["ve.proj"], i, 64, g);
+            // unsplit (72 CTAs at 2 views): the split-K exchange costs more than the 18 k-blocks it
+            // halves (graph replay -8 us against 2-way split-K, scripts/ab_env.sh)
+            add_gemm(0, "ve.proj", i, ve_attn_ + size_t(r0) * ve_w_, ve_w_, Tg, Wv["ve.proj"], i, 64, g, false);
             tag("ve.proj", i, ve_h_, T_, ve_w_, ve_w_, 0);
         }
         {   // ve.ln2 + ve.fc1: gelu((p W) * rms(p) + b)
