@@ -36,7 +36,6 @@ namespace {
 
 constexpr int kFaRows = 128;
 constexpr int kFaKeys = 64;
-constexpr int kFaThreads = 320;  // 8 softmax warps, MMA warp, TMA warp
 
 PI0B_DEV uint64_t desc_kmajor(uint32_t saddr) {
     uint64_t d = 0;
@@ -96,9 +95,16 @@ extern "C" int pi0b_fa_trace_buffer(unsigned long long* p) {
 #endif
 
 // D = real head dim, DK = QK contraction (D padded to 16), DV = PV width (D padded to 64),
-// KK / KV = key / value ring depths.
-template <int D, int DK, int DV, int KK, int KV, int KEYS>
+// KK / KV = key / value ring depths, NQ = softmax threads per query row (each takes KEYS / NQ keys
+// of a tile and DV / NQ output columns; 4 x 32 NQ softmax warps, then the MMA and TMA warps).
+template <int D, int DK, int DV, int KK, int KV, int KEYS, int NQ>
 struct FaCfg {
+    static constexpr int SOFT = 128 * NQ;           // softmax / epilogue threads
+    static constexpr int THREADS = SOFT + 64;
+    static constexpr int MMA_WARP = SOFT / 32, TMA_WARP = MMA_WARP + 1;
+    // row-max / row-sum exchange between a row's NQ threads: double-buffered by tile parity at
+    // NQ = 2; NQ = 4 single-buffered (shared memory is full) with a second barrier per exchange
+    static constexpr int XBUF = NQ == 2 ? 2 : 1;
     static constexpr int QA = (DK + 63) / 64;  // 64-col regions of Q / K
     static constexpr int VA = DV / 64;         // 64-col regions of V
     static constexpr int Q_BYTES = QA * kFaRows * 128;
@@ -106,7 +112,7 @@ struct FaCfg {
     static constexpr int V_BYTES = VA * KEYS * 128;
     static constexpr int PR = KEYS / 64;                // 64-key regions of a P buffer
     static constexpr int P_BYTES = PR * kFaRows * 128;  // one P buffer; two are allocated
-    static constexpr int XCH_BYTES = 2 * 2 * kFaRows * 4;  // [2 tiles][2 halves][128 rows] row maxima
+    static constexpr int XCH_BYTES = XBUF * NQ * kFaRows * 4;  // [XBUF][NQ parts][128 rows]
     static constexpr int SMEM = Q_BYTES + KK * K_BYTES + KV * V_BYTES + 2 * P_BYTES + XCH_BYTES + 256;
     static constexpr int TMEM_S = 0;  // two KEYS-column S buffers
     static constexpr int TMEM_O = 2 * KEYS;
@@ -115,17 +121,18 @@ struct FaCfg {
     static_assert(KEYS == 64 || KEYS == 128, "key tile");
     static constexpr int ROW_BYTES = DV * 2;  // staged bf16 output row
     static_assert(Q_BYTES >= kFaRows * ROW_BYTES, "output staging fits the Q region");
+    static_assert((NQ == 2 || NQ == 4) && (DV / NQ) % 32 == 0 && (KEYS / NQ) % 8 == 0, "softmax split");
 };
 
-template <int D, int DK, int DV, int KK, int KV, int KEYS>
-__global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_constant__ FaMaps maps, const AttnParams p) {
-    using C = FaCfg<D, DK, DV, KK, KV, KEYS>;
+template <int D, int DK, int DV, int KK, int KV, int KEYS, int NQ>
+__global__ void __launch_bounds__(128 * NQ + 64, 1) fattn_kernel(const __grid_constant__ FaMaps maps, const AttnParams p) {
+    using C = FaCfg<D, DK, DV, KK, KV, KEYS, NQ>;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sQ = smem;
     uint8_t* sK = sQ + C::Q_BYTES;
     uint8_t* sV = sK + KK * C::K_BYTES;
     uint8_t* sP = sV + KV * C::V_BYTES;
-    float* xch = reinterpret_cast<float*>(sP + 2 * C::P_BYTES);  // [2][2][128]
+    float* xch = reinterpret_cast<float*>(sP + 2 * C::P_BYTES);  // [XBUF][NQ][128]
     uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES + C::XCH_BYTES);
     uint64_t* k_full = bars;            // [KK]
     uint64_t* k_empty = k_full + KK;    // [KK]
@@ -172,8 +179,8 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&s_full[s], 1);
-            mbar_init(&s_free[s], 256);
-            mbar_init(&p_full[s], 256);
+            mbar_init(&s_free[s], C::SOFT);
+            mbar_init(&p_full[s], C::SOFT);
             mbar_init(&o_done[s], 1);
         }
         mbar_init(q_full, 1);
@@ -182,7 +189,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
         mbar_init(recv_full, 1);
         fence_barrier_init();
     }
-    if (warp == 8) tmem_alloc(tmem_slot, C::TMEM_COLS);
+    if (warp == C::MMA_WARP) tmem_alloc(tmem_slot, C::TMEM_COLS);
     if (tid == 0) pdl_launch_dependents();
     tc_fence_before();
     __syncthreads();  // (key splits touch no peer barrier or shared memory: one cluster barrier in the combine)
@@ -190,7 +197,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
     const uint32_t tmem = *tmem_slot;
     if (tid == 0) FA_STAMP(2);
 
-    if (warp == 9) {
+    if (warp == C::TMA_WARP) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
             pdl_wait();  // Q, K, V are the previous kernel's outputs
@@ -242,7 +249,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             }
         }
         __syncwarp();
-    } else if (warp == 8) {
+    } else if (warp == C::MMA_WARP) {
         // ------------------------------------------------------------ MMA issuer
         {  // warp-uniform loop; one elected lane issues (see gemm.cu)
             constexpr uint32_t idesc_qk = umma_idesc_bf16(kFaRows, KEYS);
@@ -290,12 +297,12 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
         __syncwarp();
     } else {
         // ------------------------------------------------------------ softmax + epilogue
-        const int qd = warp & 3, hf = warp >> 2;  // TMEM lane quarter, key / O-column half
+        const int qd = warp & 3, hf = warp >> 2;  // TMEM lane quarter; key / O-column part (of NQ)
         const int r = qd * 32 + lane;
         const int g = qt * kFaRows + r;
         const bool row_ok = g < grows;
         const uint32_t trow = tmem + (uint32_t(qd * 32) << 16);
-        const uint32_t pair_bar = 1 + qd;  // named barrier of warps qd and qd + 4 (64 threads)
+        const uint32_t pair_bar = 1 + qd;  // named barrier of the row's NQ warps qd, qd + 4, ..
         mbar_wait(q_full, 0);  // (also orders every thread after the producer's pdl_wait)
         if (hf == 0) {
             // Q columns D..DK of the last region belong to the next head (or are OOB zeros): clear
@@ -315,7 +322,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             mbar_wait(&s_full[sb], (t >> 1) & 1);
             if (tid == 0 && t == 0) FA_STAMP(3);
             tc_fence_after();
-            constexpr int KH = KEYS / 2;  // keys of this thread's half of the tile
+            constexpr int KH = KEYS / NQ;  // keys of this thread's part of the tile
             float sv[KH];
 #pragma unroll
             for (int i = 0; i < KH / 32; ++i)
@@ -340,10 +347,13 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                     mx = fmaxf(mx, sv[j]);
                 }
             }
-            // row max over both key halves (the partner thread is in warp w ^ 4)
-            xch[(sb * 2 + hf) * kFaRows + r] = mx;
-            named_bar_sync(pair_bar, 64);
-            mx = fmaxf(xch[(sb * 2) * kFaRows + r], xch[(sb * 2 + 1) * kFaRows + r]);
+            // row max over the NQ key parts (the row's other threads are in warps w +- 4 ..)
+            const int xb0 = C::XBUF == 2 ? sb * NQ : 0;
+            xch[(xb0 + hf) * kFaRows + r] = mx;
+            named_bar_sync(pair_bar, NQ * 32);
+#pragma unroll
+            for (int h = 0; h < NQ; ++h) mx = fmaxf(mx, xch[(xb0 + h) * kFaRows + r]);
+            if (C::XBUF == 1) named_bar_sync(pair_bar, NQ * 32);  // all read before the next write
             // P is double-buffered: buffer t & 1 is free once PV(t - 2) is done; O may only be
             // rescaled once PV(t - 1) is done (rare: lazy rescale).  Both threads of a row make
             // the same decisions (same maxima).
@@ -363,12 +373,12 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             }
             if (rescale) {
 #pragma unroll 1
-                for (int c = 0; c < DV / 64; ++c) {
+                for (int c = 0; c < DV / (32 * NQ); ++c) {
                     float o[32];
-                    tmem_ld32(trow + C::TMEM_O + hf * (DV / 2) + c * 32, o);
+                    tmem_ld32(trow + C::TMEM_O + hf * (DV / NQ) + c * 32, o);
 #pragma unroll
                     for (int j = 0; j < 32; ++j) o[j] *= factor;
-                    tmem_st32(trow + C::TMEM_O + hf * (DV / 2) + c * 32, o);
+                    tmem_st32(trow + C::TMEM_O + hf * (DV / NQ) + c * 32, o);
                 }
             }
             float ls = 0.f;
@@ -393,19 +403,22 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             mbar_arrive(&p_full[sb]);
         }
         if (tid == 0) FA_STAMP(4);
-        // row sum over both halves (exchange slot of a tile two back: free, see the max exchange)
+        // row sum over the NQ parts (XBUF 2: the slot of a tile two back is free, see the max
+        // exchange; XBUF 1: the last max exchange ended with a barrier)
         {
-            const int xb = ntiles & 1;
-            xch[(xb * 2 + hf) * kFaRows + r] = l;
-            named_bar_sync(pair_bar, 64);
-            l = xch[(xb * 2) * kFaRows + r] + xch[(xb * 2 + 1) * kFaRows + r];
+            const int xb0 = C::XBUF == 2 ? (ntiles & 1) * NQ : 0;
+            xch[(xb0 + hf) * kFaRows + r] = l;
+            named_bar_sync(pair_bar, NQ * 32);
+            l = 0.f;
+#pragma unroll
+            for (int h = 0; h < NQ; ++h) l += xch[(xb0 + h) * kFaRows + r];
         }
         if (ntiles > 0) mbar_wait(&o_done[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
         tc_fence_after();
         if (tid == 0) FA_STAMP(5);
-        // This thread's output columns: [hf * DV / 2, (hf + 1) * DV / 2) of row r, as 16-byte
+        // This thread's output columns: [hf * DV / NQ, (hf + 1) * DV / NQ) of row r, as 16-byte
         // chunks q of the staged row (bf16, row r at r * ROW_BYTES, chunk q at (q ^ (r & 7))).
-        constexpr int HC = DV / 2 / 8;  // chunks per half row
+        constexpr int HC = DV / NQ / 8;  // chunks per row part
         auto stage_row = [&](int row, const float* o, int c32, float scale) {
             uint8_t* srow = sQ + row * C::ROW_BYTES;
 #pragma unroll
@@ -420,9 +433,9 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
         if (S == 1) {
             const float il = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll 1
-            for (int c = 0; c < DV / 64; ++c) {
+            for (int c = 0; c < DV / (32 * NQ); ++c) {
                 float o[32];
-                if (ntiles > 0) tmem_ld32(trow + C::TMEM_O + hf * (DV / 2) + c * 32, o);
+                if (ntiles > 0) tmem_ld32(trow + C::TMEM_O + hf * (DV / NQ) + c * 32, o);
                 else
 #pragma unroll
                     for (int j = 0; j < 32; ++j) o[j] = 0.f;
@@ -451,9 +464,9 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             uint8_t* ob = owner != y ? sV + slot_of(owner, y) * blk                              // outgoing
                                      : sQ + (row_lo < kFaRows / 2 ? kFaRows / 2 : 0) * C::ROW_BYTES;  // own
 #pragma unroll 1
-            for (int c = 0; c < DV / 64; ++c) {
+            for (int c = 0; c < DV / (32 * NQ); ++c) {
                 float o[32];
-                if (ntiles > 0) tmem_ld32(trow + C::TMEM_O + hf * (DV / 2) + c * 32, o);
+                if (ntiles > 0) tmem_ld32(trow + C::TMEM_O + hf * (DV / NQ) + c * 32, o);
                 else
 #pragma unroll
                     for (int j = 0; j < 32; ++j) o[j] = 0.f;  // a split without keys never reads TMEM
@@ -468,14 +481,14 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             if (hf == 0)  // (max, sum) of every row: into the outgoing block, or for own rows into sP + 2 KB
                 (owner != y ? reinterpret_cast<float2*>(ob + own_rows * C::ROW_BYTES) : reinterpret_cast<float2*>(sP + 2048))[lrow] =
                     make_float2(l > 0.f ? m_ref : -INFINITY, l);
-            named_bar_sync(6, 256);
+            named_bar_sync(6, C::SOFT);
             if (tid == 0) FA_STAMP(14);
             // outgoing blocks -> workspace [tile][sender][owner]
             for (int k = 0; k < S; ++k) {
                 if (k == y) continue;
                 const uint4* src = reinterpret_cast<const uint4*>(sV + slot_of(k, y) * blk);
                 uint4* dst = reinterpret_cast<uint4*>(wsb + size_t(y * S + k) * blk);
-                for (int e = tid; e < blk / 16; e += 256) dst[e] = src[e];
+                for (int e = tid; e < blk / 16; e += C::SOFT) dst[e] = src[e];
             }
             if (tid == 0) FA_STAMP(7);
             cluster_sync_all();  // (warps 8 and 9 arrive at the end of their roles)
@@ -485,18 +498,18 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
                 if (k == y) continue;
                 const uint8_t* src = wsb + size_t(k * S + y) * blk;
                 uint8_t* dst = sK + slot_of(k, y) * blk;
-                for (int e = tid; e < blk / 16; e += 256) cp_async16(dst + e * 16, src + e * 16, true);
+                for (int e = tid; e < blk / 16; e += C::SOFT) cp_async16(dst + e * 16, src + e * 16, true);
             }
             cp_async_commit();
             cp_async_wait<0>();
-            named_bar_sync(6, 256);
+            named_bar_sync(6, C::SOFT);
             // o = sum_j w_j O_j / sum_j w_j over the S normalised partials, w_j = l_j 2^(m_j - M),
-            // spread over all 256 threads (own_rows rows x DV columns; a per-row-thread combine
-            // leaves the work to the two warps of one sub-partition)
-            {
-                constexpr int DVC = DV / 8;                 // 16-byte chunks per row
-                const int segs = 256 / own_rows;             // threads per row
-                const int cps = DVC / segs;                  // chunks per thread (>= 1: own_rows >= 16)
+            // spread over all softmax threads (own_rows rows x DV columns; a per-row-thread combine
+            // leaves the work to the warps of one sub-partition)
+            if (tid < own_rows * min(C::SOFT / own_rows, DV / 8)) {
+                constexpr int DVC = DV / 8;                       // 16-byte chunks per row
+                const int segs = min(C::SOFT / own_rows, DVC);    // threads per row
+                const int cps = DVC / segs;                       // chunks per thread
                 const int lr = tid / segs, c0 = (tid % segs) * cps;
                 const float2* ml_own = reinterpret_cast<const float2*>(sP + 2048);
                 auto ml_of = [&](int k) {
@@ -551,11 +564,11 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             rowptr[tid] = gg < grows ? p.out + (long long)(gg % p.q_rows) * p.ldo + (kvh + p.kv_heads * (gg / p.q_rows)) * D
                                      : nullptr;
         }
-        named_bar_sync(5, 256);
+        named_bar_sync(5, C::SOFT);
         if (tid == 0) FA_STAMP(12);
         constexpr int CPR = (D * 2 + 15) / 16;  // 16-byte chunks per output row
         if constexpr (CPR == 32) {  // D = 256: one row per warp and iteration, lane = chunk
-            for (int rr = row_lo + warp; rr < row_hi; rr += 8) {
+            for (int rr = row_lo + warp; rr < row_hi; rr += C::SOFT / 32) {
                 __nv_bfloat16* orow = rowptr[rr];
                 if (!orow) continue;
                 const uint4 v = *reinterpret_cast<const uint4*>(sQ + rr * C::ROW_BYTES + ((lane ^ (rr & 7)) << 4));
@@ -563,7 +576,7 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
             }
         } else {
             const int n = (row_hi - row_lo) * CPR;
-            for (int e = tid; e < n; e += 256) {
+            for (int e = tid; e < n; e += C::SOFT) {
                 const int rr = row_lo + e / CPR, q = e - (e / CPR) * CPR;
                 __nv_bfloat16* orow = rowptr[rr];
                 if (!orow) continue;
@@ -577,27 +590,28 @@ __global__ void __launch_bounds__(kFaThreads, 1) fattn_kernel(const __grid_const
     // Key splits: the MMA and TMA warps take part in the softmax warps' cluster barrier (the
     // workspace exchange above); nothing crosses CTAs after it.
     tc_fence_before();
-    if (S > 1 && warp >= 8) cluster_sync_all();
+    if (S > 1 && warp >= C::MMA_WARP) cluster_sync_all();
     __syncthreads();
     if (tid == 0) FA_STAMP(9);
     KT_END((2ull << 62) | (static_cast<unsigned long long>(D) << 40) | (reinterpret_cast<uintptr_t>(p.out) >> 4 & 0xffffff));
-    if (warp == 8) tmem_dealloc(tmem, C::TMEM_COLS);
+    if (warp == C::MMA_WARP) tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
 CUtensorMap make_tmap_bf16(const void* base, long long rows, long long cols, long long ld, int box_rows);
 
 namespace {
-template <int D, int DK, int DV, int KK, int KV, int KEYS>
+template <int D, int DK, int DV, int KK, int KV, int KEYS, int NQ>
 cudaError_t fa_configure_t() {
-    return cudaFuncSetAttribute(fattn_kernel<D, DK, DV, KK, KV, KEYS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                FaCfg<D, DK, DV, KK, KV, KEYS>::SMEM);
+    return cudaFuncSetAttribute(fattn_kernel<D, DK, DV, KK, KV, KEYS, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                FaCfg<D, DK, DV, KK, KV, KEYS, NQ>::SMEM);
 }
 }  // namespace
 
 cudaError_t fattn_configure() {
-    cudaError_t e = fa_configure_t<72, 80, 128, 3, 3, 64>();
-    if (e == cudaSuccess) e = fa_configure_t<72, 80, 128, 2, 2, 128>();
-    if (e == cudaSuccess) e = fa_configure_t<256, 256, 256, 2, 2, 64>();
+    cudaError_t e = fa_configure_t<72, 80, 128, 3, 3, 64, 2>();
+    if (e == cudaSuccess) e = fa_configure_t<72, 80, 128, 2, 2, 128, 2>();
+    if (e == cudaSuccess) e = fa_configure_t<72, 80, 128, 2, 2, 128, 4>();
+    if (e == cudaSuccess) e = fa_configure_t<256, 256, 256, 2, 2, 64, 2>();
     return e;
 }
 
@@ -609,6 +623,14 @@ static int fa72_keys() {
     static const int k = [] {
         const char* e = std::getenv("PI0B_FA72_KEYS");
         return e && std::atoi(e) == 64 ? 64 : 128;
+    }();
+    return k;
+}
+// d = 72, 128-key tiles: softmax threads per query row (PI0B_FA72_NQ, 2 or 4).
+static int fa72_nq() {
+    static const int k = [] {
+        const char* e = std::getenv("PI0B_FA72_NQ");
+        return e && std::atoi(e) == 2 ? 2 : 4;
     }();
     return k;
 }
@@ -631,12 +653,13 @@ FaMaps make_fattn_maps(const AttnParams& p, int head_dim) {
 static bool g_fa_pdl = true;
 void fattn_set_pdl(bool on) { g_fa_pdl = on; }
 
-template <int D, int DK, int DV, int KK, int KV, int KEYS>
+template <int D, int DK, int DV, int KK, int KV, int KEYS, int NQ>
 static cudaError_t fa_launch_t(const FaMaps& maps, const AttnParams& p, dim3 grid, cudaStream_t stream) {
+    using C = FaCfg<D, DK, DV, KK, KV, KEYS, NQ>;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(kFaThreads, 1, 1);
-    cfg.dynamicSmemBytes = FaCfg<D, DK, DV, KK, KV, KEYS>::SMEM;
+    cfg.blockDim = dim3(C::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     int na = 0;
@@ -654,7 +677,7 @@ static cudaError_t fa_launch_t(const FaMaps& maps, const AttnParams& p, dim3 gri
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, fattn_kernel<D, DK, DV, KK, KV, KEYS>, maps, p);
+    return cudaLaunchKernelEx(&cfg, fattn_kernel<D, DK, DV, KK, KV, KEYS, NQ>, maps, p);
 }
 
 // grid = (stacked q tiles of 128, key splits (p.kv_splits: 1, 2, 4 or 8), kv groups).
@@ -668,9 +691,10 @@ cudaError_t launch_fattn(int head_dim, const FaMaps& maps, const AttnParams& p, 
     if ((p.rows1 > 0 && (p.rows0 % 32)) || (p.rows1 % 32) || (p.q_rows % 32)) return cudaErrorInvalidValue;
     switch (head_dim) {
         case 72:
-            return fa72_keys() == 128 ? fa_launch_t<72, 80, 128, 2, 2, 128>(maps, p, grid, stream)
-                                      : fa_launch_t<72, 80, 128, 3, 3, 64>(maps, p, grid, stream);
-        case 256: return fa_launch_t<256, 256, 256, 2, 2, 64>(maps, p, grid, stream);
+            if (fa72_keys() == 64) return fa_launch_t<72, 80, 128, 3, 3, 64, 2>(maps, p, grid, stream);
+            return fa72_nq() == 4 ? fa_launch_t<72, 80, 128, 2, 2, 128, 4>(maps, p, grid, stream)
+                                  : fa_launch_t<72, 80, 128, 2, 2, 128, 2>(maps, p, grid, stream);
+        case 256: return fa_launch_t<256, 256, 256, 2, 2, 64, 2>(maps, p, grid, stream);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -16,13 +16,14 @@ from paper_2510_26742_b200.config import default_config  # noqa: E402
 from paper_2510_26742_b200.inputs import gen_inputs  # noqa: E402
 
 views = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-cfg = default_config(views=views)
+prompt = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+cfg = default_config(views=views, prompt_tokens=prompt)
 eng = E.Engine(cfg)
 t = time.time()
 eng.gen_weights(1)
 print(f"gen_weights {time.time() - t:.2f}s")
 x = gen_inputs(cfg, 1)
-y = eng.run(x["patches"], x["state"], x["noise"])
+y = eng.run(x["patches"], x["state"], x["noise"], x.get("prompt"))
 plan = eng.describe()
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 open(os.path.join(ROOT, "gpurun_out", "plan.txt"), "w").write("\n".join(plan))
@@ -52,7 +53,7 @@ print(f"graph replay p50 {np.median(ms):.3f} ms  (kernels/inference {eng.kernel_
 t = []
 for _ in range(10):
     t0 = time.perf_counter()
-    eng.run(x["patches"], x["state"], x["noise"])
+    eng.run(x["patches"], x["state"], x["noise"], x.get("prompt"))
     t.append((time.perf_counter() - t0) * 1e3)
 print(f"run() e2e p50 {np.median(t):.3f} ms")
 json.dump({"rows": rows, "replay_ms": ms, "e2e_ms": t}, open(os.path.join(ROOT, "gpurun_out", "node_times.json"), "w"))
