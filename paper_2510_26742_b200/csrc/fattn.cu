@@ -121,7 +121,8 @@ struct FaCfg {
     static_assert(KEYS == 64 || KEYS == 128, "key tile");
     static constexpr int ROW_BYTES = DV * 2;  // staged bf16 output row
     static_assert(Q_BYTES >= kFaRows * ROW_BYTES, "output staging fits the Q region");
-    static_assert((NQ == 2 || NQ == 4) && (DV / NQ) % 32 == 0 && (KEYS / NQ) % 8 == 0, "softmax split");
+    // (each thread's S part is read in 32-column TMEM loads)
+    static_assert((NQ == 2 || NQ == 4) && (DV / NQ) % 32 == 0 && (KEYS / NQ) % 32 == 0, "softmax split");
 };
 
 template <int D, int DK, int DV, int KK, int KV, int KEYS, int NQ>
