@@ -1,0 +1,18 @@
+#!/bin/bash
+# Round-end evidence on one GPU box: the whole -m gpu suite with measured parity
+# (gpurun_out/parity), the default bench line, the three BASELINE configs, node times, megakernel
+# trace, streaming runs, the ncu launch list of one inference, an ncu --set full capture of the
+# production megakernel, and the whole-graph timeline (-DPI0B_KTRACE variant, built beforehand).
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out/final gpurun_out/parity
+PI0B_PARITY_OUT=gpurun_out/parity timeout 1500 python -m pytest tests -m gpu -q -s -rA --timeout=600 > gpurun_out/final/tests.log 2>&1
+grep -E "passed|failed" gpurun_out/final/tests.log | tail -3
+timeout 900 python bench.py > gpurun_out/final/bench.json 2> gpurun_out/final/bench.err
+tail -c 2000 gpurun_out/final/bench.json
+bash scripts/refresh_profiles.sh > gpurun_out/final/refresh.log 2>&1
+timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/final/launches.csv python scripts/ncu_launches.py 2 > gpurun_out/final/launches.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:aemk -c 1 \
+    -o gpurun_out/final/prof_ae -f python scripts/ncu_node.py ae.mega 2 run > gpurun_out/final/ncu_ae.log 2>&1
+timeout 300 python scripts/graph_timeline.py 2 > gpurun_out/final/graph_timeline.txt 2>&1
+ls -la gpurun_out/final gpurun_out/refresh
