@@ -12,7 +12,10 @@ tail -c 2000 gpurun_out/final/bench.json
 bash scripts/refresh_profiles.sh > gpurun_out/final/refresh.log 2>&1
 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/final/launches.csv python scripts/ncu_launches.py 2 > gpurun_out/final/launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:aemk -c 1 \
-    -o gpurun_out/final/prof_ae -f python scripts/ncu_node.py ae.mega 2 run > gpurun_out/final/ncu_ae.log 2>&1
+# (a --set full capture of the megakernel fails with LaunchFailed on its replay; the metric list
+# that profiles/ncu_ae_mega.json needs replays cleanly in 9 passes)
+timeout 900 ncu --profile-from-start off --clock-control none -k regex:aemk -c 1 --metrics \
+    gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_bytes.sum,launch__grid_size,launch__block_size,launch__registers_per_thread \
+    -o gpurun_out/final/prof_ae_m -f python scripts/ncu_launches.py 2 > gpurun_out/final/ncu_ae_m.log 2>&1
 timeout 300 python scripts/graph_timeline.py 2 > gpurun_out/final/graph_timeline.txt 2>&1
 ls -la gpurun_out/final gpurun_out/refresh
