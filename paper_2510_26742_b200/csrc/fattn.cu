@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(128 * NQ + 64, 1) fattn_kernel(const __grid_co
     }
     if (warp == C::MMA_WARP) tmem_alloc(tmem_slot, C::TMEM_COLS);
     if (tid == 0) pdl_launch_dependents();
+    __syncwarp();  // warp 0 reconverged after thread 0's set-up before the (.aligned) block barrier
     tc_fence_before();
     __syncthreads();  // (key splits touch no peer barrier or shared memory: one cluster barrier in the combine)
     tc_fence_after();
