@@ -472,7 +472,8 @@ private:
     void alloc_activations();
     void build_plan();
     void add_gemm(int part, const std::string& node, int inst, const __nv_bfloat16* A, long long lda,
-                  int M, const NodeWeights& W, int widx, int bn, GemmParams gp, bool allow_split = true);
+                  int M, const NodeWeights& W, int widx, int bn, GemmParams gp, bool allow_split = true,
+                  int force_splits = 0);
     void add_skinny(int part, const std::string& node, int inst, const __nv_bfloat16* X, long long ldx, int M,
                     const NodeWeights& W, int widx, GemmParams gp);
     void add_attn(int part, const std::string& node, int inst, int hd, AttnParams ap);
@@ -883,7 +884,7 @@ void Engine::tag(const std::string& node, int inst, const void* ptr, int rows, i
 
 void Engine::add_gemm(int part, const std::string& node, int inst, const __nv_bfloat16* A,
                       long long lda, int M, const NodeWeights& W, int widx, int bn, GemmParams gp,
-                      bool allow_split) {
+                      bool allow_split, int force_splits) {
     // Tuning overrides (sweeps): PI0B_BN_<NODE> / PI0B_SPLIT_<NODE>, NODE = id with '.' -> '_',
     // upper case (e.g. PI0B_BN_VE_PROJ=64).
     std::string key = node;
@@ -905,6 +906,7 @@ void Engine::add_gemm(int part, const std::string& node, int inst, const __nv_bf
     const int m_tiles = (M + 127) / 128, n_tiles = (N + bn - 1) / bn;
     const int kb = (K + 63) / 64;
     int splits = allow_split ? choose_splits(m_tiles, n_tiles, K, bn, num_sms_) : 1;
+    if (force_splits > 0) splits = std::min({force_splits, kb, kGemmMaxSplits});
     if (split_env > 0) splits = std::min({split_env, kb, kGemmMaxSplits});
     gp.kb_per_split = (kb + splits - 1) / splits;
     gp.splits = (kb + gp.kb_per_split - 1) / gp.kb_per_split;
@@ -1280,7 +1282,16 @@ void Engine::build_plan() {
             g.outb = xb_;
             g.ldob = llm_w_;
             g.out_stats = xs;
-            add_gemm(0, "llm.down", l, llm_g_, c.llm_mlp, Lp_, Wv["llm.down"], l, 128, g);
+            // Tile width and split-K from the prefix's m-tiles (measured, scripts/down_sweep.sh:
+            // 2 m-tiles -> bn 128 x 4 splits, 4 -> 128 x 2, 5 -> 256 x 3, 6 / 7 -> 256 x 2): the
+            // widest split keeping <= 128 CTAs, bn 128 while that split is >= 2, else bn 256.
+            const int dmt = (Lp_ + 127) / 128;
+            int dbn = 128, dsp = std::min(4, 128 / (dmt * 16));
+            if (dsp < 2) {
+                dbn = 256;
+                dsp = std::max(1, std::min(3, 128 / (dmt * 8)));
+            }
+            add_gemm(0, "llm.down", l, llm_g_, c.llm_mlp, Lp_, Wv["llm.down"], l, dbn, g, true, dsp);
             tag("llm.down", l, x_, L_, llm_w_, llm_w_, 0);
         }
     }
