@@ -973,10 +973,16 @@ void Engine::add_attn(int part, const std::string& node, int inst, int hd, AttnP
         for (char& ch : key) ch = ch == '.' ? '_' : char(std::toupper(static_cast<unsigned char>(ch)));
         const int base = ((ap.heads / ap.kv_heads) * ap.q_rows + 127) / 128 * ap.kv_heads;
         const int tiles = (ap.rows0 + ap.rows1 + 63) / 64;
-        // Measured in graph replays (scripts/ab_env.sh, 2 views): d 256 (llm.attn, 32 q tiles) at
-        // S = 4 saves ~5 us per inference (S = 2: +14 us); d 72 (ve.attn) is best unsplit.  S = 4 only
-        // when the split grid fits one wave and every split keeps two 64-key tiles.
-        int S = node == "llm.attn" && base * 4 <= num_sms_ && tiles >= 8 ? 4 : 1;
+        // Measured in graph replays (scripts/ab_env.sh, scripts/attn_split_sweep.sh): llm.attn (d 256)
+        // at S = 4 when the key tiles split evenly four ways (2 views, no prompt: -5 us per
+        // inference), S = 2 for other prefixes of >= 8 key tiles (2v + 17/64-token prompts, 3 views:
+        // -5..-18 us; S = 4 there is 150-170 us slower), unsplit below 8 tiles (1 view) and for
+        // d 72 (ve.attn); always within one wave of CTAs.
+        int S = 1;
+        if (node == "llm.attn" && tiles >= 8) {
+            if (tiles % 4 == 0 && base * 4 <= num_sms_) S = 4;
+            else if (base * 2 <= num_sms_) S = 2;
+        }
         S = env_int(("PI0B_ATTN_SPLITS_" + key).c_str(), env_int("PI0B_ATTN_SPLITS", S));
         ap.kv_splits = (S == 2 || S == 4 || S == 8) ? S : 1;
     }
@@ -1255,7 +1261,10 @@ void Engine::build_plan() {
             g.outb = xb_;
             g.ldob = llm_w_;
             g.out_stats = ps;
-            add_gemm(0, "llm.proj", l, llm_attn_, llm_q_, Lp_, Wv["llm.proj"], l, 64, g);
+            // bn 64 while its tiles fit one wave (2 views: 128 CTAs), else bn 128 (a 2v + 17-token
+            // prefix: 160 -> 80 tiles, -55 us per inference)
+            const int pbn = ((Lp_ + 127) / 128) * (llm_w_ / 64) > num_sms_ ? 128 : 64;
+            add_gemm(0, "llm.proj", l, llm_attn_, llm_q_, Lp_, Wv["llm.proj"], l, pbn, g);
             tag("llm.proj", l, x_, L_, llm_w_, llm_w_, 0);
         }
         {   // llm.ln2 + fused gated FFN: up * gelu(gate)
