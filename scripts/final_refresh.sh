@@ -18,4 +18,7 @@ timeout 900 ncu --profile-from-start off --clock-control none -k regex:aemk -c 1
     gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_bytes.sum,launch__grid_size,launch__block_size,launch__registers_per_thread \
     -o gpurun_out/final/prof_ae_m -f python scripts/ncu_launches.py 2 > gpurun_out/final/ncu_ae_m.log 2>&1
 timeout 300 python scripts/graph_timeline.py 2 > gpurun_out/final/graph_timeline.txt 2>&1
+# full report of the production megakernel: application replay (kernel replay of --set full fails)
+timeout 3300 ncu --replay-mode application --profile-from-start off --set full --clock-control none --import-source on \
+    -k regex:aemk -c 1 -o gpurun_out/final/prof_ae_full -f python scripts/ncu_launches.py 2 > gpurun_out/final/ncu_ae_full.log 2>&1
 ls -la gpurun_out/final gpurun_out/refresh
