@@ -79,6 +79,14 @@ constexpr int kBlocksPerSplit = 2;    // 64-key blocks per attention task
 #ifndef PI0B_AE_ADUP
 #define PI0B_AE_ADUP 1
 #endif
+// Per-task timestamps (PI0B_AE_TRACE, scripts/ae_trace.py), the per-k-block debug stamps and the
+// stop-after-phase switch (PI0B_AE_LIMIT) exist only in the -DPI0B_AE_TRACE_CODE=1 variant
+// (variants/libpi0b_aetrace.so): the runtime checks alone cost the production launch ~0.1 ms
+// (5.88 -> 5.77 ms).
+#ifndef PI0B_AE_TRACE_CODE
+#define PI0B_AE_TRACE_CODE 0
+#endif
+constexpr bool kAeTraceCode = PI0B_AE_TRACE_CODE != 0;
 constexpr bool kAttnDup = PI0B_AE_ADUP != 0;  // single-head attention with duplicated query rows
 constexpr int kOReg = 5;              // ae.proj staging combines up to this many key ranges in registers
 constexpr int kOffW = 0;
@@ -297,11 +305,11 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
         bool pend = false;
         for (int i = 0;; ++i) {
             const AeTask t = load_task(my + i);
-            if (t.kind == kAeEnd || t.phase >= p.limit_phase) break;
+            if (t.kind == kAeEnd || (kAeTraceCode && t.phase >= p.limit_phase)) break;
             if (pj <= i) pj = i;
             while (!pend && ahead < kWPrefetch) {
                 const AeTask u = load_task(my + pj);
-                if (u.kind == kAeEnd || u.phase >= p.limit_phase) {
+                if (u.kind == kAeEnd || (kAeTraceCode && u.phase >= p.limit_phase)) {
                     pend = true;
                     break;
                 }
@@ -320,7 +328,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             // k-block image: 8 KB (64-feature tile) or 16 KB (128); a slot takes 16 KB of them
             const int blk = (t.ncol == 128 ? 2 : 1) * kWBlk, kpc = kWSlot / blk;
             if (pj > i) ahead -= (long long)t.nkb * blk;
-            unsigned long long* tr = (p.trace && lane == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
+            unsigned long long* tr = (kAeTraceCode && p.trace && lane == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
             const AeMat wm = load_mat(p.mats + t.wmat);
             const uint8_t* base = reinterpret_cast<const uint8_t*>(wm.ptr) + ((size_t)t.tile * wm.ld + t.kb0) * blk;
             const int rot = ae_rot(t);
@@ -353,10 +361,10 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             constexpr uint32_t idesc_o = umma_idesc_bf16(128, 256) | (1u << 16);  // B (V) MN-major
             for (int i = 0;; ++i) {
                 const AeTask t = load_task(my + i);
-                if (t.kind == kAeEnd || t.phase >= p.limit_phase) break;
-                unsigned long long* tr = (p.trace && lane == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
+                if (t.kind == kAeEnd || (kAeTraceCode && t.phase >= p.limit_phase)) break;
+                unsigned long long* tr = (kAeTraceCode && p.trace && lane == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
                 if (t.kind == kAeGemm) {
-                    unsigned long long* dbg = (p.dbg && lane == 0 && t.epi == kEpiQkv && t.step == 1 && t.layer == 5)
+                    unsigned long long* dbg = (kAeTraceCode && p.dbg && lane == 0 && t.epi == kEpiQkv && t.step == 1 && t.layer == 5)
                                                   ? p.dbg + size_t(blockIdx.x) * 128 + 64 : nullptr;
                     mbar_wait(acc_empty, (gidx & 1) ^ 1);
                     // one X slot (two k-blocks) per handshake; a 64-feature task takes one W slot per
@@ -450,8 +458,8 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
 
         for (int i = 0;; ++i) {
             const AeTask t = load_task(my + i);
-            if (t.kind == kAeEnd || t.phase >= p.limit_phase) break;
-            unsigned long long* tr = (p.trace && wtid == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
+            if (t.kind == kAeEnd || (kAeTraceCode && t.phase >= p.limit_phase)) break;
+            unsigned long long* tr = (kAeTraceCode && p.trace && wtid == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
             if (tr) tr[0] = gtimer();
             // Pair owner: its receive buffer (union tail) is free from here on -- tell the helper.
             if ((t.pair == 1 || t.pair >= 3) && wtid == 0) {
@@ -1066,7 +1074,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 }
                 if (tr) tr[10] = gtimer();
                 unsigned long long* trs =
-                    (p.trace && threadIdx.x == 128) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
+                    (kAeTraceCode && p.trace && threadIdx.x == 128) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
                 if (one && kAttnDup) {
                     // Single head, duplicated rows: TMEM lane L holds query row R = L & 63; lane half
                     // kh = L >> 6 takes key block kh and, for O, output columns [128 kh, 128 kh + 128);

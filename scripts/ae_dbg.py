@@ -3,6 +3,12 @@ megakernel with PI0B_AE_LIMIT=<phases> and under compute-sanitizer."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+# the per-task timestamps are compiled only into the trace variant of the library
+_VAR = os.path.join(ROOT, "variants", "libpi0b_aetrace.so")
+if not os.path.exists(_VAR):
+    from paper_2510_26742_b200.build import build  # noqa: E402
+    build(lib=_VAR, defines=["-DPI0B_AE_TRACE_CODE=1"])
+os.environ.setdefault("PI0B_LIB", _VAR)
 from oracle import oracle as O
 from paper_2510_26742_b200 import engine as E
 from paper_2510_26742_b200.config import mid_config
