@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             const AeTask t = load_task(my + i);
             if (t.kind == kAeEnd || (kAeTraceCode && t.phase >= p.limit_phase)) break;
             if (pj <= i) pj = i;
-            while (!pend && ahead < kWPrefetch) {
+            while (kWPrefetch > 0 && !pend && ahead < kWPrefetch) {
                 const AeTask u = load_task(my + pj);
                 if (u.kind == kAeEnd || (kAeTraceCode && u.phase >= p.limit_phase)) {
                     pend = true;
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             if (t.kind != kAeGemm) continue;
             // k-block image: 8 KB (64-feature tile) or 16 KB (128); a slot takes 16 KB of them
             const int blk = (t.ncol == 128 ? 2 : 1) * kWBlk, kpc = kWSlot / blk;
-            if (pj > i) ahead -= (long long)t.nkb * blk;
+            if (kWPrefetch > 0 && pj > i) ahead -= (long long)t.nkb * blk;
             unsigned long long* tr = (kAeTraceCode && p.trace && lane == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
             const AeMat wm = load_mat(p.mats + t.wmat);
             const uint8_t* base = reinterpret_cast<const uint8_t*>(wm.ptr) + ((size_t)t.tile * wm.ld + t.kb0) * blk;
