@@ -87,6 +87,11 @@ constexpr int kBlocksPerSplit = 2;    // 64-key blocks per attention task
 #define PI0B_AE_TRACE_CODE 0
 #endif
 constexpr bool kAeTraceCode = PI0B_AE_TRACE_CODE != 0;
+// Asymmetric ae.qkv pairs (owner / helper, PI0B_AE_SYM_QKV=0): compiled only on request.
+#ifndef PI0B_AE_ASYM
+#define PI0B_AE_ASYM 0
+#endif
+constexpr bool kAeAsym = PI0B_AE_ASYM != 0;
 constexpr bool kAttnDup = PI0B_AE_ADUP != 0;  // single-head attention with duplicated query rows
 constexpr int kOReg = 5;              // ae.proj staging combines up to this many key ranges in registers
 constexpr int kOffW = 0;
@@ -462,7 +467,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
             unsigned long long* tr = (kAeTraceCode && p.trace && wtid == 0) ? p.trace + (size_t(blockIdx.x) * p.task_stride + i) * 16 : nullptr;
             if (tr) tr[0] = gtimer();
             // Pair owner: its receive buffer (union tail) is free from here on -- tell the helper.
-            if ((t.pair == 1 || t.pair >= 3) && wtid == 0) {
+            if (((kAeAsym && t.pair == 1) || t.pair >= 3) && wtid == 0) {
                 // the partner's st.async bytes: its partial of this CTA's columns + 64 row sums
                 mbar_arrive_expect_tx(pair_full, (t.pair >= 5 ? 64 * 32 * 4 : 64 * 64 * 4) + 64 * 4);
                 mbar_arrive_remote(partner_addr(pair_ready));
@@ -799,7 +804,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                 mbar_wait(acc_full, gidx & 1);
                 tc_fence_after();
                 if (tr) tr[8] = gtimer();
-                if (t.pair == 2) {
+                if (kAeAsym && t.pair == 2) {
                     // Pair helper: push the fp32 partial + row sums of squares into the owner's
                     // receive buffer once the owner has started this tile.
                     mbar_wait_cluster(pair_ready, hidx & 1);
@@ -823,7 +828,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                     if (wtid < 64) st_async_f32(partner_addr(recv_ss + wtid), sm_ss[wtid], rbar);
                     if (tr) tr[11] = gtimer();
                     ++hidx;
-                } else if (t.pair == 1) {
+                } else if (kAeAsym && t.pair == 1) {
                     mbar_wait_cluster(pair_full, oidx & 1);
                     ++oidx;
                 } else if (t.pair >= 3) {
@@ -874,7 +879,7 @@ __global__ void __launch_bounds__(kAeThreads, 1) aemk_kernel(const AeParams p) {
                         // paired tile (aemk.cuh AeTileOrder): feature column i and its partner
                         // (RoPE pair / gate); NI columns per thread: i in [NI dhalf, NI dhalf + NI)
                         // of this CTA's features
-                        const bool pr = t.pair == 1 || t.pair >= 3;  // add the partner's half-K partial
+                        const bool pr = (kAeAsym && t.pair == 1) || t.pair >= 3;  // add the partner's half-K partial
                         const float rs = pr ? 1.0f / sqrtf((sm_ss[r] + recv_ss[r]) * p.inv_width + p.eps) : sm_rs[r];
                         const bool sym128 = t.pair == 3 || t.pair == 4, sym64 = t.pair >= 5;
                         const int hf = sym128 ? t.pair - 3 : (sym64 ? t.pair - 5 : 0);
@@ -1398,7 +1403,7 @@ AePlan ae_plan(const AePlanInput& in) {
                 AeTask x = gemm(kXY, epi, wmat, xmat, 0, t, r ? h : 0, r ? kbt - h : h, wbar, wcnt, sbar);
                 x.step = uint16_t(step);
                 x.layer = uint16_t(layer);
-                x.pair = uint16_t(sym ? (r ? 4 : 3) : (in.sym_qkv ? (r ? 6 : 5) : (r ? 2 : 1)));
+                x.pair = uint16_t(sym ? (r ? 4 : 3) : ((in.sym_qkv || !kAeAsym) ? (r ? 6 : 5) : (r ? 2 : 1)));
                 if (sym) x.ncol = 128;
                 const int cta = r ? own ^ 1 : own;
                 load[size_t(cta)] += (r ? kbt - h : h) * kWB * (2.0 + wscale);
